@@ -1,0 +1,29 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) GPU")
+    config.addinivalue_line("markers", "multigpu: needs >= 2 GPUs")
+
+
+def pytest_collection_modifyitems(config, items):
+    try:
+        import torch
+        have_gpu = torch.cuda.is_available()
+        ngpu = torch.cuda.device_count() if have_gpu else 0
+    except Exception:
+        have_gpu, ngpu = False, 0
+    skip_gpu = pytest.mark.skip(reason="no CUDA device")
+    skip_multi = pytest.mark.skip(reason="needs >= 2 CUDA devices")
+    for it in items:
+        if "gpu" in it.keywords and not have_gpu:
+            it.add_marker(skip_gpu)
+        if "multigpu" in it.keywords and ngpu < 2:
+            it.add_marker(skip_multi)
