@@ -1,0 +1,214 @@
+/*
+ * dconv.h -- C ABI of the B200-native spatially / hybrid sample-spatial
+ * partitioned 2D convolution library (libdconv.so), after Dryden et al.,
+ * "Improving Strong-Scaling of CNN Training by Exploiting Finer-Grained
+ * Parallelism", arXiv:1903.06681 (cited below as PAPER.md:<line>).
+ *
+ * One process per GPU. Every tensor argument is a plain device pointer
+ * unless stated; every size is in elements. No torch types cross this ABI.
+ *
+ * Problem: input x N x C x H x W, weights w F x C x K x K,
+ * output y N x F x Ho x Wo with stride S and padding P,
+ *   Ho = floor((H + 2P - K)/S) + 1   (reading R2).
+ * The operation is cross-correlation, Eq. 1 (reading R1).
+ *
+ * Device layouts:
+ *   activations  NHWC bf16, channels padded to c_pad = roundup(C, 16)
+ *                (padded channels must be zero); x and dy live in
+ *                "margined" buffers [n][hb][wb][c_pad] holding the owned
+ *                block plus the halo rows/cols from the neighbours;
+ *   y, dx        dense NHWC bf16 over the owned block [n][h][w][c_pad];
+ *   w            bf16 [F][K][K][c_pad(C)]  (replicated on every rank,
+ *                PAPER.md:137 "w and dL/dw are replicated");
+ *   dw           fp32 [F][K][K][c_pad(C)]  (padded-channel entries are 0).
+ *
+ * Semantics: every call enqueues work on the caller's stream and returns
+ * without a host sync; internal streams are joined back with events before
+ * returning. Calls marked COLLECTIVE must be made by all ranks of the comm
+ * in the same order (as in NCCL). A plan is not thread-safe; distinct plans
+ * are independent. Nothing is thrown across the ABI: every entry point
+ * returns a dc_status_t and dc_last_error() gives a thread-local message.
+ */
+#ifndef DCONV_H
+#define DCONV_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    DC_OK = 0,
+    DC_ERR_ARG = 1,          /* null pointer, bad enum, bad flag             */
+    DC_ERR_SHAPE = 2,        /* even K, P > K/2, non-positive extent, ...     */
+    DC_ERR_PARTITION = 3,    /* grid invalid for the shape     */
+    DC_ERR_UNSUPPORTED = 4,  /* valid but not implemented (e.g. stride > 2)   */
+    DC_ERR_CUDA = 5,         /* CUDA failure; the plan becomes unusable       */
+    DC_ERR_COMM = 6,         /* NCCL / IPC failure; the plan becomes unusable */
+    DC_ERR_OOM = 7
+} dc_status_t;
+
+typedef enum { DC_BF16 = 0, DC_FP32_3XTF32 = 1 /* reserved, not yet implemented */ } dc_dtype_t;
+
+typedef enum { DC_X = 0, DC_Y = 1, DC_DY = 2, DC_DX = 3, DC_W = 4, DC_DW = 5 } dc_tensor_t;
+
+/* Process grid (p_N, p_H, p_W); rank = (i_N * p_H + i_H) * p_W + i_W
+ * (row-major, reading R8). {0,0,0} asks the performance model to choose
+ * (per layer). */
+typedef struct { int32_t pn, ph, pw; } dc_decomp_t;
+
+/* Local shard of one tensor on this rank (dc_plan_query). */
+typedef struct {
+    int64_t n0, h0, w0;         /* global offset of the owned block (samples, rows, cols)   */
+    int64_t n, h, w;            /* owned extents                                            */
+    int64_t c, c_pad;           /* logical channels, padded channels (innermost)           */
+    int32_t halo_n, halo_s;     /* margin rows above / below the owned block (x, dy only)  */
+    int32_t halo_w, halo_e;     /* margin cols left / right of the owned block             */
+    int64_t hb, wb;             /* buffer extents: hb = halo_n + h + halo_s, wb likewise    */
+    int64_t stride_n, stride_h, stride_w; /* element strides of the buffer (stride_c = 1)   */
+    size_t bytes;               /* bytes the caller must provide                            */
+} dc_shard_desc_t;
+
+typedef struct dc_comm_s *dc_comm_t;
+typedef struct dc_plan_s *dc_plan_t;
+
+/* ---- flags ---- */
+#define DC_EXCHANGE      0x1u  /* conv_fwd / conv_bwd_data: do the halo exchange inside the
+                                  call, overlapped with the interior tiles  */
+#define DC_ALLREDUCE     0x2u  /* conv_bwd_filter: sum dW over all ranks    */
+#define DC_HALO_NCCL     0x4u  /* use grouped ncclSend/ncclRecv instead of direct P2P       */
+#define DC_DEFAULT_FLAGS (DC_EXCHANGE | DC_ALLREDUCE)
+
+/* COLLECTIVE. Create the communicator of `world` ranks. nccl_uid128 points to
+ * the 128-byte ncclUniqueId produced by dc_comm_unique_id on rank 0 and
+ * broadcast by the caller (e.g. through torch.distributed). world == 1
+ * needs no id (may be NULL). cuda_device is this rank's device ordinal.
+ * Errors: DC_ERR_ARG (rank/world), DC_ERR_COMM (NCCL). */
+dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cuda_device,
+                           dc_comm_t *out);
+/* Write a fresh 128-byte ncclUniqueId to uid128 (rank 0 only). */
+dc_status_t dc_comm_unique_id(void *uid128);
+dc_status_t dc_comm_destroy(dc_comm_t comm);
+
+/* COLLECTIVE. Plan one convolution layer: global N, C, H, W, F, odd K,
+ * stride in {1, 2}, pad 0 <= P <= K/2, grid `decomp` (product == world, or
+ * {0,0,0} for the model's choice), on `comm`.
+ * Computes the blocked splits, the owned output blocks, the
+ * per-side halo widths of x and dy from the interval formula (PAPER.md:139,
+ * 145; reading R5) and validates the partition.
+ * Errors: DC_ERR_SHAPE (even K, P > K/2, extent < K without padding),
+ * DC_ERR_PARTITION (p_N > N, a part with no output rows, a halo wider than the
+ * adjacent rank's block -- PAPER.md:145's degenerate case -- or product !=
+ * world), DC_ERR_UNSUPPORTED (stride > 2, dtype != DC_BF16). */
+dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                           int stride, int pad, dc_decomp_t decomp, dc_dtype_t dtype,
+                           dc_comm_t comm, dc_plan_t *out);
+/* NOT collective. Plan of rank `rank` of a virtual grid without a
+ * communicator: index math only (dc_plan_query / dc_plan_halo_msgs /
+ * dc_plan_decomp work; compute calls need decomp product 1). Used by the
+ * host-side tests and by the replica mode of bench.py. */
+dc_status_t dc_plan_create_virtual(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                                   int stride, int pad, dc_decomp_t decomp, dc_dtype_t dtype,
+                                   int rank, dc_plan_t *out);
+
+/* One halo message of this rank (global rows [row0, row0+rows) x cols
+ * [col0, col0+cols), all local samples and channels). */
+typedef struct {
+    int32_t peer;       /* the other rank                                        */
+    int32_t is_send;    /* 1: this rank sends the block, 0: it receives it       */
+    int64_t row0, rows, col0, cols;
+} dc_halo_msg_t;
+/* Messages of the x (t = DC_X, before forward) or dy (t = DC_DY, before
+ * backward-data) exchange. *count is in/out: capacity in, number out. */
+dc_status_t dc_plan_halo_msgs(dc_plan_t plan, dc_tensor_t t, dc_halo_msg_t *msgs, int *count);
+
+/* Shard descriptor of `t` on this rank (sizes the caller must allocate). */
+dc_status_t dc_plan_query(dc_plan_t plan, dc_tensor_t t, dc_shard_desc_t *desc);
+/* The grid in use and the model's predicted seconds for fwd+bwd of the layer
+ * (PAPER.md:206 Cost_D(l)); predicted may be NULL. */
+dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicted_seconds);
+dc_status_t dc_plan_destroy(dc_plan_t plan);
+
+/* COLLECTIVE. Allocate (and zero) the margined buffer of t in {DC_X, DC_DY}
+ * with cudaMalloc and map it into the neighbours' address spaces for direct
+ * P2P halo stores. Owned by the plan; freed by dc_plan_destroy. */
+dc_status_t dc_buffer_alloc(dc_plan_t plan, dc_tensor_t t, void **dev_ptr);
+
+/* COLLECTIVE. Halo exchange of buffer `buf` (t in {DC_X, DC_DY}): copies each
+ * rank's boundary slabs (all local samples and channels) into the
+ * neighbours' margins, the 8 neighbours of a 2D grid directly (PAPER.md:127,
+ * 137-141, 193-194). Bit-exact copy; positions outside the global tensor are
+ * never sent (they are zero padding). flags: DC_HALO_NCCL selects the NCCL
+ * send/recv baseline, otherwise direct P2P stores over NVLink.
+ * buf must be the pointer returned by dc_buffer_alloc for t. */
+dc_status_t dc_halo_exchange(dc_plan_t plan, dc_tensor_t t, void *buf, unsigned flags,
+                             void *stream);
+
+/* Forward (Eq. 1 on the owned outputs): y = conv(x, w).
+ * x_margined: DC_X buffer (from dc_buffer_alloc when world > 1 and a halo
+ * exists; any buffer of the DC_X layout otherwise); w: DC_W; y: DC_Y.
+ * With DC_EXCHANGE the x halo exchange runs concurrently with the interior
+ * tiles and the boundary tiles run after it. */
+dc_status_t dc_conv_fwd(dc_plan_t plan, void *x_margined, const void *w, void *y,
+                        unsigned flags, void *stream);
+
+/* Backward-data (Eq. 3 on the owned inputs): dx = conv^T(dy, w).
+ * dy_margined: DC_DY buffer; w: DC_W; dx: DC_DX. DC_EXCHANGE as above. */
+dc_status_t dc_conv_bwd_data(dc_plan_t plan, void *dy_margined, const void *w, void *dx,
+                             unsigned flags, void *stream);
+
+/* Backward-filter (Eq. 2 restricted to the owned outputs):
+ * dw = sum over owned (n, i, j) of dy * x, using the halo'd x retained from
+ * the forward call (its margins must be unchanged since dc_conv_fwd) and dy
+ * WITHOUT its halo. With DC_ALLREDUCE the result is summed over
+ * all ranks (reading R10: a SUM, not a mean). dw: DC_DW fp32. */
+dc_status_t dc_conv_bwd_filter(dc_plan_t plan, const void *x_margined, const void *dy_margined,
+                               float *dw, unsigned flags, void *stream);
+
+/* Whole backward of the layer with the paper's overlap (PAPER.md:143, 177,
+ * 204): dy halo exchange concurrent with backward-filter, then
+ * backward-data, with the dW allreduce concurrent with backward-data.
+ * Equivalent to dc_conv_bwd_filter + dc_conv_bwd_data with the same flags. */
+dc_status_t dc_conv_bwd(dc_plan_t plan, const void *x_margined, void *dy_margined,
+                        const void *w, void *dx, float *dw, unsigned flags, void *stream);
+
+/* Spatially-aggregated batch-norm statistics (reading R11):
+ * per channel, mean and biased variance of `t` over the local samples and
+ * the whole spatial extent of the ranks that share this rank's samples
+ * (equal i_N). t is a dense NHWC bf16 tensor of the DC_Y layout of this plan
+ * (channels = F, padded); mean_dev/var_dev are device fp64 arrays of F
+ * entries. COLLECTIVE over the spatial group. local_only != 0 gives the
+ * purely local variant ("purely local batch normalization"). */
+dc_status_t dc_bn_spatial_stats(dc_plan_t plan, const void *t, double *mean_dev,
+                                double *var_dev, int local_only, void *stream);
+
+/* Number of kernels this library launched on this thread so far (for the
+ * bench's gpu_launches claim). */
+uint64_t dc_kernel_launches(void);
+
+/* Thread-local message of the last failing call (valid until the next call
+ * on the same thread). */
+const char *dc_last_error(void);
+
+/* ---- performance model, host only ---- */
+/* alpha [s], beta [s/byte] of the linear point-to-point model. */
+dc_status_t dc_model_set_comm(double alpha, double beta);
+/* Load an empirical cost table (CSV "op,n,c,h,w,f,k,s,pad,seconds",
+ * op in {fp,bpx,bpw}). Entries missing from the table
+ * fall back to a roofline estimate. */
+dc_status_t dc_model_load_table(const char *csv_path);
+/* Predicted seconds of fwd+bwd of the layer on grid d (PAPER.md:190-206,
+ * overlap per reading R16); returns DC_ERR_PARTITION if d is invalid. */
+dc_status_t dc_model_layer_cost(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                                int stride, int pad, dc_decomp_t d, int include_allreduce,
+                                double *seconds);
+/* Argmin over all valid grids of `world` ranks (tie-break reading R17). */
+dc_status_t dc_model_choose(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                            int stride, int pad, int world, dc_decomp_t *best, double *seconds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DCONV_H */

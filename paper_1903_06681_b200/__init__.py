@@ -1,0 +1,243 @@
+"""paper_1903_06681_b200 -- B200-native spatially / hybrid sample-spatial
+partitioned convolution (Dryden et al., arXiv:1903.06681).
+
+Thin ctypes binding of libdconv.so (include/dconv.h): the same entry points,
+argument marshalling only. Every step of the hot path runs in the library's
+sm_100a kernels and NCCL; nothing here computes. Importing fails loudly if
+the shared library is missing (build it with
+`python -m paper_1903_06681_b200.build`); there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdconv.so")
+
+DC_OK, DC_ERR_ARG, DC_ERR_SHAPE, DC_ERR_PARTITION, DC_ERR_UNSUPPORTED, DC_ERR_CUDA, DC_ERR_COMM, DC_ERR_OOM = range(8)
+STATUS_NAMES = ["DC_OK", "DC_ERR_ARG", "DC_ERR_SHAPE", "DC_ERR_PARTITION", "DC_ERR_UNSUPPORTED",
+                "DC_ERR_CUDA", "DC_ERR_COMM", "DC_ERR_OOM"]
+DC_BF16, DC_FP32_3XTF32 = 0, 1
+DC_X, DC_Y, DC_DY, DC_DX, DC_W, DC_DW = range(6)
+DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL = 0x1, 0x2, 0x4
+DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
+
+# every symbol include/dconv.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "dc_comm_create", "dc_comm_unique_id", "dc_comm_destroy", "dc_plan_create",
+    "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp",
+    "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
+    "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
+    "dc_last_error", "dc_model_set_comm", "dc_model_load_table", "dc_model_layer_cost",
+    "dc_model_choose",
+]
+
+
+class dc_decomp_t(ctypes.Structure):
+    _fields_ = [("pn", ctypes.c_int32), ("ph", ctypes.c_int32), ("pw", ctypes.c_int32)]
+
+
+class dc_shard_desc_t(ctypes.Structure):
+    _fields_ = [("n0", ctypes.c_int64), ("h0", ctypes.c_int64), ("w0", ctypes.c_int64),
+                ("n", ctypes.c_int64), ("h", ctypes.c_int64), ("w", ctypes.c_int64),
+                ("c", ctypes.c_int64), ("c_pad", ctypes.c_int64),
+                ("halo_n", ctypes.c_int32), ("halo_s", ctypes.c_int32),
+                ("halo_w", ctypes.c_int32), ("halo_e", ctypes.c_int32),
+                ("hb", ctypes.c_int64), ("wb", ctypes.c_int64),
+                ("stride_n", ctypes.c_int64), ("stride_h", ctypes.c_int64),
+                ("stride_w", ctypes.c_int64), ("bytes", ctypes.c_size_t)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class dc_halo_msg_t(ctypes.Structure):
+    _fields_ = [("peer", ctypes.c_int32), ("is_send", ctypes.c_int32), ("row0", ctypes.c_int64),
+                ("rows", ctypes.c_int64), ("col0", ctypes.c_int64), ("cols", ctypes.c_int64)]
+
+
+class DCError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 8 else status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdconv.so (raises if it was not built: no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1903_06681_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, i32, vp, st = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p, ctypes.c_int
+    P = ctypes.POINTER
+    sig = {
+        "dc_comm_create": [i32, i32, vp, i32, P(vp)],
+        "dc_comm_unique_id": [vp],
+        "dc_comm_destroy": [vp],
+        "dc_plan_create": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, vp, P(vp)],
+        "dc_plan_create_virtual": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, i32, P(vp)],
+        "dc_plan_halo_msgs": [vp, i32, P(dc_halo_msg_t), P(i32)],
+        "dc_plan_query": [vp, i32, P(dc_shard_desc_t)],
+        "dc_plan_decomp": [vp, P(dc_decomp_t), P(ctypes.c_double)],
+        "dc_plan_destroy": [vp],
+        "dc_buffer_alloc": [vp, i32, P(vp)],
+        "dc_halo_exchange": [vp, i32, vp, ctypes.c_uint, vp],
+        "dc_conv_fwd": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_conv_bwd_data": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_conv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_conv_bwd": [vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_bn_spatial_stats": [vp, vp, vp, vp, i32, vp],
+        "dc_model_set_comm": [ctypes.c_double, ctypes.c_double],
+        "dc_model_load_table": [ctypes.c_char_p],
+        "dc_model_layer_cost": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, P(ctypes.c_double)],
+        "dc_model_choose": [i64] * 5 + [i32, i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = st
+    L.dc_last_error.restype = ctypes.c_char_p
+    L.dc_last_error.argtypes = []
+    L.dc_kernel_launches.restype = ctypes.c_uint64
+    L.dc_kernel_launches.argtypes = []
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != DC_OK:
+        raise DCError(status, lib().dc_last_error().decode(errors="replace"))
+
+
+def _ptr(t) -> int | None:
+    """Device/host pointer of a torch tensor (or an int address)."""
+    if t is None:
+        return None
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+def _stream(s) -> int | None:
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return s if isinstance(s, int) else s.cuda_stream
+
+
+# ---------------- same names as the C ABI ----------------
+
+def dc_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().dc_comm_unique_id(buf))
+    return buf.raw
+
+
+def dc_comm_create(rank: int, world: int, uid: bytes | None, device: int) -> int:
+    out = ctypes.c_void_p()
+    ub = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+    _check(lib().dc_comm_create(rank, world, ub, device, ctypes.byref(out)))
+    return out.value
+
+
+def dc_comm_destroy(comm: int):
+    _check(lib().dc_comm_destroy(comm))
+
+
+def dc_plan_create(N, C, H, W, F, K, stride, pad, decomp=(0, 0, 0), dtype=DC_BF16, comm=None) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().dc_plan_create(N, C, H, W, F, K, stride, pad, dc_decomp_t(*decomp), dtype, comm,
+                                ctypes.byref(out)))
+    return out.value
+
+
+def dc_plan_create_virtual(N, C, H, W, F, K, stride, pad, decomp, rank, dtype=DC_BF16) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().dc_plan_create_virtual(N, C, H, W, F, K, stride, pad, dc_decomp_t(*decomp), dtype,
+                                        rank, ctypes.byref(out)))
+    return out.value
+
+
+def dc_plan_query(plan: int, t: int) -> dict:
+    d = dc_shard_desc_t()
+    _check(lib().dc_plan_query(plan, t, ctypes.byref(d)))
+    return d.as_dict()
+
+
+def dc_plan_halo_msgs(plan: int, t: int) -> list[dict]:
+    n = ctypes.c_int(0)
+    _check(lib().dc_plan_halo_msgs(plan, t, None, ctypes.byref(n)))
+    arr = (dc_halo_msg_t * max(n.value, 1))()
+    _check(lib().dc_plan_halo_msgs(plan, t, arr, ctypes.byref(n)))
+    return [{k: getattr(arr[i], k) for k, _ in dc_halo_msg_t._fields_} for i in range(n.value)]
+
+
+def dc_plan_decomp(plan: int) -> tuple[tuple[int, int, int], float]:
+    d, s = dc_decomp_t(), ctypes.c_double()
+    _check(lib().dc_plan_decomp(plan, ctypes.byref(d), ctypes.byref(s)))
+    return (d.pn, d.ph, d.pw), s.value
+
+
+def dc_plan_destroy(plan: int):
+    _check(lib().dc_plan_destroy(plan))
+
+
+def dc_buffer_alloc(plan: int, t: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().dc_buffer_alloc(plan, t, ctypes.byref(out)))
+    return out.value
+
+
+def dc_halo_exchange(plan: int, t: int, buf, flags: int = 0, stream=None):
+    _check(lib().dc_halo_exchange(plan, t, _ptr(buf), flags, _stream(stream)))
+
+
+def dc_conv_fwd(plan: int, x, w, y, flags: int = DC_EXCHANGE, stream=None):
+    _check(lib().dc_conv_fwd(plan, _ptr(x), _ptr(w), _ptr(y), flags, _stream(stream)))
+
+
+def dc_conv_bwd_data(plan: int, dy, w, dx, flags: int = DC_EXCHANGE, stream=None):
+    _check(lib().dc_conv_bwd_data(plan, _ptr(dy), _ptr(w), _ptr(dx), flags, _stream(stream)))
+
+
+def dc_conv_bwd_filter(plan: int, x, dy, dw, flags: int = DC_ALLREDUCE, stream=None):
+    _check(lib().dc_conv_bwd_filter(plan, _ptr(x), _ptr(dy), _ptr(dw), flags, _stream(stream)))
+
+
+def dc_conv_bwd(plan: int, x, dy, w, dx, dw, flags: int = DC_DEFAULT_FLAGS, stream=None):
+    _check(lib().dc_conv_bwd(plan, _ptr(x), _ptr(dy), _ptr(w), _ptr(dx), _ptr(dw), flags,
+                             _stream(stream)))
+
+
+def dc_bn_spatial_stats(plan: int, t, mean, var, local_only: bool = False, stream=None):
+    _check(lib().dc_bn_spatial_stats(plan, _ptr(t), _ptr(mean), _ptr(var), int(local_only),
+                                     _stream(stream)))
+
+
+def dc_kernel_launches() -> int:
+    return int(lib().dc_kernel_launches())
+
+
+def dc_model_set_comm(alpha: float, beta: float):
+    _check(lib().dc_model_set_comm(alpha, beta))
+
+
+def dc_model_load_table(path: str):
+    _check(lib().dc_model_load_table(path.encode()))
+
+
+def dc_model_layer_cost(N, C, H, W, F, K, stride, pad, decomp, include_allreduce=True) -> float:
+    s = ctypes.c_double()
+    _check(lib().dc_model_layer_cost(N, C, H, W, F, K, stride, pad, dc_decomp_t(*decomp),
+                                     int(include_allreduce), ctypes.byref(s)))
+    return s.value
+
+
+def dc_model_choose(N, C, H, W, F, K, stride, pad, world) -> tuple[tuple[int, int, int], float]:
+    d, s = dc_decomp_t(), ctypes.c_double()
+    _check(lib().dc_model_choose(N, C, H, W, F, K, stride, pad, world, ctypes.byref(d), ctypes.byref(s)))
+    return (d.pn, d.ph, d.pw), s.value

@@ -1,0 +1,990 @@
+// capi.cu -- L5: the C ABI of libdconv (include/dconv.h).
+//
+// Orchestrates one layer of spatially / hybrid-partitioned convolution on
+// this rank: plan (L1, plan.cpp), sm_100a kernels (L2, conv_tc.cu, halo.cu),
+// communication (L3: NCCL + CUDA-IPC peer mappings), model (L4,
+// perfmodel.cpp). Stream structure:
+//   forward       comm stream: x halo exchange  ||  caller stream: interior
+//                 tiles; then boundary tiles after the exchange event.
+//   backward      comm stream: dy halo exchange ||  caller stream: filter
+//                 gradient (needs no dy halo); then data
+//                 gradient, with the dW allreduce on the comm stream
+//                 concurrently.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "conv_tc.cuh"
+#include "halo.cuh"
+#include "plan.hpp"
+
+namespace dc {
+thread_local uint64_t g_launches = 0;
+static thread_local std::string g_err;
+void set_last_error(const std::string &m) { g_err = m; }
+
+double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce);
+bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t);
+}  // namespace dc
+
+using namespace dc;
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t _e = (x);                                                              \
+        DC_REQUIRE(_e == cudaSuccess, DC_ERR_CUDA, "%s: %s", #x, cudaGetErrorString(_e));  \
+    } while (0)
+#define NK(x)                                                                              \
+    do {                                                                                   \
+        ncclResult_t _r = (x);                                                             \
+        DC_REQUIRE(_r == ncclSuccess, DC_ERR_COMM, "%s: %s", #x, ncclGetErrorString(_r));  \
+    } while (0)
+
+struct dc_comm_s {
+    int rank = 0, world = 1, device = 0;
+    ncclComm_t nccl = nullptr;
+};
+
+namespace {
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda).
+typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+PFN_wait32 get_wait32() {
+    static PFN_wait32 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault,
+                                             &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_wait32>(p);
+    });
+    DC_REQUIRE(fn != nullptr, DC_ERR_CUDA, "cuStreamWaitValue32 unavailable");
+    return fn;
+}
+
+struct BufState {  // a margined buffer (X or DY) known to the plan
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    bool owned = false;
+    std::map<int, void *> peer;  // peer rank -> that rank's buffer mapped here
+    uint32_t epoch = 0;
+    void *stage = nullptr;       // NCCL baseline staging: [send | recv]
+    size_t stage_bytes = 0;
+};
+
+enum { FLAG_READY = 0, FLAG_DATA = 1 };
+
+}  // namespace
+
+struct dc_plan_s {
+    RankPlan rp;
+    dc_comm_s *comm = nullptr;
+    bool is_virtual = false;
+    ncclComm_t bn_comm = nullptr;
+    bool bn_comm_owned = false;
+    int bn_group = 1;
+    cudaStream_t s_comm = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    BufState buf[2];                 // 0: X, 1: DY
+    uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
+    std::map<int, uint32_t *> peer_flags;
+    bool can_flush = false;
+    __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases
+    size_t wt_bytes = 0;
+    float *ws = nullptr;             // split-K workspace
+    size_t ws_bytes = 0;
+    double *bn_part = nullptr;
+    size_t bn_part_bytes = 0;
+    double *bn_sums = nullptr;
+    double predicted = 0.0;
+
+    ~dc_plan_s() {
+        for (auto &b : buf) {
+            for (auto &kv : b.peer) cudaIpcCloseMemHandle(kv.second);
+            if (b.owned && b.ptr) cudaFree(b.ptr);
+            if (b.stage) cudaFree(b.stage);
+        }
+        for (auto &kv : peer_flags) cudaIpcCloseMemHandle(kv.second);
+        if (flags) cudaFree(flags);
+        if (wt) cudaFree(wt);
+        if (ws) cudaFree(ws);
+        if (bn_part) cudaFree(bn_part);
+        if (bn_sums) cudaFree(bn_sums);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (s_comm) cudaStreamDestroy(s_comm);
+        if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
+    }
+    int world() const { return rp.grid.size(); }
+    ncclComm_t nccl() const { return comm ? comm->nccl : nullptr; }
+    uint32_t *flag(uint32_t *base, int which, int kind, int src) const {
+        return base + ((which * 2 + kind) * world() + src);
+    }
+};
+
+namespace {
+
+template <class T>
+void ensure_alloc(T *&p, size_t &have, size_t need) {
+    if (need <= have) return;
+    if (p) CK(cudaFree(p));
+    p = nullptr;
+    CK(cudaMalloc(reinterpret_cast<void **>(&p), need));
+    have = need;
+}
+
+// ---------------------------------------------------------------------------
+// shard descriptors
+// ---------------------------------------------------------------------------
+dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
+    const ConvGeom &g = rp.g;
+    dc_shard_desc_t d{};
+    d.n0 = rp.nrange.lo;
+    d.n = rp.nrange.size();
+    auto fill = [&](int64_t h0, int64_t h, int64_t w0, int64_t w, int64_t c, int64_t cp, int64_t hn,
+                    int64_t hs, int64_t hw, int64_t he) {
+        d.h0 = h0, d.h = h, d.w0 = w0, d.w = w, d.c = c, d.c_pad = cp;
+        d.halo_n = (int32_t)hn, d.halo_s = (int32_t)hs, d.halo_w = (int32_t)hw,
+        d.halo_e = (int32_t)he;
+        d.hb = hn + h + hs;
+        d.wb = hw + w + he;
+        d.stride_w = cp;
+        d.stride_h = d.wb * cp;
+        d.stride_n = d.hb * d.wb * cp;
+        d.bytes = (size_t)(d.n * d.stride_n) * 2;
+    };
+    switch (t) {
+    case DC_X:
+        fill(rp.h.in.lo, rp.h.in.size(), rp.w.in.lo, rp.w.in.size(), g.C, g.Cp, rp.h.x_halo_lo(),
+             rp.h.x_halo_hi(), rp.w.x_halo_lo(), rp.w.x_halo_hi());
+        break;
+    case DC_DX:
+        fill(rp.h.in.lo, rp.h.in.size(), rp.w.in.lo, rp.w.in.size(), g.C, g.Cp, 0, 0, 0, 0);
+        break;
+    case DC_Y:
+        fill(rp.h.out.lo, rp.h.out.size(), rp.w.out.lo, rp.w.out.size(), g.F, g.Fp, 0, 0, 0, 0);
+        break;
+    case DC_DY:
+        fill(rp.h.out.lo, rp.h.out.size(), rp.w.out.lo, rp.w.out.size(), g.F, g.Fp,
+             rp.h.d_halo_lo(), rp.h.d_halo_hi(), rp.w.d_halo_lo(), rp.w.d_halo_hi());
+        break;
+    case DC_W:
+    case DC_DW:
+        d.n0 = 0, d.n = g.F, d.h = g.K, d.w = g.K, d.c = g.C, d.c_pad = g.Cp;
+        d.hb = g.K, d.wb = g.K;
+        d.stride_w = g.Cp, d.stride_h = g.K * g.Cp, d.stride_n = g.K * g.K * g.Cp;
+        d.bytes = (size_t)(g.F * g.K * g.K * g.Cp) * (t == DC_W ? 2 : 4);
+        break;
+    default:
+        fail(DC_ERR_ARG, "unknown tensor kind");
+    }
+    return d;
+}
+
+// ---------------------------------------------------------------------------
+// kernel configuration helpers
+// ---------------------------------------------------------------------------
+int pick_bkc(int64_t cin_p) { return cin_p % 64 == 0 ? 64 : cin_p % 32 == 0 ? 32 : 16; }
+int pick_bn(int64_t nout_p) { return nout_p <= 256 ? (int)nout_p : 256; }
+int pick_stages(int bkc, int bn) {
+    const int stage = 128 * bkc * 2 + bn * bkc * 2;
+    if (stage <= 32 * 1024) return std::max(2, std::min(8, (96 * 1024) / stage));
+    return std::max(2, std::min(8, (192 * 1024) / stage));
+}
+// Tile shape of `pixels`-pixel tiles (TH x TW, TW = 2^twl) with the least
+// waste over an nh x nw rectangle; ties go to wider tiles.
+int pick_twl(int64_t nh, int64_t nw, int pixels) {
+    int best = 3;
+    int64_t best_cells = -1;
+    for (int twl = 3; (1 << twl) <= pixels; ++twl) {
+        const int64_t tw = 1 << twl, th = pixels / tw;
+        const int64_t cells = ceil_div(nh, th) * th * ceil_div(nw, tw) * tw;
+        if (best_cells < 0 || cells <= best_cells) {
+            best = twl;
+            best_cells = cells;
+        }
+    }
+    return best;
+}
+
+// Interior / boundary split of an nh x nw output grid: lo/hi counts of
+// halo-dependent rows and cols ("decomposes ... into its
+// interior domain and boundary domains").
+struct Split2D {
+    int64_t nh, nw, bl, bh, bwl, bwh;
+};
+void make_rects(const Split2D &s, std::vector<OutRect> &interior, std::vector<OutRect> &boundary) {
+    interior.clear();
+    boundary.clear();
+    int64_t bl = std::min(s.bl, s.nh), bh = std::min(s.bh, s.nh - bl);
+    int64_t bwl = std::min(s.bwl, s.nw), bwh = std::min(s.bwh, s.nw - bwl);
+    const int64_t ih = s.nh - bl - bh, iw = s.nw - bwl - bwh;
+    auto add = [](std::vector<OutRect> &v, int64_t h0, int64_t w0, int64_t nh, int64_t nw) {
+        if (nh > 0 && nw > 0) v.push_back(OutRect{(int)h0, (int)w0, (int)nh, (int)nw});
+    };
+    add(interior, bl, bwl, ih, iw);
+    add(boundary, 0, 0, bl, s.nw);
+    add(boundary, s.nh - bh, 0, bh, s.nw);
+    add(boundary, bl, 0, ih, bwl);
+    add(boundary, bl, s.nw - bwh, ih, bwh);
+}
+
+void set_rects(ConvGemmParams &p, const std::vector<OutRect> &rects) {
+    DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
+    p.nrect = (int)rects.size();
+    p.rect_start[0] = 0;
+    for (int r = 0; r < p.nrect; ++r) {
+        p.rect[r] = rects[r];
+        const int twl = pick_twl(rects[r].nh, rects[r].nw, 128);
+        const int tw = 1 << twl, th = 128 >> twl;
+        p.rect_twl[r] = twl;
+        p.rect_tiles_w[r] = (int)ceil_div(rects[r].nw, tw);
+        p.rect_start[r + 1] = p.rect_start[r] + (int)ceil_div(rects[r].nh, th) * p.rect_tiles_w[r];
+    }
+}
+
+// 4D tensor map over an NHWC buffer [n][hb][wb][cp] with a box of
+// (bc channels) x (tw cols) x (th rows) x 1 sample, element stride s.
+void nhwc_map(CUtensorMap *m, const void *base, int64_t n, int64_t hb, int64_t wb, int64_t cp,
+              int64_t row_pitch_px, int64_t img_pitch_px, int bc, int tw, int th, int s) {
+    const uint64_t dims[4] = {(uint64_t)cp, (uint64_t)wb, (uint64_t)hb, (uint64_t)n};
+    const uint64_t strides[3] = {(uint64_t)(cp * 2), (uint64_t)(row_pitch_px * cp * 2),
+                                 (uint64_t)(img_pitch_px * cp * 2)};
+    const uint32_t box[4] = {(uint32_t)bc, (uint32_t)(tw * s), (uint32_t)(th * s), 1};
+    const uint32_t es[4] = {1, (uint32_t)s, (uint32_t)s, 1};
+    make_tmap(m, base, 4, dims, strides, box, es, bc * 2);
+}
+
+void weight_map(CUtensorMap *m, const void *base, int64_t rows, int64_t kcols, int bkc, int bn) {
+    const uint64_t dims[2] = {(uint64_t)kcols, (uint64_t)rows};
+    const uint64_t strides[1] = {(uint64_t)(kcols * 2)};
+    const uint32_t box[2] = {(uint32_t)bkc, (uint32_t)bn};
+    make_tmap(m, base, 2, dims, strides, box, nullptr, bkc * 2);
+}
+
+// ---------------------------------------------------------------------------
+// forward
+// ---------------------------------------------------------------------------
+struct GemmLaunch {
+    CUtensorMap amap, bmap;
+    ConvGemmParams p;
+    std::vector<OutRect> interior, boundary;
+    int nout_tiles = 0;
+};
+
+void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunch &L) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    const dc_shard_desc_t xd = describe(rp, DC_X), yd = describe(rp, DC_Y);
+    ConvGemmParams &p = L.p;
+    std::memset(&p, 0, sizeof p);
+    p.bkc = pick_bkc(g.Cp);
+    p.kc = (int)(g.Cp / p.bkc);
+    p.bn = pick_bn(g.Fp);
+    p.stages = pick_stages(p.bkc, p.bn);
+    p.T = g.K * g.K;
+    DC_REQUIRE(p.T <= kMaxTaps, DC_ERR_UNSUPPORTED, "K=%d too large", g.K);
+    for (int a = 0; a < g.K; ++a)
+        for (int b = 0; b < g.K; ++b) {
+            p.tap_h[a * g.K + b] = (int8_t)a;
+            p.tap_w[a * g.K + b] = (int8_t)b;
+        }
+    p.s_in = g.S;
+    p.origin_h = (int)(g.S * rp.h.out.lo - g.P - rp.h.xbuf.lo);
+    p.origin_w = (int)(g.S * rp.w.out.lo - g.P - rp.w.xbuf.lo);
+    p.out = reinterpret_cast<__nv_bfloat16 *>(y);
+    p.out_sn = yd.stride_n, p.out_sh = yd.stride_h, p.out_sw = yd.stride_w;
+    p.out_h0 = 0, p.out_w0 = 0, p.out_dh = 1, p.out_dw = 1;
+    p.nout_p = (int)g.Fp;
+    L.nout_tiles = (int)ceil_div(g.Fp, p.bn);
+    // the A map's box depends on the tile shape of each rect: encoded in launch_rects
+    (void)x;
+    (void)xd;
+    weight_map(&L.bmap, w, g.F, (int64_t)g.K * g.K * g.Cp, p.bkc, p.bn);
+    // halo-dependent output rows/cols (only toward existing neighbours)
+    auto count = [&](const DimSplit &d, bool lo) -> int64_t {
+        const bool nb = lo ? d.idx > 0 : d.idx + 1 < d.parts;
+        if (!nb) return 0;
+        int64_t c = 0;
+        const int64_t n = d.out.size();
+        for (int64_t k = 0; k < n; ++k) {
+            const int64_t i = lo ? k : n - 1 - k;
+            const int64_t gl = g.S * (d.out.lo + i) - g.P;
+            const bool dep = lo ? gl < d.in.lo : gl + g.K - 1 >= d.in.hi;
+            if (!dep) break;
+            ++c;
+        }
+        return c;
+    };
+    Split2D s{rp.h.out.size(), rp.w.out.size(), count(rp.h, true), count(rp.h, false),
+              count(rp.w, true), count(rp.w, false)};
+    make_rects(s, L.interior, L.boundary);
+}
+
+// Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
+// box shape is baked into the tensor map).
+void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
+                  const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
+    if (rects.empty()) return;
+    std::map<int, std::vector<OutRect>> by_twl;
+    for (auto &r : rects) by_twl[pick_twl(r.nh, r.nw, 128)].push_back(r);
+    for (auto &kv : by_twl) {
+        const int twl = kv.first, tw = 1 << twl, th = 128 >> twl;
+        nhwc_map(&L.amap, in_base, ind.n, ind.hb, ind.wb, cin_p, ind.wb, ind.hb * ind.wb, L.p.bkc,
+                 tw, th, L.p.s_in);
+        set_rects(L.p, kv.second);
+        launch_conv_gemm(L.amap, L.bmap, L.p, nsamples, L.nout_tiles, st);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// halo exchange
+// ---------------------------------------------------------------------------
+void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t st) {
+    const RankPlan &rp = pl->rp;
+    const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
+    const auto &recvs = which == 0 ? rp.x_recv : rp.dy_recv;
+    if (sends.empty() && recvs.empty()) return;
+    DC_REQUIRE(!pl->is_virtual && pl->comm && pl->comm->nccl, DC_ERR_ARG,
+               "halo exchange needs a communicator (virtual plan or world 1)");
+    const int64_t cp = which == 0 ? rp.g.Cp : rp.g.Fp;
+    const int vec16 = (int)(cp * 2 / 16);
+    const int64_t nl = rp.nrange.size();
+    BufState &B = pl->buf[which];
+    const bool use_nccl = (flags & DC_HALO_NCCL) != 0;
+    if (!use_nccl)
+        DC_REQUIRE(B.ptr == buf, DC_ERR_ARG,
+                   "direct P2P halo exchange needs the buffer from dc_buffer_alloc (or pass "
+                   "DC_HALO_NCCL)");
+    auto strides = [&](int64_t hb, int64_t wb, BlockCopy &c, bool src) {
+        const long long sw = vec16, sh = wb * vec16, sn = hb * wb * vec16;
+        if (src) c.s_sn = sn, c.s_sh = sh, c.s_sw = sw;
+        else c.d_sn = sn, c.d_sh = sh, c.d_sw = sw;
+    };
+    if (use_nccl) {
+        size_t send_bytes = 0, recv_bytes = 0;
+        for (auto &m : sends) send_bytes += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+        for (auto &m : recvs) recv_bytes += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+        ensure_alloc(reinterpret_cast<uint8_t *&>(B.stage), B.stage_bytes, send_bytes + recv_bytes);
+        uint8_t *sbuf = reinterpret_cast<uint8_t *>(B.stage), *rbuf = sbuf + send_bytes;
+        CopyBatch pack{};
+        size_t off = 0;
+        for (auto &m : sends) {
+            BlockCopy &c = pack.c[pack.count++];
+            c.src = reinterpret_cast<const uint4 *>(buf) +
+                    (m.src_row0 * m.src_wb + m.src_col0) * vec16;
+            c.dst = reinterpret_cast<uint4 *>(sbuf + off);
+            strides(m.src_hb, m.src_wb, c, true);
+            c.d_sw = vec16, c.d_sh = m.cols.size() * vec16, c.d_sn = m.rows.size() * c.d_sh;
+            c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
+            off += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+        }
+        launch_block_copies(pack, st);
+        NK(ncclGroupStart());
+        off = 0;
+        for (auto &m : sends) {
+            const size_t b = (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+            NK(ncclSend(sbuf + off, b, ncclUint8, m.peer, pl->nccl(), st));
+            off += b;
+        }
+        off = 0;
+        for (auto &m : recvs) {
+            const size_t b = (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+            NK(ncclRecv(rbuf + off, b, ncclUint8, m.peer, pl->nccl(), st));
+            off += b;
+        }
+        NK(ncclGroupEnd());
+        CopyBatch unpack{};
+        off = 0;
+        for (auto &m : recvs) {
+            BlockCopy &c = unpack.c[unpack.count++];
+            c.src = reinterpret_cast<const uint4 *>(rbuf + off);
+            c.s_sw = vec16, c.s_sh = m.cols.size() * vec16, c.s_sn = m.rows.size() * c.s_sh;
+            c.dst = reinterpret_cast<uint4 *>(buf) + (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
+            strides(m.dst_hb, m.dst_wb, c, false);
+            c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
+            off += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
+        }
+        launch_block_copies(unpack, st);
+        return;
+    }
+    // ---- direct P2P stores into the neighbours' margins + epoch flags ----
+    const uint32_t e = ++B.epoch;
+    const int me = rp.rank;
+    std::vector<uint32_t *> fl;
+    for (auto &m : recvs) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me));
+    launch_signal(fl.data(), (int)fl.size(), e, st);  // "my margin is free for epoch e"
+    const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (pl->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+    for (auto &m : sends) {
+        CUresult r = get_wait32()((CUstream)st,
+                                  (CUdeviceptr)pl->flag(pl->flags, which, FLAG_READY, m.peer), e,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+        DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    }
+    CopyBatch cb{};
+    for (auto &m : sends) {
+        BlockCopy &c = cb.c[cb.count++];
+        c.src = reinterpret_cast<const uint4 *>(buf) + (m.src_row0 * m.src_wb + m.src_col0) * vec16;
+        strides(m.src_hb, m.src_wb, c, true);
+        c.dst = reinterpret_cast<uint4 *>(B.peer.at(m.peer)) +
+                (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
+        strides(m.dst_hb, m.dst_wb, c, false);
+        c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
+    }
+    launch_block_copies(cb, st);
+    fl.clear();
+    for (auto &m : sends) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_DATA, me));
+    launch_signal(fl.data(), (int)fl.size(), e, st);  // "your margin holds epoch e"
+    for (auto &m : recvs) {
+        CUresult r = get_wait32()((CUstream)st,
+                                  (CUdeviceptr)pl->flag(pl->flags, which, FLAG_DATA, m.peer), e,
+                                  wflags);
+        DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+    }
+}
+
+// All-gather fixed-size blobs over NCCL (host in/out); used for IPC handles.
+std::vector<uint8_t> allgather_bytes(dc_plan_s *pl, const void *mine, size_t n) {
+    const int W = pl->world();
+    uint8_t *d = nullptr;
+    CK(cudaMalloc(&d, n * (W + 1)));
+    CK(cudaMemcpy(d + n * W, mine, n, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(d + n * W, d, n, ncclUint8, pl->nccl(), pl->s_comm));
+    CK(cudaStreamSynchronize(pl->s_comm));
+    std::vector<uint8_t> out(n * W);
+    CK(cudaMemcpy(out.data(), d, n * W, cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    return out;
+}
+
+std::vector<int> neighbours(const RankPlan &rp, int which) {
+    std::vector<int> v;
+    for (auto *L : {which == 0 ? &rp.x_send : &rp.dy_send, which == 0 ? &rp.x_recv : &rp.dy_recv})
+        for (auto &m : *L)
+            if (std::find(v.begin(), v.end(), m.peer) == v.end()) v.push_back(m.peer);
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// backward-data
+// ---------------------------------------------------------------------------
+struct Phase {
+    bool active = false;
+    int T = 0;
+    int8_t tap_h[kMaxTaps], tap_w[kMaxTaps], ka[kMaxTaps], kb[kMaxTaps];
+    int origin_h, origin_w, out_h0, out_w0;
+    int64_t nt_h, nt_w;
+    int64_t bl, bh, bwl, bwh;
+};
+
+// Phase decomposition of Eq. 3 for stride S (reading R4):
+// input rows u = S t + rho read dy rows t + e - m through taps a = a0 + S m.
+struct DimPhase {
+    int M = 0;
+    int64_t t0 = 0, nt = 0;
+    int origin = 0, out0 = 0;
+    int a0 = 0;
+    int64_t bl = 0, bh = 0;
+};
+DimPhase dim_phase(const DimSplit &d, int K, int S, int P, int rho) {
+    DimPhase r;
+    r.a0 = (rho + P) % S;
+    r.M = r.a0 < K ? (int)ceil_div(K - r.a0, S) : 0;
+    const int e = (rho + P - r.a0) / S;
+    const int64_t q = d.in.lo, rr = d.in.hi - 1;
+    r.t0 = -floor_div(-(q - rho), S);
+    const int64_t t1 = floor_div(rr - rho, S);
+    r.nt = std::max<int64_t>(0, t1 - r.t0 + 1);
+    r.origin = (int)(r.t0 + e - d.dbuf.lo - r.M + 1);
+    r.out0 = (int)(S * r.t0 + rho - q);
+    if (r.M > 0) {
+        if (d.idx > 0)
+            for (int64_t k = 0; k < r.nt; ++k) {
+                if (k + r.origin + d.dbuf.lo < d.out.lo) ++r.bl;
+                else break;
+            }
+        if (d.idx + 1 < d.parts)
+            for (int64_t k = r.nt - 1; k >= 0; --k) {
+                if (k + r.origin + r.M - 1 + d.dbuf.lo >= d.out.hi) ++r.bh;
+                else break;
+            }
+    }
+    return r;
+}
+
+void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned flags,
+                  cudaStream_t st) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
+    const int S = g.S;
+    // per-phase weights: [Cp][T][Fp] each, at increasing offsets
+    std::vector<Phase> ph;
+    size_t wt_need = 0;
+    for (int rh = 0; rh < S; ++rh)
+        for (int rw = 0; rw < S; ++rw) {
+            DimPhase a = dim_phase(rp.h, g.K, S, g.P, rh), b = dim_phase(rp.w, g.K, S, g.P, rw);
+            Phase f;
+            f.active = a.nt > 0 && b.nt > 0;
+            f.T = a.M * b.M;
+            for (int mh = 0; mh < a.M; ++mh)
+                for (int mw = 0; mw < b.M; ++mw) {
+                    const int t = mh * b.M + mw;
+                    f.tap_h[t] = (int8_t)mh;
+                    f.tap_w[t] = (int8_t)mw;
+                    f.ka[t] = (int8_t)(a.a0 + S * (a.M - 1 - mh));
+                    f.kb[t] = (int8_t)(b.a0 + S * (b.M - 1 - mw));
+                }
+            f.origin_h = a.origin, f.origin_w = b.origin;
+            f.out_h0 = a.out0, f.out_w0 = b.out0;
+            f.nt_h = a.nt, f.nt_w = b.nt;
+            f.bl = a.bl, f.bh = a.bh, f.bwl = b.bl, f.bwh = b.bh;
+            ph.push_back(f);
+            wt_need += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+        }
+    ensure_alloc(pl->wt, pl->wt_bytes, wt_need);
+    std::vector<GemmLaunch> L(ph.size());
+    size_t off = 0;
+    for (size_t i = 0; i < ph.size(); ++i) {
+        Phase &f = ph[i];
+        __nv_bfloat16 *wt = pl->wt + off / 2;
+        off += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+        if (!f.active) continue;
+        if (f.T > 0)
+            launch_weight_transform(reinterpret_cast<const __nv_bfloat16 *>(w), wt, (int)g.F,
+                                    (int)g.Fp, (int)g.C, (int)g.Cp, g.K, f.T, f.ka, f.kb, st);
+        ConvGemmParams &p = L[i].p;
+        std::memset(&p, 0, sizeof p);
+        p.bkc = pick_bkc(g.Fp);
+        p.kc = (int)(g.Fp / p.bkc);
+        p.bn = pick_bn(g.Cp);
+        p.stages = pick_stages(p.bkc, p.bn);
+        p.T = f.T;
+        std::memcpy(p.tap_h, f.tap_h, sizeof p.tap_h);
+        std::memcpy(p.tap_w, f.tap_w, sizeof p.tap_w);
+        p.s_in = 1;
+        p.origin_h = f.origin_h, p.origin_w = f.origin_w;
+        p.out = reinterpret_cast<__nv_bfloat16 *>(dx);
+        p.out_sn = dxd.stride_n, p.out_sh = dxd.stride_h, p.out_sw = dxd.stride_w;
+        p.out_h0 = f.out_h0, p.out_w0 = f.out_w0, p.out_dh = S, p.out_dw = S;
+        p.nout_p = (int)g.Cp;
+        L[i].nout_tiles = (int)ceil_div(g.Cp, p.bn);
+        weight_map(&L[i].bmap, wt, g.Cp, (int64_t)std::max(f.T, 1) * g.Fp, p.bkc, p.bn);
+        Split2D s{f.nt_h, f.nt_w, f.bl, f.bh, f.bwl, f.bwh};
+        make_rects(s, L[i].interior, L[i].boundary);
+    }
+    const bool overlap = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
+    if (overlap) {
+        CK(cudaEventRecord(pl->ev[0], st));
+        CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
+        exchange(pl, 1, dy, flags, pl->s_comm);
+        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
+    }
+    for (size_t i = 0; i < ph.size(); ++i) {
+        if (!ph[i].active) continue;
+        std::vector<OutRect> rects = L[i].interior;
+        if (!overlap) rects.insert(rects.end(), L[i].boundary.begin(), L[i].boundary.end());
+        launch_rects(L[i], rects, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
+    }
+    if (overlap) {
+        CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
+        for (size_t i = 0; i < ph.size(); ++i)
+            if (ph[i].active)
+                launch_rects(L[i], L[i].boundary, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// backward-filter
+// ---------------------------------------------------------------------------
+void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cudaStream_t st) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    const dc_shard_desc_t xd = describe(rp, DC_X), dyd = describe(rp, DC_DY);
+    WgradParams p;
+    std::memset(&p, 0, sizeof p);
+    p.T = g.K * g.K;
+    p.bkc = pick_bkc(g.Cp);
+    p.kc = (int)(g.Cp / p.bkc);
+    p.pairs_total = p.T * p.kc;
+    p.bf = g.Fp % 64 == 0 ? 64 : g.Fp % 32 == 0 ? 32 : 16;
+    p.bn = g.Fp <= 256 ? (int)g.Fp : 256;
+    p.stages = (16384 + p.bn * 128) <= 32768 ? 4 : 4;
+    for (int a = 0; a < g.K; ++a)
+        for (int b = 0; b < g.K; ++b) {
+            p.tap_h[a * g.K + b] = (int8_t)a;
+            p.tap_w[a * g.K + b] = (int8_t)b;
+        }
+    p.s_in = g.S;
+    p.origin_h = (int)(g.S * rp.h.out.lo - g.P - rp.h.xbuf.lo);
+    p.origin_w = (int)(g.S * rp.w.out.lo - g.P - rp.w.xbuf.lo);
+    const int64_t ho = rp.h.out.size(), wo = rp.w.out.size(), nl = rp.nrange.size();
+    p.tw_log2 = pick_twl(ho, wo, 64);
+    const int tw = 1 << p.tw_log2, th = 64 >> p.tw_log2;
+    p.tiles_h = (int)ceil_div(ho, th);
+    p.tiles_w = (int)ceil_div(wo, tw);
+    p.nblocks = (int)(nl * p.tiles_h * p.tiles_w);
+    const int ppm = 128 / p.bkc;
+    const int m_tiles = (int)ceil_div(p.pairs_total, ppm);
+    const int n_tiles = (int)ceil_div(g.F, p.bn);
+    const long long per_split = (long long)g.F * p.T * g.Cp;
+    int splits = (int)ceil_div(296, (int64_t)m_tiles * n_tiles);
+    splits = std::max(1, std::min(splits, std::max(1, p.nblocks / 4)));
+    while (splits > 1 && (size_t)splits * per_split * 4 > ((size_t)1 << 30)) --splits;
+    p.splits = splits;
+    p.F = (int)g.F;
+    p.cp = (int)g.Cp;
+    p.ws_split = per_split;
+    if (splits > 1) {
+        ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * per_split * 4);
+        p.ws = pl->ws;
+    } else {
+        p.ws = dw;
+    }
+    CUtensorMap xmap, dymap;
+    nhwc_map(&xmap, x, xd.n, xd.hb, xd.wb, g.Cp, xd.wb, xd.hb * xd.wb, p.bkc, tw, th, g.S);
+    // dy WITHOUT its halo: a map over the owned block only
+    const __nv_bfloat16 *dy_owned = reinterpret_cast<const __nv_bfloat16 *>(dy) +
+                                    (dyd.halo_n * dyd.wb + dyd.halo_w) * g.Fp;
+    nhwc_map(&dymap, dy_owned, nl, ho, wo, g.Fp, dyd.wb, dyd.hb * dyd.wb, p.bf, tw, th, 1);
+    launch_wgrad(xmap, dymap, p, m_tiles, n_tiles, st);
+    if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+}
+
+void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
+    if (pl->world() <= 1) return;
+    DC_REQUIRE(pl->nccl() != nullptr, DC_ERR_ARG, "allreduce needs a communicator");
+    const ConvGeom &g = pl->rp.g;
+    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, pl->nccl(), st));
+}
+
+// Streams, events and small scratch of this rank (created lazily for virtual
+// plans, which may compute when no exchange / allreduce is requested).
+void ensure_local_resources(dc_plan_s *pl) {
+    if (pl->s_comm) return;
+    CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
+    for (auto &e : pl->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 2 * pl->rp.g.Fp));
+    int dev = 0, flush = 0;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, dev);
+    pl->can_flush = flush != 0;
+}
+
+dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, bool is_virtual) {
+    auto *pl = new dc_plan_s();
+    try {
+        pl->rp = make_rank_plan(g, grid, rank);
+        pl->comm = comm;
+        pl->is_virtual = is_virtual;
+        pl->bn_group = grid.ph * grid.pw;  // BN group: ranks with equal i_N
+        if (!is_virtual) {
+            ensure_local_resources(pl);
+            if (grid.size() > 1) {
+                if (pl->bn_group > 1) {
+                    if (grid.pn == 1) {
+                        pl->bn_comm = comm->nccl;
+                    } else {
+                        NK(ncclCommSplit(comm->nccl, pl->rp.in, rank, &pl->bn_comm, nullptr));
+                        pl->bn_comm_owned = true;
+                    }
+                }
+                // P2P flags, mapped into the neighbours
+                const size_t fb = sizeof(uint32_t) * 4 * grid.size();
+                CK(cudaMalloc(&pl->flags, fb));
+                CK(cudaMemset(pl->flags, 0, fb));
+                cudaIpcMemHandle_t h;
+                CK(cudaIpcGetMemHandle(&h, pl->flags));
+                auto all = allgather_bytes(pl, &h, sizeof h);
+                std::vector<int> nb = neighbours(pl->rp, 0);
+                for (int p : neighbours(pl->rp, 1))
+                    if (std::find(nb.begin(), nb.end(), p) == nb.end()) nb.push_back(p);
+                for (int p : nb) {
+                    cudaIpcMemHandle_t ph;
+                    std::memcpy(&ph, all.data() + p * sizeof ph, sizeof ph);
+                    void *ptr = nullptr;
+                    CK(cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess));
+                    pl->peer_flags[p] = reinterpret_cast<uint32_t *>(ptr);
+                }
+                CK(cudaDeviceSynchronize());
+            }
+        }
+    } catch (...) {
+        delete pl;
+        throw;
+    }
+    return pl;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char *dc_last_error(void) { return g_err.c_str(); }
+uint64_t dc_kernel_launches(void) { return g_launches; }
+
+dc_status_t dc_comm_unique_id(void *uid128) {
+    DC_API_BEGIN
+    DC_REQUIRE(uid128 != nullptr, DC_ERR_ARG, "null uid");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(uid128, &id, sizeof id);
+    DC_API_END
+}
+
+dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, dc_comm_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr && world >= 1 && rank >= 0 && rank < world, DC_ERR_ARG,
+               "bad rank/world (%d/%d)", rank, world);
+    CK(cudaSetDevice(device));
+    auto *c = new dc_comm_s();
+    c->rank = rank, c->world = world, c->device = device;
+    if (world > 1) {
+        DC_REQUIRE(uid128 != nullptr, DC_ERR_ARG, "world > 1 needs an NCCL unique id");
+        ncclUniqueId id;
+        std::memcpy(&id, uid128, sizeof id);
+        ncclResult_t r = ncclCommInitRank(&c->nccl, world, id, rank);
+        if (r != ncclSuccess) {
+            delete c;
+            fail(DC_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        }
+    }
+    *out = c;
+    DC_API_END
+}
+
+dc_status_t dc_comm_destroy(dc_comm_t c) {
+    DC_API_BEGIN
+    if (c) {
+        if (c->nccl) ncclCommDestroy(c->nccl);
+        delete c;
+    }
+    DC_API_END
+}
+
+dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                           int stride, int pad, dc_decomp_t decomp, dc_dtype_t dtype,
+                           dc_comm_t comm, dc_plan_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
+    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "only DC_BF16 is implemented");
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
+    Grid grid{decomp.pn, decomp.ph, decomp.pw};
+    double pred = 0;
+    if (decomp.pn == 0 && decomp.ph == 0 && decomp.pw == 0) {
+        DC_REQUIRE(model_choose(g, world, grid, pred), DC_ERR_PARTITION,
+                   "no valid decomposition of %d ranks", world);
+    } else {
+        DC_REQUIRE(grid.size() == world, DC_ERR_PARTITION, "grid (%d,%d,%d) has %d ranks, world is %d",
+                   grid.pn, grid.ph, grid.pw, grid.size(), world);
+    }
+    dc_plan_s *pl = create_plan(g, grid, rank, comm, false);
+    pl->predicted = model_layer_cost(g, grid, true);
+    *out = pl;
+    DC_API_END
+}
+
+dc_status_t dc_plan_create_virtual(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                                   int stride, int pad, dc_decomp_t decomp, dc_dtype_t dtype,
+                                   int rank, dc_plan_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
+    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "only DC_BF16 is implemented");
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    Grid grid{decomp.pn, decomp.ph, decomp.pw};
+    dc_plan_s *pl = create_plan(g, grid, rank, nullptr, true);
+    pl->predicted = model_layer_cost(g, grid, true);
+    *out = pl;
+    DC_API_END
+}
+
+dc_status_t dc_plan_query(dc_plan_t plan, dc_tensor_t t, dc_shard_desc_t *desc) {
+    DC_API_BEGIN
+    DC_REQUIRE(plan && desc, DC_ERR_ARG, "null argument");
+    *desc = describe(plan->rp, t);
+    DC_API_END
+}
+
+dc_status_t dc_plan_halo_msgs(dc_plan_t plan, dc_tensor_t t, dc_halo_msg_t *msgs, int *count) {
+    DC_API_BEGIN
+    DC_REQUIRE(plan && count && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    const auto &S = t == DC_X ? plan->rp.x_send : plan->rp.dy_send;
+    const auto &R = t == DC_X ? plan->rp.x_recv : plan->rp.dy_recv;
+    const int n = (int)(S.size() + R.size());
+    if (msgs) {
+        DC_REQUIRE(*count >= n, DC_ERR_ARG, "capacity %d < %d messages", *count, n);
+        int k = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (auto &m : pass == 0 ? S : R)
+                msgs[k++] = dc_halo_msg_t{m.peer, pass == 0 ? 1 : 0, m.rows.lo, m.rows.size(),
+                                          m.cols.lo, m.cols.size()};
+    }
+    *count = n;
+    DC_API_END
+}
+
+dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicted) {
+    DC_API_BEGIN
+    DC_REQUIRE(plan && chosen, DC_ERR_ARG, "null argument");
+    *chosen = dc_decomp_t{plan->rp.grid.pn, plan->rp.grid.ph, plan->rp.grid.pw};
+    if (predicted) *predicted = plan->predicted;
+    DC_API_END
+}
+
+dc_status_t dc_plan_destroy(dc_plan_t plan) {
+    DC_API_BEGIN
+    delete plan;
+    DC_API_END
+}
+
+dc_status_t dc_buffer_alloc(dc_plan_t pl, dc_tensor_t t, void **dev_ptr) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && dev_ptr && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    DC_REQUIRE(!pl->is_virtual, DC_ERR_ARG, "virtual plan has no device buffers");
+    const int which = t == DC_X ? 0 : 1;
+    BufState &B = pl->buf[which];
+    const dc_shard_desc_t d = describe(pl->rp, t);
+    DC_REQUIRE(B.ptr == nullptr, DC_ERR_ARG, "buffer already allocated for this tensor");
+    cudaError_t e = cudaMalloc(&B.ptr, std::max<size_t>(d.bytes, 256));
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_OOM, "cudaMalloc(%zu): %s", d.bytes, cudaGetErrorString(e));
+    B.owned = true;
+    B.bytes = d.bytes;
+    CK(cudaMemset(B.ptr, 0, std::max<size_t>(d.bytes, 256)));
+    if (pl->world() > 1) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, B.ptr));
+        auto all = allgather_bytes(pl, &h, sizeof h);
+        for (int p : neighbours(pl->rp, which)) {
+            cudaIpcMemHandle_t ph;
+            std::memcpy(&ph, all.data() + p * sizeof ph, sizeof ph);
+            void *ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess));
+            B.peer[p] = ptr;
+        }
+    }
+    CK(cudaDeviceSynchronize());
+    *dev_ptr = B.ptr;
+    DC_API_END
+}
+
+dc_status_t dc_halo_exchange(dc_plan_t pl, dc_tensor_t t, void *buf, unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && buf && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    exchange(pl, t == DC_X ? 0 : 1, buf, flags, (cudaStream_t)stream);
+    DC_API_END
+}
+
+dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned flags,
+                        void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && x && w && y, DC_ERR_ARG, "null argument");
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    GemmLaunch L;
+    prepare_fwd(pl, x, w, y, L);
+    const dc_shard_desc_t xd = describe(pl->rp, DC_X);
+    const int nl = (int)pl->rp.nrange.size();
+    const bool overlap =
+        (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
+    if (overlap) {
+        CK(cudaEventRecord(pl->ev[0], st));
+        CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
+        exchange(pl, 0, x, flags, pl->s_comm);
+        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
+        launch_rects(L, L.interior, x, xd, pl->rp.g.Cp, nl, st);
+        CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
+        launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, st);
+    } else {
+        std::vector<OutRect> all = L.interior;
+        all.insert(all.end(), L.boundary.begin(), L.boundary.end());
+        launch_rects(L, all, x, xd, pl->rp.g.Cp, nl, st);
+    }
+    DC_API_END
+}
+
+dc_status_t dc_conv_bwd_data(dc_plan_t pl, void *dy, const void *w, void *dx, unsigned flags,
+                             void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && dy && w && dx, DC_ERR_ARG, "null argument");
+    ensure_local_resources(pl);
+    run_bwd_data(pl, dy, w, dx, flags, (cudaStream_t)stream);
+    DC_API_END
+}
+
+dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, float *dw,
+                               unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && x && dy && dw, DC_ERR_ARG, "null argument");
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    run_bwd_filter(pl, x, dy, dw, st);
+    if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
+    DC_API_END
+}
+
+dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, void *dx, float *dw,
+                        unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && x && dy && w && dx && dw, DC_ERR_ARG, "null argument");
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool halo = (flags & DC_EXCHANGE) && (!pl->rp.dy_send.empty() || !pl->rp.dy_recv.empty());
+    const bool ar = (flags & DC_ALLREDUCE) && pl->world() > 1;
+    if (halo) {  // dy halo on the comm stream, concurrent with the filter gradient
+        CK(cudaEventRecord(pl->ev[0], st));
+        CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
+        exchange(pl, 1, dy, flags, pl->s_comm);
+        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
+    }
+    run_bwd_filter(pl, x, dy, dw, st);
+    if (ar) {  // dW allreduce on the comm stream, concurrent with the data gradient
+        CK(cudaEventRecord(pl->ev[2], st));
+        CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[2], 0));
+        allreduce_dw(pl, dw, pl->s_comm);
+        CK(cudaEventRecord(pl->ev[3], pl->s_comm));
+    }
+    if (halo) CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
+    run_bwd_data(pl, dy, w, dx, flags & ~DC_EXCHANGE, st);
+    if (ar) CK(cudaStreamWaitEvent(st, pl->ev[3], 0));
+    DC_API_END
+}
+
+dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, double *var,
+                                int local_only, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && t && mean && var, DC_ERR_ARG, "null argument");
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    const long long npix = rp.nrange.size() * rp.h.out.size() * rp.w.out.size();
+    const size_t need = sizeof(double) * 2 * g.Fp * bn_partial_blocks(npix, (int)g.Fp);
+    ensure_alloc(pl->bn_part, pl->bn_part_bytes, need);
+    launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part,
+                   pl->bn_sums, st);
+    double count = (double)npix;
+    if (!local_only && pl->bn_group > 1) {
+        DC_REQUIRE(pl->bn_comm != nullptr, DC_ERR_ARG, "spatial BN statistics need a communicator");
+        NK(ncclAllReduce(pl->bn_sums, pl->bn_sums, 2 * g.Fp, ncclFloat64, ncclSum, pl->bn_comm, st));
+        count = (double)rp.nrange.size() * g.Ho * g.Wo;
+    }
+    launch_bn_finalize(pl->bn_sums, (int)g.Fp, (int)g.F, count, mean, var, st);
+    DC_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,159 @@
+// halo.cu -- halo slab copies and the
+// spatially-aggregated BN statistics kernels.
+//
+// In NHWC a halo slab of an H split is, per sample, a contiguous run of
+// rows*wb*c_pad elements; a W split slab is `rows` runs of cols*c_pad. One
+// kernel handles both: each thread moves one 16-byte vector, consecutive
+// threads walk the contiguous (col, channel) run, so loads and stores are
+// fully coalesced whether the destination is local staging (NCCL baseline)
+// or a neighbour's margin mapped over NVLink (direct P2P stores).
+#include "common.hpp"
+#include "halo.cuh"
+
+namespace dc {
+
+__global__ void block_copy_kernel(const CopyBatch b) {
+    const BlockCopy &c = b.c[blockIdx.y];
+    const long long run = (long long)c.cols * c.vec16;        // vectors per (n, row)
+    const long long total = (long long)c.nn * c.rows * run;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const long long nr = idx / run, k = idx - nr * run;
+        const int n = (int)(nr / c.rows), r = (int)(nr - (long long)n * c.rows);
+        const int col = (int)(k / c.vec16), v = (int)(k - (long long)col * c.vec16);
+        const uint4 val = c.src[n * c.s_sn + r * c.s_sh + col * c.s_sw + v];
+        c.dst[n * c.d_sn + r * c.d_sh + col * c.d_sw + v] = val;
+    }
+}
+
+void launch_block_copies(const CopyBatch &b, cudaStream_t st) {
+    if (b.count == 0) return;
+    long long mx = 0;
+    for (int i = 0; i < b.count; ++i)
+        mx = std::max(mx, (long long)b.c[i].nn * b.c[i].rows * b.c[i].cols * b.c[i].vec16);
+    if (mx == 0) return;
+    const int blocks = (int)std::min<long long>((mx + 255) / 256, 148 * 4);
+    block_copy_kernel<<<dim3(blocks, b.count), 256, 0, st>>>(b);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "block copy launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
+struct FlagList {
+    uint32_t *f[16];
+};
+
+__global__ void signal_kernel(FlagList fl, int n, uint32_t value) {
+    __threadfence_system();
+    for (int i = threadIdx.x; i < n; i += blockDim.x)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl.f[i]), "r"(value) : "memory");
+}
+
+void launch_signal(uint32_t *const *flags, int n, uint32_t value, cudaStream_t st) {
+    if (n == 0) return;
+    DC_REQUIRE(n <= 16, DC_ERR_ARG, "too many flags");
+    FlagList fl{};
+    for (int i = 0; i < n; ++i) fl.f[i] = flags[i];
+    signal_kernel<<<1, 32, 0, st>>>(fl, n, value);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "signal launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
+// ---------------------------------------------------------------------------
+// BN statistics: per-channel sum and sum of squares in fp64.
+// Block: 256 threads; thread -> (pixel lane, 8-channel vector).
+// ---------------------------------------------------------------------------
+constexpr int kBnThreads = 256;
+
+int bn_partial_blocks(long long npix, int cpad) {
+    const int vecs = cpad / 8;
+    const int pix_per_iter = std::max(1, kBnThreads / vecs);
+    const long long iters = (npix + pix_per_iter - 1) / pix_per_iter;
+    return (int)std::max<long long>(1, std::min<long long>(iters, 148 * 2));
+}
+
+__global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t,
+                                                             long long npix, int cpad,
+                                                             double *__restrict__ partials) {
+    // sh[pl][2][cpad]: per-pixel-lane partials, summed below in a fixed order
+    // so the result does not depend on scheduling (deterministic).
+    extern __shared__ double sh[];
+    const int vecs = cpad / 8;
+    const int pix_lanes = max(1, kBnThreads / vecs);
+    const int v = threadIdx.x % vecs, pl = threadIdx.x / vecs;
+    if (pl < pix_lanes) {
+        double s[8], q[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s[e] = q[e] = 0.0;
+        for (long long p = (long long)blockIdx.x * pix_lanes + pl; p < npix;
+             p += (long long)gridDim.x * pix_lanes) {
+            const uint4 raw = t[p * vecs + v];
+            const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&raw);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const double x = (double)__bfloat162float(h[e]);
+                s[e] += x;
+                q[e] += x * x;
+            }
+        }
+        double *row = sh + (long long)pl * 2 * cpad;
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            row[v * 8 + e] = s[e];
+            row[cpad + v * 8 + e] = q[e];
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * cpad; i += blockDim.x) {
+        double acc = 0.0;
+        for (int l = 0; l < pix_lanes; ++l) acc += sh[(long long)l * 2 * cpad + i];
+        partials[(long long)blockIdx.x * 2 * cpad + i] = acc;
+    }
+}
+
+// Fixed-order reduction of the per-block partials (deterministic).
+__global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks, int n2,
+                                 double *__restrict__ out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int b = 0; b < blocks; ++b) acc += partials[(long long)b * n2 + i];
+        out[i] = acc;
+    }
+}
+
+void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
+                    double *out, cudaStream_t st) {
+    DC_REQUIRE(cpad % 8 == 0 && cpad / 8 <= kBnThreads, DC_ERR_UNSUPPORTED,
+               "BN stats: channels must be a multiple of 8 and <= 2048");
+    const int blocks = bn_partial_blocks(npix, cpad);
+    const int pix_lanes = std::max(1, kBnThreads / (cpad / 8));
+    bn_sums_kernel<<<blocks, kBnThreads, (size_t)pix_lanes * 2 * cpad * sizeof(double), st>>>(
+        reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn sums launch: %s", cudaGetErrorString(e));
+    bn_reduce_kernel<<<(2 * cpad + 255) / 256, 256, 0, st>>>(partials, blocks, 2 * cpad, out);
+    e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
+    g_launches += 2;
+}
+
+__global__ void bn_finalize_kernel(const double *sums, int cpad, int c, double count, double *mean,
+                                   double *var) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+        const double mu = sums[i] / count;
+        const double v = sums[cpad + i] / count - mu * mu;
+        mean[i] = mu;
+        var[i] = v > 0.0 ? v : 0.0;
+    }
+}
+
+void launch_bn_finalize(const double *sums, int cpad, int c, double count, double *mean,
+                        double *var, cudaStream_t st) {
+    bn_finalize_kernel<<<(c + 255) / 256, 256, 0, st>>>(sums, cpad, c, count, mean, var);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn finalize launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
+}  // namespace dc

@@ -1,0 +1,186 @@
+// perfmodel.cpp -- L4: the paper's performance model and
+// the per-layer decomposition choice, host only.
+//
+//   SR(n)   = alpha + beta n
+//   AR(p,n) = min(recursive doubling, ring)           PAPER.md:82 (Thakur; reading R15)
+//   FP_l    = C(local) + 2SR(O N C H) + 2SR(O N C W) + 4SR(O^2 N C)
+//   BPx_l   = Cx(local) + the same halo terms with F channels          PAPER.md:198-203 (R13)
+//   BPw_l   = Cw(local);  BPa_l = AR(P, F C K^2)
+//   Cost    = FP + BPx + BPw + BPa adjusted for overlap                PAPER.md:206 (R16)
+//   candidates: every (pN,pH,pW) with product P that is valid; ties to
+//   sample parallelism first                                           PAPER.md:222 (R17)
+// C, Cx, Cw come from an empirical table measured on B200
+// with this library's own kernels (bench.py --cost-table); shapes missing
+// from the table use a roofline estimate.
+#include <cmath>
+#include <cstdio>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <tuple>
+
+#include "plan.hpp"
+
+namespace dc {
+
+namespace {
+struct Model {
+    double alpha = 5e-6;          // s (NVLink P2P latency incl. launch)
+    double beta = 1.0 / 700e9;    // s/byte (measured-class NVLink 5 per direction)
+    double peak_flops = 1.36e15;  // sustained bf16 dense, MEASURED_PEAKS.json
+    double peak_bw = 6.55e12;     // HBM copy, MEASURED_PEAKS.json
+    double launch = 4e-6;         // fixed per-kernel overhead
+    std::map<std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int>, double> table;
+    std::mutex mu;
+};
+Model &model() {
+    static Model m;
+    return m;
+}
+
+int op_id(const std::string &s) { return s == "fp" ? 0 : s == "bpx" ? 1 : s == "bpw" ? 2 : -1; }
+
+double sr(double words, int word_bytes) {
+    Model &m = model();
+    return m.alpha + m.beta * words * word_bytes;
+}
+
+double ar(int p, double words, int word_bytes) {
+    if (p <= 1) return 0.0;
+    Model &m = model();
+    const double bp = m.beta * word_bytes;
+    const double rd = std::ceil(std::log2((double)p)) * (m.alpha + words * bp);
+    const double ring = 2.0 * (p - 1) * m.alpha + 2.0 * ((double)(p - 1) / p) * words * bp;
+    return std::min(rd, ring);
+}
+
+// Local conv time: table entry if present, else roofline estimate.
+double conv_time(int op, int64_t n, int64_t c, int64_t h, int64_t w, int64_t f, int K, int S, int P) {
+    Model &m = model();
+    {
+        std::lock_guard<std::mutex> lk(m.mu);
+        auto it = m.table.find(std::make_tuple(op, n, c, h, w, f, K, S, P));
+        if (it != m.table.end()) return it->second;
+    }
+    const int64_t ho = (h + 2 * P - K) / S + 1, wo = (w + 2 * P - K) / S + 1;
+    const double flops = 2.0 * n * f * c * K * K * (double)std::max<int64_t>(ho, 1) * std::max<int64_t>(wo, 1);
+    const double bytes = 2.0 * ((double)n * h * w * c + (double)n * ho * wo * f) + 2.0 * f * c * K * K;
+    return m.launch + std::max(flops / m.peak_flops, bytes / m.peak_bw);
+}
+
+double halo_terms(int64_t Nl, int64_t Ch, int64_t Hl, int64_t Wl, int O, bool hs, bool ws) {
+    if (O == 0) return 0.0;
+    double t = 0.0;
+    if (ws) t += 2 * sr((double)O * Nl * Ch * Hl, 2);
+    if (hs) t += 2 * sr((double)O * Nl * Ch * Wl, 2);
+    if (hs && ws) t += 4 * sr((double)O * O * Nl * Ch, 2);
+    return t;
+}
+}  // namespace
+
+double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce) {
+    const int64_t Nl = blocked(g.N, d.pn, 0).size();
+    const int64_t Hl = blocked(g.H, d.ph, 0).size(), Wl = blocked(g.W, d.pw, 0).size();
+    const int O = g.K / 2;
+    const double c_fp = conv_time(0, Nl, g.C, Hl, Wl, g.F, g.K, g.S, g.P);
+    const double c_bx = conv_time(1, Nl, g.C, Hl, Wl, g.F, g.K, g.S, g.P);
+    const double c_bw = conv_time(2, Nl, g.C, Hl, Wl, g.F, g.K, g.S, g.P);
+    const double hx = halo_terms(Nl, g.C, Hl, Wl, O, d.ph > 1, d.pw > 1);
+    const double hdy = halo_terms(Nl, g.F, Hl, Wl, O, d.ph > 1, d.pw > 1);
+    const double bpa = include_allreduce ? ar(d.size(), (double)g.F * g.C * g.K * g.K, 4) : 0.0;
+    const double fp = std::max(c_fp, hx);
+    const double bp = std::max(c_bw, hdy) + std::max(c_bx, bpa);
+    return fp + bp;
+}
+
+bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t) {
+    bool found = false;
+    for (int pn = world; pn >= 1; --pn) {
+        if (world % pn) continue;
+        const int rest = world / pn;
+        for (int ph = rest; ph >= 1; --ph) {
+            if (rest % ph) continue;
+            Grid d{pn, ph, rest / ph};
+            if (!grid_valid(g, d)) continue;
+            const double t = model_layer_cost(g, d, true);
+            // strict '<': enumeration order (larger pN, then larger pH first) is the tie-break
+            if (!found || t < best_t) {
+                best = d;
+                best_t = t;
+                found = true;
+            }
+        }
+    }
+    return found;
+}
+
+}  // namespace dc
+
+using namespace dc;
+
+extern "C" dc_status_t dc_model_set_comm(double alpha, double beta) {
+    DC_API_BEGIN
+    DC_REQUIRE(alpha >= 0 && beta >= 0, DC_ERR_ARG, "alpha, beta must be >= 0");
+    model().alpha = alpha;
+    model().beta = beta;
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_load_table(const char *path) {
+    DC_API_BEGIN
+    DC_REQUIRE(path != nullptr, DC_ERR_ARG, "null path");
+    std::ifstream f(path);
+    DC_REQUIRE(f.good(), DC_ERR_ARG, "cannot open cost table %s", path);
+    std::string line;
+    std::getline(f, line);
+    DC_REQUIRE(line.rfind("op,n,c,h,w,f,k,s,pad,seconds", 0) == 0, DC_ERR_ARG,
+               "cost table header must be op,n,c,h,w,f,k,s,pad,seconds (SPEC.md:418)");
+    Model &m = model();
+    std::lock_guard<std::mutex> lk(m.mu);
+    while (std::getline(f, line)) {
+        if (line.empty()) continue;
+        std::stringstream ss(line);
+        std::string op, tok;
+        std::getline(ss, op, ',');
+        long long v[8];
+        for (int i = 0; i < 8; ++i) {
+            std::getline(ss, tok, ',');
+            v[i] = std::stoll(tok);
+        }
+        std::getline(ss, tok, ',');
+        const int id = op_id(op);
+        DC_REQUIRE(id >= 0, DC_ERR_ARG, "unknown op '%s' in cost table", op.c_str());
+        m.table[std::make_tuple(id, (int64_t)v[0], (int64_t)v[1], (int64_t)v[2], (int64_t)v[3],
+                                (int64_t)v[4], (int)v[5], (int)v[6], (int)v[7])] = std::stod(tok);
+    }
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_layer_cost(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                                           int K, int stride, int pad, dc_decomp_t d,
+                                           int include_allreduce, double *seconds) {
+    DC_API_BEGIN
+    DC_REQUIRE(seconds != nullptr, DC_ERR_ARG, "null output");
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    Grid grid{d.pn, d.ph, d.pw};
+    std::string why;
+    DC_REQUIRE(grid_valid(g, grid, &why), DC_ERR_PARTITION, "%s", why.c_str());
+    *seconds = model_layer_cost(g, grid, include_allreduce != 0);
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_choose(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                                       int K, int stride, int pad, int world, dc_decomp_t *best,
+                                       double *seconds) {
+    DC_API_BEGIN
+    DC_REQUIRE(best != nullptr && world >= 1, DC_ERR_ARG, "bad arguments");
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    Grid b;
+    double t = 0;
+    DC_REQUIRE(model_choose(g, world, b, t), DC_ERR_PARTITION, "no valid grid of %d ranks", world);
+    *best = dc_decomp_t{b.pn, b.ph, b.pw};
+    if (seconds) *seconds = t;
+    DC_API_END
+}

@@ -1,0 +1,156 @@
+"""GPU parity: the sm_100a kernels through the C ABI vs the fp64 oracle on the
+same seeded, bf16-exact inputs (DESIGN.md §7 tolerances):
+  fwd y, bwd-data dx (bf16 out)  : ||g-o||_2/||o||_2 <= 2e-2 (north_star) and
+                                   <= 4e-3 (derived: bf16 output rounding 2^-9
+                                   plus fp32 accumulation of exact products)
+  bwd-filter dW (fp32 out)       : max|g-o|/max|o| <= 1e-4 (north_star fp32 bar)
+  BN statistics (fp64)           : abs error <= 1e-9
+and partition invariance: each rank's owned y / dx computed from its
+margined shard is BITWISE equal to the 1-GPU result (north_star)."""
+import numpy as np
+import pytest
+import torch
+
+import datagen
+import oracle
+from tests.gpu_util import (dw_to_fckk, empty_dense, fill_buffer, owned_nchw, rel_l2, rel_max,
+                            weights_gpu)
+
+pytestmark = pytest.mark.gpu
+
+TOL_L2_SPEC, TOL_L2_DERIVED, TOL_DW = 2e-2, 4e-3, 1e-4
+
+
+@pytest.fixture(scope="module")
+def dc():
+    from paper_1903_06681_b200 import build
+    build.build()
+    import paper_1903_06681_b200 as dc
+    torch.cuda.init()
+    return dc
+
+
+def make_inputs(N, C, H, W, F, K, S, P):
+    Ho, Wo = oracle.out_extent(H, K, S, P), oracle.out_extent(W, K, S, P)
+    x = datagen.gen_x(N, C, H, W)
+    w = datagen.gen_w(F, C, K)
+    dy = datagen.gen_dy(N, F, Ho, Wo)
+    return x, w, dy
+
+
+def run_layer(dc, shape, decomp=(1, 1, 1), rank=0, x=None, w=None, dy=None, virtual=True):
+    """Forward, backward-data and backward-filter of one rank's shard
+    (halo rows filled by the test from the global tensor: no exchange)."""
+    N, C, H, W, F, K, S, P = shape
+    plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, decomp, rank)
+    try:
+        xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
+        dyd, dxd = dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(plan, dc.DC_DX)
+        xb = fill_buffer(x, xd)
+        wb = weights_gpu(w, xd["c_pad"])
+        y = empty_dense(yd)
+        dc.dc_conv_fwd(plan, xb, wb, y, 0)
+        dyb = fill_buffer(dy, dyd)
+        dx = empty_dense(dxd)
+        dc.dc_conv_bwd_data(plan, dyb, wb, dx, 0)
+        dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+        dc.dc_conv_bwd_filter(plan, xb, dyb, dw, 0)
+        torch.cuda.synchronize()
+        return dict(y=y, dx=dx, dw=dw, xd=xd, yd=yd, dxd=dxd, dyd=dyd)
+    finally:
+        dc.dc_plan_destroy(plan)
+
+
+SHAPES = [  # (N, C, H, W, F, K, S, P)
+    (1, 2, 16, 16, 4, 3, 1, 1),        # C1 (BASELINE configs[0])
+    (2, 16, 20, 18, 32, 3, 1, 1),
+    (1, 64, 24, 40, 64, 3, 1, 1),      # 128B swizzle, 2 K-chunks per tap
+    (2, 32, 17, 23, 48, 3, 2, 1),      # stride 2, ragged, 64B swizzle
+    (1, 3, 30, 30, 64, 7, 2, 3),       # conv1-like (C=3 padded to 16, K=7 S=2)
+    (2, 128, 14, 14, 256, 1, 1, 0),    # 1x1
+    (1, 64, 15, 13, 32, 1, 2, 0),      # 1x1 stride 2 (dx phases with no taps)
+    (1, 24, 19, 21, 16, 5, 1, 2),      # K=5, C=24 -> 32
+    (1, 64, 12, 12, 320, 3, 1, 1),     # F > 256: two N tiles
+    (1, 18, 33, 35, 64, 3, 2, 1),      # mesh conv1_1-like (C=18)
+    (3, 16, 9, 9, 16, 3, 1, 0),        # P=0 (valid conv)
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_single_gpu_parity(dc, shape):
+    N, C, H, W, F, K, S, P = shape
+    x, w, dy = make_inputs(*shape)
+    r = run_layer(dc, shape, x=x, w=w, dy=dy)
+    y_ref = oracle.conv_fwd(x, w, S, P)
+    dx_ref = oracle.conv_bwd_data(dy, w, H, W, S, P)
+    dw_ref = oracle.conv_bwd_filter(x, dy, K, S, P)
+    y = owned_nchw(r["y"], r["yd"])
+    dx = owned_nchw(r["dx"], r["dxd"])
+    dw = dw_to_fckk(r["dw"], C)
+    assert np.isfinite(y).all() and np.isfinite(dx).all() and np.isfinite(dw).all()
+    e_y, e_dx, e_dw = rel_l2(y, y_ref), rel_l2(dx, dx_ref), rel_max(dw, dw_ref)
+    assert e_y <= TOL_L2_SPEC and e_y <= TOL_L2_DERIVED, e_y
+    assert e_dx <= TOL_L2_SPEC and e_dx <= TOL_L2_DERIVED, e_dx
+    assert e_dw <= TOL_DW, e_dw
+    # padded channels of y / dx are written as zeros
+    assert float(r["y"][..., F:].abs().max() if r["y"].shape[-1] > F else 0) == 0.0
+    assert float(r["dx"][..., C:].abs().max() if r["dx"].shape[-1] > C else 0) == 0.0
+
+
+GRIDS = [(1, 2, 1), (1, 1, 2), (1, 2, 2), (2, 2, 1), (1, 3, 1), (1, 4, 2)]
+
+
+@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[2], SHAPES[3], SHAPES[4], SHAPES[9]])
+@pytest.mark.parametrize("grid", GRIDS)
+def test_partition_bitwise(dc, shape, grid):
+    """Every rank's owned y and dx from its own margined shard is bitwise equal
+    to the unpartitioned result of the same kernel (north_star); the sum of
+    the per-rank dW partials equals the 1-GPU dW within the fp32 bar."""
+    N, C, H, W, F, K, S, P = shape
+    try:
+        dc.dc_plan_destroy(dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, grid, 0))
+    except dc.DCError:
+        pytest.skip("grid invalid for this shape")
+    x, w, dy = make_inputs(*shape)
+    full = run_layer(dc, shape, x=x, w=w, dy=dy)
+    Y = full["y"].float().cpu()
+    DX = full["dx"].float().cpu()
+    dw_sum = torch.zeros_like(full["dw"])
+    for rank in range(grid[0] * grid[1] * grid[2]):
+        r = run_layer(dc, shape, grid, rank, x=x, w=w, dy=dy)
+        yd, dxd = r["yd"], r["dxd"]
+        ys = Y[yd["n0"]:yd["n0"] + yd["n"], yd["h0"]:yd["h0"] + yd["h"], yd["w0"]:yd["w0"] + yd["w"]]
+        assert torch.equal(r["y"].float().cpu(), ys), f"rank {rank} y differs"
+        dxs = DX[dxd["n0"]:dxd["n0"] + dxd["n"], dxd["h0"]:dxd["h0"] + dxd["h"], dxd["w0"]:dxd["w0"] + dxd["w"]]
+        assert torch.equal(r["dx"].float().cpu(), dxs), f"rank {rank} dx differs"
+        dw_sum += r["dw"]
+    assert rel_max(dw_to_fckk(dw_sum, C), dw_to_fckk(full["dw"], C)) <= TOL_DW
+
+
+def test_bn_stats_local(dc):
+    N, C, H, W, F, K, S, P = 2, 8, 20, 24, 48, 3, 1, 1
+    plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, (1, 1, 1), 0)
+    yd = dc.dc_plan_query(plan, dc.DC_Y)
+    t = datagen.gen_block((N, F, H, W), 7, 9)
+    tb = fill_buffer(t, yd)
+    mean = torch.zeros(F, dtype=torch.float64, device="cuda")
+    var = torch.zeros(F, dtype=torch.float64, device="cuda")
+    dc.dc_bn_spatial_stats(plan, tb, mean, var, local_only=True)
+    torch.cuda.synchronize()
+    m_ref, v_ref = oracle.bn_stats(t)
+    assert np.abs(mean.cpu().numpy() - m_ref).max() <= 1e-9
+    assert np.abs(var.cpu().numpy() - v_ref).max() <= 1e-9
+    dc.dc_plan_destroy(plan)
+
+
+def test_launch_counter_and_errors(dc):
+    before = dc.dc_kernel_launches()
+    run_layer(dc, SHAPES[0], *[None] * 0, x=make_inputs(*SHAPES[0])[0], w=make_inputs(*SHAPES[0])[1],
+              dy=make_inputs(*SHAPES[0])[2])
+    assert dc.dc_kernel_launches() > before
+    plan = dc.dc_plan_create_virtual(1, 2, 16, 16, 4, 3, 1, 1, (1, 2, 1), 0)
+    with pytest.raises(dc.DCError):   # exchange requested without a communicator
+        xd = dc.dc_plan_query(plan, dc.DC_X)
+        xb = torch.zeros(xd["bytes"] // 2, dtype=torch.bfloat16, device="cuda")
+        dc.dc_conv_fwd(plan, xb, xb, xb, dc.DC_EXCHANGE)
+    dc.dc_plan_destroy(plan)
