@@ -1,0 +1,427 @@
+"""bench.py -- conv fwd+bwd time & TFLOP/s (% peak) of the spatially / hybrid
+partitioned convolution hot path (arXiv:1903.06681) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME]
+  torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+  python bench.py --impl reference ...                      (fp64 CPU oracle arm)
+
+One step = for every layer of the workload: forward (with x halo exchange
+overlapped with interior tiles) + backward (dy halo || filter gradient, then
+data gradient || dW allreduce), i.e. every row of SURVEY.md 8(a) on the
+hot path, through the C ABI (libdconv.so). Global batch fixed as N grows
+(strong scaling); the per-layer decomposition is chosen by the library's
+performance model unless --decomp is given.
+Rank 0 prints ONE JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# (name, N, C, H, W, F, K, S, P)
+WORKLOADS = {
+    # BASELINE.json configs[1]: ResNet-50 conv layers at N=32, 224x224
+    "resnet_layers": [("conv1", 32, 3, 224, 224, 64, 7, 2, 3),
+                      ("res2a_branch2b", 32, 64, 56, 56, 64, 3, 1, 1),
+                      ("res3b_branch2a", 32, 512, 28, 28, 128, 1, 1, 0)],
+    # BASELINE.json configs[3] (per-layer proxy): 2K mesh conv1_1 / conv1_2 at N=1
+    "mesh2k_layers": [("conv1_1", 1, 18, 2048, 2048, 64, 3, 2, 1),
+                      ("conv1_2", 1, 64, 1024, 1024, 64, 3, 1, 1)],
+    # BASELINE.json configs[0]
+    "c1": [("c1", 1, 2, 16, 16, 4, 3, 1, 1)],
+}
+
+
+def layer_flops(l) -> float:
+    """Algorithmic FLOPs of one conv op (fwd; bwd-data and bwd-filter are the
+    same count): 2 N F C K^2 Ho Wo."""
+    _, N, C, H, W, F, K, S, P = l
+    Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
+    return 2.0 * N * F * C * K * K * Ho * Wo
+
+
+def layer_bytes(l, op: str) -> float:
+    """Minimum HBM bytes of one conv op (bf16 in/out once)."""
+    _, N, C, H, W, F, K, S, P = l
+    Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
+    act = 2.0 * (N * H * W * C + N * Ho * Wo * F)
+    return act + (4.0 if op == "bpw" else 2.0) * F * C * K * K
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.proc, self.lines = gpu, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=lambda: self.lines.extend(iter(self.proc.stdout.readline, "")),
+                                      daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        load = [s for s in sm if mx and s > 0.3 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ----------------------------------------------------------------------------
+def oracle_sample(layers, budget_s: float = 15.0):
+    """Times the fp64 oracle (as it stands) on a bounded sample of the
+    workload: for every layer, fwd on the first output rows, bwd-data on the
+    first input rows and a few dW entries, scaled to FLOPs. Returns
+    (flops, seconds, description)."""
+    import numpy as np
+    import datagen
+    import oracle
+    flops = secs = 0.0
+    desc = []
+    per_layer = budget_s / len(layers)
+    for l in layers:
+        name, N, C, H, W, F, K, S, P = l
+        Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
+        n = min(N, 2)
+        x = datagen.gen_x(n, C, H, W)
+        w = datagen.gen_w(F, C, K)
+        dy = datagen.gen_dy(n, F, Ho, Wo)
+        row_flops = 2.0 * n * F * C * K * K * Wo
+        rows = 1
+        t0 = time.perf_counter()
+        oracle.conv_fwd(x, w, S, P, rows=(0, 1))
+        t1 = time.perf_counter() - t0
+        rows = int(max(1, min(Ho - 1, (per_layer / 3) / max(t1, 1e-6))))
+        t0 = time.perf_counter()
+        oracle.conv_fwd(x, w, S, P, rows=(0, rows))
+        oracle.conv_bwd_data(dy, w, H, W, S, P, rows=(0, max(1, rows * S)))
+        nent = 0
+        tb = time.perf_counter()
+        while time.perf_counter() - tb < per_layer / 3 and nent < F * C * K * K:
+            f, c = nent % F, (nent // F) % C
+            oracle.conv_bwd_filter_entry(x, dy, K, S, P, f, c, (nent // (F * C)) % K, 0)
+            nent += 1
+        secs += time.perf_counter() - t0
+        flops += row_flops * rows + 2.0 * n * C * F * K * K * W * max(1, rows * S) / S / S \
+            + 2.0 * n * Ho * Wo * nent
+        desc.append(f"{name}: n={n} fwd rows 0-{rows}, bwd-data rows 0-{max(1, rows * S)}, {nent} dW entries")
+    return flops, secs, "; ".join(desc)
+
+
+def run_reference(args, layers, wl_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    steps = []
+    for _ in range(args.warmup):
+        oracle_sample(layers, budget_s=2.0)
+    desc = ""
+    for _ in range(args.steps):
+        f, s, desc = oracle_sample(layers, budget_s=args.ref_budget)
+        steps.append((f, s))
+    flops = sum(f for f, _ in steps)
+    secs = sum(s for _, s in steps)
+    value = flops / secs / 1e12
+    threads = oracle.num_threads()
+    print(json.dumps({
+        "impl": "reference", "metric": "conv fwd+bwd TFLOP/s", "value": value, "unit": "TFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * secs / max(1, args.steps), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl_name, "layers": [l[0] for l in layers], "global_batch": layers[0][1]},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="resnet_layers", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--decomp", default="auto", help="auto | pn,ph,pw")
+    ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
+    args = ap.parse_args()
+    layers = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, layers, args.workload)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1903_06681_b200 import build
+    build.build()
+    import paper_1903_06681_b200 as dc
+    import datagen
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        uid = [dc.dc_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = dc.dc_comm_create(rank, world, uid[0], local)
+    else:
+        comm = dc.dc_comm_create(0, 1, None, local)
+    stream = torch.cuda.Stream()
+    sp = stream.cuda_stream
+    halo_flag = dc.DC_HALO_NCCL if args.halo == "nccl" else 0
+    FLAGS = dc.DC_EXCHANGE | dc.DC_ALLREDUCE | halo_flag
+
+    # ---- per-layer plans and resident inputs ----
+    L = []
+    for l in layers:
+        name, N, C, H, W, F, K, S, P = l
+        decomp = (0, 0, 0) if args.decomp == "auto" else tuple(int(v) for v in args.decomp.split(","))
+        plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, dc.DC_BF16, comm)
+        chosen, pred = dc.dc_plan_decomp(plan)
+        xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
+        dyd, dxd = dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(plan, dc.DC_DX)
+        xb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_X), (xd["n"], xd["hb"], xd["wb"], xd["c_pad"]))
+        dyb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_DY), (dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]))
+
+        def owned(desc, gen, tid_shape):
+            blk = gen(*tid_shape, n=(desc["n0"], desc["n0"] + desc["n"]), h=(desc["h0"], desc["h0"] + desc["h"]),
+                      w=(desc["w0"], desc["w0"] + desc["w"]))
+            t = np.zeros((desc["n"], desc["h"], desc["w"], desc["c_pad"]), dtype=np.float32)
+            t[..., :desc["c"]] = blk.transpose(0, 2, 3, 1)
+            return torch.tensor(t, dtype=torch.bfloat16)
+
+        Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
+        x_own = owned(xd, datagen.gen_x, (N, C, H, W))
+        dy_own = owned(dyd, datagen.gen_dy, (N, F, Ho, Wo))
+        xb[:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]] = x_own.cuda()
+        dyb[:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]] = dy_own.cuda()
+        wnp = np.zeros((F, K, K, xd["c_pad"]), dtype=np.float32)
+        wnp[..., :C] = datagen.gen_w(F, C, K).transpose(0, 2, 3, 1)
+        wt = torch.tensor(wnp, dtype=torch.bfloat16).cuda()
+        y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
+        dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
+        dw = torch.empty((F, K, K, xd["c_pad"]), dtype=torch.float32, device="cuda")
+        # pinned host copies for the end-to-end leg
+        host = {"x": x_own.pin_memory(), "dy": dy_own.pin_memory(), "w": wt.cpu().pin_memory(),
+                "dw": torch.empty(dw.shape, dtype=torch.float32).pin_memory()}
+        L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
+                      dx=dx, dw=dw, host=host, x_own_dev=x_own.cuda(), dy_own_dev=dy_own.cuda()))
+    torch.cuda.synchronize()
+
+    def step(events=None, e2e=False):
+        for i, d in enumerate(L):
+            xd, dyd = d["xd"], d["dyd"]
+            if e2e:  # inputs arrive from pinned host memory every step
+                xs = d["xb"][:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]]
+                xs.copy_(d["host"]["x"], non_blocking=True)
+                d["dyb"][:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]].copy_(
+                    d["host"]["dy"], non_blocking=True)
+                d["w"].copy_(d["host"]["w"], non_blocking=True)
+            if events is not None:
+                events[i][0].record(stream)
+            dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)
+            if events is not None:
+                events[i][1].record(stream)
+            if world == 1:
+                # no halo / allreduce at one rank: the two backward kernels are
+                # called separately so each gets its own event pair
+                dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["dw"], FLAGS, sp)
+                if events is not None:
+                    events[i][2].record(stream)
+                dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"], FLAGS, sp)
+            else:
+                dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"], d["dx"], d["dw"],
+                               FLAGS, sp)
+                if events is not None:
+                    events[i][2].record(stream)
+            if events is not None:
+                events[i][3].record(stream)
+            if e2e:
+                d["host"]["dw"].copy_(d["dw"], non_blocking=True)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        # ---- timed region: exactly K steps ----
+        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in L] for _ in range(args.steps)]
+        start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        clocks = ClockSampler(local)
+        clocks.start()
+        barrier()
+        torch.cuda.synchronize()
+        launches0 = dc.dc_kernel_launches()
+        start.record(stream)
+        for k in range(args.steps):
+            step(ev[k])
+        stop.record(stream)
+        torch.cuda.synchronize()
+        launches = dc.dc_kernel_launches() - launches0
+        barrier()
+        clk = clocks.stop()
+        ms = start.elapsed_time(stop)
+        # ---- end-to-end leg: same steps with H2D of inputs / D2H of dW ----
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for k in range(args.steps):
+            step(e2e=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms_e2e = e0.elapsed_time(e1)
+
+    t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, ms_e2e = float(t[0]), float(t[1])
+    flops_step = sum(3 * layer_flops(d["l"]) for d in L)
+    value = flops_step * args.steps / (ms / 1e3) / 1e12
+    value_e2e = flops_step * args.steps / (ms_e2e / 1e3) / 1e12
+    h2d = sum(d["host"][k].numel() * d["host"][k].element_size() for d in L for k in ("x", "dy", "w"))
+    d2h = sum(d["host"]["dw"].numel() * 4 for d in L)
+
+    # ---- per-op device times on the launching stream, from the timed steps ----
+    def avg(i, a, b):
+        return statistics.mean(ev[k][i][a].elapsed_time(ev[k][i][b]) for k in range(args.steps))
+    per = []
+    for i, d in enumerate(L):
+        f_ms, w_ms, x_ms = avg(i, 0, 1), avg(i, 1, 2), avg(i, 2, 3)
+        per.append((d, f_ms, w_ms, x_ms))
+    peaks, peak_src = load_peaks()
+    # dominant kernel: the (layer, op) with the largest device time
+    cands = []
+    for d, f_ms, w_ms, x_ms in per:
+        cands.append((f_ms, d, "fp", "conv_gemm_kernel (forward)"))
+        if world == 1:
+            cands.append((w_ms, d, "bpw", "wgrad_kernel (+ split-K reduce)"))
+            cands.append((x_ms, d, "bpx", "conv_gemm_kernel (backward-data, + weight transform)"))
+    op_ms, d, op, kname = max(cands, key=lambda c: c[0])
+    loc = d["l"]
+    # algorithmic work of THIS rank's shard (blocked split: global / world)
+    fl = layer_flops(loc) / world
+    by = layer_bytes(loc, op) / world
+    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if fl / by >= ridge:
+        roof = {"bound": "tensor", "achieved": fl / (op_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
+                "unit": "TFLOP/s"}
+    else:
+        roof = {"bound": "hbm", "achieved": by / (op_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = None
+    roof["kernel"] = f"{loc[0]} {op}: {kname}"
+    roof["avg_launch_ms"] = op_ms
+    roof["peak_source"] = peak_src + " burst (MEASURED_PEAKS.json)"
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            import oracle
+            oracle.build()
+            f, s, desc = oracle_sample(layers, budget_s=15.0)
+            cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
+                   "sample": desc}
+        out = {
+            "metric": "conv fwd+bwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded counter-based generator, bf16-exact values)",
+            "config": {"workload": args.workload, "global_batch": layers[0][1],
+                       "layers": [{"name": d["l"][0], "shape_NCHW_F_K_S_P": list(d["l"][1:]),
+                                   "decomp": list(d["decomp"]), "model_pred_ms": d["pred"] * 1e3,
+                                   "fwd_ms": f_ms, "bwd_ms": w_ms + x_ms, "bwd_filter_ms": w_ms,
+                                   "bwd_data_ms": x_ms,
+                                   "fwd_tflops": layer_flops(d["l"]) / (f_ms / 1e3) / 1e12,
+                                   "bwd_tflops": 2 * layer_flops(d["l"]) / ((w_ms + x_ms) / 1e3) / 1e12}
+                                  for d, f_ms, w_ms, x_ms in per],
+                       "parallelism": "per-layer model-chosen (pN,pH,pW)" if args.decomp == "auto" else args.decomp,
+                       "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
+                       "flops_per_step": flops_step},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": value_e2e, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(out), flush=True)
+    if args.cost_table and rank == 0:
+        with open(args.cost_table, "w") as f:
+            f.write("op,n,c,h,w,f,k,s,pad,seconds\n")
+            for d, f_ms, w_ms, x_ms in per:
+                _, N, C, H, W, F, K, S, P = d["l"]
+                xd = d["xd"]
+                for op, t in (("fp", f_ms), ("bpw", w_ms), ("bpx", x_ms)):
+                    f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{t / 1e3}\n")
+    for d in L:
+        dc.dc_plan_destroy(d["plan"])
+    dc.dc_comm_destroy(comm)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -192,6 +192,25 @@ def dc_buffer_alloc(plan: int, t: int) -> int:
     return out.value
 
 
+class _CudaArray:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def wrap_device_buffer(ptr: int, shape, dtype=None):
+    """Zero-copy torch view of library-owned device memory (e.g. a buffer from
+    dc_buffer_alloc) through __cuda_array_interface__. dtype: torch.bfloat16
+    (default) or torch.float32."""
+    import torch
+    dtype = dtype or torch.bfloat16
+    if dtype == torch.bfloat16:
+        return torch.as_tensor(_CudaArray(ptr, shape, "<u2"), device="cuda").view(torch.bfloat16)
+    if dtype == torch.float32:
+        return torch.as_tensor(_CudaArray(ptr, shape, "<f4"), device="cuda")
+    raise ValueError("dtype must be bfloat16 or float32")
+
+
 def dc_halo_exchange(plan: int, t: int, buf, flags: int = 0, stream=None):
     _check(lib().dc_halo_exchange(plan, t, _ptr(buf), flags, _stream(stream)))
 
