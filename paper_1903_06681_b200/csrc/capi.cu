@@ -15,6 +15,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -23,6 +24,7 @@
 
 #include "common.hpp"
 #include "conv_tc.cuh"
+#include "conv_v2.cuh"
 #include "halo.cuh"
 #include "plan.hpp"
 
@@ -333,9 +335,61 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
 
 // Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
 // box shape is baked into the tensor map).
+bool use_v1() {
+    static const int v = std::getenv("DC_CONV_V1") ? 1 : 0;
+    return v != 0;
+}
+
+// The persistent tile-reuse kernel (conv_v2.cu); false if it does not apply.
+bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
+                     const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
+    if (use_v1() || L.p.T == 0) return false;
+    ConvV2Params q;
+    std::memset(&q, 0, sizeof q);
+    q.s_in = L.p.s_in;
+    q.origin_h = L.p.origin_h;
+    q.origin_w = L.p.origin_w;
+    q.T = L.p.T;
+    std::memcpy(q.tap_h, L.p.tap_h, sizeof q.tap_h);
+    std::memcpy(q.tap_w, L.p.tap_w, sizeof q.tap_w);
+    q.cin_p = (int)cin_p;
+    q.bn = L.p.bn;
+    q.nout_tiles = L.nout_tiles;
+    q.nsamples = nsamples;
+    q.out = L.p.out;
+    q.out_sn = L.p.out_sn, q.out_sh = L.p.out_sh, q.out_sw = L.p.out_sw;
+    q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
+    q.nout_p = L.p.nout_p;
+    if (!conv_v2_configure(q, kV2SmemLimit)) return false;
+    DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
+    q.nrect = (int)rects.size();
+    q.rect_start[0] = 0;
+    for (int r = 0; r < q.nrect; ++r) {
+        q.rect[r] = rects[r];
+        q.rect_tiles_w[r] = (int)ceil_div(rects[r].nw, kV2TW);
+        q.rect_start[r + 1] = q.rect_start[r] + (int)ceil_div(rects[r].nh, kV2TH) * q.rect_tiles_w[r];
+    }
+    q.total_tiles = q.nout_tiles * q.nsamples * q.rect_start[q.nrect];
+    CUtensorMap amap;
+    const uint64_t dims[4] = {(uint64_t)cin_p, (uint64_t)ind.wb, (uint64_t)ind.hb, (uint64_t)ind.n};
+    const uint64_t strides[3] = {(uint64_t)(cin_p * 2), (uint64_t)(ind.wb * cin_p * 2),
+                                 (uint64_t)(ind.hb * ind.wb * cin_p * 2)};
+    if (q.a_swz == 128) {
+        const uint32_t box[4] = {64, 16, (uint32_t)q.PH, 1};
+        make_tmap(&amap, in_base, 4, dims, strides, box, nullptr, 128);
+    } else {
+        const uint32_t box[4] = {8, (uint32_t)(q.PWs * q.s_in), (uint32_t)q.PH, 1};
+        const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
+        make_tmap(&amap, in_base, 4, dims, strides, box, es, 0);
+    }
+    launch_conv_v2(amap, L.bmap, q, st);
+    return true;
+}
+
 void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
                   const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
     if (rects.empty()) return;
+    if (launch_rects_v2(L, rects, in_base, ind, cin_p, nsamples, st)) return;
     std::map<int, std::vector<OutRect>> by_twl;
     for (auto &r : rects) by_twl[pick_twl(r.nh, r.nw, 128)].push_back(r);
     for (auto &kv : by_twl) {

@@ -1,0 +1,469 @@
+// conv_v2.cu -- persistent tile-reuse implicit-GEMM convolution on sm_100a
+// (forward Eq. 1 PAPER.md:61 and backward-data Eq. 3).
+//
+// Warp roles (192 threads, 1 CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: per tile and channel group, the halo'd input
+//               tile as 16-byte core-matrix planes (one box per 8-channel
+//               chunk and column parity); weights either resident (loaded
+//               once) or streamed per (tap, channel group) through a ring.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer: for each
+//               tap, the A descriptor is the same smem tile at a shifted
+//               start address (no data movement per tap).
+//   warps 2-5   epilogue: tcgen05.ld (32 lanes x 16 cols) -> bf16 -> NHWC
+//               global stores; double-buffered TMEM accumulators let the
+//               epilogue of tile i overlap the MMAs of tile i+1.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "common.hpp"
+#include "conv_v2.cuh"
+#include "sm100.cuh"
+
+namespace dc {
+using namespace sm100;
+
+namespace {
+__device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
+    const uint32_t a = smem_u32(p);
+    return p + ((1024 - (a & 1023)) & 1023);
+}
+__device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+__host__ __device__ inline uint32_t pow2_cols(int n) {
+    uint32_t c = 32;
+    while ((int)c < n) c <<= 1;
+    return c;
+}
+struct TileCoord {
+    int o0, n, i0, j0, r;
+};
+__device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
+    const int per_o = p.nsamples * p.rect_start[p.nrect];
+    TileCoord c;
+    const int ot = u / per_o;
+    int rem = u - ot * per_o;
+    c.n = rem / p.rect_start[p.nrect];
+    const int lt = rem - c.n * p.rect_start[p.nrect];
+    int r = 0;
+    while (r + 1 < p.nrect && lt >= p.rect_start[r + 1]) ++r;
+    const int t = lt - p.rect_start[r];
+    c.r = r;
+    c.i0 = p.rect[r].h0 + (t / p.rect_tiles_w[r]) * kV2TH;
+    c.j0 = p.rect[r].w0 + (t % p.rect_tiles_w[r]) * kV2TW;
+    c.o0 = ot * p.bn;
+    return c;
+}
+}  // namespace
+
+constexpr int kMaxBar = 16;
+
+// Fully unrolled MMA issue for one channel group of one tile (resident
+// weights): every descriptor offset is a compile-time multiple of a runtime
+// stride hoisted out of the loop, so the single issuing thread spends a few
+// uniform instructions per tcgen05.mma instead of a dependent chain of
+// constant loads and 64-bit adds per tap (measured: ~180 cycles per tap).
+template <int KH, int KW, int NK, int SSH>
+__device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, uint64_t bd,
+                                           uint32_t a_row16, uint32_t a_col16, uint32_t a_par16,
+                                           uint32_t a_kstep, uint32_t b_slot16, uint32_t idesc,
+                                           bool first_group) {
+#pragma unroll
+    for (int th = 0; th < KH; ++th)
+#pragma unroll
+        for (int tw = 0; tw < KW; ++tw) {
+            const uint64_t ad = a_stage + (uint32_t)th * a_row16 + (uint32_t)(tw >> SSH) * a_col16 +
+                                (uint32_t)(tw & SSH) * a_par16;
+            const uint64_t b = bd + (uint32_t)(th * KW + tw) * b_slot16;
+#pragma unroll
+            for (int k = 0; k < NK; ++k)
+                mma_bf16(d_tmem, ad + (uint32_t)k * a_kstep, b + 2 * k, idesc,
+                         (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
+        }
+}
+
+// Dispatch to an unrolled specialisation; false if none matches.
+__device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16, uint32_t d_tmem,
+                                                 uint64_t a_stage, uint64_t bd, uint32_t a_kstep,
+                                                 uint32_t b_slot16, uint32_t idesc, bool first) {
+    const int key = (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
+#define DC_TAPS(KH, KW, NK, SS)                                                                  \
+    case ((KH << 12) | (KW << 8) | (NK << 4) | SS):                                              \
+        issue_taps<KH, KW, NK, SS>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16, a_kstep, \
+                                   b_slot16, idesc, first);                                      \
+        return true;
+    switch (key) {
+        DC_TAPS(3, 3, 4, 0)  // 3x3 stride 1, 64-channel groups (fwd and bwd-data)
+        DC_TAPS(1, 1, 4, 0)  // 1x1 (fwd, bwd-data, stride-2 phase)
+        DC_TAPS(3, 3, 1, 0)
+        DC_TAPS(3, 3, 2, 0)
+        DC_TAPS(5, 5, 4, 0)
+        DC_TAPS(7, 7, 1, 1)  // ResNet conv1 forward (C=3 -> 16, stride 2)
+        DC_TAPS(3, 3, 2, 1)  // mesh conv1_1 forward (C=18 -> 32, stride 2)
+        DC_TAPS(3, 3, 4, 1)  // 3x3 stride-2 forward, 64-channel groups (planes)
+        DC_TAPS(4, 4, 4, 0)  // conv1 backward-data phases (7x7 / 2)
+        DC_TAPS(4, 3, 4, 0)
+        DC_TAPS(3, 4, 4, 0)
+        DC_TAPS(2, 2, 4, 0)  // 3x3 / 2 backward-data phases
+        DC_TAPS(2, 1, 4, 0)
+        DC_TAPS(1, 2, 4, 0)
+    default:
+        return false;
+    }
+#undef DC_TAPS
+}
+
+
+__global__ void __launch_bounds__(192, 1)
+    conv_v2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
+                   const __grid_constant__ ConvV2Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = align1024(smem_raw);
+    uint8_t *sB = smem;  // B first: its slots need 1024-byte alignment (swizzle)
+    const int b_bytes = p.b_resident ? p.T * p.ncg * p.b_slot_bytes : p.b_stages * p.b_slot_bytes;
+    uint8_t *sA = sB + b_bytes;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sA + p.a_stages * p.a_stage_bytes);
+    uint64_t *a_full = bars, *a_empty = bars + kMaxBar;
+    uint64_t *b_full = bars + 2 * kMaxBar, *b_empty = bars + 3 * kMaxBar;
+    uint64_t *acc_full = bars + 4 * kMaxBar, *acc_empty = acc_full + 2;
+    uint64_t *b_res = acc_empty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_res + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t acc_cols = pow2_cols(p.bn);
+    const uint32_t ncols = 2 * acc_cols;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.a_stages; ++s) {
+            mbar_init(&a_full[s], 1);
+            mbar_init(&a_empty[s], 1);
+        }
+        for (int s = 0; s < p.b_stages; ++s) {
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&acc_full[s], 1);
+            mbar_init(&acc_empty[s], 4);
+        }
+        mbar_init(b_res, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, ncols);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int total = p.total_tiles;
+
+    if (warp == 0) {
+        // ============ TMA producer: the whole warp runs the (warp-uniform) ============
+        // ============ loop, one elected lane issues the copies             ============
+        if (elect_one()) {
+            tma_prefetch(&amap);
+            tma_prefetch(&bmap);
+        }
+        int cur_o0 = -1;
+        int a_it = 0, b_it = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+            const TileCoord c = decode(p, u);
+            if (p.b_resident && c.o0 != cur_o0) {
+                // (a resident weight tile never changes for a CTA: nout_tiles == 1)
+                if (elect_one()) {
+                    mbar_arrive_expect_tx(b_res, p.T * p.ncg * p.bn * p.cg * 2);
+                    for (int g = 0; g < p.ncg; ++g)
+                        for (int t = 0; t < p.T; ++t)
+                            tma_load_2d(sB + (g * p.T + t) * p.b_slot_bytes, &bmap, b_res,
+                                        t * p.cin_p + g * p.cg, c.o0);
+                }
+                __syncwarp();
+                cur_o0 = c.o0;
+            }
+            const int h0 = p.s_in * c.i0 + p.origin_h, w0 = p.s_in * c.j0 + p.origin_w;
+            for (int g = 0; g < p.ncg; ++g) {
+                const int s = a_it % p.a_stages;
+                if (a_it >= p.a_stages) mbar_wait(&a_empty[s], ((a_it / p.a_stages) - 1) & 1);
+                if (elect_one()) {
+                    uint8_t *dst = sA + s * p.a_stage_bytes;
+                    if ((p.dbg & 1) && a_it >= p.a_stages) {
+                        mbar_arrive(&a_full[s]);
+                    } else if (p.a_swz == 128) {
+                        // one box: PH rows x 16 cols x 64 channels (128-byte swizzled rows)
+                        mbar_arrive_expect_tx(&a_full[s], p.PH * p.PWs * 128);
+                        tma_load_4d(dst, &amap, &a_full[s], g * p.cg, w0, h0, c.n);
+                    } else {
+                        mbar_arrive_expect_tx(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
+                        for (int k8 = 0; k8 < p.cg / 8; ++k8)
+                            for (int par = 0; par < p.s_in; ++par)
+                                tma_load_4d(dst + (k8 * p.s_in + par) * p.plane_bytes, &amap,
+                                            &a_full[s], g * p.cg + k8 * 8, w0 + par, h0, c.n);
+                    }
+                }
+                __syncwarp();
+                ++a_it;
+                if (!p.b_resident) {
+                    for (int t = 0; t < p.T; ++t) {
+                        const int sb = b_it % p.b_stages;
+                        if (b_it >= p.b_stages) mbar_wait(&b_empty[sb], ((b_it / p.b_stages) - 1) & 1);
+                        if (elect_one()) {
+                            mbar_arrive_expect_tx(&b_full[sb], p.bn * p.cg * 2);
+                            tma_load_2d(sB + sb * p.b_slot_bytes, &bmap, &b_full[sb],
+                                        t * p.cin_p + g * p.cg, c.o0);
+                        }
+                        __syncwarp();
+                        ++b_it;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============ tcgen05.mma issuer: warp-uniform loop, elected lane issues ============
+        // Descriptor arithmetic: the start-address field is bits [0,14) in 16-byte
+        // units and never carries (smem < 256 KB), so an operand at byte offset
+        // `off` from a base descriptor is base + (off >> 4).
+        const uint32_t idesc = idesc_bf16(128, p.bn, 0, 0);
+        const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
+        const uint64_t a_desc0 = p.a_swz == 128
+                                     ? smem_desc(sA_u, 16, 16 * 128, 2)  // SBO: next output row
+                                     : smem_desc(sA_u, p.s_in * p.plane_bytes, p.s_in * p.PWs * 16, 0);
+        const uint64_t b_desc0 = smem_desc(sB_u, 16, 8 * p.cg * 2, swizzle_layout(p.cg * 2));
+        const uint32_t a_kstep = p.a_kstep16, b_slot16 = p.b_slot_bytes >> 4;
+        const int nk16 = p.cg / 16;
+        const bool do_mma = !(p.dbg & 4);
+        int a_it = 0, b_it = 0, acc_it = 0;
+        bool res_ready = false;
+        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+            if (p.b_resident && !res_ready) {
+                mbar_wait(b_res, 0);
+                res_ready = true;
+            }
+            const int acc = acc_it & 1;
+            const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && lane == 0;
+            if (tr) p.dbg_out[acc_it * 8 + 0] = clock64();
+            if (acc_it >= 2) mbar_wait(&acc_empty[acc], ((acc_it >> 1) - 1) & 1);
+            if (tr) p.dbg_out[acc_it * 8 + 1] = clock64();
+            tc_fence_after();
+            const uint32_t d_tmem = tmem + acc * acc_cols;
+            for (int g = 0; g < p.ncg; ++g) {
+                const int s = a_it % p.a_stages;
+                mbar_wait(&a_full[s], (a_it / p.a_stages) & 1);
+                if (tr && g == 0) p.dbg_out[acc_it * 8 + 2] = clock64();
+                tc_fence_after();
+                const uint64_t a_stage = a_desc0 + ((uint32_t)(s * p.a_stage_bytes) >> 4);
+                if (p.b_resident) {
+                    if (elect_one()) {
+                        uint64_t bd = b_desc0 + (uint32_t)(g * p.T) * b_slot16;
+                        if (!do_mma ||
+                            !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16, idesc, g == 0)) {
+                        uint64_t arow = a_stage;
+                        for (int th = 0; th < p.kh; ++th) {
+                            for (int tw = 0; tw < p.kw; ++tw) {
+                                const uint64_t ad = arow + (uint32_t)(tw >> p.s_shift) * p.a_col16 +
+                                                    (uint32_t)(tw & p.s_shift) * p.a_par16;
+                                for (int k16 = 0; k16 < nk16; ++k16)
+                                    if (do_mma)
+                                        mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
+                                                 (g | th | tw | k16) != 0);
+                                bd += b_slot16;
+                            }
+                            arow += p.a_row16;
+                        }
+                        }
+                        mma_commit(&a_empty[s]);
+                    }
+                    __syncwarp();
+                } else {
+                    for (int t = 0; t < p.T; ++t) {
+                        const int sb = b_it % p.b_stages;
+                        mbar_wait(&b_full[sb], (b_it / p.b_stages) & 1);
+                        tc_fence_after();
+                        if (elect_one()) {
+                            const int th = t / p.kw, tw = t - th * p.kw;
+                            const uint64_t ad = a_stage + (uint32_t)th * p.a_row16 +
+                                                (uint32_t)(tw >> p.s_shift) * p.a_col16 +
+                                                (uint32_t)(tw & p.s_shift) * p.a_par16;
+                            const uint64_t bd = b_desc0 + (uint32_t)sb * b_slot16;
+                            for (int k16 = 0; k16 < nk16; ++k16)
+                                if (do_mma)
+                                    mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
+                                             (g | t | k16) != 0);
+                            mma_commit(&b_empty[sb]);
+                        }
+                        __syncwarp();
+                        ++b_it;
+                    }
+                    if (elect_one()) mma_commit(&a_empty[s]);
+                    __syncwarp();
+                }
+                ++a_it;
+            }
+            if (elect_one()) mma_commit(&acc_full[acc]);
+            __syncwarp();
+            if (tr) p.dbg_out[acc_it * 8 + 3] = clock64();
+            ++acc_it;
+        }
+    } else {
+        // ========================= epilogue =========================
+        const int eq = warp & 3;  // TMEM lane quarter this warp may access
+        const int m = eq * 32 + lane;
+        const int ti = m >> 3, tj = m & 7;
+        int acc_it = 0;
+        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+            const TileCoord c = decode(p, u);
+            const int acc = acc_it & 1;
+            const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
+            if (tr) p.dbg_out[acc_it * 8 + 4] = clock64();
+            mbar_wait(&acc_full[acc], (acc_it >> 1) & 1);
+            if (tr) p.dbg_out[acc_it * 8 + 5] = clock64();
+            tc_fence_after();
+            const int i = c.i0 + ti, j = c.j0 + tj;
+            const bool valid = i < p.rect[c.r].h0 + p.rect[c.r].nh && j < p.rect[c.r].w0 + p.rect[c.r].nw;
+            __nv_bfloat16 *orow = p.out + (long long)c.n * p.out_sn +
+                                  (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+                                  (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0;
+            const uint32_t t_lane = tmem + acc * acc_cols + ((uint32_t)(eq * 32) << 16);
+            for (int c16 = 0; c16 < p.bn / 16; ++c16) {
+                uint32_t v[16];
+                tmem_ld16(t_lane + c16 * 16, v);
+                tmem_ld_wait();
+                if (valid && c.o0 + c16 * 16 < p.nout_p && !(p.dbg & 2)) {
+                    uint4 lo, hi;
+                    lo.x = pack2(v[0], v[1]);
+                    lo.y = pack2(v[2], v[3]);
+                    lo.z = pack2(v[4], v[5]);
+                    lo.w = pack2(v[6], v[7]);
+                    hi.x = pack2(v[8], v[9]);
+                    hi.y = pack2(v[10], v[11]);
+                    hi.z = pack2(v[12], v[13]);
+                    hi.w = pack2(v[14], v[15]);
+                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
+                    dst[0] = lo;
+                    dst[1] = hi;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (tr) p.dbg_out[acc_it * 8 + 6] = clock64();
+            ++acc_it;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) tmem_dealloc(tmem, ncols);
+}
+
+// ---------------------------------------------------------------------------
+size_t conv_v2_smem_bytes(const ConvV2Params &p) {
+    const size_t b = p.b_resident ? (size_t)p.T * p.ncg * p.b_slot_bytes : (size_t)p.b_stages * p.b_slot_bytes;
+    return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16;
+}
+
+bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
+    int kh = 1, kw = 1;
+    for (int t = 0; t < p.T; ++t) {
+        kh = std::max(kh, (int)p.tap_h[t] + 1);
+        kw = std::max(kw, (int)p.tap_w[t] + 1);
+    }
+    p.cg = p.cin_p % 64 == 0 ? 64 : p.cin_p % 32 == 0 ? 32 : 16;
+    p.ncg = p.cin_p / p.cg;
+    p.PH = p.s_in * (kV2TH - 1) + kh;
+    static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
+    static const int dbg = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
+    p.dbg = dbg;
+    if (!force_planes && p.cg == 64 && p.s_in == 1 && kV2TW + kw - 1 <= 16) {
+        p.a_swz = 128;
+        p.PWs = 16;
+        p.plane_bytes = p.PH * 16 * 128;
+        p.a_stage_bytes = p.plane_bytes;
+    } else {
+        p.a_swz = 0;
+        p.PWs = kV2TW + (kw - 1) / p.s_in;
+        if (p.PWs * p.s_in > 256 || p.PH > 256) return false;
+        p.plane_bytes = (int)round_up((int64_t)p.PH * p.PWs * 16, 128);
+        p.a_stage_bytes = (p.cg / 8) * p.s_in * p.plane_bytes;
+    }
+    p.kh = kh;
+    p.kw = kw;
+    for (int t = 0; t < p.T; ++t)  // the tap list must be the row-major (th, tw) grid
+        if (p.tap_h[t] != t / kw || p.tap_w[t] != t % kw || p.T != kh * kw) return false;
+    p.s_shift = p.s_in == 2 ? 1 : 0;
+    if (p.a_swz == 128) {
+        p.a_row16 = (16 * 128) >> 4;
+        p.a_col16 = 128 >> 4;
+        p.a_par16 = 0;
+    } else {
+        p.a_row16 = (p.PWs * 16) >> 4;
+        p.a_col16 = 1;
+        p.a_par16 = p.plane_bytes >> 4;
+    }
+    p.a_kstep16 = p.a_swz == 128 ? 32 >> 4 : (2 * p.s_in * p.plane_bytes) >> 4;
+    p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
+    const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16;
+    const int resident_b = p.T * p.ncg * p.b_slot_bytes;
+    // prefer resident weights with >= 2 A stages
+    if (p.nout_tiles == 1 && resident_b + 2 * p.a_stage_bytes + fixed <= smem_limit &&
+        resident_b <= 160 * 1024) {
+        p.b_resident = 1;
+        p.b_stages = 0;
+        p.a_stages = std::min(4, (smem_limit - fixed - resident_b) / p.a_stage_bytes);
+    } else {
+        p.b_resident = 0;
+        p.a_stages = 2;
+        p.b_stages = std::min(8, (smem_limit - fixed - 2 * p.a_stage_bytes) / p.b_slot_bytes);
+        if (p.b_stages < 2) {
+            p.a_stages = 1;  // (cannot happen for cg <= 64, bn <= 256)
+            p.b_stages = std::min(8, (smem_limit - fixed - p.a_stage_bytes) / p.b_slot_bytes);
+        }
+        if (p.b_stages < 2) return false;
+    }
+    return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
+}
+
+int device_sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p,
+                    cudaStream_t st) {
+    if (p.total_tiles == 0) return;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(conv_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+    });
+    const int grid = std::min(p.total_tiles, device_sm_count());
+    if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
+        ConvV2Params q = p;
+        cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
+        cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));
+        conv_v2_kernel<<<grid, 192, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
+        cudaStreamSynchronize(st);
+        long long h[64 * 8];
+        cudaMemcpy(h, q.dbg_out, sizeof h, cudaMemcpyDeviceToHost);
+        cudaFree(q.dbg_out);
+        long long t0 = h[0];
+        fprintf(stderr, "trace (cycles from first stamp): mma[acc_wait0, acc_ok, afull_ok, committed] epi[wait0, acc_ok, arrived]\n");
+        for (int i = 0; i < 12; ++i)
+            fprintf(stderr, "tile %2d: mma %7lld %7lld %7lld %7lld | epi %7lld %7lld %7lld\n", i, h[i * 8] - t0,
+                    h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
+                    h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
+    } else {
+        conv_v2_kernel<<<grid, 192, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
+    }
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
+}  // namespace dc
