@@ -26,6 +26,7 @@
 #include "conv_tc.cuh"
 #include "conv_v2.cuh"
 #include "halo.cuh"
+#include "wgrad_v2.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -665,6 +666,57 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t xd = describe(rp, DC_X), dyd = describe(rp, DC_DY);
+    const int64_t ho = rp.h.out.size(), wo = rp.w.out.size(), nl = rp.nrange.size();
+    const __nv_bfloat16 *dy_owned = reinterpret_cast<const __nv_bfloat16 *>(dy) +
+                                    (dyd.halo_n * dyd.wb + dyd.halo_w) * g.Fp;
+    if (!use_v1() && g.Cp % 64 == 0 && g.Fp % 64 == 0) {
+        // tile-reuse kernel (wgrad_v2.cu)
+        WgradV2Params q;
+        std::memset(&q, 0, sizeof q);
+        q.s_in = g.S;
+        q.origin_h = (int)(g.S * rp.h.out.lo - g.P - rp.h.xbuf.lo);
+        q.origin_w = (int)(g.S * rp.w.out.lo - g.P - rp.w.xbuf.lo);
+        q.kh = q.kw = g.K;
+        q.T = g.K * g.K;
+        q.F = (int)g.F, q.Fp = (int)g.Fp, q.cp = (int)g.Cp;
+        if (wgrad_v2_configure(q, kV2SmemLimit)) {
+            q.tiles_h = (int)ceil_div(ho, 8);
+            q.tiles_w = (int)ceil_div(wo, 8);
+            q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
+            const int mgroups = (int)ceil_div(q.n_mtiles, q.G), ntiles = (int)ceil_div(g.Fp, q.bn);
+            const long long per_split = (long long)g.F * q.T * g.Cp;
+            int splits = (int)ceil_div(device_sm_count(), (int64_t)mgroups * ntiles);
+            splits = std::max(1, std::min(splits, std::max(1, q.nblocks / 2)));
+            while (splits > 1 && (size_t)splits * per_split * 4 > ((size_t)1 << 30)) --splits;
+            q.splits = splits;
+            q.ws_split = per_split;
+            if (splits > 1) {
+                ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * per_split * 4);
+                q.ws = pl->ws;
+            } else {
+                q.ws = dw;
+            }
+            CUtensorMap xmap, dymap;
+            {
+                const uint64_t dims[4] = {(uint64_t)g.Cp, (uint64_t)xd.wb, (uint64_t)xd.hb, (uint64_t)xd.n};
+                const uint64_t strides[3] = {(uint64_t)(g.Cp * 2), (uint64_t)(xd.wb * g.Cp * 2),
+                                             (uint64_t)(xd.hb * xd.wb * g.Cp * 2)};
+                const uint32_t box[4] = {64, (uint32_t)(16 * g.S), (uint32_t)q.PH, 1};
+                const uint32_t es[4] = {1, (uint32_t)g.S, 1, 1};
+                make_tmap(&xmap, x, 4, dims, strides, box, es, 128);
+            }
+            {
+                const uint64_t dims[4] = {(uint64_t)g.Fp, (uint64_t)wo, (uint64_t)ho, (uint64_t)nl};
+                const uint64_t strides[3] = {(uint64_t)(g.Fp * 2), (uint64_t)(dyd.wb * g.Fp * 2),
+                                             (uint64_t)(dyd.hb * dyd.wb * g.Fp * 2)};
+                const uint32_t box[4] = {64, 8, 8, 1};
+                make_tmap(&dymap, dy_owned, 4, dims, strides, box, nullptr, 128);
+            }
+            launch_wgrad_v2(xmap, dymap, q, st);
+            if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+            return;
+        }
+    }
     WgradParams p;
     std::memset(&p, 0, sizeof p);
     p.T = g.K * g.K;
@@ -682,7 +734,6 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     p.s_in = g.S;
     p.origin_h = (int)(g.S * rp.h.out.lo - g.P - rp.h.xbuf.lo);
     p.origin_w = (int)(g.S * rp.w.out.lo - g.P - rp.w.xbuf.lo);
-    const int64_t ho = rp.h.out.size(), wo = rp.w.out.size(), nl = rp.nrange.size();
     p.tw_log2 = pick_twl(ho, wo, 64);
     const int tw = 1 << p.tw_log2, th = 64 >> p.tw_log2;
     p.tiles_h = (int)ceil_div(ho, th);
@@ -708,8 +759,6 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     CUtensorMap xmap, dymap;
     nhwc_map(&xmap, x, xd.n, xd.hb, xd.wb, g.Cp, xd.wb, xd.hb * xd.wb, p.bkc, tw, th, g.S);
     // dy WITHOUT its halo: a map over the owned block only
-    const __nv_bfloat16 *dy_owned = reinterpret_cast<const __nv_bfloat16 *>(dy) +
-                                    (dyd.halo_n * dyd.wb + dyd.halo_w) * g.Fp;
     nhwc_map(&dymap, dy_owned, nl, ho, wo, g.Fp, dyd.wb, dyd.hb * dyd.wb, p.bf, tw, th, 1);
     launch_wgrad(xmap, dymap, p, m_tiles, n_tiles, st);
     if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);

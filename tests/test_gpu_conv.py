@@ -73,6 +73,10 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     (1, 64, 12, 12, 320, 3, 1, 1),     # F > 256: two N tiles
     (1, 18, 33, 35, 64, 3, 2, 1),      # mesh conv1_1-like (C=18)
     (3, 16, 9, 9, 16, 3, 1, 0),        # P=0 (valid conv)
+    (2, 64, 17, 19, 64, 3, 2, 1),      # stride 2, 64-channel groups (wgrad parity planes)
+    (1, 128, 9, 11, 64, 3, 1, 1),      # two channel groups: 18 atoms across groups
+    (1, 192, 10, 10, 64, 1, 2, 0),     # 1x1 stride 2, three channel groups (odd atom count)
+    (2, 64, 20, 20, 128, 5, 1, 2),     # K=5 (25 taps)
 ]
 
 
