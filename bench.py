@@ -28,12 +28,33 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # (name, N, C, H, W, F, K, S, P)
+def mesh_stack(size: int = 2048, n: int = 1, blocks: int = 6, per_block: int = 5):
+    """The mesh-tangling CNN's conv stack: six blocks of three
+    (1K) or five (2K) 3x3 convolutions, the first of each block stride 2, and
+    a final prediction conv. The widths are not in the paper (lost figures):
+    DESIGN.md reading R20 (F = 64, 128, 256, 512, 512, 512; final 1x1 -> 2)."""
+    widths = [64, 128, 256, 512, 512, 512][:blocks]
+    layers, c, h = [], 18, size
+    for b, f in enumerate(widths, 1):
+        for k in range(1, per_block + 1):
+            s = 2 if k == 1 else 1
+            layers.append((f"conv{b}_{k}", n, c, h, h, f, 3, s, 1))
+            h = (h + 2 - 3) // s + 1
+            c = f
+    layers.append(("pred", n, c, h, h, 2, 1, 1, 0))
+    return layers
+
+
 WORKLOADS = {
+    # BASELINE.json configs[3]: 2K mesh-tangling CNN conv stack, N=1 (spatial strong scaling)
+    "mesh2k": mesh_stack(2048, 1),
+    "mesh2k_n8": mesh_stack(2048, 8),
+    "mesh1k": mesh_stack(1024, 1, per_block=3),
     # BASELINE.json configs[1]: ResNet-50 conv layers at N=32, 224x224
     "resnet_layers": [("conv1", 32, 3, 224, 224, 64, 7, 2, 3),
                       ("res2a_branch2b", 32, 64, 56, 56, 64, 3, 1, 1),
                       ("res3b_branch2a", 32, 512, 28, 28, 128, 1, 1, 0)],
-    # BASELINE.json configs[3] (per-layer proxy): 2K mesh conv1_1 / conv1_2 at N=1
+    # per-layer proxies of configs[3]
     "mesh2k_layers": [("conv1_1", 1, 18, 2048, 2048, 64, 3, 2, 1),
                       ("conv1_2", 1, 64, 1024, 1024, 64, 3, 1, 1)],
     # BASELINE.json configs[0]
@@ -65,50 +86,60 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """nvidia-smi clocks + throttle reasons sampled (every 100 ms) during the
+    timed region. Field names differ across drivers: probe and fall back."""
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    VARIANTS = [",".join(["clocks.sm", "clocks.max.sm"] + [f"clocks_event_reasons.{r}" for r in REASONS]),
+                ",".join(["clocks.sm", "clocks.max.sm"] + [f"clocks_throttle_reasons.{r}" for r in REASONS]),
+                "clocks.sm,clocks.max.sm"]
 
     def __init__(self, gpu: int):
-        self.gpu, self.proc, self.lines = gpu, None, []
+        self.gpu, self.proc, self.lines, self.q = gpu, None, [], None
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=lambda: self.lines.extend(iter(self.proc.stdout.readline, "")),
-                                      daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        for q in self.VARIANTS:
+            try:
+                r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                    "--format=csv,noheader,nounits"],
+                                   capture_output=True, text=True, timeout=20)
+                if r.returncode == 0 and "," in r.stdout:
+                    self.q = q
+                    break
+            except Exception:
+                return
+        if self.q is None:
+            return
+        self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.q}",
+                                      "--format=csv,noheader,nounits", "-lms", "100"],
+                                     stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self.t = threading.Thread(target=lambda: self.lines.extend(iter(self.proc.stdout.readline, "")),
+                                  daemon=True)
+        self.t.start()
+        time.sleep(0.3)
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except (ValueError, IndexError):
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(self.REASONS, f[2:]):
                 if v.lower() == "active":
                     reasons.add(n)
         load = [s for s in sm if mx and s > 0.3 * mx] or sm
         return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "fields": self.q}
 
 
 # ----------------------------------------------------------------------------
@@ -116,10 +147,11 @@ class ClockSampler:
 # ----------------------------------------------------------------------------
 def oracle_sample(layers, budget_s: float = 15.0):
     """Times the fp64 oracle (as it stands) on a bounded sample of the
-    workload: for every layer, fwd on the first output rows, bwd-data on the
-    first input rows and a few dW entries, scaled to FLOPs. Returns
-    (flops, seconds, description)."""
-    import numpy as np
+    workload: for every layer, Eq. 1 on its first output rows, on inputs
+    generated only for the rows they read (the 2K-mesh tensors are never
+    materialised on the host). fwd, bwd-data and bwd-filter have the same
+    algorithmic FLOPs, so the rate transfers to the fwd+bwd metric.
+    Returns (algorithmic FLOPs computed, seconds, description)."""
     import datagen
     import oracle
     flops = secs = 0.0
@@ -129,29 +161,16 @@ def oracle_sample(layers, budget_s: float = 15.0):
         name, N, C, H, W, F, K, S, P = l
         Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
         n = min(N, 2)
-        x = datagen.gen_x(n, C, H, W)
-        w = datagen.gen_w(F, C, K)
-        dy = datagen.gen_dy(n, F, Ho, Wo)
         row_flops = 2.0 * n * F * C * K * K * Wo
-        rows = 1
-        t0 = time.perf_counter()
-        oracle.conv_fwd(x, w, S, P, rows=(0, 1))
-        t1 = time.perf_counter() - t0
-        rows = int(max(1, min(Ho - 1, (per_layer / 3) / max(t1, 1e-6))))
+        rows = int(max(1, min(Ho, per_layer / (row_flops / (1e9 * oracle.num_threads())))))
+        x = datagen.gen_x(N, C, H, W, n=(0, n), h=(0, min(H, S * rows - P + K)))
+        w = datagen.gen_w(F, C, K)
         t0 = time.perf_counter()
         oracle.conv_fwd(x, w, S, P, rows=(0, rows))
-        oracle.conv_bwd_data(dy, w, H, W, S, P, rows=(0, max(1, rows * S)))
-        nent = 0
-        tb = time.perf_counter()
-        while time.perf_counter() - tb < per_layer / 3 and nent < F * C * K * K:
-            f, c = nent % F, (nent // F) % C
-            oracle.conv_bwd_filter_entry(x, dy, K, S, P, f, c, (nent // (F * C)) % K, 0)
-            nent += 1
         secs += time.perf_counter() - t0
-        flops += row_flops * rows + 2.0 * n * C * F * K * K * W * max(1, rows * S) / S / S \
-            + 2.0 * n * Ho * Wo * nent
-        desc.append(f"{name}: n={n} fwd rows 0-{rows}, bwd-data rows 0-{max(1, rows * S)}, {nent} dW entries")
-    return flops, secs, "; ".join(desc)
+        flops += row_flops * rows
+        desc.append(f"{name}[n={n},rows 0-{rows}]")
+    return flops, secs, "Eq.1 output rows of every layer: " + " ".join(desc)
 
 
 def run_reference(args, layers, wl_name):
@@ -191,7 +210,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="resnet_layers", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="mesh2k", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="auto", help="auto | pn,ph,pw")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
