@@ -104,7 +104,9 @@ struct dc_plan_s {
     bool can_flush = false;
     __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases
     size_t wt_bytes = 0;
-    float *ws = nullptr;             // split-K workspace
+    float *ws = nullptr;             // split-K workspace (backward-filter)
+    size_t ws2_bytes = 0;
+    float *ws2 = nullptr;            // split-K workspace (forward / backward-data)
     size_t ws_bytes = 0;
     double *bn_part = nullptr;
     size_t bn_part_bytes = 0;
@@ -121,6 +123,7 @@ struct dc_plan_s {
         if (flags) cudaFree(flags);
         if (wt) cudaFree(wt);
         if (ws) cudaFree(ws);
+        if (ws2) cudaFree(ws2);
         if (bn_part) cudaFree(bn_part);
         if (bn_sums) cudaFree(bn_sums);
         for (auto e : ev)
@@ -242,6 +245,19 @@ void make_rects(const Split2D &s, std::vector<OutRect> &interior, std::vector<Ou
     add(boundary, bl, s.nw - bwh, ih, bwh);
 }
 
+// The whole output grid of a launch (union of its interior and boundary rects):
+// used when there is no exchange to overlap, so all tiles run in one launch.
+struct GemmLaunch;
+OutRect whole_of(const std::vector<OutRect> &a, const std::vector<OutRect> &b) {
+    int h = 0, w = 0;
+    for (auto *v : {&a, &b})
+        for (auto &r : *v) {
+            h = std::max(h, r.h0 + r.nh);
+            w = std::max(w, r.w0 + r.nw);
+        }
+    return OutRect{0, 0, h, w};
+}
+
 void set_rects(ConvGemmParams &p, const std::vector<OutRect> &rects) {
     DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
     p.nrect = (int)rects.size();
@@ -283,7 +299,37 @@ struct GemmLaunch {
     ConvGemmParams p;
     std::vector<OutRect> interior, boundary;
     int nout_tiles = 0;
+    const void *w_base = nullptr;  // B matrix [w_rows][w_kcols] (for re-tiling N)
+    int64_t w_rows = 0, w_kcols = 0;
+    int ksplit = 1;            // v2 split-K over channel groups (from the GLOBAL shape)
+    float *ws = nullptr;       // its fp32 partials
+    int ws_h = 0, ws_w = 0;
 };
+
+OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
+
+// Split-K over channel groups for the v2 kernel, chosen from the GLOBAL problem
+// (tiles of the unpartitioned layer) so that every decomposition sums each
+// output element in the same order (partitioned == 1 GPU, bitwise).
+bool use_v1();
+int choose_ksplit(int64_t global_tiles, int64_t cin_p) {
+    if (use_v1()) return 1;
+    const int ncg = (int)(cin_p / pick_bkc(cin_p));
+    int k = 1;
+    while (2 * k <= ncg && ncg % (2 * k) == 0 && global_tiles * 2 * k <= device_sm_count() * 3 / 2) k *= 2;
+    return k;
+}
+size_t ksplit_bytes(const GemmLaunch &L, int nl) {
+    const OutRect b = whole(L);
+    return L.ksplit > 1 ? (size_t)L.ksplit * nl * b.nh * b.nw * L.p.nout_p * 4 : 0;
+}
+void attach_ksplit(dc_plan_s *pl, GemmLaunch &L, int nl) {
+    if (L.ksplit <= 1) return;
+    const OutRect b = whole(L);
+    L.ws_h = b.nh, L.ws_w = b.nw;
+    ensure_alloc(pl->ws2, pl->ws2_bytes, ksplit_bytes(L, nl));
+    L.ws = pl->ws2;
+}
 
 void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunch &L) {
     const RankPlan &rp = pl->rp;
@@ -314,6 +360,7 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     (void)x;
     (void)xd;
     weight_map(&L.bmap, w, g.F, (int64_t)g.K * g.K * g.Cp, p.bkc, p.bn);
+    L.w_base = w, L.w_rows = g.F, L.w_kcols = (int64_t)g.K * g.K * g.Cp;
     // halo-dependent output rows/cols (only toward existing neighbours)
     auto count = [&](const DimSplit &d, bool lo) -> int64_t {
         const bool nb = lo ? d.idx > 0 : d.idx + 1 < d.parts;
@@ -332,6 +379,8 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     Split2D s{rp.h.out.size(), rp.w.out.size(), count(rp.h, true), count(rp.h, false),
               count(rp.w, true), count(rp.w, false)};
     make_rects(s, L.interior, L.boundary);
+    L.ksplit = choose_ksplit(g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles, g.Cp);
+    attach_ksplit(pl, L, (int)rp.nrange.size());
 }
 
 // Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
@@ -342,9 +391,10 @@ bool use_v1() {
 }
 
 // The persistent tile-reuse kernel (conv_v2.cu); false if it does not apply.
-bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
+// One launch of the persistent tile-reuse kernel (conv_v2.cu) over `rects`
+// with tile shape 2^twl columns; false if the configuration does not fit.
+bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, const void *in_base,
                      const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
-    if (use_v1() || L.p.T == 0) return false;
     ConvV2Params q;
     std::memset(&q, 0, sizeof q);
     q.s_in = L.p.s_in;
@@ -355,20 +405,26 @@ bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const voi
     std::memcpy(q.tap_w, L.p.tap_w, sizeof q.tap_w);
     q.cin_p = (int)cin_p;
     q.bn = L.p.bn;
-    q.nout_tiles = L.nout_tiles;
+    q.nout_tiles = (int)ceil_div(L.p.nout_p, q.bn);
+    q.ksplit = L.ksplit;
+    q.ws = L.ws;
+    q.ws_h = L.ws_h;
+    q.ws_w = L.ws_w;
     q.nsamples = nsamples;
+    q.tw_log2 = twl;
     q.out = L.p.out;
     q.out_sn = L.p.out_sn, q.out_sh = L.p.out_sh, q.out_sw = L.p.out_sw;
     q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
     q.nout_p = L.p.nout_p;
     if (!conv_v2_configure(q, kV2SmemLimit)) return false;
     DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
+    const int TW = 1 << twl, TH = 128 >> twl;
     q.nrect = (int)rects.size();
     q.rect_start[0] = 0;
     for (int r = 0; r < q.nrect; ++r) {
         q.rect[r] = rects[r];
-        q.rect_tiles_w[r] = (int)ceil_div(rects[r].nw, kV2TW);
-        q.rect_start[r + 1] = q.rect_start[r] + (int)ceil_div(rects[r].nh, kV2TH) * q.rect_tiles_w[r];
+        q.rect_tiles_w[r] = (int)ceil_div(rects[r].nw, TW);
+        q.rect_start[r + 1] = q.rect_start[r] + (int)ceil_div(rects[r].nh, TH) * q.rect_tiles_w[r];
     }
     q.total_tiles = q.nout_tiles * q.nsamples * q.rect_start[q.nrect];
     CUtensorMap amap;
@@ -376,7 +432,7 @@ bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const voi
     const uint64_t strides[3] = {(uint64_t)(cin_p * 2), (uint64_t)(ind.wb * cin_p * 2),
                                  (uint64_t)(ind.hb * ind.wb * cin_p * 2)};
     if (q.a_swz == 128) {
-        const uint32_t box[4] = {64, 16, (uint32_t)q.PH, 1};
+        const uint32_t box[4] = {64, (uint32_t)q.PWs, (uint32_t)q.PH, 1};
         make_tmap(&amap, in_base, 4, dims, strides, box, nullptr, 128);
     } else {
         const uint32_t box[4] = {8, (uint32_t)(q.PWs * q.s_in), (uint32_t)q.PH, 1};
@@ -384,7 +440,21 @@ bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const voi
         make_tmap(&amap, in_base, 4, dims, strides, box, es, 0);
     }
     launch_conv_v2(amap, L.bmap, q, st);
+    if (q.ksplit > 1) launch_conv_v2_reduce(q, st);
     return true;
+}
+
+// Thin rects (boundary strips of an H split) use 1 x 128 tiles, the rest 16 x 8.
+bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
+                     const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
+    if (use_v1() || L.p.T == 0) return false;
+    std::vector<OutRect> tall, thin;
+    for (auto &r : rects)
+        (L.p.s_in == 1 && r.nh < 8 && r.nw >= 64 ? thin : tall).push_back(r);
+    if (!thin.empty() && !launch_v2_shape(L, thin, 7, in_base, ind, cin_p, nsamples, st))
+        tall.insert(tall.end(), thin.begin(), thin.end());
+    if (tall.empty()) return true;
+    return launch_v2_shape(L, tall, 3, in_base, ind, cin_p, nsamples, st);
 }
 
 void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
@@ -474,36 +544,29 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
         return;
     }
     // ---- direct P2P stores into the neighbours' margins + epoch flags ----
+    // one kernel: ready handshake, NVLink stores, per-block completion counters
+    // (halo.cu: p2p_exchange_kernel); then a stream wait on my own counters.
     const uint32_t e = ++B.epoch;
     const int me = rp.rank;
-    std::vector<uint32_t *> fl;
-    for (auto &m : recvs) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me));
-    launch_signal(fl.data(), (int)fl.size(), e, st);  // "my margin is free for epoch e"
-    const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (pl->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
+    DC_REQUIRE(sends.size() <= 8 && recvs.size() <= 8, DC_ERR_ARG, "too many halo neighbours");
+    P2PExchange x{};
+    x.epoch = e;
+    for (auto &m : recvs) x.ready_out[x.n_ready_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me);
     for (auto &m : sends) {
-        CUresult r = get_wait32()((CUstream)st,
-                                  (CUdeviceptr)pl->flag(pl->flags, which, FLAG_READY, m.peer), e,
-                                  CU_STREAM_WAIT_VALUE_GEQ);
-        DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-    }
-    CopyBatch cb{};
-    for (auto &m : sends) {
-        BlockCopy &c = cb.c[cb.count++];
+        x.ready_in[x.n_ready_in++] = pl->flag(pl->flags, which, FLAG_READY, m.peer);
+        x.data_out[x.n_data_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_DATA, me);
+        BlockCopy &c = x.copies.c[x.copies.count++];
         c.src = reinterpret_cast<const uint4 *>(buf) + (m.src_row0 * m.src_wb + m.src_col0) * vec16;
         strides(m.src_hb, m.src_wb, c, true);
-        c.dst = reinterpret_cast<uint4 *>(B.peer.at(m.peer)) +
-                (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
+        c.dst = reinterpret_cast<uint4 *>(B.peer.at(m.peer)) + (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
         strides(m.dst_hb, m.dst_wb, c, false);
         c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
     }
-    launch_block_copies(cb, st);
-    fl.clear();
-    for (auto &m : sends) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_DATA, me));
-    launch_signal(fl.data(), (int)fl.size(), e, st);  // "your margin holds epoch e"
+    launch_p2p_exchange(x, st);
+    const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (pl->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
     for (auto &m : recvs) {
-        CUresult r = get_wait32()((CUstream)st,
-                                  (CUdeviceptr)pl->flag(pl->flags, which, FLAG_DATA, m.peer), e,
-                                  wflags);
+        CUresult r = get_wait32()((CUstream)st, (CUdeviceptr)pl->flag(pl->flags, which, FLAG_DATA, m.peer),
+                                  (cuuint32_t)(kP2PBlocks * e), wflags);
         DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
     }
 }
@@ -635,9 +698,21 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         p.nout_p = (int)g.Cp;
         L[i].nout_tiles = (int)ceil_div(g.Cp, p.bn);
         weight_map(&L[i].bmap, wt, g.Cp, (int64_t)std::max(f.T, 1) * g.Fp, p.bkc, p.bn);
+        L[i].w_base = wt, L[i].w_rows = g.Cp, L[i].w_kcols = (int64_t)std::max(f.T, 1) * g.Fp;
         Split2D s{f.nt_h, f.nt_w, f.bl, f.bh, f.bwl, f.bwh};
         make_rects(s, L[i].interior, L[i].boundary);
+        L[i].ksplit = choose_ksplit(g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) *
+                                        L[i].nout_tiles, g.Fp);
     }
+    size_t ks_need = 0;
+    for (size_t i = 0; i < ph.size(); ++i)
+        if (ph[i].active) ks_need = std::max(ks_need, ksplit_bytes(L[i], (int)rp.nrange.size()));
+    ensure_alloc(pl->ws2, pl->ws2_bytes, ks_need);
+    for (size_t i = 0; i < ph.size(); ++i)
+        if (ph[i].active && L[i].ksplit > 1) {
+            const OutRect b = whole(L[i]);
+            L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2;
+        }
     const bool overlap = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
     if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
@@ -647,8 +722,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     }
     for (size_t i = 0; i < ph.size(); ++i) {
         if (!ph[i].active) continue;
-        std::vector<OutRect> rects = L[i].interior;
-        if (!overlap) rects.insert(rects.end(), L[i].boundary.begin(), L[i].boundary.end());
+        std::vector<OutRect> rects = overlap ? L[i].interior : std::vector<OutRect>{whole(L[i])};
         launch_rects(L[i], rects, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
     }
     if (overlap) {
@@ -1013,9 +1087,7 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
         launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, st);
     } else {
-        std::vector<OutRect> all = L.interior;
-        all.insert(all.end(), L.boundary.begin(), L.boundary.end());
-        launch_rects(L, all, x, xd, pl->rp.g.Cp, nl, st);
+        launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
     }
     DC_API_END
 }

@@ -306,18 +306,26 @@ struct TapTable {
 };
 
 // Backward-data weights: wt[c][t][f] = w[f][a_t][b_t][c].
+// 32 x 32 (f, c) tiles through shared memory so that both the read of
+// w[f][a][b][c] (c contiguous) and the write of wt[c][t][f] (f contiguous) are
+// coalesced. grid = (ceil(Cp/32), ceil(Fp/32), T), block = 32 x 8.
 __global__ void weight_transform_kernel(const __nv_bfloat16 *__restrict__ w,
                                         __nv_bfloat16 *__restrict__ wt, int F, int Fp, int C,
-                                        int Cp, int K, int T, TapTable tt) {
-    const long long total = (long long)Cp * T * Fp;
-    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        const int f = (int)(idx % Fp);
-        const int t = (int)((idx / Fp) % T);
-        const int c = (int)(idx / ((long long)Fp * T));
+                                        int Cp, int K, int T, const __grid_constant__ TapTable tt) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 32, t = blockIdx.z;
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const long long tap_off = ((long long)tt.a[t] * K + tt.b[t]) * Cp;
+    for (int r = ty; r < 32; r += 8) {
+        const int f = f0 + r, c = c0 + tx;
         __nv_bfloat16 v = __float2bfloat16(0.0f);
-        if (c < C && f < F) v = w[(((long long)f * K + tt.a[t]) * K + tt.b[t]) * Cp + c];
-        wt[idx] = v;
+        if (f < F && c < C) v = w[(long long)f * K * K * Cp + tap_off + c];
+        tile[r][tx] = v;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int c = c0 + r, f = f0 + tx;
+        if (c < Cp && f < Fp) wt[((long long)c * T + t) * Fp + f] = tile[tx][r];
     }
 }
 
@@ -428,9 +436,8 @@ void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, i
         tt.a[t] = ka[t];
         tt.b[t] = kb[t];
     }
-    const long long total = (long long)Cp * T * Fp;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
-    weight_transform_kernel<<<blocks, 256, 0, st>>>(w, wt, F, Fp, C, Cp, K, T, tt);
+    weight_transform_kernel<<<dim3((Cp + 31) / 32, (Fp + 31) / 32, T), dim3(32, 8), 0, st>>>(
+        w, wt, F, Fp, C, Cp, K, T, tt);
     CUDA_OK(cudaGetLastError());
     ++g_launches;
 }

@@ -52,8 +52,8 @@ __device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
     while (r + 1 < p.nrect && lt >= p.rect_start[r + 1]) ++r;
     const int t = lt - p.rect_start[r];
     c.r = r;
-    c.i0 = p.rect[r].h0 + (t / p.rect_tiles_w[r]) * kV2TH;
-    c.j0 = p.rect[r].w0 + (t % p.rect_tiles_w[r]) * kV2TW;
+    c.i0 = p.rect[r].h0 + (t / p.rect_tiles_w[r]) * (128 >> p.tw_log2);
+    c.j0 = p.rect[r].w0 + (t % p.rect_tiles_w[r]) * (1 << p.tw_log2);
     c.o0 = ot * p.bn;
     return c;
 }
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(192, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sB = smem;  // B first: its slots need 1024-byte alignment (swizzle)
-    const int b_bytes = p.b_resident ? p.T * p.ncg * p.b_slot_bytes : p.b_stages * p.b_slot_bytes;
+    const int b_bytes =
+        p.b_resident ? p.T * (p.ncg / p.ksplit) * p.b_slot_bytes : p.b_stages * p.b_slot_bytes;
     uint8_t *sA = sB + b_bytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(sA + p.a_stages * p.a_stage_bytes);
     uint64_t *a_full = bars, *a_empty = bars + kMaxBar;
@@ -159,6 +160,10 @@ __global__ void __launch_bounds__(192, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     const int total = p.total_tiles;
+    const int ks = p.ksplit;
+    const int split = blockIdx.x % ks;
+    const int tile0 = blockIdx.x / ks, tile_step = gridDim.x / ks;
+    const int g0 = split * p.ncg / ks, g1 = (split + 1) * p.ncg / ks;
 
     if (warp == 0) {
         // ============ TMA producer: the whole warp runs the (warp-uniform) ============
@@ -169,22 +174,22 @@ __global__ void __launch_bounds__(192, 1)
         }
         int cur_o0 = -1;
         int a_it = 0, b_it = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        for (int u = tile0; u < total; u += tile_step) {
             const TileCoord c = decode(p, u);
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(b_res, p.T * p.ncg * p.bn * p.cg * 2);
-                    for (int g = 0; g < p.ncg; ++g)
+                    mbar_arrive_expect_tx(b_res, p.T * (g1 - g0) * p.bn * p.cg * 2);
+                    for (int g = g0; g < g1; ++g)
                         for (int t = 0; t < p.T; ++t)
-                            tma_load_2d(sB + (g * p.T + t) * p.b_slot_bytes, &bmap, b_res,
+                            tma_load_2d(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, b_res,
                                         t * p.cin_p + g * p.cg, c.o0);
                 }
                 __syncwarp();
                 cur_o0 = c.o0;
             }
             const int h0 = p.s_in * c.i0 + p.origin_h, w0 = p.s_in * c.j0 + p.origin_w;
-            for (int g = 0; g < p.ncg; ++g) {
+            for (int g = g0; g < g1; ++g) {
                 const int s = a_it % p.a_stages;
                 if (a_it >= p.a_stages) mbar_wait(&a_empty[s], ((a_it / p.a_stages) - 1) & 1);
                 if (elect_one()) {
@@ -227,16 +232,15 @@ __global__ void __launch_bounds__(192, 1)
         // `off` from a base descriptor is base + (off >> 4).
         const uint32_t idesc = idesc_bf16(128, p.bn, 0, 0);
         const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
-        const uint64_t a_desc0 = p.a_swz == 128
-                                     ? smem_desc(sA_u, 16, 16 * 128, 2)  // SBO: next output row
-                                     : smem_desc(sA_u, p.s_in * p.plane_bytes, p.s_in * p.PWs * 16, 0);
+        const uint64_t a_desc0 = p.a_swz == 128 ? smem_desc(sA_u, 16, p.a_sbo, 2)
+                                                : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
         const uint64_t b_desc0 = smem_desc(sB_u, 16, 8 * p.cg * 2, swizzle_layout(p.cg * 2));
         const uint32_t a_kstep = p.a_kstep16, b_slot16 = p.b_slot_bytes >> 4;
         const int nk16 = p.cg / 16;
         const bool do_mma = !(p.dbg & 4);
         int a_it = 0, b_it = 0, acc_it = 0;
         bool res_ready = false;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        for (int u = tile0; u < total; u += tile_step) {
             if (p.b_resident && !res_ready) {
                 mbar_wait(b_res, 0);
                 res_ready = true;
@@ -248,7 +252,7 @@ __global__ void __launch_bounds__(192, 1)
             if (tr) p.dbg_out[acc_it * 8 + 1] = clock64();
             tc_fence_after();
             const uint32_t d_tmem = tmem + acc * acc_cols;
-            for (int g = 0; g < p.ncg; ++g) {
+            for (int g = g0; g < g1; ++g) {
                 const int s = a_it % p.a_stages;
                 mbar_wait(&a_full[s], (a_it / p.a_stages) & 1);
                 if (tr && g == 0) p.dbg_out[acc_it * 8 + 2] = clock64();
@@ -256,9 +260,9 @@ __global__ void __launch_bounds__(192, 1)
                 const uint64_t a_stage = a_desc0 + ((uint32_t)(s * p.a_stage_bytes) >> 4);
                 if (p.b_resident) {
                     if (elect_one()) {
-                        uint64_t bd = b_desc0 + (uint32_t)(g * p.T) * b_slot16;
+                        uint64_t bd = b_desc0 + (uint32_t)((g - g0) * p.T) * b_slot16;
                         if (!do_mma ||
-                            !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16, idesc, g == 0)) {
+                            !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16, idesc, g == g0)) {
                         uint64_t arow = a_stage;
                         for (int th = 0; th < p.kh; ++th) {
                             for (int tw = 0; tw < p.kw; ++tw) {
@@ -267,7 +271,7 @@ __global__ void __launch_bounds__(192, 1)
                                 for (int k16 = 0; k16 < nk16; ++k16)
                                     if (do_mma)
                                         mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
-                                                 (g | th | tw | k16) != 0);
+                                                 ((g - g0) | th | tw | k16) != 0);
                                 bd += b_slot16;
                             }
                             arow += p.a_row16;
@@ -290,7 +294,7 @@ __global__ void __launch_bounds__(192, 1)
                             for (int k16 = 0; k16 < nk16; ++k16)
                                 if (do_mma)
                                     mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
-                                             (g | t | k16) != 0);
+                                             ((g - g0) | t | k16) != 0);
                             mma_commit(&b_empty[sb]);
                         }
                         __syncwarp();
@@ -310,9 +314,9 @@ __global__ void __launch_bounds__(192, 1)
         // ========================= epilogue =========================
         const int eq = warp & 3;  // TMEM lane quarter this warp may access
         const int m = eq * 32 + lane;
-        const int ti = m >> 3, tj = m & 7;
+        const int ti = m >> p.tw_log2, tj = m & ((1 << p.tw_log2) - 1);
         int acc_it = 0;
-        for (int u = blockIdx.x; u < total; u += gridDim.x) {
+        for (int u = tile0; u < total; u += tile_step) {
             const TileCoord c = decode(p, u);
             const int acc = acc_it & 1;
             const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
@@ -326,11 +330,22 @@ __global__ void __launch_bounds__(192, 1)
                                   (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
                                   (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0;
             const uint32_t t_lane = tmem + acc * acc_cols + ((uint32_t)(eq * 32) << 16);
+            float *wrow = ks > 1 ? p.ws + (long long)split * p.nsamples * p.ws_h * p.ws_w * p.nout_p +
+                                       (((long long)c.n * p.ws_h + i) * p.ws_w + j) * p.nout_p + c.o0
+                                 : nullptr;
             for (int c16 = 0; c16 < p.bn / 16; ++c16) {
                 uint32_t v[16];
                 tmem_ld16(t_lane + c16 * 16, v);
                 tmem_ld_wait();
-                if (valid && c.o0 + c16 * 16 < p.nout_p && !(p.dbg & 2)) {
+                if (ks > 1) {
+                    if (valid && c.o0 + c16 * 16 < p.nout_p) {
+                        float4 *dst = reinterpret_cast<float4 *>(wrow + c16 * 16);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
+                                                 __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    }
+                } else if (valid && c.o0 + c16 * 16 < p.nout_p && !(p.dbg & 2)) {
                     uint4 lo, hi;
                     lo.x = pack2(v[0], v[1]);
                     lo.y = pack2(v[2], v[3]);
@@ -359,7 +374,8 @@ __global__ void __launch_bounds__(192, 1)
 
 // ---------------------------------------------------------------------------
 size_t conv_v2_smem_bytes(const ConvV2Params &p) {
-    const size_t b = p.b_resident ? (size_t)p.T * p.ncg * p.b_slot_bytes : (size_t)p.b_stages * p.b_slot_bytes;
+    const size_t b = p.b_resident ? (size_t)p.T * (p.ncg / p.ksplit) * p.b_slot_bytes
+                                  : (size_t)p.b_stages * p.b_slot_bytes;
     return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16;
 }
 
@@ -371,21 +387,25 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     }
     p.cg = p.cin_p % 64 == 0 ? 64 : p.cin_p % 32 == 0 ? 32 : 16;
     p.ncg = p.cin_p / p.cg;
-    p.PH = p.s_in * (kV2TH - 1) + kh;
+    const int TW = 1 << p.tw_log2, TH = 128 >> p.tw_log2;
+    if (TW != 8 && !(TW == 128 && p.s_in == 1)) return false;
+    p.PH = p.s_in * (TH - 1) + kh;
     static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
-    static const int dbg = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
-    p.dbg = dbg;
-    if (!force_planes && p.cg == 64 && p.s_in == 1 && kV2TW + kw - 1 <= 16) {
+    if (!force_planes && p.cg == 64 && p.s_in == 1 && TW + kw - 1 <= (TW == 8 ? 16 : 136)) {
+        // 128-byte swizzled rows; pitch a multiple of 8 pixels (1024 B) so a tap
+        // shift only moves the start address (the swizzle is address-based)
         p.a_swz = 128;
-        p.PWs = 16;
-        p.plane_bytes = p.PH * 16 * 128;
+        p.PWs = TW == 8 ? 16 : 136;
+        p.plane_bytes = p.PH * p.PWs * 128;
         p.a_stage_bytes = p.plane_bytes;
+        p.a_sbo = TW == 8 ? p.PWs * 128 : 8 * 128;
     } else {
         p.a_swz = 0;
-        p.PWs = kV2TW + (kw - 1) / p.s_in;
+        p.PWs = TW + (kw - 1) / p.s_in;
         if (p.PWs * p.s_in > 256 || p.PH > 256) return false;
         p.plane_bytes = (int)round_up((int64_t)p.PH * p.PWs * 16, 128);
         p.a_stage_bytes = (p.cg / 8) * p.s_in * p.plane_bytes;
+        p.a_sbo = TW == 8 ? p.s_in * p.PWs * 16 : 8 * 16;
     }
     p.kh = kh;
     p.kw = kw;
@@ -393,7 +413,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         if (p.tap_h[t] != t / kw || p.tap_w[t] != t % kw || p.T != kh * kw) return false;
     p.s_shift = p.s_in == 2 ? 1 : 0;
     if (p.a_swz == 128) {
-        p.a_row16 = (16 * 128) >> 4;
+        p.a_row16 = (p.PWs * 128) >> 4;
         p.a_col16 = 128 >> 4;
         p.a_par16 = 0;
     } else {
@@ -404,7 +424,8 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     p.a_kstep16 = p.a_swz == 128 ? 32 >> 4 : (2 * p.s_in * p.plane_bytes) >> 4;
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
     const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16;
-    const int resident_b = p.T * p.ncg * p.b_slot_bytes;
+    if (p.ksplit < 1 || p.ncg % p.ksplit) return false;
+    const int resident_b = p.T * (p.ncg / p.ksplit) * p.b_slot_bytes;
     // prefer resident weights with >= 2 A stages
     if (p.nout_tiles == 1 && resident_b + 2 * p.a_stage_bytes + fixed <= smem_limit &&
         resident_b <= 160 * 1024) {
@@ -422,6 +443,55 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         if (p.b_stages < 2) return false;
     }
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
+}
+
+// out[pixel][o] = bf16( sum_{s in order} ws[s][pixel][o] ) over the launch's rects.
+__global__ void conv_v2_reduce_kernel(const __grid_constant__ ConvV2Params p) {
+    const int vecs = p.nout_p / 8;
+    long long npix_rects = 0;
+    for (int r = 0; r < p.nrect; ++r) npix_rects += (long long)p.rect[r].nh * p.rect[r].nw;
+    const long long work = npix_rects * p.nsamples * vecs;
+    const long long split_stride = (long long)p.nsamples * p.ws_h * p.ws_w * p.nout_p;
+    for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < work;
+         idx += (long long)gridDim.x * blockDim.x) {
+        const int v = (int)(idx % vecs);
+        long long pix = idx / vecs;
+        const int n = (int)(pix / npix_rects);
+        long long rp = pix - (long long)n * npix_rects;
+        int r = 0;
+        while (rp >= (long long)p.rect[r].nh * p.rect[r].nw) {
+            rp -= (long long)p.rect[r].nh * p.rect[r].nw;
+            ++r;
+        }
+        const int i = p.rect[r].h0 + (int)(rp / p.rect[r].nw), j = p.rect[r].w0 + (int)(rp % p.rect[r].nw);
+        const float *src = p.ws + (((long long)n * p.ws_h + i) * p.ws_w + j) * p.nout_p + v * 8;
+        float4 a = reinterpret_cast<const float4 *>(src)[0], b = reinterpret_cast<const float4 *>(src)[1];
+        for (int s = 1; s < p.ksplit; ++s) {
+            const float4 *q = reinterpret_cast<const float4 *>(src + s * split_stride);
+            const float4 c = q[0], d = q[1];
+            a.x += c.x, a.y += c.y, a.z += c.z, a.w += c.w;
+            b.x += d.x, b.y += d.y, b.z += d.z, b.w += d.w;
+        }
+        uint4 o;
+        o.x = pack2(__float_as_uint(a.x), __float_as_uint(a.y));
+        o.y = pack2(__float_as_uint(a.z), __float_as_uint(a.w));
+        o.z = pack2(__float_as_uint(b.x), __float_as_uint(b.y));
+        o.w = pack2(__float_as_uint(b.z), __float_as_uint(b.w));
+        *reinterpret_cast<uint4 *>(p.out + (long long)n * p.out_sn + (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+                                   (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + v * 8) = o;
+    }
+}
+
+void launch_conv_v2_reduce(const ConvV2Params &p, cudaStream_t st) {
+    long long npix = 0;
+    for (int r = 0; r < p.nrect; ++r) npix += (long long)p.rect[r].nh * p.rect[r].nw;
+    const long long work = npix * p.nsamples * (p.nout_p / 8);
+    if (work == 0) return;
+    const int blocks = (int)std::min<long long>((work + 255) / 256, device_sm_count() * 8);
+    conv_v2_reduce_kernel<<<blocks, 256, 0, st>>>(p);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 reduce launch: %s", cudaGetErrorString(e));
+    ++g_launches;
 }
 
 int device_sm_count() {
@@ -442,7 +512,7 @@ void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const Conv
     std::call_once(once, [] {
         cudaFuncSetAttribute(conv_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
-    const int grid = std::min(p.total_tiles, device_sm_count());
+    const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, device_sm_count() / p.ksplit));
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
         ConvV2Params q = p;
         cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));

@@ -39,6 +39,9 @@ struct ConvV2Params {
     //   th*a_row16 + (tw >> s_shift)*a_col16 + (tw & (s_in-1))*a_par16
     int kh, kw, s_shift;
     uint32_t a_row16, a_col16, a_par16;
+    int tw_log2;                   // GEMM tile: (128 >> tw_log2) rows x (1 << tw_log2) cols:
+                                   // 3 -> 16 x 8 (default), 7 -> 1 x 128 (thin boundary strips)
+    uint32_t a_sbo;                // A descriptor SBO: byte distance between 8-pixel groups
     uint32_t a_kstep16;            // A descriptor delta between 16-channel K slices
     int dbg;                   // timing experiments: 1 skip steady-state A TMA, 2 skip stores, 4 skip MMAs, 8 trace
     long long *dbg_out;        // trace buffer (dbg & 8): CTA 0, [tile][8] clock64 stamps
@@ -62,6 +65,13 @@ struct ConvV2Params {
     int rect_tiles_w[kMaxRects];
     int rect_start[kMaxRects + 1];
     int nsamples, nout_tiles, total_tiles;
+    // split-K over channel groups (small-spatial, many-channel layers): CTA b
+    // takes split b % ksplit; partial sums (fp32) go to ws[split][n][ws_h][ws_w][nout_p]
+    // and conv_v2_reduce sums them in split order. ksplit depends only on the
+    // global layer shape, so partitioned results stay bitwise equal to 1 GPU.
+    int ksplit;
+    float *ws;
+    int ws_h, ws_w;
     __nv_bfloat16 *out;
     long long out_sn, out_sh, out_sw;
     int out_h0, out_w0, out_dh, out_dw;
@@ -70,13 +80,16 @@ struct ConvV2Params {
 
 size_t conv_v2_smem_bytes(const ConvV2Params &p);
 // Fills the derived fields (PH, PWs, stage sizes, residency, stages) from the
-// taps / stride / channels / bn already set; returns false if it cannot fit.
+// taps / stride / channels / bn / tw_log2 already set; returns false if it
+// cannot fit (e.g. a 1 x 128 strip with stride 2).
 bool conv_v2_configure(ConvV2Params &p, int smem_limit);
 // amap: 4D map over the input buffer with box {8, PWs * s_in, PH, 1} and
 // element strides {1, s_in, 1, 1}, no swizzle. bmap: [N rows][T * cin_p]
 // weights with box {cg, bn}, swizzle cg * 2 bytes.
 void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p,
                     cudaStream_t st);
+// Fixed-order sum of the split-K partials -> bf16 output (rects / out mapping of p).
+void launch_conv_v2_reduce(const ConvV2Params &p, cudaStream_t st);
 int device_sm_count();
 
 }  // namespace dc

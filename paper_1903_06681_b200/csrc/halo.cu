@@ -157,3 +157,46 @@ void launch_bn_finalize(const double *sums, int cpad, int c, double count, doubl
 }
 
 }  // namespace dc
+
+namespace dc {
+
+__global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant__ P2PExchange x) {
+    const uint32_t e = x.epoch;
+    if (blockIdx.x == 0 && (int)threadIdx.x < x.n_ready_out) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[threadIdx.x]), "r"(e) : "memory");
+    }
+    if ((int)threadIdx.x < x.n_ready_in) {
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.ready_in[threadIdx.x]) : "memory");
+        } while ((int)(v - e) < 0);
+    }
+    __syncthreads();
+    for (int k = 0; k < x.copies.count; ++k) {
+        const BlockCopy &c = x.copies.c[k];
+        const long long run = (long long)c.cols * c.vec16;
+        const long long total = (long long)c.nn * c.rows * run;
+        for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+             idx += (long long)gridDim.x * blockDim.x) {
+            const long long nr = idx / run, kk = idx - nr * run;
+            const int n = (int)(nr / c.rows), r = (int)(nr - (long long)n * c.rows);
+            const int col = (int)(kk / c.vec16), v = (int)(kk - (long long)col * c.vec16);
+            c.dst[n * c.d_sn + r * c.d_sh + col * c.d_sw + v] = c.src[n * c.s_sn + r * c.s_sh + col * c.s_sw + v];
+        }
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < x.n_data_out) {
+        __threadfence_system();
+        atomicAdd_system(x.data_out[threadIdx.x], 1u);
+    }
+}
+
+void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st) {
+    p2p_exchange_kernel<<<kP2PBlocks, 256, 0, st>>>(x);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "p2p exchange launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
+}  // namespace dc

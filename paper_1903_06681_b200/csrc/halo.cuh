@@ -43,3 +43,27 @@ void launch_bn_finalize(const double *sums, int cpad, int c, double count, doubl
                         double *var, cudaStream_t st);
 
 }  // namespace dc
+
+namespace dc {
+
+// One-launch direct P2P halo exchange (epoch e):
+//   1. block 0 stores e (release, system scope) into each receiver-side
+//      "ready" flag of the peers that send to me  (my margins are free);
+//   2. every block waits (acquire polling) until each peer I send to has
+//      flagged ready for epoch e;
+//   3. all blocks copy the slabs straight into the peers' margins (NVLink);
+//   4. each block, after a system fence, atomically adds 1 to the peer's
+//      "data" counter for me; a receiver's margin for epoch e is complete when
+//      its counter reaches kP2PBlocks * e (waited with cuStreamWaitValue32).
+constexpr int kP2PBlocks = 32;
+struct P2PExchange {
+    CopyBatch copies;
+    uint32_t *ready_out[8];  // peers' ready flags for me (I am their receiver)
+    uint32_t *ready_in[8];   // my flags written by the peers I send to
+    uint32_t *data_out[8];   // peers' data counters for me (I am their sender)
+    int n_ready_out, n_ready_in, n_data_out;
+    uint32_t epoch;
+};
+void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);
+
+}  // namespace dc

@@ -77,6 +77,7 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     (1, 128, 9, 11, 64, 3, 1, 1),      # two channel groups: 18 atoms across groups
     (1, 192, 10, 10, 64, 1, 2, 0),     # 1x1 stride 2, three channel groups (odd atom count)
     (2, 64, 20, 20, 128, 5, 1, 2),     # K=5 (25 taps)
+    (1, 512, 16, 18, 256, 3, 1, 1),    # deep layer: split-K over 8 channel groups
 ]
 
 
@@ -104,7 +105,7 @@ def test_single_gpu_parity(dc, shape):
 GRIDS = [(1, 2, 1), (1, 1, 2), (1, 2, 2), (2, 2, 1), (1, 3, 1), (1, 4, 2)]
 
 
-@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[2], SHAPES[3], SHAPES[4], SHAPES[9]])
+@pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[2], SHAPES[3], SHAPES[4], SHAPES[9], SHAPES[12], SHAPES[15]])
 @pytest.mark.parametrize("grid", GRIDS)
 def test_partition_bitwise(dc, shape, grid):
     """Every rank's owned y and dx from its own margined shard is bitwise equal
