@@ -6,9 +6,11 @@ partitioned convolution hot path (arXiv:1903.06681) on B200.
   python bench.py --impl reference ...                      (fp64 CPU oracle arm)
 
 One step = for every layer of the workload: forward (with x halo exchange
-overlapped with interior tiles) + backward (dy halo || filter gradient, then
-data gradient || dW allreduce), i.e. every row of SURVEY.md 8(a) on the
-hot path, through the C ABI (libdconv.so). Global batch fixed as N grows
+overlapped with interior tiles), spatially aggregated BN statistics of its
+output, and backward (dy halo || filter gradient, then data gradient || dW
+allreduce), i.e. every row of SURVEY.md 8(a) on the hot path, through the C
+ABI (libdconv.so); the decomposition of every layer comes from the library's
+performance model (a8) unless --decomp is given. Global batch fixed as N grows
 (strong scaling); the per-layer decomposition is chosen by the library's
 performance model unless --decomp is given.
 Rank 0 prints ONE JSON line.
@@ -279,11 +281,13 @@ def main():
         y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
         dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
         dw = torch.empty((F, K, K, xd["c_pad"]), dtype=torch.float32, device="cuda")
+        bn_mean = torch.empty(F, dtype=torch.float64, device="cuda")
+        bn_var = torch.empty(F, dtype=torch.float64, device="cuda")
         # pinned host copies for the end-to-end leg
         host = {"x": x_own.pin_memory(), "dy": dy_own.pin_memory(), "w": wt.cpu().pin_memory(),
                 "dw": torch.empty(dw.shape, dtype=torch.float32).pin_memory()}
         L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
-                      dx=dx, dw=dw, host=host, x_own_dev=x_own.cuda(), dy_own_dev=dy_own.cuda()))
+                      dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, host=host))
     torch.cuda.synchronize()
 
     def step(events=None, e2e=False):
@@ -298,6 +302,8 @@ def main():
             if events is not None:
                 events[i][0].record(stream)
             dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)
+            # spatially aggregated BN statistics of the layer output
+            dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp)
             if events is not None:
                 events[i][1].record(stream)
             if world == 1:

@@ -562,7 +562,11 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
         strides(m.dst_hb, m.dst_wb, c, false);
         c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
     }
+    for (auto &m : recvs) x.data_in[x.n_data_in++] = pl->flag(pl->flags, which, FLAG_DATA, m.peer);
+    static const bool stream_wait = std::getenv("DC_P2P_STREAM_WAIT") != nullptr;
+    x.wait_in_kernel = stream_wait ? 0 : 1;
     launch_p2p_exchange(x, st);
+    if (x.wait_in_kernel) return;
     const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (pl->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
     for (auto &m : recvs) {
         CUresult r = get_wait32()((CUstream)st, (CUdeviceptr)pl->flag(pl->flags, which, FLAG_DATA, m.peer),
@@ -704,32 +708,38 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         L[i].ksplit = choose_ksplit(g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) *
                                         L[i].nout_tiles, g.Fp);
     }
+    // one split-K workspace region per phase: the phases' interior and
+    // boundary launches may run concurrently on two streams
     size_t ks_need = 0;
+    std::vector<size_t> ks_off(ph.size(), 0);
     for (size_t i = 0; i < ph.size(); ++i)
-        if (ph[i].active) ks_need = std::max(ks_need, ksplit_bytes(L[i], (int)rp.nrange.size()));
+        if (ph[i].active) {
+            ks_off[i] = ks_need;
+            ks_need += ksplit_bytes(L[i], (int)rp.nrange.size());
+        }
     ensure_alloc(pl->ws2, pl->ws2_bytes, ks_need);
     for (size_t i = 0; i < ph.size(); ++i)
         if (ph[i].active && L[i].ksplit > 1) {
             const OutRect b = whole(L[i]);
-            L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2;
+            L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2 + ks_off[i] / sizeof(float);
         }
     const bool overlap = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
     if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
         exchange(pl, 1, dy, flags, pl->s_comm);
-        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
     }
     for (size_t i = 0; i < ph.size(); ++i) {
         if (!ph[i].active) continue;
         std::vector<OutRect> rects = overlap ? L[i].interior : std::vector<OutRect>{whole(L[i])};
         launch_rects(L[i], rects, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
     }
-    if (overlap) {
-        CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
+    if (overlap) {  // boundary tiles on the comm stream after the exchange, joined
         for (size_t i = 0; i < ph.size(); ++i)
             if (ph[i].active)
-                launch_rects(L[i], L[i].boundary, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
+                launch_rects(L[i], L[i].boundary, dy, dyd, g.Fp, (int)rp.nrange.size(), pl->s_comm);
+        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
+        CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
     }
 }
 
@@ -836,6 +846,22 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     nhwc_map(&dymap, dy_owned, nl, ho, wo, g.Fp, dyd.wb, dyd.hb * dyd.wb, p.bf, tw, th, 1);
     launch_wgrad(xmap, dymap, p, m_tiles, n_tiles, st);
     if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+}
+
+// Early "ready" signal (P2P halo protocol): after the last consumer of a
+// margined buffer (x: backward-filter, retention contract; dy: backward-data),
+// tell the neighbours that send into it that the next epoch may be written, so
+// the next exchange does not wait for a handshake. The exchange kernel also
+// signals ready for its own epoch, so this is an optimisation, never required.
+void signal_ready_next(dc_plan_s *pl, int which, const void *buf, cudaStream_t st) {
+    if (pl->is_virtual || pl->world() <= 1 || pl->peer_flags.empty()) return;
+    const BufState &B = pl->buf[which];
+    if (B.ptr != buf) return;  // the P2P protocol applies to dc_buffer_alloc buffers only
+    const auto &recvs = which == 0 ? pl->rp.x_recv : pl->rp.dy_recv;
+    if (recvs.empty()) return;
+    std::vector<uint32_t *> fl;
+    for (auto &m : recvs) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, pl->rp.rank));
+    launch_signal(fl.data(), (int)fl.size(), B.epoch + 1, st);
 }
 
 void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
@@ -1082,10 +1108,13 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
         exchange(pl, 0, x, flags, pl->s_comm);
-        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
+        // interior tiles on the caller's stream, concurrently with the exchange;
+        // the halo-dependent boundary tiles right after it on the comm stream
+        // (disjoint outputs, and disjoint split-K workspace pixels), joined below
         launch_rects(L, L.interior, x, xd, pl->rp.g.Cp, nl, st);
+        launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, pl->s_comm);
+        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
-        launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, st);
     } else {
         launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
     }
@@ -1098,6 +1127,7 @@ dc_status_t dc_conv_bwd_data(dc_plan_t pl, void *dy, const void *w, void *dx, un
     DC_REQUIRE(pl && dy && w && dx, DC_ERR_ARG, "null argument");
     ensure_local_resources(pl);
     run_bwd_data(pl, dy, w, dx, flags, (cudaStream_t)stream);
+    signal_ready_next(pl, 1, dy, (cudaStream_t)stream);
     DC_API_END
 }
 
@@ -1108,6 +1138,7 @@ dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, floa
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
     run_bwd_filter(pl, x, dy, dw, st);
+    signal_ready_next(pl, 0, x, st);
     if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
     DC_API_END
 }
@@ -1127,6 +1158,7 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
     }
     run_bwd_filter(pl, x, dy, dw, st);
+    signal_ready_next(pl, 0, x, st);
     if (ar) {  // dW allreduce on the comm stream, concurrent with the data gradient
         CK(cudaEventRecord(pl->ev[2], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[2], 0));
@@ -1135,6 +1167,7 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
     }
     if (halo) CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
     run_bwd_data(pl, dy, w, dx, flags & ~DC_EXCHANGE, st);
+    signal_ready_next(pl, 1, dy, st);
     if (ar) CK(cudaStreamWaitEvent(st, pl->ev[3], 0));
     DC_API_END
 }

@@ -190,6 +190,14 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
         __threadfence_system();
         atomicAdd_system(x.data_out[threadIdx.x], 1u);
     }
+    if (x.wait_in_kernel && blockIdx.x == 0 && (int)threadIdx.x < x.n_data_in) {
+        const uint32_t target = kP2PBlocks * e;
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.data_in[threadIdx.x]) : "memory");
+        } while ((int)(v - target) < 0);
+        __threadfence_system();
+    }
 }
 
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st) {

@@ -61,7 +61,9 @@ struct P2PExchange {
     uint32_t *ready_out[8];  // peers' ready flags for me (I am their receiver)
     uint32_t *ready_in[8];   // my flags written by the peers I send to
     uint32_t *data_out[8];   // peers' data counters for me (I am their sender)
-    int n_ready_out, n_ready_in, n_data_out;
+    uint32_t *data_in[8];    // my counters written by the peers that send to me
+    int n_ready_out, n_ready_in, n_data_out, n_data_in;
+    int wait_in_kernel;      // block 0 polls data_in >= kP2PBlocks*epoch before exiting
     uint32_t epoch;
 };
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);

@@ -60,6 +60,10 @@ def main():
         "bpx_noexch": lambda: dc.dc_conv_bwd_data(plan, DY, w, dx, 0),
         "bpx_exch": lambda: dc.dc_conv_bwd_data(plan, DY, w, dx, dc.DC_EXCHANGE),
         "bwd_fused": lambda: dc.dc_conv_bwd(plan, X, DY, w, dx, dw, dc.DC_DEFAULT_FLAGS),
+        "step": lambda: (dc.dc_conv_fwd(plan, X, w, y, dc.DC_EXCHANGE),
+                         dc.dc_conv_bwd(plan, X, DY, w, dx, dw, dc.DC_DEFAULT_FLAGS)),
+        "step_noexch": lambda: (dc.dc_conv_fwd(plan, X, w, y, 0),
+                                dc.dc_conv_bwd(plan, X, DY, w, dx, dw, dc.DC_ALLREDUCE)),
     }
     res = {}
     for name, f in ops.items():
