@@ -431,9 +431,10 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     const uint64_t dims[4] = {(uint64_t)cin_p, (uint64_t)ind.wb, (uint64_t)ind.hb, (uint64_t)ind.n};
     const uint64_t strides[3] = {(uint64_t)(cin_p * 2), (uint64_t)(ind.wb * cin_p * 2),
                                  (uint64_t)(ind.hb * ind.wb * cin_p * 2)};
-    if (q.a_swz == 128) {
-        const uint32_t box[4] = {64, (uint32_t)q.PWs, (uint32_t)q.PH, 1};
-        make_tmap(&amap, in_base, 4, dims, strides, box, nullptr, 128);
+    if (q.a_swz) {
+        const uint32_t box[4] = {(uint32_t)q.cg, (uint32_t)(q.PWs * q.s_in), (uint32_t)q.PH, 1};
+        const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
+        make_tmap(&amap, in_base, 4, dims, strides, box, es, q.a_swz);
     } else {
         const uint32_t box[4] = {8, (uint32_t)(q.PWs * q.s_in), (uint32_t)q.PH, 1};
         const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};

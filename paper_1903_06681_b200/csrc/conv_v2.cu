@@ -196,10 +196,12 @@ __global__ void __launch_bounds__(192, 1)
                     uint8_t *dst = sA + s * p.a_stage_bytes;
                     if ((p.dbg & 1) && a_it >= p.a_stages) {
                         mbar_arrive(&a_full[s]);
-                    } else if (p.a_swz == 128) {
-                        // one box: PH rows x 16 cols x 64 channels (128-byte swizzled rows)
-                        mbar_arrive_expect_tx(&a_full[s], p.PH * p.PWs * 128);
-                        tma_load_4d(dst, &amap, &a_full[s], g * p.cg, w0, h0, c.n);
+                    } else if (p.a_swz) {
+                        // one box per column parity: PH rows x PWs cols x cg channels
+                        mbar_arrive_expect_tx(&a_full[s], p.s_in * p.plane_bytes);
+                        for (int par = 0; par < p.s_in; ++par)
+                            tma_load_4d(dst + par * p.plane_bytes, &amap, &a_full[s], g * p.cg,
+                                        w0 + par, h0, c.n);
                     } else {
                         mbar_arrive_expect_tx(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
                         for (int k8 = 0; k8 < p.cg / 8; ++k8)
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(192, 1)
         // `off` from a base descriptor is base + (off >> 4).
         const uint32_t idesc = idesc_bf16(128, p.bn, 0, 0);
         const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
-        const uint64_t a_desc0 = p.a_swz == 128 ? smem_desc(sA_u, 16, p.a_sbo, 2)
+        const uint64_t a_desc0 = p.a_swz ? smem_desc(sA_u, 16, p.a_sbo, swizzle_layout(p.a_swz))
                                                 : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
         const uint64_t b_desc0 = smem_desc(sB_u, 16, 8 * p.cg * 2, swizzle_layout(p.cg * 2));
         const uint32_t a_kstep = p.a_kstep16, b_slot16 = p.b_slot_bytes >> 4;
@@ -391,14 +393,17 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     if (TW != 8 && !(TW == 128 && p.s_in == 1)) return false;
     p.PH = p.s_in * (TH - 1) + kh;
     static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
-    if (!force_planes && p.cg == 64 && p.s_in == 1 && TW + kw - 1 <= (TW == 8 ? 16 : 136)) {
-        // 128-byte swizzled rows; pitch a multiple of 8 pixels (1024 B) so a tap
-        // shift only moves the start address (the swizzle is address-based)
-        p.a_swz = 128;
-        p.PWs = TW == 8 ? 16 : 136;
-        p.plane_bytes = p.PH * p.PWs * 128;
-        p.a_stage_bytes = p.plane_bytes;
-        p.a_sbo = TW == 8 ? p.PWs * 128 : 8 * 128;
+    const int pitch = TW == 8 ? 16 : 136;  // pixels per smem row: a multiple of 8 (swizzle atom)
+    if (!force_planes && TW + (kw - 1) / p.s_in <= pitch && pitch * p.s_in <= 256) {
+        // swizzled rows of cg channels (32/64/128-byte swizzle), one plane per
+        // column parity (TMA element stride = s_in); the row pitch is a multiple
+        // of 8 pixels so a tap shift only moves the start address (the swizzle
+        // is a function of the absolute smem address, measured)
+        p.a_swz = p.cg * 2;
+        p.PWs = pitch;
+        p.plane_bytes = p.PH * p.PWs * p.cg * 2;
+        p.a_stage_bytes = p.s_in * p.plane_bytes;
+        p.a_sbo = TW == 8 ? p.s_in * p.PWs * p.cg * 2 : 8 * p.cg * 2;
     } else {
         p.a_swz = 0;
         p.PWs = TW + (kw - 1) / p.s_in;
@@ -412,16 +417,17 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     for (int t = 0; t < p.T; ++t)  // the tap list must be the row-major (th, tw) grid
         if (p.tap_h[t] != t / kw || p.tap_w[t] != t % kw || p.T != kh * kw) return false;
     p.s_shift = p.s_in == 2 ? 1 : 0;
-    if (p.a_swz == 128) {
-        p.a_row16 = (p.PWs * 128) >> 4;
-        p.a_col16 = 128 >> 4;
-        p.a_par16 = 0;
+    if (p.a_swz) {
+        p.a_row16 = (p.PWs * p.cg * 2) >> 4;
+        p.a_col16 = (p.cg * 2) >> 4;
+        p.a_par16 = p.plane_bytes >> 4;
+        p.a_kstep16 = 32 >> 4;  // next 16 channels inside the swizzled row
     } else {
         p.a_row16 = (p.PWs * 16) >> 4;
         p.a_col16 = 1;
         p.a_par16 = p.plane_bytes >> 4;
+        p.a_kstep16 = (2 * p.s_in * p.plane_bytes) >> 4;
     }
-    p.a_kstep16 = p.a_swz == 128 ? 32 >> 4 : (2 * p.s_in * p.plane_bytes) >> 4;
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
     const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16;
     if (p.ksplit < 1 || p.ncg % p.ksplit) return false;
