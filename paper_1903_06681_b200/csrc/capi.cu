@@ -424,7 +424,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     for (int r = 0; r < q.nrect; ++r) {
         q.rect[r] = rects[r];
         q.rect_tiles_w[r] = (int)ceil_div(rects[r].nw, TW);
-        q.rect_start[r + 1] = q.rect_start[r] + (int)ceil_div(rects[r].nh, TH) * q.rect_tiles_w[r];
+        q.rect_start[r + 1] = q.rect_start[r] + (int)ceil_div(rects[r].nh, TH * q.tpw) * q.rect_tiles_w[r];
     }
     q.total_tiles = q.nout_tiles * q.nsamples * q.rect_start[q.nrect];
     CUtensorMap amap;

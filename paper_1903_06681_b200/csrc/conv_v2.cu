@@ -52,7 +52,7 @@ __device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
     while (r + 1 < p.nrect && lt >= p.rect_start[r + 1]) ++r;
     const int t = lt - p.rect_start[r];
     c.r = r;
-    c.i0 = p.rect[r].h0 + (t / p.rect_tiles_w[r]) * (128 >> p.tw_log2);
+    c.i0 = p.rect[r].h0 + (t / p.rect_tiles_w[r]) * ((128 >> p.tw_log2) * p.tpw);
     c.j0 = p.rect[r].w0 + (t % p.rect_tiles_w[r]) * (1 << p.tw_log2);
     c.o0 = ot * p.bn;
     return c;
@@ -66,11 +66,11 @@ constexpr int kMaxBar = 16;
 // stride hoisted out of the loop, so the single issuing thread spends a few
 // uniform instructions per tcgen05.mma instead of a dependent chain of
 // constant loads and 64-bit adds per tap (measured: ~180 cycles per tap).
-template <int KH, int KW, int NK, int SSH>
+template <int KH, int KW, int NK, int SSH, int TPW>
 __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, uint64_t bd,
                                            uint32_t a_row16, uint32_t a_col16, uint32_t a_par16,
                                            uint32_t a_kstep, uint32_t b_slot16, uint32_t idesc,
-                                           bool first_group) {
+                                           bool first_group, uint32_t acc_cols, uint32_t a_tile16) {
 #pragma unroll
     for (int th = 0; th < KH; ++th)
 #pragma unroll
@@ -80,20 +80,27 @@ __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, ui
             const uint64_t b = bd + (uint32_t)(th * KW + tw) * b_slot16;
 #pragma unroll
             for (int k = 0; k < NK; ++k)
-                mma_bf16(d_tmem, ad + (uint32_t)k * a_kstep, b + 2 * k, idesc,
-                         (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
+#pragma unroll
+                for (int tt = 0; tt < TPW; ++tt)  // the tiles of the work item share the B slice
+                    mma_bf16(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
+                             idesc, (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
         }
 }
 
 // Dispatch to an unrolled specialisation; false if none matches.
 __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16, uint32_t d_tmem,
                                                  uint64_t a_stage, uint64_t bd, uint32_t a_kstep,
-                                                 uint32_t b_slot16, uint32_t idesc, bool first) {
-    const int key = (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
-#define DC_TAPS(KH, KW, NK, SS)                                                                  \
-    case ((KH << 12) | (KW << 8) | (NK << 4) | SS):                                              \
-        issue_taps<KH, KW, NK, SS>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16, a_kstep, \
-                                   b_slot16, idesc, first);                                      \
+                                                 uint32_t b_slot16, uint32_t idesc, bool first,
+                                                 uint32_t acc_cols, uint32_t a_tile16) {
+    const int key = (p.tpw << 16) | (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
+#define DC_TAPS(KH, KW, NK, SS)                                                                   \
+    case ((1 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
+        issue_taps<KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+                                      a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
+        return true;                                                                              \
+    case ((2 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
+        issue_taps<KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+                                      a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;
     switch (key) {
         DC_TAPS(3, 3, 4, 0)  // 3x3 stride 1, 64-channel groups (fwd and bwd-data)
@@ -135,8 +142,11 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
+    // TMEM: NB accumulator buffers (double-buffered when they fit) of tpw tiles x acc_cols
     const uint32_t acc_cols = pow2_cols(p.bn);
-    const uint32_t ncols = 2 * acc_cols;
+    const int NB = 2 * p.tpw * (int)acc_cols <= 512 ? 2 : 1;
+    const uint32_t buf_cols = p.tpw * acc_cols;
+    const uint32_t ncols = NB * buf_cols;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.a_stages; ++s) {
@@ -238,6 +248,8 @@ __global__ void __launch_bounds__(192, 1)
                                                 : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
         const uint64_t b_desc0 = smem_desc(sB_u, 16, 8 * p.cg * 2, swizzle_layout(p.cg * 2));
         const uint32_t a_kstep = p.a_kstep16, b_slot16 = p.b_slot_bytes >> 4;
+        // second tile of a work item: 16 output rows (= 16 SBO strides) further down
+        const uint32_t a_tile16 = (16 * p.a_sbo) >> 4;
         const int nk16 = p.cg / 16;
         const bool do_mma = !(p.dbg & 4);
         int a_it = 0, b_it = 0, acc_it = 0;
@@ -247,13 +259,13 @@ __global__ void __launch_bounds__(192, 1)
                 mbar_wait(b_res, 0);
                 res_ready = true;
             }
-            const int acc = acc_it & 1;
+            const int acc = acc_it % NB;
             const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && lane == 0;
             if (tr) p.dbg_out[acc_it * 8 + 0] = clock64();
-            if (acc_it >= 2) mbar_wait(&acc_empty[acc], ((acc_it >> 1) - 1) & 1);
+            if (acc_it >= NB) mbar_wait(&acc_empty[acc], ((acc_it / NB) - 1) & 1);
             if (tr) p.dbg_out[acc_it * 8 + 1] = clock64();
             tc_fence_after();
-            const uint32_t d_tmem = tmem + acc * acc_cols;
+            const uint32_t d_tmem = tmem + acc * buf_cols;
             for (int g = g0; g < g1; ++g) {
                 const int s = a_it % p.a_stages;
                 mbar_wait(&a_full[s], (a_it / p.a_stages) & 1);
@@ -263,17 +275,18 @@ __global__ void __launch_bounds__(192, 1)
                 if (p.b_resident) {
                     if (elect_one()) {
                         uint64_t bd = b_desc0 + (uint32_t)((g - g0) * p.T) * b_slot16;
-                        if (!do_mma ||
-                            !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16, idesc, g == g0)) {
+                        if (!do_mma || !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
+                                                         idesc, g == g0, acc_cols, a_tile16)) {
                         uint64_t arow = a_stage;
                         for (int th = 0; th < p.kh; ++th) {
                             for (int tw = 0; tw < p.kw; ++tw) {
                                 const uint64_t ad = arow + (uint32_t)(tw >> p.s_shift) * p.a_col16 +
                                                     (uint32_t)(tw & p.s_shift) * p.a_par16;
                                 for (int k16 = 0; k16 < nk16; ++k16)
-                                    if (do_mma)
-                                        mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
-                                                 ((g - g0) | th | tw | k16) != 0);
+                                    for (int tt = 0; tt < p.tpw; ++tt)
+                                        if (do_mma)
+                                            mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
+                                                     bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
                                 bd += b_slot16;
                             }
                             arow += p.a_row16;
@@ -294,9 +307,10 @@ __global__ void __launch_bounds__(192, 1)
                                                 (uint32_t)(tw & p.s_shift) * p.a_par16;
                             const uint64_t bd = b_desc0 + (uint32_t)sb * b_slot16;
                             for (int k16 = 0; k16 < nk16; ++k16)
-                                if (do_mma)
-                                    mma_bf16(d_tmem, ad + k16 * a_kstep, bd + 2 * k16, idesc,
-                                             ((g - g0) | t | k16) != 0);
+                                for (int tt = 0; tt < p.tpw; ++tt)
+                                    if (do_mma)
+                                        mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
+                                                 bd + 2 * k16, idesc, ((g - g0) | t | k16) != 0);
                             mma_commit(&b_empty[sb]);
                         }
                         __syncwarp();
@@ -320,18 +334,19 @@ __global__ void __launch_bounds__(192, 1)
         int acc_it = 0;
         for (int u = tile0; u < total; u += tile_step) {
             const TileCoord c = decode(p, u);
-            const int acc = acc_it & 1;
+            const int acc = acc_it % NB;
             const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
             if (tr) p.dbg_out[acc_it * 8 + 4] = clock64();
-            mbar_wait(&acc_full[acc], (acc_it >> 1) & 1);
+            mbar_wait(&acc_full[acc], (acc_it / NB) & 1);
             if (tr) p.dbg_out[acc_it * 8 + 5] = clock64();
             tc_fence_after();
-            const int i = c.i0 + ti, j = c.j0 + tj;
+            for (int tt = 0; tt < p.tpw; ++tt) {
+            const int i = c.i0 + tt * 16 + ti, j = c.j0 + tj;
             const bool valid = i < p.rect[c.r].h0 + p.rect[c.r].nh && j < p.rect[c.r].w0 + p.rect[c.r].nw;
             __nv_bfloat16 *orow = p.out + (long long)c.n * p.out_sn +
                                   (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
                                   (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0;
-            const uint32_t t_lane = tmem + acc * acc_cols + ((uint32_t)(eq * 32) << 16);
+            const uint32_t t_lane = tmem + acc * buf_cols + tt * acc_cols + ((uint32_t)(eq * 32) << 16);
             float *wrow = ks > 1 ? p.ws + (long long)split * p.nsamples * p.ws_h * p.ws_w * p.nout_p +
                                        (((long long)c.n * p.ws_h + i) * p.ws_w + j) * p.nout_p + c.o0
                                  : nullptr;
@@ -362,6 +377,7 @@ __global__ void __launch_bounds__(192, 1)
                     dst[1] = hi;
                 }
             }
+            }  // tt
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
@@ -391,7 +407,9 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     p.ncg = p.cin_p / p.cg;
     const int TW = 1 << p.tw_log2, TH = 128 >> p.tw_log2;
     if (TW != 8 && !(TW == 128 && p.s_in == 1)) return false;
-    p.PH = p.s_in * (TH - 1) + kh;
+    if (p.tpw < 1) p.tpw = 1;
+    if (TW != 8) p.tpw = 1;
+    p.PH = p.s_in * (TH * p.tpw - 1) + kh;
     static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
     const int pitch = TW == 8 ? 16 : 136;  // pixels per smem row: a multiple of 8 (swizzle atom)
     if (!force_planes && TW + (kw - 1) / p.s_in <= pitch && pitch * p.s_in <= 256) {
@@ -447,6 +465,13 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
             p.b_stages = std::min(8, (smem_limit - fixed - p.a_stage_bytes) / p.b_slot_bytes);
         }
         if (p.b_stages < 2) return false;
+        // streamed weights: let a work item cover two stacked 16 x 8 tiles that
+        // share every weight stage (halves the L2 weight traffic per FLOP)
+        if (p.tpw == 1 && TW == 8 && !std::getenv("DC_V2_TPW1")) {
+            ConvV2Params q = p;
+            q.tpw = 2;
+            if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) p = q;
+        }
     }
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
 }

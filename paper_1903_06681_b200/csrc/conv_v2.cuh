@@ -39,6 +39,8 @@ struct ConvV2Params {
     //   th*a_row16 + (tw >> s_shift)*a_col16 + (tw & (s_in-1))*a_par16
     int kh, kw, s_shift;
     uint32_t a_row16, a_col16, a_par16;
+    int tpw;                       // tiles per work item (1, or 2 stacked 16 x 8 tiles sharing
+                                   // each streamed weight stage; set by conv_v2_configure)
     int tw_log2;                   // GEMM tile: (128 >> tw_log2) rows x (1 << tw_log2) cols:
                                    // 3 -> 16 x 8 (default), 7 -> 1 x 128 (thin boundary strips)
     uint32_t a_sbo;                // A descriptor SBO: byte distance between 8-pixel groups
