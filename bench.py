@@ -302,24 +302,26 @@ def main():
             if events is not None:
                 events[i][0].record(stream)
             dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)
+            if events is not None:
+                events[i][1].record(stream)
             # spatially aggregated BN statistics of the layer output
             dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp)
             if events is not None:
-                events[i][1].record(stream)
+                events[i][2].record(stream)
             if world == 1:
                 # no halo / allreduce at one rank: the two backward kernels are
                 # called separately so each gets its own event pair
                 dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["dw"], FLAGS, sp)
                 if events is not None:
-                    events[i][2].record(stream)
+                    events[i][3].record(stream)
                 dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"], FLAGS, sp)
             else:
                 dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"], d["dx"], d["dw"],
                                FLAGS, sp)
                 if events is not None:
-                    events[i][2].record(stream)
+                    events[i][3].record(stream)
             if events is not None:
-                events[i][3].record(stream)
+                events[i][4].record(stream)
             if e2e:
                 d["host"]["dw"].copy_(d["dw"], non_blocking=True)
 
@@ -332,7 +334,7 @@ def main():
             step()
         torch.cuda.synchronize()
         # ---- timed region: exactly K steps ----
-        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in L] for _ in range(args.steps)]
+        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in L] for _ in range(args.steps)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(local)
         clocks.start()
@@ -374,7 +376,8 @@ def main():
         return statistics.mean(ev[k][i][a].elapsed_time(ev[k][i][b]) for k in range(args.steps))
     per = []
     for i, d in enumerate(L):
-        f_ms, w_ms, x_ms = avg(i, 0, 1), avg(i, 1, 2), avg(i, 2, 3)
+        f_ms, bn_ms, w_ms, x_ms = avg(i, 0, 1), avg(i, 1, 2), avg(i, 2, 3), avg(i, 3, 4)
+        d["bn_ms"] = bn_ms
         per.append((d, f_ms, w_ms, x_ms))
     peaks, peak_src = load_peaks()
     # dominant kernel: the (layer, op) with the largest device time
@@ -418,7 +421,8 @@ def main():
             "config": {"workload": args.workload, "global_batch": layers[0][1],
                        "layers": [{"name": d["l"][0], "shape_NCHW_F_K_S_P": list(d["l"][1:]),
                                    "decomp": list(d["decomp"]), "model_pred_ms": d["pred"] * 1e3,
-                                   "fwd_ms": f_ms, "bwd_ms": w_ms + x_ms, "bwd_filter_ms": w_ms,
+                                   "fwd_ms": f_ms, "bn_stats_ms": d["bn_ms"], "bwd_ms": w_ms + x_ms,
+                                   "bwd_filter_ms": w_ms,
                                    "bwd_data_ms": x_ms,
                                    "fwd_tflops": layer_flops(d["l"]) / (f_ms / 1e3) / 1e12,
                                    "bwd_tflops": 2 * layer_flops(d["l"]) / ((w_ms + x_ms) / 1e3) / 1e12}

@@ -70,7 +70,7 @@ int bn_partial_blocks(long long npix, int cpad) {
     const int vecs = cpad / 8;
     const int pix_per_iter = std::max(1, kBnThreads / vecs);
     const long long iters = (npix + pix_per_iter - 1) / pix_per_iter;
-    return (int)std::max<long long>(1, std::min<long long>(iters, 148 * 2));
+    return (int)std::max<long long>(1, std::min<long long>(iters / 8 + 1, 148 * 8));
 }
 
 __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t,
@@ -86,15 +86,43 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
         double s[8], q[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) s[e] = q[e] = 0.0;
-        for (long long p = (long long)blockIdx.x * pix_lanes + pl; p < npix;
-             p += (long long)gridDim.x * pix_lanes) {
-            const uint4 raw = t[p * vecs + v];
+        // 4 independent 16-byte loads in flight per thread (memory-level
+        // parallelism), then fp64 accumulation (x^2 of a bf16 is exact in fp32)
+        // groups of 8 pixels are summed in fp32 (|x| <= 1 values; group error
+        // <= 8 * 2^-24) and flushed to the fp64 accumulators once per group
+        const long long step = (long long)gridDim.x * pix_lanes;
+        long long p = (long long)blockIdx.x * pix_lanes + pl;
+        for (; p + 7 * step < npix; p += 8 * step) {
+            uint4 raw[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) raw[u] = __ldg(&t[(p + u * step) * vecs + v]);
+            float fs[8], fq[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) fs[e] = fq[e] = 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&raw[u]);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const float x = __bfloat162float(h[e]);
+                    fs[e] += x;
+                    fq[e] = fmaf(x, x, fq[e]);
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                s[e] += (double)fs[e];
+                q[e] += (double)fq[e];
+            }
+        }
+        for (; p < npix; p += step) {
+            const uint4 raw = __ldg(&t[p * vecs + v]);
             const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&raw);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const double x = (double)__bfloat162float(h[e]);
-                s[e] += x;
-                q[e] += x * x;
+                const float x = __bfloat162float(h[e]);
+                s[e] += (double)x;
+                q[e] += (double)(x * x);
             }
         }
         double *row = sh + (long long)pl * 2 * cpad;
@@ -113,13 +141,17 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
 }
 
 // Fixed-order reduction of the per-block partials (deterministic).
+// One warp per output value: lane l sums the partials of blocks l, l+32, ...
+// (independent loads in flight), then a fixed xor-shuffle tree (deterministic).
 __global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks, int n2,
                                  double *__restrict__ out) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int b = 0; b < blocks; ++b) acc += partials[(long long)b * n2 + i];
-        out[i] = acc;
-    }
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= n2) return;
+    double acc = 0.0;
+    for (int b = lane; b < blocks; b += 32) acc += __ldg(&partials[(long long)b * n2 + warp]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) out[warp] = acc;
 }
 
 void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
@@ -132,7 +164,7 @@ void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *pa
         reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn sums launch: %s", cudaGetErrorString(e));
-    bn_reduce_kernel<<<(2 * cpad + 255) / 256, 256, 0, st>>>(partials, blocks, 2 * cpad, out);
+    bn_reduce_kernel<<<(2 * cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, 2 * cpad, out);
     e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
     g_launches += 2;
