@@ -747,6 +747,30 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
 // ---------------------------------------------------------------------------
 // backward-filter
 // ---------------------------------------------------------------------------
+// Split-K factor of the tile-reuse wgrad kernel from a small cost model:
+// a CTA spends max(MMA issue, TMA bytes at its share of L2 bandwidth) per
+// 8x8 pixel block (MMA 128xNx16 ~ 27 + 0.41 N cycles, measured with
+// tools/mbar_bench.cu), CTAs beyond one per SM run in further waves, and every
+// split costs one more fp32 partial of dW written and read back by the reduce.
+int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split) {
+    const int sms = device_sm_count();
+    const double mma_ns = 4.0 * q.G * (27.0 + 0.41 * q.bn) / 1.9;
+    const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
+    int best = 1;
+    double best_t = 1e30;
+    for (int s = 1; s <= std::min(q.nblocks, 256); ++s) {
+        if ((size_t)s * per_split * 4 > ((size_t)1 << 30)) break;
+        const long long active = std::min<long long>((long long)ctas * s, sms);
+        const double bw = std::min(200.0, 7000.0 / (double)active);  // GB/s = bytes/ns per SM
+        const double blk_ns = std::max(mma_ns, stage_bytes / bw);
+        const long long waves = ceil_div((long long)ctas * s, (long long)sms);
+        double t = (double)waves * (double)ceil_div((long long)q.nblocks, (long long)s) * blk_ns;
+        t += s > 1 ? 2.0 * s * 4.0 * (double)per_split / 6500.0 + 3000.0 : 0.0;
+        if (t < best_t * 0.97) best_t = t, best = s;
+    }
+    return best;
+}
+
 void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cudaStream_t st) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
@@ -754,7 +778,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     const int64_t ho = rp.h.out.size(), wo = rp.w.out.size(), nl = rp.nrange.size();
     const __nv_bfloat16 *dy_owned = reinterpret_cast<const __nv_bfloat16 *>(dy) +
                                     (dyd.halo_n * dyd.wb + dyd.halo_w) * g.Fp;
-    if (!use_v1() && g.Cp % 64 == 0 && g.Fp % 64 == 0) {
+    if (!use_v1() && g.Fp % 64 == 0) {
         // tile-reuse kernel (wgrad_v2.cu)
         WgradV2Params q;
         std::memset(&q, 0, sizeof q);
@@ -768,11 +792,9 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
             q.tiles_h = (int)ceil_div(ho, 8);
             q.tiles_w = (int)ceil_div(wo, 8);
             q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
-            const int mgroups = (int)ceil_div(q.n_mtiles, q.G), ntiles = (int)ceil_div(g.Fp, q.bn);
+            const int mgroups = wgrad_v2_mgroups(q), ntiles = (int)ceil_div(g.Fp, q.bn);
             const long long per_split = (long long)g.F * q.T * g.Cp;
-            int splits = (int)ceil_div(device_sm_count(), (int64_t)mgroups * ntiles);
-            splits = std::max(1, std::min(splits, std::max(1, q.nblocks / 2)));
-            while (splits > 1 && (size_t)splits * per_split * 4 > ((size_t)1 << 30)) --splits;
+            const int splits = wgrad_splits(q, mgroups * ntiles, per_split);
             q.splits = splits;
             q.ws_split = per_split;
             if (splits > 1) {
@@ -786,9 +808,9 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
                 const uint64_t dims[4] = {(uint64_t)g.Cp, (uint64_t)xd.wb, (uint64_t)xd.hb, (uint64_t)xd.n};
                 const uint64_t strides[3] = {(uint64_t)(g.Cp * 2), (uint64_t)(xd.wb * g.Cp * 2),
                                              (uint64_t)(xd.hb * xd.wb * g.Cp * 2)};
-                const uint32_t box[4] = {64, (uint32_t)(16 * g.S), (uint32_t)q.PH, 1};
+                const uint32_t box[4] = {(uint32_t)q.cgw, (uint32_t)(q.pitch * g.S), (uint32_t)q.PH, 1};
                 const uint32_t es[4] = {1, (uint32_t)g.S, 1, 1};
-                make_tmap(&xmap, x, 4, dims, strides, box, es, 128);
+                make_tmap(&xmap, x, 4, dims, strides, box, es, q.cgw * 2);
             }
             {
                 const uint64_t dims[4] = {(uint64_t)g.Fp, (uint64_t)wo, (uint64_t)ho, (uint64_t)nl};

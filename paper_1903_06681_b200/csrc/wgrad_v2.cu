@@ -3,13 +3,19 @@
 //   D[(tap, c), f] = sum over the owned output pixels of X_tap[pixel, c] * DY[pixel, f]
 // K = output pixels, processed in blocks of 8 output rows x 8 output cols.
 // For each block the x tile that ALL taps read is loaded once into shared
-// memory (128B-swizzled rows of 64 channels, row pitch 16 pixels, one plane
-// per column parity for stride 2); an "MN atom" of the A operand is 64
-// channels of one tap, i.e. the same tile at a shifted start address, and an
-// M = 128 tile pairs two atoms (LBO = their distance). dy (without halo,
-// PAPER.md:143) is streamed once per block. A CTA keeps the accumulators of
-// all its M tiles in TMEM across its whole split-K range; partial sums go to
-// a workspace reduced in a fixed order (splitk_reduce_kernel).
+// memory (swizzled rows of cgw channels, row pitch 8+(kw-1)/s pixels, one plane per
+// column parity for stride 2). An "MN atom" of the A operand is cgw channels
+// of one tap, i.e. the same tile at a shifted start address; an M = 128 tile
+// stacks 128/cgw atoms at a uniform distance (LBO):
+//   mode 0 (cgw = 64, >= 2 taps): two taps of one channel group (any pair;
+//          LBO = their distance, the lower address first);
+//   mode 1 (cgw = 16/32): 128/cgw taps of one filter column (th, th+1, ...):
+//          LBO = one input row of the tile; taps past the filter are phantoms;
+//   mode 2 (1x1, cgw = 64): the single tap of two channel groups.
+// dy (without halo) is streamed once per block. A CTA keeps
+// the accumulators of all its M tiles in TMEM across its split-K range;
+// partial sums go to a workspace reduced in a fixed order
+// (splitk_reduce_kernel) -> deterministic.
 #include <algorithm>
 #include <mutex>
 
@@ -25,6 +31,45 @@ namespace {
 __device__ __forceinline__ uint8_t *align1024w(uint8_t *p) {
     const uint32_t a = smem_u32(p);
     return p + ((1024 - (a & 1023)) & 1023);
+}
+
+// Atom `a` (0 .. 128/cgw - 1) of M tile `mt`: its tap (or -1: phantom) and
+// channel group, and its byte offset inside the CTA's x stage.
+struct Atom {
+    int tap, cg;
+    uint32_t off;
+};
+__host__ __device__ inline Atom atom_of(const WgradV2Params &p, int mt, int a, int cg_lo) {
+    Atom r{-1, 0, 0};
+    const int A = 128 / p.cgw;
+    auto offset = [&](int cg, int th, int tw) -> uint32_t {
+        return (uint32_t)(((cg - cg_lo) * p.s_in + (tw % p.s_in)) * p.x_plane_bytes +
+                          (th * p.pitch + tw / p.s_in) * p.cgw * 2);
+    };
+    if (p.mode == 2) {  // 1x1: channel groups 2mt, 2mt+1
+        const int cg = 2 * mt + a;
+        r.cg = cg < p.ncg ? cg : 2 * mt;
+        r.tap = cg < p.ncg ? 0 : -1;
+        r.off = offset(r.cg, 0, 0);
+    } else if (p.mode == 0) {  // pairs of taps inside one channel group
+        const int per = (p.T + 1) / 2;
+        const int cg = mt / per, pair = mt % per;
+        const int t = 2 * pair + a;
+        r.cg = cg;
+        r.tap = t < p.T ? t : -1;
+        const int tt = t < p.T ? t : 2 * pair;
+        r.off = offset(cg, tt / p.kw, tt % p.kw);
+    } else {  // filter column tw, taps th = thb*A + a
+        const int nthb = (p.kh + A - 1) / A;
+        const int per = p.kw * nthb;
+        const int cg = mt / per, rem = mt % per;
+        const int tw = rem % p.kw, thb = rem / p.kw;
+        const int th = thb * A + a;
+        r.cg = cg;
+        r.tap = th < p.kh ? th * p.kw + tw : -1;
+        r.off = offset(cg, th, tw);  // phantom rows exist in the tile (PH padded)
+    }
+    return r;
 }
 }  // namespace
 
@@ -44,13 +89,21 @@ __global__ void __launch_bounds__(192, 1)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
-    const int mg = blockIdx.x, f0 = blockIdx.y * p.bn, split = blockIdx.z;
-    const int mt0 = mg * p.G;
-    const int G = min(p.G, p.n_mtiles - mt0);
-    const int a_lo = 2 * mt0;
-    const int cg_lo = a_lo / p.T;
-    const int a_hi = min(2 * (mt0 + G), p.natoms) - 1;
-    const int cg_hi = a_hi / p.T;
+    const int A = 128 / p.cgw;
+    // this CTA's M tiles: [mt0, mt0 + G) (never crossing a channel group in modes 0/1)
+    const int f0 = blockIdx.y * p.bn, split = blockIdx.z;
+    int mt0, G;
+    if (p.mode == 2) {
+        mt0 = blockIdx.x * p.G;
+        G = min(p.G, p.n_mtiles - mt0);
+    } else {
+        const int per_cg = p.n_mtiles / p.ncg, groups = (per_cg + p.G - 1) / p.G;
+        const int cg = blockIdx.x / groups, gi = blockIdx.x % groups;
+        mt0 = cg * per_cg + gi * p.G;
+        G = min(p.G, per_cg - gi * p.G);
+    }
+    const int cg_lo = atom_of(p, mt0, 0, 0).cg;
+    const int cg_hi = p.mode == 2 ? min(p.ncg, 2 * (mt0 + G)) - 1 : cg_lo;
     const int ncg = cg_hi - cg_lo + 1;
     const int b_begin = (int)((long long)split * p.nblocks / p.splits);
     const int b_end = (int)((long long)(split + 1) * p.nblocks / p.splits);
@@ -78,7 +131,7 @@ __global__ void __launch_bounds__(192, 1)
             tma_prefetch(&dymap);
         }
         const int per_n = p.tiles_h * p.tiles_w;
-        const uint32_t x_bytes = ncg * p.s_in * p.PH * 16 * 128;
+        const uint32_t x_bytes = ncg * p.s_in * p.PH * p.pitch * p.cgw * 2;  // bytes the boxes deliver
         const uint32_t d_bytes = (p.bn / 64) * 64 * 64 * 2;
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % p.stages;
@@ -93,7 +146,7 @@ __global__ void __launch_bounds__(192, 1)
                 for (int c = 0; c < ncg; ++c)
                     for (int par = 0; par < p.s_in; ++par)
                         tma_load_4d(xs + (c * p.s_in + par) * p.x_plane_bytes, &xmap, &full[s],
-                                    (cg_lo + c) * 64, w0 + par, h0, n);
+                                    (cg_lo + c) * p.cgw, w0 + par, h0, n);
                 uint8_t *ds = sD + s * p.dy_stage_bytes;
                 for (int q = 0; q < p.bn / 64; ++q)
                     tma_load_4d(ds + q * 64 * 64 * 2, &dymap, &full[s], f0 + q * 64, j0, i0, n);
@@ -102,30 +155,25 @@ __global__ void __launch_bounds__(192, 1)
         }
     } else if (warp == 1) {
         // ===================== tcgen05.mma issuer (warp-uniform) =====================
-        // A (x, MN-major SW128): atom = 64 channels of one tap; K rows = 8 output
-        // pixels of one output row (128 B each); SBO = next output row.
-        const uint32_t a_sbo = p.s_in * 16 * 128;
+        // A (x, MN-major, swizzle = cgw*2 bytes): K rows = 8 output pixels of one
+        // output row (cgw*2 bytes each); SBO = next output row; LBO = next atom.
+        const uint32_t a_sbo = p.s_in * p.pitch * p.cgw * 2;
+        const uint32_t layout = swizzle_layout(p.cgw * 2);
         uint64_t adesc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             adesc[i] = 0;
             if (i < G) {
-                int a0 = 2 * (mt0 + i), a1 = a0 + 1;
-                if (a1 >= p.natoms) a1 = a0;
-                auto off = [&](int a) -> uint32_t {
-                    const int cg = a / p.T, t = a - cg * p.T;
-                    const int th = t / p.kw, tw = t - th * p.kw;
-                    return (uint32_t)(((cg - cg_lo) * p.s_in + (tw % p.s_in)) * p.x_plane_bytes +
-                                      (th * 16 + tw / p.s_in) * 128);
-                };
-                uint32_t o0 = off(a0), o1 = off(a1);
-                const bool swap = o1 < o0;
-                if (swap) {
-                    const uint32_t t = o0;
-                    o0 = o1;
-                    o1 = t;
+                const Atom a0 = atom_of(p, mt0 + i, 0, cg_lo), a1 = atom_of(p, mt0 + i, 1, cg_lo);
+                uint32_t lo = a0.off, lbo;
+                if (p.mode == 0) {  // arbitrary pair: lower address first
+                    lo = min(a0.off, a1.off);
+                    lbo = max(a0.off, a1.off) - lo;
+                    if (lbo == 0) lbo = 16;  // phantom partner: rows discarded
+                } else {
+                    lbo = a1.off - a0.off;  // uniform spacing (input row / channel group)
                 }
-                adesc[i] = smem_desc(smem_u32(sX) + o0, o1 - o0 > 0 ? o1 - o0 : 16, a_sbo, 2);
+                adesc[i] = smem_desc(smem_u32(sX) + lo, lbo, a_sbo, layout);
             }
         }
         // B (dy, MN-major SW128): atom = 64 filters; K rows = 8 pixels x 128 B;
@@ -163,22 +211,16 @@ __global__ void __launch_bounds__(192, 1)
         float *wsb = p.ws + (long long)split * p.ws_split;
         const long long fstride = (long long)p.T * p.cp;
         for (int i = 0; i < G; ++i) {
-            int a0 = 2 * (mt0 + i), a1 = a0 + 1;
-            const bool phantom = a1 >= p.natoms;
-            if (phantom) a1 = a0;
-            // recompute the pair order the issuer used
-            auto off = [&](int a) -> uint32_t {
-                const int cg = a / p.T, t = a - cg * p.T;
-                const int th = t / p.kw, tw = t - th * p.kw;
-                return (uint32_t)(((cg - cg_lo) * p.s_in + (tw % p.s_in)) * p.x_plane_bytes +
-                                  (th * 16 + tw / p.s_in) * 128);
-            };
-            const bool swap = off(a1) < off(a0);
-            const int a = (m < 64) == !swap ? a0 : a1;  // rows 0-63: the atom at the lower address
-            const bool valid = !(phantom && m >= 64);
-            const int cg = a / p.T, t = a - cg * p.T;
-            const int c = cg * 64 + (m & 63);
-            float *wrow = wsb + (long long)t * p.cp + c;
+            const Atom a0 = atom_of(p, mt0 + i, 0, cg_lo);
+            int ai = m / p.cgw;
+            if (p.mode == 0) {  // rows 0-63 hold the atom at the lower address
+                const Atom a1 = atom_of(p, mt0 + i, 1, cg_lo);
+                if (a1.off < a0.off) ai = 1 - ai;
+            }
+            const Atom at = atom_of(p, mt0 + i, ai, cg_lo);
+            const int c = at.cg * p.cgw + (m % p.cgw);
+            const bool valid = at.tap >= 0 && c < p.cp;
+            float *wrow = wsb + (long long)(valid ? at.tap : 0) * p.cp + c;
             const uint32_t t_lane = tmem + i * p.bn_cols + ((uint32_t)(eq * 32) << 16);
             for (int c16 = 0; c16 < p.bn / 16; ++c16) {
                 uint32_t v[16];
@@ -189,7 +231,7 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0;
                 }
-                if (valid && c < p.cp) {
+                if (valid) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
                         const int f = f0 + c16 * 16 + e;
@@ -198,6 +240,7 @@ __global__ void __launch_bounds__(192, 1)
                 }
             }
         }
+        (void)A;
     }
     tc_fence_before();
     __syncthreads();
@@ -208,31 +251,48 @@ size_t wgrad_v2_smem_bytes(const WgradV2Params &p) {
     return 1024 + (size_t)p.stages * (p.x_stage_bytes + p.dy_stage_bytes) + (2 * kWMaxStages + 1) * 8 + 16;
 }
 
+int wgrad_v2_mgroups(const WgradV2Params &p) {
+    if (p.mode == 2) return (p.n_mtiles + p.G - 1) / p.G;
+    const int per_cg = p.n_mtiles / p.ncg;
+    return p.ncg * ((per_cg + p.G - 1) / p.G);
+}
+
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
-    if (p.cp % 64 != 0 || p.Fp % 64 != 0 || p.kh * p.kw != p.T) return false;
-    p.PH = p.s_in * 7 + p.kh;
-    if (p.PH > 256 || 8 + (p.kw - 1) / p.s_in > 16) return false;
-    p.x_plane_bytes = p.PH * 16 * 128;
+    if (p.Fp % 64 != 0 || p.kh * p.kw != p.T) return false;
+    p.cgw = p.cp % 64 == 0 ? 64 : p.cp % 32 == 0 ? 32 : 16;
+    p.ncg = p.cp / p.cgw;
+    if (8 + (p.kw - 1) / p.s_in > 32) return false;
+    const int A = 128 / p.cgw;
+    if (p.T == 1 && p.cgw == 64) {
+        p.mode = 2;
+        p.n_mtiles = (p.ncg + 1) / 2;
+    } else if (p.cgw == 64) {
+        p.mode = 0;
+        p.n_mtiles = p.ncg * ((p.T + 1) / 2);
+    } else {
+        p.mode = 1;
+        p.n_mtiles = p.ncg * p.kw * ((p.kh + A - 1) / A);
+    }
+    // tile rows: 8 output rows -> s*7 + kh input rows (+ phantom rows of mode 1)
+    const int kh_alloc = p.mode == 1 ? ((p.kh + A - 1) / A) * A : p.kh;
+    p.PH = p.s_in * 7 + kh_alloc;
+    if (p.PH > 256) return false;
+    // row pitch = the 8 + (kw-1)/s columns one parity plane needs; the
+    // swizzle is a function of the smem address, so rows need not start on
+    // a swizzle-atom boundary (only 16-byte alignment)
+    p.pitch = 8 + (p.kw - 1) / p.s_in;
+    p.x_plane_bytes = (p.PH * p.pitch * p.cgw * 2 + 1023) / 1024 * 1024;
     p.bn = p.Fp <= 256 ? p.Fp : 256;
     p.bn_cols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
-    p.natoms = (p.cp / 64) * p.T;
-    p.n_mtiles = (p.natoms + 1) / 2;
     p.G = std::max(1, std::min(8, 512 / p.bn_cols));
-    // channel groups an M group can touch: atoms [2 mt0, 2 mt0 + 2G) span
-    const int span_atoms = 2 * p.G;
-    const int ncg_max = std::min(p.cp / 64, (span_atoms + p.T - 2) / p.T + 1);
-    p.x_stage_bytes = ncg_max * p.s_in * p.x_plane_bytes;
     p.dy_stage_bytes = (p.bn / 64) * 64 * 64 * 2;
     const int fixed = 1024 + (2 * kWMaxStages + 1) * 8 + 16;
-    p.stages = std::min(kWMaxStages, (smem_limit - fixed) / (p.x_stage_bytes + p.dy_stage_bytes));
-    if (p.stages < 2) {
-        // fewer M tiles per CTA -> fewer channel groups per stage
-        while (p.G > 1 && p.stages < 2) {
-            p.G /= 2;
-            const int ncg2 = std::min(p.cp / 64, (2 * p.G + p.T - 2) / p.T + 1);
-            p.x_stage_bytes = ncg2 * p.s_in * p.x_plane_bytes;
-            p.stages = std::min(kWMaxStages, (smem_limit - fixed) / (p.x_stage_bytes + p.dy_stage_bytes));
-        }
+    for (;;) {
+        const int ncg_stage = p.mode == 2 ? std::min(p.ncg, 2 * p.G) : 1;
+        p.x_stage_bytes = (ncg_stage * p.s_in * p.x_plane_bytes + 1023) / 1024 * 1024;
+        p.stages = std::min(kWMaxStages, (smem_limit - fixed) / (p.x_stage_bytes + p.dy_stage_bytes));
+        if (p.stages >= 2 || p.G == 1) break;
+        p.G /= 2;
     }
     return p.stages >= 2;
 }
@@ -243,9 +303,9 @@ void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const Wg
     std::call_once(once, [] {
         cudaFuncSetAttribute(wgrad_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
-    const int mgroups = (p.n_mtiles + p.G - 1) / p.G;
     const int ntiles = (p.Fp + p.bn - 1) / p.bn;
-    wgrad_v2_kernel<<<dim3(mgroups, ntiles, p.splits), 192, wgrad_v2_smem_bytes(p), st>>>(xmap, dymap, p);
+    wgrad_v2_kernel<<<dim3(wgrad_v2_mgroups(p), ntiles, p.splits), 192, wgrad_v2_smem_bytes(p), st>>>(
+        xmap, dymap, p);
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "wgrad_v2 launch: %s", cudaGetErrorString(e));
     ++g_launches;

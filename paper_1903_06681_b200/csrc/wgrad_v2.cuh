@@ -9,11 +9,13 @@ namespace dc {
 struct WgradV2Params {
     int s_in, origin_h, origin_w;  // x coord of output pixel (0,0) at tap offset 0
     int kh, kw, T;                 // tap grid (T = kh * kw)
-    int PH;                        // x tile rows = s_in * 7 + kh (8 output rows per block)
-    int x_plane_bytes;             // PH * 16 px * 128 B
+    int cgw, ncg, mode;            // channel-group width (16/32/64), groups, M-tile mode (see .cu)
+    int PH;                        // x tile rows = s_in * 7 + kh (+ phantom rows, mode 1)
+    int pitch;                     // pixels per tile row (per parity plane)
+    int x_plane_bytes;             // PH * pitch * cgw * 2 B, rounded up to 1 KB
     int x_stage_bytes, dy_stage_bytes, stages;
     int bn, bn_cols;               // N tile (filters) and its TMEM column stride
-    int natoms, n_mtiles, G;       // (cp/64)*T atoms of 64 channels; M tiles = atom pairs; per CTA
+    int n_mtiles, G;               // M = 128 tiles (atoms stacked), M tiles per CTA
     int tiles_h, tiles_w, nblocks; // 8x8 output-pixel blocks per sample, total
     int splits;
     float *ws;                     // [splits][F][T][cp] fp32
@@ -23,8 +25,9 @@ struct WgradV2Params {
 
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit);
 size_t wgrad_v2_smem_bytes(const WgradV2Params &p);
-// xmap: 4D over the x buffer, box {64, 16 * s_in, PH, 1}, element strides
-// {1, s_in, 1, 1}, 128B swizzle. dymap: 4D over the OWNED dy block, box
+int wgrad_v2_mgroups(const WgradV2Params &p);  // grid.x
+// xmap: 4D over the x buffer, box {cgw, pitch * s_in, PH, 1}, element strides
+// {1, s_in, 1, 1}, swizzle cgw * 2 bytes. dymap: 4D over the OWNED dy block, box
 // {64, 8, 8, 1}, 128B swizzle.
 void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const WgradV2Params &p,
                      cudaStream_t st);

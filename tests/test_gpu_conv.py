@@ -78,6 +78,9 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     (1, 192, 10, 10, 64, 1, 2, 0),     # 1x1 stride 2, three channel groups (odd atom count)
     (2, 64, 20, 20, 128, 5, 1, 2),     # K=5 (25 taps)
     (1, 512, 16, 18, 256, 3, 1, 1),    # deep layer: split-K over 8 channel groups
+    (1, 32, 21, 19, 128, 3, 1, 1),     # wgrad mode 1: 32-channel atoms stacked along th
+    (2, 16, 13, 15, 64, 5, 1, 2),      # wgrad mode 1: 16-channel atoms, phantom taps
+    (1, 256, 12, 14, 128, 3, 2, 1),    # wgrad mode 0, stride 2, four channel groups
 ]
 
 
