@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(192, 1)
                         mbar_arrive(&a_full[s]);
                     } else if (p.a_swz) {
                         // one box per column parity: PH rows x PWs cols x cg channels
-                        mbar_arrive_expect_tx(&a_full[s], p.s_in * p.plane_bytes);
+                        mbar_arrive_expect_tx(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
                         for (int par = 0; par < p.s_in; ++par)
                             tma_load_4d(dst + par * p.plane_bytes, &amap, &a_full[s], g * p.cg,
                                         w0 + par, h0, c.n);
@@ -411,15 +411,17 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     if (TW != 8) p.tpw = 1;
     p.PH = p.s_in * (TH * p.tpw - 1) + kh;
     static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
-    const int pitch = TW == 8 ? 16 : 136;  // pixels per smem row: a multiple of 8 (swizzle atom)
+    static const bool wide_pitch = std::getenv("DC_V2_PITCH16") != nullptr;
+    const int pitch = wide_pitch ? (TW == 8 ? 16 : 136) : TW + (kw - 1) / p.s_in;  // pixels per smem row
     if (!force_planes && TW + (kw - 1) / p.s_in <= pitch && pitch * p.s_in <= 256) {
         // swizzled rows of cg channels (32/64/128-byte swizzle), one plane per
-        // column parity (TMA element stride = s_in); the row pitch is a multiple
-        // of 8 pixels so a tap shift only moves the start address (the swizzle
-        // is a function of the absolute smem address, measured)
+        // column parity (TMA element stride = s_in). The swizzle is a function
+        // of the absolute smem address (measured), so a tap shift only moves
+        // the start address and the row pitch can be exactly the TW + (kw-1)/s
+        // pixels a tile needs; planes start on 1 KB boundaries.
         p.a_swz = p.cg * 2;
         p.PWs = pitch;
-        p.plane_bytes = p.PH * p.PWs * p.cg * 2;
+        p.plane_bytes = (int)round_up((int64_t)p.PH * p.PWs * p.cg * 2, 1024);
         p.a_stage_bytes = p.s_in * p.plane_bytes;
         p.a_sbo = TW == 8 ? p.s_in * p.PWs * p.cg * 2 : 8 * p.cg * 2;
     } else {
