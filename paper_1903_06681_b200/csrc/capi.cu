@@ -302,6 +302,7 @@ struct GemmLaunch {
     const void *w_base = nullptr;  // B matrix [w_rows][w_kcols] (for re-tiling N)
     int64_t w_rows = 0, w_kcols = 0;
     int ksplit = 1;            // v2 split-K over channel groups (from the GLOBAL shape)
+    int64_t work_hint = 0;     // GLOBAL 16x8 tiles x N tiles (v2 tile-pairing choice)
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
 };
@@ -379,7 +380,8 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     Split2D s{rp.h.out.size(), rp.w.out.size(), count(rp.h, true), count(rp.h, false),
               count(rp.w, true), count(rp.w, false)};
     make_rects(s, L.interior, L.boundary);
-    L.ksplit = choose_ksplit(g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles, g.Cp);
+    L.work_hint = g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles;
+    L.ksplit = choose_ksplit(L.work_hint, g.Cp);
     attach_ksplit(pl, L, (int)rp.nrange.size());
 }
 
@@ -407,6 +409,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.bn = L.p.bn;
     q.nout_tiles = (int)ceil_div(L.p.nout_p, q.bn);
     q.ksplit = L.ksplit;
+    q.work_hint = (int)std::min<int64_t>(L.work_hint * L.ksplit, 1 << 30);
     q.ws = L.ws;
     q.ws_h = L.ws_h;
     q.ws_w = L.ws_w;
@@ -440,7 +443,13 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
         const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
         make_tmap(&amap, in_base, 4, dims, strides, box, es, 0);
     }
-    launch_conv_v2(amap, L.bmap, q, st);
+    if (q.cg != L.p.bkc) {  // the kernel chose narrower channel stages: re-tile the weights
+        CUtensorMap bmap;
+        weight_map(&bmap, L.w_base, L.w_rows, L.w_kcols, q.cg, q.bn);
+        launch_conv_v2(amap, bmap, q, st);
+    } else {
+        launch_conv_v2(amap, L.bmap, q, st);
+    }
     if (q.ksplit > 1) launch_conv_v2_reduce(q, st);
     return true;
 }
@@ -706,8 +715,8 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         L[i].w_base = wt, L[i].w_rows = g.Cp, L[i].w_kcols = (int64_t)std::max(f.T, 1) * g.Fp;
         Split2D s{f.nt_h, f.nt_w, f.bl, f.bh, f.bwl, f.bwh};
         make_rects(s, L[i].interior, L[i].boundary);
-        L[i].ksplit = choose_ksplit(g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) *
-                                        L[i].nout_tiles, g.Fp);
+        L[i].work_hint = g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) * L[i].nout_tiles;
+        L[i].ksplit = choose_ksplit(L[i].work_hint, g.Fp);
     }
     // one split-K workspace region per phase: the phases' interior and
     // boundary launches may run concurrently on two streams

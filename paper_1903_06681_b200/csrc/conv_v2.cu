@@ -397,13 +397,18 @@ size_t conv_v2_smem_bytes(const ConvV2Params &p) {
     return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16;
 }
 
+// Pair tiles only when the GLOBAL layer has this many tpw = 1 work items
+// (measured: pairing wins 1.5x on 128^2..512^2 layers, loses on 64^2/32^2).
+constexpr int kPairMinItems = 200;
+
 bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     int kh = 1, kw = 1;
     for (int t = 0; t < p.T; ++t) {
         kh = std::max(kh, (int)p.tap_h[t] + 1);
         kw = std::max(kw, (int)p.tap_w[t] + 1);
     }
-    p.cg = p.cin_p % 64 == 0 ? 64 : p.cin_p % 32 == 0 ? 32 : 16;
+    const int cg_nat = p.cin_p % 64 == 0 ? 64 : p.cin_p % 32 == 0 ? 32 : 16;
+    p.cg = p.cg > 0 && p.cg < cg_nat ? p.cg : cg_nat;  // a caller may ask for narrower stages
     p.ncg = p.cin_p / p.cg;
     const int TW = 1 << p.tw_log2, TH = 128 >> p.tw_log2;
     if (TW != 8 && !(TW == 128 && p.s_in == 1)) return false;
@@ -469,10 +474,17 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         if (p.b_stages < 2) return false;
         // streamed weights: let a work item cover two stacked 16 x 8 tiles that
         // share every weight stage (halves the L2 weight traffic per FLOP)
-        if (p.tpw == 1 && TW == 8 && !std::getenv("DC_V2_TPW1")) {
+        if (p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems && !std::getenv("DC_V2_TPW1")) {
             ConvV2Params q = p;
             q.tpw = 2;
-            if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) p = q;
+            if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) {
+                p = q;
+            } else if (p.cg == 64 && p.s_in == 2 && !std::getenv("DC_V2_NO_CG32")) {
+                // stride 2: a 32-row stacked tile pair is too tall for 64-channel
+                // stages; 32-channel stages make it fit (same weight reuse)
+                q.cg = 32;
+                if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) p = q;
+            }
         }
     }
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;

@@ -72,6 +72,7 @@ struct ConvV2Params {
     // and conv_v2_reduce sums them in split order. ksplit depends only on the
     // global layer shape, so partitioned results stay bitwise equal to 1 GPU.
     int ksplit;
+    int work_hint;             // work items of the GLOBAL layer at tpw = 1 (x ksplit): pairing only when plentiful
     float *ws;
     int ws_h, ws_w;
     __nv_bfloat16 *out;
