@@ -218,6 +218,8 @@ def main():
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="replay the step as a CUDA graph (auto: unless the P2P halo runs)")
     ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
     args = ap.parse_args()
     layers = WORKLOADS[args.workload]
@@ -290,8 +292,25 @@ def main():
                       dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, host=host))
     torch.cuda.synchronize()
 
-    def step(events=None, e2e=False):
-        for i, d in enumerate(L):
+    def op_calls(d):
+        """The calls of one layer, in step order: (name, fn)."""
+        ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)),
+               # spatially aggregated BN statistics of the layer output (SURVEY.md 8(a) a7)
+               ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp))]
+        if world == 1:
+            # no halo / allreduce at one rank: the two backward kernels are
+            # called separately so each gets its own timing
+            ops.append(("bpw", lambda: dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(),
+                                                             d["dw"], FLAGS, sp)))
+            ops.append(("bpx", lambda: dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"],
+                                                           FLAGS, sp)))
+        else:
+            ops.append(("bwd", lambda: dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"],
+                                                      d["dx"], d["dw"], FLAGS, sp)))
+        return ops
+
+    def step(e2e=False):
+        for d in L:
             xd, dyd = d["xd"], d["dyd"]
             if e2e:  # inputs arrive from pinned host memory every step
                 xs = d["xb"][:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]]
@@ -299,29 +318,8 @@ def main():
                 d["dyb"][:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]].copy_(
                     d["host"]["dy"], non_blocking=True)
                 d["w"].copy_(d["host"]["w"], non_blocking=True)
-            if events is not None:
-                events[i][0].record(stream)
-            dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)
-            if events is not None:
-                events[i][1].record(stream)
-            # spatially aggregated BN statistics of the layer output
-            dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp)
-            if events is not None:
-                events[i][2].record(stream)
-            if world == 1:
-                # no halo / allreduce at one rank: the two backward kernels are
-                # called separately so each gets its own event pair
-                dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["dw"], FLAGS, sp)
-                if events is not None:
-                    events[i][3].record(stream)
-                dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"], FLAGS, sp)
-            else:
-                dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"], d["dx"], d["dw"],
-                               FLAGS, sp)
-                if events is not None:
-                    events[i][3].record(stream)
-            if events is not None:
-                events[i][4].record(stream)
+            for _, f in op_calls(d):
+                f()
             if e2e:
                 d["host"]["dw"].copy_(d["dw"], non_blocking=True)
 
@@ -329,12 +327,32 @@ def main():
         if world > 1:
             dist.barrier()
 
+    # CUDA graphs: the step's ~300 launches are recorded once and replayed, so
+    # small layers are not bound by host launch cost. The P2P halo protocol
+    # carries host-side epochs, so it runs eagerly.
+    use_graph = args.graph == "on" or (args.graph == "auto" and (world == 1 or args.halo == "nccl"))
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream, capture_error_mode="thread_local"):
+            fn()
+        return g
+
     with torch.cuda.stream(stream):
         for _ in range(args.warmup):
             step()
         torch.cuda.synchronize()
+        if use_graph:
+            g_step, g_e2e = capture(step), capture(lambda: step(e2e=True))
+            g_ops = [[(name, capture(f)) for name, f in op_calls(d)] for d in L]
+            run_step, run_e2e = g_step.replay, g_e2e.replay
+            for _ in range(2):
+                run_step()
+            torch.cuda.synchronize()
+        else:
+            g_ops = None
+            run_step, run_e2e = step, lambda: step(e2e=True)
         # ---- timed region: exactly K steps ----
-        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in L] for _ in range(args.steps)]
         start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         clocks = ClockSampler(local)
         clocks.start()
@@ -343,23 +361,41 @@ def main():
         launches0 = dc.dc_kernel_launches()
         start.record(stream)
         for k in range(args.steps):
-            step(ev[k])
+            run_step()
         stop.record(stream)
         torch.cuda.synchronize()
         launches = dc.dc_kernel_launches() - launches0
         barrier()
         clk = clocks.stop()
         ms = start.elapsed_time(stop)
+        if use_graph:  # the replays launch the recorded kernels without calling the library
+            launches0 = dc.dc_kernel_launches()
+            step()
+            torch.cuda.synchronize()
+            launches = (dc.dc_kernel_launches() - launches0) * args.steps
         # ---- end-to-end leg: same steps with H2D of inputs / D2H of dW ----
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for k in range(args.steps):
-            step(e2e=True)
+            run_e2e()
         e1.record(stream)
         torch.cuda.synchronize()
         ms_e2e = e0.elapsed_time(e1)
+        # ---- per-op device times: an instrumented pass, events between ops ----
+        barrier()
+        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in L] for _ in range(args.steps)]
+        for k in range(args.steps):
+            for i, d in enumerate(L):
+                ops = g_ops[i] if g_ops else op_calls(d)
+                ev[k][i][0].record(stream)
+                for j, (name, f) in enumerate(ops):
+                    (f.replay if g_ops else f)()
+                    ev[k][i][j + 1].record(stream)
+                for j in range(len(ops) + 1, 5):
+                    ev[k][i][j].record(stream)
+        torch.cuda.synchronize()
 
     t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -429,6 +465,8 @@ def main():
                                   for d, f_ms, w_ms, x_ms in per],
                        "parallelism": "per-layer model-chosen (pN,pH,pW)" if args.decomp == "auto" else args.decomp,
                        "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
+                       "cuda_graph": use_graph,
+                       "per_layer_times": "instrumented pass after the timed region (events between ops)",
                        "flops_per_step": flops_step},
             "roofline": roof,
             "cpu_baseline": cpu,

@@ -1215,15 +1215,16 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     const long long npix = rp.nrange.size() * rp.h.out.size() * rp.w.out.size();
     const size_t need = sizeof(double) * 2 * g.Fp * bn_partial_blocks(npix, (int)g.Fp);
     ensure_alloc(pl->bn_part, pl->bn_part_bytes, need);
-    launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part,
-                   pl->bn_sums, st);
-    double count = (double)npix;
-    if (!local_only && pl->bn_group > 1) {
+    const bool global = !local_only && pl->bn_group > 1;
+    // single group: the reduce kernel also finalises mean/var (no allreduce between)
+    launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
+                   (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
+    if (global) {
         DC_REQUIRE(pl->bn_comm != nullptr, DC_ERR_ARG, "spatial BN statistics need a communicator");
         NK(ncclAllReduce(pl->bn_sums, pl->bn_sums, 2 * g.Fp, ncclFloat64, ncclSum, pl->bn_comm, st));
-        count = (double)rp.nrange.size() * g.Ho * g.Wo;
+        launch_bn_finalize(pl->bn_sums, (int)g.Fp, (int)g.F, (double)rp.nrange.size() * g.Ho * g.Wo, mean,
+                           var, st);
     }
-    launch_bn_finalize(pl->bn_sums, (int)g.Fp, (int)g.F, count, mean, var, st);
     DC_API_END
 }
 

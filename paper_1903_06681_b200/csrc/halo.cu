@@ -66,15 +66,25 @@ void launch_signal(uint32_t *const *flags, int n, uint32_t value, cudaStream_t s
 // ---------------------------------------------------------------------------
 constexpr int kBnThreads = 256;
 
+__global__ void bn_sums_kernel(const uint4 *__restrict__ t, long long npix, int cpad,
+                               double *__restrict__ partials);
+
+// One wave of resident blocks (never more blocks than the tensor has
+// 8-load batches): a function of (npix, cpad) only, so deterministic.
 int bn_partial_blocks(long long npix, int cpad) {
+    static int per_sm = -1;
+    if (per_sm < 0) {
+        int b = 0;  // dynamic smem = pix_lanes * 2 * cpad doubles = 32 KB for any cpad
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bn_sums_kernel, kBnThreads, 32 * 1024);
+        per_sm = std::max(1, std::min(b, 4));
+    }
     const int vecs = cpad / 8;
     const int pix_per_iter = std::max(1, kBnThreads / vecs);
     const long long iters = (npix + pix_per_iter - 1) / pix_per_iter;
-    return (int)std::max<long long>(1, std::min<long long>(iters / 8 + 1, 148 * 8));
+    return (int)std::max<long long>(1, std::min<long long>((iters + 7) / 8, 148LL * per_sm));
 }
 
-__global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t,
-                                                             long long npix, int cpad,
+__global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t, long long npix, int cpad,
                                                              double *__restrict__ partials) {
     // sh[pl][2][cpad]: per-pixel-lane partials, summed below in a fixed order
     // so the result does not depend on scheduling (deterministic).
@@ -142,20 +152,46 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
 
 // Fixed-order reduction of the per-block partials (deterministic).
 // One warp per output value: lane l sums the partials of blocks l, l+32, ...
-// (independent loads in flight), then a fixed xor-shuffle tree (deterministic).
-__global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks, int n2,
-                                 double *__restrict__ out) {
+// in that order, loading 8 of them at a time (independent loads in flight),
+// then a fixed xor-shuffle tree. With `mean` set, lane 0 of the warps of
+// channel i also finalises mean/var (the single-group case: no allreduce).
+__global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks, int cpad,
+                                 double *__restrict__ out, int c, double count,
+                                 double *__restrict__ mean, double *__restrict__ var) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= n2) return;
-    double acc = 0.0;
-    for (int b = lane; b < blocks; b += 32) acc += __ldg(&partials[(long long)b * n2 + warp]);
+    const int n2 = 2 * cpad;
+    if (warp >= cpad) return;
+    // warp w reduces sum (w) and sum of squares (cpad + w) of channel w
+    double acc[2] = {0.0, 0.0};
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) out[warp] = acc;
+    for (int k = 0; k < 2; ++k) {
+        const int col = warp + k * cpad;
+        int b = lane;
+        for (; b + 32 * 7 < blocks; b += 32 * 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldg(&partials[(long long)(b + 32 * u) * n2 + col]);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[k] += v[u];
+        }
+        for (; b < blocks; b += 32) acc[k] += __ldg(&partials[(long long)b * n2 + col]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+    }
+    if (lane == 0) {
+        out[warp] = acc[0];
+        out[cpad + warp] = acc[1];
+        if (mean && warp < c) {
+            const double mu = acc[0] / count;
+            const double v = acc[1] / count - mu * mu;
+            mean[warp] = mu;
+            var[warp] = v > 0.0 ? v : 0.0;
+        }
+    }
 }
 
 void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
-                    double *out, cudaStream_t st) {
+                    double *out, int c, double count, double *mean, double *var, cudaStream_t st) {
     DC_REQUIRE(cpad % 8 == 0 && cpad / 8 <= kBnThreads, DC_ERR_UNSUPPORTED,
                "BN stats: channels must be a multiple of 8 and <= 2048");
     const int blocks = bn_partial_blocks(npix, cpad);
@@ -164,7 +200,7 @@ void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *pa
         reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn sums launch: %s", cudaGetErrorString(e));
-    bn_reduce_kernel<<<(2 * cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, 2 * cpad, out);
+    bn_reduce_kernel<<<(cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, cpad, out, c, count, mean, var);
     e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
     g_launches += 2;

@@ -36,8 +36,10 @@ void launch_signal(uint32_t *const *flags, int n, uint32_t value, cudaStream_t s
 // partials must hold blocks * 2 * cpad doubles; out holds 2 * cpad doubles
 // (sums then sums of squares).
 int bn_partial_blocks(long long npix, int cpad);
+// Per-channel sum / sum of squares of an owned NHWC bf16 block into out[2][cpad]
+// (fp64, fixed order); with `mean` non-null also mean/var over `count` pixels.
 void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
-                    double *out, cudaStream_t st);
+                    double *out, int c, double count, double *mean, double *var, cudaStream_t st);
 // mean = s / count, var = ss / count - mean^2 (biased), first `c` channels.
 void launch_bn_finalize(const double *sums, int cpad, int c, double count, double *mean,
                         double *var, cudaStream_t st);

@@ -41,7 +41,10 @@ def main():
     flops = 2.0 * N * F * C * K * K * Ho * Wo
     ops = {"fwd": lambda: dc.dc_conv_fwd(plan, x, w, y, 0),
            "bpw": lambda: dc.dc_conv_bwd_filter(plan, x, dy, dw, 0),
-           "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0)}
+           "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0),
+           "bn": lambda: dc.dc_bn_spatial_stats(plan, y, mean, var, 1, 0)}
+    mean = torch.empty(F, dtype=torch.float64, device="cuda")
+    var = torch.empty(F, dtype=torch.float64, device="cuda")
     for name in a.ops.split(","):
         f = ops[name]
         for _ in range(a.warmup):
@@ -54,7 +57,10 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / a.iters
-        print(f"{name} {a.shape}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s", flush=True)
+        if name == "bn":
+            print(f"{name} {a.shape}: {us:8.1f} us  {y.numel() * 2 / us / 1e3:7.1f} GB/s", flush=True)
+        else:
+            print(f"{name} {a.shape}: {us:8.1f} us  {flops / us / 1e6:7.1f} TFLOP/s", flush=True)
     dc.dc_plan_destroy(plan)
 
 
