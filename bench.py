@@ -218,8 +218,9 @@ def main():
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--ar-sync", action="store_true", help="join each dW allreduce inside its layer's call")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
-                    help="replay the step as a CUDA graph (auto: unless the P2P halo runs)")
+                    help="replay the step as a CUDA graph")
     ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
     args = ap.parse_args()
     layers = WORKLOADS[args.workload]
@@ -251,7 +252,9 @@ def main():
     stream = torch.cuda.Stream()
     sp = stream.cuda_stream
     halo_flag = dc.DC_HALO_NCCL if args.halo == "nccl" else 0
-    FLAGS = dc.DC_EXCHANGE | dc.DC_ALLREDUCE | halo_flag
+    # dW allreduces are queued on the communicator's gradient stream and joined
+    # once at the end of the step (overlapped with later layers)
+    FLAGS = dc.DC_EXCHANGE | dc.DC_ALLREDUCE | halo_flag | (0 if args.ar_sync else dc.DC_ALLREDUCE_ASYNC)
 
     # ---- per-layer plans and resident inputs ----
     L = []
@@ -320,7 +323,9 @@ def main():
                 d["w"].copy_(d["host"]["w"], non_blocking=True)
             for _, f in op_calls(d):
                 f()
-            if e2e:
+        dc.dc_comm_sync(comm, sp)
+        if e2e:  # dW is final after the queued allreduces are joined
+            for d in L:
                 d["host"]["dw"].copy_(d["dw"], non_blocking=True)
 
     def barrier():
@@ -328,9 +333,9 @@ def main():
             dist.barrier()
 
     # CUDA graphs: the step's ~300 launches are recorded once and replayed, so
-    # small layers are not bound by host launch cost. The P2P halo protocol
-    # carries host-side epochs, so it runs eagerly.
-    use_graph = args.graph == "on" or (args.graph == "auto" and (world == 1 or args.halo == "nccl"))
+    # small layers are not bound by host launch cost (the P2P halo and BN
+    # protocols keep their epochs on the device, so replays stay in step).
+    use_graph = args.graph in ("on", "auto")
 
     def capture(fn):
         g = torch.cuda.CUDAGraph()
@@ -344,7 +349,8 @@ def main():
         torch.cuda.synchronize()
         if use_graph:
             g_step, g_e2e = capture(step), capture(lambda: step(e2e=True))
-            g_ops = [[(name, capture(f)) for name, f in op_calls(d)] for d in L]
+            g_ops = [[(name, capture(lambda f=f: (f(), dc.dc_comm_sync(comm, sp)))) for name, f in op_calls(d)]
+                     for d in L]
             run_step, run_e2e = g_step.replay, g_e2e.replay
             for _ in range(2):
                 run_step()
@@ -391,7 +397,11 @@ def main():
                 ops = g_ops[i] if g_ops else op_calls(d)
                 ev[k][i][0].record(stream)
                 for j, (name, f) in enumerate(ops):
-                    (f.replay if g_ops else f)()
+                    if g_ops:
+                        f.replay()
+                    else:
+                        f()
+                        dc.dc_comm_sync(comm, sp)
                     ev[k][i][j + 1].record(stream)
                 for j in range(len(ops) + 1, 5):
                     ev[k][i][j].record(stream)
@@ -465,7 +475,7 @@ def main():
                                   for d, f_ms, w_ms, x_ms in per],
                        "parallelism": "per-layer model-chosen (pN,pH,pW)" if args.decomp == "auto" else args.decomp,
                        "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
-                       "cuda_graph": use_graph,
+                       "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",
                        "per_layer_times": "instrumented pass after the timed region (events between ops)",
                        "flops_per_step": flops_step},
             "roofline": roof,

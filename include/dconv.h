@@ -79,6 +79,10 @@ typedef struct dc_plan_s *dc_plan_t;
                                   call, overlapped with the interior tiles  */
 #define DC_ALLREDUCE     0x2u  /* conv_bwd_filter: sum dW over all ranks    */
 #define DC_HALO_NCCL     0x4u  /* use grouped ncclSend/ncclRecv instead of direct P2P       */
+#define DC_ALLREDUCE_ASYNC 0x8u /* with DC_ALLREDUCE: queue the dW allreduce on the
+                                  communicator's gradient stream instead of joining it
+                                  into the call (overlaps the later layers' work,
+                                  PAPER.md:204, 214); dW is final after dc_comm_sync */
 #define DC_DEFAULT_FLAGS (DC_EXCHANGE | DC_ALLREDUCE)
 
 /* COLLECTIVE. Create the communicator of `world` ranks. nccl_uid128 points to
@@ -91,6 +95,10 @@ dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cud
 /* Write a fresh 128-byte ncclUniqueId to uid128 (rank 0 only). */
 dc_status_t dc_comm_unique_id(void *uid128);
 dc_status_t dc_comm_destroy(dc_comm_t comm);
+/* Make `stream` wait for every dW allreduce queued with DC_ALLREDUCE_ASYNC on
+ * this communicator so far (an event wait: does not block the host; may be
+ * recorded into a CUDA graph). world == 1: no-op. */
+dc_status_t dc_comm_sync(dc_comm_t comm, void *stream);
 
 /* COLLECTIVE. Plan one convolution layer: global N, C, H, W, F, odd K,
  * stride in {1, 2}, pad 0 <= P <= K/2, grid `decomp` (product == world, or

@@ -20,12 +20,12 @@ STATUS_NAMES = ["DC_OK", "DC_ERR_ARG", "DC_ERR_SHAPE", "DC_ERR_PARTITION", "DC_E
                 "DC_ERR_CUDA", "DC_ERR_COMM", "DC_ERR_OOM"]
 DC_BF16, DC_FP32_3XTF32 = 0, 1
 DC_X, DC_Y, DC_DY, DC_DX, DC_W, DC_DW = range(6)
-DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL = 0x1, 0x2, 0x4
+DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC = 0x1, 0x2, 0x4, 0x8
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "dc_comm_create", "dc_comm_unique_id", "dc_comm_destroy", "dc_plan_create",
+    "dc_comm_create", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
         "dc_comm_create": [i32, i32, vp, i32, P(vp)],
         "dc_comm_unique_id": [vp],
         "dc_comm_destroy": [vp],
+        "dc_comm_sync": [vp, vp],
         "dc_plan_create": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, vp, P(vp)],
         "dc_plan_create_virtual": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, i32, P(vp)],
         "dc_plan_halo_msgs": [vp, i32, P(dc_halo_msg_t), P(i32)],
@@ -146,6 +147,11 @@ def dc_comm_create(rank: int, world: int, uid: bytes | None, device: int) -> int
 
 def dc_comm_destroy(comm: int):
     _check(lib().dc_comm_destroy(comm))
+
+
+def dc_comm_sync(comm: int, stream=None):
+    """Make `stream` wait for the dW allreduces queued with DC_ALLREDUCE_ASYNC."""
+    _check(lib().dc_comm_sync(comm, _stream(stream)))
 
 
 def dc_plan_create(N, C, H, W, F, K, stride, pad, decomp=(0, 0, 0), dtype=DC_BF16, comm=None) -> int:

@@ -54,33 +54,26 @@ using namespace dc;
 struct dc_comm_s {
     int rank = 0, world = 1, device = 0;
     ncclComm_t nccl = nullptr;
+    // dW allreduces queued with DC_ALLREDUCE_ASYNC: their own communicator
+    // (so they never serialise behind / ahead of halo or BN traffic) and stream
+    ncclComm_t grad_nccl = nullptr;
+    cudaStream_t s_grad = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    // P2P BN statistics mailbox (halo.cuh: BnP2P): [flags (256 B)][2][world][slot]
+    uint8_t *bn_mail = nullptr;
+    std::vector<uint8_t *> bn_peer_mail;  // every rank's mailbox, mapped (mine for me)
+    uint32_t *bn_epoch = nullptr;
+    bool bn_p2p = false;
 };
 
 namespace {
-
-// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda).
-typedef CUresult (*PFN_wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-PFN_wait32 get_wait32() {
-    static PFN_wait32 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void *p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPointByVersion("cuStreamWaitValue32", &p, 12000, cudaEnableDefault,
-                                             &q) == cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_wait32>(p);
-    });
-    DC_REQUIRE(fn != nullptr, DC_ERR_CUDA, "cuStreamWaitValue32 unavailable");
-    return fn;
-}
 
 struct BufState {  // a margined buffer (X or DY) known to the plan
     void *ptr = nullptr;
     size_t bytes = 0;
     bool owned = false;
     std::map<int, void *> peer;  // peer rank -> that rank's buffer mapped here
-    uint32_t epoch = 0;
+    uint32_t *dev_epoch = nullptr;  // P2P protocol epoch {epoch, blocks done} (device)
     void *stage = nullptr;       // NCCL baseline staging: [send | recv]
     size_t stage_bytes = 0;
 };
@@ -101,7 +94,7 @@ struct dc_plan_s {
     BufState buf[2];                 // 0: X, 1: DY
     uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
     std::map<int, uint32_t *> peer_flags;
-    bool can_flush = false;
+    uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local)
     __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases
     size_t wt_bytes = 0;
     float *ws = nullptr;             // split-K workspace (backward-filter)
@@ -121,6 +114,7 @@ struct dc_plan_s {
         }
         for (auto &kv : peer_flags) cudaIpcCloseMemHandle(kv.second);
         if (flags) cudaFree(flags);
+        if (dev_epochs) cudaFree(dev_epochs);
         if (wt) cudaFree(wt);
         if (ws) cudaFree(ws);
         if (ws2) cudaFree(ws2);
@@ -556,11 +550,11 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
     // ---- direct P2P stores into the neighbours' margins + epoch flags ----
     // one kernel: ready handshake, NVLink stores, per-block completion counters
     // (halo.cu: p2p_exchange_kernel); then a stream wait on my own counters.
-    const uint32_t e = ++B.epoch;
     const int me = rp.rank;
     DC_REQUIRE(sends.size() <= 8 && recvs.size() <= 8, DC_ERR_ARG, "too many halo neighbours");
+    DC_REQUIRE(B.dev_epoch != nullptr, DC_ERR_ARG, "P2P halo exchange: buffer not registered");
     P2PExchange x{};
-    x.epoch = e;
+    x.epoch_ctr = B.dev_epoch;
     for (auto &m : recvs) x.ready_out[x.n_ready_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me);
     for (auto &m : sends) {
         x.ready_in[x.n_ready_in++] = pl->flag(pl->flags, which, FLAG_READY, m.peer);
@@ -573,16 +567,7 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
         c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
     }
     for (auto &m : recvs) x.data_in[x.n_data_in++] = pl->flag(pl->flags, which, FLAG_DATA, m.peer);
-    static const bool stream_wait = std::getenv("DC_P2P_STREAM_WAIT") != nullptr;
-    x.wait_in_kernel = stream_wait ? 0 : 1;
     launch_p2p_exchange(x, st);
-    if (x.wait_in_kernel) return;
-    const unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (pl->can_flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
-    for (auto &m : recvs) {
-        CUresult r = get_wait32()((CUstream)st, (CUdeviceptr)pl->flag(pl->flags, which, FLAG_DATA, m.peer),
-                                  (cuuint32_t)(kP2PBlocks * e), wflags);
-        DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-    }
 }
 
 // All-gather fixed-size blobs over NCCL (host in/out); used for IPC handles.
@@ -893,7 +878,7 @@ void signal_ready_next(dc_plan_s *pl, int which, const void *buf, cudaStream_t s
     if (recvs.empty()) return;
     std::vector<uint32_t *> fl;
     for (auto &m : recvs) fl.push_back(pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, pl->rp.rank));
-    launch_signal(fl.data(), (int)fl.size(), B.epoch + 1, st);
+    launch_signal(fl.data(), (int)fl.size(), 0, B.dev_epoch, st);
 }
 
 void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
@@ -903,17 +888,26 @@ void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
     NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, pl->nccl(), st));
 }
 
+// DC_ALLREDUCE_ASYNC: the allreduce waits for the work queued on `st` so far
+// (the filter gradient) and runs on the communicator's gradient stream; `st`
+// does not wait for it (dc_comm_sync joins).
+void allreduce_dw_async(dc_plan_s *pl, float *dw, cudaStream_t st) {
+    if (pl->world() <= 1) return;
+    dc_comm_s *c = pl->comm;
+    DC_REQUIRE(c && c->grad_nccl, DC_ERR_ARG, "allreduce needs a communicator");
+    const ConvGeom &g = pl->rp.g;
+    CK(cudaEventRecord(c->ev_in, st));
+    CK(cudaStreamWaitEvent(c->s_grad, c->ev_in, 0));
+    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
+}
+
 // Streams, events and small scratch of this rank (created lazily for virtual
 // plans, which may compute when no exchange / allreduce is requested).
 void ensure_local_resources(dc_plan_s *pl) {
     if (pl->s_comm) return;
     CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
     for (auto &e : pl->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 2 * pl->rp.g.Fp));
-    int dev = 0, flush = 0;
-    CK(cudaGetDevice(&dev));
-    cudaDeviceGetAttribute(&flush, cudaDevAttrCanFlushRemoteWrites, dev);
-    pl->can_flush = flush != 0;
+    CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 4 * pl->rp.g.Fp));  // local sums, global sums
 }
 
 dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, bool is_virtual) {
@@ -938,6 +932,10 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
                 const size_t fb = sizeof(uint32_t) * 4 * grid.size();
                 CK(cudaMalloc(&pl->flags, fb));
                 CK(cudaMemset(pl->flags, 0, fb));
+                CK(cudaMalloc(&pl->dev_epochs, sizeof(uint32_t) * 4));
+                CK(cudaMemset(pl->dev_epochs, 0, sizeof(uint32_t) * 4));
+                pl->buf[0].dev_epoch = pl->dev_epochs;
+                pl->buf[1].dev_epoch = pl->dev_epochs + 2;
                 cudaIpcMemHandle_t h;
                 CK(cudaIpcGetMemHandle(&h, pl->flags));
                 auto all = allgather_bytes(pl, &h, sizeof h);
@@ -981,6 +979,42 @@ dc_status_t dc_comm_unique_id(void *uid128) {
     DC_API_END
 }
 
+// Mailbox for the P2P BN allreduce: allocated here, its IPC handle all-gathered
+// over NCCL, every peer's opened (one node, <= 8 ranks with peer access;
+// otherwise the BN allreduce stays on NCCL).
+void setup_bn_mailbox(dc_comm_s *c) {
+    if (c->world > kMaxBnGroup || std::getenv("DC_BN_NCCL")) return;
+    const size_t bytes = 256 + (size_t)2 * c->world * kBnMaxDoubles * sizeof(double);
+    CK(cudaMalloc(&c->bn_mail, bytes));
+    CK(cudaMemset(c->bn_mail, 0, bytes));
+    CK(cudaMalloc(&c->bn_epoch, sizeof(uint32_t)));
+    CK(cudaMemset(c->bn_epoch, 0, sizeof(uint32_t)));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, c->bn_mail));
+    cudaStream_t s;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint8_t *d = nullptr;
+    CK(cudaMalloc(&d, sizeof h * (c->world + 1)));
+    CK(cudaMemcpy(d + sizeof h * c->world, &h, sizeof h, cudaMemcpyHostToDevice));
+    NK(ncclAllGather(d + sizeof h * c->world, d, sizeof h, ncclUint8, c->nccl, s));
+    CK(cudaStreamSynchronize(s));
+    std::vector<cudaIpcMemHandle_t> all(c->world);
+    CK(cudaMemcpy(all.data(), d, sizeof h * c->world, cudaMemcpyDeviceToHost));
+    CK(cudaFree(d));
+    CK(cudaStreamDestroy(s));
+    c->bn_peer_mail.assign(c->world, nullptr);
+    for (int r = 0; r < c->world; ++r) {
+        if (r == c->rank) {
+            c->bn_peer_mail[r] = c->bn_mail;
+            continue;
+        }
+        void *ptr = nullptr;
+        CK(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
+        c->bn_peer_mail[r] = reinterpret_cast<uint8_t *>(ptr);
+    }
+    c->bn_p2p = true;
+}
+
 dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, dc_comm_t *out) {
     DC_API_BEGIN
     DC_REQUIRE(out != nullptr && world >= 1 && rank >= 0 && rank < world, DC_ERR_ARG,
@@ -997,6 +1031,11 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
             delete c;
             fail(DC_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
         }
+        NK(ncclCommSplit(c->nccl, 0, rank, &c->grad_nccl, nullptr));
+        setup_bn_mailbox(c);
+        CK(cudaStreamCreateWithFlags(&c->s_grad, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
     }
     *out = c;
     DC_API_END
@@ -1005,8 +1044,28 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
 dc_status_t dc_comm_destroy(dc_comm_t c) {
     DC_API_BEGIN
     if (c) {
+        if (c->s_grad) cudaStreamSynchronize(c->s_grad);
+        cudaDeviceSynchronize();
+        for (int r = 0; r < (int)c->bn_peer_mail.size(); ++r)
+            if (r != c->rank && c->bn_peer_mail[r]) cudaIpcCloseMemHandle(c->bn_peer_mail[r]);
+        if (c->bn_mail) cudaFree(c->bn_mail);
+        if (c->bn_epoch) cudaFree(c->bn_epoch);
+        if (c->grad_nccl) ncclCommDestroy(c->grad_nccl);
         if (c->nccl) ncclCommDestroy(c->nccl);
+        if (c->s_grad) cudaStreamDestroy(c->s_grad);
+        if (c->ev_in) cudaEventDestroy(c->ev_in);
+        if (c->ev_out) cudaEventDestroy(c->ev_out);
         delete c;
+    }
+    DC_API_END
+}
+
+dc_status_t dc_comm_sync(dc_comm_t c, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(c != nullptr, DC_ERR_ARG, "null communicator");
+    if (c->s_grad) {
+        CK(cudaEventRecord(c->ev_out, c->s_grad));
+        CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_out, 0));
     }
     DC_API_END
 }
@@ -1171,7 +1230,8 @@ dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, floa
     cudaStream_t st = (cudaStream_t)stream;
     run_bwd_filter(pl, x, dy, dw, st);
     signal_ready_next(pl, 0, x, st);
-    if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
+    if ((flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC)) allreduce_dw_async(pl, dw, st);
+    else if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
     DC_API_END
 }
 
@@ -1182,7 +1242,8 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
     const bool halo = (flags & DC_EXCHANGE) && (!pl->rp.dy_send.empty() || !pl->rp.dy_recv.empty());
-    const bool ar = (flags & DC_ALLREDUCE) && pl->world() > 1;
+    const bool ar_async = (flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC) && pl->world() > 1;
+    const bool ar = (flags & DC_ALLREDUCE) && pl->world() > 1 && !ar_async;
     if (halo) {  // dy halo on the comm stream, concurrent with the filter gradient
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
@@ -1191,6 +1252,7 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
     }
     run_bwd_filter(pl, x, dy, dw, st);
     signal_ready_next(pl, 0, x, st);
+    if (ar_async) allreduce_dw_async(pl, dw, st);
     if (ar) {  // dW allreduce on the comm stream, concurrent with the data gradient
         CK(cudaEventRecord(pl->ev[2], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[2], 0));
@@ -1219,7 +1281,28 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     // single group: the reduce kernel also finalises mean/var (no allreduce between)
     launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
                    (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
-    if (global) {
+    if (global && pl->comm && pl->comm->bn_p2p) {
+        // one-shot NVLink allreduce among the ranks with this rank's i_N
+        dc_comm_s *c = pl->comm;
+        BnP2P b{};
+        b.gsize = pl->bn_group;
+        const int lo = rp.in * pl->bn_group;
+        for (int k = 0; k < b.gsize; ++k) {
+            b.ranks[k] = lo + k;
+            b.peer_box[k] = reinterpret_cast<double *>(c->bn_peer_mail[lo + k] + 256);
+            b.peer_flags[k] = reinterpret_cast<uint32_t *>(c->bn_peer_mail[lo + k]);
+        }
+        b.my_box = reinterpret_cast<const double *>(c->bn_mail + 256);
+        b.my_flags = reinterpret_cast<const uint32_t *>(c->bn_mail);
+        b.my_rank = c->rank, b.world = c->world;
+        b.epoch = c->bn_epoch;
+        b.local = pl->bn_sums;
+        b.cpad = (int)g.Fp, b.c = (int)g.F;
+        b.count = (double)rp.nrange.size() * g.Ho * g.Wo;
+        b.sums = pl->bn_sums + 2 * g.Fp;
+        b.mean = mean, b.var = var;
+        launch_bn_allreduce_p2p(b, st);
+    } else if (global) {
         DC_REQUIRE(pl->bn_comm != nullptr, DC_ERR_ARG, "spatial BN statistics need a communicator");
         NK(ncclAllReduce(pl->bn_sums, pl->bn_sums, 2 * g.Fp, ncclFloat64, ncclSum, pl->bn_comm, st));
         launch_bn_finalize(pl->bn_sums, (int)g.Fp, (int)g.F, (double)rp.nrange.size() * g.Ho * g.Wo, mean,

@@ -43,18 +43,19 @@ struct FlagList {
     uint32_t *f[16];
 };
 
-__global__ void signal_kernel(FlagList fl, int n, uint32_t value) {
+__global__ void signal_kernel(FlagList fl, int n, uint32_t value, const uint32_t *epoch_src) {
+    if (epoch_src) value = *reinterpret_cast<const volatile uint32_t *>(epoch_src) + 1;
     __threadfence_system();
     for (int i = threadIdx.x; i < n; i += blockDim.x)
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl.f[i]), "r"(value) : "memory");
 }
 
-void launch_signal(uint32_t *const *flags, int n, uint32_t value, cudaStream_t st) {
+void launch_signal(uint32_t *const *flags, int n, uint32_t value, const uint32_t *epoch_src, cudaStream_t st) {
     if (n == 0) return;
     DC_REQUIRE(n <= 16, DC_ERR_ARG, "too many flags");
     FlagList fl{};
     for (int i = 0; i < n; ++i) fl.f[i] = flags[i];
-    signal_kernel<<<1, 32, 0, st>>>(fl, n, value);
+    signal_kernel<<<1, 32, 0, st>>>(fl, n, value, epoch_src);
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "signal launch: %s", cudaGetErrorString(e));
     ++g_launches;
@@ -229,7 +230,7 @@ void launch_bn_finalize(const double *sums, int cpad, int c, double count, doubl
 namespace dc {
 
 __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant__ P2PExchange x) {
-    const uint32_t e = x.epoch;
+    const uint32_t e = *reinterpret_cast<volatile uint32_t *>(x.epoch_ctr) + 1;
     if (blockIdx.x == 0 && (int)threadIdx.x < x.n_ready_out) {
         __threadfence_system();
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[threadIdx.x]), "r"(e) : "memory");
@@ -258,13 +259,19 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
         __threadfence_system();
         atomicAdd_system(x.data_out[threadIdx.x], 1u);
     }
-    if (x.wait_in_kernel && blockIdx.x == 0 && (int)threadIdx.x < x.n_data_in) {
+    // block 0 returns only when every sender's blocks have delivered epoch e
+    if (blockIdx.x == 0 && (int)threadIdx.x < x.n_data_in) {
         const uint32_t target = kP2PBlocks * e;
         uint32_t v;
         do {
             asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.data_in[threadIdx.x]) : "memory");
         } while ((int)(v - target) < 0);
         __threadfence_system();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t prev = atomicAdd(x.epoch_ctr + 1, 1u);
+        if (prev == kP2PBlocks * e - 1) *reinterpret_cast<volatile uint32_t *>(x.epoch_ctr) = e;
     }
 }
 
@@ -275,4 +282,55 @@ void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st) {
     ++g_launches;
 }
 
+__global__ void __launch_bounds__(256) bn_allreduce_p2p_kernel(const __grid_constant__ BnP2P b) {
+    const uint32_t e = *reinterpret_cast<volatile uint32_t *>(b.epoch) + 1;
+    const int par = e & 1;
+    const int n2 = 2 * b.cpad;
+    const long long slot = (long long)kBnMaxDoubles;
+    const long long par_stride = (long long)b.world * slot;
+    // 1. my sums into slot [par][my_rank] of every member (me included)
+    for (int k = 0; k < b.gsize; ++k) {
+        double *dst = b.peer_box[k] + par * par_stride + b.my_rank * slot;
+        for (int i = threadIdx.x; i < n2; i += blockDim.x) dst[i] = b.local[i];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if ((int)threadIdx.x < b.gsize)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b.peer_flags[threadIdx.x] + b.my_rank), "r"(e)
+                     : "memory");
+    // 2. wait until every member has delivered epoch e
+    if ((int)threadIdx.x < b.gsize) {
+        const uint32_t *f = b.my_flags + b.ranks[threadIdx.x];
+        uint32_t v;
+        do {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while ((int)(v - e) < 0);
+    }
+    __syncthreads();
+    // 3. fixed-order sum over the members (uncached loads: peers wrote them)
+    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        double acc = 0.0;
+        for (int k = 0; k < b.gsize; ++k) acc += __ldcv(b.my_box + par * par_stride + b.ranks[k] * slot + i);
+        b.sums[i] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < b.c; i += blockDim.x) {
+        const double mu = b.sums[i] / b.count;
+        const double v = b.sums[b.cpad + i] / b.count - mu * mu;
+        b.mean[i] = mu;
+        b.var[i] = v > 0.0 ? v : 0.0;
+    }
+    if (threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(b.epoch) = e;
+}
+
+void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st) {
+    DC_REQUIRE(2 * b.cpad <= kBnMaxDoubles && b.gsize <= kMaxBnGroup, DC_ERR_UNSUPPORTED,
+               "P2P BN allreduce: too many channels or members");
+    bn_allreduce_p2p_kernel<<<1, 256, 0, st>>>(b);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn p2p launch: %s", cudaGetErrorString(e));
+    ++g_launches;
+}
+
 }  // namespace dc
+

@@ -29,7 +29,8 @@ void launch_block_copies(const CopyBatch &b, cudaStream_t st);
 
 // Stores `value` to each of `n` flags (possibly peer-mapped) with release
 // semantics at system scope, after a system-scope fence.
-void launch_signal(uint32_t *const *flags, int n, uint32_t value, cudaStream_t st);
+// value = *epoch_src + 1 when epoch_src is set (device epoch, graph-replayable)
+void launch_signal(uint32_t *const *flags, int n, uint32_t value, const uint32_t *epoch_src, cudaStream_t st);
 
 // BN statistics of a dense NHWC bf16 tensor [npix][cpad]: per-channel fp64
 // sum and sum of squares over all pixels (deterministic two-stage reduce).
@@ -65,9 +66,40 @@ struct P2PExchange {
     uint32_t *data_out[8];   // peers' data counters for me (I am their sender)
     uint32_t *data_in[8];    // my counters written by the peers that send to me
     int n_ready_out, n_ready_in, n_data_out, n_data_in;
-    int wait_in_kernel;      // block 0 polls data_in >= kP2PBlocks*epoch before exiting
-    uint32_t epoch;
+    // device epoch of this (plan, buffer): {epoch, blocks done}. Every block
+    // reads epoch + 1 at start; the last block to finish publishes it (so the
+    // launch can be replayed from a CUDA graph)
+    uint32_t *epoch_ctr;
 };
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);
+
+// ---------------------------------------------------------------------------
+// Spatial BN statistics allreduce over NVLink (one kernel, one block): every
+// group member stores its 2*cpad fp64 sums into slot [parity][its rank] of
+// every member's mailbox (peer memory mapped through CUDA IPC), raises its
+// flag to the epoch, waits for all members' flags, and sums the slots in rank
+// order (deterministic, identical on every member). The epoch lives on the
+// device (read at start, published at the end) so the kernel can be replayed
+// from a CUDA graph. Mailbox data alternates parity per epoch: a member can
+// be at most one epoch ahead of any other (it needs everyone's flag to finish).
+// ---------------------------------------------------------------------------
+constexpr int kMaxBnGroup = 8;
+constexpr int kBnMaxDoubles = 2 * 2048;  // per slot: sums then sums of squares, cpad <= 2048
+
+struct BnP2P {
+    double *peer_box[kMaxBnGroup];    // member k's mailbox base (mapped)
+    uint32_t *peer_flags[kMaxBnGroup];  // member k's flag array base (mapped)
+    const double *my_box;             // my mailbox base
+    const uint32_t *my_flags;         // my flag array base
+    int ranks[kMaxBnGroup];           // global rank of member k (slot / flag index)
+    int gsize, my_rank, world;
+    uint32_t *epoch;                  // device epoch counter (this communicator)
+    const double *local;              // my 2 * cpad sums
+    int cpad, c;
+    double count;
+    double *sums;                     // out: global sums [2 * cpad]
+    double *mean, *var;               // out: first c channels
+};
+void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st);
 
 }  // namespace dc

@@ -113,6 +113,48 @@ def _worker(rank, world, port, errq):
             if grid[0] == 1:  # group = all ranks = the whole batch
                 assert (mean - mean_r).abs().max().item() <= 1e-9, f"{tag}: BN mean"
                 assert (var - var_r).abs().max().item() <= 1e-9, f"{tag}: BN var"
+            # (5) repeated BN calls cycle the P2P mailbox parities; results identical
+            for _ in range(3):
+                m2, v2 = torch.zeros_like(mean), torch.zeros_like(var)
+                dc.dc_bn_spatial_stats(plan, y, m2, v2, False)
+                torch.cuda.synchronize()
+                assert torch.equal(m2, mean) and torch.equal(v2, var), f"{tag}: repeated BN differs"
+            # (6) dW allreduce queued on the gradient stream, joined by dc_comm_sync
+            dw2 = torch.empty_like(dw)
+            dist.barrier()
+            dc.dc_conv_bwd(plan, xb.data_ptr(), dyb.data_ptr(), wb, dx, dw2,
+                           dc.DC_DEFAULT_FLAGS | dc.DC_ALLREDUCE_ASYNC)
+            dc.dc_comm_sync(comm)
+            torch.cuda.synchronize()
+            e = rel_max(dw_to_fckk(dw2, C), dw_to_fckk(DW, C))
+            assert e <= 1e-4, f"{tag}: async dW rel err {e}"
+            assert torch.equal(dx, dxs), f"{tag}: dx (async allreduce) not bitwise equal to 1-GPU"
+            # (7) the P2P protocol replayed from CUDA graphs (device-side epochs)
+            s = torch.cuda.Stream()
+            y2 = torch.empty_like(y)
+            torch.cuda.synchronize()
+            dist.barrier()
+            with torch.cuda.stream(s):
+                g_ex, g_fwd = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g_ex, stream=s):
+                    dc.dc_halo_exchange(plan, dc.DC_X, xb, 0)
+                with torch.cuda.graph(g_fwd, stream=s):
+                    dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y2, dc.DC_EXCHANGE)
+                for rep in range(3):
+                    xb.copy_(fill_owned_only(x, xd))
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    g_ex.replay()
+                    torch.cuda.synchronize()
+                    assert torch.equal(xb, full_x), f"{tag}: graph replay {rep}: x halo not bit-exact"
+                    xb.copy_(fill_owned_only(x, xd))
+                    y2.zero_()
+                    torch.cuda.synchronize()
+                    dist.barrier()
+                    g_fwd.replay()
+                    torch.cuda.synchronize()
+                    assert torch.equal(y2, ys), f"{tag}: graph replay {rep}: y not bitwise equal"
+            dist.barrier()
             dc.dc_plan_destroy(plan)
             dc.dc_plan_destroy(ref)
         dc.dc_comm_destroy(comm)
