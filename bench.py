@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--ablate", default="", help="DIAGNOSTIC: comma list of exchange,bn,allreduce to skip")
     ap.add_argument("--ar-sync", action="store_true", help="join each dW allreduce inside its layer's call")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph")
@@ -255,6 +256,11 @@ def main():
     # dW allreduces are queued on the communicator's gradient stream and joined
     # once at the end of the step (overlapped with later layers)
     FLAGS = dc.DC_EXCHANGE | dc.DC_ALLREDUCE | halo_flag | (0 if args.ar_sync else dc.DC_ALLREDUCE_ASYNC)
+    ablate = set(a for a in args.ablate.split(",") if a)  # diagnostics only: the JSON says so
+    if "exchange" in ablate:
+        FLAGS &= ~dc.DC_EXCHANGE
+    if "allreduce" in ablate:
+        FLAGS &= ~dc.DC_ALLREDUCE
 
     # ---- per-layer plans and resident inputs ----
     L = []
@@ -300,6 +306,8 @@ def main():
         ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)),
                # spatially aggregated BN statistics of the layer output
                ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp))]
+        if "bn" in ablate:
+            ops.pop()
         if world == 1:
             # no halo / allreduce at one rank: the two backward kernels are
             # called separately so each gets its own timing
@@ -460,6 +468,7 @@ def main():
             cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": oracle.num_threads(), "kind": "oracle",
                    "sample": desc}
         out = {
+            **({"DIAGNOSTIC_ablated": sorted(ablate)} if ablate else {}),
             "metric": "conv fwd+bwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
@@ -493,6 +502,12 @@ def main():
                 xd = d["xd"]
                 for op, t in (("fp", f_ms), ("bpw", w_ms), ("bpx", x_ms)):
                     f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{t / 1e3}\n")
+    # graphs hold NCCL persistent resources: release them before the communicator
+    del run_step, run_e2e
+    g_step = g_e2e = g_ops = ops = f = None
+    import gc
+    gc.collect()
+    torch.cuda.synchronize()
     for d in L:
         dc.dc_plan_destroy(d["plan"])
     dc.dc_comm_destroy(comm)

@@ -96,8 +96,9 @@ dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cud
 dc_status_t dc_comm_unique_id(void *uid128);
 dc_status_t dc_comm_destroy(dc_comm_t comm);
 /* Make `stream` wait for every dW allreduce queued with DC_ALLREDUCE_ASYNC on
- * this communicator so far (an event wait: does not block the host; may be
- * recorded into a CUDA graph). world == 1: no-op. */
+ * this communicator since the previous dc_comm_sync (an event wait: does not
+ * block the host; may be recorded into a CUDA graph, in the same capture as
+ * the queuing calls). Nothing queued, or world == 1: no-op. */
 dc_status_t dc_comm_sync(dc_comm_t comm, void *stream);
 
 /* COLLECTIVE. Plan one convolution layer: global N, C, H, W, F, odd K,

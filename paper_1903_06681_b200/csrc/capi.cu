@@ -59,6 +59,7 @@ struct dc_comm_s {
     ncclComm_t grad_nccl = nullptr;
     cudaStream_t s_grad = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    bool grad_pending = false;  // allreduces queued since the last dc_comm_sync
     // P2P BN statistics mailbox (halo.cuh: BnP2P): [flags (256 B)][2][world][slot]
     uint8_t *bn_mail = nullptr;
     std::vector<uint8_t *> bn_peer_mail;  // every rank's mailbox, mapped (mine for me)
@@ -400,10 +401,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     std::memcpy(q.tap_h, L.p.tap_h, sizeof q.tap_h);
     std::memcpy(q.tap_w, L.p.tap_w, sizeof q.tap_w);
     q.cin_p = (int)cin_p;
-    q.bn = L.p.bn;
-    q.nout_tiles = (int)ceil_div(L.p.nout_p, q.bn);
     q.ksplit = L.ksplit;
-    q.work_hint = (int)std::min<int64_t>(L.work_hint * L.ksplit, 1 << 30);
     q.ws = L.ws;
     q.ws_h = L.ws_h;
     q.ws_w = L.ws_w;
@@ -413,9 +411,30 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.out_sn = L.p.out_sn, q.out_sh = L.p.out_sh, q.out_sw = L.p.out_sw;
     q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
     q.nout_p = L.p.nout_p;
+    const int TW = 1 << twl, TH = 128 >> twl;
+    // (1) choices that change the summation order (channel-stage width) come
+    // from the GLOBAL layer, so every partition computes the 1-GPU bits
+    {
+        ConvV2Params probe = q;
+        probe.bn = L.p.bn;
+        probe.nout_tiles = (int)ceil_div(L.p.nout_p, probe.bn);
+        probe.work_hint = (int)std::min<int64_t>(L.work_hint * L.ksplit, 1 << 30);
+        probe.allow_cg32 = 1;
+        if (!conv_v2_configure(probe, kV2SmemLimit)) return false;
+        q.cg = probe.cg;
+        q.allow_cg32 = 0;
+    }
+    // (2) bitwise-neutral choices from THIS launch's work: no tile pairing
+    // when the shard is too small to fill the GPU. (A narrower N tile for small
+    // shards was measured slower: every N tile reloads the whole input tile.)
+    int64_t local_tiles = 0;
+    for (auto &r : rects) local_tiles += ceil_div(r.nh, TH) * ceil_div(r.nw, TW);
+    local_tiles *= nsamples;
+    q.bn = L.p.bn;
+    q.nout_tiles = (int)ceil_div(L.p.nout_p, q.bn);
+    q.work_hint = (int)std::min<int64_t>(local_tiles * q.nout_tiles * L.ksplit, 1 << 30);
     if (!conv_v2_configure(q, kV2SmemLimit)) return false;
     DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
-    const int TW = 1 << twl, TH = 128 >> twl;
     q.nrect = (int)rects.size();
     q.rect_start[0] = 0;
     for (int r = 0; r < q.nrect; ++r) {
@@ -437,9 +456,11 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
         const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
         make_tmap(&amap, in_base, 4, dims, strides, box, es, 0);
     }
-    if (q.cg != L.p.bkc) {  // the kernel chose narrower channel stages: re-tile the weights
+    if (q.cg != L.p.bkc || q.bn != L.p.bn || q.cluster > 1) {
+        // narrower channel stages, or half-height boxes (each CTA of a pair
+        // loads half of every weight stage): re-tile the weights
         CUtensorMap bmap;
-        weight_map(&bmap, L.w_base, L.w_rows, L.w_kcols, q.cg, q.bn);
+        weight_map(&bmap, L.w_base, L.w_rows, L.w_kcols, q.cg, q.bn / q.cluster);
         launch_conv_v2(amap, bmap, q, st);
     } else {
         launch_conv_v2(amap, L.bmap, q, st);
@@ -899,6 +920,7 @@ void allreduce_dw_async(dc_plan_s *pl, float *dw, cudaStream_t st) {
     CK(cudaEventRecord(c->ev_in, st));
     CK(cudaStreamWaitEvent(c->s_grad, c->ev_in, 0));
     NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
+    c->grad_pending = true;
 }
 
 // Streams, events and small scratch of this rank (created lazily for virtual
@@ -1063,9 +1085,10 @@ dc_status_t dc_comm_destroy(dc_comm_t c) {
 dc_status_t dc_comm_sync(dc_comm_t c, void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(c != nullptr, DC_ERR_ARG, "null communicator");
-    if (c->s_grad) {
+    if (c->s_grad && c->grad_pending) {  // (nothing queued: no-op, also inside a graph capture)
         CK(cudaEventRecord(c->ev_out, c->s_grad));
         CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_out, 0));
+        c->grad_pending = false;
     }
     DC_API_END
 }

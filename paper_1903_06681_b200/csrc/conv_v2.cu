@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "common.hpp"
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(192, 1)
         }
         for (int s = 0; s < p.b_stages; ++s) {
             mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], 1);
+            mbar_init(&b_empty[s], p.cluster);  // released by the MMAs of every CTA that reads it
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
@@ -166,13 +167,35 @@ __global__ void __launch_bounds__(192, 1)
     }
     if (warp == 1) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
-    __syncthreads();
+    if (p.cluster > 1)
+        cluster_sync();  // the partner's barriers exist before any multicast reaches them
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const int total = p.total_tiles;
+    // Work units: a CTA (cluster == 1) or a CTA pair (cluster == 2: tiles 2k and
+    // 2k+1 of the same N tile, each CTA loading half of every weight stage and
+    // multicasting it to both; an odd tail tile gives the second CTA a phantom
+    // copy of its partner's tile whose results are not stored).
+    const int cl = p.cluster;
+    const uint32_t cr = cl > 1 ? cluster_ctarank() : 0;
     const int ks = p.ksplit;
-    const int split = blockIdx.x % ks;
-    const int tile0 = blockIdx.x / ks, tile_step = gridDim.x / ks;
+    const int unit = blockIdx.x / cl;
+    const int split = unit % ks;
+    const int w0_ = unit / ks, w_step = (gridDim.x / cl) / ks;
+    const int per_o = p.nsamples * p.rect_start[p.nrect];
+    const int per_o2 = (per_o + cl - 1) / cl;
+    const int total_w = cl > 1 ? p.nout_tiles * per_o2 : p.total_tiles;
+    auto item_of = [&](int w, bool &phantom) -> int {
+        if (cl == 1) {
+            phantom = false;
+            return w;
+        }
+        const int ot = w / per_o2, kk = w - ot * per_o2;
+        const int lt = 2 * kk + (int)cr;
+        phantom = lt >= per_o;
+        return ot * per_o + (phantom ? 2 * kk : lt);
+    };
     const int g0 = split * p.ncg / ks, g1 = (split + 1) * p.ncg / ks;
 
     if (warp == 0) {
@@ -184,8 +207,9 @@ __global__ void __launch_bounds__(192, 1)
         }
         int cur_o0 = -1;
         int a_it = 0, b_it = 0;
-        for (int u = tile0; u < total; u += tile_step) {
-            const TileCoord c = decode(p, u);
+        for (int w = w0_; w < total_w; w += w_step) {
+            bool phantom;
+            const TileCoord c = decode(p, item_of(w, phantom));
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {
@@ -228,8 +252,13 @@ __global__ void __launch_bounds__(192, 1)
                         if (b_it >= p.b_stages) mbar_wait(&b_empty[sb], ((b_it / p.b_stages) - 1) & 1);
                         if (elect_one()) {
                             mbar_arrive_expect_tx(&b_full[sb], p.bn * p.cg * 2);
-                            tma_load_2d(sB + sb * p.b_slot_bytes, &bmap, &b_full[sb],
-                                        t * p.cin_p + g * p.cg, c.o0);
+                            if (cl > 1)  // my half of the slot, into both CTAs
+                                tma_load_2d_mc(sB + sb * p.b_slot_bytes + cr * (p.bn / 2) * p.cg * 2, &bmap,
+                                               &b_full[sb], t * p.cin_p + g * p.cg, c.o0 + (int)cr * (p.bn / 2),
+                                               0x3);
+                            else
+                                tma_load_2d(sB + sb * p.b_slot_bytes, &bmap, &b_full[sb],
+                                            t * p.cin_p + g * p.cg, c.o0);
                         }
                         __syncwarp();
                         ++b_it;
@@ -254,7 +283,7 @@ __global__ void __launch_bounds__(192, 1)
         const bool do_mma = !(p.dbg & 4);
         int a_it = 0, b_it = 0, acc_it = 0;
         bool res_ready = false;
-        for (int u = tile0; u < total; u += tile_step) {
+        for (int w = w0_; w < total_w; w += w_step) {
             if (p.b_resident && !res_ready) {
                 mbar_wait(b_res, 0);
                 res_ready = true;
@@ -311,7 +340,10 @@ __global__ void __launch_bounds__(192, 1)
                                     if (do_mma)
                                         mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
                                                  bd + 2 * k16, idesc, ((g - g0) | t | k16) != 0);
-                            mma_commit(&b_empty[sb]);
+                            if (cl > 1)
+                                mma_commit_mc(&b_empty[sb], 0x3);  // the slot is shared by both CTAs
+                            else
+                                mma_commit(&b_empty[sb]);
                         }
                         __syncwarp();
                         ++b_it;
@@ -332,8 +364,9 @@ __global__ void __launch_bounds__(192, 1)
         const int m = eq * 32 + lane;
         const int ti = m >> p.tw_log2, tj = m & ((1 << p.tw_log2) - 1);
         int acc_it = 0;
-        for (int u = tile0; u < total; u += tile_step) {
-            const TileCoord c = decode(p, u);
+        for (int w = w0_; w < total_w; w += w_step) {
+            bool phantom;
+            const TileCoord c = decode(p, item_of(w, phantom));
             const int acc = acc_it % NB;
             const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
             if (tr) p.dbg_out[acc_it * 8 + 4] = clock64();
@@ -342,7 +375,8 @@ __global__ void __launch_bounds__(192, 1)
             tc_fence_after();
             for (int tt = 0; tt < p.tpw; ++tt) {
             const int i = c.i0 + tt * 16 + ti, j = c.j0 + tj;
-            const bool valid = i < p.rect[c.r].h0 + p.rect[c.r].nh && j < p.rect[c.r].w0 + p.rect[c.r].nw;
+            const bool valid = !phantom && i < p.rect[c.r].h0 + p.rect[c.r].nh &&
+                               j < p.rect[c.r].w0 + p.rect[c.r].nw;
             __nv_bfloat16 *orow = p.out + (long long)c.n * p.out_sn +
                                   (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
                                   (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0;
@@ -386,7 +420,10 @@ __global__ void __launch_bounds__(192, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    if (p.cluster > 1)
+        cluster_sync();  // no CTA leaves while its partner may still multicast into it
+    else
+        __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, ncols);
 }
 
@@ -397,7 +434,7 @@ size_t conv_v2_smem_bytes(const ConvV2Params &p) {
     return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16;
 }
 
-// Pair tiles only when the GLOBAL layer has this many tpw = 1 work items
+// Pair tiles only when the launch has this many tpw = 1 work items
 // (measured: pairing wins 1.5x on 128^2..512^2 layers, loses on 64^2/32^2).
 constexpr int kPairMinItems = 200;
 
@@ -479,7 +516,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
             q.tpw = 2;
             if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) {
                 p = q;
-            } else if (p.cg == 64 && p.s_in == 2 && !std::getenv("DC_V2_NO_CG32")) {
+            } else if (p.cg == 64 && p.s_in == 2 && p.allow_cg32 && !std::getenv("DC_V2_NO_CG32")) {
                 // stride 2: a 32-row stacked tile pair is too tall for 64-channel
                 // stages; 32-channel stages make it fit (same weight reuse)
                 q.cg = 32;
@@ -487,6 +524,10 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
             }
         }
     }
+    // streamed weights: CTA pairs multicast each weight stage (half each), which
+    // halves the L2 -> SM weight traffic without reducing the number of CTAs
+    static const bool no_cluster = std::getenv("DC_V2_NO_CLUSTER") != nullptr;
+    p.cluster = (!p.b_resident && p.bn % 32 == 0 && !no_cluster) ? 2 : 1;
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
 }
 
@@ -557,8 +598,45 @@ void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const Conv
     std::call_once(once, [] {
         cudaFuncSetAttribute(conv_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
+    if (p.cluster > 1 && !(p.dbg & 8)) {
+        // persistent CTA pairs: as many as can be co-resident (GPCs need not hold
+        // an even number of free SMs), a multiple of the split-K factor
+        const size_t smem = conv_v2_smem_bytes(p);
+        static std::map<size_t, int> max_clusters;
+        if (!max_clusters.count(smem)) {
+            cudaLaunchConfig_t cfg{};
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+            cfg.gridDim = dim3(2 * (device_sm_count() / 2));
+            cfg.blockDim = dim3(192);
+            cfg.dynamicSmemBytes = smem;
+            cfg.attrs = at, cfg.numAttrs = 1;
+            int n = 0;
+            cudaError_t e = cudaOccupancyMaxActiveClusters(&n, conv_v2_kernel, &cfg);
+            DC_REQUIRE(e == cudaSuccess && n > 0, DC_ERR_CUDA, "cluster occupancy: %s", cudaGetErrorString(e));
+            max_clusters[smem] = n;
+        }
+        const int per_o = p.nsamples * p.rect_start[p.nrect];
+        const int total_w = p.nout_tiles * ((per_o + 1) / 2);
+        const int units = p.ksplit * std::max(1, std::min(total_w, max_clusters[smem] / p.ksplit));
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * units);
+        cfg.blockDim = dim3(192);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cfg.attrs = at, cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, conv_v2_kernel, amap, bmap, p);
+        DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 cluster launch: %s", cudaGetErrorString(e));
+        ++g_launches;
+        return;
+    }
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, device_sm_count() / p.ksplit));
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
+        DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER");
         ConvV2Params q = p;
         cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
         cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));

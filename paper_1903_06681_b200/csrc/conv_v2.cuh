@@ -72,7 +72,10 @@ struct ConvV2Params {
     // and conv_v2_reduce sums them in split order. ksplit depends only on the
     // global layer shape, so partitioned results stay bitwise equal to 1 GPU.
     int ksplit;
-    int work_hint;             // work items of the GLOBAL layer at tpw = 1 (x ksplit): pairing only when plentiful
+    int work_hint;             // work items of THIS launch at tpw = 1 (x ksplit): pairing only when plentiful
+    int cluster;               // 2: CTA pairs share (multicast) every streamed weight stage; 1: none
+    int allow_cg32;            // stride 2: may narrow 64-channel stages to 32 for tile pairs (changes the
+                               // summation order: decided from the GLOBAL layer, see capi.cu)
     float *ws;
     int ws_h, ws_w;
     __nv_bfloat16 *out;
