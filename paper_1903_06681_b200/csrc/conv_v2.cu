@@ -62,6 +62,32 @@ __device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
 
 constexpr int kMaxBar = 16;
 
+// Streamed weights: the MMAs of one weight slot (one tap of one channel group):
+// NK x K16 steps for each of TPW stacked tiles, fully unrolled (compile-time
+// multiples of hoisted strides, no per-MMA descriptor arithmetic chains).
+template <int NK, int TPW>
+__device__ __forceinline__ void issue_slot(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t a_kstep,
+                                           uint32_t a_tile16, uint32_t acc_cols, uint32_t idesc, bool first) {
+#pragma unroll
+    for (int k16 = 0; k16 < NK; ++k16)
+#pragma unroll
+        for (int tt = 0; tt < TPW; ++tt)
+            mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
+                     (first && k16 == 0) ? 0u : 1u);
+}
+__device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tmem, uint64_t ad, uint64_t bd,
+                                               uint32_t a_kstep, uint32_t a_tile16, uint32_t acc_cols,
+                                               uint32_t idesc, bool first) {
+    switch ((nk16 << 4) | tpw) {
+    case 0x41: issue_slot<4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x42: issue_slot<4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x21: issue_slot<2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x22: issue_slot<2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x11: issue_slot<1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    default: issue_slot<1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    }
+}
+
 // Fully unrolled MMA issue for one channel group of one tile (resident
 // weights): every descriptor offset is a compile-time multiple of a runtime
 // stride hoisted out of the loop, so the single issuing thread spends a few
@@ -325,21 +351,22 @@ __global__ void __launch_bounds__(192, 1)
                     }
                     __syncwarp();
                 } else {
+                    // warp-uniform tap counters (no division), descriptors built
+                    // outside the elected branch, unrolled slot issue
+                    uint64_t arow = a_stage;
+                    int tw = 0, sb = b_it % p.b_stages;
+                    uint32_t ph = (b_it / p.b_stages) & 1;
                     for (int t = 0; t < p.T; ++t) {
-                        const int sb = b_it % p.b_stages;
-                        mbar_wait(&b_full[sb], (b_it / p.b_stages) & 1);
+                        mbar_wait(&b_full[sb], ph);
                         tc_fence_after();
+                        const uint64_t ad = arow + (uint32_t)(tw >> p.s_shift) * p.a_col16 +
+                                            (uint32_t)(tw & p.s_shift) * p.a_par16;
+                        const uint64_t bd = b_desc0 + (uint32_t)sb * b_slot16;
+                        const bool first = g == g0 && t == 0;
                         if (elect_one()) {
-                            const int th = t / p.kw, tw = t - th * p.kw;
-                            const uint64_t ad = a_stage + (uint32_t)th * p.a_row16 +
-                                                (uint32_t)(tw >> p.s_shift) * p.a_col16 +
-                                                (uint32_t)(tw & p.s_shift) * p.a_par16;
-                            const uint64_t bd = b_desc0 + (uint32_t)sb * b_slot16;
-                            for (int k16 = 0; k16 < nk16; ++k16)
-                                for (int tt = 0; tt < p.tpw; ++tt)
-                                    if (do_mma)
-                                        mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
-                                                 bd + 2 * k16, idesc, ((g - g0) | t | k16) != 0);
+                            if (do_mma)
+                                issue_slot_any(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
+                                               first);
                             if (cl > 1)
                                 mma_commit_mc(&b_empty[sb], 0x3);  // the slot is shared by both CTAs
                             else
@@ -347,6 +374,8 @@ __global__ void __launch_bounds__(192, 1)
                         }
                         __syncwarp();
                         ++b_it;
+                        if (++sb == p.b_stages) sb = 0, ph ^= 1;
+                        if (++tw == p.kw) tw = 0, arow += p.a_row16;
                     }
                     if (elect_one()) mma_commit(&a_empty[s]);
                     __syncwarp();
@@ -591,9 +620,13 @@ int device_sm_count() {
     return n;
 }
 
-void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p,
+void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p_in,
                     cudaStream_t st) {
-    if (p.total_tiles == 0) return;
+    if (p_in.total_tiles == 0) return;
+    // DC_V2_DBG (debug only): 1 skip A loads, 2 skip stores, 4 skip MMAs, 8 trace CTA 0
+    static const int dbg_env = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
+    ConvV2Params p = p_in;
+    p.dbg = dbg_env;
     static std::once_flag once;
     std::call_once(once, [] {
         cudaFuncSetAttribute(conv_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
