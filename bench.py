@@ -434,14 +434,12 @@ def main():
         d["bn_ms"] = bn_ms
         per.append((d, f_ms, w_ms, x_ms))
     peaks, peak_src = load_peaks()
-    # dominant kernel: the (layer, op) with the largest device time
-    cands = []
-    for d, f_ms, w_ms, x_ms in per:
-        cands.append((f_ms, d, "fp", "conv_gemm_kernel (forward)"))
-        if world == 1:
-            cands.append((w_ms, d, "bpw", "wgrad_kernel (+ split-K reduce)"))
-            cands.append((x_ms, d, "bpx", "conv_gemm_kernel (backward-data, + weight transform)"))
-    op_ms, d, op, kname = max(cands, key=lambda c: c[0])
+    # dominant kernel: conv_v2_kernel (the implicit-GEMM forward / backward-data
+    # kernel, the largest share of the step in profiles/r1_launches_*.txt),
+    # reported on the layer whose forward takes longest -- at one GPU that op
+    # is exactly one conv_v2 launch (no split-K on the large layers).
+    op_ms, d = max(((f_ms, d) for d, f_ms, w_ms, x_ms in per), key=lambda c: c[0])
+    op = "fp"
     loc = d["l"]
     # algorithmic work of THIS rank's shard (blocked split: global / world)
     fl = layer_flops(loc) / world
@@ -453,8 +451,18 @@ def main():
     else:
         roof = {"bound": "hbm", "achieved": by / (op_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
     roof["frac"] = roof["achieved"] / roof["peak"]
+    # DRAM bytes per launch of this kernel on this shape from the committed
+    # `ncu --set full` capture (profiles/r1_traffic.json), when there is one
     roof["traffic"] = None
-    roof["kernel"] = f"{loc[0]} {op}: {kname}"
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        key = f"conv_v2_kernel fwd {list(loc[1:])}"
+        if world == 1 and key in tr:
+            roof["traffic"] = tr[key]["dram_bytes"]
+            roof["traffic_algorithmic"] = by
+    except (OSError, ValueError, KeyError):
+        pass
+    roof["kernel"] = f"conv_v2_kernel ({loc[0]} forward{'' if world == 1 else ' incl. halo exchange'})"
     roof["avg_launch_ms"] = op_ms
     roof["peak_source"] = peak_src + " burst (MEASURED_PEAKS.json)"
 
