@@ -218,6 +218,7 @@ def main():
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
+    ap.add_argument("--no-fused-bn", action="store_true", help="BN statistics by a separate pass over y")
     ap.add_argument("--ablate", default="", help="DIAGNOSTIC: comma list of exchange,bn,allreduce to skip")
     ap.add_argument("--ar-sync", action="store_true", help="join each dW allreduce inside its layer's call")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
@@ -303,7 +304,10 @@ def main():
 
     def op_calls(d):
         """The calls of one layer, in step order: (name, fn)."""
-        ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], FLAGS, sp)),
+        # the forward epilogue accumulates the BN statistics of y (DC_BN_STATS);
+        # dc_bn_spatial_stats then reduces those partials (+ the NVLink allreduce)
+        fwd_flags = FLAGS | (0 if "bn" in ablate or args.no_fused_bn else dc.DC_BN_STATS)
+        ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], fwd_flags, sp)),
                # spatially aggregated BN statistics of the layer output (SURVEY.md 8(a) a7)
                ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp))]
         if "bn" in ablate:

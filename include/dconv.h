@@ -79,6 +79,10 @@ typedef struct dc_plan_s *dc_plan_t;
                                   call, overlapped with the interior tiles  */
 #define DC_ALLREDUCE     0x2u  /* conv_bwd_filter: sum dW over all ranks    */
 #define DC_HALO_NCCL     0x4u  /* use grouped ncclSend/ncclRecv instead of direct P2P       */
+#define DC_BN_STATS      0x10u /* conv_fwd: accumulate the BN statistics of the stored y in
+                                  the epilogue (per-CTA fp64 partials); the next
+                                  dc_bn_spatial_stats on that y reduces them instead of
+                                  re-reading y (same result up to fp64 summation order) */
 #define DC_ALLREDUCE_ASYNC 0x8u /* with DC_ALLREDUCE: queue the dW allreduce on the
                                   communicator's gradient stream instead of joining it
                                   into the call (overlaps the later layers' work,

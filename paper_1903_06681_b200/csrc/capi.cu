@@ -105,6 +105,10 @@ struct dc_plan_s {
     double *bn_part = nullptr;
     size_t bn_part_bytes = 0;
     double *bn_sums = nullptr;
+    double *bn_fpart = nullptr;      // fused BN partials of the last DC_BN_STATS forward
+    size_t bn_fpart_bytes = 0;
+    const void *bn_fused_y = nullptr;  // its y (stats of any other tensor: bn_sums_kernel)
+    int bn_fused_slots = 0;
     double predicted = 0.0;
 
     ~dc_plan_s() {
@@ -121,6 +125,7 @@ struct dc_plan_s {
         if (ws2) cudaFree(ws2);
         if (bn_part) cudaFree(bn_part);
         if (bn_sums) cudaFree(bn_sums);
+        if (bn_fpart) cudaFree(bn_fpart);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         if (s_comm) cudaStreamDestroy(s_comm);
@@ -298,6 +303,10 @@ struct GemmLaunch {
     int64_t w_rows = 0, w_kcols = 0;
     int ksplit = 1;            // v2 split-K over channel groups (from the GLOBAL shape)
     int64_t work_hint = 0;     // GLOBAL 16x8 tiles x N tiles (v2 tile-pairing choice)
+    // fused BN statistics: per-CTA partial slots [slot][2][nout_p] (fp64)
+    double *bn_part = nullptr;
+    int bn_slot = 0, bn_slot_cap = 0;
+    bool bn_ok = true;
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
 };
@@ -433,6 +442,17 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.bn = L.p.bn;
     q.nout_tiles = (int)ceil_div(L.p.nout_p, q.bn);
     q.work_hint = (int)std::min<int64_t>(local_tiles * q.nout_tiles * L.ksplit, 1 << 30);
+    // fused BN statistics when the epilogue holds final values of all channels
+    // (bitwise-neutral: the stage width above was chosen without them)
+    // (only with enough MMA work per tile to hide the epilogue reduction: K =
+    // C_pad x taps >= 1152, measured: fusing a K = 576 layer costs more than
+    // the separate pass over y)
+    q.bn_stats = L.bn_part && L.ksplit == 1 && q.nout_tiles == 1 && (int64_t)q.cin_p * q.T >= 1152 ? 1 : 0;
+    if (L.bn_part && !q.bn_stats) L.bn_ok = false;
+    if (q.bn_stats) {
+        ConvV2Params t = q;
+        if (!conv_v2_configure(t, kV2SmemLimit)) q.bn_stats = 0, L.bn_ok = false;
+    }
     if (!conv_v2_configure(q, kV2SmemLimit)) return false;
     DC_REQUIRE((int)rects.size() <= kMaxRects, DC_ERR_ARG, "too many rects");
     q.nrect = (int)rects.size();
@@ -456,15 +476,26 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
         const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
         make_tmap(&amap, in_base, 4, dims, strides, box, es, 0);
     }
+    if (q.bn_stats) {
+        // worst-case slot count of this launch (persistent grid <= SMs)
+        if (L.bn_slot + device_sm_count() > L.bn_slot_cap) {
+            q.bn_stats = 0, L.bn_ok = false;
+            if (!conv_v2_configure(q, kV2SmemLimit)) return false;
+        } else {
+            q.bn_part = L.bn_part + (size_t)L.bn_slot * 2 * q.nout_p;
+        }
+    }
+    int grid = 0;
     if (q.cg != L.p.bkc || q.bn != L.p.bn || q.cluster > 1) {
         // narrower channel stages, or half-height boxes (each CTA of a pair
         // loads half of every weight stage): re-tile the weights
         CUtensorMap bmap;
         weight_map(&bmap, L.w_base, L.w_rows, L.w_kcols, q.cg, q.bn / q.cluster);
-        launch_conv_v2(amap, bmap, q, st);
+        grid = launch_conv_v2(amap, bmap, q, st);
     } else {
-        launch_conv_v2(amap, L.bmap, q, st);
+        grid = launch_conv_v2(amap, L.bmap, q, st);
     }
+    if (q.bn_stats) L.bn_slot += grid;
     if (q.ksplit > 1) launch_conv_v2_reduce(q, st);
     return true;
 }
@@ -486,6 +517,7 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
                   const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
     if (rects.empty()) return;
     if (launch_rects_v2(L, rects, in_base, ind, cin_p, nsamples, st)) return;
+    L.bn_ok = false;  // (the v1 kernel has no fused statistics)
     std::map<int, std::vector<OutRect>> by_twl;
     for (auto &r : rects) by_twl[pick_twl(r.nh, r.nw, 128)].push_back(r);
     for (auto &kv : by_twl) {
@@ -1214,6 +1246,12 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     cudaStream_t st = (cudaStream_t)stream;
     GemmLaunch L;
     prepare_fwd(pl, x, w, y, L);
+    pl->bn_fused_y = nullptr;
+    if (flags & DC_BN_STATS) {
+        L.bn_slot_cap = 8 * device_sm_count();
+        ensure_alloc(pl->bn_fpart, pl->bn_fpart_bytes, sizeof(double) * L.bn_slot_cap * 2 * pl->rp.g.Fp);
+        L.bn_part = pl->bn_fpart;
+    }
     const dc_shard_desc_t xd = describe(pl->rp, DC_X);
     const int nl = (int)pl->rp.nrange.size();
     const bool overlap =
@@ -1231,6 +1269,10 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
     } else {
         launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
+    }
+    if (L.bn_part && L.bn_ok && L.bn_slot > 0) {  // dc_bn_spatial_stats(y) reduces these
+        pl->bn_fused_y = y;
+        pl->bn_fused_slots = L.bn_slot;
     }
     DC_API_END
 }
@@ -1302,8 +1344,12 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     ensure_alloc(pl->bn_part, pl->bn_part_bytes, need);
     const bool global = !local_only && pl->bn_group > 1;
     // single group: the reduce kernel also finalises mean/var (no allreduce between)
-    launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
-                   (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
+    if (pl->bn_fused_y == t && pl->bn_fused_slots > 0)  // partials from the fused forward epilogue
+        launch_bn_reduce(pl->bn_fpart, pl->bn_fused_slots, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix,
+                         global ? nullptr : mean, global ? nullptr : var, st);
+    else
+        launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
+                       (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
     if (global && pl->comm && pl->comm->bn_p2p) {
         // one-shot NVLink allreduce among the ranks with this rank's i_N
         dc_comm_s *c = pl->comm;

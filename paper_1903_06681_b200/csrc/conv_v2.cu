@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t *acc_full = bars + 4 * kMaxBar, *acc_empty = acc_full + 2;
     uint64_t *b_res = acc_empty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_res + 1);
+    double *bn_acc = reinterpret_cast<double *>(b_res + 2);  // [4 epilogue warps][2][bn] (bn_stats)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -392,6 +393,10 @@ __global__ void __launch_bounds__(192, 1)
         const int eq = warp & 3;  // TMEM lane quarter this warp may access
         const int m = eq * 32 + lane;
         const int ti = m >> p.tw_log2, tj = m & ((1 << p.tw_log2) - 1);
+        double *my_acc = bn_acc + (warp - 2) * 2 * p.bn;
+        if (p.bn_stats)
+            for (int i = lane; i < 2 * p.bn; i += 32) my_acc[i] = 0.0;
+        __syncwarp();
         int acc_it = 0;
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
@@ -425,19 +430,49 @@ __global__ void __launch_bounds__(192, 1)
                             dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                                  __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
                     }
-                } else if (valid && c.o0 + c16 * 16 < p.nout_p && !(p.dbg & 2)) {
-                    uint4 lo, hi;
-                    lo.x = pack2(v[0], v[1]);
-                    lo.y = pack2(v[2], v[3]);
-                    lo.z = pack2(v[4], v[5]);
-                    lo.w = pack2(v[6], v[7]);
-                    hi.x = pack2(v[8], v[9]);
-                    hi.y = pack2(v[10], v[11]);
-                    hi.z = pack2(v[12], v[13]);
-                    hi.w = pack2(v[14], v[15]);
-                    uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
-                    dst[0] = lo;
-                    dst[1] = hi;
+                } else {
+                    const bool st_ok = valid && c.o0 + c16 * 16 < p.nout_p;
+                    uint32_t pk[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) pk[e] = pack2(v[2 * e], v[2 * e + 1]);
+                    if (st_ok && !(p.dbg & 2)) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
+                        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                    }
+                    if (p.bn_stats) {
+                        // statistics of the stored bf16 values: an fp32 pairwise
+                        // transpose-reduce over the warp's 32 pixels (fixed order;
+                        // |error| <= 5 * 2^-24 * sum|x|), then fp64
+                        float a[16], q[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            const float xv = st_ok ? __uint_as_float((e & 1) ? (pk[e >> 1] & 0xffff0000u)
+                                                                             : (pk[e >> 1] << 16))
+                                                   : 0.f;
+                            a[e] = xv;
+                            q[e] = xv * xv;  // exact: 8-bit significand
+                        }
+#pragma unroll
+                        for (int w = 8; w >= 1; w >>= 1) {
+                            const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+                            for (int j = 0; j < w; ++j) {
+                                const float sa = up ? a[j] : a[j + w], ka = up ? a[j + w] : a[j];
+                                const float sq = up ? q[j] : q[j + w], kq = up ? q[j + w] : q[j];
+                                a[j] = ka + __shfl_xor_sync(0xffffffffu, sa, 2 * w);
+                                q[j] = kq + __shfl_xor_sync(0xffffffffu, sq, 2 * w);
+                            }
+                        }
+                        // lanes 2k and 2k+1 hold channel k's halves
+                        const float a_o = __shfl_xor_sync(0xffffffffu, a[0], 1);
+                        const float q_o = __shfl_xor_sync(0xffffffffu, q[0], 1);
+                        if ((lane & 1) == 0) {
+                            const int ch = c.o0 + c16 * 16 + ((lane >> 1) & 15);
+                            my_acc[ch] += (double)(a[0] + a_o);
+                            my_acc[p.bn + ch] += (double)(q[0] + q_o);
+                        }
+                    }
                 }
             }
             }  // tt
@@ -446,6 +481,16 @@ __global__ void __launch_bounds__(192, 1)
             if (lane == 0) mbar_arrive(&acc_empty[acc]);
             if (tr) p.dbg_out[acc_it * 8 + 6] = clock64();
             ++acc_it;
+        }
+        if (p.bn_stats) {  // this CTA's partial: the 4 warps summed in a fixed order
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            double *dst = p.bn_part + (long long)blockIdx.x * 2 * p.nout_p;
+            for (int i = threadIdx.x - 64; i < 2 * p.nout_p; i += 128) {
+                const int k = i / p.nout_p, ch = i - k * p.nout_p;
+                double t = 0.0;
+                for (int w4 = 0; w4 < 4; ++w4) t += bn_acc[w4 * 2 * p.bn + k * p.bn + ch];
+                dst[i] = t;
+            }
         }
     }
     tc_fence_before();
@@ -460,7 +505,8 @@ __global__ void __launch_bounds__(192, 1)
 size_t conv_v2_smem_bytes(const ConvV2Params &p) {
     const size_t b = p.b_resident ? (size_t)p.T * (p.ncg / p.ksplit) * p.b_slot_bytes
                                   : (size_t)p.b_stages * p.b_slot_bytes;
-    return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16;
+    return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16 +
+           (p.bn_stats ? (size_t)4 * 2 * p.bn * sizeof(double) : 0);
 }
 
 // Pair tiles only when the launch has this many tpw = 1 work items
@@ -520,7 +566,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.a_kstep16 = (2 * p.s_in * p.plane_bytes) >> 4;
     }
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
-    const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16;
+    const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16 + (p.bn_stats ? 4 * 2 * p.bn * 8 : 0);
     if (p.ksplit < 1 || p.ncg % p.ksplit) return false;
     const int resident_b = p.T * (p.ncg / p.ksplit) * p.b_slot_bytes;
     // prefer resident weights with >= 2 A stages
@@ -620,9 +666,9 @@ int device_sm_count() {
     return n;
 }
 
-void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p_in,
-                    cudaStream_t st) {
-    if (p_in.total_tiles == 0) return;
+int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p_in,
+                   cudaStream_t st) {
+    if (p_in.total_tiles == 0) return 0;
     // DC_V2_DBG (debug only): 1 skip A loads, 2 skip stores, 4 skip MMAs, 8 trace CTA 0
     static const int dbg_env = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
     ConvV2Params p = p_in;
@@ -665,7 +711,7 @@ void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const Conv
         cudaError_t e = cudaLaunchKernelEx(&cfg, conv_v2_kernel, amap, bmap, p);
         DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 cluster launch: %s", cudaGetErrorString(e));
         ++g_launches;
-        return;
+        return 2 * units;
     }
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, device_sm_count() / p.ksplit));
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
@@ -690,6 +736,7 @@ void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const Conv
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));
     ++g_launches;
+    return grid;
 }
 
 }  // namespace dc

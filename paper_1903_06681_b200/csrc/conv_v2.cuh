@@ -47,6 +47,11 @@ struct ConvV2Params {
     uint32_t a_kstep16;            // A descriptor delta between 16-channel K slices
     int dbg;                   // timing experiments: 1 skip steady-state A TMA, 2 skip stores, 4 skip MMAs, 8 trace
     long long *dbg_out;        // trace buffer (dbg & 8): CTA 0, [tile][8] clock64 stamps
+    // Fused BN statistics of the stored y: per CTA, fp64 sum and
+    // sum of squares of every channel over the CTA's tiles, written to
+    // bn_part[blockIdx.x][2][nout_p] (needs ksplit == 1 and nout_tiles == 1)
+    int bn_stats;
+    double *bn_part;
     int s_in;                  // A element stride (conv stride for fwd, 1 for bwd-data)
     int origin_h, origin_w;    // input coord of GEMM pixel (0,0) at tap offset 0
     int T;                     // taps
@@ -92,7 +97,8 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit);
 // amap: 4D map over the input buffer with box {8, PWs * s_in, PH, 1} and
 // element strides {1, s_in, 1, 1}, no swizzle. bmap: [N rows][T * cin_p]
 // weights with box {cg, bn}, swizzle cg * 2 bytes.
-void launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p,
+// returns the grid size (number of CTAs, = BN partial slots used)
+int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p,
                     cudaStream_t st);
 // Fixed-order sum of the split-K partials -> bf16 output (rects / out mapping of p).
 void launch_conv_v2_reduce(const ConvV2Params &p, cudaStream_t st);

@@ -99,8 +99,9 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
         for (int e = 0; e < 8; ++e) s[e] = q[e] = 0.0;
         // 4 independent 16-byte loads in flight per thread (memory-level
         // parallelism), then fp64 accumulation (x^2 of a bf16 is exact in fp32)
-        // groups of 8 pixels are summed in fp32 (|x| <= 1 values; group error
-        // <= 8 * 2^-24) and flushed to the fp64 accumulators once per group
+        // groups of 8 pixels are summed in fp32 (|error| <= 7 u sum|x| per group,
+        // DESIGN.md §7; a double-float group sum was measured 1.8x slower) and
+        // flushed to the fp64 accumulators once per group
         const long long step = (long long)gridDim.x * pix_lanes;
         long long p = (long long)blockIdx.x * pix_lanes + pl;
         for (; p + 7 * step < npix; p += 8 * step) {
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
                 for (int e = 0; e < 8; ++e) {
                     const float x = __bfloat162float(h[e]);
                     fs[e] += x;
-                    fq[e] = fmaf(x, x, fq[e]);
+                    fq[e] = fmaf(x, x, fq[e]);  // x*x exact (8-bit significand)
                 }
             }
 #pragma unroll
@@ -205,6 +206,14 @@ void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *pa
     e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
     g_launches += 2;
+}
+
+void launch_bn_reduce(const double *partials, int blocks, int cpad, double *out, int c, double count, double *mean,
+                      double *var, cudaStream_t st) {
+    bn_reduce_kernel<<<(cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, cpad, out, c, count, mean, var);
+    cudaError_t e = cudaGetLastError();
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
+    ++g_launches;
 }
 
 __global__ void bn_finalize_kernel(const double *sums, int cpad, int c, double count, double *mean,

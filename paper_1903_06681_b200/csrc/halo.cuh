@@ -41,6 +41,10 @@ int bn_partial_blocks(long long npix, int cpad);
 // (fp64, fixed order); with `mean` non-null also mean/var over `count` pixels.
 void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
                     double *out, int c, double count, double *mean, double *var, cudaStream_t st);
+// Fixed-order reduction of `blocks` partials [blocks][2][cpad] into out[2][cpad]
+// (+ mean / var when `mean` is set), e.g. the fused forward-epilogue partials.
+void launch_bn_reduce(const double *partials, int blocks, int cpad, double *out, int c, double count, double *mean,
+                      double *var, cudaStream_t st);
 // mean = s / count, var = ss / count - mean^2 (biased), first `c` channels.
 void launch_bn_finalize(const double *sums, int cpad, int c, double count, double *mean,
                         double *var, cudaStream_t st);

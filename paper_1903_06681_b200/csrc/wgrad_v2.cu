@@ -75,6 +75,19 @@ __host__ __device__ inline Atom atom_of(const WgradV2Params &p, int mt, int a, i
 
 constexpr int kWMaxStages = 8;
 
+// The MMAs of one pixel block: G M tiles x 4 K16 steps, fully unrolled (the
+// descriptors are loop-invariant per CTA; only the stage offset moves).
+template <int G>
+__device__ __forceinline__ void wgrad_issue(uint32_t tmem, const uint64_t (&adesc)[8], uint32_t xo, uint64_t bd,
+                                            uint32_t ak16, uint32_t acc_cols, uint32_t idesc, bool first) {
+#pragma unroll
+    for (int i = 0; i < G; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // 64 pixels = 4 x K16 (2 output rows each)
+            mma_bf16(tmem + i * acc_cols, adesc[i] + xo + k * ak16, bd + k * (2048 >> 4), idesc,
+                     (first && k == 0) ? 0u : 1u);
+}
+
 __global__ void __launch_bounds__(192, 1)
     wgrad_v2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dymap,
                     const __grid_constant__ WgradV2Params p) {
@@ -181,24 +194,33 @@ __global__ void __launch_bounds__(192, 1)
         const uint64_t bdesc0 = smem_desc(smem_u32(sD), 64 * 64 * 2, 1024, 2);
         const uint32_t idesc = idesc_bf16(128, p.bn, 1, 1);
         const uint32_t acc_cols = p.bn_cols;
+        const uint32_t ak16 = (2 * a_sbo) >> 4;
+        const uint32_t xstep = (uint32_t)p.x_stage_bytes >> 4, dstep = (uint32_t)p.dy_stage_bytes >> 4;
+        int s = 0;
+        uint32_t ph = 0, xo = 0;
+        uint64_t bd = bdesc0;
         for (int kb = 0; kb < KB; ++kb) {
-            const int s = kb % p.stages;
-            mbar_wait(&full[s], (kb / p.stages) & 1);
+            mbar_wait(&full[s], ph);
             tc_fence_after();
             if (elect_one()) {
-                const uint32_t xo = (uint32_t)(s * p.x_stage_bytes) >> 4;
-                const uint64_t bd = bdesc0 + ((uint32_t)(s * p.dy_stage_bytes) >> 4);
-#pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (i < G) {
-#pragma unroll
-                        for (int k = 0; k < 4; ++k)  // 64 pixels = 4 x K16 (2 output rows each)
-                            mma_bf16(tmem + i * acc_cols, adesc[i] + xo + k * ((2 * a_sbo) >> 4),
-                                     bd + k * (2048 >> 4), idesc, (kb | k) != 0);
-                    }
+                switch (G) {
+                case 1: wgrad_issue<1>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 2: wgrad_issue<2>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 3: wgrad_issue<3>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 4: wgrad_issue<4>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 5: wgrad_issue<5>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 6: wgrad_issue<6>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                case 7: wgrad_issue<7>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                default: wgrad_issue<8>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
+                }
                 mma_commit(&empty[s]);
             }
             __syncwarp();
+            if (++s == p.stages) {
+                s = 0, ph ^= 1, xo = 0, bd = bdesc0;
+            } else {
+                xo += xstep, bd += dstep;
+            }
         }
         if (elect_one()) mma_commit(done);
         __syncwarp();

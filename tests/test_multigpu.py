@@ -5,7 +5,8 @@
     kernel computed on the same device (north_star);
   * the allreduced dW matches the 1-GPU dW within the fp32 bar (1e-4,
     different summation tree, reading R10);
-  * spatially aggregated BN statistics match the 1-GPU statistics (1e-9)."""
+  * spatially aggregated BN statistics match the 1-GPU statistics within the
+    derived fp32-group bound."""
 import os
 import socket
 import traceback
@@ -111,8 +112,31 @@ def _worker(rank, world, port, errq):
             dc.dc_bn_spatial_stats(plan, y, mean, var, False)
             torch.cuda.synchronize()
             if grid[0] == 1:  # group = all ranks = the whole batch
-                assert (mean - mean_r).abs().max().item() <= 1e-9, f"{tag}: BN mean"
-                assert (var - var_r).abs().max().item() <= 1e-9, f"{tag}: BN var"
+                # both sides: fp32 groups of 8 then fp64, different groupings
+                Yl = Y[..., :F].double()
+                u = 2.0 ** -24
+                tm = 2 * 7 * u * Yl.abs().mean(dim=(0, 1, 2)).max().item() + 1e-12
+                tv = 2 * 7 * u * (Yl * Yl).mean(dim=(0, 1, 2)).max().item() + 2 * mean_r.abs().max().item() * tm + 1e-12
+                assert (mean - mean_r).abs().max().item() <= tm, f"{tag}: BN mean"
+                assert (var - var_r).abs().max().item() <= tv, f"{tag}: BN var"
+            # (4b) BN statistics fused into the overlapped forward (interior and
+            # boundary launches each contribute partial slots)
+            y3 = torch.empty_like(y)
+            xb.copy_(fill_owned_only(x, xd))
+            torch.cuda.synchronize()
+            dist.barrier()
+            dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y3, dc.DC_EXCHANGE | dc.DC_BN_STATS)
+            m3, v3 = torch.zeros_like(mean), torch.zeros_like(var)
+            dc.dc_bn_spatial_stats(plan, y3, m3, v3, False)
+            torch.cuda.synchronize()
+            assert torch.equal(y3, ys), f"{tag}: y (fused BN) not bitwise equal to 1-GPU"
+            # fused path: fp32 pairwise tree per warp (depth 5), DESIGN.md §7
+            yl = y3[..., :F].double()
+            u = 2.0 ** -24
+            tm = 5 * u * yl.abs().mean(dim=(0, 1, 2)).max().item() + 1e-12
+            tv = 5 * u * (yl * yl).mean(dim=(0, 1, 2)).max().item() + 2 * mean.abs().max().item() * tm + 1e-12
+            assert (m3 - mean).abs().max().item() <= 4 * tm and (v3 - var).abs().max().item() <= 4 * tv, \
+                f"{tag}: fused BN statistics differ"
             # (5) repeated BN calls cycle the P2P mailbox parities; results identical
             for _ in range(3):
                 m2, v2 = torch.zeros_like(mean), torch.zeros_like(var)
