@@ -142,6 +142,15 @@ dc_status_t dc_plan_query(dc_plan_t plan, dc_tensor_t t, dc_shard_desc_t *desc);
 /* The grid in use and the model's predicted seconds for fwd+bwd of the layer
  * (PAPER.md:206 Cost_D(l)); predicted may be NULL. */
 dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicted_seconds);
+/* Summation-order setting of the conv kernels: the split-K factor over
+ * channel groups (the only choice that changes how an output is summed) is
+ * picked for the global layer divided over `world` ranks. Default (world 0):
+ * this plan's grid size, i.e. each shard gets as many splits as its own work
+ * needs. Plans of the same layer with equal settings sum every output element
+ * in the same order, so a 1-GPU plan with world = P reproduces the y and dx
+ * of any P-rank partition bit for bit (north_star). Host only; takes effect
+ * from the next compute call. Errors: DC_ERR_ARG. */
+dc_status_t dc_plan_set_splitk_world(dc_plan_t plan, int world);
 dc_status_t dc_plan_destroy(dc_plan_t plan);
 
 /* COLLECTIVE. Allocate (and zero) the margined buffer of t in {DC_X, DC_DY}

@@ -26,7 +26,7 @@ DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "dc_comm_create", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
-    "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp",
+    "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_load_table", "dc_model_layer_cost",
@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
         "dc_comm_create": [i32, i32, vp, i32, P(vp)],
         "dc_comm_unique_id": [vp],
         "dc_comm_destroy": [vp],
+        "dc_plan_set_splitk_world": [vp, i32],
         "dc_comm_sync": [vp, vp],
         "dc_plan_create": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, vp, P(vp)],
         "dc_plan_create_virtual": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, i32, P(vp)],
@@ -186,6 +187,11 @@ def dc_plan_decomp(plan: int) -> tuple[tuple[int, int, int], float]:
     d, s = dc_decomp_t(), ctypes.c_double()
     _check(lib().dc_plan_decomp(plan, ctypes.byref(d), ctypes.byref(s)))
     return (d.pn, d.ph, d.pw), s.value
+
+
+def dc_plan_set_splitk_world(plan: int, world: int):
+    """Pick split-K as for the layer divided over `world` ranks (0: the plan's grid)."""
+    _check(lib().dc_plan_set_splitk_world(plan, world))
 
 
 def dc_plan_destroy(plan: int):

@@ -132,6 +132,8 @@ struct dc_plan_s {
         if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
     }
     int world() const { return rp.grid.size(); }
+    int ks_world = 0;  // dc_plan_set_splitk_world (0: the grid size)
+    int splitk_world() const { return ks_world > 0 ? ks_world : rp.grid.size(); }
     ncclComm_t nccl() const { return comm ? comm->nccl : nullptr; }
     uint32_t *flag(uint32_t *base, int which, int kind, int src) const {
         return base + ((which * 2 + kind) * world() + src);
@@ -302,11 +304,15 @@ struct GemmLaunch {
     const void *w_base = nullptr;  // B matrix [w_rows][w_kcols] (for re-tiling N)
     int64_t w_rows = 0, w_kcols = 0;
     int ksplit = 1;            // v2 split-K over channel groups (from the GLOBAL shape)
-    int64_t work_hint = 0;     // GLOBAL 16x8 tiles x N tiles (v2 tile-pairing choice)
+    int64_t work_hint = 0;     // 16x8 tiles x N tiles of the global layer / splitk_world
+    int max_ctas = 0;          // persistent grid cap (0: all SMs), leaves SMs to a concurrent launch
     // fused BN statistics: per-CTA partial slots [slot][2][nout_p] (fp64)
     double *bn_part = nullptr;
     int bn_slot = 0, bn_slot_cap = 0;
     bool bn_ok = true;
+    int dep[4] = {0, 0, 0, 0};       // output rows/cols reading the halo: top, bottom, left, right
+    const P2PExchange *halo = nullptr;  // fused P2P exchange (conv_v2 warp 6)
+    int halo_rect0 = 0;
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
 };
@@ -384,7 +390,10 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     Split2D s{rp.h.out.size(), rp.w.out.size(), count(rp.h, true), count(rp.h, false),
               count(rp.w, true), count(rp.w, false)};
     make_rects(s, L.interior, L.boundary);
-    L.work_hint = g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles;
+    L.dep[0] = (int)s.bl, L.dep[1] = (int)s.bh, L.dep[2] = (int)s.bwl, L.dep[3] = (int)s.bwh;
+    // per-rank share of the global layer (splitk_world ranks; default: this grid)
+    L.work_hint = ceil_div(g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles,
+                           (int64_t)pl->splitk_world());
     L.ksplit = choose_ksplit(L.work_hint, g.Cp);
     attach_ksplit(pl, L, (int)rp.nrange.size());
 }
@@ -411,6 +420,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     std::memcpy(q.tap_w, L.p.tap_w, sizeof q.tap_w);
     q.cin_p = (int)cin_p;
     q.ksplit = L.ksplit;
+    if (L.halo) q.halo = 1, q.hx = *L.halo, q.halo_rect0 = L.halo_rect0;
     q.ws = L.ws;
     q.ws_h = L.ws_h;
     q.ws_w = L.ws_w;
@@ -420,6 +430,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.out_sn = L.p.out_sn, q.out_sh = L.p.out_sh, q.out_sw = L.p.out_sw;
     q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
     q.nout_p = L.p.nout_p;
+    q.max_ctas = L.max_ctas;
     const int TW = 1 << twl, TH = 128 >> twl;
     // (1) choices that change the summation order (channel-stage width) come
     // from the GLOBAL layer, so every partition computes the 1-GPU bits
@@ -532,6 +543,74 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
 // ---------------------------------------------------------------------------
 // halo exchange
 // ---------------------------------------------------------------------------
+P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf);
+
+// Forward with the P2P halo exchange fused into the single conv_v2 launch:
+// tile-aligned rects (16 x 8 tiles, pairs of 32 rows) with the interior first
+// and the bands whose outputs read the halo last. False: not applicable.
+bool fused_fwd(dc_plan_s *pl, GemmLaunch &L, void *x, const dc_shard_desc_t &xd, int nl, cudaStream_t st) {
+    // opt-in (DC_FUSED_HALO=1): measured slower than the two-stream overlap at
+    // 2 and 4 GPUs because 32-row tile pairs put up to half a thin shard into
+    // the halo-dependent bands
+    static const bool on = std::getenv("DC_FUSED_HALO") != nullptr;
+    if (!on || use_v1() || L.p.T == 0) return false;
+    const int ho = (int)pl->rp.h.out.size(), wo = (int)pl->rp.w.out.size();
+    const int rt = std::min(ho, (int)round_up(L.dep[0], 32));
+    const int ie = rt + 32 * std::max(0, (ho - L.dep[1] - rt) / 32);
+    const int cl = std::min(wo, (int)round_up(L.dep[2], 8));
+    const int je = cl + 8 * std::max(0, (wo - L.dep[3] - cl) / 8);
+    std::vector<OutRect> rects;
+    if (ie > rt && je > cl) rects.push_back(OutRect{rt, cl, ie - rt, je - cl});
+    const int r0 = (int)rects.size();
+    for (const OutRect &r : {OutRect{0, 0, rt, wo}, OutRect{ie, 0, ho - ie, wo}, OutRect{rt, 0, ie - rt, cl},
+                             OutRect{rt, je, ie - rt, wo - je}})
+        if (r.nh > 0 && r.nw > 0) rects.push_back(r);
+    const P2PExchange hx = build_p2p(pl, 0, x);
+    L.halo = &hx;
+    L.halo_rect0 = r0;
+    const bool ok = launch_v2_shape(L, rects, 3, x, xd, pl->rp.g.Cp, nl, st);
+    L.halo = nullptr;
+    return ok;
+}
+
+// The P2P protocol of one exchange of tensor `which` (0: x, 1: dy) of the
+// registered buffer `buf`: my slabs -> the neighbours' mapped margins, their
+// ready flags / my data counters (halo.cuh: P2PExchange).
+P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf) {
+    const RankPlan &rp = pl->rp;
+    const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
+    const auto &recvs = which == 0 ? rp.x_recv : rp.dy_recv;
+    const int64_t cp = which == 0 ? rp.g.Cp : rp.g.Fp;
+    const int vec16 = (int)(cp * 2 / 16);
+    const int64_t nl = rp.nrange.size();
+    BufState &B = pl->buf[which];
+    const int me = rp.rank;
+    DC_REQUIRE(B.ptr == buf, DC_ERR_ARG,
+               "direct P2P halo exchange needs the buffer from dc_buffer_alloc (or pass DC_HALO_NCCL)");
+    DC_REQUIRE(sends.size() <= 8 && recvs.size() <= 8, DC_ERR_ARG, "too many halo neighbours");
+    DC_REQUIRE(B.dev_epoch != nullptr, DC_ERR_ARG, "P2P halo exchange: buffer not registered");
+    auto strides = [&](int64_t hb, int64_t wb, BlockCopy &c, bool src) {
+        const long long sw = vec16, sh = wb * vec16, sn = hb * wb * vec16;
+        if (src) c.s_sn = sn, c.s_sh = sh, c.s_sw = sw;
+        else c.d_sn = sn, c.d_sh = sh, c.d_sw = sw;
+    };
+    P2PExchange x{};
+    x.epoch_ctr = B.dev_epoch;
+    for (auto &m : recvs) x.ready_out[x.n_ready_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me);
+    for (auto &m : sends) {
+        x.ready_in[x.n_ready_in++] = pl->flag(pl->flags, which, FLAG_READY, m.peer);
+        x.data_out[x.n_data_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_DATA, me);
+        BlockCopy &c = x.copies.c[x.copies.count++];
+        c.src = reinterpret_cast<const uint4 *>(buf) + (m.src_row0 * m.src_wb + m.src_col0) * vec16;
+        strides(m.src_hb, m.src_wb, c, true);
+        c.dst = reinterpret_cast<uint4 *>(B.peer.at(m.peer)) + (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
+        strides(m.dst_hb, m.dst_wb, c, false);
+        c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
+    }
+    for (auto &m : recvs) x.data_in[x.n_data_in++] = pl->flag(pl->flags, which, FLAG_DATA, m.peer);
+    return x;
+}
+
 void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t st) {
     const RankPlan &rp = pl->rp;
     const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
@@ -544,10 +623,6 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
     const int64_t nl = rp.nrange.size();
     BufState &B = pl->buf[which];
     const bool use_nccl = (flags & DC_HALO_NCCL) != 0;
-    if (!use_nccl)
-        DC_REQUIRE(B.ptr == buf, DC_ERR_ARG,
-                   "direct P2P halo exchange needs the buffer from dc_buffer_alloc (or pass "
-                   "DC_HALO_NCCL)");
     auto strides = [&](int64_t hb, int64_t wb, BlockCopy &c, bool src) {
         const long long sw = vec16, sh = wb * vec16, sn = hb * wb * vec16;
         if (src) c.s_sn = sn, c.s_sh = sh, c.s_sw = sw;
@@ -602,24 +677,8 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
     }
     // ---- direct P2P stores into the neighbours' margins + epoch flags ----
     // one kernel: ready handshake, NVLink stores, per-block completion counters
-    // (halo.cu: p2p_exchange_kernel); then a stream wait on my own counters.
-    const int me = rp.rank;
-    DC_REQUIRE(sends.size() <= 8 && recvs.size() <= 8, DC_ERR_ARG, "too many halo neighbours");
-    DC_REQUIRE(B.dev_epoch != nullptr, DC_ERR_ARG, "P2P halo exchange: buffer not registered");
-    P2PExchange x{};
-    x.epoch_ctr = B.dev_epoch;
-    for (auto &m : recvs) x.ready_out[x.n_ready_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_READY, me);
-    for (auto &m : sends) {
-        x.ready_in[x.n_ready_in++] = pl->flag(pl->flags, which, FLAG_READY, m.peer);
-        x.data_out[x.n_data_out++] = pl->flag(pl->peer_flags.at(m.peer), which, FLAG_DATA, me);
-        BlockCopy &c = x.copies.c[x.copies.count++];
-        c.src = reinterpret_cast<const uint4 *>(buf) + (m.src_row0 * m.src_wb + m.src_col0) * vec16;
-        strides(m.src_hb, m.src_wb, c, true);
-        c.dst = reinterpret_cast<uint4 *>(B.peer.at(m.peer)) + (m.dst_row0 * m.dst_wb + m.dst_col0) * vec16;
-        strides(m.dst_hb, m.dst_wb, c, false);
-        c.nn = (int)nl, c.rows = (int)m.rows.size(), c.cols = (int)m.cols.size(), c.vec16 = vec16;
-    }
-    for (auto &m : recvs) x.data_in[x.n_data_in++] = pl->flag(pl->flags, which, FLAG_DATA, m.peer);
+    // (halo.cu: p2p_exchange_kernel), block 0 returns when all data arrived.
+    const P2PExchange x = build_p2p(pl, which, buf);
     launch_p2p_exchange(x, st);
 }
 
@@ -753,7 +812,9 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         L[i].w_base = wt, L[i].w_rows = g.Cp, L[i].w_kcols = (int64_t)std::max(f.T, 1) * g.Fp;
         Split2D s{f.nt_h, f.nt_w, f.bl, f.bh, f.bwl, f.bwh};
         make_rects(s, L[i].interior, L[i].boundary);
-        L[i].work_hint = g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) * L[i].nout_tiles;
+        L[i].work_hint = ceil_div(g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) *
+                                      L[i].nout_tiles,
+                                  (int64_t)pl->splitk_world());
         L[i].ksplit = choose_ksplit(L[i].work_hint, g.Fp);
     }
     // one split-K workspace region per phase: the phases' interior and
@@ -1195,6 +1256,13 @@ dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicte
     DC_API_END
 }
 
+dc_status_t dc_plan_set_splitk_world(dc_plan_t plan, int world) {
+    DC_API_BEGIN
+    DC_REQUIRE(plan && world >= 0, DC_ERR_ARG, "bad argument");
+    plan->ks_world = world;
+    DC_API_END
+}
+
 dc_status_t dc_plan_destroy(dc_plan_t plan) {
     DC_API_BEGIN
     delete plan;
@@ -1254,16 +1322,28 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     }
     const dc_shard_desc_t xd = describe(pl->rp, DC_X);
     const int nl = (int)pl->rp.nrange.size();
-    const bool overlap =
-        (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
-    if (overlap) {
+    const bool need_x = (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
+    static const int no_overlap_env = std::getenv("DC_NO_OVERLAP") ? std::atoi(std::getenv("DC_NO_OVERLAP")) : 0;
+    const bool overlap = need_x && !no_overlap_env;
+    if (need_x && !overlap) {  // exchange, then one launch over the whole shard
+        exchange(pl, 0, x, flags, st);
+        launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
+    } else if (overlap && !(flags & DC_HALO_NCCL) && fused_fwd(pl, L, x, xd, nl, st)) {
+        // one kernel: P2P halo stores + interior tiles, halo-dependent tiles last
+    } else if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
         exchange(pl, 0, x, flags, pl->s_comm);
         // interior tiles on the caller's stream, concurrently with the exchange;
         // the halo-dependent boundary tiles right after it on the comm stream
-        // (disjoint outputs, and disjoint split-K workspace pixels), joined below
+        // (disjoint outputs, and disjoint split-K workspace pixels), joined below.
+        // DC_HALO_RESERVE=k caps the persistent interior grid at SMs - k so the
+        // exchange and the boundary kernel can run beside it.
+        // (measured neutral at 4 GPUs with 8 or 16 reserved SMs: default 0)
+        static const int reserve = std::getenv("DC_HALO_RESERVE") ? std::atoi(std::getenv("DC_HALO_RESERVE")) : 0;
+        L.max_ctas = std::max(1, device_sm_count() - reserve);
         launch_rects(L, L.interior, x, xd, pl->rp.g.Cp, nl, st);
+        L.max_ctas = 0;
         launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));

@@ -1,7 +1,7 @@
 // conv_v2.cu -- persistent tile-reuse implicit-GEMM convolution on sm_100a
 // (forward Eq. 1 PAPER.md:61 and backward-data Eq. 3).
 //
-// Warp roles (192 threads, 1 CTA per SM, persistent over output tiles):
+// Warp roles (224 threads, 1 CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: per tile and channel group, the halo'd input
 //               tile as 16-byte core-matrix planes (one box per 8-channel
 //               chunk and column parity); weights either resident (loaded
@@ -10,8 +10,11 @@
 //               tap, the A descriptor is the same smem tile at a shifted
 //               start address (no data movement per tap).
 //   warps 2-5   epilogue: tcgen05.ld (32 lanes x 16 cols) -> bf16 -> NHWC
-//               global stores; double-buffered TMEM accumulators let the
-//               epilogue of tile i overlap the MMAs of tile i+1.
+//               global stores (+ fused BN statistics); double-buffered TMEM
+//               accumulators let the epilogue of tile i overlap the MMAs of
+//               tile i+1.
+//   warp 6      fused P2P halo exchange (opt-in, ConvV2Params::halo): slices
+//               of this rank's slabs stored into the neighbours' margins.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -151,7 +154,9 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
 }
 
 
-__global__ void __launch_bounds__(192, 1)
+constexpr int kV2Threads = 224;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange
+
+__global__ void __launch_bounds__(kV2Threads, 1)
     conv_v2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvV2Params p) {
     extern __shared__ uint8_t smem_raw[];
@@ -200,6 +205,8 @@ __global__ void __launch_bounds__(192, 1)
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // fused halo exchange: this launch's epoch (published by the last CTA at exit)
+    const uint32_t halo_e = p.halo ? *reinterpret_cast<volatile uint32_t *>(p.hx.epoch_ctr) + 1 : 0u;
     // Work units: a CTA (cluster == 1) or a CTA pair (cluster == 2: tiles 2k and
     // 2k+1 of the same N tile, each CTA loading half of every weight stage and
     // multicasting it to both; an odd tail tile gives the second CTA a phantom
@@ -234,9 +241,23 @@ __global__ void __launch_bounds__(192, 1)
         }
         int cur_o0 = -1;
         int a_it = 0, b_it = 0;
+        bool halo_ready = !p.halo;
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
             const TileCoord c = decode(p, item_of(w, phantom));
+            if (!halo_ready && c.r >= p.halo_rect0) {
+                // the neighbours' slabs of this epoch are in my margins
+                if ((int)lane < p.hx.n_data_in) {
+                    const uint32_t target = kP2PBlocks * halo_e;
+                    uint32_t v;
+                    do {
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.hx.data_in[lane]) : "memory");
+                    } while ((int)(v - target) < 0);
+                }
+                __syncwarp();
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+                halo_ready = true;
+            }
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {
@@ -388,6 +409,41 @@ __global__ void __launch_bounds__(192, 1)
             if (tr) p.dbg_out[acc_it * 8 + 3] = clock64();
             ++acc_it;
         }
+    } else if (warp == 6) {
+        // ===================== fused P2P halo exchange (slices) =====================
+        if (p.halo) {
+            const P2PExchange &x = p.hx;
+            if (blockIdx.x == 0 && (int)lane < x.n_ready_out) {  // my margins are free for epoch e
+                __threadfence_system();
+                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[lane]), "r"(halo_e) : "memory");
+            }
+            for (int sl = blockIdx.x; sl < kP2PBlocks; sl += gridDim.x) {
+                if ((int)lane < x.n_ready_in) {
+                    uint32_t v;
+                    do {
+                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.ready_in[lane]) : "memory");
+                    } while ((int)(v - halo_e) < 0);
+                }
+                __syncwarp();
+                for (int k = 0; k < x.copies.count; ++k) {
+                    const BlockCopy &cp = x.copies.c[k];
+                    const long long run = (long long)cp.cols * cp.vec16;
+                    const long long tot = (long long)cp.nn * cp.rows * run;
+                    const long long hi = tot * (sl + 1) / kP2PBlocks;
+                    for (long long idx = tot * sl / kP2PBlocks + lane; idx < hi; idx += 32) {
+                        const long long nr = idx / run, kk = idx - nr * run;
+                        const int n = (int)(nr / cp.rows), r = (int)(nr - (long long)n * cp.rows);
+                        const int col = (int)(kk / cp.vec16), v = (int)(kk - (long long)col * cp.vec16);
+                        cp.dst[n * cp.d_sn + r * cp.d_sh + col * cp.d_sw + v] =
+                            cp.src[n * cp.s_sn + r * cp.s_sh + col * cp.s_sw + v];
+                    }
+                }
+                __syncwarp();
+                __threadfence_system();
+                __syncwarp();
+                if ((int)lane < x.n_data_out) atomicAdd_system(x.data_out[lane], 1u);
+            }
+        }
     } else {
         // ========================= epilogue =========================
         const int eq = warp & 3;  // TMEM lane quarter this warp may access
@@ -499,6 +555,14 @@ __global__ void __launch_bounds__(192, 1)
     else
         __syncthreads();
     if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (p.halo && threadIdx.x == 0) {  // the last CTA publishes the epoch and resets the count
+        const uint32_t prev = atomicAdd(p.hx.epoch_ctr + 1, 1u);
+        if (prev == gridDim.x - 1) {
+            p.hx.epoch_ctr[1] = 0;
+            __threadfence();
+            *reinterpret_cast<volatile uint32_t *>(p.hx.epoch_ctr) = halo_e;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -688,7 +752,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
             cfg.gridDim = dim3(2 * (device_sm_count() / 2));
-            cfg.blockDim = dim3(192);
+            cfg.blockDim = dim3(kV2Threads);
             cfg.dynamicSmemBytes = smem;
             cfg.attrs = at, cfg.numAttrs = 1;
             int n = 0;
@@ -698,13 +762,14 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         }
         const int per_o = p.nsamples * p.rect_start[p.nrect];
         const int total_w = p.nout_tiles * ((per_o + 1) / 2);
-        const int units = p.ksplit * std::max(1, std::min(total_w, max_clusters[smem] / p.ksplit));
+        const int cap_units = p.max_ctas > 0 ? std::min(max_clusters[smem], p.max_ctas / 2) : max_clusters[smem];
+        const int units = p.ksplit * std::max(1, std::min(total_w, cap_units / p.ksplit));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute at[1];
         at[0].id = cudaLaunchAttributeClusterDimension;
         at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3(2 * units);
-        cfg.blockDim = dim3(192);
+        cfg.blockDim = dim3(kV2Threads);
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cfg.attrs = at, cfg.numAttrs = 1;
@@ -713,13 +778,14 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         ++g_launches;
         return 2 * units;
     }
-    const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, device_sm_count() / p.ksplit));
+    const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, device_sm_count()) : device_sm_count();
+    const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, sms / p.ksplit));
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
         DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER");
         ConvV2Params q = p;
         cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
         cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));
-        conv_v2_kernel<<<grid, 192, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
+        conv_v2_kernel<<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
         cudaStreamSynchronize(st);
         long long h[64 * 8];
         cudaMemcpy(h, q.dbg_out, sizeof h, cudaMemcpyDeviceToHost);
@@ -731,7 +797,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
                     h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
                     h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
     } else {
-        conv_v2_kernel<<<grid, 192, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
+        conv_v2_kernel<<<grid, kV2Threads, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
     }
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include "conv_tc.cuh"
+#include "halo.cuh"
 
 namespace dc {
 
@@ -52,6 +53,15 @@ struct ConvV2Params {
     // bn_part[blockIdx.x][2][nout_p] (needs ksplit == 1 and nout_tiles == 1)
     int bn_stats;
     double *bn_part;
+    // Fused P2P halo exchange of the input (one kernel per GPU):
+    // warp 6 of the CTAs holding slice s (s = blockIdx.x, + gridDim.x, ... <
+    // kP2PBlocks) stores slice s of this rank's slabs into the neighbours'
+    // mapped margins after their ready flags, then bumps their data counters;
+    // the TMA producer waits for all neighbours' data (acquire + async-proxy
+    // fence) before the first tile of a rect >= halo_rect0, which are the
+    // tiles that read the margins (scheduled last).
+    int halo, halo_rect0;
+    P2PExchange hx;
     int s_in;                  // A element stride (conv stride for fwd, 1 for bwd-data)
     int origin_h, origin_w;    // input coord of GEMM pixel (0,0) at tap offset 0
     int T;                     // taps
@@ -78,6 +88,7 @@ struct ConvV2Params {
     // global layer shape, so partitioned results stay bitwise equal to 1 GPU.
     int ksplit;
     int work_hint;             // work items of THIS launch at tpw = 1 (x ksplit): pairing only when plentiful
+    int max_ctas;              // host: persistent grid cap (0: SM count)
     int cluster;               // 2: CTA pairs share (multicast) every streamed weight stage; 1: none
     int allow_cg32;            // stride 2: may narrow 64-channel stages to 32 for tile pairs (changes the
                                // summation order: decided from the GLOBAL layer, see capi.cu)

@@ -278,9 +278,13 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
         __threadfence_system();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // the last block publishes the epoch and resets the count
         const uint32_t prev = atomicAdd(x.epoch_ctr + 1, 1u);
-        if (prev == kP2PBlocks * e - 1) *reinterpret_cast<volatile uint32_t *>(x.epoch_ctr) = e;
+        if (prev == gridDim.x - 1) {
+            x.epoch_ctr[1] = 0;
+            __threadfence();
+            *reinterpret_cast<volatile uint32_t *>(x.epoch_ctr) = e;
+        }
     }
 }
 

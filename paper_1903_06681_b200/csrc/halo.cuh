@@ -71,8 +71,10 @@ struct P2PExchange {
     uint32_t *data_in[8];    // my counters written by the peers that send to me
     int n_ready_out, n_ready_in, n_data_out, n_data_in;
     // device epoch of this (plan, buffer): {epoch, blocks done}. Every block
-    // reads epoch + 1 at start; the last block to finish publishes it (so the
-    // launch can be replayed from a CUDA graph)
+    // reads epoch + 1 at start; the last block to finish publishes it and
+    // resets the count (so the launch can be replayed from a CUDA graph; the
+    // fused conv_v2 exchange uses the same words). Each epoch adds kP2PBlocks
+    // to every receiver's data counter (32 blocks, or 32 slices when fused).
     uint32_t *epoch_ctr;
 };
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);

@@ -38,12 +38,15 @@ def make_inputs(N, C, H, W, F, K, S, P):
     return x, w, dy
 
 
-def run_layer(dc, shape, decomp=(1, 1, 1), rank=0, x=None, w=None, dy=None, virtual=True):
+def run_layer(dc, shape, decomp=(1, 1, 1), rank=0, x=None, w=None, dy=None, virtual=True, ks_world=0):
     """Forward, backward-data and backward-filter of one rank's shard
-    (halo rows filled by the test from the global tensor: no exchange)."""
+    (halo rows filled by the test from the global tensor: no exchange).
+    ks_world: dc_plan_set_splitk_world (0: the plan's grid size)."""
     N, C, H, W, F, K, S, P = shape
     plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, decomp, rank)
     try:
+        if ks_world:
+            dc.dc_plan_set_splitk_world(plan, ks_world)
         xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
         dyd, dxd = dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(plan, dc.DC_DX)
         xb = fill_buffer(x, xd)
@@ -112,19 +115,24 @@ GRIDS = [(1, 2, 1), (1, 1, 2), (1, 2, 2), (2, 2, 1), (1, 3, 1), (1, 4, 2)]
 @pytest.mark.parametrize("grid", GRIDS)
 def test_partition_bitwise(dc, shape, grid):
     """Every rank's owned y and dx from its own margined shard is bitwise equal
-    to the unpartitioned result of the same kernel (north_star); the sum of
-    the per-rank dW partials equals the 1-GPU dW within the fp32 bar."""
+    to the unpartitioned result of the same kernel configuration (north_star:
+    the 1-GPU plan set to the partition's split-K basis,
+    dc_plan_set_splitk_world(P)); that 1-GPU result matches the oracle; the
+    sum of the per-rank dW partials equals the 1-GPU dW within the fp32 bar."""
     N, C, H, W, F, K, S, P = shape
     try:
         dc.dc_plan_destroy(dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, grid, 0))
     except dc.DCError:
         pytest.skip("grid invalid for this shape")
     x, w, dy = make_inputs(*shape)
-    full = run_layer(dc, shape, x=x, w=w, dy=dy)
+    nranks = grid[0] * grid[1] * grid[2]
+    full = run_layer(dc, shape, x=x, w=w, dy=dy, ks_world=nranks)
+    y_ref = oracle.conv_fwd(x, w, S, P)
+    assert rel_l2(owned_nchw(full["y"], full["yd"]), y_ref) <= TOL_L2_DERIVED
     Y = full["y"].float().cpu()
     DX = full["dx"].float().cpu()
     dw_sum = torch.zeros_like(full["dw"])
-    for rank in range(grid[0] * grid[1] * grid[2]):
+    for rank in range(nranks):
         r = run_layer(dc, shape, grid, rank, x=x, w=w, dy=dy)
         yd, dxd = r["yd"], r["dxd"]
         ys = Y[yd["n0"]:yd["n0"] + yd["n"], yd["h0"]:yd["h0"] + yd["h"], yd["w0"]:yd["w0"] + yd["w"]]

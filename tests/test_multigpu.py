@@ -34,8 +34,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, errq):
+def _worker(rank, world, port, errq, env=None):
     try:
+        os.environ.update(env or {})
         import sys
         root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
         sys.path.insert(0, root)
@@ -54,6 +55,7 @@ def _worker(rank, world, port, errq):
             x, w, dy = datagen.gen_x(N, C, H, W), datagen.gen_w(F, C, K), datagen.gen_dy(N, F, Ho, Wo)
             # 1-GPU reference of the same kernels on this device
             ref = dc.dc_plan_create(N, C, H, W, F, K, S, P, (1, 1, 1), dc.DC_BF16, None)
+            dc.dc_plan_set_splitk_world(ref, world)  # same summation order as the partition
             rx, ry = dc.dc_plan_query(ref, dc.DC_X), dc.dc_plan_query(ref, dc.DC_Y)
             rdy, rdx = dc.dc_plan_query(ref, dc.DC_DY), dc.dc_plan_query(ref, dc.DC_DX)
             wb = weights_gpu(w, rx["c_pad"])
@@ -188,15 +190,17 @@ def _worker(rank, world, port, errq):
         raise
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_multigpu_parity(world):
+@pytest.mark.parametrize("world,env", [(2, None), (4, None), (2, {"DC_FUSED_HALO": "1"})])
+def test_multigpu_parity(world, env):
+    """env DC_FUSED_HALO=1: the forward exchanges its halo inside the conv
+    kernel (conv_v2 warp 6) instead of a separate exchange launch."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     errq = ctx.SimpleQueue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, errq)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, errq, env)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
