@@ -91,6 +91,8 @@ struct dc_plan_s {
     bool bn_comm_owned = false;
     int bn_group = 1;
     cudaStream_t s_comm = nullptr;
+    cudaStream_t s_ph[4] = {nullptr, nullptr, nullptr, nullptr};  // stride-phase streams (bwd-data)
+    cudaEvent_t ev_ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     BufState buf[2];                 // 0: X, 1: DY
     uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
@@ -129,6 +131,10 @@ struct dc_plan_s {
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         if (s_comm) cudaStreamDestroy(s_comm);
+        for (auto sp : s_ph)
+            if (sp) cudaStreamDestroy(sp);
+        for (auto e : ev_ph)
+            if (e) cudaEventDestroy(e);
         if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
     }
     int world() const { return rp.grid.size(); }
@@ -782,6 +788,23 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             wt_need += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
         }
     ensure_alloc(pl->wt, pl->wt_bytes, wt_need);
+    {   // the rotated / transposed weights of every active phase in one launch
+        int8_t ka[kMaxTaps], kb[kMaxTaps];
+        int Ts[kMaxTaps], ts[kMaxTaps];
+        long long offs[kMaxTaps];
+        int nt = 0;
+        size_t o = 0;
+        for (auto &f : ph) {
+            if (f.active)
+                for (int t = 0; t < f.T; ++t) {
+                    ka[nt] = f.ka[t], kb[nt] = f.kb[t], Ts[nt] = f.T, ts[nt] = t, offs[nt] = (long long)(o / 2);
+                    ++nt;
+                }
+            o += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+        }
+        launch_weight_transform_multi(reinterpret_cast<const __nv_bfloat16 *>(w), pl->wt, (int)g.F, (int)g.Fp,
+                                      (int)g.C, (int)g.Cp, g.K, nt, ka, kb, Ts, ts, offs, st);
+    }
     std::vector<GemmLaunch> L(ph.size());
     size_t off = 0;
     for (size_t i = 0; i < ph.size(); ++i) {
@@ -789,9 +812,6 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         __nv_bfloat16 *wt = pl->wt + off / 2;
         off += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
         if (!f.active) continue;
-        if (f.T > 0)
-            launch_weight_transform(reinterpret_cast<const __nv_bfloat16 *>(w), wt, (int)g.F,
-                                    (int)g.Fp, (int)g.C, (int)g.Cp, g.K, f.T, f.ka, f.kb, st);
         ConvGemmParams &p = L[i].p;
         std::memset(&p, 0, sizeof p);
         p.bkc = pick_bkc(g.Fp);
@@ -837,6 +857,25 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
         exchange(pl, 1, dy, flags, pl->s_comm);
+    }
+    int nactive = 0;
+    for (auto &f : ph) nactive += f.active ? 1 : 0;
+    static const bool serial_phases = std::getenv("DC_SERIAL_PHASES") != nullptr;
+    if (!overlap && nactive > 1 && !serial_phases) {
+        // stride phases are independent GEMMs with disjoint outputs and split-K
+        // workspaces: one stream each, so their ramp-up / tail / reduce overlap
+        CK(cudaEventRecord(pl->ev_ph[0], st));
+        int k = 0;
+        for (size_t i = 0; i < ph.size(); ++i) {
+            if (!ph[i].active) continue;
+            cudaStream_t sp = pl->s_ph[k];
+            CK(cudaStreamWaitEvent(sp, pl->ev_ph[0], 0));
+            launch_rects(L[i], {whole(L[i])}, dy, dyd, g.Fp, (int)rp.nrange.size(), sp);
+            CK(cudaEventRecord(pl->ev_ph[1 + k], sp));
+            ++k;
+        }
+        for (int j = 0; j < k; ++j) CK(cudaStreamWaitEvent(st, pl->ev_ph[1 + j], 0));
+        return;
     }
     for (size_t i = 0; i < ph.size(); ++i) {
         if (!ph[i].active) continue;
@@ -1022,6 +1061,8 @@ void ensure_local_resources(dc_plan_s *pl) {
     if (pl->s_comm) return;
     CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
     for (auto &e : pl->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto &sp : pl->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
+    for (auto &e : pl->ev_ph) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 4 * pl->rp.g.Fp));  // local sums, global sums
 }
 

@@ -301,8 +301,10 @@ __global__ void splitk_reduce_kernel(const float4 *__restrict__ ws, int splits, 
     }
 }
 
-struct TapTable {
-    int8_t a[kMaxTaps], b[kMaxTaps];
+struct TapTable {  // grid.z = tap j (of any stride phase)
+    int8_t a[kMaxTaps], b[kMaxTaps];  // source tap of w
+    uint8_t T[kMaxTaps], t[kMaxTaps];  // its phase's tap count and index in it
+    int off[kMaxTaps];                 // element offset of its phase's [Cp][T][Fp] block
 };
 
 // Backward-data weights: wt[c][t][f] = w[f][a_t][b_t][c].
@@ -310,12 +312,14 @@ struct TapTable {
 // w[f][a][b][c] (c contiguous) and the write of wt[c][t][f] (f contiguous) are
 // coalesced. grid = (ceil(Cp/32), ceil(Fp/32), T), block = 32 x 8.
 __global__ void weight_transform_kernel(const __nv_bfloat16 *__restrict__ w,
-                                        __nv_bfloat16 *__restrict__ wt, int F, int Fp, int C,
-                                        int Cp, int K, int T, const __grid_constant__ TapTable tt) {
+                                        __nv_bfloat16 *__restrict__ wt_base, int F, int Fp, int C,
+                                        int Cp, int K, const __grid_constant__ TapTable tt) {
     __shared__ __nv_bfloat16 tile[32][33];
-    const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 32, t = blockIdx.z;
+    const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 32, j = blockIdx.z;
+    const int T = tt.T[j], t = tt.t[j];
+    __nv_bfloat16 *__restrict__ wt = wt_base + tt.off[j];
     const int tx = threadIdx.x, ty = threadIdx.y;
-    const long long tap_off = ((long long)tt.a[t] * K + tt.b[t]) * Cp;
+    const long long tap_off = ((long long)tt.a[j] * K + tt.b[j]) * Cp;
     for (int r = ty; r < 32; r += 8) {
         const int f = f0 + r, c = c0 + tx;
         __nv_bfloat16 v = __float2bfloat16(0.0f);
@@ -428,18 +432,31 @@ void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, c
     ++g_launches;
 }
 
+void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_base, int F, int Fp, int C, int Cp,
+                                   int K, int ntaps, const int8_t *ka, const int8_t *kb, const int *T,
+                                   const int *t, const long long *off, cudaStream_t st) {
+    if (ntaps == 0) return;
+    DC_REQUIRE(ntaps <= kMaxTaps, DC_ERR_ARG, "too many taps");
+    TapTable tt{};
+    for (int j = 0; j < ntaps; ++j) {
+        tt.a[j] = ka[j], tt.b[j] = kb[j];
+        tt.T[j] = (uint8_t)T[j], tt.t[j] = (uint8_t)t[j];
+        DC_REQUIRE(off[j] < (1LL << 31), DC_ERR_ARG, "weight block too large");
+        tt.off[j] = (int)off[j];
+    }
+    weight_transform_kernel<<<dim3((Cp + 31) / 32, (Fp + 31) / 32, ntaps), dim3(32, 8), 0, st>>>(
+        w, wt_base, F, Fp, C, Cp, K, tt);
+    CUDA_OK(cudaGetLastError());
+    ++g_launches;
+}
+
 void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C,
                              int Cp, int K, int T, const int8_t *ka, const int8_t *kb,
                              cudaStream_t st) {
-    TapTable tt{};
-    for (int t = 0; t < T; ++t) {
-        tt.a[t] = ka[t];
-        tt.b[t] = kb[t];
-    }
-    weight_transform_kernel<<<dim3((Cp + 31) / 32, (Fp + 31) / 32, T), dim3(32, 8), 0, st>>>(
-        w, wt, F, Fp, C, Cp, K, T, tt);
-    CUDA_OK(cudaGetLastError());
-    ++g_launches;
+    int Ts[kMaxTaps], ts[kMaxTaps];
+    long long off[kMaxTaps];
+    for (int i = 0; i < T; ++i) Ts[i] = T, ts[i] = i, off[i] = 0;
+    launch_weight_transform_multi(w, wt, F, Fp, C, Cp, K, T, ka, kb, Ts, ts, off, st);
 }
 
 }  // namespace dc

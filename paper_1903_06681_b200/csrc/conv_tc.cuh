@@ -72,6 +72,11 @@ void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradP
                   int m_tiles, int n_tiles, cudaStream_t st);
 void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, cudaStream_t st);
 // W'[c][t][f] = w[f][ka[t]][kb[t]][c] for the backward-data taps (zero if c >= C or f >= F)
+// All stride phases at once: tap j (of ntaps) reads w tap (ka[j], kb[j]) and
+// writes index t[j] of its phase's [Cp][T[j]][Fp] block at wt_base + off[j].
+void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_base, int F, int Fp, int C, int Cp,
+                                   int K, int ntaps, const int8_t *ka, const int8_t *kb, const int *T,
+                                   const int *t, const long long *off, cudaStream_t st);
 void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C,
                              int Cp, int K, int T, const int8_t *ka, const int8_t *kb,
                              cudaStream_t st);
