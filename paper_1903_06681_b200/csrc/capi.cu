@@ -901,7 +901,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
 // split costs one more fp32 partial of dW written and read back by the reduce.
 int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split) {
     const int sms = device_sm_count();
-    const double mma_ns = 4.0 * q.G * (27.0 + 0.41 * q.bn) / 1.9;
+    const double mma_ns = (q.bw / 2) * q.G * (27.0 + 0.41 * q.bn) / 1.9;
     const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
     int best = 1;
     double best_t = 1e30;
@@ -937,7 +937,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
         q.F = (int)g.F, q.Fp = (int)g.Fp, q.cp = (int)g.Cp;
         if (wgrad_v2_configure(q, kV2SmemLimit)) {
             q.tiles_h = (int)ceil_div(ho, 8);
-            q.tiles_w = (int)ceil_div(wo, 8);
+            q.tiles_w = (int)ceil_div(wo, (int64_t)q.bw);
             q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
             const int mgroups = wgrad_v2_mgroups(q), ntiles = (int)ceil_div(g.Fp, q.bn);
             const long long per_split = (long long)g.F * q.T * g.Cp;
@@ -963,7 +963,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
                 const uint64_t dims[4] = {(uint64_t)g.Fp, (uint64_t)wo, (uint64_t)ho, (uint64_t)nl};
                 const uint64_t strides[3] = {(uint64_t)(g.Fp * 2), (uint64_t)(dyd.wb * g.Fp * 2),
                                              (uint64_t)(dyd.hb * dyd.wb * g.Fp * 2)};
-                const uint32_t box[4] = {64, 8, 8, 1};
+                const uint32_t box[4] = {64, (uint32_t)q.bw, 8, 1};
                 make_tmap(&dymap, dy_owned, 4, dims, strides, box, nullptr, 128);
             }
             launch_wgrad_v2(xmap, dymap, q, st);

@@ -3,7 +3,7 @@
 //   D[(tap, c), f] = sum over the owned output pixels of X_tap[pixel, c] * DY[pixel, f]
 // K = output pixels, processed in blocks of 8 output rows x 8 output cols.
 // For each block the x tile that ALL taps read is loaded once into shared
-// memory (swizzled rows of cgw channels, row pitch 8+(kw-1)/s pixels, one plane per
+// memory (swizzled rows of cgw channels, row pitch bw+(kw-1)/s pixels, one plane per
 // column parity for stride 2). An "MN atom" of the A operand is cgw channels
 // of one tap, i.e. the same tile at a shifted start address; an M = 128 tile
 // stacks 128/cgw atoms at a uniform distance (LBO):
@@ -17,6 +17,7 @@
 // partial sums go to a workspace reduced in a fixed order
 // (splitk_reduce_kernel) -> deterministic.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.hpp"
@@ -77,15 +78,30 @@ constexpr int kWMaxStages = 8;
 
 // The MMAs of one pixel block: G M tiles x 4 K16 steps, fully unrolled (the
 // descriptors are loop-invariant per CTA; only the stage offset moves).
-template <int G>
+template <int G, int NKS>
 __device__ __forceinline__ void wgrad_issue(uint32_t tmem, const uint64_t (&adesc)[8], uint32_t xo, uint64_t bd,
                                             uint32_t ak16, uint32_t acc_cols, uint32_t idesc, bool first) {
 #pragma unroll
     for (int i = 0; i < G; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)  // 64 pixels = 4 x K16 (2 output rows each)
+        for (int k = 0; k < NKS; ++k)  // NKS x K16 steps of 16 pixels each
             mma_bf16(tmem + i * acc_cols, adesc[i] + xo + k * ak16, bd + k * (2048 >> 4), idesc,
                      (first && k == 0) ? 0u : 1u);
+}
+template <int NKS>
+__device__ __forceinline__ void wgrad_issue_g(int G, uint32_t tmem, const uint64_t (&adesc)[8], uint32_t xo,
+                                              uint64_t bd, uint32_t ak16, uint32_t acc_cols, uint32_t idesc,
+                                              bool first) {
+    switch (G) {
+    case 1: wgrad_issue<1, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 2: wgrad_issue<2, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 3: wgrad_issue<3, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 4: wgrad_issue<4, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 5: wgrad_issue<5, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 6: wgrad_issue<6, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 7: wgrad_issue<7, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    default: wgrad_issue<8, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    }
 }
 
 __global__ void __launch_bounds__(192, 1)
@@ -145,13 +161,13 @@ __global__ void __launch_bounds__(192, 1)
         }
         const int per_n = p.tiles_h * p.tiles_w;
         const uint32_t x_bytes = ncg * p.s_in * p.PH * p.pitch * p.cgw * 2;  // bytes the boxes deliver
-        const uint32_t d_bytes = (p.bn / 64) * 64 * 64 * 2;
+        const uint32_t d_bytes = (p.bn / 64) * 8 * p.bw * 128;
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % p.stages;
             if (kb >= p.stages) mbar_wait(&empty[s], ((kb / p.stages) - 1) & 1);
             const int blk = b_begin + kb;
             const int n = blk / per_n, rem = blk - n * per_n;
-            const int i0 = (rem / p.tiles_w) * 8, j0 = (rem % p.tiles_w) * 8;
+            const int i0 = (rem / p.tiles_w) * 8, j0 = (rem % p.tiles_w) * p.bw;
             if (elect_one()) {
                 mbar_arrive_expect_tx(&full[s], x_bytes + d_bytes);
                 uint8_t *xs = sX + s * p.x_stage_bytes;
@@ -162,7 +178,7 @@ __global__ void __launch_bounds__(192, 1)
                                     (cg_lo + c) * p.cgw, w0 + par, h0, n);
                 uint8_t *ds = sD + s * p.dy_stage_bytes;
                 for (int q = 0; q < p.bn / 64; ++q)
-                    tma_load_4d(ds + q * 64 * 64 * 2, &dymap, &full[s], f0 + q * 64, j0, i0, n);
+                    tma_load_4d(ds + q * 8 * p.bw * 128, &dymap, &full[s], f0 + q * 64, j0, i0, n);
             }
             __syncwarp();
         }
@@ -170,7 +186,10 @@ __global__ void __launch_bounds__(192, 1)
         // ===================== tcgen05.mma issuer (warp-uniform) =====================
         // A (x, MN-major, swizzle = cgw*2 bytes): K rows = 8 output pixels of one
         // output row (cgw*2 bytes each); SBO = next output row; LBO = next atom.
-        const uint32_t a_sbo = p.s_in * p.pitch * p.cgw * 2;
+        // K rows = pixels: 8-pixel groups (SBO) are the next 8 output pixels of a
+        // row (bw = 16) or the next output row (bw = 8); a K16 step is 16 pixels
+        const uint32_t row_bytes = p.s_in * p.pitch * p.cgw * 2;
+        const uint32_t a_sbo = p.bw == 16 ? 8 * p.cgw * 2 : row_bytes;
         const uint32_t layout = swizzle_layout(p.cgw * 2);
         uint64_t adesc[8];
 #pragma unroll
@@ -191,10 +210,10 @@ __global__ void __launch_bounds__(192, 1)
         }
         // B (dy, MN-major SW128): atom = 64 filters; K rows = 8 pixels x 128 B;
         // SBO = 1024 (next 8 pixels = next output row), LBO = next 64 filters.
-        const uint64_t bdesc0 = smem_desc(smem_u32(sD), 64 * 64 * 2, 1024, 2);
+        const uint64_t bdesc0 = smem_desc(smem_u32(sD), 8 * p.bw * 128, 1024, 2);
         const uint32_t idesc = idesc_bf16(128, p.bn, 1, 1);
         const uint32_t acc_cols = p.bn_cols;
-        const uint32_t ak16 = (2 * a_sbo) >> 4;
+        const uint32_t ak16 = (p.bw == 16 ? row_bytes : 2 * row_bytes) >> 4;
         const uint32_t xstep = (uint32_t)p.x_stage_bytes >> 4, dstep = (uint32_t)p.dy_stage_bytes >> 4;
         int s = 0;
         uint32_t ph = 0, xo = 0;
@@ -203,16 +222,10 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             if (elect_one()) {
-                switch (G) {
-                case 1: wgrad_issue<1>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 2: wgrad_issue<2>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 3: wgrad_issue<3>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 4: wgrad_issue<4>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 5: wgrad_issue<5>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 6: wgrad_issue<6>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                case 7: wgrad_issue<7>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                default: wgrad_issue<8>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0); break;
-                }
+                if (p.bw == 16)
+                    wgrad_issue_g<8>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
+                else
+                    wgrad_issue_g<4>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
                 mma_commit(&empty[s]);
             }
             __syncwarp();
@@ -302,12 +315,21 @@ bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
     // row pitch = the 8 + (kw-1)/s columns one parity plane needs; the
     // swizzle is a function of the smem address, so rows need not start on
     // a swizzle-atom boundary (only 16-byte alignment)
-    p.pitch = 8 + (p.kw - 1) / p.s_in;
+    // pixel blocks of 8 rows x bw columns (16 by default: half the barrier
+    // round trips per pixel and fewer halo columns than 8 x 8)
+    static const bool bw8 = std::getenv("DC_WGRAD_BW8") != nullptr;
+    p.bw = bw8 ? 8 : 16;
+    p.pitch = p.bw + (p.kw - 1) / p.s_in;
     p.x_plane_bytes = (p.PH * p.pitch * p.cgw * 2 + 1023) / 1024 * 1024;
     p.bn = p.Fp <= 256 ? p.Fp : 256;
     p.bn_cols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
     p.G = std::max(1, std::min(8, 512 / p.bn_cols));
-    p.dy_stage_bytes = (p.bn / 64) * 64 * 64 * 2;
+    if (p.mode != 2) {  // equal groups per channel group (e.g. 5 M tiles: 3 + 2, not 4 + 1):
+        // the largest group sets the time, the loads are paid per group
+        const int per_cg = p.n_mtiles / p.ncg;
+        p.G = (per_cg + (per_cg + p.G - 1) / p.G - 1) / ((per_cg + p.G - 1) / p.G);
+    }
+    p.dy_stage_bytes = (p.bn / 64) * 8 * p.bw * 128;
     const int fixed = 1024 + (2 * kWMaxStages + 1) * 8 + 16;
     for (;;) {
         const int ncg_stage = p.mode == 2 ? std::min(p.ncg, 2 * p.G) : 1;

@@ -11,12 +11,13 @@ struct WgradV2Params {
     int kh, kw, T;                 // tap grid (T = kh * kw)
     int cgw, ncg, mode;            // channel-group width (16/32/64), groups, M-tile mode (see .cu)
     int PH;                        // x tile rows = s_in * 7 + kh (+ phantom rows, mode 1)
+    int bw;                        // pixel block = 8 output rows x bw (8 or 16) columns
     int pitch;                     // pixels per tile row (per parity plane)
     int x_plane_bytes;             // PH * pitch * cgw * 2 B, rounded up to 1 KB
     int x_stage_bytes, dy_stage_bytes, stages;
     int bn, bn_cols;               // N tile (filters) and its TMEM column stride
     int n_mtiles, G;               // M = 128 tiles (atoms stacked), M tiles per CTA
-    int tiles_h, tiles_w, nblocks; // 8x8 output-pixel blocks per sample, total
+    int tiles_h, tiles_w, nblocks; // 8 x bw output-pixel blocks per sample, total
     int splits;
     float *ws;                     // [splits][F][T][cp] fp32
     long long ws_split;
