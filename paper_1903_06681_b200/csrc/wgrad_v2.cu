@@ -292,7 +292,7 @@ int wgrad_v2_mgroups(const WgradV2Params &p) {
     return p.ncg * ((per_cg + p.G - 1) / p.G);
 }
 
-bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
+static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
     if (p.Fp % 64 != 0 || p.kh * p.kw != p.T) return false;
     p.cgw = p.cp % 64 == 0 ? 64 : p.cp % 32 == 0 ? 32 : 16;
     p.ncg = p.cp / p.cgw;
@@ -317,8 +317,7 @@ bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
     // a swizzle-atom boundary (only 16-byte alignment)
     // pixel blocks of 8 rows x bw columns (16 by default: half the barrier
     // round trips per pixel and fewer halo columns than 8 x 8)
-    static const bool bw8 = std::getenv("DC_WGRAD_BW8") != nullptr;
-    p.bw = bw8 ? 8 : 16;
+    p.bw = bw;
     p.pitch = p.bw + (p.kw - 1) / p.s_in;
     p.x_plane_bytes = (p.PH * p.pitch * p.cgw * 2 + 1023) / 1024 * 1024;
     p.bn = p.Fp <= 256 ? p.Fp : 256;
@@ -339,6 +338,16 @@ bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
         p.G /= 2;
     }
     return p.stages >= 2;
+}
+
+bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
+    // 8 x 16 pixel blocks unless two stages of them do not fit (stride 2 with
+    // 256-filter tiles), then 8 x 8
+    static const bool bw8 = std::getenv("DC_WGRAD_BW8") != nullptr;
+    const WgradV2Params in = p;
+    if (!bw8 && wgrad_v2_configure_bw(p, smem_limit, 16)) return true;
+    p = in;
+    return wgrad_v2_configure_bw(p, smem_limit, 8);
 }
 
 void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const WgradV2Params &p,
