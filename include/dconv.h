@@ -83,6 +83,11 @@ typedef struct dc_plan_s *dc_plan_t;
                                   the epilogue (per-CTA fp64 partials); the next
                                   dc_bn_spatial_stats on that y reduces them instead of
                                   re-reading y (same result up to fp64 summation order) */
+#define DC_DETERMINISTIC 0x20u /* conv_bwd_filter / conv_bwd: sum the split-K partials of
+                                  dW in a fixed order (bitwise reproducible). Default:
+                                  the splits add into dW with fp32 atomics (faster;
+                                  last-bit differences between runs). y and dx are
+                                  always reproducible. */
 #define DC_ALLREDUCE_ASYNC 0x8u /* with DC_ALLREDUCE: queue the dW allreduce on the
                                   communicator's gradient stream instead of joining it
                                   into the call (overlaps the later layers' work,

@@ -20,7 +20,8 @@ STATUS_NAMES = ["DC_OK", "DC_ERR_ARG", "DC_ERR_SHAPE", "DC_ERR_PARTITION", "DC_E
                 "DC_ERR_CUDA", "DC_ERR_COMM", "DC_ERR_OOM"]
 DC_BF16, DC_FP32_3XTF32 = 0, 1
 DC_X, DC_Y, DC_DY, DC_DX, DC_W, DC_DW = range(6)
-DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS = 0x1, 0x2, 0x4, 0x8, 0x10
+DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DETERMINISTIC = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)

@@ -899,11 +899,15 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
 // 8x8 pixel block (MMA 128xNx16 ~ 27 + 0.41 N cycles, measured with
 // tools/mbar_bench.cu), CTAs beyond one per SM run in further waves, and every
 // split costs one more fp32 partial of dW written and read back by the reduce.
-int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split) {
+// Returns the split count; *atomic tells whether the splits should add into dW
+// with fp32 reductions (allowed unless DC_DETERMINISTIC) rather than through
+// partials + the fixed-order reduce launch, whichever the model finds cheaper.
+int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split, bool allow_atomic, bool *atomic) {
     const int sms = device_sm_count();
     const double mma_ns = (q.bw / 2) * q.G * (27.0 + 0.41 * q.bn) / 1.9;
     const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
     int best = 1;
+    bool best_atomic = false;
     double best_t = 1e30;
     for (int s = 1; s <= std::min(q.nblocks, 256); ++s) {
         if ((size_t)s * per_split * 4 > ((size_t)1 << 30)) break;
@@ -911,14 +915,26 @@ int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split) {
         const double bw = std::min(200.0, 7000.0 / (double)active);  // GB/s = bytes/ns per SM
         const double blk_ns = std::max(mma_ns, stage_bytes / bw);
         const long long waves = ceil_div((long long)ctas * s, (long long)sms);
-        double t = (double)waves * (double)ceil_div((long long)q.nblocks, (long long)s) * blk_ns;
-        t += s > 1 ? 2.0 * s * 4.0 * (double)per_split / 6500.0 + 3000.0 : 0.0;
-        if (t < best_t * 0.97) best_t = t, best = s;
+        const double t0 = (double)waves * (double)ceil_div((long long)q.nblocks, (long long)s) * blk_ns;
+        // partials written + read by the reduce launch (HBM), or fp32 reductions
+        // in L2 (~1.5 TB/s effective, measured on 9.4 MB dW) after a memset
+        const double t_red = s > 1 ? 2.0 * s * 4.0 * (double)per_split / 6500.0 + 3000.0 : 0.0;
+        const double t_atm = s > 1 ? s * 4.0 * (double)per_split / 1500.0 + 1000.0 : 0.0;
+        // measured: atomics win for small dW (conv1_2 129 -> 109 us, its quarter
+        // shard 64 -> 50 us) and lose for the 9.4 MB dW of the 512-channel
+        // layers (49 -> 56 us), where the model's two estimates are too close
+        // to call -- decide by size, count splits with the reduce model
+        const bool use_atm = allow_atomic && s > 1 && per_split < (1LL << 20);
+        (void)t_atm;
+        const double t = t0 + t_red;
+        if (t < best_t * 0.97) best_t = t, best = s, best_atomic = use_atm;
     }
+    *atomic = best_atomic;
     return best;
 }
 
-void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cudaStream_t st) {
+void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cudaStream_t st,
+                    bool deterministic) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t xd = describe(rp, DC_X), dyd = describe(rp, DC_DY);
@@ -941,10 +957,17 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
             q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
             const int mgroups = wgrad_v2_mgroups(q), ntiles = (int)ceil_div(g.Fp, q.bn);
             const long long per_split = (long long)g.F * q.T * g.Cp;
-            const int splits = wgrad_splits(q, mgroups * ntiles, per_split);
+            bool atomic = false;
+            static const bool force_det = std::getenv("DC_WGRAD_DETERMINISTIC") != nullptr;
+            const int splits = wgrad_splits(q, mgroups * ntiles, per_split, !deterministic && !force_det, &atomic);
             q.splits = splits;
             q.ws_split = per_split;
-            if (splits > 1) {
+            if (splits > 1 && atomic) {
+                // splits accumulate into the zeroed dW (no partials, no reduce
+                // launch); fp32 addition order varies run to run (DC_DETERMINISTIC)
+                CK(cudaMemsetAsync(dw, 0, (size_t)per_split * 4, st));
+                q.ws = dw, q.ws_split = 0, q.atomic_out = 1;
+            } else if (splits > 1) {
                 ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * per_split * 4);
                 q.ws = pl->ws;
             } else {
@@ -967,7 +990,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
                 make_tmap(&dymap, dy_owned, 4, dims, strides, box, nullptr, 128);
             }
             launch_wgrad_v2(xmap, dymap, q, st);
-            if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+            if (splits > 1 && !q.atomic_out) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
             return;
         }
     }
@@ -1414,7 +1437,7 @@ dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, floa
     DC_REQUIRE(pl && x && dy && dw, DC_ERR_ARG, "null argument");
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
-    run_bwd_filter(pl, x, dy, dw, st);
+    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DETERMINISTIC) != 0);
     signal_ready_next(pl, 0, x, st);
     if ((flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC)) allreduce_dw_async(pl, dw, st);
     else if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
@@ -1436,7 +1459,7 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
         exchange(pl, 1, dy, flags, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
     }
-    run_bwd_filter(pl, x, dy, dw, st);
+    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DETERMINISTIC) != 0);
     signal_ready_next(pl, 0, x, st);
     if (ar_async) allreduce_dw_async(pl, dw, st);
     if (ar) {  // dW allreduce on the comm stream, concurrent with the data gradient

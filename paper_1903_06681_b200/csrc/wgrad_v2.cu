@@ -266,7 +266,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0;
                 }
-                if (valid) {
+                if (valid && p.atomic_out) {
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) {
+                        const int f = f0 + c16 * 16 + e;
+                        if (f < p.F) atomicAdd(&wrow[f * fstride], __uint_as_float(v[e]));  // RED.ADD.F32
+                    }
+                } else if (valid) {
 #pragma unroll
                     for (int e = 0; e < 16; ++e) {
                         const int f = f0 + c16 * 16 + e;

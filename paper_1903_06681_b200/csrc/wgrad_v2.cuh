@@ -19,7 +19,8 @@ struct WgradV2Params {
     int n_mtiles, G;               // M = 128 tiles (atoms stacked), M tiles per CTA
     int tiles_h, tiles_w, nblocks; // 8 x bw output-pixel blocks per sample, total
     int splits;
-    float *ws;                     // [splits][F][T][cp] fp32
+    float *ws;                     // [splits][F][T][cp] fp32 (or dW itself when atomic_out)
+    int atomic_out;                // splits add their partials into a zeroed dW (RED.ADD.F32)
     long long ws_split;
     int F, Fp, cp;
 };

@@ -204,6 +204,31 @@ def test_fused_bn_stats(dc, shape):
         dc.dc_plan_destroy(plan)
 
 
+@pytest.mark.parametrize("shape", [SHAPES[2], SHAPES[9], SHAPES[15]])
+def test_wgrad_deterministic_flag(dc, shape):
+    """DC_DETERMINISTIC: the split-K partials of dW are summed in a fixed order,
+    so two runs agree bit for bit; the default (fp32 atomics into dW) agrees
+    with it within the fp32 bar."""
+    N, C, H, W, F, K, S, P = shape
+    x, w, dy = make_inputs(*shape)
+    plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, (1, 1, 1), 0)
+    try:
+        xd, dyd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_DY)
+        xb, dyb = fill_buffer(x, xd), fill_buffer(dy, dyd)
+        outs = []
+        for flags in (dc.DC_DETERMINISTIC, dc.DC_DETERMINISTIC, 0):
+            dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+            dc.dc_conv_bwd_filter(plan, xb, dyb, dw, flags)
+            outs.append(dw)
+        torch.cuda.synchronize()
+        assert torch.equal(outs[0], outs[1]), "DC_DETERMINISTIC dW differs between runs"
+        assert rel_max(dw_to_fckk(outs[2], C), dw_to_fckk(outs[0], C)) <= TOL_DW
+        dw_ref = oracle.conv_bwd_filter(x, dy, K, S, P)
+        assert rel_max(dw_to_fckk(outs[2], C), dw_ref) <= TOL_DW
+    finally:
+        dc.dc_plan_destroy(plan)
+
+
 def test_launch_counter_and_errors(dc):
     before = dc.dc_kernel_launches()
     run_layer(dc, SHAPES[0], *[None] * 0, x=make_inputs(*SHAPES[0])[0], w=make_inputs(*SHAPES[0])[1],
