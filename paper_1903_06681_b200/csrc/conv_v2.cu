@@ -639,6 +639,14 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.b_resident = 1;
         p.b_stages = 0;
         p.a_stages = std::min(4, (smem_limit - fixed - resident_b) / p.a_stage_bytes);
+        // resident weights: a work item of two stacked tiles halves the per-item
+        // overheads (barriers, accumulator hand-off) and the A halo rows
+        static const bool res_pair = std::getenv("DC_V2_RES_TPW1") == nullptr;
+        if (res_pair && p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems && !std::getenv("DC_V2_TPW1")) {
+            ConvV2Params q = p;
+            q.tpw = 2;
+            if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.b_resident && q.a_stages >= 2) p = q;
+        }
     } else {
         p.b_resident = 0;
         p.a_stages = 2;
