@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--ops", default="fwd,bpw,bpx")
+    ap.add_argument("--bn-fused", action="store_true", help="forward with DC_BN_STATS (as bench.py runs it)")
     a = ap.parse_args()
     import torch
     from paper_1903_06681_b200 import build
@@ -39,7 +40,8 @@ def main():
     dw = torch.empty(F, K, K, q[dc.DC_X]["c_pad"], device="cuda")
     Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
     flops = 2.0 * N * F * C * K * K * Ho * Wo
-    ops = {"fwd": lambda: dc.dc_conv_fwd(plan, x, w, y, 0),
+    fwd_flags = dc.DC_BN_STATS if a.bn_fused else 0
+    ops = {"fwd": lambda: dc.dc_conv_fwd(plan, x, w, y, fwd_flags),
            "bpw": lambda: dc.dc_conv_bwd_filter(plan, x, dy, dw, 0),
            "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0),
            "bn": lambda: dc.dc_bn_spatial_stats(plan, y, mean, var, 1, 0)}
