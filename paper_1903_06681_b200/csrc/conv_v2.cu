@@ -65,29 +65,39 @@ __device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
 
 constexpr int kMaxBar = 16;
 
+// one tcgen05.mma of the kernel's CTA group (1: this SM; 2: the pair, M = 256)
+template <int CG>
+__device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (CG == 2)
+        mma_bf16_cg2(d, a, b, idesc, acc);
+    else
+        mma_bf16(d, a, b, idesc, acc);
+}
+
 // Streamed weights: the MMAs of one weight slot (one tap of one channel group):
 // NK x K16 steps for each of TPW stacked tiles, fully unrolled (compile-time
 // multiples of hoisted strides, no per-MMA descriptor arithmetic chains).
-template <int NK, int TPW>
+template <int CG, int NK, int TPW>
 __device__ __forceinline__ void issue_slot(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t a_kstep,
                                            uint32_t a_tile16, uint32_t acc_cols, uint32_t idesc, bool first) {
 #pragma unroll
     for (int k16 = 0; k16 < NK; ++k16)
 #pragma unroll
         for (int tt = 0; tt < TPW; ++tt)
-            mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
-                     (first && k16 == 0) ? 0u : 1u);
+            mma_cg<CG>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
+                       (first && k16 == 0) ? 0u : 1u);
 }
+template <int CG>
 __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tmem, uint64_t ad, uint64_t bd,
                                                uint32_t a_kstep, uint32_t a_tile16, uint32_t acc_cols,
                                                uint32_t idesc, bool first) {
     switch ((nk16 << 4) | tpw) {
-    case 0x41: issue_slot<4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x42: issue_slot<4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x21: issue_slot<2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x22: issue_slot<2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x11: issue_slot<1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    default: issue_slot<1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x41: issue_slot<CG, 4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x42: issue_slot<CG, 4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x21: issue_slot<CG, 2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x22: issue_slot<CG, 2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x11: issue_slot<CG, 1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    default: issue_slot<CG, 1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
     }
 }
 
@@ -96,7 +106,7 @@ __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tme
 // stride hoisted out of the loop, so the single issuing thread spends a few
 // uniform instructions per tcgen05.mma instead of a dependent chain of
 // constant loads and 64-bit adds per tap (measured: ~180 cycles per tap).
-template <int KH, int KW, int NK, int SSH, int TPW>
+template <int CG, int KH, int KW, int NK, int SSH, int TPW>
 __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, uint64_t bd,
                                            uint32_t a_row16, uint32_t a_col16, uint32_t a_par16,
                                            uint32_t a_kstep, uint32_t b_slot16, uint32_t idesc,
@@ -112,12 +122,13 @@ __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, ui
             for (int k = 0; k < NK; ++k)
 #pragma unroll
                 for (int tt = 0; tt < TPW; ++tt)  // the tiles of the work item share the B slice
-                    mma_bf16(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
-                             idesc, (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
+                    mma_cg<CG>(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
+                               idesc, (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
         }
 }
 
 // Dispatch to an unrolled specialisation; false if none matches.
+template <int CG>
 __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16, uint32_t d_tmem,
                                                  uint64_t a_stage, uint64_t bd, uint32_t a_kstep,
                                                  uint32_t b_slot16, uint32_t idesc, bool first,
@@ -125,11 +136,11 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
     const int key = (p.tpw << 16) | (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
 #define DC_TAPS(KH, KW, NK, SS)                                                                   \
     case ((1 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<CG, KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;                                                                              \
     case ((2 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<CG, KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;
     switch (key) {
@@ -156,9 +167,13 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
 
 constexpr int kV2Threads = 224;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange
 
+// CG = 2: CTA pairs run tcgen05 with cta_group::2 (M = 256 per MMA; each CTA
+// holds its own A tile and half of every weight slot; the leader issues).
+template <int CG>
 __global__ void __launch_bounds__(kV2Threads, 1)
     conv_v2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvV2Params p) {
+    constexpr bool PAIR = CG == 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sB = smem;  // B first: its slots need 1024-byte alignment (swizzle)
@@ -181,23 +196,30 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const uint32_t buf_cols = p.tpw * acc_cols;
     const uint32_t ncols = NB * buf_cols;
 
+    // PAIR: the leader's full barriers collect both CTAs' loads (2 arrivals),
+    // its accumulator-empty barriers both CTAs' epilogue warps (8)
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.a_stages; ++s) {
-            mbar_init(&a_full[s], 1);
+            mbar_init(&a_full[s], PAIR ? 2 : 1);
             mbar_init(&a_empty[s], 1);
         }
         for (int s = 0; s < p.b_stages; ++s) {
-            mbar_init(&b_full[s], 1);
-            mbar_init(&b_empty[s], p.cluster);  // released by the MMAs of every CTA that reads it
+            mbar_init(&b_full[s], PAIR ? 2 : 1);
+            mbar_init(&b_empty[s], PAIR ? 1 : p.cluster);  // released by the MMAs of every CTA that reads it
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], 4);
+            mbar_init(&acc_empty[s], PAIR ? 8 : 4);
         }
-        mbar_init(b_res, 1);
+        mbar_init(b_res, PAIR ? 2 : 1);
         fence_mbar_init();
     }
-    if (warp == 1) tmem_alloc(tmem_slot, ncols);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tmem_alloc_cg2(tmem_slot, ncols);
+        else
+            tmem_alloc(tmem_slot, ncols);
+    }
     tc_fence_before();
     if (p.cluster > 1)
         cluster_sync();  // the partner's barriers exist before any multicast reaches them
@@ -213,6 +235,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     // copy of its partner's tile whose results are not stored).
     const int cl = p.cluster;
     const uint32_t cr = cl > 1 ? cluster_ctarank() : 0;
+    const bool leader = cr == 0;
+    // PAIR: arrive-with-bytes on the leader's barrier (remote for CTA 1)
+    auto expect_lead = [&](uint64_t *bar, uint32_t bytes) {
+        if (leader) mbar_arrive_expect_tx(bar, bytes);
+        else mbar_arrive_expect_tx_cluster(mapa_u32(smem_u32(bar), 0), bytes);
+    };
     const int ks = p.ksplit;
     const int unit = blockIdx.x / cl;
     const int split = unit % ks;
@@ -261,11 +289,20 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {
-                    mbar_arrive_expect_tx(b_res, p.T * (g1 - g0) * p.bn * p.cg * 2);
-                    for (int g = g0; g < g1; ++g)
-                        for (int t = 0; t < p.T; ++t)
-                            tma_load_2d(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, b_res,
-                                        t * p.cin_p + g * p.cg, c.o0);
+                    if constexpr (PAIR) {  // my half (bn/2 rows) of every slot
+                        expect_lead(b_res, p.T * (g1 - g0) * (p.bn / 2) * p.cg * 2);
+                        const uint32_t lb = mapa_u32(smem_u32(b_res), 0);
+                        for (int g = g0; g < g1; ++g)
+                            for (int t = 0; t < p.T; ++t)
+                                tma_load_2d_cg2(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, lb,
+                                                t * p.cin_p + g * p.cg, c.o0 + (int)cr * (p.bn / 2));
+                    } else {
+                        mbar_arrive_expect_tx(b_res, p.T * (g1 - g0) * p.bn * p.cg * 2);
+                        for (int g = g0; g < g1; ++g)
+                            for (int t = 0; t < p.T; ++t)
+                                tma_load_2d(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, b_res,
+                                            t * p.cin_p + g * p.cg, c.o0);
+                    }
                 }
                 __syncwarp();
                 cur_o0 = c.o0;
@@ -278,6 +315,19 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                     uint8_t *dst = sA + s * p.a_stage_bytes;
                     if ((p.dbg & 1) && a_it >= p.a_stages) {
                         mbar_arrive(&a_full[s]);
+                    } else if (PAIR) {  // my tile, completing on the leader's barrier
+                        const uint32_t lb = mapa_u32(smem_u32(&a_full[s]), 0);
+                        if (p.a_swz) {
+                            expect_lead(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
+                            for (int par = 0; par < p.s_in; ++par)
+                                tma_load_4d_cg2(dst + par * p.plane_bytes, &amap, lb, g * p.cg, w0 + par, h0, c.n);
+                        } else {
+                            expect_lead(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
+                            for (int k8 = 0; k8 < p.cg / 8; ++k8)
+                                for (int par = 0; par < p.s_in; ++par)
+                                    tma_load_4d_cg2(dst + (k8 * p.s_in + par) * p.plane_bytes, &amap, lb,
+                                                    g * p.cg + k8 * 8, w0 + par, h0, c.n);
+                        }
                     } else if (p.a_swz) {
                         // one box per column parity: PH rows x PWs cols x cg channels
                         mbar_arrive_expect_tx(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
@@ -299,6 +349,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const int sb = b_it % p.b_stages;
                         if (b_it >= p.b_stages) mbar_wait(&b_empty[sb], ((b_it / p.b_stages) - 1) & 1);
                         if (elect_one()) {
+                            if constexpr (PAIR) {  // my half of the slot, in my smem
+                                expect_lead(&b_full[sb], (p.bn / 2) * p.cg * 2);
+                                tma_load_2d_cg2(sB + sb * p.b_slot_bytes, &bmap, mapa_u32(smem_u32(&b_full[sb]), 0),
+                                                t * p.cin_p + g * p.cg, c.o0 + (int)cr * (p.bn / 2));
+                            } else {
                             mbar_arrive_expect_tx(&b_full[sb], p.bn * p.cg * 2);
                             if (cl > 1)  // my half of the slot, into both CTAs
                                 tma_load_2d_mc(sB + sb * p.b_slot_bytes + cr * (p.bn / 2) * p.cg * 2, &bmap,
@@ -307,6 +362,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                             else
                                 tma_load_2d(sB + sb * p.b_slot_bytes, &bmap, &b_full[sb],
                                             t * p.cin_p + g * p.cg, c.o0);
+                            }
                         }
                         __syncwarp();
                         ++b_it;
@@ -315,11 +371,19 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             }
         }
     } else if (warp == 1) {
+      if (!PAIR || leader) {  // (the non-leader's warp 1 only owns TMEM)
         // ============ tcgen05.mma issuer: warp-uniform loop, elected lane issues ============
+        // (PAIR: the leader issues for both CTAs; its commits multicast to both)
+        auto commit = [&](uint64_t *bar) {
+            if constexpr (PAIR)
+                mma_commit_cg2(bar, 0x3);
+            else
+                mma_commit(bar);
+        };
         // Descriptor arithmetic: the start-address field is bits [0,14) in 16-byte
         // units and never carries (smem < 256 KB), so an operand at byte offset
         // `off` from a base descriptor is base + (off >> 4).
-        const uint32_t idesc = idesc_bf16(128, p.bn, 0, 0);
+        const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, p.bn, 0, 0);
         const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
         const uint64_t a_desc0 = p.a_swz ? smem_desc(sA_u, 16, p.a_sbo, swizzle_layout(p.a_swz))
                                                 : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
@@ -352,8 +416,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 if (p.b_resident) {
                     if (elect_one()) {
                         uint64_t bd = b_desc0 + (uint32_t)((g - g0) * p.T) * b_slot16;
-                        if (!do_mma || !issue_taps_fixed(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
-                                                         idesc, g == g0, acc_cols, a_tile16)) {
+                        if (!do_mma || !issue_taps_fixed<CG>(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
+                                                             idesc, g == g0, acc_cols, a_tile16)) {
                         uint64_t arow = a_stage;
                         for (int th = 0; th < p.kh; ++th) {
                             for (int tw = 0; tw < p.kw; ++tw) {
@@ -362,14 +426,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                                 for (int k16 = 0; k16 < nk16; ++k16)
                                     for (int tt = 0; tt < p.tpw; ++tt)
                                         if (do_mma)
-                                            mma_bf16(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
-                                                     bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
+                                            mma_cg<CG>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
+                                                       bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
                                 bd += b_slot16;
                             }
                             arow += p.a_row16;
                         }
                         }
-                        mma_commit(&a_empty[s]);
+                        commit(&a_empty[s]);
                     }
                     __syncwarp();
                 } else {
@@ -387,9 +451,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const bool first = g == g0 && t == 0;
                         if (elect_one()) {
                             if (do_mma)
-                                issue_slot_any(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
-                                               first);
-                            if (cl > 1)
+                                issue_slot_any<CG>(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
+                                                   first);
+                            if (PAIR)
+                                commit(&b_empty[sb]);
+                            else if (cl > 1)
                                 mma_commit_mc(&b_empty[sb], 0x3);  // the slot is shared by both CTAs
                             else
                                 mma_commit(&b_empty[sb]);
@@ -399,16 +465,17 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         if (++sb == p.b_stages) sb = 0, ph ^= 1;
                         if (++tw == p.kw) tw = 0, arow += p.a_row16;
                     }
-                    if (elect_one()) mma_commit(&a_empty[s]);
+                    if (elect_one()) commit(&a_empty[s]);
                     __syncwarp();
                 }
                 ++a_it;
             }
-            if (elect_one()) mma_commit(&acc_full[acc]);
+            if (elect_one()) commit(&acc_full[acc]);
             __syncwarp();
             if (tr) p.dbg_out[acc_it * 8 + 3] = clock64();
             ++acc_it;
         }
+      }
     } else if (warp == 6) {
         // ===================== fused P2P halo exchange (slices) =====================
         if (p.halo) {
@@ -534,7 +601,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             }  // tt
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[acc]);
+            if (lane == 0) {
+                if (PAIR && !leader)  // the leader's MMA warp reuses this buffer of both CTAs
+                    mbar_arrive_cluster(mapa_u32(smem_u32(&acc_empty[acc]), 0));
+                else
+                    mbar_arrive(&acc_empty[acc]);
+            }
             if (tr) p.dbg_out[acc_it * 8 + 6] = clock64();
             ++acc_it;
         }
@@ -554,7 +626,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         cluster_sync();  // no CTA leaves while its partner may still multicast into it
     else
         __syncthreads();
-    if (warp == 1) tmem_dealloc(tmem, ncols);
+    if (warp == 1) {
+        if constexpr (PAIR)
+            tmem_dealloc_cg2(tmem, ncols);
+        else
+            tmem_dealloc(tmem, ncols);
+    }
     if (p.halo && threadIdx.x == 0) {  // the last CTA publishes the epoch and resets the count
         const uint32_t prev = atomicAdd(p.hx.epoch_ctr + 1, 1u);
         if (prev == gridDim.x - 1) {
@@ -629,6 +706,14 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.a_par16 = p.plane_bytes >> 4;
         p.a_kstep16 = (2 * p.s_in * p.plane_bytes) >> 4;
     }
+    // CTA pairs (cta_group::2, each CTA stages half of every weight slot),
+    // opt-in DC_V2_CG2=1: faster for streamed 128-wide weight tiles at stride 1
+    // with warm L2 (conv2_2 fwd 85 -> 69 us) but slower in the bench step with
+    // cold inputs (92 -> 128 us: the leader waits for the slower of two tile
+    // loads) and for 256-wide, resident or stride-2 tiles
+    static const bool cg2 = std::getenv("DC_V2_CG2") != nullptr;
+    const bool cand2 = cg2 && p.bn == 128 && p.s_in == 1;
+    p.cta2 = 0;
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
     const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16 + (p.bn_stats ? 4 * 2 * p.bn * 8 : 0);
     if (p.ksplit < 1 || p.ncg % p.ksplit) return false;
@@ -649,6 +734,10 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         }
     } else {
         p.b_resident = 0;
+        if (cand2) {
+            p.cta2 = 1;
+            p.b_slot_bytes = (int)round_up((int64_t)(p.bn / 2) * p.cg * 2, 1024);
+        }
         p.a_stages = 2;
         p.b_stages = std::min(8, (smem_limit - fixed - 2 * p.a_stage_bytes) / p.b_slot_bytes);
         if (p.b_stages < 2) {
@@ -674,7 +763,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     // streamed weights: CTA pairs multicast each weight stage (half each), which
     // halves the L2 -> SM weight traffic without reducing the number of CTAs
     static const bool no_cluster = std::getenv("DC_V2_NO_CLUSTER") != nullptr;
-    p.cluster = (!p.b_resident && p.bn % 32 == 0 && !no_cluster) ? 2 : 1;
+    p.cluster = p.cta2 ? 2 : (!p.b_resident && p.bn % 32 == 0 && !no_cluster) ? 2 : 1;
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
 }
 
@@ -747,14 +836,17 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     p.dbg = dbg_env;
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(conv_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
     if (p.cluster > 1 && !(p.dbg & 8)) {
         // persistent CTA pairs: as many as can be co-resident (GPCs need not hold
         // an even number of free SMs), a multiple of the split-K factor
         const size_t smem = conv_v2_smem_bytes(p);
+        auto kern = p.cta2 ? conv_v2_kernel<2> : conv_v2_kernel<1>;
+        const size_t key = smem * 2 + (size_t)p.cta2;
         static std::map<size_t, int> max_clusters;
-        if (!max_clusters.count(smem)) {
+        if (!max_clusters.count(key)) {
             cudaLaunchConfig_t cfg{};
             cudaLaunchAttribute at[1];
             at[0].id = cudaLaunchAttributeClusterDimension;
@@ -764,13 +856,13 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
             cfg.dynamicSmemBytes = smem;
             cfg.attrs = at, cfg.numAttrs = 1;
             int n = 0;
-            cudaError_t e = cudaOccupancyMaxActiveClusters(&n, conv_v2_kernel, &cfg);
+            cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
             DC_REQUIRE(e == cudaSuccess && n > 0, DC_ERR_CUDA, "cluster occupancy: %s", cudaGetErrorString(e));
-            max_clusters[smem] = n;
+            max_clusters[key] = n;
         }
         const int per_o = p.nsamples * p.rect_start[p.nrect];
         const int total_w = p.nout_tiles * ((per_o + 1) / 2);
-        const int cap_units = p.max_ctas > 0 ? std::min(max_clusters[smem], p.max_ctas / 2) : max_clusters[smem];
+        const int cap_units = p.max_ctas > 0 ? std::min(max_clusters[key], p.max_ctas / 2) : max_clusters[key];
         const int units = p.ksplit * std::max(1, std::min(total_w, cap_units / p.ksplit));
         cudaLaunchConfig_t cfg{};
         cudaLaunchAttribute at[1];
@@ -781,7 +873,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cfg.attrs = at, cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, conv_v2_kernel, amap, bmap, p);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, amap, bmap, p);
         DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 cluster launch: %s", cudaGetErrorString(e));
         ++g_launches;
         return 2 * units;
@@ -789,11 +881,11 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, device_sm_count()) : device_sm_count();
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, sms / p.ksplit));
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
-        DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER");
+        DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER=1 (and no DC_V2_CG2)");
         ConvV2Params q = p;
         cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
         cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));
-        conv_v2_kernel<<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
+        conv_v2_kernel<1><<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
         cudaStreamSynchronize(st);
         long long h[64 * 8];
         cudaMemcpy(h, q.dbg_out, sizeof h, cudaMemcpyDeviceToHost);
@@ -805,7 +897,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
                     h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
                     h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
     } else {
-        conv_v2_kernel<<<grid, kV2Threads, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
+        conv_v2_kernel<1><<<grid, kV2Threads, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
     }
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));

@@ -90,6 +90,8 @@ struct ConvV2Params {
     int work_hint;             // work items of THIS launch at tpw = 1 (x ksplit): pairing only when plentiful
     int max_ctas;              // host: persistent grid cap (0: SM count)
     int cluster;               // 2: CTA pairs share (multicast) every streamed weight stage; 1: none
+    int cta2;                  // 1: CTA pairs with tcgen05 cta_group::2 (M = 256; each CTA holds half of
+                               // every weight slot, bn/2 rows); implies cluster = 2
     int allow_cg32;            // stride 2: may narrow 64-channel stages to 32 for tile pairs (changes the
                                // summation order: decided from the GLOBAL layer, see capi.cu)
     float *ws;

@@ -7,6 +7,8 @@ same seeded, bf16-exact inputs (DESIGN.md §7 tolerances):
   BN statistics                  : derived fp32-group bound (bn_tol)
 and partition invariance: each rank's owned y / dx computed from its
 margined shard is BITWISE equal to the 1-GPU result (north_star)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -227,6 +229,19 @@ def test_wgrad_deterministic_flag(dc, shape):
         assert rel_max(dw_to_fckk(outs[2], C), dw_ref) <= TOL_DW
     finally:
         dc.dc_plan_destroy(plan)
+
+
+def test_cta_pair_mode_parity():
+    """The opt-in CTA-pair path (DC_V2_CG2=1: tcgen05 cta_group::2, M = 256)
+    must produce the same parity as the default kernel: run the single-GPU
+    parity tests of the shapes it applies to in a child process."""
+    import subprocess
+    import sys
+    env = dict(os.environ, DC_V2_CG2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
+                        "test_single_gpu_parity or test_partition_bitwise"],
+                       env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 def test_launch_counter_and_errors(dc):

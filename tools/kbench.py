@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--ops", default="fwd,bpw,bpx")
     ap.add_argument("--bn-fused", action="store_true", help="forward with DC_BN_STATS (as bench.py runs it)")
+    ap.add_argument("--flush", action="store_true",
+                    help="evict L2 before every timed op (cold inputs, like the bench step)")
     a = ap.parse_args()
     import torch
     from paper_1903_06681_b200 import build
@@ -52,13 +54,25 @@ def main():
         for _ in range(a.warmup):
             f()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(a.iters):
-            f()
-        e1.record()
-        torch.cuda.synchronize()
-        us = e0.elapsed_time(e1) * 1e3 / a.iters
+        if a.flush:
+            scrub = torch.empty(384 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(a.iters)]
+            for e0, e1 in ev:
+                scrub.fill_(1)
+                e0.record()
+                f()
+                e1.record()
+            torch.cuda.synchronize()
+            us = sum(e0.elapsed_time(e1) for e0, e1 in ev) * 1e3 / a.iters
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.iters):
+                f()
+            e1.record()
+            torch.cuda.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / a.iters
         if name == "bn":
             print(f"{name} {a.shape}: {us:8.1f} us  {y.numel() * 2 / us / 1e3:7.1f} GB/s", flush=True)
         else:
