@@ -209,7 +209,10 @@ dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
 // kernel configuration helpers
 // ---------------------------------------------------------------------------
 int pick_bkc(int64_t cin_p) { return cin_p % 64 == 0 ? 64 : cin_p % 32 == 0 ? 32 : 16; }
-int pick_bn(int64_t nout_p) { return nout_p <= 256 ? (int)nout_p : 256; }
+int pick_bn(int64_t nout_p) {
+    static const int cap = std::getenv("DC_V2_BN") ? std::atoi(std::getenv("DC_V2_BN")) : 256;
+    return nout_p <= cap ? (int)nout_p : cap;
+}
 int pick_stages(int bkc, int bn) {
     const int stage = 128 * bkc * 2 + bn * bkc * 2;
     if (stage <= 32 * 1024) return std::max(2, std::min(8, (96 * 1024) / stage));
