@@ -734,12 +734,16 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         }
     } else {
         p.b_resident = 0;
+        p.a_stages = 2;
         if (cand2) {
             p.cta2 = 1;
             p.b_slot_bytes = (int)round_up((int64_t)(p.bn / 2) * p.cg * 2, 1024);
+            // half-size weight slots leave room for a deeper A ring: each stage
+            // waits for both CTAs' tile loads
+            static const int a2 = std::getenv("DC_V2_CG2_ASTAGES") ? std::atoi(std::getenv("DC_V2_CG2_ASTAGES")) : 3;
+            if (smem_limit - fixed - a2 * p.a_stage_bytes >= 4 * p.b_slot_bytes) p.a_stages = a2;
         }
-        p.a_stages = 2;
-        p.b_stages = std::min(8, (smem_limit - fixed - 2 * p.a_stage_bytes) / p.b_slot_bytes);
+        p.b_stages = std::min(8, (smem_limit - fixed - p.a_stages * p.a_stage_bytes) / p.b_slot_bytes);
         if (p.b_stages < 2) {
             p.a_stages = 1;  // (cannot happen for cg <= 64, bn <= 256)
             p.b_stages = std::min(8, (smem_limit - fixed - p.a_stage_bytes) / p.b_slot_bytes);
