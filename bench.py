@@ -223,6 +223,8 @@ def main():
     ap.add_argument("--ar-sync", action="store_true", help="join each dW allreduce inside its layer's call")
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay the step as a CUDA graph")
+    ap.add_argument("--cost-table-in", default=os.path.join(ROOT, "profiles", "cost_table_b200.csv"),
+                    help="measured local conv costs for the performance model ('' = roofline estimate)")
     ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
     args = ap.parse_args()
     layers = WORKLOADS[args.workload]
@@ -263,6 +265,13 @@ def main():
     if "allreduce" in ablate:
         FLAGS &= ~dc.DC_ALLREDUCE
 
+    # the performance model's local conv costs: measured on B200 by
+    # tools/calibrate.py, roofline fallback otherwise
+    table = args.cost_table_in
+    if table and os.path.exists(table):
+        dc.dc_model_load_table(table)
+    else:
+        table = None
     # ---- per-layer plans and resident inputs ----
     L = []
     for l in layers:
@@ -496,6 +505,7 @@ def main():
                                   for d, f_ms, w_ms, x_ms in per],
                        "parallelism": "per-layer model-chosen (pN,pH,pW)" if args.decomp == "auto" else args.decomp,
                        "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
+                       "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
                        "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",
                        "per_layer_times": "instrumented pass after the timed region (events between ops)",
                        "flops_per_step": flops_step},

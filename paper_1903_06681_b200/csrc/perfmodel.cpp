@@ -65,7 +65,11 @@ double conv_time(int op, int64_t n, int64_t c, int64_t h, int64_t w, int64_t f, 
         if (it != m.table.end()) return it->second;
     }
     const int64_t ho = (h + 2 * P - K) / S + 1, wo = (w + 2 * P - K) / S + 1;
-    const double flops = 2.0 * n * f * c * K * K * (double)std::max<int64_t>(ho, 1) * std::max<int64_t>(wo, 1);
+    // the kernels compute whole 16 x 8 output tiles (conv_v2; 8 x 16 pixel
+    // blocks in wgrad_v2): a 4-row shard costs a 16-row tile
+    const double tiled = (double)(16 * ((std::max<int64_t>(ho, 1) + 15) / 16)) *
+                         (double)(8 * ((std::max<int64_t>(wo, 1) + 7) / 8));
+    const double flops = 2.0 * n * f * c * K * K * tiled;
     const double bytes = 2.0 * ((double)n * h * w * c + (double)n * ho * wo * f) + 2.0 * f * c * K * K;
     return m.launch + std::max(flops / m.peak_flops, bytes / m.peak_bw);
 }
