@@ -322,6 +322,7 @@ struct GemmLaunch {
     int dep[4] = {0, 0, 0, 0};       // output rows/cols reading the halo: top, bottom, left, right
     const P2PExchange *halo = nullptr;  // fused P2P exchange (conv_v2 warp 6)
     int halo_rect0 = 0;
+    int subpix = 0, sub_cp = 0, out_hmax = 0, out_wmax = 0;  // sub-pixel backward-data
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
 };
@@ -430,6 +431,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.cin_p = (int)cin_p;
     q.ksplit = L.ksplit;
     if (L.halo) q.halo = 1, q.hx = *L.halo, q.halo_rect0 = L.halo_rect0;
+    q.subpix = L.subpix, q.sub_cp = L.sub_cp, q.out_hmax = L.out_hmax, q.out_wmax = L.out_wmax;
     q.ws = L.ws;
     q.ws_h = L.ws_h;
     q.ws_w = L.ws_w;
@@ -760,8 +762,74 @@ DimPhase dim_phase(const DimSplit &d, int K, int S, int P, int rho) {
     return r;
 }
 
+// Stride 2 with few input channels (C_pad <= 32): the four stride phases as ONE
+// stride-1 GEMM over a D x D dy window with 4 C_pad output columns (N = 64 or
+// 128 instead of four N = 16/32 GEMMs); phase taps outside the filter carry
+// zero weights and the epilogue scatters each 16-column chunk to its phase's
+// pixel (depth-to-space). dx = sum over the window in a fixed tap order, the
+// same on every rank (partitioned == 1 GPU bitwise). False: not applicable.
+bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned flags, cudaStream_t st,
+                         bool *exchanged) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    static const bool off = std::getenv("DC_NO_SUBPIX") != nullptr;
+    if (off || use_v1() || g.S != 2 || g.Cp > 32) return false;
+    const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
+    const int K = g.K, P = g.P;
+    const int dmin = -(int)floor_div(K - 1 - P, 2), dmax = (int)floor_div(P + 1, 2);
+    const int D = dmax - dmin + 1, T = D * D;
+    if (T > kMaxTaps) return false;
+    auto dim = [&](const DimSplit &d, int &t0, int &nt, int &origin, int &out0, int &omax) {
+        const int64_t q = d.in.lo, r = d.in.hi;
+        t0 = (int)floor_div(q, 2);
+        nt = (int)(floor_div(r - 1, 2) - t0 + 1);
+        origin = (int)(t0 + dmin - d.dbuf.lo);
+        out0 = (int)(2 * t0 - q);
+        omax = (int)(r - q);
+    };
+    int t0h, nth, orh, o0h, omh, t0w, ntw, orw, o0w, omw;
+    dim(rp.h, t0h, nth, orh, o0h, omh);
+    dim(rp.w, t0w, ntw, orw, o0w, omw);
+    if (nth <= 0 || ntw <= 0) return true;  // nothing owned
+    const int64_t rows = 4 * g.Cp, kcols = (int64_t)T * g.Fp;
+    ensure_alloc(pl->wt, pl->wt_bytes, (size_t)rows * kcols * 2);
+    GemmLaunch L;
+    ConvGemmParams &p = L.p;
+    std::memset(&p, 0, sizeof p);
+    p.bkc = pick_bkc(g.Fp);
+    p.kc = (int)(g.Fp / p.bkc);
+    p.bn = (int)rows;
+    p.stages = pick_stages(p.bkc, p.bn);
+    p.T = T;
+    for (int t = 0; t < T; ++t) p.tap_h[t] = (int8_t)(t / D), p.tap_w[t] = (int8_t)(t % D);
+    p.s_in = 1;
+    p.origin_h = orh, p.origin_w = orw;
+    p.out = reinterpret_cast<__nv_bfloat16 *>(dx);
+    p.out_sn = dxd.stride_n, p.out_sh = dxd.stride_h, p.out_sw = dxd.stride_w;
+    p.out_h0 = o0h, p.out_w0 = o0w, p.out_dh = 2, p.out_dw = 2;
+    p.nout_p = (int)rows;
+    L.nout_tiles = 1;
+    L.subpix = 1, L.sub_cp = (int)g.Cp, L.out_hmax = omh, L.out_wmax = omw;
+    L.w_base = pl->wt, L.w_rows = rows, L.w_kcols = kcols;
+    weight_map(&L.bmap, pl->wt, rows, kcols, p.bkc, p.bn);
+    L.ksplit = 1;  // (the split-K reduce has no sub-pixel mapping)
+    L.work_hint = ceil_div(g.N * ceil_div(ceil_div(g.H, 2), kV2TH) * ceil_div(ceil_div(g.W, 2), kV2TW),
+                           (int64_t)pl->splitk_world());
+    if ((flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty())) {
+        exchange(pl, 1, dy, flags, st);
+        *exchanged = true;
+    }
+    launch_subpix_weights(reinterpret_cast<const __nv_bfloat16 *>(w), pl->wt, (int)g.F, (int)g.Fp, (int)g.C,
+                          (int)g.Cp, K, P, dmin, D, st);
+    const std::vector<OutRect> whole_rect{OutRect{0, 0, nth, ntw}};
+    return launch_v2_shape(L, whole_rect, 3, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
+}
+
 void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned flags,
                   cudaStream_t st) {
+    bool exchanged = false;
+    if (run_bwd_data_subpix(pl, dy, w, dx, flags, st, &exchanged)) return;
+    if (exchanged) flags &= ~DC_EXCHANGE;  // (the sub-pixel launch did not configure)
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);

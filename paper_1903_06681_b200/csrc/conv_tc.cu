@@ -450,6 +450,31 @@ void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_bas
     ++g_launches;
 }
 
+// Sub-pixel backward-data weights (stride 2): row n = phase * Cp + c, phase =
+// 2 rho_h + rho_w, tap (dh, dw) of the D x D dy window starting at offset
+// dmin: wt[n][dh * D + dw][f] = w[f][a_h][a_w][c] with a = rho + P - 2 (d + dmin),
+// zero when a falls outside the filter (the phase does not use that tap).
+__global__ void subpix_weight_kernel(const __nv_bfloat16 *__restrict__ w, __nv_bfloat16 *__restrict__ wt, int F,
+                                     int Fp, int C, int Cp, int K, int P, int dmin, int D) {
+    const int n = blockIdx.x, tap = blockIdx.y, T = D * D;
+    const int ph = n / Cp, c = n - ph * Cp, rh = ph >> 1, rw = ph & 1;
+    const int dh = tap / D, dw = tap - dh * D;
+    const int ah = rh + P - 2 * (dh + dmin), aw = rw + P - 2 * (dw + dmin);
+    const bool in = c < C && ah >= 0 && ah < K && aw >= 0 && aw < K;
+    for (int f = threadIdx.x; f < Fp; f += blockDim.x) {
+        __nv_bfloat16 v = __float2bfloat16(0.0f);
+        if (in && f < F) v = w[(((long long)f * K + ah) * K + aw) * Cp + c];
+        wt[((long long)n * T + tap) * Fp + f] = v;
+    }
+}
+
+void launch_subpix_weights(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C, int Cp, int K, int P,
+                           int dmin, int D, cudaStream_t st) {
+    subpix_weight_kernel<<<dim3(4 * Cp, D * D), 64, 0, st>>>(w, wt, F, Fp, C, Cp, K, P, dmin, D);
+    CUDA_OK(cudaGetLastError());
+    ++g_launches;
+}
+
 void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C,
                              int Cp, int K, int T, const int8_t *ka, const int8_t *kb,
                              cudaStream_t st) {

@@ -77,6 +77,9 @@ void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, c
 void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_base, int F, int Fp, int C, int Cp,
                                    int K, int ntaps, const int8_t *ka, const int8_t *kb, const int *T,
                                    const int *t, const long long *off, cudaStream_t st);
+// Sub-pixel backward-data weights for stride 2 (see conv_tc.cu): [4 Cp][D*D][Fp].
+void launch_subpix_weights(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C, int Cp, int K, int P,
+                           int dmin, int D, cudaStream_t st);
 void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C,
                              int Cp, int K, int T, const int8_t *ka, const int8_t *kb,
                              cudaStream_t st);

@@ -559,9 +559,22 @@ __global__ void __launch_bounds__(kV2Threads, 1)
 #pragma unroll
                     for (int e = 0; e < 8; ++e) pk[e] = pack2(v[2 * e], v[2 * e + 1]);
                     if (st_ok && !(p.dbg & 2)) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
-                        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        if (p.subpix) {  // this 16-channel chunk belongs to one stride phase
+                            const int col = c.o0 + c16 * 16, ph = col / p.sub_cp, ch = col - ph * p.sub_cp;
+                            const int row = p.out_h0 + p.out_dh * i + (ph >> 1);
+                            const int cw = p.out_w0 + p.out_dw * j + (ph & 1);
+                            if (row >= 0 && row < p.out_hmax && cw >= 0 && cw < p.out_wmax) {
+                                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (long long)c.n * p.out_sn +
+                                                                       (long long)row * p.out_sh +
+                                                                       (long long)cw * p.out_sw + ch);
+                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            }
+                        } else {
+                            uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
+                            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                        }
                     }
                     if (p.bn_stats) {
                         // statistics of the stored bf16 values: an fp32 pairwise

@@ -99,6 +99,10 @@ struct ConvV2Params {
     __nv_bfloat16 *out;
     long long out_sn, out_sh, out_sw;
     int out_h0, out_w0, out_dh, out_dw;
+    // sub-pixel backward-data (stride 2, small C): output column n = phase *
+    // sub_cp + c goes to pixel (out_h0 + 2 i + phase/2, out_w0 + 2 j + phase%2),
+    // kept only inside [0, out_hmax) x [0, out_wmax)
+    int subpix, sub_cp, out_hmax, out_wmax;
     int nout_p;
 };
 
