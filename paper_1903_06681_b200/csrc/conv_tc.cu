@@ -19,6 +19,7 @@
 
 #include "common.hpp"
 #include "conv_tc.cuh"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace dc {
@@ -287,6 +288,7 @@ __global__ void __launch_bounds__(128, 1)
 // Deterministic split-K reduction: dw[i] = sum_{s in order} ws[s][i].
 __global__ void splitk_reduce_kernel(const float4 *__restrict__ ws, int splits, long long n4,
                                      long long split4, float4 *__restrict__ dw) {
+    pdl_wait();  // (launch.cuh: PDL)
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
          i += (long long)gridDim.x * blockDim.x) {
         float4 acc = ws[i];
@@ -314,6 +316,7 @@ struct TapTable {  // grid.z = tap j (of any stride phase)
 __global__ void weight_transform_kernel(const __nv_bfloat16 *__restrict__ w,
                                         __nv_bfloat16 *__restrict__ wt_base, int F, int Fp, int C,
                                         int Cp, int K, const __grid_constant__ TapTable tt) {
+    pdl_wait();  // (launch.cuh: PDL)
     __shared__ __nv_bfloat16 tile[32][33];
     const int c0 = blockIdx.x * 32, f0 = blockIdx.y * 32, j = blockIdx.z;
     const int T = tt.T[j], t = tt.t[j];
@@ -426,10 +429,8 @@ void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, c
     DC_REQUIRE(n % 4 == 0, DC_ERR_ARG, "split-K reduce needs a multiple of 4 elements");
     const long long n4 = n / 4;
     const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148 * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4 *>(ws), splits, n4,
-                                                 n4, reinterpret_cast<float4 *>(dw));
-    CUDA_OK(cudaGetLastError());
-    ++g_launches;
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "split-K reduce",
+             reinterpret_cast<const float4 *>(ws), splits, n4, n4, reinterpret_cast<float4 *>(dw));
 }
 
 void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_base, int F, int Fp, int C, int Cp,
@@ -444,10 +445,8 @@ void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_bas
         DC_REQUIRE(off[j] < (1LL << 31), DC_ERR_ARG, "weight block too large");
         tt.off[j] = (int)off[j];
     }
-    weight_transform_kernel<<<dim3((Cp + 31) / 32, (Fp + 31) / 32, ntaps), dim3(32, 8), 0, st>>>(
-        w, wt_base, F, Fp, C, Cp, K, tt);
-    CUDA_OK(cudaGetLastError());
-    ++g_launches;
+    launch_k(weight_transform_kernel, dim3((Cp + 31) / 32, (Fp + 31) / 32, ntaps), dim3(32, 8), 0, st, 1,
+             "weight transform", w, wt_base, F, Fp, C, Cp, K, tt);
 }
 
 // Sub-pixel backward-data weights (stride 2): row n = phase * Cp + c, phase =
@@ -456,6 +455,7 @@ void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_bas
 // zero when a falls outside the filter (the phase does not use that tap).
 __global__ void subpix_weight_kernel(const __nv_bfloat16 *__restrict__ w, __nv_bfloat16 *__restrict__ wt, int F,
                                      int Fp, int C, int Cp, int K, int P, int dmin, int D) {
+    pdl_wait();  // (launch.cuh: PDL)
     const int n = blockIdx.x, tap = blockIdx.y, T = D * D;
     const int ph = n / Cp, c = n - ph * Cp, rh = ph >> 1, rw = ph & 1;
     const int dh = tap / D, dw = tap - dh * D;
@@ -470,9 +470,8 @@ __global__ void subpix_weight_kernel(const __nv_bfloat16 *__restrict__ w, __nv_b
 
 void launch_subpix_weights(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C, int Cp, int K, int P,
                            int dmin, int D, cudaStream_t st) {
-    subpix_weight_kernel<<<dim3(4 * Cp, D * D), 64, 0, st>>>(w, wt, F, Fp, C, Cp, K, P, dmin, D);
-    CUDA_OK(cudaGetLastError());
-    ++g_launches;
+    launch_k(subpix_weight_kernel, dim3(4 * Cp, D * D), dim3(64), 0, st, 1, "sub-pixel weights", w, wt, F, Fp, C,
+             Cp, K, P, dmin, D);
 }
 
 void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, int Fp, int C,

@@ -23,6 +23,7 @@
 
 #include "common.hpp"
 #include "conv_v2.cuh"
+#include "launch.cuh"
 #include "sm100.cuh"
 
 namespace dc {
@@ -227,6 +228,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // everything above touched only this CTA's smem / TMEM: with PDL it overlaps
+    // the previous kernel's tail; global memory only after its completion
+    pdl_wait();
     // fused halo exchange: this launch's epoch (published by the last CTA at exit)
     const uint32_t halo_e = p.halo ? *reinterpret_cast<volatile uint32_t *>(p.hx.epoch_ctr) + 1 : 0u;
     // Work units: a CTA (cluster == 1) or a CTA pair (cluster == 2: tiles 2k and
@@ -563,17 +567,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                             const int col = c.o0 + c16 * 16, ph = col / p.sub_cp, ch = col - ph * p.sub_cp;
                             const int row = p.out_h0 + p.out_dh * i + (ph >> 1);
                             const int cw = p.out_w0 + p.out_dw * j + (ph & 1);
-                            if (row >= 0 && row < p.out_hmax && cw >= 0 && cw < p.out_wmax) {
-                                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (long long)c.n * p.out_sn +
-                                                                       (long long)row * p.out_sh +
-                                                                       (long long)cw * p.out_sw + ch);
-                                dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                                dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                            }
+                            if (row >= 0 && row < p.out_hmax && cw >= 0 && cw < p.out_wmax)
+                                st_global_v8(p.out + (long long)c.n * p.out_sn + (long long)row * p.out_sh +
+                                                 (long long)cw * p.out_sw + ch,
+                                             pk);
                         } else {
-                            uint4 *dst = reinterpret_cast<uint4 *>(orow + c16 * 16);
-                            dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                            dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                            st_global_v8(orow + c16 * 16, pk);  // a whole 32-byte sector
                         }
                     }
                     if (p.bn_stats) {
@@ -786,6 +785,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
 
 // out[pixel][o] = bf16( sum_{s in order} ws[s][pixel][o] ) over the launch's rects.
 __global__ void conv_v2_reduce_kernel(const __grid_constant__ ConvV2Params p) {
+    pdl_wait();  // (launch.cuh: PDL)
     const int vecs = p.nout_p / 8;
     long long npix_rects = 0;
     for (int r = 0; r < p.nrect; ++r) npix_rects += (long long)p.rect[r].nh * p.rect[r].nw;
@@ -827,10 +827,7 @@ void launch_conv_v2_reduce(const ConvV2Params &p, cudaStream_t st) {
     const long long work = npix * p.nsamples * (p.nout_p / 8);
     if (work == 0) return;
     const int blocks = (int)std::min<long long>((work + 255) / 256, device_sm_count() * 8);
-    conv_v2_reduce_kernel<<<blocks, 256, 0, st>>>(p);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 reduce launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(conv_v2_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "conv_v2 reduce", p);
 }
 
 int device_sm_count() {
@@ -890,9 +887,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         cfg.dynamicSmemBytes = smem;
         cfg.stream = st;
         cfg.attrs = at, cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, amap, bmap, p);
-        DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 cluster launch: %s", cudaGetErrorString(e));
-        ++g_launches;
+        launch_k(kern, dim3(2 * units), dim3(kV2Threads), smem, st, 2, "conv_v2 (pairs)", amap, bmap, p);
         return 2 * units;
     }
     const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, device_sm_count()) : device_sm_count();
@@ -914,7 +909,9 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
                     h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
                     h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
     } else {
-        conv_v2_kernel<1><<<grid, kV2Threads, conv_v2_smem_bytes(p), st>>>(amap, bmap, p);
+        launch_k(conv_v2_kernel<1>, dim3(grid), dim3(kV2Threads), conv_v2_smem_bytes(p), st, 1, "conv_v2", amap,
+                 bmap, p);
+        return grid;
     }
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));

@@ -9,10 +9,12 @@
 // or a neighbour's margin mapped over NVLink (direct P2P stores).
 #include "common.hpp"
 #include "halo.cuh"
+#include "launch.cuh"
 
 namespace dc {
 
 __global__ void block_copy_kernel(const CopyBatch b) {
+    pdl_wait();  // (launch.cuh: PDL)
     const BlockCopy &c = b.c[blockIdx.y];
     const long long run = (long long)c.cols * c.vec16;        // vectors per (n, row)
     const long long total = (long long)c.nn * c.rows * run;
@@ -33,10 +35,7 @@ void launch_block_copies(const CopyBatch &b, cudaStream_t st) {
         mx = std::max(mx, (long long)b.c[i].nn * b.c[i].rows * b.c[i].cols * b.c[i].vec16);
     if (mx == 0) return;
     const int blocks = (int)std::min<long long>((mx + 255) / 256, 148 * 4);
-    block_copy_kernel<<<dim3(blocks, b.count), 256, 0, st>>>(b);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "block copy launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(block_copy_kernel, dim3(blocks, b.count), dim3(256), 0, st, 1, "block copy", b);
 }
 
 struct FlagList {
@@ -44,6 +43,7 @@ struct FlagList {
 };
 
 __global__ void signal_kernel(FlagList fl, int n, uint32_t value, const uint32_t *epoch_src) {
+    pdl_wait();  // (launch.cuh: PDL)
     if (epoch_src) value = *reinterpret_cast<const volatile uint32_t *>(epoch_src) + 1;
     __threadfence_system();
     for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -55,10 +55,7 @@ void launch_signal(uint32_t *const *flags, int n, uint32_t value, const uint32_t
     DC_REQUIRE(n <= 16, DC_ERR_ARG, "too many flags");
     FlagList fl{};
     for (int i = 0; i < n; ++i) fl.f[i] = flags[i];
-    signal_kernel<<<1, 32, 0, st>>>(fl, n, value, epoch_src);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "signal launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(signal_kernel, dim3(1), dim3(32), 0, st, 1, "signal", fl, n, value, epoch_src);
 }
 
 // ---------------------------------------------------------------------------
@@ -87,6 +84,7 @@ int bn_partial_blocks(long long npix, int cpad) {
 
 __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t, long long npix, int cpad,
                                                              double *__restrict__ partials) {
+    pdl_wait();  // (launch.cuh: PDL)
     // sh[pl][2][cpad]: per-pixel-lane partials, summed below in a fixed order
     // so the result does not depend on scheduling (deterministic).
     extern __shared__ double sh[];
@@ -160,6 +158,7 @@ __global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__rest
 __global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks, int cpad,
                                  double *__restrict__ out, int c, double count,
                                  double *__restrict__ mean, double *__restrict__ var) {
+    pdl_wait();  // (launch.cuh: PDL)
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     const int n2 = 2 * cpad;
     if (warp >= cpad) return;
@@ -198,26 +197,21 @@ void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *pa
                "BN stats: channels must be a multiple of 8 and <= 2048");
     const int blocks = bn_partial_blocks(npix, cpad);
     const int pix_lanes = std::max(1, kBnThreads / (cpad / 8));
-    bn_sums_kernel<<<blocks, kBnThreads, (size_t)pix_lanes * 2 * cpad * sizeof(double), st>>>(
-        reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn sums launch: %s", cudaGetErrorString(e));
-    bn_reduce_kernel<<<(cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, cpad, out, c, count, mean, var);
-    e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
-    g_launches += 2;
+    launch_k(bn_sums_kernel, dim3(blocks), dim3(kBnThreads), (size_t)pix_lanes * 2 * cpad * sizeof(double), st, 1,
+             "bn sums", reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
+    launch_k(bn_reduce_kernel, dim3((cpad * 32 + 255) / 256), dim3(256), 0, st, 1, "bn reduce",
+             (const double *)partials, blocks, cpad, out, c, count, mean, var);
 }
 
 void launch_bn_reduce(const double *partials, int blocks, int cpad, double *out, int c, double count, double *mean,
                       double *var, cudaStream_t st) {
-    bn_reduce_kernel<<<(cpad * 32 + 255) / 256, 256, 0, st>>>(partials, blocks, cpad, out, c, count, mean, var);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn reduce launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(bn_reduce_kernel, dim3((cpad * 32 + 255) / 256), dim3(256), 0, st, 1, "bn reduce", partials, blocks,
+             cpad, out, c, count, mean, var);
 }
 
 __global__ void bn_finalize_kernel(const double *sums, int cpad, int c, double count, double *mean,
                                    double *var) {
+    pdl_wait();  // (launch.cuh: PDL)
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
         const double mu = sums[i] / count;
         const double v = sums[cpad + i] / count - mu * mu;
@@ -228,10 +222,8 @@ __global__ void bn_finalize_kernel(const double *sums, int cpad, int c, double c
 
 void launch_bn_finalize(const double *sums, int cpad, int c, double count, double *mean,
                         double *var, cudaStream_t st) {
-    bn_finalize_kernel<<<(c + 255) / 256, 256, 0, st>>>(sums, cpad, c, count, mean, var);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn finalize launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(bn_finalize_kernel, dim3((c + 255) / 256), dim3(256), 0, st, 1, "bn finalize", sums, cpad, c, count,
+             mean, var);
 }
 
 }  // namespace dc
@@ -239,6 +231,7 @@ void launch_bn_finalize(const double *sums, int cpad, int c, double count, doubl
 namespace dc {
 
 __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant__ P2PExchange x) {
+    pdl_wait();  // (launch.cuh: PDL)
     const uint32_t e = *reinterpret_cast<volatile uint32_t *>(x.epoch_ctr) + 1;
     if (blockIdx.x == 0 && (int)threadIdx.x < x.n_ready_out) {
         __threadfence_system();
@@ -289,13 +282,11 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
 }
 
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st) {
-    p2p_exchange_kernel<<<kP2PBlocks, 256, 0, st>>>(x);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "p2p exchange launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(p2p_exchange_kernel, dim3(kP2PBlocks), dim3(256), 0, st, 1, "p2p exchange", x);
 }
 
 __global__ void __launch_bounds__(256) bn_allreduce_p2p_kernel(const __grid_constant__ BnP2P b) {
+    pdl_wait();  // (launch.cuh: PDL)
     const uint32_t e = *reinterpret_cast<volatile uint32_t *>(b.epoch) + 1;
     const int par = e & 1;
     const int n2 = 2 * b.cpad;
@@ -339,10 +330,7 @@ __global__ void __launch_bounds__(256) bn_allreduce_p2p_kernel(const __grid_cons
 void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st) {
     DC_REQUIRE(2 * b.cpad <= kBnMaxDoubles && b.gsize <= kMaxBnGroup, DC_ERR_UNSUPPORTED,
                "P2P BN allreduce: too many channels or members");
-    bn_allreduce_p2p_kernel<<<1, 256, 0, st>>>(b);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "bn p2p launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(bn_allreduce_p2p_kernel, dim3(1), dim3(256), 0, st, 1, "bn p2p", b);
 }
 
 }  // namespace dc

@@ -1,0 +1,48 @@
+// launch.cuh -- kernel launches with Programmatic Dependent Launch (PDL).
+//
+// A kernel launched through launch_k may begin (launch, prologue: barrier
+// init, TMEM allocation, descriptor prefetch) while the previous kernel on the
+// stream is still finishing; it executes pdl_wait() (griddepcontrol.wait)
+// before it touches global memory, which returns once the previous grid has
+// completed and its writes are visible. Without the attribute pdl_wait is a
+// no-op. DC_NO_PDL=1 launches without it.
+#pragma once
+#include <cstdlib>
+#include <utility>
+#include <cuda_runtime.h>
+
+#include "common.hpp"
+
+namespace dc {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = std::getenv("DC_NO_PDL") == nullptr;
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+              const char *what, Args &&...args) {
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = cluster, at[na].val.clusterDim.y = 1, at[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    cfg.gridDim = grid, cfg.blockDim = block, cfg.dynamicSmemBytes = smem, cfg.stream = st;
+    cfg.attrs = at, cfg.numAttrs = na;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "%s launch: %s", what, cudaGetErrorString(e));
+    ++g_launches;
+}
+
+}  // namespace dc

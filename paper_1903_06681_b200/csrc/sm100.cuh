@@ -91,6 +91,14 @@ __device__ __forceinline__ void tma_load_2d_mc(void *dst, const CUtensorMap *m, 
         : "memory");
 }
 
+// One 32-byte global store per thread (sm_100 256-bit STG): a whole L2 sector,
+// no partial-sector writes. dst must be 32-byte aligned.
+__device__ __forceinline__ void st_global_v8(void *dst, const uint32_t (&v)[8]) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+
 // ---------------- clusters ----------------
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;

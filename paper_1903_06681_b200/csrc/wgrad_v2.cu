@@ -24,6 +24,7 @@
 #include "conv_v2.cuh"
 #include "sm100.cuh"
 #include "wgrad_v2.cuh"
+#include "launch.cuh"
 
 namespace dc {
 using namespace sm100;
@@ -152,6 +153,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();  // (launch.cuh: PDL) the prologue above touched only smem / TMEM
 
     if (warp == 0) {
         // ===================== TMA producer (warp-uniform) =====================
@@ -366,11 +368,8 @@ void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const Wg
         cudaFuncSetAttribute(wgrad_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
     const int ntiles = (p.Fp + p.bn - 1) / p.bn;
-    wgrad_v2_kernel<<<dim3(wgrad_v2_mgroups(p), ntiles, p.splits), 192, wgrad_v2_smem_bytes(p), st>>>(
-        xmap, dymap, p);
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "wgrad_v2 launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(wgrad_v2_kernel, dim3(wgrad_v2_mgroups(p), ntiles, p.splits), dim3(192), wgrad_v2_smem_bytes(p), st, 1,
+             "wgrad_v2", xmap, dymap, p);
 }
 
 }  // namespace dc
