@@ -469,7 +469,11 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     // (only with enough MMA work per tile to hide the epilogue reduction: K =
     // C_pad x taps >= 1152, measured: fusing a K = 576 layer costs more than
     // the separate pass over y)
-    q.bn_stats = L.bn_part && L.ksplit == 1 && q.nout_tiles == 1 && (int64_t)q.cin_p * q.T >= 1152 ? 1 : 0;
+    // (N tiles <= 64: register accumulation, cheap enough for any K)
+    q.bn_stats = !(L.bn_part && L.ksplit == 1 && q.nout_tiles == 1) ? 0
+                 : q.bn <= 64                                      ? 2
+                 : (int64_t)q.cin_p * q.T >= 1152                  ? 1
+                                                                   : 0;
     if (L.bn_part && !q.bn_stats) L.bn_ok = false;
     if (q.bn_stats) {
         ConvV2Params t = q;

@@ -166,6 +166,23 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
 }
 
 
+// Per-channel sums of 16 channel values over the warp's 32 lanes (pixels):
+// a fixed-order fp32 pairwise transpose-reduce; afterwards lanes 2k and 2k+1
+// hold halves of channel k in a[0] / q[0] (caller adds them, lane order).
+__device__ __forceinline__ void warp_chunk_reduce(float (&a)[16], float (&q)[16], uint32_t lane) {
+#pragma unroll
+    for (int w = 8; w >= 1; w >>= 1) {
+        const bool up = (lane & (2 * w)) != 0;
+#pragma unroll
+        for (int j = 0; j < w; ++j) {
+            const float sa = up ? a[j] : a[j + w], ka = up ? a[j + w] : a[j];
+            const float sq = up ? q[j] : q[j + w], kq = up ? q[j + w] : q[j];
+            a[j] = ka + __shfl_xor_sync(0xffffffffu, sa, 2 * w);
+            q[j] = kq + __shfl_xor_sync(0xffffffffu, sq, 2 * w);
+        }
+    }
+}
+
 constexpr int kV2Threads = 224;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange
 
 // CG = 2: CTA pairs run tcgen05 with cta_group::2 (M = 256 per MMA; each CTA
@@ -524,6 +541,83 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         if (p.bn_stats)
             for (int i = lane; i < 2 * p.bn; i += 32) my_acc[i] = 0.0;
         __syncwarp();
+        if (p.bn_stats == 2) {
+            // N tile <= 64 channels: every thread always holds the same <= 64
+            // channels, so it accumulates x and x^2 in registers across tiles
+            // (fp32, sequential) and the warp reduction runs once per 16 items
+            // (error depth <= 2 * 16 + 5) instead of per tile
+            float rs[64], rq[64];
+#pragma unroll
+            for (int k = 0; k < 64; ++k) rs[k] = rq[k] = 0.f;
+            auto flush = [&]() {
+#pragma unroll
+                for (int c16 = 0; c16 < 4; ++c16)
+                    if (c16 < p.bn / 16) {
+                        float a[16], q[16];
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) {
+                            a[e] = rs[c16 * 16 + e], q[e] = rq[c16 * 16 + e];
+                            rs[c16 * 16 + e] = rq[c16 * 16 + e] = 0.f;
+                        }
+                        warp_chunk_reduce(a, q, lane);
+                        const float a_o = __shfl_xor_sync(0xffffffffu, a[0], 1);
+                        const float q_o = __shfl_xor_sync(0xffffffffu, q[0], 1);
+                        if ((lane & 1) == 0) {
+                            const int ch = c16 * 16 + ((lane >> 1) & 15);
+                            my_acc[ch] += (double)(a[0] + a_o);
+                            my_acc[p.bn + ch] += (double)(q[0] + q_o);
+                        }
+                    }
+            };
+            int acc_it = 0, since = 0;
+            for (int w = w0_; w < total_w; w += w_step) {
+                bool phantom;
+                const TileCoord c = decode(p, item_of(w, phantom));
+                const int acc = acc_it % NB;
+                mbar_wait(&acc_full[acc], (acc_it / NB) & 1);
+                tc_fence_after();
+                for (int tt = 0; tt < p.tpw; ++tt) {
+                    const int i = c.i0 + tt * 16 + ti, j = c.j0 + tj;
+                    const bool valid = !phantom && i < p.rect[c.r].h0 + p.rect[c.r].nh &&
+                                       j < p.rect[c.r].w0 + p.rect[c.r].nw;
+                    __nv_bfloat16 *orow = p.out + (long long)c.n * p.out_sn +
+                                          (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+                                          (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0;
+                    const uint32_t t_lane = tmem + acc * buf_cols + tt * acc_cols + ((uint32_t)(eq * 32) << 16);
+#pragma unroll
+                    for (int c16 = 0; c16 < 4; ++c16)
+                        if (c16 < p.bn / 16) {
+                            uint32_t v[16];
+                            tmem_ld16(t_lane + c16 * 16, v);
+                            tmem_ld_wait();
+                            const bool st_ok = valid && c.o0 + c16 * 16 < p.nout_p;
+                            uint32_t pk[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) pk[e] = pack2(v[2 * e], v[2 * e + 1]);
+                            if (st_ok) st_global_v8(orow + c16 * 16, pk);
+#pragma unroll
+                            for (int e = 0; e < 16; ++e) {
+                                const float xv = st_ok ? __uint_as_float((e & 1) ? (pk[e >> 1] & 0xffff0000u)
+                                                                                 : (pk[e >> 1] << 16))
+                                                       : 0.f;
+                                rs[c16 * 16 + e] += xv;
+                                rq[c16 * 16 + e] = fmaf(xv, xv, rq[c16 * 16 + e]);  // x^2 exact
+                            }
+                        }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (PAIR && !leader)
+                        mbar_arrive_cluster(mapa_u32(smem_u32(&acc_empty[acc]), 0));
+                    else
+                        mbar_arrive(&acc_empty[acc]);
+                }
+                ++acc_it;
+                if (++since == 16) flush(), since = 0;
+            }
+            flush();
+        } else {
         int acc_it = 0;
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
@@ -622,6 +716,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             if (tr) p.dbg_out[acc_it * 8 + 6] = clock64();
             ++acc_it;
         }
+        }  // (bn_stats != 2)
         if (p.bn_stats) {  // this CTA's partial: the 4 warps summed in a fixed order
             asm volatile("bar.sync 1, 128;" ::: "memory");
             double *dst = p.bn_part + (long long)blockIdx.x * 2 * p.nout_p;

@@ -199,7 +199,7 @@ def test_fused_bn_stats(dc, shape):
         # (layers that cannot fuse fall back to bn_sums_kernel: depth 7 covers both)
         yn = y1[..., :F].permute(0, 3, 1, 2).double().cpu().numpy()
         m_ref, v_ref = oracle.bn_stats(yn)
-        tm, tv = bn_tol(yn, 7)
+        tm, tv = bn_tol(yn, 40)  # fused: <= 2 x 16 in-register adds + depth-5 tree
         assert (np.abs(mean.cpu().numpy() - m_ref) <= tm).all()
         assert (np.abs(var.cpu().numpy() - v_ref) <= tv).all()
     finally:
