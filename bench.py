@@ -11,8 +11,10 @@ output, and backward (dy halo || filter gradient, then data gradient || dW
 allreduce), i.e. every row of SURVEY.md 8(a) on the hot path, through the C
 ABI (libdconv.so); the decomposition of every layer comes from the library's
 performance model (a8) unless --decomp is given. Global batch fixed as N grows
-(strong scaling); the per-layer decomposition is chosen by the library's
-performance model unless --decomp is given.
+(strong scaling). Default workload: the 2K mesh-tangling conv stack at N = 8
+(BASELINE.json configs[3], "N=1-8, pure spatial decomposition"), every layer
+on the pure spatial grid (1, pH, pW) the library's performance model picks
+(PAPER.md:218-226); --decomp auto lets it use sample parallelism too.
 Rank 0 prints ONE JSON line.
 """
 from __future__ import annotations
@@ -48,9 +50,11 @@ def mesh_stack(size: int = 2048, n: int = 1, blocks: int = 6, per_block: int = 5
 
 
 WORKLOADS = {
-    # BASELINE.json configs[3]: 2K mesh-tangling CNN conv stack, N=1 (spatial strong scaling)
-    "mesh2k": mesh_stack(2048, 1),
+    # BASELINE.json configs[3]: 2K mesh-tangling CNN conv stack, N = 1-8, pure
+    # spatial strong scaling. Default: N = 8 (a global mini-batch fixed as the
+    # GPUs grow); N = 1 is the latency-bound end of the same config.
     "mesh2k_n8": mesh_stack(2048, 8),
+    "mesh2k": mesh_stack(2048, 1),
     "mesh1k": mesh_stack(1024, 1, per_block=3),
     # BASELINE.json configs[1]: ResNet-50 conv layers at N=32, 224x224
     "resnet_layers": [("conv1", 32, 3, 224, 224, 64, 7, 2, 3),
@@ -212,9 +216,11 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--workload", default="mesh2k", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="mesh2k_n8", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--decomp", default="auto", help="auto | pn,ph,pw")
+    ap.add_argument("--decomp", default="spatial",
+                    help="spatial (model picks pH x pW, pN = 1: BASELINE configs[3]) | auto (model, all grids) | "
+                         "pn,ph,pw (0 entries: model's choice)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
@@ -276,7 +282,8 @@ def main():
     L = []
     for l in layers:
         name, N, C, H, W, F, K, S, P = l
-        decomp = (0, 0, 0) if args.decomp == "auto" else tuple(int(v) for v in args.decomp.split(","))
+        decomp = {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
+            int(v) for v in args.decomp.split(","))
         plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, dc.DC_BF16, comm)
         chosen, pred = dc.dc_plan_decomp(plan)
         xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
@@ -284,18 +291,19 @@ def main():
         xb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_X), (xd["n"], xd["hb"], xd["wb"], xd["c_pad"]))
         dyb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_DY), (dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]))
 
-        def owned(desc, gen, tid_shape):
-            blk = gen(*tid_shape, n=(desc["n0"], desc["n0"] + desc["n"]), h=(desc["h0"], desc["h0"] + desc["h"]),
-                      w=(desc["w0"], desc["w0"] + desc["w"]))
-            t = np.zeros((desc["n"], desc["h"], desc["w"], desc["c_pad"]), dtype=np.float32)
-            t[..., :desc["c"]] = blk.transpose(0, 2, 3, 1)
-            return torch.tensor(t, dtype=torch.bfloat16)
+        def owned(desc, tid, shape):
+            # the counter-based generator run on the GPU (bitwise equal to the
+            # numpy one, tests/test_datagen.py): no host hashing of gigabytes
+            return datagen.gen_block_nhwc_torch(
+                shape, datagen.SEED, tid, n=(desc["n0"], desc["n0"] + desc["n"]),
+                h=(desc["h0"], desc["h0"] + desc["h"]), w=(desc["w0"], desc["w0"] + desc["w"]),
+                c_pad=desc["c_pad"], dtype=torch.bfloat16, device="cuda")
 
         Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
-        x_own = owned(xd, datagen.gen_x, (N, C, H, W))
-        dy_own = owned(dyd, datagen.gen_dy, (N, F, Ho, Wo))
-        xb[:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]] = x_own.cuda()
-        dyb[:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]] = dy_own.cuda()
+        x_own = owned(xd, datagen.TID_X, (N, C, H, W))
+        dy_own = owned(dyd, datagen.TID_DY, (N, F, Ho, Wo))
+        xb[:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]] = x_own
+        dyb[:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]] = dy_own
         wnp = np.zeros((F, K, K, xd["c_pad"]), dtype=np.float32)
         wnp[..., :C] = datagen.gen_w(F, C, K).transpose(0, 2, 3, 1)
         wt = torch.tensor(wnp, dtype=torch.bfloat16).cuda()
@@ -305,7 +313,7 @@ def main():
         bn_mean = torch.empty(F, dtype=torch.float64, device="cuda")
         bn_var = torch.empty(F, dtype=torch.float64, device="cuda")
         # pinned host copies for the end-to-end leg
-        host = {"x": x_own.pin_memory(), "dy": dy_own.pin_memory(), "w": wt.cpu().pin_memory(),
+        host = {"x": x_own.cpu().pin_memory(), "dy": dy_own.cpu().pin_memory(), "w": wt.cpu().pin_memory(),
                 "dw": torch.empty(dw.shape, dtype=torch.float32).pin_memory()}
         L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
                       dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, host=host))
@@ -503,7 +511,9 @@ def main():
                                    "fwd_tflops": layer_flops(d["l"]) / (f_ms / 1e3) / 1e12,
                                    "bwd_tflops": 2 * layer_flops(d["l"]) / ((w_ms + x_ms) / 1e3) / 1e12}
                                   for d, f_ms, w_ms, x_ms in per],
-                       "parallelism": "per-layer model-chosen (pN,pH,pW)" if args.decomp == "auto" else args.decomp,
+                       "parallelism": {"auto": "per-layer model-chosen (pN,pH,pW)",
+                                       "spatial": "pure spatial, per-layer model-chosen (1,pH,pW)"}.get(
+                                           args.decomp, args.decomp),
                        "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
                        "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
                        "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",

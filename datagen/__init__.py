@@ -90,3 +90,60 @@ def gen_w(F, C, K, seed=SEED, kind="act"):
     """Weights F x C x K x K (the paper's layout)."""
     s = weight_scale(C, K)
     return gen_block((F, C, K, K), seed, TID_W, kind, scale=s)
+
+
+# ----------------------------------------------------------------------------
+# The same counter-based generator as torch ops (any device): the bench builds
+# its resident inputs on the GPU with it instead of hashing gigabytes on the
+# host. uint64 arithmetic is emulated in int64 (multiplication wraps mod 2^64;
+# right shifts are made logical by masking). Bitwise equal to gen_block
+# (tests/test_oracle.py::test_datagen_torch_matches_numpy).
+# ----------------------------------------------------------------------------
+def _s64(v: int) -> int:
+    v &= 0xFFFFFFFFFFFFFFFF
+    return v - (1 << 64) if v >= 1 << 63 else v
+
+
+def _srl(z, s: int):
+    import torch
+    return torch.bitwise_and(torch.bitwise_right_shift(z, s), (1 << (64 - s)) - 1)
+
+
+def _splitmix64_t(z):
+    z = z + _s64(0x9E3779B97F4A7C15)
+    z = torch_xor(z, _srl(z, 30)) * _s64(0xBF58476D1CE4E5B9)
+    z = torch_xor(z, _srl(z, 27)) * _s64(0x94D049BB133111EB)
+    return torch_xor(z, _srl(z, 31))
+
+
+def torch_xor(a, b):
+    import torch
+    return torch.bitwise_xor(a, b)
+
+
+def gen_block_nhwc_torch(shape, seed: int, tensor_id: int, kind: str = "act", n=None, c=None, h=None,
+                         w=None, scale: float = 1.0, c_pad: int | None = None, dtype=None, device="cpu"):
+    """gen_block's values of the block, laid out NHWC (channels padded with
+    zeros to c_pad), generated with torch ops on `device`, one sample at a
+    time; returned in `dtype` (default float64)."""
+    import torch
+    N, C, H, W = shape
+    (n0, n1), (c0, c1), (h0, h1), (w0, w1) = (n or (0, N)), (c or (0, C)), (h or (0, H)), (w or (0, W))
+    cp = c_pad if c_pad is not None else c1 - c0
+    out = torch.zeros((n1 - n0, h1 - h0, w1 - w0, cp), dtype=dtype or torch.float64, device=device)
+    key = int(_key(seed, tensor_id))
+    i64 = dict(dtype=torch.int64, device=device)
+    rc, rh, rw = torch.arange(c0, c1, **i64), torch.arange(h0, h1, **i64), torch.arange(w0, w1, **i64)
+    for k, nn in enumerate(range(n0, n1)):
+        idx = ((nn * C + rc[None, None, :]) * H + rh[:, None, None]) * W + rw[None, :, None]  # [h][w][c]
+        hv = _splitmix64_t(idx + _s64(key))
+        if kind in ("act", "weight"):
+            v = torch.bitwise_and(hv, 255).to(torch.float64) / 128.0 - 1.0
+        elif kind == "act24":
+            v = _srl(hv, 40).to(torch.float64) / float(1 << 23) - 1.0
+        else:
+            raise ValueError(f"unknown kind {kind!r}")
+        if scale != 1.0:
+            v = v * scale
+        out[k, :, :, :c1 - c0] = v.to(out.dtype)
+    return out

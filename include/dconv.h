@@ -112,7 +112,9 @@ dc_status_t dc_comm_sync(dc_comm_t comm, void *stream);
 
 /* COLLECTIVE. Plan one convolution layer: global N, C, H, W, F, odd K,
  * stride in {1, 2}, pad 0 <= P <= K/2, grid `decomp` (product == world, or
- * {0,0,0} for the model's choice), on `comm`.
+ * {0,0,0} for the model's choice -- PAPER.md:206, 222 -- or some entries 0:
+ * the model chooses those with the others fixed, e.g. {1,0,0} = the best pure
+ * spatial grid), on `comm`.
  * Computes the blocked splits, the owned output blocks, the
  * per-side halo widths of x and dy from the interval formula (PAPER.md:139,
  * 145; reading R5) and validates the partition.
@@ -234,6 +236,13 @@ dc_status_t dc_model_layer_cost(int64_t N, int64_t C, int64_t H, int64_t W, int6
 /* Argmin over all valid grids of `world` ranks (tie-break reading R17). */
 dc_status_t dc_model_choose(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
                             int stride, int pad, int world, dc_decomp_t *best, double *seconds);
+/* The same argmin over the grids whose entries equal fix's non-zero entries
+ * (e.g. fix = {1,0,0}: the best pure spatial grid, BASELINE configs[3]);
+ * what dc_plan_create does with a partly-zero decomp. DC_ERR_PARTITION if no
+ * valid grid matches. */
+dc_status_t dc_model_choose_fixed(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
+                                  int stride, int pad, int world, dc_decomp_t fix, dc_decomp_t *best,
+                                  double *seconds);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,7 @@ EXPORTS = [
     "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_load_table", "dc_model_layer_cost",
-    "dc_model_choose",
+    "dc_model_choose", "dc_model_choose_fixed",
 ]
 
 
@@ -100,6 +100,7 @@ def lib() -> ctypes.CDLL:
         "dc_model_load_table": [ctypes.c_char_p],
         "dc_model_layer_cost": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, P(ctypes.c_double)],
         "dc_model_choose": [i64] * 5 + [i32, i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
+        "dc_model_choose_fixed": [i64] * 5 + [i32, i32, i32, i32, dc_decomp_t, P(dc_decomp_t), P(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -272,4 +273,12 @@ def dc_model_layer_cost(N, C, H, W, F, K, stride, pad, decomp, include_allreduce
 def dc_model_choose(N, C, H, W, F, K, stride, pad, world) -> tuple[tuple[int, int, int], float]:
     d, s = dc_decomp_t(), ctypes.c_double()
     _check(lib().dc_model_choose(N, C, H, W, F, K, stride, pad, world, ctypes.byref(d), ctypes.byref(s)))
+    return (d.pn, d.ph, d.pw), s.value
+
+
+def dc_model_choose_fixed(N, C, H, W, F, K, stride, pad, world, fix) -> tuple[tuple[int, int, int], float]:
+    """Argmin over the grids matching fix's non-zero entries ((1, 0, 0): pure spatial)."""
+    d, s = dc_decomp_t(), ctypes.c_double()
+    _check(lib().dc_model_choose_fixed(N, C, H, W, F, K, stride, pad, world, dc_decomp_t(*fix), ctypes.byref(d),
+                                       ctypes.byref(s)))
     return (d.pn, d.ph, d.pw), s.value

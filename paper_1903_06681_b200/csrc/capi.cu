@@ -35,7 +35,7 @@ static thread_local std::string g_err;
 void set_last_error(const std::string &m) { g_err = m; }
 
 double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce);
-bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t);
+bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
 }  // namespace dc
 
 using namespace dc;
@@ -1335,9 +1335,11 @@ dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
     Grid grid{decomp.pn, decomp.ph, decomp.pw};
     double pred = 0;
-    if (decomp.pn == 0 && decomp.ph == 0 && decomp.pw == 0) {
-        DC_REQUIRE(model_choose(g, world, grid, pred), DC_ERR_PARTITION,
-                   "no valid decomposition of %d ranks", world);
+    DC_REQUIRE(decomp.pn >= 0 && decomp.ph >= 0 && decomp.pw >= 0, DC_ERR_ARG, "negative grid entry");
+    if (decomp.pn == 0 || decomp.ph == 0 || decomp.pw == 0) {  // zeros: the model's choice
+        DC_REQUIRE(model_choose(g, world, grid, pred, grid), DC_ERR_PARTITION,
+                   "no valid decomposition of %d ranks with (%d,%d,%d) fixed", world, decomp.pn, decomp.ph,
+                   decomp.pw);
     } else {
         DC_REQUIRE(grid.size() == world, DC_ERR_PARTITION, "grid (%d,%d,%d) has %d ranks, world is %d",
                    grid.pn, grid.ph, grid.pw, grid.size(), world);

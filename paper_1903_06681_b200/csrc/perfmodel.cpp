@@ -99,13 +99,15 @@ double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce) {
     return fp + bp;
 }
 
-bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t) {
+// fix: entries > 0 pin that grid dimension (e.g. {1,0,0}: pure spatial, the
+// model picks p_H x p_W); {0,0,0} searches every factorisation of world
+bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix) {
     bool found = false;
     for (int pn = world; pn >= 1; --pn) {
-        if (world % pn) continue;
+        if (world % pn || (fix.pn > 0 && pn != fix.pn)) continue;
         const int rest = world / pn;
         for (int ph = rest; ph >= 1; --ph) {
-            if (rest % ph) continue;
+            if (rest % ph || (fix.ph > 0 && ph != fix.ph) || (fix.pw > 0 && rest / ph != fix.pw)) continue;
             Grid d{pn, ph, rest / ph};
             if (!grid_valid(g, d)) continue;
             const double t = model_layer_cost(g, d, true);
@@ -183,7 +185,23 @@ extern "C" dc_status_t dc_model_choose(int64_t N, int64_t C, int64_t H, int64_t 
     ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
     Grid b;
     double t = 0;
-    DC_REQUIRE(model_choose(g, world, b, t), DC_ERR_PARTITION, "no valid grid of %d ranks", world);
+    DC_REQUIRE(model_choose(g, world, b, t, Grid{0, 0, 0}), DC_ERR_PARTITION, "no valid grid of %d ranks", world);
+    *best = dc_decomp_t{b.pn, b.ph, b.pw};
+    if (seconds) *seconds = t;
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_choose_fixed(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F,
+                                             int K, int stride, int pad, int world, dc_decomp_t fix,
+                                             dc_decomp_t *best, double *seconds) {
+    DC_API_BEGIN
+    DC_REQUIRE(best != nullptr && world >= 1 && fix.pn >= 0 && fix.ph >= 0 && fix.pw >= 0, DC_ERR_ARG,
+               "bad arguments");
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    Grid b;
+    double t = 0;
+    DC_REQUIRE(model_choose(g, world, b, t, Grid{fix.pn, fix.ph, fix.pw}), DC_ERR_PARTITION,
+               "no valid grid of %d ranks with (%d,%d,%d) fixed", world, fix.pn, fix.ph, fix.pw);
     *best = dc_decomp_t{b.pn, b.ph, b.pw};
     if (seconds) *seconds = t;
     DC_API_END

@@ -153,3 +153,14 @@ def test_model_matches_oracle(dc, layer):
         best, t = dc.dc_model_choose(*args, P_tot)
         ob, ot = pm.choose(layer, P_tot, cost, alpha, beta)
         assert best == ob and abs(t - ot) <= 1e-12 * max(1.0, ot)
+        # pure spatial (p_N fixed to 1): the argmin of the oracle's costs over those grids,
+        # first in the enumeration order on ties (larger p_H first, reading R17)
+        spatial = [g for g in pm.candidates(P_tot) if g[0] == 1 and pm.valid(layer, g)]
+        if spatial:
+            costs = [pm.layer_cost(layer, g, cost, alpha, beta)["total"] for g in spatial]
+            want = spatial[min(range(len(spatial)), key=lambda i: (costs[i], -spatial[i][1]))]
+            got, ts = dc.dc_model_choose_fixed(*args, P_tot, (1, 0, 0))
+            assert got == want and abs(ts - min(costs)) <= 1e-12 * max(1.0, ts), (got, want)
+        else:
+            with pytest.raises(dc.DCError):
+                dc.dc_model_choose_fixed(*args, P_tot, (1, 0, 0))
