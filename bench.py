@@ -278,6 +278,14 @@ def main():
         dc.dc_model_load_table(table)
     else:
         table = None
+    # communication terms fitted to this implementation on B200:
+    # the exposed cost of one halo message (handshake + boundary tiles), strided
+    # east/west messages dearer, exchanges charged without overlap (measured:
+    # not hidden, profiles/r1_NOTES.md)
+    MODEL_COMM = {"alpha_s": 13e-6, "beta_s_per_byte": 1 / 700e9, "alpha_strided_extra_s": 6e-6, "overlap": False}
+    dc.dc_model_set_comm(MODEL_COMM["alpha_s"], MODEL_COMM["beta_s_per_byte"])
+    dc.dc_model_set_strided_latency(MODEL_COMM["alpha_strided_extra_s"])
+    dc.dc_model_set_overlap(MODEL_COMM["overlap"])
     # ---- per-layer plans and resident inputs ----
     L = []
     for l in layers:
@@ -516,6 +524,7 @@ def main():
                                            args.decomp, args.decomp),
                        "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
                        "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
+                       "perf_model_comm": MODEL_COMM,
                        "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",
                        "per_layer_times": "instrumented pass after the timed region (events between ops)",
                        "flops_per_step": flops_step},

@@ -224,6 +224,16 @@ const char *dc_last_error(void);
 /* ---- performance model, host only ---- */
 /* alpha [s], beta [s/byte] of the linear point-to-point model. */
 dc_status_t dc_model_set_comm(double alpha, double beta);
+/* Overlap accounting of the model ("adjusting for overlap if
+ * necessary"): 1 (default) = reading R16, FP = max(C, halo_x), BP = max(Cw,
+ * halo_dy) + max(Cx, BPa); 0 = plain sums (every exchange exposed), for an
+ * implementation whose measured exchanges are not hidden. */
+dc_status_t dc_model_set_overlap(int overlap);
+/* Extra latency [s] added to every east/west and corner halo message of the
+ * model (default 0 = the paper's SR for all messages): in
+ * NHWC those slabs are H_l strided runs rather than one contiguous block, and
+ * their boundary tiles are column strips (measured). */
+dc_status_t dc_model_set_strided_latency(double alpha_w);
 /* Load an empirical cost table (CSV "op,n,c,h,w,f,k,s,pad,seconds",
  * op in {fp,bpx,bpw}). Entries missing from the table
  * fall back to a roofline estimate. */

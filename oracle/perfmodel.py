@@ -36,25 +36,28 @@ def ar(p: int, n_words: float, alpha: float, beta: float, word_bytes: int = 4) -
 
 
 def halo_terms(Nl: int, Ch: int, Hl: int, Wl: int, O: int, h_split: bool, w_split: bool,
-               alpha: float, beta: float, word_bytes: int) -> float:
+               alpha: float, beta: float, word_bytes: int, alpha_w: float = 0.0) -> float:
     """The halo part of FP_l / BPx_l:
     2 SR(O N C H) [east/west] + 2 SR(O N C W) [north/south] + 4 SR(O^2 N C)
     [corners]; e/w and corners omitted if W is undivided, n/s and corners if
-    H is undivided ("can be omitted")."""
+    H is undivided ("can be omitted"). alpha_w: extra latency of each
+    east/west and corner message (strided slabs in NHWC; 0 = the paper's
+    model)."""
     t = 0.0
     if O == 0:
         return 0.0
     if w_split:
-        t += 2 * sr(O * Nl * Ch * Hl, alpha, beta, word_bytes)
+        t += 2 * (sr(O * Nl * Ch * Hl, alpha, beta, word_bytes) + alpha_w)
     if h_split:
         t += 2 * sr(O * Nl * Ch * Wl, alpha, beta, word_bytes)
     if h_split and w_split:
-        t += 4 * sr(O * O * Nl * Ch, alpha, beta, word_bytes)
+        t += 4 * (sr(O * O * Nl * Ch, alpha, beta, word_bytes) + alpha_w)
     return t
 
 
 def layer_cost(layer: dict, grid: tuple[int, int, int], cost, alpha: float, beta: float,
-               word_bytes: int = 2, overlap: bool = True, include_allreduce: bool = True) -> dict:
+               word_bytes: int = 2, overlap: bool = True, include_allreduce: bool = True,
+               alpha_w: float = 0.0) -> dict:
     """Cost_D(l) = FP + BPx + BPw + BPa, local extents of
     the largest (rank 0) block. `cost(op, n, c, h, w, f)` returns the
     empirical local time of op in {"fp", "bpx", "bpw"}.
@@ -69,8 +72,8 @@ def layer_cost(layer: dict, grid: tuple[int, int, int], cost, alpha: float, beta
     c_fp = cost("fp", Nl, C, Hl, Wl, F)
     c_bx = cost("bpx", Nl, C, Hl, Wl, F)
     c_bw = cost("bpw", Nl, C, Hl, Wl, F)
-    hx = halo_terms(Nl, C, Hl, Wl, O, ph > 1, pw > 1, alpha, beta, word_bytes)
-    hdy = halo_terms(Nl, F, Hl, Wl, O, ph > 1, pw > 1, alpha, beta, word_bytes)
+    hx = halo_terms(Nl, C, Hl, Wl, O, ph > 1, pw > 1, alpha, beta, word_bytes, alpha_w)
+    hdy = halo_terms(Nl, F, Hl, Wl, O, ph > 1, pw > 1, alpha, beta, word_bytes, alpha_w)
     bpa = ar(pn * ph * pw, F * C * K * K, alpha, beta, 4) if include_allreduce else 0.0
     if overlap:
         fp = max(c_fp, hx)

@@ -30,7 +30,7 @@ EXPORTS = [
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
-    "dc_last_error", "dc_model_set_comm", "dc_model_load_table", "dc_model_layer_cost",
+    "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
     "dc_model_choose", "dc_model_choose_fixed",
 ]
 
@@ -98,6 +98,8 @@ def lib() -> ctypes.CDLL:
         "dc_bn_spatial_stats": [vp, vp, vp, vp, i32, vp],
         "dc_model_set_comm": [ctypes.c_double, ctypes.c_double],
         "dc_model_load_table": [ctypes.c_char_p],
+        "dc_model_set_overlap": [i32],
+        "dc_model_set_strided_latency": [ctypes.c_double],
         "dc_model_layer_cost": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, P(ctypes.c_double)],
         "dc_model_choose": [i64] * 5 + [i32, i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
         "dc_model_choose_fixed": [i64] * 5 + [i32, i32, i32, i32, dc_decomp_t, P(dc_decomp_t), P(ctypes.c_double)],
@@ -257,6 +259,14 @@ def dc_kernel_launches() -> int:
 
 def dc_model_set_comm(alpha: float, beta: float):
     _check(lib().dc_model_set_comm(alpha, beta))
+
+
+def dc_model_set_overlap(overlap: bool):
+    _check(lib().dc_model_set_overlap(1 if overlap else 0))
+
+
+def dc_model_set_strided_latency(alpha_w: float):
+    _check(lib().dc_model_set_strided_latency(alpha_w))
 
 
 def dc_model_load_table(path: str):

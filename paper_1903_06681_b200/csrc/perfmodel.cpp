@@ -32,6 +32,8 @@ struct Model {
     double peak_flops = 1.36e15;  // sustained bf16 dense, MEASURED_PEAKS.json
     double peak_bw = 6.55e12;     // HBM copy, MEASURED_PEAKS.json
     double launch = 4e-6;         // fixed per-kernel overhead
+    bool overlap = true;          // reading R16; false: plain sums (halo and allreduce exposed)
+    double alpha_w = 0.0;         // extra latency of a strided (east/west, corner) halo message
     std::map<std::tuple<int, int64_t, int64_t, int64_t, int64_t, int64_t, int, int, int>, double> table;
     std::mutex mu;
 };
@@ -76,10 +78,11 @@ double conv_time(int op, int64_t n, int64_t c, int64_t h, int64_t w, int64_t f, 
 
 double halo_terms(int64_t Nl, int64_t Ch, int64_t Hl, int64_t Wl, int O, bool hs, bool ws) {
     if (O == 0) return 0.0;
+    const double aw = model().alpha_w;  // NHWC: e/w and corner slabs are strided runs
     double t = 0.0;
-    if (ws) t += 2 * sr((double)O * Nl * Ch * Hl, 2);
+    if (ws) t += 2 * (sr((double)O * Nl * Ch * Hl, 2) + aw);
     if (hs) t += 2 * sr((double)O * Nl * Ch * Wl, 2);
-    if (hs && ws) t += 4 * sr((double)O * O * Nl * Ch, 2);
+    if (hs && ws) t += 4 * (sr((double)O * O * Nl * Ch, 2) + aw);
     return t;
 }
 }  // namespace
@@ -94,6 +97,7 @@ double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce) {
     const double hx = halo_terms(Nl, g.C, Hl, Wl, O, d.ph > 1, d.pw > 1);
     const double hdy = halo_terms(Nl, g.F, Hl, Wl, O, d.ph > 1, d.pw > 1);
     const double bpa = include_allreduce ? ar(d.size(), (double)g.F * g.C * g.K * g.K, 4) : 0.0;
+    if (!model().overlap) return c_fp + hx + c_bw + hdy + c_bx + bpa;
     const double fp = std::max(c_fp, hx);
     const double bp = std::max(c_bw, hdy) + std::max(c_bx, bpa);
     return fp + bp;
@@ -131,6 +135,19 @@ extern "C" dc_status_t dc_model_set_comm(double alpha, double beta) {
     DC_REQUIRE(alpha >= 0 && beta >= 0, DC_ERR_ARG, "alpha, beta must be >= 0");
     model().alpha = alpha;
     model().beta = beta;
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_set_strided_latency(double alpha_w) {
+    DC_API_BEGIN
+    DC_REQUIRE(alpha_w >= 0, DC_ERR_ARG, "alpha_w must be >= 0");
+    model().alpha_w = alpha_w;
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_set_overlap(int overlap) {
+    DC_API_BEGIN
+    model().overlap = overlap != 0;
     DC_API_END
 }
 

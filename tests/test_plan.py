@@ -120,10 +120,13 @@ def _table_cost(layer):
     return cost
 
 
+@pytest.mark.parametrize("overlap,alpha_w", [(True, 0.0), (False, 0.0), (False, 4e-6)])
 @pytest.mark.parametrize("layer", LAYERS)
-def test_model_matches_oracle(dc, layer):
+def test_model_matches_oracle(dc, layer, overlap, alpha_w):
     alpha, beta = 3e-6, 1.0 / 600e9
     dc.dc_model_set_comm(alpha, beta)
+    dc.dc_model_set_overlap(overlap)
+    dc.dc_model_set_strided_latency(alpha_w)
     cost = _table_cost(layer)
     rows = ["op,n,c,h,w,f,k,s,pad,seconds"]
     for P_tot in (1, 2, 4, 8):
@@ -148,19 +151,21 @@ def test_model_matches_oracle(dc, layer):
                     dc.dc_model_layer_cost(*args, g)
                 continue
             got = dc.dc_model_layer_cost(*args, g)
-            want = pm.layer_cost(layer, g, cost, alpha, beta)["total"]
+            want = pm.layer_cost(layer, g, cost, alpha, beta, overlap=overlap, alpha_w=alpha_w)["total"]
             assert abs(got - want) <= 1e-12 * max(1.0, want), (g, got, want)
         best, t = dc.dc_model_choose(*args, P_tot)
-        ob, ot = pm.choose(layer, P_tot, cost, alpha, beta)
+        ob, ot = pm.choose(layer, P_tot, cost, alpha, beta, overlap=overlap, alpha_w=alpha_w)
         assert best == ob and abs(t - ot) <= 1e-12 * max(1.0, ot)
         # pure spatial (p_N fixed to 1): the argmin of the oracle's costs over those grids,
         # first in the enumeration order on ties (larger p_H first, reading R17)
         spatial = [g for g in pm.candidates(P_tot) if g[0] == 1 and pm.valid(layer, g)]
         if spatial:
-            costs = [pm.layer_cost(layer, g, cost, alpha, beta)["total"] for g in spatial]
+            costs = [pm.layer_cost(layer, g, cost, alpha, beta, overlap=overlap, alpha_w=alpha_w)["total"] for g in spatial]
             want = spatial[min(range(len(spatial)), key=lambda i: (costs[i], -spatial[i][1]))]
             got, ts = dc.dc_model_choose_fixed(*args, P_tot, (1, 0, 0))
             assert got == want and abs(ts - min(costs)) <= 1e-12 * max(1.0, ts), (got, want)
         else:
             with pytest.raises(dc.DCError):
                 dc.dc_model_choose_fixed(*args, P_tot, (1, 0, 0))
+    dc.dc_model_set_overlap(True)
+    dc.dc_model_set_strided_latency(0.0)
