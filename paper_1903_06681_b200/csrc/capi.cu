@@ -981,13 +981,18 @@ int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split, bool all
     const int sms = device_sm_count();
     const double mma_ns = (q.bw / 2) * q.G * (27.0 + 0.41 * q.bn) / 1.9;
     const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
+    static const double sm_gbs = std::getenv("DC_WGRAD_SM_GBS") ? std::atof(std::getenv("DC_WGRAD_SM_GBS")) : 40.0;
     int best = 1;
     bool best_atomic = false;
     double best_t = 1e30;
     for (int s = 1; s <= std::min(q.nblocks, 256); ++s) {
         if ((size_t)s * per_split * 4 > ((size_t)1 << 30)) break;
         const long long active = std::min<long long>((long long)ctas * s, sms);
-        const double bw = std::min(200.0, 7000.0 / (double)active);  // GB/s = bytes/ns per SM
+        // per-SM ingest: measured 45-60 GB/s on the TMA-fed wgrad_v2 (stride-2
+        // conv2_1 at 64 CTAs: 1.66 GB in 577 us; conv1_1 at 80 CTAs: 3.49 GB in
+        // 731 us, profiles/r1_wgrad_s2_n8.txt), so memory-heavy layers need all
+        // SMs; the whole GPU caps at ~7 TB/s
+        const double bw = std::min(sm_gbs, 7000.0 / (double)active);  // GB/s = bytes/ns per SM
         const double blk_ns = std::max(mma_ns, stage_bytes / bw);
         const long long waves = ceil_div((long long)ctas * s, (long long)sms);
         const double t0 = (double)waves * (double)ceil_div((long long)q.nblocks, (long long)s) * blk_ns;

@@ -169,3 +169,22 @@ def test_model_matches_oracle(dc, layer, overlap, alpha_w):
                 dc.dc_model_choose_fixed(*args, P_tot, (1, 0, 0))
     dc.dc_model_set_overlap(True)
     dc.dc_model_set_strided_latency(0.0)
+
+
+@pytest.mark.gpu
+def test_plan_create_partial_decomp(dc):
+    """dc_plan_create with zero entries lets the model choose those (here on
+    one rank: the only grid)."""
+    for decomp in ((0, 0, 0), (1, 0, 0), (0, 1, 0), (1, 1, 0)):
+        plan = dc.dc_plan_create(1, 18, 64, 64, 16, 3, 1, 1, decomp)
+        assert dc.dc_plan_decomp(plan)[0] == (1, 1, 1)
+        dc.dc_plan_destroy(plan)
+
+
+def test_plan_create_partial_decomp_errors(dc):
+    """Fixed entries that cannot cover the world, or negative ones, fail
+    before any device work."""
+    with pytest.raises(dc.DCError):
+        dc.dc_plan_create(2, 18, 64, 64, 16, 3, 1, 1, (2, 0, 0))  # p_N = 2 on one rank
+    with pytest.raises(dc.DCError):
+        dc.dc_plan_create(1, 18, 64, 64, 16, 3, 1, 1, (-1, 0, 0))
