@@ -205,13 +205,28 @@ def run_reference(args, layers, wl_name):
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": "oracle",
                          "sample": desc},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }), flush=True)
+    }), file=JSON_OUT, flush=True)
 
 
 # ----------------------------------------------------------------------------
 # GPU arm
 # ----------------------------------------------------------------------------
+def _claim_stdout():
+    """The JSON line is the only thing bench.py writes to stdout: everything
+    else that writes to fd 1 (NCCL's version banner at communicator init,
+    library prints) is redirected to stderr; the line goes to a dup of the
+    original stdout."""
+    global JSON_OUT
+    sys.stdout.flush()
+    JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+JSON_OUT = sys.stdout
+
+
 def main():
+    _claim_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -534,7 +549,7 @@ def main():
             "gpu_launches": int(launches),
             "clocks": clk,
         }
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=JSON_OUT, flush=True)
     if args.cost_table and rank == 0:
         with open(args.cost_table, "w") as f:
             f.write("op,n,c,h,w,f,k,s,pad,seconds\n")

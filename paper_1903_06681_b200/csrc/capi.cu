@@ -777,7 +777,8 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     static const bool off = std::getenv("DC_NO_SUBPIX") != nullptr;
-    if (off || use_v1() || g.S != 2 || g.Cp > 32) return false;
+    static const int max_c = std::getenv("DC_SUBPIX_MAXC") ? std::atoi(std::getenv("DC_SUBPIX_MAXC")) : 32;
+    if (off || use_v1() || g.S != 2 || g.Cp > max_c || 4 * g.Cp > 256) return false;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
     const int K = g.K, P = g.P;
     const int dmin = -(int)floor_div(K - 1 - P, 2), dmax = (int)floor_div(P + 1, 2);

@@ -183,7 +183,10 @@ __device__ __forceinline__ void warp_chunk_reduce(float (&a)[16], float (&q)[16]
     }
 }
 
-constexpr int kV2Threads = 224;  // warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange
+// warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange, 7-10 second epilogue
+// group (p.epi2: the two groups split each tile's 16-column chunks, so twice as
+// many TMEM loads and stores are in flight; the other warps idle when !epi2)
+constexpr int kV2Threads = 352;
 
 // CG = 2: CTA pairs run tcgen05 with cta_group::2 (M = 256 per MMA; each CTA
 // holds its own A tile and half of every weight slot; the leader issues).
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     uint64_t *acc_full = bars + 4 * kMaxBar, *acc_empty = acc_full + 2;
     uint64_t *b_res = acc_empty + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(b_res + 1);
-    double *bn_acc = reinterpret_cast<double *>(b_res + 2);  // [4 epilogue warps][2][bn] (bn_stats)
+    double *bn_acc = reinterpret_cast<double *>(b_res + 2);  // [4 or 8 epilogue warps][2][bn] (bn_stats)
 
     const int warp = threadIdx.x >> 5;
     const uint32_t lane = threadIdx.x & 31;
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], PAIR ? 8 : 4);
+            mbar_init(&acc_empty[s], (PAIR ? 2 : 1) * (p.epi2 ? 8 : 4));
         }
         mbar_init(b_res, PAIR ? 2 : 1);
         fence_mbar_init();
@@ -532,12 +535,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 if ((int)lane < x.n_data_out) atomicAdd_system(x.data_out[lane], 1u);
             }
         }
-    } else {
+    } else if (warp < 6 || p.epi2) {
         // ========================= epilogue =========================
         const int eq = warp & 3;  // TMEM lane quarter this warp may access
         const int m = eq * 32 + lane;
         const int ti = m >> p.tw_log2, tj = m & ((1 << p.tw_log2) - 1);
-        double *my_acc = bn_acc + (warp - 2) * 2 * p.bn;
+        const int egrp = warp >= 7;                      // chunk half of this warp's group
+        const int ewarp = warp < 6 ? warp - 2 : warp - 3;  // 0..3 group 0, 4..7 group 1
+        double *my_acc = bn_acc + ewarp * 2 * p.bn;
         if (p.bn_stats)
             for (int i = lane; i < 2 * p.bn; i += 32) my_acc[i] = 0.0;
         __syncwarp();
@@ -639,10 +644,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             float *wrow = ks > 1 ? p.ws + (long long)split * p.nsamples * p.ws_h * p.ws_w * p.nout_p +
                                        (((long long)c.n * p.ws_h + i) * p.ws_w + j) * p.nout_p + c.o0
                                  : nullptr;
-            for (int c16 = 0; c16 < p.bn / 16; ++c16) {
-                uint32_t v[16];
-                tmem_ld16(t_lane + c16 * 16, v);
-                tmem_ld_wait();
+            // TMEM loads double-buffered: chunk c16 + 1 is in flight while
+            // chunk c16 is packed and stored (tcgen05.wait::ld covers both)
+            auto body = [&](const uint32_t (&v)[16], const int c16) {
                 if (ks > 1) {
                     if (valid && c.o0 + c16 * 16 < p.nout_p) {
                         float4 *dst = reinterpret_cast<float4 *>(wrow + c16 * 16);
@@ -703,6 +707,24 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         }
                     }
                 }
+            };
+            const int nc16 = p.bn / 16;
+            const int c_lo = p.epi2 && egrp ? (nc16 + 1) / 2 : 0;
+            const int c_hi = p.epi2 && !egrp ? (nc16 + 1) / 2 : nc16;
+            uint32_t va[16], vb[16];
+            if (c_lo < c_hi) {
+                tmem_ld16(t_lane + c_lo * 16, va);
+                tmem_ld_wait();
+            }
+            for (int c16 = c_lo; c16 < c_hi; c16 += 2) {
+                if (c16 + 1 < c_hi) tmem_ld16(t_lane + (c16 + 1) * 16, vb);
+                body(va, c16);
+                tmem_ld_wait();
+                if (c16 + 1 < c_hi) {
+                    if (c16 + 2 < c_hi) tmem_ld16(t_lane + (c16 + 2) * 16, va);
+                    body(vb, c16 + 1);
+                    tmem_ld_wait();
+                }
             }
             }  // tt
             tc_fence_before();
@@ -717,13 +739,17 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             ++acc_it;
         }
         }  // (bn_stats != 2)
-        if (p.bn_stats) {  // this CTA's partial: the 4 warps summed in a fixed order
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (p.bn_stats) {  // this CTA's partial: the 4 (8) warps summed in a fixed order
+            const int ne = p.epi2 ? 8 : 4;
+            if (p.epi2)
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            else
+                asm volatile("bar.sync 1, 128;" ::: "memory");
             double *dst = p.bn_part + (long long)blockIdx.x * 2 * p.nout_p;
-            for (int i = threadIdx.x - 64; i < 2 * p.nout_p; i += 128) {
+            for (int i = ewarp * 32 + lane; i < 2 * p.nout_p; i += 32 * ne) {
                 const int k = i / p.nout_p, ch = i - k * p.nout_p;
                 double t = 0.0;
-                for (int w4 = 0; w4 < 4; ++w4) t += bn_acc[w4 * 2 * p.bn + k * p.bn + ch];
+                for (int w4 = 0; w4 < ne; ++w4) t += bn_acc[w4 * 2 * p.bn + k * p.bn + ch];
                 dst[i] = t;
             }
         }
@@ -754,7 +780,7 @@ size_t conv_v2_smem_bytes(const ConvV2Params &p) {
     const size_t b = p.b_resident ? (size_t)p.T * (p.ncg / p.ksplit) * p.b_slot_bytes
                                   : (size_t)p.b_stages * p.b_slot_bytes;
     return 1024 + b + (size_t)p.a_stages * p.a_stage_bytes + (4 * kMaxBar + 5) * 8 + 16 +
-           (p.bn_stats ? (size_t)4 * 2 * p.bn * sizeof(double) : 0);
+           (p.bn_stats ? (size_t)(p.epi2 ? 8 : 4) * 2 * p.bn * sizeof(double) : 0);
 }
 
 // Pair tiles only when the launch has this many tpw = 1 work items
@@ -943,6 +969,20 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     static const int dbg_env = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
     ConvV2Params p = p_in;
     p.dbg = dbg_env;
+    // second epilogue warp group, where the epilogue paces the tile loop
+    // (measured A/B, N = 8 mesh layers, cold L2): the sub-pixel backward-data
+    // (4 phases per tile, short K: conv1_1 1183 -> 783 us) and 256-wide N
+    // tiles (conv3_2 fwd 579 -> 518 us, 512-ch 32^2 47.5 -> 45.3 us); it
+    // slows the 64/128-wide stride-1/2 tiles (conv1_2 bwd-data 633 -> 680 us,
+    // conv2_1 fwd 322 -> 343 us). Not for the register-accumulated BN path
+    // (bn_stats == 2) and only while the wider BN scratch still fits.
+    static const bool epi4 = std::getenv("DC_V2_EPI4") != nullptr;
+    static const bool epi8 = std::getenv("DC_V2_EPI8") != nullptr;  // force on (A/B runs)
+    p.epi2 = 0;
+    if (!epi4 && p.bn_stats != 2 && (epi8 || p.subpix || p.bn >= 256)) {
+        p.epi2 = 1;
+        if (conv_v2_smem_bytes(p) > (size_t)kV2SmemLimit) p.epi2 = 0;
+    }
     static std::once_flag once;
     std::call_once(once, [] {
         cudaFuncSetAttribute(conv_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);

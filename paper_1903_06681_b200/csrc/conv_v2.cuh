@@ -52,6 +52,7 @@ struct ConvV2Params {
     // sum of squares of every channel over the CTA's tiles, written to
     // bn_part[blockIdx.x][2][nout_p] (needs ksplit == 1 and nout_tiles == 1)
     int bn_stats;
+    int epi2;                  // device: 8 epilogue warps (two groups split the 16-column chunks)
     double *bn_part;
     // Fused P2P halo exchange of the input (one kernel per GPU):
     // warp 6 of the CTAs holding slice s (s = blockIdx.x, + gridDim.x, ... <
