@@ -1,0 +1,158 @@
+"""Parity at BASELINE.json's full sizes (the bench's mesh2k_n8 layers, N = 8,
+1 GPU, the kernels and flags bench.py times) on SAMPLED outputs.
+
+The GPU runs each whole layer (forward with the fused BN statistics,
+backward-data, backward-filter); the fp64 oracle then computes, one by one:
+  * whole output rows of y (Eq. 1) for the first, a middle and
+    the last output row of the first and last sample, from the x rows those
+    outputs read (the halo-slicing reading of SURVEY.md §8(c) item 4: a row
+    window of the global input, same column padding);
+  * whole rows of dx (Eq. 3; strided adjoint, reading R4) from
+    the dy rows that reach them;
+  * dW entries (Eq. 2) at the corners and the middle of
+    (f, c, a, b) from one channel of x and one of dy over all samples;
+and the BN statistics of the whole stored y are checked against fp64 sums of
+that same y (a property that holds at any size).
+
+Tolerances: DESIGN.md §7 (bf16 rows ‖g−o‖₂/‖o‖₂ ≤ 4e-3 derived; dW fp32
+max|g−o|/max|o| ≤ 1e-4 over the sampled entries, north_star's bar).
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+import oracle  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+# (name, N, C, H, W, F, K, S, P): a cross-section of bench.py's mesh2k_n8
+# stack (reading R20) covering every kernel mode the step uses
+LAYERS = [
+    ("conv1_1", 8, 18, 2048, 2048, 64, 3, 2, 1),    # 18 -> 32 padded channels, sub-pixel backward-data
+    ("conv1_2", 8, 64, 1024, 1024, 64, 3, 1, 1),    # register-accumulated fused BN, resident weights
+    ("conv2_1", 8, 64, 1024, 1024, 128, 3, 2, 1),   # stride 2: four phase GEMMs
+    ("conv3_2", 8, 256, 256, 256, 256, 3, 1, 1),    # 256-wide N tiles: two epilogue warp groups
+    ("conv4_2", 8, 512, 128, 128, 512, 3, 1, 1),    # streamed weights, two N tiles
+    ("conv6_2", 8, 512, 32, 32, 512, 3, 1, 1),      # small spatial extent: split-K
+    ("pred", 8, 512, 32, 32, 2, 1, 1, 0),           # 1x1, F = 2
+]
+
+
+@pytest.fixture(scope="module")
+def dc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_1903_06681_b200 as dc
+    torch.cuda.init()
+    return dc
+
+
+def _fwd_window(i, H, K, S, P):
+    """Global input rows [r0, r0 + L) and the local output row i' such that
+    the oracle's Eq. 1 on that window (same P) gives global output row i."""
+    ip = 0 if i == 0 else 1
+    r0 = S * (i - ip)
+    L = min(S * ip - P + K, H - r0)
+    return r0, L, ip
+
+
+def _bwd_window(u, Ho, H, K, S, P):
+    """dy rows [i0, i1) reaching dx row u, the local dx height Hl and row u'
+    such that the oracle's Eq. 3 on that window gives global dx row u."""
+    i0 = max(0, -((K - 1 - P - u) // S))           # ceil((u + P - K + 1) / S), clamped
+    i1 = min(Ho, (u + P) // S + 1)
+    L = i1 - i0
+    up = u - S * i0
+    for Hl in range(max(1, S * (L - 1) + K - 2 * P), S * (L - 1) + K - 2 * P + S + up + 2):
+        if Hl > up and oracle.out_extent(Hl, K, S, P) == L:
+            return i0, i1, Hl, up
+    raise AssertionError("no window")
+
+
+def _rel_l2(g, o):
+    return float(np.linalg.norm((g - o).ravel()) / max(np.linalg.norm(o.ravel()), 1e-300))
+
+
+@pytest.mark.parametrize("layer", LAYERS, ids=[l[0] for l in LAYERS])
+def test_full_size_sampled_parity(dc, layer):
+    import torch
+    from tests.gpu_util import empty_dense
+
+    name, N, C, H, W, F, K, S, P = layer
+    Ho, Wo = oracle.out_extent(H, K, S, P), oracle.out_extent(W, K, S, P)
+    plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, (1, 1, 1), 0)
+    try:
+        xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
+        dyd, dxd = dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(plan, dc.DC_DX)
+        assert (xd["halo_n"], xd["halo_s"], xd["halo_w"], xd["halo_e"]) == (0, 0, 0, 0)
+        gen = dict(c_pad=xd["c_pad"], dtype=torch.bfloat16, device="cuda")
+        xb = datagen.gen_block_nhwc_torch((N, C, H, W), datagen.SEED, datagen.TID_X, **gen).contiguous()
+        dyb = datagen.gen_block_nhwc_torch((N, F, Ho, Wo), datagen.SEED, datagen.TID_DY,
+                                           c_pad=dyd["c_pad"], dtype=torch.bfloat16, device="cuda").contiguous()
+        w = datagen.gen_w(F, C, K)
+        wnp = np.zeros((F, K, K, xd["c_pad"]))
+        wnp[..., :C] = w.transpose(0, 2, 3, 1)
+        wb = torch.tensor(wnp, dtype=torch.bfloat16, device="cuda").contiguous()
+        y, dx = empty_dense(yd), empty_dense(dxd)
+        assert y.shape[:3] == (N, Ho, Wo) and dx.shape[:3] == (N, H, W)
+        dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+        mean = torch.zeros(F, dtype=torch.float64, device="cuda")
+        var = torch.zeros(F, dtype=torch.float64, device="cuda")
+        dc.dc_conv_fwd(plan, xb, wb, y, dc.DC_BN_STATS)
+        dc.dc_bn_spatial_stats(plan, y, mean, var, local_only=True)
+        dc.dc_conv_bwd_data(plan, dyb, wb, dx, 0)
+        dc.dc_conv_bwd_filter(plan, xb, dyb, dw, 0)
+        torch.cuda.synchronize()
+        del xb, dyb
+
+        # BN statistics of the whole stored y (property at any size)
+        y64 = y[..., :F].double()
+        m_ref = y64.mean(dim=(0, 1, 2))
+        v_ref = ((y64 - m_ref) ** 2).mean(dim=(0, 1, 2))
+        yabs = y64.abs().mean(dim=(0, 1, 2)).cpu().numpy()
+        y2 = (y64 ** 2).mean(dim=(0, 1, 2)).cpu().numpy()
+        u = 2.0 ** -24
+        d = 40  # fused-path depth
+        tm = d * u * yabs
+        tv = d * u * y2 + 2 * np.abs(m_ref.cpu().numpy()) * tm
+        assert (np.abs(mean.cpu().numpy() - m_ref.cpu().numpy()) <= tm + 1e-12).all(), f"{name}: BN mean"
+        assert (np.abs(var.cpu().numpy() - v_ref.cpu().numpy()) <= tv + 1e-12).all(), f"{name}: BN var"
+        del y64
+
+        for n in (0, N - 1):
+            for i in sorted({0, Ho // 2, Ho - 1}):
+                r0, L, ip = _fwd_window(i, H, K, S, P)
+                xw = datagen.gen_x(N, C, H, W, n=(n, n + 1), h=(r0, r0 + L))
+                ref = oracle.conv_fwd(xw, w, S, P, rows=(ip, ip + 1))[0, :, ip, :]        # F x Wo
+                got = y[n, i, :, :F].double().cpu().numpy().T
+                e = _rel_l2(got, ref)
+                assert e <= 4e-3, f"{name}: y[{n}, :, {i}, :] rel L2 {e:.2e}"
+            for uu in sorted({0, H // 2, H - 1}):
+                i0, i1, Hl, up = _bwd_window(uu, Ho, H, K, S, P)
+                dyw = datagen.gen_dy(N, F, Ho, Wo, n=(n, n + 1), h=(i0, i1))
+                ref = oracle.conv_bwd_data(dyw, w, Hl, W, S, P, rows=(up, up + 1))[0, :, up, :]  # C x W
+                got = dx[n, uu, :, :C].double().cpu().numpy().T
+                e = _rel_l2(got, ref)
+                assert e <= 4e-3, f"{name}: dx[{n}, :, {uu}, :] rel L2 {e:.2e}"
+
+        dwh = dw[..., :C].double().cpu().numpy()  # F K K C
+        got, ref = [], []
+        for f, c, a, b in sorted({(0, 0, 0, 0), (F - 1, C - 1, K - 1, K - 1), (F // 2, C // 2, K // 2, K // 2)}):
+            xc = datagen.gen_x(N, C, H, W, c=(c, c + 1))
+            dyf = datagen.gen_dy(N, F, Ho, Wo, c=(f, f + 1))
+            ref.append(oracle.conv_bwd_filter_entry(xc, dyf, K, S, P, 0, 0, a, b))
+            got.append(dwh[f, a, b, c])
+        got, ref = np.array(got), np.array(ref)
+        e = np.abs(got - ref).max() / np.abs(ref).max()
+        assert e <= 1e-4, f"{name}: dW sampled {got} vs {ref}: {e:.2e}"  # north_star's fp32 bar (R19)
+    finally:
+        dc.dc_plan_destroy(plan)
