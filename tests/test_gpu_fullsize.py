@@ -1,5 +1,6 @@
 """Parity at BASELINE.json's full sizes (the bench's mesh2k_n8 layers, N = 8,
-1 GPU, the kernels and flags bench.py times) on SAMPLED outputs.
+and the ResNet-50 layers of configs[1], N = 32; 1 GPU, the kernels and flags
+bench.py times) on SAMPLED outputs.
 
 The GPU runs each whole layer (forward with the fused BN statistics,
 backward-data, backward-filter); the fp64 oracle then computes, one by one:
@@ -43,6 +44,10 @@ LAYERS = [
     ("conv4_2", 8, 512, 128, 128, 512, 3, 1, 1),    # streamed weights, two N tiles
     ("conv6_2", 8, 512, 32, 32, 512, 3, 1, 1),      # small spatial extent: split-K
     ("pred", 8, 512, 32, 32, 2, 1, 1, 0),           # 1x1, F = 2
+    # BASELINE.json configs[1]: the paper's ResNet-50 layers at N = 32
+    ("resnet_conv1", 32, 3, 224, 224, 64, 7, 2, 3),
+    ("res2a_branch2b", 32, 64, 56, 56, 64, 3, 1, 1),
+    ("res3b_branch2a", 32, 512, 28, 28, 128, 1, 1, 0),
 ]
 
 
@@ -59,7 +64,7 @@ def dc():
 def _fwd_window(i, H, K, S, P):
     """Global input rows [r0, r0 + L) and the local output row i' such that
     the oracle's Eq. 1 on that window (same P) gives global output row i."""
-    ip = 0 if i == 0 else 1
+    ip = min(i, -(-P // S))  # local row whose window starts at or after local row 0
     r0 = S * (i - ip)
     L = min(S * ip - P + K, H - r0)
     return r0, L, ip
