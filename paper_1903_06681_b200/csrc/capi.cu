@@ -470,7 +470,13 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     // C_pad x taps >= 1152, measured: fusing a K = 576 layer costs more than
     // the separate pass over y)
     // (N tiles <= 64: register accumulation, cheap enough for any K)
-    q.bn_stats = !(L.bn_part && L.ksplit == 1 && q.nout_tiles == 1) ? 0
+    // (several N tiles: the epilogue keeps per-CTA segments, one per N tile,
+    // for N tiles > 64 -- parity-green but opt-in, DC_BN_FUSE_NT=1: measured
+    // on the N = 8 mesh step it moves 0.31 ms from the BN pass into the
+    // forwards (conv4_1 fwd 0.31 -> 0.41 ms) for no net gain)
+    static const bool nt_multi = std::getenv("DC_BN_FUSE_NT") != nullptr;
+    const bool nt_ok = q.nout_tiles == 1 || (q.bn > 64 && nt_multi);
+    q.bn_stats = !(L.bn_part && L.ksplit == 1 && nt_ok) ? 0
                  : q.bn <= 64                                      ? 2
                  : (int64_t)q.cin_p * q.T >= 1152                  ? 1
                                                                    : 0;

@@ -546,6 +546,34 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         if (p.bn_stats)
             for (int i = lane; i < 2 * p.bn; i += 32) my_acc[i] = 0.0;
         __syncwarp();
+        // BN partial of this CTA: bn_part[blockIdx.x][2][nout_p]. Work items
+        // run in ascending N-tile order, so a CTA's items form contiguous
+        // segments of one N tile each; a segment's sums (the 4 / 8 warps in a
+        // fixed order) are stored when the N tile changes and at the end;
+        // channels of N tiles this CTA never ran stay zero.
+        const int n_epi = p.epi2 ? 8 : 4;
+        double *bn_dst = p.bn_part + (long long)blockIdx.x * 2 * p.nout_p;
+        auto epi_bar = [&]() {
+            if (p.epi2)
+                asm volatile("bar.sync 1, 256;" ::: "memory");
+            else
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+        };
+        auto seg_flush = [&](const int o0) {
+            epi_bar();
+            for (int i = ewarp * 32 + lane; i < 2 * p.bn; i += 32 * n_epi) {
+                const int k = i / p.bn, ch = i - k * p.bn;
+                if (o0 + ch < p.nout_p) {
+                    double t = 0.0;
+                    for (int w4 = 0; w4 < n_epi; ++w4) t += bn_acc[w4 * 2 * p.bn + k * p.bn + ch];
+                    bn_dst[k * p.nout_p + o0 + ch] = t;
+                }
+            }
+            epi_bar();
+        };
+        if (p.bn_stats && p.nout_tiles > 1)
+            for (int i = ewarp * 32 + lane; i < 2 * p.nout_p; i += 32 * n_epi) bn_dst[i] = 0.0;
+        int seg_o0 = -1;
         if (p.bn_stats == 2) {
             // N tile <= 64 channels: every thread always holds the same <= 64
             // channels, so it accumulates x and x^2 in registers across tiles
@@ -627,6 +655,14 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
             const TileCoord c = decode(p, item_of(w, phantom));
+            if (p.bn_stats && c.o0 != seg_o0) {
+                if (seg_o0 >= 0) {
+                    seg_flush(seg_o0);
+                    for (int i = lane; i < 2 * p.bn; i += 32) my_acc[i] = 0.0;
+                    __syncwarp();
+                }
+                seg_o0 = c.o0;
+            }
             const int acc = acc_it % NB;
             const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
             if (tr) p.dbg_out[acc_it * 8 + 4] = clock64();
@@ -701,7 +737,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const float a_o = __shfl_xor_sync(0xffffffffu, a[0], 1);
                         const float q_o = __shfl_xor_sync(0xffffffffu, q[0], 1);
                         if ((lane & 1) == 0) {
-                            const int ch = c.o0 + c16 * 16 + ((lane >> 1) & 15);
+                            const int ch = c16 * 16 + ((lane >> 1) & 15);  // within this N tile
                             my_acc[ch] += (double)(a[0] + a_o);
                             my_acc[p.bn + ch] += (double)(q[0] + q_o);
                         }
@@ -739,20 +775,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             ++acc_it;
         }
         }  // (bn_stats != 2)
-        if (p.bn_stats) {  // this CTA's partial: the 4 (8) warps summed in a fixed order
-            const int ne = p.epi2 ? 8 : 4;
-            if (p.epi2)
-                asm volatile("bar.sync 1, 256;" ::: "memory");
-            else
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-            double *dst = p.bn_part + (long long)blockIdx.x * 2 * p.nout_p;
-            for (int i = ewarp * 32 + lane; i < 2 * p.nout_p; i += 32 * ne) {
-                const int k = i / p.nout_p, ch = i - k * p.nout_p;
-                double t = 0.0;
-                for (int w4 = 0; w4 < ne; ++w4) t += bn_acc[w4 * 2 * p.bn + k * p.bn + ch];
-                dst[i] = t;
-            }
-        }
+        if (p.bn_stats) seg_flush(seg_o0 < 0 ? 0 : seg_o0);  // the last (or only) segment
     }
     tc_fence_before();
     if (p.cluster > 1)
