@@ -471,7 +471,9 @@ def main():
 
     # ---- per-op device times on the launching stream, from the timed steps ----
     def avg(i, a, b):
-        return statistics.mean(ev[k][i][a].elapsed_time(ev[k][i][b]) for k in range(args.steps))
+        # median over the instrumented steps: one op hit by a stray clock dip
+        # must not become the reported roofline kernel
+        return statistics.median(ev[k][i][a].elapsed_time(ev[k][i][b]) for k in range(args.steps))
     per = []
     for i, d in enumerate(L):
         f_ms, bn_ms, w_ms, x_ms = avg(i, 0, 1), avg(i, 1, 2), avg(i, 2, 3), avg(i, 3, 4)
@@ -541,7 +543,7 @@ def main():
                        "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
                        "perf_model_comm": MODEL_COMM,
                        "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",
-                       "per_layer_times": "instrumented pass after the timed region (events between ops)",
+                       "per_layer_times": "instrumented pass after the timed region (events between ops; median over its steps)",
                        "flops_per_step": flops_step},
             "roofline": roof,
             "cpu_baseline": cpu,
