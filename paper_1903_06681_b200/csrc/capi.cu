@@ -1038,6 +1038,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
         q.kh = q.kw = g.K;
         q.T = g.K * g.K;
         q.F = (int)g.F, q.Fp = (int)g.Fp, q.cp = (int)g.Cp;
+        q.pixels_hint = nl * ho * wo;
         if (wgrad_v2_configure(q, kV2SmemLimit)) {
             q.tiles_h = (int)ceil_div(ho, 8);
             q.tiles_w = (int)ceil_div(wo, (int64_t)q.bw);

@@ -328,9 +328,14 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
     p.bw = bw;
     p.pitch = p.bw + (p.kw - 1) / p.s_in;
     p.x_plane_bytes = (p.PH * p.pitch * p.cgw * 2 + 1023) / 1024 * 1024;
-    // N tile <= 128: 4 M tiles share each x / dy stage in TMEM (512 cols), half
-    // the bytes per MMA of 256-wide tiles (measured 10-17% faster, cold L2)
-    static const int bn_cap = std::getenv("DC_WGRAD_BN") ? std::atoi(std::getenv("DC_WGRAD_BN")) : 128;
+    // N tile 256 (2 M tiles per x / dy stage in TMEM) once the launch has
+    // >= 8192 output pixels, else 128 (4 M tiles per stage, half the bytes per
+    // MMA). Measured, cold L2 (profiles/r1_wgrad_bn_sweep.txt): 256 wins
+    // 8-25% from 16K pixels up (512-ch 128^2 N = 8: 561 -> 458 us; 256-ch
+    // 256^2: 510 -> 470 us), ties at 4K-8K, loses up to 14% below (512-ch
+    // 32^2 N = 1: 31 -> 36 us). DC_WGRAD_BN overrides.
+    static const int bn_env = std::getenv("DC_WGRAD_BN") ? std::atoi(std::getenv("DC_WGRAD_BN")) : 0;
+    const int bn_cap = bn_env > 0 ? bn_env : p.pixels_hint >= 8192 ? 256 : 128;
     p.bn = p.Fp <= bn_cap ? p.Fp : bn_cap;
     p.bn_cols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
     p.G = std::max(1, std::min(8, 512 / p.bn_cols));

@@ -23,6 +23,7 @@ struct WgradV2Params {
     int atomic_out;                // splits add their partials into a zeroed dW (RED.ADD.F32)
     long long ws_split;
     int F, Fp, cp;
+    long long pixels_hint;         // host: output pixels of this launch (N tile width choice)
 };
 
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit);
