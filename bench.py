@@ -332,7 +332,7 @@ def main():
         wt = torch.tensor(wnp, dtype=torch.bfloat16).cuda()
         y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
         dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
-        dw = torch.empty((F, K, K, xd["c_pad"]), dtype=torch.float32, device="cuda")
+        dw = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
         bn_mean = torch.empty(F, dtype=torch.float64, device="cuda")
         bn_var = torch.empty(F, dtype=torch.float64, device="cuda")
         # pinned host copies for the end-to-end leg
@@ -346,10 +346,12 @@ def main():
         """The calls of one layer, in step order: (name, fn)."""
         # the forward epilogue accumulates the BN statistics of y (DC_BN_STATS);
         # dc_bn_spatial_stats then reduces those partials (+ the NVLink allreduce)
-        fwd_flags = FLAGS | (0 if "bn" in ablate or args.no_fused_bn else dc.DC_BN_STATS)
+        fused = not ("bn" in ablate or args.no_fused_bn)
+        fwd_flags = FLAGS | (dc.DC_BN_STATS if fused else 0)
+        bn_flags = dc.DC_BN_FROM_FWD if fused else 0
         ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], fwd_flags, sp)),
                # spatially aggregated BN statistics of the layer output (SURVEY.md 8(a) a7)
-               ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], False, sp))]
+               ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], bn_flags, sp))]
         if "bn" in ablate:
             ops.pop()
         if world == 1:

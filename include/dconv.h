@@ -20,7 +20,8 @@
  *   y, dx        dense NHWC bf16 over the owned block [n][h][w][c_pad];
  *   w            bf16 [F][K][K][c_pad(C)]  (replicated on every rank,
  *                PAPER.md:137 "w and dL/dw are replicated");
- *   dw           fp32 [F][K][K][c_pad(C)]  (padded-channel entries are 0).
+ *   dw           fp32 [F][K][K][C]  (dense, no channel padding: the F C K^2
+ *                words the allreduce sends).
  *
  * Semantics: every call enqueues work on the caller's stream and returns
  * without a host sync; internal streams are joined back with events before
@@ -80,14 +81,16 @@ typedef struct dc_plan_s *dc_plan_t;
 #define DC_ALLREDUCE     0x2u  /* conv_bwd_filter: sum dW over all ranks    */
 #define DC_HALO_NCCL     0x4u  /* use grouped ncclSend/ncclRecv instead of direct P2P       */
 #define DC_BN_STATS      0x10u /* conv_fwd: accumulate the BN statistics of the stored y in
-                                  the epilogue (per-CTA fp64 partials); the next
-                                  dc_bn_spatial_stats on that y reduces them instead of
-                                  re-reading y (same result up to fp64 summation order) */
-#define DC_DETERMINISTIC 0x20u /* conv_bwd_filter / conv_bwd: sum the split-K partials of
-                                  dW in a fixed order (bitwise reproducible). Default:
-                                  the splits add into dW with fp32 atomics (faster;
-                                  last-bit differences between runs). y and dx are
-                                  always reproducible. */
+                                  the epilogue (per-CTA fp64 partials), reduced by a
+                                  following dc_bn_spatial_stats(..., DC_BN_FROM_FWD) on
+                                  that unchanged y instead of re-reading it */
+#define DC_DETERMINISTIC 0x20u /* accepted for compatibility: dW is deterministic by
+                                  default (split-K partials summed in a fixed order) */
+#define DC_DW_ATOMIC     0x40u /* conv_bwd_filter / conv_bwd: let the split-K partials of
+                                  small dW (< 1M elements) add into dW with fp32 atomics
+                                  (no partial buffer / reduce launch; last-bit
+                                  differences between runs). y and dx are always
+                                  reproducible. */
 #define DC_ALLREDUCE_ASYNC 0x8u /* with DC_ALLREDUCE: queue the dW allreduce on the
                                   communicator's gradient stream instead of joining it
                                   into the call (overlaps the later layers' work,
@@ -101,6 +104,18 @@ typedef struct dc_plan_s *dc_plan_t;
  * Errors: DC_ERR_ARG (rank/world), DC_ERR_COMM (NCCL). */
 dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cuda_device,
                            dc_comm_t *out);
+/* NOT collective. Loopback group: `world` virtual ranks (1..64) of THIS
+ * process on ONE device (cuda_device), written to comms[0..world-1]. Every
+ * call a real rank would make is made once per virtual rank, each on its own
+ * stream (host calls never block, so one thread can issue rank 0, 1, ... in
+ * turn; the device-side P2P protocols let the ranks' kernels rendezvous).
+ * The halo exchange (direct P2P stores, flags, interior/boundary overlap) and
+ * the spatial BN mailbox run unchanged with plain pointers in place of
+ * IPC-mapped peer memory; the NCCL transports (DC_HALO_NCCL, the dW
+ * allreduce, BN groups > 8) need real ranks and fail with
+ * DC_ERR_UNSUPPORTED. Used to test the multi-rank device protocols on one
+ * GPU. Destroy each with dc_comm_destroy. Errors: DC_ERR_ARG, DC_ERR_CUDA. */
+dc_status_t dc_comm_create_local(int world, int cuda_device, dc_comm_t *comms);
 /* Write a fresh 128-byte ncclUniqueId to uid128 (rank 0 only). */
 dc_status_t dc_comm_unique_id(void *uid128);
 dc_status_t dc_comm_destroy(dc_comm_t comm);
@@ -152,11 +167,11 @@ dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicte
 /* Summation-order setting of the conv kernels: the split-K factor over
  * channel groups (the only choice that changes how an output is summed) is
  * picked for the global layer divided over `world` ranks. Default (world 0):
- * this plan's grid size, i.e. each shard gets as many splits as its own work
- * needs. Plans of the same layer with equal settings sum every output element
- * in the same order, so a 1-GPU plan with world = P reproduces the y and dx
- * of any P-rank partition bit for bit (north_star). Host only; takes effect
- * from the next compute call. Errors: DC_ERR_ARG. */
+ * 8, whatever the plan's grid, so every partition of the same layer into up
+ * to 8 ranks and its 1-GPU plan sum every y / dx element in the same order
+ * (bit-identical outputs, north_star). Plans with equal settings agree bit
+ * for bit; a different setting trades that for a split better fitted to one
+ * grid size. Host only; takes effect from the next compute call. */
 dc_status_t dc_plan_set_splitk_world(dc_plan_t plan, int world);
 dc_status_t dc_plan_destroy(dc_plan_t plan);
 
@@ -208,10 +223,21 @@ dc_status_t dc_conv_bwd(dc_plan_t plan, const void *x_margined, void *dy_margine
  * the whole spatial extent of the ranks that share this rank's samples
  * (equal i_N). t is a dense NHWC bf16 tensor of the DC_Y layout of this plan
  * (channels = F, padded); mean_dev/var_dev are device fp64 arrays of F
- * entries. COLLECTIVE over the spatial group. local_only != 0 gives the
- * purely local variant ("purely local batch normalization"). */
+ * entries. COLLECTIVE over the spatial group (each group of <= 8 ranks uses
+ * its own one-shot NVLink mailbox of this plan; NCCL beyond).
+ * flags: DC_BN_LOCAL gives the purely local variant ("purely
+ * local batch normalization"; no communication). DC_BN_FROM_FWD states that
+ * t is the y of this plan's most recent dc_conv_fwd, which ran with
+ * DC_BN_STATS, and that t has not been written since: the per-CTA partials
+ * that forward's epilogue accumulated are reduced instead of re-reading t
+ * (same result up to fp64 summation order). The partials are used once;
+ * without the flag, or when that forward could not accumulate them (another
+ * forward of this plan ran since, or its launch shape has no fused
+ * epilogue), t is read. Errors: DC_ERR_ARG (unknown flag), DC_ERR_COMM. */
+#define DC_BN_LOCAL    0x1u
+#define DC_BN_FROM_FWD 0x2u
 dc_status_t dc_bn_spatial_stats(dc_plan_t plan, const void *t, double *mean_dev,
-                                double *var_dev, int local_only, void *stream);
+                                double *var_dev, unsigned flags, void *stream);
 
 /* Number of kernels this library launched on this thread so far (for the
  * bench's gpu_launches claim). */

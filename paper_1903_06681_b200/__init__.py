@@ -20,13 +20,14 @@ STATUS_NAMES = ["DC_OK", "DC_ERR_ARG", "DC_ERR_SHAPE", "DC_ERR_PARTITION", "DC_E
                 "DC_ERR_CUDA", "DC_ERR_COMM", "DC_ERR_OOM"]
 DC_BF16, DC_FP32_3XTF32 = 0, 1
 DC_X, DC_Y, DC_DY, DC_DX, DC_W, DC_DW = range(6)
-DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DETERMINISTIC = (
-    0x1, 0x2, 0x4, 0x8, 0x10, 0x20)
+DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DETERMINISTIC, DC_DW_ATOMIC = (
+    0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
+DC_BN_LOCAL, DC_BN_FROM_FWD = 0x1, 0x2
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "dc_comm_create", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
+    "dc_comm_create", "dc_comm_create_local", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
@@ -80,6 +81,7 @@ def lib() -> ctypes.CDLL:
     sig = {
         "dc_comm_create": [i32, i32, vp, i32, P(vp)],
         "dc_comm_unique_id": [vp],
+        "dc_comm_create_local": [i32, i32, P(vp)],
         "dc_comm_destroy": [vp],
         "dc_plan_set_splitk_world": [vp, i32],
         "dc_comm_sync": [vp, vp],
@@ -95,7 +97,7 @@ def lib() -> ctypes.CDLL:
         "dc_conv_bwd_data": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_conv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_conv_bwd": [vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp],
-        "dc_bn_spatial_stats": [vp, vp, vp, vp, i32, vp],
+        "dc_bn_spatial_stats": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_model_set_comm": [ctypes.c_double, ctypes.c_double],
         "dc_model_load_table": [ctypes.c_char_p],
         "dc_model_set_overlap": [i32],
@@ -150,6 +152,13 @@ def dc_comm_create(rank: int, world: int, uid: bytes | None, device: int) -> int
     return out.value
 
 
+def dc_comm_create_local(world: int, device: int = 0) -> list[int]:
+    """Loopback group: `world` virtual ranks of this process on one device."""
+    arr = (ctypes.c_void_p * world)()
+    _check(lib().dc_comm_create_local(world, device, arr))
+    return [arr[i] for i in range(world)]
+
+
 def dc_comm_destroy(comm: int):
     _check(lib().dc_comm_destroy(comm))
 
@@ -194,7 +203,7 @@ def dc_plan_decomp(plan: int) -> tuple[tuple[int, int, int], float]:
 
 
 def dc_plan_set_splitk_world(plan: int, world: int):
-    """Pick split-K as for the layer divided over `world` ranks (0: the plan's grid)."""
+    """Pick split-K as for the layer divided over `world` ranks (0: the library's basis, 8)."""
     _check(lib().dc_plan_set_splitk_world(plan, world))
 
 
@@ -248,9 +257,10 @@ def dc_conv_bwd(plan: int, x, dy, w, dx, dw, flags: int = DC_DEFAULT_FLAGS, stre
                              _stream(stream)))
 
 
-def dc_bn_spatial_stats(plan: int, t, mean, var, local_only: bool = False, stream=None):
-    _check(lib().dc_bn_spatial_stats(plan, _ptr(t), _ptr(mean), _ptr(var), int(local_only),
-                                     _stream(stream)))
+def dc_bn_spatial_stats(plan: int, t, mean, var, flags: int = 0, stream=None, local_only: bool = False):
+    """flags: DC_BN_LOCAL | DC_BN_FROM_FWD (local_only=True is DC_BN_LOCAL)."""
+    flags = int(flags) | (DC_BN_LOCAL if local_only else 0)
+    _check(lib().dc_bn_spatial_stats(plan, _ptr(t), _ptr(mean), _ptr(var), flags, _stream(stream)))
 
 
 def dc_kernel_launches() -> int:

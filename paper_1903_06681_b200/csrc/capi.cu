@@ -17,7 +17,9 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -51,6 +53,22 @@ using namespace dc;
         DC_REQUIRE(_r == ncclSuccess, DC_ERR_COMM, "%s: %s", #x, ncclGetErrorString(_r));  \
     } while (0)
 
+struct dc_plan_s;
+
+namespace dc {
+// Loopback group: `world` virtual ranks of one process on ONE device
+// (dc_comm_create_local). Every cross-rank pointer (halo flags, margined
+// buffers, BN mailboxes) is a plain device pointer of the same process,
+// resolved through this registry, so the P2P protocols run unchanged on one
+// GPU (tests; the NCCL transports need real ranks).
+struct LocalGroup {
+    int world = 1;
+    std::mutex mu;
+    std::map<std::pair<int, int>, dc_plan_s *> plans;  // (plan sequence number, rank)
+    std::map<int, std::array<int, 3>> grids;            // sequence number -> grid of its first rank
+};
+}  // namespace dc
+
 struct dc_comm_s {
     int rank = 0, world = 1, device = 0;
     ncclComm_t nccl = nullptr;
@@ -60,11 +78,8 @@ struct dc_comm_s {
     cudaStream_t s_grad = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool grad_pending = false;  // allreduces queued since the last dc_comm_sync
-    // P2P BN statistics mailbox (halo.cuh: BnP2P): [flags (256 B)][2][world][slot]
-    uint8_t *bn_mail = nullptr;
-    std::vector<uint8_t *> bn_peer_mail;  // every rank's mailbox, mapped (mine for me)
-    uint32_t *bn_epoch = nullptr;
-    bool bn_p2p = false;
+    std::shared_ptr<LocalGroup> group;  // loopback group (no NCCL), or null
+    int plan_seq = 0;                   // plans created on this communicator (loopback registry key)
 };
 
 namespace {
@@ -82,6 +97,14 @@ struct BufState {  // a margined buffer (X or DY) known to the plan
 enum { FLAG_READY = 0, FLAG_DATA = 1 };
 
 }  // namespace
+
+// Split-K basis: the conv kernels' split-K factor over channel
+// groups -- the only choice that changes how an output element is summed -- is
+// picked for the GLOBAL layer divided over this many ranks, whatever the
+// plan's grid, so every partition of up to 8 ranks (one NVSwitch node) and
+// the 1-GPU plan of the same layer sum each y / dx element in the same order
+// (north_star: partitioned output bit-identical to 1 GPU).
+constexpr int kSplitKBasis = 8;
 
 struct dc_plan_s {
     RankPlan rp;
@@ -111,15 +134,37 @@ struct dc_plan_s {
     size_t bn_fpart_bytes = 0;
     const void *bn_fused_y = nullptr;  // its y (stats of any other tensor: bn_sums_kernel)
     int bn_fused_slots = 0;
+    uint64_t fwd_epoch = 0;          // forwards run by this plan
+    uint64_t bn_fused_epoch = 0;     // the forward whose partials bn_fpart holds (0: none)
+    // P2P BN statistics mailbox of THIS plan's BN group (halo.cuh: BnP2P):
+    // [flags, 256 B][2 parities][bn_group][2 Fp doubles]; per plan, so every
+    // member takes part in every epoch (a member is at most one epoch ahead)
+    uint8_t *bn_mail = nullptr;
+    uint32_t *bn_epoch = nullptr;
+    std::vector<uint8_t *> bn_peer_mail;  // member k's mailbox (mine at my index)
+    bool bn_p2p = false;
+    int seq = -1;                    // creation index on the communicator (loopback registry key)
     double predicted = 0.0;
 
     ~dc_plan_s() {
         for (auto &b : buf) {
-            for (auto &kv : b.peer) cudaIpcCloseMemHandle(kv.second);
+            if (!(comm && comm->group))
+                for (auto &kv : b.peer) cudaIpcCloseMemHandle(kv.second);
             if (b.owned && b.ptr) cudaFree(b.ptr);
             if (b.stage) cudaFree(b.stage);
         }
-        for (auto &kv : peer_flags) cudaIpcCloseMemHandle(kv.second);
+        const bool ipc = !(comm && comm->group);
+        if (comm && comm->group) {
+            std::lock_guard<std::mutex> lk(comm->group->mu);
+            comm->group->plans.erase({seq, rp.rank});
+        }
+        if (ipc) {
+            for (auto &kv : peer_flags) cudaIpcCloseMemHandle(kv.second);
+            for (size_t k = 0; k < bn_peer_mail.size(); ++k)
+                if (bn_peer_mail[k] && bn_peer_mail[k] != bn_mail) cudaIpcCloseMemHandle(bn_peer_mail[k]);
+        }
+        if (bn_mail) cudaFree(bn_mail);
+        if (bn_epoch) cudaFree(bn_epoch);
         if (flags) cudaFree(flags);
         if (dev_epochs) cudaFree(dev_epochs);
         if (wt) cudaFree(wt);
@@ -138,8 +183,8 @@ struct dc_plan_s {
         if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
     }
     int world() const { return rp.grid.size(); }
-    int ks_world = 0;  // dc_plan_set_splitk_world (0: the grid size)
-    int splitk_world() const { return ks_world > 0 ? ks_world : rp.grid.size(); }
+    int ks_world = 0;  // dc_plan_set_splitk_world (0: kSplitKBasis)
+    int splitk_world() const { return ks_world > 0 ? ks_world : kSplitKBasis; }
     ncclComm_t nccl() const { return comm ? comm->nccl : nullptr; }
     uint32_t *flag(uint32_t *base, int which, int kind, int src) const {
         return base + ((which * 2 + kind) * world() + src);
@@ -193,12 +238,16 @@ dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
              rp.h.d_halo_lo(), rp.h.d_halo_hi(), rp.w.d_halo_lo(), rp.w.d_halo_hi());
         break;
     case DC_W:
-    case DC_DW:
-        d.n0 = 0, d.n = g.F, d.h = g.K, d.w = g.K, d.c = g.C, d.c_pad = g.Cp;
+    case DC_DW: {
+        // w: bf16 [F][K][K][Cp] (TMA rows); dW: fp32 [F][K][K][C], no padding
+        // (what the allreduce sends: F C K^2 words)
+        const int64_t cp = t == DC_W ? g.Cp : g.C;
+        d.n0 = 0, d.n = g.F, d.h = g.K, d.w = g.K, d.c = g.C, d.c_pad = cp;
         d.hb = g.K, d.wb = g.K;
-        d.stride_w = g.Cp, d.stride_h = g.K * g.Cp, d.stride_n = g.K * g.K * g.Cp;
-        d.bytes = (size_t)(g.F * g.K * g.K * g.Cp) * (t == DC_W ? 2 : 4);
+        d.stride_w = cp, d.stride_h = g.K * cp, d.stride_n = g.K * g.K * cp;
+        d.bytes = (size_t)(g.F * g.K * g.K * cp) * (t == DC_W ? 2 : 4);
         break;
+    }
     default:
         fail(DC_ERR_ARG, "unknown tensor kind");
     }
@@ -565,6 +614,8 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
 // halo exchange
 // ---------------------------------------------------------------------------
 P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf);
+bool is_local(const dc_plan_s *pl);
+void resolve_local_peers(dc_plan_s *pl);
 
 // Forward with the P2P halo exchange fused into the single conv_v2 launch:
 // tile-aligned rects (16 x 8 tiles, pairs of 32 rows) with the interior first
@@ -610,6 +661,13 @@ P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf) {
                "direct P2P halo exchange needs the buffer from dc_buffer_alloc (or pass DC_HALO_NCCL)");
     DC_REQUIRE(sends.size() <= 8 && recvs.size() <= 8, DC_ERR_ARG, "too many halo neighbours");
     DC_REQUIRE(B.dev_epoch != nullptr, DC_ERR_ARG, "P2P halo exchange: buffer not registered");
+    resolve_local_peers(pl);
+    for (auto &m : sends)
+        DC_REQUIRE(B.peer.count(m.peer) && pl->peer_flags.count(m.peer), DC_ERR_ARG,
+                   "P2P halo exchange: rank %d's buffer is not mapped (dc_buffer_alloc on every rank)", m.peer);
+    for (auto &m : recvs)
+        DC_REQUIRE(pl->peer_flags.count(m.peer), DC_ERR_ARG, "P2P halo exchange: rank %d's flags are not mapped",
+                   m.peer);
     auto strides = [&](int64_t hb, int64_t wb, BlockCopy &c, bool src) {
         const long long sw = vec16, sh = wb * vec16, sn = hb * wb * vec16;
         if (src) c.s_sn = sn, c.s_sh = sh, c.s_sw = sw;
@@ -637,8 +695,10 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
     const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
     const auto &recvs = which == 0 ? rp.x_recv : rp.dy_recv;
     if (sends.empty() && recvs.empty()) return;
-    DC_REQUIRE(!pl->is_virtual && pl->comm && pl->comm->nccl, DC_ERR_ARG,
+    DC_REQUIRE(!pl->is_virtual && pl->comm && (pl->comm->nccl || pl->comm->group), DC_ERR_ARG,
                "halo exchange needs a communicator (virtual plan or world 1)");
+    DC_REQUIRE(!(is_local(pl) && (flags & DC_HALO_NCCL)), DC_ERR_UNSUPPORTED,
+               "DC_HALO_NCCL needs real ranks (loopback group)");
     const int64_t cp = which == 0 ? rp.g.Cp : rp.g.Fp;
     const int vec16 = (int)(cp * 2 / 16);
     const int64_t nl = rp.nrange.size();
@@ -704,17 +764,26 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
 }
 
 // All-gather fixed-size blobs over NCCL (host in/out); used for IPC handles.
-std::vector<uint8_t> allgather_bytes(dc_plan_s *pl, const void *mine, size_t n) {
-    const int W = pl->world();
+// All-gather fixed-size blobs over the communicator's NCCL (host in/out); used
+// for IPC handles and for checking that every rank chose the same grid.
+std::vector<uint8_t> comm_allgather(dc_comm_s *c, const void *mine, size_t n) {
+    const int W = c->world;
+    DC_REQUIRE(c->nccl != nullptr, DC_ERR_ARG, "all-gather needs an NCCL communicator");
     uint8_t *d = nullptr;
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     CK(cudaMalloc(&d, n * (W + 1)));
     CK(cudaMemcpy(d + n * W, mine, n, cudaMemcpyHostToDevice));
-    NK(ncclAllGather(d + n * W, d, n, ncclUint8, pl->nccl(), pl->s_comm));
-    CK(cudaStreamSynchronize(pl->s_comm));
+    NK(ncclAllGather(d + n * W, d, n, ncclUint8, c->nccl, s));
+    CK(cudaStreamSynchronize(s));
     std::vector<uint8_t> out(n * W);
     CK(cudaMemcpy(out.data(), d, n * W, cudaMemcpyDeviceToHost));
     CK(cudaFree(d));
+    CK(cudaStreamDestroy(s));
     return out;
+}
+std::vector<uint8_t> allgather_bytes(dc_plan_s *pl, const void *mine, size_t n) {
+    return comm_allgather(pl->comm, mine, n);
 }
 
 std::vector<int> neighbours(const RankPlan &rp, int which) {
@@ -723,6 +792,37 @@ std::vector<int> neighbours(const RankPlan &rp, int which) {
         for (auto &m : *L)
             if (std::find(v.begin(), v.end(), m.peer) == v.end()) v.push_back(m.peer);
     return v;
+}
+
+bool is_local(const dc_plan_s *pl) { return pl->comm && pl->comm->group; }
+
+// Loopback group: the plan of `rank` with this plan's sequence number.
+dc_plan_s *local_peer(dc_plan_s *pl, int rank) {
+    LocalGroup &G = *pl->comm->group;
+    std::lock_guard<std::mutex> lk(G.mu);
+    auto it = G.plans.find({pl->seq, rank});
+    DC_REQUIRE(it != G.plans.end(), DC_ERR_ARG, "loopback group: rank %d has not created plan #%d", rank, pl->seq);
+    return it->second;
+}
+
+// Loopback group: resolve the cross-rank pointers (neighbours' flags and
+// margined buffers, the BN group's mailboxes) from the registry. Called before
+// every use, since a buffer may be allocated after the neighbour's plan.
+void resolve_local_peers(dc_plan_s *pl) {
+    if (!is_local(pl) || pl->world() <= 1) return;
+    std::vector<int> nb = neighbours(pl->rp, 0);
+    for (int p : neighbours(pl->rp, 1))
+        if (std::find(nb.begin(), nb.end(), p) == nb.end()) nb.push_back(p);
+    for (int p : nb) {
+        dc_plan_s *q = local_peer(pl, p);
+        pl->peer_flags[p] = q->flags;
+        for (int which = 0; which < 2; ++which)
+            if (q->buf[which].ptr) pl->buf[which].peer[p] = q->buf[which].ptr;
+    }
+    if (pl->bn_p2p) {
+        const int lo = pl->rp.in * pl->bn_group;
+        for (int k = 0; k < pl->bn_group; ++k) pl->bn_peer_mail[k] = local_peer(pl, lo + k)->bn_mail;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1021,7 +1121,7 @@ int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split, bool all
 }
 
 void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cudaStream_t st,
-                    bool deterministic) {
+                    bool allow_atomic) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t xd = describe(rp, DC_X), dyd = describe(rp, DC_DY);
@@ -1044,19 +1144,20 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
             q.tiles_w = (int)ceil_div(wo, (int64_t)q.bw);
             q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
             const int mgroups = wgrad_v2_mgroups(q), ntiles = (int)ceil_div(g.Fp, q.bn);
-            const long long per_split = (long long)g.F * q.T * g.Cp;
+            const long long per_split = (long long)g.F * q.T * g.C;  // dW: [F][K][K][C]
+            const long long split_stride = round_up(per_split, 4);
+            q.C = (int)g.C;
             bool atomic = false;
-            static const bool force_det = std::getenv("DC_WGRAD_DETERMINISTIC") != nullptr;
-            const int splits = wgrad_splits(q, mgroups * ntiles, per_split, !deterministic && !force_det, &atomic);
+            const int splits = wgrad_splits(q, mgroups * ntiles, split_stride, allow_atomic, &atomic);
             q.splits = splits;
-            q.ws_split = per_split;
+            q.ws_split = split_stride;
             if (splits > 1 && atomic) {
                 // splits accumulate into the zeroed dW (no partials, no reduce
                 // launch); fp32 addition order varies run to run (DC_DETERMINISTIC)
                 CK(cudaMemsetAsync(dw, 0, (size_t)per_split * 4, st));
                 q.ws = dw, q.ws_split = 0, q.atomic_out = 1;
             } else if (splits > 1) {
-                ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * per_split * 4);
+                ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
                 q.ws = pl->ws;
             } else {
                 q.ws = dw;
@@ -1078,7 +1179,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
                 make_tmap(&dymap, dy_owned, 4, dims, strides, box, nullptr, 128);
             }
             launch_wgrad_v2(xmap, dymap, q, st);
-            if (splits > 1 && !q.atomic_out) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+            if (splits > 1 && !q.atomic_out) launch_splitk_reduce(pl->ws, splits, per_split, split_stride, dw, st);
             return;
         }
     }
@@ -1090,7 +1191,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     p.pairs_total = p.T * p.kc;
     p.bf = g.Fp % 64 == 0 ? 64 : g.Fp % 32 == 0 ? 32 : 16;
     p.bn = g.Fp <= 256 ? (int)g.Fp : 256;
-    p.stages = (16384 + p.bn * 128) <= 32768 ? 4 : 4;
+    p.stages = 4;
     for (int a = 0; a < g.K; ++a)
         for (int b = 0; b < g.K; ++b) {
             p.tap_h[a * g.K + b] = (int8_t)a;
@@ -1107,16 +1208,18 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     const int ppm = 128 / p.bkc;
     const int m_tiles = (int)ceil_div(p.pairs_total, ppm);
     const int n_tiles = (int)ceil_div(g.F, p.bn);
-    const long long per_split = (long long)g.F * p.T * g.Cp;
+    const long long per_split = (long long)g.F * p.T * g.C;  // dW: [F][K][K][C]
+    const long long split_stride = round_up(per_split, 4);
     int splits = (int)ceil_div(296, (int64_t)m_tiles * n_tiles);
     splits = std::max(1, std::min(splits, std::max(1, p.nblocks / 4)));
-    while (splits > 1 && (size_t)splits * per_split * 4 > ((size_t)1 << 30)) --splits;
+    while (splits > 1 && (size_t)splits * split_stride * 4 > ((size_t)1 << 30)) --splits;
     p.splits = splits;
     p.F = (int)g.F;
     p.cp = (int)g.Cp;
-    p.ws_split = per_split;
+    p.C = (int)g.C;
+    p.ws_split = split_stride;
     if (splits > 1) {
-        ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * per_split * 4);
+        ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
         p.ws = pl->ws;
     } else {
         p.ws = dw;
@@ -1126,7 +1229,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     // dy WITHOUT its halo: a map over the owned block only
     nhwc_map(&dymap, dy_owned, nl, ho, wo, g.Fp, dyd.wb, dyd.hb * dyd.wb, p.bf, tw, th, 1);
     launch_wgrad(xmap, dymap, p, m_tiles, n_tiles, st);
-    if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, dw, st);
+    if (splits > 1) launch_splitk_reduce(pl->ws, splits, per_split, split_stride, dw, st);
 }
 
 // Early "ready" signal (P2P halo protocol): after the last consumer of a
@@ -1135,7 +1238,9 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
 // the next exchange does not wait for a handshake. The exchange kernel also
 // signals ready for its own epoch, so this is an optimisation, never required.
 void signal_ready_next(dc_plan_s *pl, int which, const void *buf, cudaStream_t st) {
-    if (pl->is_virtual || pl->world() <= 1 || pl->peer_flags.empty()) return;
+    if (pl->is_virtual || pl->world() <= 1) return;
+    resolve_local_peers(pl);
+    if (pl->peer_flags.empty()) return;
     const BufState &B = pl->buf[which];
     if (B.ptr != buf) return;  // the P2P protocol applies to dc_buffer_alloc buffers only
     const auto &recvs = which == 0 ? pl->rp.x_recv : pl->rp.dy_recv;
@@ -1147,9 +1252,10 @@ void signal_ready_next(dc_plan_s *pl, int which, const void *buf, cudaStream_t s
 
 void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
     if (pl->world() <= 1) return;
+    DC_REQUIRE(!is_local(pl), DC_ERR_UNSUPPORTED, "dW allreduce needs real ranks (loopback group: DC_ALLREDUCE off)");
     DC_REQUIRE(pl->nccl() != nullptr, DC_ERR_ARG, "allreduce needs a communicator");
     const ConvGeom &g = pl->rp.g;
-    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, pl->nccl(), st));
+    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.C, ncclFloat32, ncclSum, pl->nccl(), st));
 }
 
 // DC_ALLREDUCE_ASYNC: the allreduce waits for the work queued on `st` so far
@@ -1157,12 +1263,13 @@ void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
 // does not wait for it (dc_comm_sync joins).
 void allreduce_dw_async(dc_plan_s *pl, float *dw, cudaStream_t st) {
     if (pl->world() <= 1) return;
+    DC_REQUIRE(!is_local(pl), DC_ERR_UNSUPPORTED, "dW allreduce needs real ranks (loopback group: DC_ALLREDUCE off)");
     dc_comm_s *c = pl->comm;
     DC_REQUIRE(c && c->grad_nccl, DC_ERR_ARG, "allreduce needs a communicator");
     const ConvGeom &g = pl->rp.g;
     CK(cudaEventRecord(c->ev_in, st));
     CK(cudaStreamWaitEvent(c->s_grad, c->ev_in, 0));
-    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.Cp, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
+    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.C, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
     c->grad_pending = true;
 }
 
@@ -1185,9 +1292,11 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
         pl->is_virtual = is_virtual;
         pl->bn_group = grid.ph * grid.pw;  // BN group: ranks with equal i_N
         if (!is_virtual) {
+            pl->seq = comm ? comm->plan_seq++ : 0;
             ensure_local_resources(pl);
             if (grid.size() > 1) {
-                if (pl->bn_group > 1) {
+                const bool local = comm->group != nullptr;
+                if (pl->bn_group > 1 && !local) {
                     if (grid.pn == 1) {
                         pl->bn_comm = comm->nccl;
                     } else {
@@ -1203,18 +1312,51 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
                 CK(cudaMemset(pl->dev_epochs, 0, sizeof(uint32_t) * 4));
                 pl->buf[0].dev_epoch = pl->dev_epochs;
                 pl->buf[1].dev_epoch = pl->dev_epochs + 2;
-                cudaIpcMemHandle_t h;
-                CK(cudaIpcGetMemHandle(&h, pl->flags));
-                auto all = allgather_bytes(pl, &h, sizeof h);
-                std::vector<int> nb = neighbours(pl->rp, 0);
-                for (int p : neighbours(pl->rp, 1))
-                    if (std::find(nb.begin(), nb.end(), p) == nb.end()) nb.push_back(p);
-                for (int p : nb) {
-                    cudaIpcMemHandle_t ph;
-                    std::memcpy(&ph, all.data() + p * sizeof ph, sizeof ph);
-                    void *ptr = nullptr;
-                    CK(cudaIpcOpenMemHandle(&ptr, ph, cudaIpcMemLazyEnablePeerAccess));
-                    pl->peer_flags[p] = reinterpret_cast<uint32_t *>(ptr);
+                // the BN group's one-shot NVLink mailbox (<= 8 members; NCCL beyond,
+                // or with DC_BN_NCCL on real ranks)
+                const int gsz = pl->bn_group;
+                if (gsz > 1 && gsz <= kMaxBnGroup && (local || !std::getenv("DC_BN_NCCL"))) {
+                    const size_t bytes = 256 + (size_t)2 * gsz * 2 * g.Fp * sizeof(double);
+                    CK(cudaMalloc(&pl->bn_mail, bytes));
+                    CK(cudaMemset(pl->bn_mail, 0, bytes));
+                    CK(cudaMalloc(&pl->bn_epoch, sizeof(uint32_t)));
+                    CK(cudaMemset(pl->bn_epoch, 0, sizeof(uint32_t)));
+                    pl->bn_p2p = true;
+                    pl->bn_peer_mail.assign(gsz, nullptr);
+                    pl->bn_peer_mail[rank - pl->rp.in * gsz] = pl->bn_mail;
+                }
+                if (local) {
+                    std::lock_guard<std::mutex> lk(comm->group->mu);
+                    comm->group->plans[{pl->seq, rank}] = pl;
+                } else {
+                    struct Handles {
+                        cudaIpcMemHandle_t flags, bn;
+                    } h{};
+                    CK(cudaIpcGetMemHandle(&h.flags, pl->flags));
+                    if (pl->bn_p2p) CK(cudaIpcGetMemHandle(&h.bn, pl->bn_mail));
+                    auto all = allgather_bytes(pl, &h, sizeof h);
+                    auto at = [&](int r) {
+                        Handles x;
+                        std::memcpy(&x, all.data() + r * sizeof x, sizeof x);
+                        return x;
+                    };
+                    std::vector<int> nb = neighbours(pl->rp, 0);
+                    for (int p : neighbours(pl->rp, 1))
+                        if (std::find(nb.begin(), nb.end(), p) == nb.end()) nb.push_back(p);
+                    for (int p : nb) {
+                        void *ptr = nullptr;
+                        CK(cudaIpcOpenMemHandle(&ptr, at(p).flags, cudaIpcMemLazyEnablePeerAccess));
+                        pl->peer_flags[p] = reinterpret_cast<uint32_t *>(ptr);
+                    }
+                    if (pl->bn_p2p) {
+                        const int lo = pl->rp.in * gsz;
+                        for (int k = 0; k < gsz; ++k) {
+                            if (lo + k == rank) continue;
+                            void *ptr = nullptr;
+                            CK(cudaIpcOpenMemHandle(&ptr, at(lo + k).bn, cudaIpcMemLazyEnablePeerAccess));
+                            pl->bn_peer_mail[k] = reinterpret_cast<uint8_t *>(ptr);
+                        }
+                    }
                 }
                 CK(cudaDeviceSynchronize());
             }
@@ -1246,42 +1388,6 @@ dc_status_t dc_comm_unique_id(void *uid128) {
     DC_API_END
 }
 
-// Mailbox for the P2P BN allreduce: allocated here, its IPC handle all-gathered
-// over NCCL, every peer's opened (one node, <= 8 ranks with peer access;
-// otherwise the BN allreduce stays on NCCL).
-void setup_bn_mailbox(dc_comm_s *c) {
-    if (c->world > kMaxBnGroup || std::getenv("DC_BN_NCCL")) return;
-    const size_t bytes = 256 + (size_t)2 * c->world * kBnMaxDoubles * sizeof(double);
-    CK(cudaMalloc(&c->bn_mail, bytes));
-    CK(cudaMemset(c->bn_mail, 0, bytes));
-    CK(cudaMalloc(&c->bn_epoch, sizeof(uint32_t)));
-    CK(cudaMemset(c->bn_epoch, 0, sizeof(uint32_t)));
-    cudaIpcMemHandle_t h;
-    CK(cudaIpcGetMemHandle(&h, c->bn_mail));
-    cudaStream_t s;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    uint8_t *d = nullptr;
-    CK(cudaMalloc(&d, sizeof h * (c->world + 1)));
-    CK(cudaMemcpy(d + sizeof h * c->world, &h, sizeof h, cudaMemcpyHostToDevice));
-    NK(ncclAllGather(d + sizeof h * c->world, d, sizeof h, ncclUint8, c->nccl, s));
-    CK(cudaStreamSynchronize(s));
-    std::vector<cudaIpcMemHandle_t> all(c->world);
-    CK(cudaMemcpy(all.data(), d, sizeof h * c->world, cudaMemcpyDeviceToHost));
-    CK(cudaFree(d));
-    CK(cudaStreamDestroy(s));
-    c->bn_peer_mail.assign(c->world, nullptr);
-    for (int r = 0; r < c->world; ++r) {
-        if (r == c->rank) {
-            c->bn_peer_mail[r] = c->bn_mail;
-            continue;
-        }
-        void *ptr = nullptr;
-        CK(cudaIpcOpenMemHandle(&ptr, all[r], cudaIpcMemLazyEnablePeerAccess));
-        c->bn_peer_mail[r] = reinterpret_cast<uint8_t *>(ptr);
-    }
-    c->bn_p2p = true;
-}
-
 dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, dc_comm_t *out) {
     DC_API_BEGIN
     DC_REQUIRE(out != nullptr && world >= 1 && rank >= 0 && rank < world, DC_ERR_ARG,
@@ -1299,7 +1405,6 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
             fail(DC_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
         }
         NK(ncclCommSplit(c->nccl, 0, rank, &c->grad_nccl, nullptr));
-        setup_bn_mailbox(c);
         CK(cudaStreamCreateWithFlags(&c->s_grad, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
@@ -1308,15 +1413,26 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
     DC_API_END
 }
 
+dc_status_t dc_comm_create_local(int world, int device, dc_comm_t *comms) {
+    DC_API_BEGIN
+    DC_REQUIRE(comms != nullptr && world >= 1 && world <= 64, DC_ERR_ARG, "bad loopback world %d", world);
+    CK(cudaSetDevice(device));
+    auto G = std::make_shared<LocalGroup>();
+    G->world = world;
+    for (int r = 0; r < world; ++r) {
+        auto *c = new dc_comm_s();
+        c->rank = r, c->world = world, c->device = device;
+        c->group = G;
+        comms[r] = c;
+    }
+    DC_API_END
+}
+
 dc_status_t dc_comm_destroy(dc_comm_t c) {
     DC_API_BEGIN
     if (c) {
         if (c->s_grad) cudaStreamSynchronize(c->s_grad);
         cudaDeviceSynchronize();
-        for (int r = 0; r < (int)c->bn_peer_mail.size(); ++r)
-            if (r != c->rank && c->bn_peer_mail[r]) cudaIpcCloseMemHandle(c->bn_peer_mail[r]);
-        if (c->bn_mail) cudaFree(c->bn_mail);
-        if (c->bn_epoch) cudaFree(c->bn_epoch);
         if (c->grad_nccl) ncclCommDestroy(c->grad_nccl);
         if (c->nccl) ncclCommDestroy(c->nccl);
         if (c->s_grad) cudaStreamDestroy(c->s_grad);
@@ -1353,6 +1469,24 @@ dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F
         DC_REQUIRE(model_choose(g, world, grid, pred, grid), DC_ERR_PARTITION,
                    "no valid decomposition of %d ranks with (%d,%d,%d) fixed", world, decomp.pn, decomp.ph,
                    decomp.pw);
+        // every rank ran the model on its own process-local state (cost table,
+        // comm terms): check that they agree before building neighbour lists
+        if (world > 1) {
+            const std::array<int, 3> mine{grid.pn, grid.ph, grid.pw};
+            if (comm->group) {
+                std::lock_guard<std::mutex> lk(comm->group->mu);
+                auto it = comm->group->grids.emplace(comm->plan_seq, mine).first;
+                DC_REQUIRE(it->second == mine, DC_ERR_PARTITION,
+                           "ranks chose different grids: (%d,%d,%d) here, (%d,%d,%d) on the first rank", grid.pn,
+                           grid.ph, grid.pw, it->second[0], it->second[1], it->second[2]);
+            } else {
+                const auto all = comm_allgather(comm, mine.data(), sizeof mine);
+                for (int r = 0; r < world; ++r)
+                    DC_REQUIRE(std::memcmp(all.data() + r * sizeof mine, mine.data(), sizeof mine) == 0,
+                               DC_ERR_PARTITION, "ranks chose different grids (rank %d differs from rank %d)", r,
+                               rank);
+            }
+        }
     } else {
         DC_REQUIRE(grid.size() == world, DC_ERR_PARTITION, "grid (%d,%d,%d) has %d ranks, world is %d",
                    grid.pn, grid.ph, grid.pw, grid.size(), world);
@@ -1436,7 +1570,7 @@ dc_status_t dc_buffer_alloc(dc_plan_t pl, dc_tensor_t t, void **dev_ptr) {
     B.owned = true;
     B.bytes = d.bytes;
     CK(cudaMemset(B.ptr, 0, std::max<size_t>(d.bytes, 256)));
-    if (pl->world() > 1) {
+    if (pl->world() > 1 && !is_local(pl)) {  // (loopback: peers resolve it from the registry)
         cudaIpcMemHandle_t h;
         CK(cudaIpcGetMemHandle(&h, B.ptr));
         auto all = allgather_bytes(pl, &h, sizeof h);
@@ -1469,6 +1603,8 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     GemmLaunch L;
     prepare_fwd(pl, x, w, y, L);
     pl->bn_fused_y = nullptr;
+    pl->bn_fused_epoch = 0;
+    ++pl->fwd_epoch;
     if (flags & DC_BN_STATS) {
         L.bn_slot_cap = 8 * device_sm_count();
         ensure_alloc(pl->bn_fpart, pl->bn_fpart_bytes, sizeof(double) * L.bn_slot_cap * 2 * pl->rp.g.Fp);
@@ -1507,6 +1643,7 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     if (L.bn_part && L.bn_ok && L.bn_slot > 0) {  // dc_bn_spatial_stats(y) reduces these
         pl->bn_fused_y = y;
         pl->bn_fused_slots = L.bn_slot;
+        pl->bn_fused_epoch = pl->fwd_epoch;
     }
     DC_API_END
 }
@@ -1527,7 +1664,7 @@ dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, floa
     DC_REQUIRE(pl && x && dy && dw, DC_ERR_ARG, "null argument");
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
-    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DETERMINISTIC) != 0);
+    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DW_ATOMIC) != 0);
     signal_ready_next(pl, 0, x, st);
     if ((flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC)) allreduce_dw_async(pl, dw, st);
     else if (flags & DC_ALLREDUCE) allreduce_dw(pl, dw, st);
@@ -1549,7 +1686,7 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
         exchange(pl, 1, dy, flags, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
     }
-    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DETERMINISTIC) != 0);
+    run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DW_ATOMIC) != 0);
     signal_ready_next(pl, 0, x, st);
     if (ar_async) allreduce_dw_async(pl, dw, st);
     if (ar) {  // dW allreduce on the comm stream, concurrent with the data gradient
@@ -1565,10 +1702,11 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
     DC_API_END
 }
 
-dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, double *var,
-                                int local_only, void *stream) {
+dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, double *var, unsigned flags,
+                                void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && t && mean && var, DC_ERR_ARG, "null argument");
+    DC_REQUIRE((flags & ~(DC_BN_LOCAL | DC_BN_FROM_FWD)) == 0, DC_ERR_ARG, "unknown BN flags 0x%x", flags);
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
     const RankPlan &rp = pl->rp;
@@ -1576,29 +1714,35 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     const long long npix = rp.nrange.size() * rp.h.out.size() * rp.w.out.size();
     const size_t need = sizeof(double) * 2 * g.Fp * bn_partial_blocks(npix, (int)g.Fp);
     ensure_alloc(pl->bn_part, pl->bn_part_bytes, need);
-    const bool global = !local_only && pl->bn_group > 1;
+    const bool global = !(flags & DC_BN_LOCAL) && pl->bn_group > 1;
+    // the partials of this plan's latest forward, if it ran with DC_BN_STATS
+    // on this tensor and the caller states t is unchanged since (DC_BN_FROM_FWD);
+    // consumed once. Otherwise t is read (bn_sums_kernel).
+    const bool fused = (flags & DC_BN_FROM_FWD) && pl->bn_fused_y == t && pl->bn_fused_epoch != 0 &&
+                       pl->bn_fused_epoch == pl->fwd_epoch && pl->bn_fused_slots > 0;
     // single group: the reduce kernel also finalises mean/var (no allreduce between)
-    if (pl->bn_fused_y == t && pl->bn_fused_slots > 0)  // partials from the fused forward epilogue
+    if (fused)
         launch_bn_reduce(pl->bn_fpart, pl->bn_fused_slots, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix,
                          global ? nullptr : mean, global ? nullptr : var, st);
     else
         launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
                        (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
-    if (global && pl->comm && pl->comm->bn_p2p) {
+    pl->bn_fused_y = nullptr;
+    pl->bn_fused_epoch = 0;
+    if (global && pl->bn_p2p) {
         // one-shot NVLink allreduce among the ranks with this rank's i_N
-        dc_comm_s *c = pl->comm;
+        resolve_local_peers(pl);
         BnP2P b{};
         b.gsize = pl->bn_group;
-        const int lo = rp.in * pl->bn_group;
         for (int k = 0; k < b.gsize; ++k) {
-            b.ranks[k] = lo + k;
-            b.peer_box[k] = reinterpret_cast<double *>(c->bn_peer_mail[lo + k] + 256);
-            b.peer_flags[k] = reinterpret_cast<uint32_t *>(c->bn_peer_mail[lo + k]);
+            DC_REQUIRE(pl->bn_peer_mail[k] != nullptr, DC_ERR_ARG, "BN mailbox of group member %d not mapped", k);
+            b.peer_box[k] = reinterpret_cast<double *>(pl->bn_peer_mail[k] + 256);
+            b.peer_flags[k] = reinterpret_cast<uint32_t *>(pl->bn_peer_mail[k]);
         }
-        b.my_box = reinterpret_cast<const double *>(c->bn_mail + 256);
-        b.my_flags = reinterpret_cast<const uint32_t *>(c->bn_mail);
-        b.my_rank = c->rank, b.world = c->world;
-        b.epoch = c->bn_epoch;
+        b.my_box = reinterpret_cast<const double *>(pl->bn_mail + 256);
+        b.my_flags = reinterpret_cast<const uint32_t *>(pl->bn_mail);
+        b.my_idx = rp.rank - rp.in * pl->bn_group;
+        b.epoch = pl->bn_epoch;
         b.local = pl->bn_sums;
         b.cpad = (int)g.Fp, b.c = (int)g.F;
         b.count = (double)rp.nrange.size() * g.Ho * g.Wo;

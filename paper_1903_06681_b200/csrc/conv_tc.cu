@@ -258,10 +258,10 @@ __global__ void __launch_bounds__(128, 1)
     tc_fence_after();
     const int m = warp * 32 + lane;
     const int pair = mt * PPM + m / p.bkc;
-    const bool valid = pair < p.pairs_total;
     const int t = pair / p.kc, c = (pair - t * p.kc) * p.bkc + (m % p.bkc);
-    float *wrow = p.ws + (long long)split * p.ws_split + (long long)t * p.cp + c;
-    const long long fstride = (long long)p.T * p.cp;
+    const bool valid = pair < p.pairs_total && c < p.C;  // (dW holds the C logical channels)
+    float *wrow = p.ws + (long long)split * p.ws_split + (long long)t * p.C + c;
+    const long long fstride = (long long)p.T * p.C;
     const uint32_t t_lane = tmem + ((uint32_t)(warp * 32) << 16);
     for (int c16 = 0; c16 < p.bn / 16; ++c16) {
         uint32_t v[16];
@@ -285,21 +285,31 @@ __global__ void __launch_bounds__(128, 1)
     if (warp == 0) tmem_dealloc(tmem, ncols);
 }
 
-// Deterministic split-K reduction: dw[i] = sum_{s in order} ws[s][i].
-__global__ void splitk_reduce_kernel(const float4 *__restrict__ ws, int splits, long long n4,
-                                     long long split4, float4 *__restrict__ dw) {
+// Deterministic split-K reduction: dw[i] = sum_{s in order} ws[s][i]
+// (16-byte vectors; scalar when n is not a multiple of 4).
+__global__ void splitk_reduce_kernel(const float *__restrict__ ws, int splits, long long n, long long split_stride,
+                                     float *__restrict__ dw) {
     pdl_wait();  // (launch.cuh: PDL)
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+    const bool vec = (n % 4) == 0 && (reinterpret_cast<uintptr_t>(dw) & 15) == 0;
+    const long long nv = vec ? n / 4 : n;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nv;
          i += (long long)gridDim.x * blockDim.x) {
-        float4 acc = ws[i];
-        for (int s = 1; s < splits; ++s) {
-            const float4 v = ws[s * split4 + i];
-            acc.x += v.x;
-            acc.y += v.y;
-            acc.z += v.z;
-            acc.w += v.w;
+        if (vec) {
+            const float4 *w4 = reinterpret_cast<const float4 *>(ws);
+            float4 acc = w4[i];
+            for (int s = 1; s < splits; ++s) {
+                const float4 v = w4[s * (split_stride / 4) + i];
+                acc.x += v.x;
+                acc.y += v.y;
+                acc.z += v.z;
+                acc.w += v.w;
+            }
+            reinterpret_cast<float4 *>(dw)[i] = acc;
+        } else {
+            float acc = ws[i];
+            for (int s = 1; s < splits; ++s) acc += ws[s * split_stride + i];
+            dw[i] = acc;
         }
-        dw[i] = acc;
     }
 }
 
@@ -425,12 +435,13 @@ void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradP
     ++g_launches;
 }
 
-void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, cudaStream_t st) {
-    DC_REQUIRE(n % 4 == 0, DC_ERR_ARG, "split-K reduce needs a multiple of 4 elements");
-    const long long n4 = n / 4;
-    const int blocks = (int)std::min<long long>((n4 + 255) / 256, 148 * 8);
-    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "split-K reduce",
-             reinterpret_cast<const float4 *>(ws), splits, n4, n4, reinterpret_cast<float4 *>(dw));
+void launch_splitk_reduce(const float *ws, int splits, long long n, long long split_stride, float *dw,
+                          cudaStream_t st) {
+    DC_REQUIRE(split_stride % 4 == 0 && split_stride >= n, DC_ERR_ARG, "split-K workspace stride");
+    const long long nv = n % 4 == 0 ? n / 4 : n;
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((nv + 255) / 256, 148 * 8));
+    launch_k(splitk_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "split-K reduce", ws, splits, n, split_stride,
+             dw);
 }
 
 void launch_weight_transform_multi(const __nv_bfloat16 *w, __nv_bfloat16 *wt_base, int F, int Fp, int C, int Cp,

@@ -55,9 +55,9 @@ struct WgradParams {
     int tw_log2;         // pixel block = (64 >> tw_log2) x (1 << tw_log2)
     int tiles_h, tiles_w, nblocks;  // pixel blocks per sample, total over samples
     int splits;
-    float *ws;           // [splits][F][T][cp]
-    long long ws_split;  // elements per split
-    int F, cp;
+    float *ws;           // [splits][F][T][C] (dW itself when splits == 1)
+    long long ws_split;  // elements per split (>= F * T * C, a multiple of 4)
+    int F, cp, C;        // filters, padded / logical input channels
 };
 
 // ---- host helpers ----
@@ -70,7 +70,8 @@ void launch_conv_gemm(const CUtensorMap &amap, const CUtensorMap &bmap, const Co
                       int nsamples, int nout_tiles, cudaStream_t st);
 void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradParams &p,
                   int m_tiles, int n_tiles, cudaStream_t st);
-void launch_splitk_reduce(const float *ws, int splits, long long n, float *dw, cudaStream_t st);
+void launch_splitk_reduce(const float *ws, int splits, long long n, long long split_stride, float *dw,
+                          cudaStream_t st);
 // W'[c][t][f] = w[f][ka[t]][kb[t]][c] for the backward-data taps (zero if c >= C or f >= F)
 // All stride phases at once: tap j (of ntaps) reads w tap (ka[j], kb[j]) and
 // writes index t[j] of its phase's [Cp][T[j]][Fp] block at wt_base + off[j].

@@ -299,13 +299,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             const TileCoord c = decode(p, item_of(w, phantom));
             if (!halo_ready && c.r >= p.halo_rect0) {
                 // the neighbours' slabs of this epoch are in my margins
-                if ((int)lane < p.hx.n_data_in) {
-                    const uint32_t target = kP2PBlocks * halo_e;
-                    uint32_t v;
-                    do {
-                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p.hx.data_in[lane]) : "memory");
-                    } while ((int)(v - target) < 0);
-                }
+                if ((int)lane < p.hx.n_data_in) spin_until_geq(p.hx.data_in[lane], kP2PBlocks * halo_e);
                 __syncwarp();
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
                 halo_ready = true;
@@ -509,12 +503,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[lane]), "r"(halo_e) : "memory");
             }
             for (int sl = blockIdx.x; sl < kP2PBlocks; sl += gridDim.x) {
-                if ((int)lane < x.n_ready_in) {
-                    uint32_t v;
-                    do {
-                        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.ready_in[lane]) : "memory");
-                    } while ((int)(v - halo_e) < 0);
-                }
+                if ((int)lane < x.n_ready_in) spin_until_geq(x.ready_in[lane], halo_e);
                 __syncwarp();
                 for (int k = 0; k < x.copies.count; ++k) {
                     const BlockCopy &cp = x.copies.c[k];

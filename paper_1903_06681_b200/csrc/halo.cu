@@ -237,12 +237,7 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
         __threadfence_system();
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[threadIdx.x]), "r"(e) : "memory");
     }
-    if ((int)threadIdx.x < x.n_ready_in) {
-        uint32_t v;
-        do {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.ready_in[threadIdx.x]) : "memory");
-        } while ((int)(v - e) < 0);
-    }
+    if ((int)threadIdx.x < x.n_ready_in) spin_until_geq(x.ready_in[threadIdx.x], e);
     __syncthreads();
     for (int k = 0; k < x.copies.count; ++k) {
         const BlockCopy &c = x.copies.c[k];
@@ -263,11 +258,7 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
     }
     // block 0 returns only when every sender's blocks have delivered epoch e
     if (blockIdx.x == 0 && (int)threadIdx.x < x.n_data_in) {
-        const uint32_t target = kP2PBlocks * e;
-        uint32_t v;
-        do {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.data_in[threadIdx.x]) : "memory");
-        } while ((int)(v - target) < 0);
+        spin_until_geq(x.data_in[threadIdx.x], kP2PBlocks * e);
         __threadfence_system();
     }
     __syncthreads();
@@ -290,31 +281,25 @@ __global__ void __launch_bounds__(256) bn_allreduce_p2p_kernel(const __grid_cons
     const uint32_t e = *reinterpret_cast<volatile uint32_t *>(b.epoch) + 1;
     const int par = e & 1;
     const int n2 = 2 * b.cpad;
-    const long long slot = (long long)kBnMaxDoubles;
-    const long long par_stride = (long long)b.world * slot;
-    // 1. my sums into slot [par][my_rank] of every member (me included)
+    const long long slot = n2;
+    const long long par_stride = (long long)b.gsize * slot;
+    // 1. my sums into slot [par][my_idx] of every member (me included)
     for (int k = 0; k < b.gsize; ++k) {
-        double *dst = b.peer_box[k] + par * par_stride + b.my_rank * slot;
+        double *dst = b.peer_box[k] + par * par_stride + b.my_idx * slot;
         for (int i = threadIdx.x; i < n2; i += blockDim.x) dst[i] = b.local[i];
     }
     __threadfence_system();
     __syncthreads();
     if ((int)threadIdx.x < b.gsize)
-        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b.peer_flags[threadIdx.x] + b.my_rank), "r"(e)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(b.peer_flags[threadIdx.x] + b.my_idx), "r"(e)
                      : "memory");
     // 2. wait until every member has delivered epoch e
-    if ((int)threadIdx.x < b.gsize) {
-        const uint32_t *f = b.my_flags + b.ranks[threadIdx.x];
-        uint32_t v;
-        do {
-            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-        } while ((int)(v - e) < 0);
-    }
+    if ((int)threadIdx.x < b.gsize) spin_until_geq(b.my_flags + threadIdx.x, e);
     __syncthreads();
     // 3. fixed-order sum over the members (uncached loads: peers wrote them)
     for (int i = threadIdx.x; i < n2; i += blockDim.x) {
         double acc = 0.0;
-        for (int k = 0; k < b.gsize; ++k) acc += __ldcv(b.my_box + par * par_stride + b.ranks[k] * slot + i);
+        for (int k = 0; k < b.gsize; ++k) acc += __ldcv(b.my_box + par * par_stride + k * slot + i);
         b.sums[i] = acc;
     }
     __syncthreads();
@@ -328,10 +313,8 @@ __global__ void __launch_bounds__(256) bn_allreduce_p2p_kernel(const __grid_cons
 }
 
 void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st) {
-    DC_REQUIRE(2 * b.cpad <= kBnMaxDoubles && b.gsize <= kMaxBnGroup, DC_ERR_UNSUPPORTED,
-               "P2P BN allreduce: too many channels or members");
+    DC_REQUIRE(b.gsize <= kMaxBnGroup, DC_ERR_UNSUPPORTED, "P2P BN allreduce: too many members");
     launch_k(bn_allreduce_p2p_kernel, dim3(1), dim3(256), 0, st, 1, "bn p2p", b);
 }
 
 }  // namespace dc
-

@@ -81,30 +81,30 @@ void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Spatial BN statistics allreduce over NVLink (one kernel, one block): every
-// group member stores its 2*cpad fp64 sums into slot [parity][its rank] of
-// every member's mailbox (peer memory mapped through CUDA IPC), raises its
-// flag to the epoch, waits for all members' flags, and sums the slots in rank
-// order (deterministic, identical on every member). The epoch lives on the
-// device (read at start, published at the end) so the kernel can be replayed
-// from a CUDA graph. Mailbox data alternates parity per epoch: a member can
-// be at most one epoch ahead of any other (it needs everyone's flag to finish).
+// member of the plan's BN group stores its 2*cpad fp64 sums into slot
+// [parity][its index] of every member's mailbox (peer memory mapped through
+// CUDA IPC, or plain pointers in a loopback group), raises its flag to the
+// epoch, waits for all members' flags, and sums the slots in member order
+// (deterministic, identical on every member). The epoch lives on the device
+// (read at start, published at the end) so the kernel can be replayed from a
+// CUDA graph. The mailbox belongs to ONE plan, whose members all take part in
+// every epoch, so a member is at most one epoch ahead of any other (it needs
+// everyone's flag to finish) and two alternating parities suffice.
 // ---------------------------------------------------------------------------
 constexpr int kMaxBnGroup = 8;
-constexpr int kBnMaxDoubles = 2 * 2048;  // per slot: sums then sums of squares, cpad <= 2048
 
 struct BnP2P {
-    double *peer_box[kMaxBnGroup];    // member k's mailbox base (mapped)
-    uint32_t *peer_flags[kMaxBnGroup];  // member k's flag array base (mapped)
-    const double *my_box;             // my mailbox base
-    const uint32_t *my_flags;         // my flag array base
-    int ranks[kMaxBnGroup];           // global rank of member k (slot / flag index)
-    int gsize, my_rank, world;
-    uint32_t *epoch;                  // device epoch counter (this communicator)
-    const double *local;              // my 2 * cpad sums
+    double *peer_box[kMaxBnGroup];      // member k's mailbox data (mapped)
+    uint32_t *peer_flags[kMaxBnGroup];  // member k's flag array (mapped)
+    const double *my_box;               // my mailbox data
+    const uint32_t *my_flags;           // my flag array (flag k: member k's epoch)
+    int gsize, my_idx;                  // members, my index in the group
+    uint32_t *epoch;                    // device epoch counter (this plan)
+    const double *local;                // my 2 * cpad sums
     int cpad, c;
     double count;
-    double *sums;                     // out: global sums [2 * cpad]
-    double *mean, *var;               // out: first c channels
+    double *sums;                       // out: global sums [2 * cpad]
+    double *mean, *var;                 // out: first c channels
 };
 void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st);
 

@@ -17,6 +17,23 @@ namespace dc {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Acquire-poll a (possibly peer-mapped) flag until (int)(*p - target) >= 0,
+// at system scope. A peer that has not arrived after kSpinTimeoutNs is a
+// protocol error (a rank skipped a collective call), not a reason to hang the
+// GPU: the kernel traps, the launch fails and the next CUDA call reports it.
+constexpr unsigned long long kSpinTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ void spin_until_geq(const uint32_t *p, uint32_t target) {
+    unsigned long long t0, t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+        if ((int)(v - target) >= 0) return;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > kSpinTimeoutNs) __trap();
+    }
+}
+
 inline bool pdl_enabled() {
     static const bool on = std::getenv("DC_NO_PDL") == nullptr;
     return on;

@@ -15,7 +15,8 @@
 // dy (without halo) is streamed once per block. A CTA keeps
 // the accumulators of all its M tiles in TMEM across its split-K range;
 // partial sums go to a workspace reduced in a fixed order
-// (splitk_reduce_kernel) -> deterministic.
+// (splitk_reduce_kernel) -> deterministic (the default; DC_DW_ATOMIC lets small
+// dW splits add with fp32 reductions instead).
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
@@ -246,7 +247,7 @@ __global__ void __launch_bounds__(192, 1)
         const int eq = warp & 3;
         const int m = eq * 32 + lane;
         float *wsb = p.ws + (long long)split * p.ws_split;
-        const long long fstride = (long long)p.T * p.cp;
+        const long long fstride = (long long)p.T * p.C;  // dW holds the C logical channels
         for (int i = 0; i < G; ++i) {
             const Atom a0 = atom_of(p, mt0 + i, 0, cg_lo);
             int ai = m / p.cgw;
@@ -256,8 +257,8 @@ __global__ void __launch_bounds__(192, 1)
             }
             const Atom at = atom_of(p, mt0 + i, ai, cg_lo);
             const int c = at.cg * p.cgw + (m % p.cgw);
-            const bool valid = at.tap >= 0 && c < p.cp;
-            float *wrow = wsb + (long long)(valid ? at.tap : 0) * p.cp + c;
+            const bool valid = at.tap >= 0 && c < p.C;
+            float *wrow = wsb + (long long)(valid ? at.tap : 0) * p.C + c;
             const uint32_t t_lane = tmem + i * p.bn_cols + ((uint32_t)(eq * 32) << 16);
             for (int c16 = 0; c16 < p.bn / 16; ++c16) {
                 uint32_t v[16];

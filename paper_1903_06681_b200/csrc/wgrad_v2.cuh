@@ -19,10 +19,10 @@ struct WgradV2Params {
     int n_mtiles, G;               // M = 128 tiles (atoms stacked), M tiles per CTA
     int tiles_h, tiles_w, nblocks; // 8 x bw output-pixel blocks per sample, total
     int splits;
-    float *ws;                     // [splits][F][T][cp] fp32 (or dW itself when atomic_out)
+    float *ws;                     // [splits][F][T][C] fp32 (or dW itself: one split / atomic_out)
     int atomic_out;                // splits add their partials into a zeroed dW (RED.ADD.F32)
-    long long ws_split;
-    int F, Fp, cp;
+    long long ws_split;            // elements per split (a multiple of 4)
+    int F, Fp, cp, C;              // filters, padded filters, padded / logical input channels
     long long pixels_hint;         // host: output pixels of this launch (N tile width choice)
 };
 

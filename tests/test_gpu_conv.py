@@ -43,7 +43,7 @@ def make_inputs(N, C, H, W, F, K, S, P):
 def run_layer(dc, shape, decomp=(1, 1, 1), rank=0, x=None, w=None, dy=None, virtual=True, ks_world=0):
     """Forward, backward-data and backward-filter of one rank's shard
     (halo rows filled by the test from the global tensor: no exchange).
-    ks_world: dc_plan_set_splitk_world (0: the plan's grid size)."""
+    ks_world: dc_plan_set_splitk_world (0: the library's fixed basis)."""
     N, C, H, W, F, K, S, P = shape
     plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, decomp, rank)
     try:
@@ -58,7 +58,7 @@ def run_layer(dc, shape, decomp=(1, 1, 1), rank=0, x=None, w=None, dy=None, virt
         dyb = fill_buffer(dy, dyd)
         dx = empty_dense(dxd)
         dc.dc_conv_bwd_data(plan, dyb, wb, dx, 0)
-        dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+        dw = torch.full((F, K, K, C), float("nan"), dtype=torch.float32, device="cuda")
         dc.dc_conv_bwd_filter(plan, xb, dyb, dw, 0)
         torch.cuda.synchronize()
         return dict(y=y, dx=dx, dw=dw, xd=xd, yd=yd, dxd=dxd, dyd=dyd)
@@ -117,10 +117,10 @@ GRIDS = [(1, 2, 1), (1, 1, 2), (1, 2, 2), (2, 2, 1), (1, 3, 1), (1, 4, 2)]
 @pytest.mark.parametrize("grid", GRIDS)
 def test_partition_bitwise(dc, shape, grid):
     """Every rank's owned y and dx from its own margined shard is bitwise equal
-    to the unpartitioned result of the same kernel configuration (north_star:
-    the 1-GPU plan set to the partition's split-K basis,
-    dc_plan_set_splitk_world(P)); that 1-GPU result matches the oracle; the
-    sum of the per-rank dW partials equals the 1-GPU dW within the fp32 bar."""
+    to the unpartitioned 1-GPU result with the DEFAULT settings of both plans
+    (north_star; the split-K basis is fixed); that 1-GPU result
+    matches the oracle; the sum of the per-rank dW partials equals the 1-GPU
+    dW within the fp32 bar."""
     N, C, H, W, F, K, S, P = shape
     try:
         dc.dc_plan_destroy(dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, grid, 0))
@@ -128,7 +128,7 @@ def test_partition_bitwise(dc, shape, grid):
         pytest.skip("grid invalid for this shape")
     x, w, dy = make_inputs(*shape)
     nranks = grid[0] * grid[1] * grid[2]
-    full = run_layer(dc, shape, x=x, w=w, dy=dy, ks_world=nranks)
+    full = run_layer(dc, shape, x=x, w=w, dy=dy)
     y_ref = oracle.conv_fwd(x, w, S, P)
     assert rel_l2(owned_nchw(full["y"], full["yd"]), y_ref) <= TOL_L2_DERIVED
     Y = full["y"].float().cpu()
@@ -193,7 +193,7 @@ def test_fused_bn_stats(dc, shape):
         dc.dc_conv_fwd(plan, xb, wb, y1, dc.DC_BN_STATS)
         mean = torch.zeros(F, dtype=torch.float64, device="cuda")
         var = torch.zeros(F, dtype=torch.float64, device="cuda")
-        dc.dc_bn_spatial_stats(plan, y1, mean, var, local_only=True)
+        dc.dc_bn_spatial_stats(plan, y1, mean, var, dc.DC_BN_LOCAL | dc.DC_BN_FROM_FWD)
         torch.cuda.synchronize()
         assert torch.equal(y0, y1), "DC_BN_STATS changed y"
         # (layers that cannot fuse fall back to bn_sums_kernel: depth 7 covers both)
@@ -207,10 +207,10 @@ def test_fused_bn_stats(dc, shape):
 
 
 @pytest.mark.parametrize("shape", [SHAPES[2], SHAPES[9], SHAPES[15]])
-def test_wgrad_deterministic_flag(dc, shape):
-    """DC_DETERMINISTIC: the split-K partials of dW are summed in a fixed order,
-    so two runs agree bit for bit; the default (fp32 atomics into dW) agrees
-    with it within the fp32 bar."""
+def test_wgrad_deterministic_default(dc, shape):
+    """dW is deterministic by default (split-K partials summed in a fixed
+    order): two default runs agree bit for bit; DC_DW_ATOMIC (fp32 atomics
+    into dW) agrees with it within the fp32 bar."""
     N, C, H, W, F, K, S, P = shape
     x, w, dy = make_inputs(*shape)
     plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, (1, 1, 1), 0)
@@ -218,14 +218,15 @@ def test_wgrad_deterministic_flag(dc, shape):
         xd, dyd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_DY)
         xb, dyb = fill_buffer(x, xd), fill_buffer(dy, dyd)
         outs = []
-        for flags in (dc.DC_DETERMINISTIC, dc.DC_DETERMINISTIC, 0):
-            dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+        for flags in (0, 0, dc.DC_DW_ATOMIC):
+            dw = torch.full((F, K, K, C), float("nan"), dtype=torch.float32, device="cuda")
             dc.dc_conv_bwd_filter(plan, xb, dyb, dw, flags)
             outs.append(dw)
         torch.cuda.synchronize()
-        assert torch.equal(outs[0], outs[1]), "DC_DETERMINISTIC dW differs between runs"
+        assert torch.equal(outs[0], outs[1]), "default dW differs between runs"
         assert rel_max(dw_to_fckk(outs[2], C), dw_to_fckk(outs[0], C)) <= TOL_DW
         dw_ref = oracle.conv_bwd_filter(x, dy, K, S, P)
+        assert rel_max(dw_to_fckk(outs[0], C), dw_ref) <= TOL_DW
         assert rel_max(dw_to_fckk(outs[2], C), dw_ref) <= TOL_DW
     finally:
         dc.dc_plan_destroy(plan)

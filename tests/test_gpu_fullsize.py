@@ -109,11 +109,11 @@ def test_full_size_sampled_parity(dc, layer):
         wb = torch.tensor(wnp, dtype=torch.bfloat16, device="cuda").contiguous()
         y, dx = empty_dense(yd), empty_dense(dxd)
         assert y.shape[:3] == (N, Ho, Wo) and dx.shape[:3] == (N, H, W)
-        dw = torch.full((F, K, K, xd["c_pad"]), float("nan"), dtype=torch.float32, device="cuda")
+        dw = torch.full((F, K, K, C), float("nan"), dtype=torch.float32, device="cuda")
         mean = torch.zeros(F, dtype=torch.float64, device="cuda")
         var = torch.zeros(F, dtype=torch.float64, device="cuda")
         dc.dc_conv_fwd(plan, xb, wb, y, dc.DC_BN_STATS)
-        dc.dc_bn_spatial_stats(plan, y, mean, var, local_only=True)
+        dc.dc_bn_spatial_stats(plan, y, mean, var, dc.DC_BN_LOCAL | dc.DC_BN_FROM_FWD)
         dc.dc_conv_bwd_data(plan, dyb, wb, dx, 0)
         dc.dc_conv_bwd_filter(plan, xb, dyb, dw, 0)
         torch.cuda.synchronize()

@@ -55,13 +55,12 @@ def _worker(rank, world, port, errq, env=None):
             x, w, dy = datagen.gen_x(N, C, H, W), datagen.gen_w(F, C, K), datagen.gen_dy(N, F, Ho, Wo)
             # 1-GPU reference of the same kernels on this device
             ref = dc.dc_plan_create(N, C, H, W, F, K, S, P, (1, 1, 1), dc.DC_BF16, None)
-            dc.dc_plan_set_splitk_world(ref, world)  # same summation order as the partition
             rx, ry = dc.dc_plan_query(ref, dc.DC_X), dc.dc_plan_query(ref, dc.DC_Y)
             rdy, rdx = dc.dc_plan_query(ref, dc.DC_DY), dc.dc_plan_query(ref, dc.DC_DX)
             wb = weights_gpu(w, rx["c_pad"])
             Y = torch.empty((ry["n"], ry["h"], ry["w"], ry["c_pad"]), dtype=torch.bfloat16, device="cuda")
             DX = torch.empty((rdx["n"], rdx["h"], rdx["w"], rdx["c_pad"]), dtype=torch.bfloat16, device="cuda")
-            DW = torch.empty((F, K, K, rx["c_pad"]), dtype=torch.float32, device="cuda")
+            DW = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
             xr, dyr = fill_buffer(x, rx), fill_buffer(dy, rdy)
             dc.dc_conv_fwd(ref, xr, wb, Y, 0)
             dc.dc_conv_bwd_data(ref, dyr, wb, DX, 0)
@@ -98,7 +97,7 @@ def _worker(rank, world, port, errq, env=None):
             # (3) backward with dy exchange || wgrad, allreduce || dgrad
             dyb.copy_(fill_owned_only(dy, dyd))
             dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
-            dw = torch.empty((F, K, K, xd["c_pad"]), dtype=torch.float32, device="cuda")
+            dw = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
             torch.cuda.synchronize()
             dist.barrier()
             dc.dc_conv_bwd(plan, xb.data_ptr(), dyb.data_ptr(), wb, dx, dw, dc.DC_DEFAULT_FLAGS)
@@ -129,7 +128,7 @@ def _worker(rank, world, port, errq, env=None):
             dist.barrier()
             dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y3, dc.DC_EXCHANGE | dc.DC_BN_STATS)
             m3, v3 = torch.zeros_like(mean), torch.zeros_like(var)
-            dc.dc_bn_spatial_stats(plan, y3, m3, v3, False)
+            dc.dc_bn_spatial_stats(plan, y3, m3, v3, dc.DC_BN_FROM_FWD)
             torch.cuda.synchronize()
             assert torch.equal(y3, ys), f"{tag}: y (fused BN) not bitwise equal to 1-GPU"
             # fused path: <= 2 x 16 in-register fp32 adds + depth-5 warp tree, DESIGN.md §7

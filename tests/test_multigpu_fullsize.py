@@ -89,13 +89,13 @@ def _worker(rank, world, port, errq):
             wb = torch.tensor(wnp, dtype=torch.bfloat16, device="cuda").contiguous()
             y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
             dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
-            dw = torch.empty((F, K, K, xd["c_pad"]), dtype=torch.float32, device="cuda")
+            dw = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
             mean = torch.zeros(F, dtype=torch.float64, device="cuda")
             var = torch.zeros(F, dtype=torch.float64, device="cuda")
             torch.cuda.synchronize()
             dist.barrier()
             dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y, dc.DC_EXCHANGE | dc.DC_BN_STATS)
-            dc.dc_bn_spatial_stats(plan, y, mean, var, False)
+            dc.dc_bn_spatial_stats(plan, y, mean, var, dc.DC_BN_FROM_FWD)
             dc.dc_conv_bwd(plan, xb.data_ptr(), dyb.data_ptr(), wb, dx, dw, dc.DC_DEFAULT_FLAGS)
             torch.cuda.synchronize()
 

@@ -292,6 +292,65 @@ def test_perfmodel_closed_forms():
     assert g["H"] * g["W"] * g["C"] * g["word_bytes"] / 2 ** 20 == g["mib"]
 
 
+def test_perfmodel_halo_branches_pinned():
+    """halo_terms' east/west, north/south and corner branches against the
+    hand-priced SPEC.md:370 / PAPER.md:193-194 messages (golden values)."""
+    g = GOLD["perfmodel_halo_ew_conv1"]
+    a = (g["N"], g["C"], g["H_l"], g["W_l"], g["O"])
+    kw = dict(alpha=g["alpha"], beta=g["beta"], word_bytes=g["word_bytes"])
+    ew = pm.halo_terms(*a, h_split=False, w_split=True, **kw)
+    ns = pm.halo_terms(*a, h_split=True, w_split=False, **kw)
+    both = pm.halo_terms(*a, h_split=True, w_split=True, **kw)
+    assert abs(ew - g["seconds_ew_only"]) < 1e-15
+    assert abs(ns - g["seconds_ns_only"]) < 1e-15
+    assert abs(both - g["seconds_both"]) < 1e-15
+    assert abs((both - ew - ns) - g["seconds_corners"]) < 1e-15
+    # the strided extra latency lands on the 2 e/w and 4 corner messages only
+    aw = 3e-6
+    assert abs(pm.halo_terms(*a, True, True, alpha_w=aw, **kw) - (g["seconds_both"] + 6 * aw)) < 1e-15
+    assert abs(pm.halo_terms(*a, True, False, alpha_w=aw, **kw) - g["seconds_ns_only"]) < 1e-15
+
+
+def test_perfmodel_allreduce_ring_pinned():
+    """AR picks the ring at n = 1e7, p = 64 with the hand value."""
+    g = GOLD["perfmodel_ar_ring"]
+    t = pm.ar(g["p"], g["n"], g["alpha"], g["beta"], g["word_bytes"])
+    assert abs(t - g["seconds"]) < 1e-12
+    assert abs(t - g["seconds_ring"]) < 1e-12 and t < g["seconds_rd"]
+    # p = 2: recursive doubling (alpha + n beta') beats the ring (2 alpha + n beta') -- SPEC.md:360
+    assert abs(pm.ar(2, 1e6, 1e-6, 1e-9, 4) - (1e-6 + 4e-3)) < 1e-15
+
+
+def test_perfmodel_layer_cost_pinned():
+    """layer_cost's FP/BP composition against hand-priced values: P = 1 ->
+    C + Cx + Cw; pure sample parallelism -> no halo, plus BPa
+    (SPEC.md:368), with and without the R16 overlap; a 2-way H split adds
+    2 SR(O N_l C W_l) to FP and the F-channel dy halo to BP (R13)."""
+    g = GOLD["perfmodel_layer_cost"]
+    cost = lambda op, *a: g["costs"][op]
+    L, al, be = g["layer"], g["alpha"], g["beta"]
+    for ov in (True, False):
+        assert abs(pm.layer_cost(L, (1, 1, 1), cost, al, be, overlap=ov)["total"] - g["p1_total"]) < 1e-15
+    s = pm.layer_cost(L, (4, 1, 1), cost, al, be, overlap=False)
+    assert s["halo_x"] == 0.0 and s["halo_dy"] == 0.0
+    assert abs(s["bpa"] - g["sample4_bpa"]) < 1e-15
+    assert abs(s["total"] - g["sample4_total_plain"]) < 1e-15
+    assert abs(pm.layer_cost(L, (4, 1, 1), cost, al, be, overlap=True)["total"] - g["sample4_total_overlap"]) < 1e-15
+    sp = pm.layer_cost(L, (1, 2, 1), cost, al, be, overlap=False)
+    assert abs(sp["halo_x"] - g["spatial2_halo_x"]) < 1e-15
+    assert abs(sp["halo_dy"] - g["spatial2_halo_x"]) < 1e-15
+    assert abs(sp["bpa"] - g["spatial2_bpa"]) < 1e-15
+    assert abs(sp["total"] - g["spatial2_total_plain"]) < 1e-15
+    # a 2-way W split of the square layer prices the same message through the
+    # east/west branch, O N_l C H_l with H_l = 256 (W_l = 128 would differ)
+    sw = pm.layer_cost(L, (1, 1, 2), cost, al, be, overlap=False)
+    assert abs(sw["halo_x"] - g["spatial2_halo_x"]) < 1e-15
+    assert abs(sw["total"] - g["spatial2_total_plain"]) < 1e-15
+    # without the allreduce the plain total drops exactly BPa
+    nar = pm.layer_cost(L, (1, 2, 1), cost, al, be, overlap=False, include_allreduce=False)
+    assert abs(sp["total"] - nar["total"] - g["spatial2_bpa"]) < 1e-15
+
+
 def _flops_cost(op, n, c, h, w, f, K=3):
     return 2.0 * n * c * h * w * f * K * K / 1e15
 

@@ -66,7 +66,7 @@ def main():
                 x, dy = buf(q[dc.DC_X]), buf(q[dc.DC_DY])
                 y, dx = buf(q[dc.DC_Y]), buf(q[dc.DC_DX])
                 w = ((torch.rand(F, K, K, xd["c_pad"], device="cuda") - 0.5) * 0.1).to(torch.bfloat16)
-                dw = torch.empty(F, K, K, xd["c_pad"], device="cuda")
+                dw = torch.empty(F, K, K, C, device="cuda")
                 ops = {"fp": lambda: dc.dc_conv_fwd(plan, x, w, y, 0),
                        "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0),
                        "bpw": lambda: dc.dc_conv_bwd_filter(plan, x, dy, dw, 0)}

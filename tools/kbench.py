@@ -39,14 +39,14 @@ def main():
     y, dx = torch.empty_like(buf(q[dc.DC_Y])), torch.empty_like(buf(q[dc.DC_DX]))
     w = torch.randn(F, K, K, q[dc.DC_X]["c_pad"], device="cuda").to(torch.bfloat16) * 0.05
     w[..., C:] = 0
-    dw = torch.empty(F, K, K, q[dc.DC_X]["c_pad"], device="cuda")
+    dw = torch.empty(F, K, K, C, device="cuda")
     Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
     flops = 2.0 * N * F * C * K * K * Ho * Wo
     fwd_flags = dc.DC_BN_STATS if a.bn_fused else 0
     ops = {"fwd": lambda: dc.dc_conv_fwd(plan, x, w, y, fwd_flags),
            "bpw": lambda: dc.dc_conv_bwd_filter(plan, x, dy, dw, 0),
            "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0),
-           "bn": lambda: dc.dc_bn_spatial_stats(plan, y, mean, var, 1, 0)}
+           "bn": lambda: dc.dc_bn_spatial_stats(plan, y, mean, var, dc.DC_BN_LOCAL | (dc.DC_BN_FROM_FWD if a.bn_fused else 0), 0)}
     mean = torch.empty(F, dtype=torch.float64, device="cuda")
     var = torch.empty(F, dtype=torch.float64, device="cuda")
     for name in a.ops.split(","):

@@ -45,7 +45,7 @@ def main():
     w[..., C:] = 0
     y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
     dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
-    dw = torch.empty(F, K, K, xd["c_pad"], device="cuda")
+    dw = torch.empty(F, K, K, C, device="cuda")
     st = torch.cuda.current_stream()
     X, DY = xb.data_ptr(), dyb.data_ptr()
     ops = {
