@@ -49,6 +49,29 @@ def mesh_stack(size: int = 2048, n: int = 1, blocks: int = 6, per_block: int = 5
     return layers
 
 
+def resnet50_convs(n: int = 64, size: int = 224):
+    """The 53 convolutions of ResNet-50 with Caffe's
+    stride placement (stride 2 in branch2a 1x1 and branch1, reading R21):
+    conv1 7x7/2, then 3/4/6/3 bottleneck blocks (1x1, 3x3, 1x1; projection
+    branch1 in the first block of each stage). The conv-stack proxy of
+    BASELINE.json configs[2] (pooling, BN apply, ReLU, residual adds and the FC
+    layer are not convolutions: NEXT-1)."""
+    layers = [("conv1", n, 3, size, size, 64, 7, 2, 3)]
+    h, c = size // 4, 64  # after conv1 (/2) and the 3x3/2 max-pool (/2)
+    for stage, (blocks, mid, out) in enumerate([(3, 64, 256), (4, 128, 512), (6, 256, 1024), (3, 512, 2048)], 2):
+        for b in range(blocks):
+            tag = f"res{stage}{chr(ord('a') + b)}"
+            s = 2 if (b == 0 and stage > 2) else 1
+            if b == 0:
+                layers.append((f"{tag}_branch1", n, c, h, h, out, 1, s, 0))
+            layers.append((f"{tag}_branch2a", n, c, h, h, mid, 1, s, 0))
+            h2 = (h - 1) // s + 1
+            layers.append((f"{tag}_branch2b", n, mid, h2, h2, mid, 3, 1, 1))
+            layers.append((f"{tag}_branch2c", n, mid, h2, h2, out, 1, 1, 0))
+            h, c = h2, out
+    return layers
+
+
 WORKLOADS = {
     # BASELINE.json configs[3]: 2K mesh-tangling CNN conv stack, N = 1-8, pure
     # spatial strong scaling. Default: N = 8 (a global mini-batch fixed as the
@@ -56,6 +79,8 @@ WORKLOADS = {
     "mesh2k_n8": mesh_stack(2048, 8),
     "mesh2k": mesh_stack(2048, 1),
     "mesh1k": mesh_stack(1024, 1, per_block=3),
+    # BASELINE.json configs[2]: the 53 ResNet-50 convolutions at N = 64, 224^2
+    "resnet50_n64": resnet50_convs(64),
     # BASELINE.json configs[1]: ResNet-50 conv layers at N=32, 224x224
     "resnet_layers": [("conv1", 32, 3, 224, 224, 64, 7, 2, 3),
                       ("res2a_branch2b", 32, 64, 56, 56, 64, 3, 1, 1),
@@ -76,12 +101,13 @@ def layer_flops(l) -> float:
     return 2.0 * N * F * C * K * K * Ho * Wo
 
 
-def layer_bytes(l, op: str) -> float:
-    """Minimum HBM bytes of one conv op (bf16 in/out once)."""
+def layer_bytes(l, op: str, e: int = 2) -> float:
+    """Minimum HBM bytes of one conv op (activations and weights in/out once,
+    e bytes per element: 2 bf16, 4 fp32; dW fp32)."""
     _, N, C, H, W, F, K, S, P = l
     Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
-    act = 2.0 * (N * H * W * C + N * Ho * Wo * F)
-    return act + (4.0 if op == "bpw" else 2.0) * F * C * K * K
+    act = float(e) * (N * H * W * C + N * Ho * Wo * F)
+    return act + (4.0 if op == "bpw" else float(e)) * F * C * K * K
 
 
 def load_peaks():
@@ -237,6 +263,11 @@ def main():
                     help="spatial (model picks pH x pW, pN = 1: BASELINE configs[3]) | auto (model, all grids) | "
                          "pn,ph,pw (0 entries: model's choice)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"],
+                    help="bf16: bf16 x bf16 -> fp32 (DC_BF16); fp32: the paper's single precision via 3xTF32 "
+                         "(DC_FP32_3XTF32)")
+    ap.add_argument("--splitk-basis", type=int, default=0,
+                    help="dc_plan_set_splitk_world on every plan (0: the library's fixed basis; A/B only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-budget", type=float, default=8.0)
     ap.add_argument("--no-fused-bn", action="store_true", help="BN statistics by a separate pass over y")
@@ -260,6 +291,12 @@ def main():
     build.build()
     import paper_1903_06681_b200 as dc
     import datagen
+
+    fp32 = args.dtype == "fp32"
+    DTYPE = dc.DC_FP32_3XTF32 if fp32 else dc.DC_BF16
+    TDT = torch.float32 if fp32 else torch.bfloat16
+    KIND = "act24" if fp32 else "act"          # fp32-exact 24-bit grid / bf16-exact grid
+    IMPORT_SRC = 0 if fp32 else dc.DC_SRC_BF16  # the source's element type
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -307,35 +344,42 @@ def main():
         name, N, C, H, W, F, K, S, P = l
         decomp = {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
             int(v) for v in args.decomp.split(","))
-        plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, dc.DC_BF16, comm)
+        plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, DTYPE, comm)
+        if args.splitk_basis:
+            dc.dc_plan_set_splitk_world(plan, args.splitk_basis)
         chosen, pred = dc.dc_plan_decomp(plan)
         xd, yd = dc.dc_plan_query(plan, dc.DC_X), dc.dc_plan_query(plan, dc.DC_Y)
         dyd, dxd = dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(plan, dc.DC_DX)
-        xb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_X), (xd["n"], xd["hb"], xd["wb"], xd["c_pad"]))
-        dyb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_DY), (dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]))
+        wd = dc.dc_plan_query(plan, dc.DC_W)
+        xb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_X), (xd["n"], xd["hb"], xd["wb"], xd["c_pad"]),
+                                   TDT)
+        dyb = dc.wrap_device_buffer(dc.dc_buffer_alloc(plan, dc.DC_DY),
+                                    (dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]), TDT)
 
-        def owned(desc, tid, shape):
+        def owned(desc, tid, shape, ch):
             # the counter-based generator run on the GPU (bitwise equal to the
-            # numpy one, tests/test_datagen.py): no host hashing of gigabytes
+            # numpy one, tests/test_datagen.py): no host hashing of gigabytes;
+            # the owned block, dense, logical channels (dc_tensor_import's source)
             return datagen.gen_block_nhwc_torch(
-                shape, datagen.SEED, tid, n=(desc["n0"], desc["n0"] + desc["n"]),
+                shape, datagen.SEED, tid, kind=KIND, n=(desc["n0"], desc["n0"] + desc["n"]),
                 h=(desc["h0"], desc["h0"] + desc["h"]), w=(desc["w0"], desc["w0"] + desc["w"]),
-                c_pad=desc["c_pad"], dtype=torch.bfloat16, device="cuda")
+                c_pad=ch, dtype=TDT, device="cuda")
 
         Ho, Wo = (H + 2 * P - K) // S + 1, (W + 2 * P - K) // S + 1
-        x_own = owned(xd, datagen.TID_X, (N, C, H, W))
-        dy_own = owned(dyd, datagen.TID_DY, (N, F, Ho, Wo))
-        xb[:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]] = x_own
-        dyb[:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]] = dy_own
-        wnp = np.zeros((F, K, K, xd["c_pad"]), dtype=np.float32)
-        wnp[..., :C] = datagen.gen_w(F, C, K).transpose(0, 2, 3, 1)
-        wt = torch.tensor(wnp, dtype=torch.bfloat16).cuda()
-        y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
-        dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
+        x_own = owned(xd, datagen.TID_X, (N, C, H, W), C)
+        dy_own = owned(dyd, datagen.TID_DY, (N, F, Ho, Wo), F)
+        # into the margined buffers through the C ABI (fp32 plans: the 3xTF32 split)
+        dc.dc_tensor_import(plan, dc.DC_X, x_own, xb, IMPORT_SRC)
+        dc.dc_tensor_import(plan, dc.DC_DY, dy_own, dyb, IMPORT_SRC)
+        wnp = np.zeros((F, K, K, wd["c_pad"]), dtype=np.float32)
+        wnp[..., :C] = datagen.gen_w(F, C, K, kind=KIND).transpose(0, 2, 3, 1)
+        wt = torch.tensor(wnp, dtype=TDT).cuda()
+        y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=TDT, device="cuda")
+        dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=TDT, device="cuda")
         dw = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
         bn_mean = torch.empty(F, dtype=torch.float64, device="cuda")
         bn_var = torch.empty(F, dtype=torch.float64, device="cuda")
-        # pinned host copies for the end-to-end leg
+        # pinned host copies for the end-to-end leg (dense, logical channels)
         host = {"x": x_own.cpu().pin_memory(), "dy": dy_own.cpu().pin_memory(), "w": wt.cpu().pin_memory(),
                 "dw": torch.empty(dw.shape, dtype=torch.float32).pin_memory()}
         L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
@@ -367,14 +411,17 @@ def main():
         return ops
 
     def step(e2e=False):
-        for d in L:
-            xd, dyd = d["xd"], d["dyd"]
-            if e2e:  # inputs arrive from pinned host memory every step
-                xs = d["xb"][:, xd["halo_n"]:xd["halo_n"] + xd["h"], xd["halo_w"]:xd["halo_w"] + xd["w"]]
-                xs.copy_(d["host"]["x"], non_blocking=True)
-                d["dyb"][:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]].copy_(
-                    d["host"]["dy"], non_blocking=True)
+        if e2e:
+            # inputs arrive from pinned HOST memory every step through the C ABI
+            # (dc_tensor_import with host pointers): every layer's copies are
+            # queued up front on the plans' copy streams, so they overlap the
+            # compute of the earlier layers; each layer's first call joins them
+            for d in L:
+                dc.dc_tensor_import(d["plan"], dc.DC_X, d["host"]["x"], d["xb"], IMPORT_SRC | dc.DC_IMPORT_ASYNC, sp)
+                dc.dc_tensor_import(d["plan"], dc.DC_DY, d["host"]["dy"], d["dyb"], IMPORT_SRC | dc.DC_IMPORT_ASYNC,
+                                    sp)
                 d["w"].copy_(d["host"]["w"], non_blocking=True)
+        for d in L:
             for _, f in op_calls(d):
                 f()
         dc.dc_comm_sync(comm, sp)
@@ -491,10 +538,20 @@ def main():
     loc = d["l"]
     # algorithmic work of THIS rank's shard (blocked split: global / world)
     fl = layer_flops(loc) / world
-    by = layer_bytes(loc, op) / world
-    ridge = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    by = layer_bytes(loc, op, 4 if fp32 else 2) / world
+    tensor_peak, tensor_src = peaks["bf16_tflops"], "bf16 dense, measured burst (MEASURED_PEAKS.json)"
+    if fp32:
+        # 3xTF32: three tf32 tensor-core products per algorithmic multiply-add,
+        # so the peak for algorithmic FLOPs is the measured dense tf32 rate / 3
+        try:
+            tf = json.load(open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")))["tf32_tflops"]
+            tsrc = "measured burst, cuBLAS tf32 8192^3 (profiles/r2_tf32_peak.json)"
+        except (OSError, ValueError, KeyError):
+            tf, tsrc = peaks["bf16_tflops"] * 0.5, "bf16 measured x 0.5 (nominal tf32/bf16 ratio)"
+        tensor_peak, tensor_src = tf / 3.0, f"tf32 dense {tf:.1f} TFLOP/s {tsrc}, / 3 products (3xTF32)"
+    ridge = tensor_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
     if fl / by >= ridge:
-        roof = {"bound": "tensor", "achieved": fl / (op_ms / 1e3) / 1e12, "peak": peaks["bf16_tflops"],
+        roof = {"bound": "tensor", "achieved": fl / (op_ms / 1e3) / 1e12, "peak": tensor_peak,
                 "unit": "TFLOP/s"}
     else:
         roof = {"bound": "hbm", "achieved": by / (op_ms / 1e3) / 1e9, "peak": peaks["hbm_gbs"], "unit": "GB/s"}
@@ -510,9 +567,10 @@ def main():
             roof["traffic_algorithmic"] = by
     except (OSError, ValueError, KeyError):
         pass
-    roof["kernel"] = f"conv_v2_kernel ({loc[0]} forward{'' if world == 1 else ' incl. halo exchange'})"
+    roof["kernel"] = (f"conv_v2_kernel{'<tf32>' if fp32 else ''} ({loc[0]} forward"
+                      f"{'' if world == 1 else ' incl. halo exchange'})")
     roof["avg_launch_ms"] = op_ms
-    roof["peak_source"] = peak_src + " burst (MEASURED_PEAKS.json)"
+    roof["peak_source"] = tensor_src if roof["bound"] == "tensor" else peak_src + " HBM copy (MEASURED_PEAKS.json)"
 
     out = None
     if rank == 0:
@@ -527,8 +585,10 @@ def main():
             **({"DIAGNOSTIC_ablated": sorted(ablate)} if ablate else {}),
             "metric": "conv fwd+bwd TFLOP/s", "value": value, "unit": "TFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-            "data": "synthetic (seeded counter-based generator, bf16-exact values)",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "fp32 (3xTF32: tf32 x3 products, fp32 accumulate)" if fp32 else "bf16",
+            "data": "synthetic (seeded counter-based generator, " + (
+                "fp32-exact 24-bit values)" if fp32 else "bf16-exact values)"),
             "config": {"workload": args.workload, "global_batch": layers[0][1],
                        "layers": [{"name": d["l"][0], "shape_NCHW_F_K_S_P": list(d["l"][1:]),
                                    "decomp": list(d["decomp"]), "model_pred_ms": d["pred"] * 1e3,

@@ -51,7 +51,17 @@ typedef enum {
     DC_ERR_OOM = 7
 } dc_status_t;
 
-typedef enum { DC_BF16 = 0, DC_FP32_3XTF32 = 1 /* reserved, not yet implemented */ } dc_dtype_t;
+/* Arithmetic of a plan (reading R18; "single-precision"):
+ *   DC_BF16        bf16 activations / weights, fp32 accumulation (kind::f16);
+ *   DC_FP32_3XTF32 fp32 activations / weights, computed as three tf32
+ *                  products per term (x_hi w_hi + x_hi w_lo + x_lo w_hi,
+ *                  kind::tf32, fp32 accumulation): ~2^-21 relative error per
+ *                  product. Layouts of an fp32 plan: channels padded to a
+ *                  multiple of 8; the margined x / dy buffers hold each pixel
+ *                  as [hi (c_pad/2) | lo (c_pad/2)] fp32 (fill them with
+ *                  dc_tensor_import); y / dx plain fp32 [n][h][w][c_pad];
+ *                  w fp32 [F][K][K][c_pad]; dw fp32 [F][K][K][C]. */
+typedef enum { DC_BF16 = 0, DC_FP32_3XTF32 = 1 } dc_dtype_t;
 
 typedef enum { DC_X = 0, DC_Y = 1, DC_DY = 2, DC_DX = 3, DC_W = 4, DC_DW = 5 } dc_tensor_t;
 
@@ -136,7 +146,7 @@ dc_status_t dc_comm_sync(dc_comm_t comm, void *stream);
  * Errors: DC_ERR_SHAPE (even K, P > K/2, extent < K without padding),
  * DC_ERR_PARTITION (p_N > N, a part with no output rows, a halo wider than the
  * adjacent rank's block -- PAPER.md:145's degenerate case -- or product !=
- * world), DC_ERR_UNSUPPORTED (stride > 2, dtype != DC_BF16). */
+ * world), DC_ERR_UNSUPPORTED (stride > 2), DC_ERR_ARG (unknown dtype). */
 dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
                            int stride, int pad, dc_decomp_t decomp, dc_dtype_t dtype,
                            dc_comm_t comm, dc_plan_t *out);
@@ -180,6 +190,25 @@ dc_status_t dc_plan_destroy(dc_plan_t plan);
  * P2P halo stores. Owned by the plan; freed by dc_plan_destroy. */
 dc_status_t dc_buffer_alloc(dc_plan_t plan, dc_tensor_t t, void **dev_ptr);
 
+/* Fill the OWNED block of a margined buffer (t in {DC_X, DC_DY}, dst from
+ * dc_buffer_alloc or any buffer of that layout) from `src`, a dense NHWC
+ * tensor of the owned block [n][h][w][C] (C = the tensor's logical channels,
+ * no padding) in fp32 -- or bf16 with DC_SRC_BF16 (bf16 plans only) -- in
+ * HOST memory (pinned or pageable: one H2D copy into plan-owned staging) or
+ * device memory. bf16 plans round fp32 to bf16; fp32 plans store the exact
+ * 3xTF32 split [hi | lo] (x_hi = x with its low 13 mantissa bits cleared,
+ * x_lo = x - x_hi); padded channels are written as zeros, the margins are
+ * left alone (dc_halo_exchange fills them). With DC_IMPORT_ASYNC the copy and
+ * the layout kernel run on the plan's copy stream after the work queued on
+ * `stream` so far, and the plan's next call that reads that buffer waits for
+ * them (so a step can issue every layer's input copy up front and overlap it
+ * with compute); otherwise stream-ordered on `stream`. A host src must stay
+ * valid until the copy ran. Errors: DC_ERR_ARG. */
+#define DC_IMPORT_ASYNC 0x1u
+#define DC_SRC_BF16     0x2u
+dc_status_t dc_tensor_import(dc_plan_t plan, dc_tensor_t t, const void *src, void *dst, unsigned flags,
+                             void *stream);
+
 /* COLLECTIVE. Halo exchange of buffer `buf` (t in {DC_X, DC_DY}): copies each
  * rank's boundary slabs (all local samples and channels) into the
  * neighbours' margins, the 8 neighbours of a 2D grid directly (PAPER.md:127,
@@ -221,7 +250,8 @@ dc_status_t dc_conv_bwd(dc_plan_t plan, const void *x_margined, void *dy_margine
 /* Spatially-aggregated batch-norm statistics (reading R11):
  * per channel, mean and biased variance of `t` over the local samples and
  * the whole spatial extent of the ranks that share this rank's samples
- * (equal i_N). t is a dense NHWC bf16 tensor of the DC_Y layout of this plan
+ * (equal i_N). t is a dense NHWC tensor (bf16, or fp32 for DC_FP32_3XTF32
+ * plans) of the DC_Y layout of this plan
  * (channels = F, padded); mean_dev/var_dev are device fp64 arrays of F
  * entries. COLLECTIVE over the spatial group (each group of <= 8 ranks uses
  * its own one-shot NVLink mailbox of this plan; NCCL beyond).

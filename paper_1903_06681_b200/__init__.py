@@ -24,12 +24,13 @@ DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DET
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 DC_BN_LOCAL, DC_BN_FROM_FWD = 0x1, 0x2
+DC_IMPORT_ASYNC, DC_SRC_BF16 = 0x1, 0x2
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "dc_comm_create", "dc_comm_create_local", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
-    "dc_plan_destroy", "dc_buffer_alloc", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
+    "dc_plan_destroy", "dc_buffer_alloc", "dc_tensor_import", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
     "dc_model_choose", "dc_model_choose_fixed",
@@ -93,6 +94,7 @@ def lib() -> ctypes.CDLL:
         "dc_plan_destroy": [vp],
         "dc_buffer_alloc": [vp, i32, P(vp)],
         "dc_halo_exchange": [vp, i32, vp, ctypes.c_uint, vp],
+        "dc_tensor_import": [vp, i32, vp, vp, ctypes.c_uint, vp],
         "dc_conv_fwd": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_conv_bwd_data": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_conv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
@@ -234,6 +236,13 @@ def wrap_device_buffer(ptr: int, shape, dtype=None):
     if dtype == torch.float32:
         return torch.as_tensor(_CudaArray(ptr, shape, "<f4"), device="cuda")
     raise ValueError("dtype must be bfloat16 or float32")
+
+
+def dc_tensor_import(plan: int, t: int, src, dst, flags: int = 0, stream=None):
+    """Owned block of the margined buffer dst from a dense NHWC tensor
+    [n][h][w][C] (fp32, or bf16 with DC_SRC_BF16), host or device memory
+    (bf16 plans round, fp32 plans store the 3xTF32 hi/lo split)."""
+    _check(lib().dc_tensor_import(plan, t, _ptr(src), _ptr(dst), flags, _stream(stream)))
 
 
 def dc_halo_exchange(plan: int, t: int, buf, flags: int = 0, stream=None):

@@ -28,15 +28,35 @@
 #include "conv_tc.cuh"
 #include "conv_v2.cuh"
 #include "halo.cuh"
+#include "launch.cuh"
 #include "wgrad_v2.cuh"
+#include "tf32.cuh"
 #include "plan.hpp"
 
 namespace dc {
 thread_local uint64_t g_launches = 0;
+thread_local bool g_no_pdl = false;
 static thread_local std::string g_err;
 void set_last_error(const std::string &m) { g_err = m; }
 
 double model_layer_cost(const ConvGeom &g, Grid d, bool include_allreduce);
+void preload_conv_tc();
+void preload_conv_v2();
+void preload_halo();
+void preload_tf32();
+void preload_wgrad_v2();
+// Every kernel of the library loaded into this context (see preload_*):
+// once, at communicator creation.
+void preload_kernels() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        preload_conv_tc();
+        preload_conv_v2();
+        preload_halo();
+        preload_tf32();
+        preload_wgrad_v2();
+    });
+}
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
 }  // namespace dc
 
@@ -121,7 +141,9 @@ struct dc_plan_s {
     uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
     std::map<int, uint32_t *> peer_flags;
     uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local)
-    __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases
+    float *wsplit = nullptr;         // 3xTF32 forward weights [F][T][hi | lo | hi]
+    size_t wsplit_bytes = 0;
+    __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases (fp32 plans: fp32 words)
     size_t wt_bytes = 0;
     float *ws = nullptr;             // split-K workspace (backward-filter)
     size_t ws2_bytes = 0;
@@ -144,9 +166,19 @@ struct dc_plan_s {
     std::vector<uint8_t *> bn_peer_mail;  // member k's mailbox (mine at my index)
     bool bn_p2p = false;
     int seq = -1;                    // creation index on the communicator (loopback registry key)
+    // dc_tensor_import staging: host -> device copies and the import kernel
+    // on an internal copy stream (DC_IMPORT_ASYNC), joined by the next call
+    // that reads the buffer
+    cudaStream_t s_copy = nullptr;
+    cudaEvent_t ev_copy_in[2] = {nullptr, nullptr}, ev_copy_out[2] = {nullptr, nullptr};
+    bool import_pending[2] = {false, false};
+    void *stage[2] = {nullptr, nullptr};
+    size_t stage_bytes[2] = {0, 0};
+    std::vector<void *> grave;       // outgrown workspaces (freed with the plan; see ensure_alloc)
     double predicted = 0.0;
 
     ~dc_plan_s() {
+        for (void *q : grave) cudaFree(q);
         for (auto &b : buf) {
             if (!(comm && comm->group))
                 for (auto &kv : b.peer) cudaIpcCloseMemHandle(kv.second);
@@ -165,9 +197,16 @@ struct dc_plan_s {
         }
         if (bn_mail) cudaFree(bn_mail);
         if (bn_epoch) cudaFree(bn_epoch);
+        for (int i = 0; i < 2; ++i) {
+            if (stage[i]) cudaFree(stage[i]);
+            if (ev_copy_in[i]) cudaEventDestroy(ev_copy_in[i]);
+            if (ev_copy_out[i]) cudaEventDestroy(ev_copy_out[i]);
+        }
+        if (s_copy) cudaStreamDestroy(s_copy);
         if (flags) cudaFree(flags);
         if (dev_epochs) cudaFree(dev_epochs);
         if (wt) cudaFree(wt);
+        if (wsplit) cudaFree(wsplit);
         if (ws) cudaFree(ws);
         if (ws2) cudaFree(ws2);
         if (bn_part) cudaFree(bn_part);
@@ -193,10 +232,15 @@ struct dc_plan_s {
 
 namespace {
 
+// Grow a plan workspace. The old block is NOT freed here: cudaFree waits for
+// the whole device, and a compute call may run while this rank's (or, in a
+// loopback group, another virtual rank's) halo / BN kernels spin on the device
+// for a peer -- it is kept until the plan is destroyed (workspaces only grow
+// to a layer's largest need, once).
 template <class T>
-void ensure_alloc(T *&p, size_t &have, size_t need) {
+void ensure_alloc(std::vector<void *> &grave, T *&p, size_t &have, size_t need) {
     if (need <= have) return;
-    if (p) CK(cudaFree(p));
+    if (p) grave.push_back(p);
     p = nullptr;
     CK(cudaMalloc(reinterpret_cast<void **>(&p), need));
     have = need;
@@ -220,11 +264,14 @@ dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
         d.stride_w = cp;
         d.stride_h = d.wb * cp;
         d.stride_n = d.hb * d.wb * cp;
-        d.bytes = (size_t)(d.n * d.stride_n) * 2;
+        d.bytes = (size_t)(d.n * d.stride_n) * g.esz();
     };
+    // fp32 (3xTF32) plans: the margined x / dy buffers hold each pixel as
+    // [hi (c_pad/2) | lo (c_pad/2)] fp32 (tf32.cuh), y / dx plain fp32
+    const int split = g.dt ? 2 : 1;
     switch (t) {
     case DC_X:
-        fill(rp.h.in.lo, rp.h.in.size(), rp.w.in.lo, rp.w.in.size(), g.C, g.Cp, rp.h.x_halo_lo(),
+        fill(rp.h.in.lo, rp.h.in.size(), rp.w.in.lo, rp.w.in.size(), g.C, split * g.Cp, rp.h.x_halo_lo(),
              rp.h.x_halo_hi(), rp.w.x_halo_lo(), rp.w.x_halo_hi());
         break;
     case DC_DX:
@@ -234,18 +281,18 @@ dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
         fill(rp.h.out.lo, rp.h.out.size(), rp.w.out.lo, rp.w.out.size(), g.F, g.Fp, 0, 0, 0, 0);
         break;
     case DC_DY:
-        fill(rp.h.out.lo, rp.h.out.size(), rp.w.out.lo, rp.w.out.size(), g.F, g.Fp,
+        fill(rp.h.out.lo, rp.h.out.size(), rp.w.out.lo, rp.w.out.size(), g.F, split * g.Fp,
              rp.h.d_halo_lo(), rp.h.d_halo_hi(), rp.w.d_halo_lo(), rp.w.d_halo_hi());
         break;
     case DC_W:
     case DC_DW: {
-        // w: bf16 [F][K][K][Cp] (TMA rows); dW: fp32 [F][K][K][C], no padding
-        // (what the allreduce sends: F C K^2 words)
+        // w: [F][K][K][Cp] bf16 (TMA rows) or fp32; dW: fp32 [F][K][K][C], no
+        // padding (what the allreduce sends: F C K^2 words)
         const int64_t cp = t == DC_W ? g.Cp : g.C;
         d.n0 = 0, d.n = g.F, d.h = g.K, d.w = g.K, d.c = g.C, d.c_pad = cp;
         d.hb = g.K, d.wb = g.K;
         d.stride_w = cp, d.stride_h = g.K * cp, d.stride_n = g.K * g.K * cp;
-        d.bytes = (size_t)(g.F * g.K * g.K * cp) * (t == DC_W ? 2 : 4);
+        d.bytes = (size_t)(g.F * g.K * g.K * cp) * (t == DC_W ? g.esz() : 4);
         break;
     }
     default:
@@ -258,9 +305,13 @@ dc_shard_desc_t describe(const RankPlan &rp, dc_tensor_t t) {
 // kernel configuration helpers
 // ---------------------------------------------------------------------------
 int pick_bkc(int64_t cin_p) { return cin_p % 64 == 0 ? 64 : cin_p % 32 == 0 ? 32 : 16; }
+// GEMM N tile: all output channels up to 256, a multiple of 16 (tcgen05 with
+// M = 128 needs N % 16 == 0; fp32 plans pad channels only to 8, the extra
+// weight rows are TMA zero fill and the epilogue stores only nout_p)
 int pick_bn(int64_t nout_p) {
     static const int cap = std::getenv("DC_V2_BN") ? std::atoi(std::getenv("DC_V2_BN")) : 256;
-    return nout_p <= cap ? (int)nout_p : cap;
+    const int64_t n16 = round_up(nout_p, 16);
+    return n16 <= cap ? (int)n16 : cap;
 }
 int pick_stages(int bkc, int bn) {
     const int stage = 128 * bkc * 2 + bn * bkc * 2;
@@ -374,6 +425,13 @@ struct GemmLaunch {
     int subpix = 0, sub_cp = 0, out_hmax = 0, out_wmax = 0;  // sub-pixel backward-data
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
+    // 3xTF32 (fp32 plans): kind::tf32, input channels in 16-bit units a_cvirt
+    // (the [hi | lo] buffer) vs the weights' K per tap cin_p (hi | lo | hi),
+    // the remap boundary a_seg, fp32 output
+    int kind = 0, a_seg = 0;
+    int64_t a_cvirt = 0;
+    bool out_f32 = false;
+    int64_t cin = 0;           // K per tap of the B matrix, 16-bit units
 };
 
 OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
@@ -397,18 +455,29 @@ void attach_ksplit(dc_plan_s *pl, GemmLaunch &L, int nl) {
     if (L.ksplit <= 1) return;
     const OutRect b = whole(L);
     L.ws_h = b.nh, L.ws_w = b.nw;
-    ensure_alloc(pl->ws2, pl->ws2_bytes, ksplit_bytes(L, nl));
+    ensure_alloc(pl->grave, pl->ws2, pl->ws2_bytes, ksplit_bytes(L, nl));
     L.ws = pl->ws2;
 }
 
-void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunch &L) {
+void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunch &L, cudaStream_t st) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t xd = describe(rp, DC_X), yd = describe(rp, DC_Y);
     ConvGemmParams &p = L.p;
     std::memset(&p, 0, sizeof p);
-    p.bkc = pick_bkc(g.Cp);
-    p.kc = (int)(g.Cp / p.bkc);
+    // K per tap in 16-bit units: C_pad bf16, or [w_hi | w_lo | w_hi] fp32
+    // (3 x 2 C_pad) against the input's [x_hi | x_lo] (2 x 2 C_pad)
+    const bool f32 = g.dt == 1;
+    L.cin = f32 ? 6 * g.Cp : g.Cp;
+    if (f32) {
+        ensure_alloc(pl->grave, pl->wsplit, pl->wsplit_bytes, (size_t)g.F * g.K * g.K * 3 * g.Cp * 4);
+        launch_weight_split(reinterpret_cast<const float *>(w), pl->wsplit, (int)g.F, g.K * g.K, (int)g.C, (int)g.Cp,
+                            st);
+        w = pl->wsplit;
+        L.kind = 1, L.a_seg = (int)(2 * g.Cp), L.a_cvirt = 4 * g.Cp, L.out_f32 = true;
+    }
+    p.bkc = pick_bkc(L.cin);
+    p.kc = (int)(L.cin / p.bkc);
     p.bn = pick_bn(g.Fp);
     p.stages = pick_stages(p.bkc, p.bn);
     p.T = g.K * g.K;
@@ -429,8 +498,8 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     // the A map's box depends on the tile shape of each rect: encoded in launch_rects
     (void)x;
     (void)xd;
-    weight_map(&L.bmap, w, g.F, (int64_t)g.K * g.K * g.Cp, p.bkc, p.bn);
-    L.w_base = w, L.w_rows = g.F, L.w_kcols = (int64_t)g.K * g.K * g.Cp;
+    weight_map(&L.bmap, w, g.F, (int64_t)g.K * g.K * L.cin, p.bkc, p.bn);
+    L.w_base = w, L.w_rows = g.F, L.w_kcols = (int64_t)g.K * g.K * L.cin;
     // halo-dependent output rows/cols (only toward existing neighbours)
     auto count = [&](const DimSplit &d, bool lo) -> int64_t {
         const bool nb = lo ? d.idx > 0 : d.idx + 1 < d.parts;
@@ -453,7 +522,7 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     // per-rank share of the global layer (splitk_world ranks; default: this grid)
     L.work_hint = ceil_div(g.N * ceil_div(g.Ho, kV2TH) * ceil_div(g.Wo, kV2TW) * L.nout_tiles,
                            (int64_t)pl->splitk_world());
-    L.ksplit = choose_ksplit(L.work_hint, g.Cp);
+    L.ksplit = choose_ksplit(L.work_hint, L.cin);
     attach_ksplit(pl, L, (int)rp.nrange.size());
 }
 
@@ -479,6 +548,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     std::memcpy(q.tap_w, L.p.tap_w, sizeof q.tap_w);
     q.cin_p = (int)cin_p;
     q.ksplit = L.ksplit;
+    q.kind = L.kind, q.a_seg = L.a_seg, q.out_f32 = L.out_f32 ? 1 : 0;
     if (L.halo) q.halo = 1, q.hx = *L.halo, q.halo_rect0 = L.halo_rect0;
     q.subpix = L.subpix, q.sub_cp = L.sub_cp, q.out_hmax = L.out_hmax, q.out_wmax = L.out_wmax;
     q.ws = L.ws;
@@ -524,7 +594,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     // on the N = 8 mesh step it moves 0.31 ms from the BN pass into the
     // forwards (conv4_1 fwd 0.31 -> 0.41 ms) for no net gain)
     static const bool nt_multi = std::getenv("DC_BN_FUSE_NT") != nullptr;
-    const bool nt_ok = q.nout_tiles == 1 || (q.bn > 64 && nt_multi);
+    const bool nt_ok = (q.nout_tiles == 1 || (q.bn > 64 && nt_multi)) && !L.out_f32;
     q.bn_stats = !(L.bn_part && L.ksplit == 1 && nt_ok) ? 0
                  : q.bn <= 64                                      ? 2
                  : (int64_t)q.cin_p * q.T >= 1152                  ? 1
@@ -545,9 +615,10 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     }
     q.total_tiles = q.nout_tiles * q.nsamples * q.rect_start[q.nrect];
     CUtensorMap amap;
-    const uint64_t dims[4] = {(uint64_t)cin_p, (uint64_t)ind.wb, (uint64_t)ind.hb, (uint64_t)ind.n};
-    const uint64_t strides[3] = {(uint64_t)(cin_p * 2), (uint64_t)(ind.wb * cin_p * 2),
-                                 (uint64_t)(ind.hb * ind.wb * cin_p * 2)};
+    const int64_t a_c = L.a_cvirt > 0 ? L.a_cvirt : cin_p;  // 16-bit units per input pixel
+    const uint64_t dims[4] = {(uint64_t)a_c, (uint64_t)ind.wb, (uint64_t)ind.hb, (uint64_t)ind.n};
+    const uint64_t strides[3] = {(uint64_t)(a_c * 2), (uint64_t)(ind.wb * a_c * 2),
+                                 (uint64_t)(ind.hb * ind.wb * a_c * 2)};
     if (q.a_swz) {
         const uint32_t box[4] = {(uint32_t)q.cg, (uint32_t)(q.PWs * q.s_in), (uint32_t)q.PH, 1};
         const uint32_t es[4] = {1, (uint32_t)q.s_in, 1, 1};
@@ -598,6 +669,7 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
                   const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
     if (rects.empty()) return;
     if (launch_rects_v2(L, rects, in_base, ind, cin_p, nsamples, st)) return;
+    DC_REQUIRE(L.kind == 0, DC_ERR_UNSUPPORTED, "3xTF32: the tile-reuse kernel does not fit this layer");
     L.bn_ok = false;  // (the v1 kernel has no fused statistics)
     std::map<int, std::vector<OutRect>> by_twl;
     for (auto &r : rects) by_twl[pick_twl(r.nh, r.nw, 128)].push_back(r);
@@ -625,7 +697,7 @@ bool fused_fwd(dc_plan_s *pl, GemmLaunch &L, void *x, const dc_shard_desc_t &xd,
     // 2 and 4 GPUs because 32-row tile pairs put up to half a thin shard into
     // the halo-dependent bands
     static const bool on = std::getenv("DC_FUSED_HALO") != nullptr;
-    if (!on || use_v1() || L.p.T == 0) return false;
+    if (!on || use_v1() || L.p.T == 0 || L.kind != 0) return false;
     const int ho = (int)pl->rp.h.out.size(), wo = (int)pl->rp.w.out.size();
     const int rt = std::min(ho, (int)round_up(L.dep[0], 32));
     const int ie = rt + 32 * std::max(0, (ho - L.dep[1] - rt) / 32);
@@ -640,7 +712,7 @@ bool fused_fwd(dc_plan_s *pl, GemmLaunch &L, void *x, const dc_shard_desc_t &xd,
     const P2PExchange hx = build_p2p(pl, 0, x);
     L.halo = &hx;
     L.halo_rect0 = r0;
-    const bool ok = launch_v2_shape(L, rects, 3, x, xd, pl->rp.g.Cp, nl, st);
+    const bool ok = launch_v2_shape(L, rects, 3, x, xd, L.cin, nl, st);
     L.halo = nullptr;
     return ok;
 }
@@ -652,7 +724,8 @@ P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf) {
     const RankPlan &rp = pl->rp;
     const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
     const auto &recvs = which == 0 ? rp.x_recv : rp.dy_recv;
-    const int64_t cp = which == 0 ? rp.g.Cp : rp.g.Fp;
+    // bytes per pixel of the margined buffer (bf16 c_pad, or fp32 [hi | lo])
+    const int64_t cp = describe(rp, which == 0 ? DC_X : DC_DY).c_pad * rp.g.esz() / 2;  // in 16-bit units
     const int vec16 = (int)(cp * 2 / 16);
     const int64_t nl = rp.nrange.size();
     BufState &B = pl->buf[which];
@@ -699,7 +772,8 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
                "halo exchange needs a communicator (virtual plan or world 1)");
     DC_REQUIRE(!(is_local(pl) && (flags & DC_HALO_NCCL)), DC_ERR_UNSUPPORTED,
                "DC_HALO_NCCL needs real ranks (loopback group)");
-    const int64_t cp = which == 0 ? rp.g.Cp : rp.g.Fp;
+    // bytes per pixel of the margined buffer (bf16 c_pad, or fp32 [hi | lo])
+    const int64_t cp = describe(rp, which == 0 ? DC_X : DC_DY).c_pad * rp.g.esz() / 2;  // in 16-bit units
     const int vec16 = (int)(cp * 2 / 16);
     const int64_t nl = rp.nrange.size();
     BufState &B = pl->buf[which];
@@ -713,7 +787,7 @@ void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t 
         size_t send_bytes = 0, recv_bytes = 0;
         for (auto &m : sends) send_bytes += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
         for (auto &m : recvs) recv_bytes += (size_t)nl * m.rows.size() * m.cols.size() * cp * 2;
-        ensure_alloc(reinterpret_cast<uint8_t *&>(B.stage), B.stage_bytes, send_bytes + recv_bytes);
+        ensure_alloc(pl->grave, reinterpret_cast<uint8_t *&>(B.stage), B.stage_bytes, send_bytes + recv_bytes);
         uint8_t *sbuf = reinterpret_cast<uint8_t *>(B.stage), *rbuf = sbuf + send_bytes;
         CopyBatch pack{};
         size_t off = 0;
@@ -884,7 +958,7 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
     const ConvGeom &g = rp.g;
     static const bool off = std::getenv("DC_NO_SUBPIX") != nullptr;
     static const int max_c = std::getenv("DC_SUBPIX_MAXC") ? std::atoi(std::getenv("DC_SUBPIX_MAXC")) : 32;
-    if (off || use_v1() || g.S != 2 || g.Cp > max_c || 4 * g.Cp > 256) return false;
+    if (off || use_v1() || g.dt != 0 || g.S != 2 || g.Cp > max_c || 4 * g.Cp > 256) return false;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
     const int K = g.K, P = g.P;
     const int dmin = -(int)floor_div(K - 1 - P, 2), dmax = (int)floor_div(P + 1, 2);
@@ -903,7 +977,7 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
     dim(rp.w, t0w, ntw, orw, o0w, omw);
     if (nth <= 0 || ntw <= 0) return true;  // nothing owned
     const int64_t rows = 4 * g.Cp, kcols = (int64_t)T * g.Fp;
-    ensure_alloc(pl->wt, pl->wt_bytes, (size_t)rows * kcols * 2);
+    ensure_alloc(pl->grave, pl->wt, pl->wt_bytes, (size_t)rows * kcols * 2);
     GemmLaunch L;
     ConvGemmParams &p = L.p;
     std::memset(&p, 0, sizeof p);
@@ -922,6 +996,7 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
     L.nout_tiles = 1;
     L.subpix = 1, L.sub_cp = (int)g.Cp, L.out_hmax = omh, L.out_wmax = omw;
     L.w_base = pl->wt, L.w_rows = rows, L.w_kcols = kcols;
+    L.cin = g.Fp;
     weight_map(&L.bmap, pl->wt, rows, kcols, p.bkc, p.bn);
     L.ksplit = 1;  // (the split-K reduce has no sub-pixel mapping)
     L.work_hint = ceil_div(g.N * ceil_div(ceil_div(g.H, 2), kV2TH) * ceil_div(ceil_div(g.W, 2), kV2TW),
@@ -945,7 +1020,11 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
     const int S = g.S;
-    // per-phase weights: [Cp][T][Fp] each, at increasing offsets
+    // K per tap of a phase GEMM in 16-bit units: F_pad bf16, or the 3xTF32
+    // [w_hi | w_lo | w_hi] fp32 segments against dy's [hi | lo] (tf32.cuh)
+    const bool f32 = g.dt == 1;
+    const int64_t kc = f32 ? 6 * g.Fp : g.Fp;
+    // per-phase weights: [Cp][T][kc] each (16-bit units), at increasing offsets
     std::vector<Phase> ph;
     size_t wt_need = 0;
     for (int rh = 0; rh < S; ++rh)
@@ -967,9 +1046,9 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             f.nt_h = a.nt, f.nt_w = b.nt;
             f.bl = a.bl, f.bh = a.bh, f.bwl = b.bl, f.bwh = b.bh;
             ph.push_back(f);
-            wt_need += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+            wt_need += (size_t)g.Cp * std::max(f.T, 1) * kc * 2;
         }
-    ensure_alloc(pl->wt, pl->wt_bytes, wt_need);
+    ensure_alloc(pl->grave, pl->wt, pl->wt_bytes, wt_need);
     {   // the rotated / transposed weights of every active phase in one launch
         int8_t ka[kMaxTaps], kb[kMaxTaps];
         int Ts[kMaxTaps], ts[kMaxTaps];
@@ -979,25 +1058,32 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         for (auto &f : ph) {
             if (f.active)
                 for (int t = 0; t < f.T; ++t) {
-                    ka[nt] = f.ka[t], kb[nt] = f.kb[t], Ts[nt] = f.T, ts[nt] = t, offs[nt] = (long long)(o / 2);
+                    ka[nt] = f.ka[t], kb[nt] = f.kb[t], Ts[nt] = f.T, ts[nt] = t,
+                    offs[nt] = (long long)(o / (f32 ? 4 : 2));  // in elements
                     ++nt;
                 }
-            o += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+            o += (size_t)g.Cp * std::max(f.T, 1) * kc * 2;
         }
-        launch_weight_transform_multi(reinterpret_cast<const __nv_bfloat16 *>(w), pl->wt, (int)g.F, (int)g.Fp,
-                                      (int)g.C, (int)g.Cp, g.K, nt, ka, kb, Ts, ts, offs, st);
+        if (f32)
+            launch_weight_transform_tf32(reinterpret_cast<const float *>(w), reinterpret_cast<float *>(pl->wt),
+                                         (int)g.F, (int)g.Fp, (int)g.C, (int)g.Cp, g.K, nt, ka, kb, Ts, ts, offs, st);
+        else
+            launch_weight_transform_multi(reinterpret_cast<const __nv_bfloat16 *>(w), pl->wt, (int)g.F, (int)g.Fp,
+                                          (int)g.C, (int)g.Cp, g.K, nt, ka, kb, Ts, ts, offs, st);
     }
     std::vector<GemmLaunch> L(ph.size());
     size_t off = 0;
     for (size_t i = 0; i < ph.size(); ++i) {
         Phase &f = ph[i];
         __nv_bfloat16 *wt = pl->wt + off / 2;
-        off += (size_t)g.Cp * std::max(f.T, 1) * g.Fp * 2;
+        off += (size_t)g.Cp * std::max(f.T, 1) * kc * 2;
         if (!f.active) continue;
         ConvGemmParams &p = L[i].p;
         std::memset(&p, 0, sizeof p);
-        p.bkc = pick_bkc(g.Fp);
-        p.kc = (int)(g.Fp / p.bkc);
+        L[i].cin = kc;
+        if (f32) L[i].kind = 1, L[i].a_seg = (int)(2 * g.Fp), L[i].a_cvirt = 4 * g.Fp, L[i].out_f32 = true;
+        p.bkc = pick_bkc(kc);
+        p.kc = (int)(kc / p.bkc);
         p.bn = pick_bn(g.Cp);
         p.stages = pick_stages(p.bkc, p.bn);
         p.T = f.T;
@@ -1010,14 +1096,14 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
         p.out_h0 = f.out_h0, p.out_w0 = f.out_w0, p.out_dh = S, p.out_dw = S;
         p.nout_p = (int)g.Cp;
         L[i].nout_tiles = (int)ceil_div(g.Cp, p.bn);
-        weight_map(&L[i].bmap, wt, g.Cp, (int64_t)std::max(f.T, 1) * g.Fp, p.bkc, p.bn);
-        L[i].w_base = wt, L[i].w_rows = g.Cp, L[i].w_kcols = (int64_t)std::max(f.T, 1) * g.Fp;
+        weight_map(&L[i].bmap, wt, g.Cp, (int64_t)std::max(f.T, 1) * kc, p.bkc, p.bn);
+        L[i].w_base = wt, L[i].w_rows = g.Cp, L[i].w_kcols = (int64_t)std::max(f.T, 1) * kc;
         Split2D s{f.nt_h, f.nt_w, f.bl, f.bh, f.bwl, f.bwh};
         make_rects(s, L[i].interior, L[i].boundary);
         L[i].work_hint = ceil_div(g.N * ceil_div(ceil_div(g.H, S), kV2TH) * ceil_div(ceil_div(g.W, S), kV2TW) *
                                       L[i].nout_tiles,
                                   (int64_t)pl->splitk_world());
-        L[i].ksplit = choose_ksplit(L[i].work_hint, g.Fp);
+        L[i].ksplit = choose_ksplit(L[i].work_hint, kc);
     }
     // one split-K workspace region per phase: the phases' interior and
     // boundary launches may run concurrently on two streams
@@ -1028,7 +1114,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             ks_off[i] = ks_need;
             ks_need += ksplit_bytes(L[i], (int)rp.nrange.size());
         }
-    ensure_alloc(pl->ws2, pl->ws2_bytes, ks_need);
+    ensure_alloc(pl->grave, pl->ws2, pl->ws2_bytes, ks_need);
     for (size_t i = 0; i < ph.size(); ++i)
         if (ph[i].active && L[i].ksplit > 1) {
             const OutRect b = whole(L[i]);
@@ -1052,7 +1138,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             if (!ph[i].active) continue;
             cudaStream_t sp = pl->s_ph[k];
             CK(cudaStreamWaitEvent(sp, pl->ev_ph[0], 0));
-            launch_rects(L[i], {whole(L[i])}, dy, dyd, g.Fp, (int)rp.nrange.size(), sp);
+            launch_rects(L[i], {whole(L[i])}, dy, dyd, kc, (int)rp.nrange.size(), sp);
             CK(cudaEventRecord(pl->ev_ph[1 + k], sp));
             ++k;
         }
@@ -1062,12 +1148,12 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     for (size_t i = 0; i < ph.size(); ++i) {
         if (!ph[i].active) continue;
         std::vector<OutRect> rects = overlap ? L[i].interior : std::vector<OutRect>{whole(L[i])};
-        launch_rects(L[i], rects, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
+        launch_rects(L[i], rects, dy, dyd, kc, (int)rp.nrange.size(), st);
     }
     if (overlap) {  // boundary tiles on the comm stream after the exchange, joined
         for (size_t i = 0; i < ph.size(); ++i)
             if (ph[i].active)
-                launch_rects(L[i], L[i].boundary, dy, dyd, g.Fp, (int)rp.nrange.size(), pl->s_comm);
+                launch_rects(L[i], L[i].boundary, dy, dyd, kc, (int)rp.nrange.size(), pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
     }
@@ -1086,7 +1172,8 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
 // partials + the fixed-order reduce launch, whichever the model finds cheaper.
 int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split, bool allow_atomic, bool *atomic) {
     const int sms = device_sm_count();
-    const double mma_ns = (q.bw / 2) * q.G * (27.0 + 0.41 * q.bn) / 1.9;
+    const int nks = q.kind == 1 ? 8 : q.bw / 2;  // MMAs per block and M tile (K = 8 tf32 / 16 bf16)
+    const double mma_ns = nks * q.G * (27.0 + 0.41 * q.bn) / 1.9;
     const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
     static const double sm_gbs = std::getenv("DC_WGRAD_SM_GBS") ? std::atof(std::getenv("DC_WGRAD_SM_GBS")) : 40.0;
     int best = 1;
@@ -1126,12 +1213,16 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     const ConvGeom &g = rp.g;
     const dc_shard_desc_t xd = describe(rp, DC_X), dyd = describe(rp, DC_DY);
     const int64_t ho = rp.h.out.size(), wo = rp.w.out.size(), nl = rp.nrange.size();
-    const __nv_bfloat16 *dy_owned = reinterpret_cast<const __nv_bfloat16 *>(dy) +
-                                    (dyd.halo_n * dyd.wb + dyd.halo_w) * g.Fp;
-    if (!use_v1() && g.Fp % 64 == 0) {
+    const bool f32 = g.dt == 1;
+    const int esz = g.esz();
+    // dy WITHOUT its halo: maps over the owned block only
+    const void *dy_owned = reinterpret_cast<const uint8_t *>(dy) +
+                           (size_t)(dyd.halo_n * dyd.wb + dyd.halo_w) * dyd.c_pad * esz;
+    if (!use_v1() && (f32 || g.Fp % 64 == 0)) {
         // tile-reuse kernel (wgrad_v2.cu)
         WgradV2Params q;
         std::memset(&q, 0, sizeof q);
+        q.kind = f32 ? 1 : 0;
         q.s_in = g.S;
         q.origin_h = (int)(g.S * rp.h.out.lo - g.P - rp.h.xbuf.lo);
         q.origin_w = (int)(g.S * rp.w.out.lo - g.P - rp.w.xbuf.lo);
@@ -1142,7 +1233,13 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
         if (wgrad_v2_configure(q, kV2SmemLimit)) {
             q.tiles_h = (int)ceil_div(ho, 8);
             q.tiles_w = (int)ceil_div(wo, (int64_t)q.bw);
-            q.nblocks = (int)(nl * q.tiles_h * q.tiles_w);
+            // 3xTF32: three passes over the pixel blocks, one accumulation
+            // (x_hi dy_hi, x_hi dy_lo, x_lo dy_hi; the lo halves sit Cp / Fp
+            // channels after the hi halves in the [hi | lo] buffers)
+            q.passes = f32 ? 3 : 1;
+            q.nblocks_pix = (int)(nl * q.tiles_h * q.tiles_w);
+            q.nblocks = q.passes * q.nblocks_pix;
+            q.x_lo = (int)g.Cp, q.dy_lo = (int)g.Fp;
             const int mgroups = wgrad_v2_mgroups(q), ntiles = (int)ceil_div(g.Fp, q.bn);
             const long long per_split = (long long)g.F * q.T * g.C;  // dW: [F][K][K][C]
             const long long split_stride = round_up(per_split, 4);
@@ -1153,36 +1250,41 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
             q.ws_split = split_stride;
             if (splits > 1 && atomic) {
                 // splits accumulate into the zeroed dW (no partials, no reduce
-                // launch); fp32 addition order varies run to run (DC_DETERMINISTIC)
+                // launch); fp32 addition order varies run to run (DC_DW_ATOMIC)
                 CK(cudaMemsetAsync(dw, 0, (size_t)per_split * 4, st));
                 q.ws = dw, q.ws_split = 0, q.atomic_out = 1;
             } else if (splits > 1) {
-                ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
+                ensure_alloc(pl->grave, pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
                 q.ws = pl->ws;
             } else {
                 q.ws = dw;
             }
             CUtensorMap xmap, dymap;
-            {
-                const uint64_t dims[4] = {(uint64_t)g.Cp, (uint64_t)xd.wb, (uint64_t)xd.hb, (uint64_t)xd.n};
-                const uint64_t strides[3] = {(uint64_t)(g.Cp * 2), (uint64_t)(xd.wb * g.Cp * 2),
-                                             (uint64_t)(xd.hb * xd.wb * g.Cp * 2)};
-                const uint32_t box[4] = {(uint32_t)q.cgw, (uint32_t)(q.pitch * g.S), (uint32_t)q.PH, 1};
-                const uint32_t es[4] = {1, (uint32_t)g.S, 1, 1};
-                make_tmap(&xmap, x, 4, dims, strides, box, es, q.cgw * 2);
-            }
-            {
-                const uint64_t dims[4] = {(uint64_t)g.Fp, (uint64_t)wo, (uint64_t)ho, (uint64_t)nl};
-                const uint64_t strides[3] = {(uint64_t)(g.Fp * 2), (uint64_t)(dyd.wb * g.Fp * 2),
-                                             (uint64_t)(dyd.hb * dyd.wb * g.Fp * 2)};
-                const uint32_t box[4] = {64, (uint32_t)q.bw, 8, 1};
-                make_tmap(&dymap, dy_owned, 4, dims, strides, box, nullptr, 128);
+            const int64_t xc = xd.c_pad, fc = dyd.c_pad;  // elements per pixel of the buffers
+            const uint64_t xdims[4] = {(uint64_t)xc, (uint64_t)xd.wb, (uint64_t)xd.hb, (uint64_t)xd.n};
+            const uint64_t xstr[3] = {(uint64_t)(xc * esz), (uint64_t)(xd.wb * xc * esz),
+                                      (uint64_t)(xd.hb * xd.wb * xc * esz)};
+            const uint32_t xbox[4] = {(uint32_t)q.cgw, (uint32_t)(q.pitch * g.S), (uint32_t)q.PH, 1};
+            const uint32_t xes[4] = {1, (uint32_t)g.S, 1, 1};
+            const uint64_t ddims[4] = {(uint64_t)fc, (uint64_t)wo, (uint64_t)ho, (uint64_t)nl};
+            const uint64_t dstr[3] = {(uint64_t)(fc * esz), (uint64_t)(dyd.wb * fc * esz),
+                                      (uint64_t)(dyd.hb * dyd.wb * fc * esz)};
+            const uint32_t dbox[4] = {(uint32_t)(128 / esz), (uint32_t)q.bw, 8, 1};
+            if (f32) {  // MN-major tf32 operands: 128-byte rows, 32-byte-granule swizzle
+                make_tmap_ex(&xmap, x, 4, xdims, xstr, xbox, xes, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                             CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+                make_tmap_ex(&dymap, dy_owned, 4, ddims, dstr, dbox, nullptr, CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                             CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+            } else {
+                make_tmap(&xmap, x, 4, xdims, xstr, xbox, xes, q.cgw * 2);
+                make_tmap(&dymap, dy_owned, 4, ddims, dstr, dbox, nullptr, 128);
             }
             launch_wgrad_v2(xmap, dymap, q, st);
             if (splits > 1 && !q.atomic_out) launch_splitk_reduce(pl->ws, splits, per_split, split_stride, dw, st);
             return;
         }
     }
+    DC_REQUIRE(!f32, DC_ERR_UNSUPPORTED, "3xTF32 backward-filter: the tile-reuse kernel does not fit this layer");
     WgradParams p;
     std::memset(&p, 0, sizeof p);
     p.T = g.K * g.K;
@@ -1219,7 +1321,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     p.C = (int)g.C;
     p.ws_split = split_stride;
     if (splits > 1) {
-        ensure_alloc(pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
+        ensure_alloc(pl->grave, pl->ws, pl->ws_bytes, (size_t)splits * split_stride * 4);
         p.ws = pl->ws;
     } else {
         p.ws = dw;
@@ -1282,6 +1384,13 @@ void ensure_local_resources(dc_plan_s *pl) {
     for (auto &sp : pl->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
     for (auto &e : pl->ev_ph) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 4 * pl->rp.g.Fp));  // local sums, global sums
+}
+
+// Make `st` wait for a DC_IMPORT_ASYNC import into buffer `which` (0: x, 1: dy).
+void join_import(dc_plan_s *pl, int which, cudaStream_t st) {
+    if (!pl->import_pending[which]) return;
+    CK(cudaStreamWaitEvent(st, pl->ev_copy_out[which], 0));
+    pl->import_pending[which] = false;
 }
 
 dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, bool is_virtual) {
@@ -1393,6 +1502,7 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
     DC_REQUIRE(out != nullptr && world >= 1 && rank >= 0 && rank < world, DC_ERR_ARG,
                "bad rank/world (%d/%d)", rank, world);
     CK(cudaSetDevice(device));
+    preload_kernels();
     auto *c = new dc_comm_s();
     c->rank = rank, c->world = world, c->device = device;
     if (world > 1) {
@@ -1417,6 +1527,7 @@ dc_status_t dc_comm_create_local(int world, int device, dc_comm_t *comms) {
     DC_API_BEGIN
     DC_REQUIRE(comms != nullptr && world >= 1 && world <= 64, DC_ERR_ARG, "bad loopback world %d", world);
     CK(cudaSetDevice(device));
+    preload_kernels();
     auto G = std::make_shared<LocalGroup>();
     G->world = world;
     for (int r = 0; r < world; ++r) {
@@ -1459,8 +1570,8 @@ dc_status_t dc_plan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F
                            dc_comm_t comm, dc_plan_t *out) {
     DC_API_BEGIN
     DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
-    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "only DC_BF16 is implemented");
-    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    DC_REQUIRE(dtype == DC_BF16 || dtype == DC_FP32_3XTF32, DC_ERR_ARG, "unknown dtype %d", (int)dtype);
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad, dtype == DC_FP32_3XTF32 ? 1 : 0);
     const int world = comm ? comm->world : 1, rank = comm ? comm->rank : 0;
     Grid grid{decomp.pn, decomp.ph, decomp.pw};
     double pred = 0;
@@ -1502,8 +1613,8 @@ dc_status_t dc_plan_create_virtual(int64_t N, int64_t C, int64_t H, int64_t W, i
                                    int rank, dc_plan_t *out) {
     DC_API_BEGIN
     DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
-    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "only DC_BF16 is implemented");
-    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad);
+    DC_REQUIRE(dtype == DC_BF16 || dtype == DC_FP32_3XTF32, DC_ERR_ARG, "unknown dtype %d", (int)dtype);
+    ConvGeom g = make_geom(N, C, H, W, F, K, stride, pad, dtype == DC_FP32_3XTF32 ? 1 : 0);
     Grid grid{decomp.pn, decomp.ph, decomp.pw};
     dc_plan_s *pl = create_plan(g, grid, rank, nullptr, true);
     pl->predicted = model_layer_cost(g, grid, true);
@@ -1587,9 +1698,57 @@ dc_status_t dc_buffer_alloc(dc_plan_t pl, dc_tensor_t t, void **dev_ptr) {
     DC_API_END
 }
 
+dc_status_t dc_tensor_import(dc_plan_t pl, dc_tensor_t t, const void *src, void *dst, unsigned flags,
+                             void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && src && dst && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    DC_REQUIRE((flags & ~(DC_IMPORT_ASYNC | DC_SRC_BF16)) == 0, DC_ERR_ARG, "unknown import flags 0x%x", flags);
+    const ConvGeom &g = pl->rp.g;
+    DC_REQUIRE(!((flags & DC_SRC_BF16) && g.dt), DC_ERR_ARG, "DC_SRC_BF16 needs a DC_BF16 plan");
+    NoPdlScope no_pdl(is_local(pl));
+    ensure_local_resources(pl);
+    const int which = t == DC_X ? 0 : 1;
+    const dc_shard_desc_t d = describe(pl->rp, t);
+    const int cp = (int)(g.dt ? d.c_pad / 2 : d.c_pad);
+    const bool bf16_src = (flags & DC_SRC_BF16) != 0;
+    const size_t src_bytes = (size_t)d.n * d.h * d.w * d.c * (bf16_src ? 2 : 4);
+    cudaPointerAttributes pa{};
+    CK(cudaPointerGetAttributes(&pa, src));
+    const bool host = pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged;
+    cudaStream_t st = (cudaStream_t)stream, cs = st;
+    if (flags & DC_IMPORT_ASYNC) {  // on the copy stream, after the caller's work so far
+        if (!pl->s_copy) {
+            CK(cudaStreamCreateWithFlags(&pl->s_copy, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaEventCreateWithFlags(&pl->ev_copy_in[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&pl->ev_copy_out[i], cudaEventDisableTiming));
+            }
+        }
+        cs = pl->s_copy;
+        CK(cudaEventRecord(pl->ev_copy_in[which], st));
+        CK(cudaStreamWaitEvent(cs, pl->ev_copy_in[which], 0));
+    }
+    const void *dsrc = src;
+    if (host) {  // host buffer: one H2D copy into the plan's staging, then the layout kernel
+        uint8_t *&sp = reinterpret_cast<uint8_t *&>(pl->stage[which]);
+        ensure_alloc(pl->grave, sp, pl->stage_bytes[which], std::max<size_t>(src_bytes, 16));
+        CK(cudaMemcpyAsync(sp, src, src_bytes, cudaMemcpyHostToDevice, cs));
+        dsrc = sp;
+    }
+    launch_import(dsrc, bf16_src, dst, (int)d.n, (int)d.h, (int)d.w, (int)d.c, cp, (int)d.hb, (int)d.wb, d.halo_n,
+                  d.halo_w, g.dt, cs);
+    if (flags & DC_IMPORT_ASYNC) {
+        CK(cudaEventRecord(pl->ev_copy_out[which], cs));
+        pl->import_pending[which] = true;
+    }
+    DC_API_END
+}
+
 dc_status_t dc_halo_exchange(dc_plan_t pl, dc_tensor_t t, void *buf, unsigned flags, void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && buf && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
+    join_import(pl, t == DC_X ? 0 : 1, (cudaStream_t)stream);
     exchange(pl, t == DC_X ? 0 : 1, buf, flags, (cudaStream_t)stream);
     DC_API_END
 }
@@ -1598,16 +1757,18 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
                         void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && x && w && y, DC_ERR_ARG, "null argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
+    join_import(pl, 0, st);
     GemmLaunch L;
-    prepare_fwd(pl, x, w, y, L);
+    prepare_fwd(pl, x, w, y, L, st);
     pl->bn_fused_y = nullptr;
     pl->bn_fused_epoch = 0;
     ++pl->fwd_epoch;
     if (flags & DC_BN_STATS) {
         L.bn_slot_cap = 8 * device_sm_count();
-        ensure_alloc(pl->bn_fpart, pl->bn_fpart_bytes, sizeof(double) * L.bn_slot_cap * 2 * pl->rp.g.Fp);
+        ensure_alloc(pl->grave, pl->bn_fpart, pl->bn_fpart_bytes, sizeof(double) * L.bn_slot_cap * 2 * pl->rp.g.Fp);
         L.bn_part = pl->bn_fpart;
     }
     const dc_shard_desc_t xd = describe(pl->rp, DC_X);
@@ -1617,7 +1778,7 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     const bool overlap = need_x && !no_overlap_env;
     if (need_x && !overlap) {  // exchange, then one launch over the whole shard
         exchange(pl, 0, x, flags, st);
-        launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
+        launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);
     } else if (overlap && !(flags & DC_HALO_NCCL) && fused_fwd(pl, L, x, xd, nl, st)) {
         // one kernel: P2P halo stores + interior tiles, halo-dependent tiles last
     } else if (overlap) {
@@ -1632,13 +1793,13 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         // (measured neutral at 4 GPUs with 8 or 16 reserved SMs: default 0)
         static const int reserve = std::getenv("DC_HALO_RESERVE") ? std::atoi(std::getenv("DC_HALO_RESERVE")) : 0;
         L.max_ctas = std::max(1, device_sm_count() - reserve);
-        launch_rects(L, L.interior, x, xd, pl->rp.g.Cp, nl, st);
+        launch_rects(L, L.interior, x, xd, L.cin, nl, st);
         L.max_ctas = 0;
-        launch_rects(L, L.boundary, x, xd, pl->rp.g.Cp, nl, pl->s_comm);
+        launch_rects(L, L.boundary, x, xd, L.cin, nl, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
     } else {
-        launch_rects(L, {whole(L)}, x, xd, pl->rp.g.Cp, nl, st);
+        launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);
     }
     if (L.bn_part && L.bn_ok && L.bn_slot > 0) {  // dc_bn_spatial_stats(y) reduces these
         pl->bn_fused_y = y;
@@ -1652,7 +1813,9 @@ dc_status_t dc_conv_bwd_data(dc_plan_t pl, void *dy, const void *w, void *dx, un
                              void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && dy && w && dx, DC_ERR_ARG, "null argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
     ensure_local_resources(pl);
+    join_import(pl, 1, (cudaStream_t)stream);
     run_bwd_data(pl, dy, w, dx, flags, (cudaStream_t)stream);
     signal_ready_next(pl, 1, dy, (cudaStream_t)stream);
     DC_API_END
@@ -1662,8 +1825,11 @@ dc_status_t dc_conv_bwd_filter(dc_plan_t pl, const void *x, const void *dy, floa
                                unsigned flags, void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && x && dy && dw, DC_ERR_ARG, "null argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
+    join_import(pl, 0, st);
+    join_import(pl, 1, st);
     run_bwd_filter(pl, x, dy, dw, st, (flags & DC_DW_ATOMIC) != 0);
     signal_ready_next(pl, 0, x, st);
     if ((flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC)) allreduce_dw_async(pl, dw, st);
@@ -1675,8 +1841,11 @@ dc_status_t dc_conv_bwd(dc_plan_t pl, const void *x, void *dy, const void *w, vo
                         unsigned flags, void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && x && dy && w && dx && dw, DC_ERR_ARG, "null argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
+    join_import(pl, 0, st);
+    join_import(pl, 1, st);
     const bool halo = (flags & DC_EXCHANGE) && (!pl->rp.dy_send.empty() || !pl->rp.dy_recv.empty());
     const bool ar_async = (flags & DC_ALLREDUCE) && (flags & DC_ALLREDUCE_ASYNC) && pl->world() > 1;
     const bool ar = (flags & DC_ALLREDUCE) && pl->world() > 1 && !ar_async;
@@ -1706,14 +1875,15 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
                                 void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(pl && t && mean && var, DC_ERR_ARG, "null argument");
+    NoPdlScope no_pdl(is_local(pl));  // (loopback: ranks share the SMs)
     DC_REQUIRE((flags & ~(DC_BN_LOCAL | DC_BN_FROM_FWD)) == 0, DC_ERR_ARG, "unknown BN flags 0x%x", flags);
     ensure_local_resources(pl);
     cudaStream_t st = (cudaStream_t)stream;
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const long long npix = rp.nrange.size() * rp.h.out.size() * rp.w.out.size();
-    const size_t need = sizeof(double) * 2 * g.Fp * bn_partial_blocks(npix, (int)g.Fp);
-    ensure_alloc(pl->bn_part, pl->bn_part_bytes, need);
+    const int nblk = g.dt ? bn_partial_blocks_f32(npix, (int)g.Fp) : bn_partial_blocks(npix, (int)g.Fp);
+    ensure_alloc(pl->grave, pl->bn_part, pl->bn_part_bytes, sizeof(double) * 2 * g.Fp * nblk);
     const bool global = !(flags & DC_BN_LOCAL) && pl->bn_group > 1;
     // the partials of this plan's latest forward, if it ran with DC_BN_STATS
     // on this tensor and the caller states t is unchanged since (DC_BN_FROM_FWD);
@@ -1721,10 +1891,14 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     const bool fused = (flags & DC_BN_FROM_FWD) && pl->bn_fused_y == t && pl->bn_fused_epoch != 0 &&
                        pl->bn_fused_epoch == pl->fwd_epoch && pl->bn_fused_slots > 0;
     // single group: the reduce kernel also finalises mean/var (no allreduce between)
-    if (fused)
+    if (fused) {
         launch_bn_reduce(pl->bn_fpart, pl->bn_fused_slots, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix,
                          global ? nullptr : mean, global ? nullptr : var, st);
-    else
+    } else if (g.dt) {  // fp32 y (3xTF32 plans): fp64 partials per block, the same reduction
+        launch_bn_partials_f32(reinterpret_cast<const float *>(t), npix, (int)g.Fp, pl->bn_part, st);
+        launch_bn_reduce(pl->bn_part, nblk, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix, global ? nullptr : mean,
+                         global ? nullptr : var, st);
+    } else
         launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
                        (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
     pl->bn_fused_y = nullptr;

@@ -393,6 +393,23 @@ void make_tmap(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims,
                rank > 1 ? b[1] : 0, swizzle_bytes);
 }
 
+void make_tmap_ex(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
+                  const uint32_t *box, const uint32_t *estrides, CUtensorMapDataType dt, CUtensorMapSwizzle sw) {
+    cuuint64_t d[5], s[4];
+    cuuint32_t b[5], e[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        e[i] = estrides ? estrides[i] : 1;
+        if (i < rank - 1) s[i] = strides_bytes[i];
+    }
+    CUresult r = get_encode()(m, dt, rank, const_cast<void *>(ptr), d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    DC_REQUIRE(r == CUDA_SUCCESS, DC_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): rank %d dims %llu,%llu box %u,%u",
+               (int)r, rank, (unsigned long long)d[0], (unsigned long long)(rank > 1 ? d[1] : 0), b[0],
+               rank > 1 ? b[1] : 0);
+}
+
 size_t conv_gemm_smem_bytes(int bkc, int bn, int stages) {
     return 1024 + (size_t)stages * (128 * bkc * 2 + bn * bkc * 2) + (2 * stages + 1) * 8 + 16;
 }
@@ -492,6 +509,20 @@ void launch_weight_transform(const __nv_bfloat16 *w, __nv_bfloat16 *wt, int F, i
     long long off[kMaxTaps];
     for (int i = 0; i < T; ++i) Ts[i] = T, ts[i] = i, off[i] = 0;
     launch_weight_transform_multi(w, wt, F, Fp, C, Cp, K, T, ka, kb, Ts, ts, off, st);
+}
+
+
+// Loads this file's kernels now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which waits for the device: with the spinning
+// halo / BN protocol kernels of a loopback group in flight, that wait never
+// ends).
+void preload_conv_tc() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_gemm_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(wgrad_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(splitk_reduce_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(weight_transform_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(subpix_weight_kernel));
 }
 
 }  // namespace dc

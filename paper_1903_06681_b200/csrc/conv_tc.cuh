@@ -66,6 +66,11 @@ void make_tmap(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims,
                const uint64_t *strides_bytes /* rank-1 */, const uint32_t *box,
                const uint32_t *estrides, int swizzle_bytes);
 
+// The same with an explicit element type and swizzle mode (e.g. fp32 with
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B for MN-major tf32 operands).
+void make_tmap_ex(CUtensorMap *m, const void *ptr, int rank, const uint64_t *dims, const uint64_t *strides_bytes,
+                  const uint32_t *box, const uint32_t *estrides, CUtensorMapDataType dt, CUtensorMapSwizzle sw);
+
 void launch_conv_gemm(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvGemmParams &p,
                       int nsamples, int nout_tiles, cudaStream_t st);
 void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradParams &p,

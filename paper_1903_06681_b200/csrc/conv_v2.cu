@@ -67,38 +67,44 @@ __device__ __forceinline__ TileCoord decode(const ConvV2Params &p, int u) {
 constexpr int kMaxBar = 16;
 
 // one tcgen05.mma of the kernel's CTA group (1: this SM; 2: the pair, M = 256)
-template <int CG>
+// KIND 0: kind::f16 (bf16 x bf16 -> fp32); KIND 1: kind::tf32 (fp32 operands
+// read as tf32, 8 per 32-byte K step: the same smem geometry as 16 bf16)
+template <int CG, int KIND>
 __device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if constexpr (CG == 2)
+    if constexpr (KIND == 1) {
+        static_assert(CG == 1, "tf32 kernels run on single CTAs");
+        mma_tf32(d, a, b, idesc, acc);
+    } else if constexpr (CG == 2) {
         mma_bf16_cg2(d, a, b, idesc, acc);
-    else
+    } else {
         mma_bf16(d, a, b, idesc, acc);
+    }
 }
 
 // Streamed weights: the MMAs of one weight slot (one tap of one channel group):
 // NK x K16 steps for each of TPW stacked tiles, fully unrolled (compile-time
 // multiples of hoisted strides, no per-MMA descriptor arithmetic chains).
-template <int CG, int NK, int TPW>
+template <int CG, int KIND, int NK, int TPW>
 __device__ __forceinline__ void issue_slot(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t a_kstep,
                                            uint32_t a_tile16, uint32_t acc_cols, uint32_t idesc, bool first) {
 #pragma unroll
     for (int k16 = 0; k16 < NK; ++k16)
 #pragma unroll
         for (int tt = 0; tt < TPW; ++tt)
-            mma_cg<CG>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
+            mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
                        (first && k16 == 0) ? 0u : 1u);
 }
-template <int CG>
+template <int CG, int KIND>
 __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tmem, uint64_t ad, uint64_t bd,
                                                uint32_t a_kstep, uint32_t a_tile16, uint32_t acc_cols,
                                                uint32_t idesc, bool first) {
     switch ((nk16 << 4) | tpw) {
-    case 0x41: issue_slot<CG, 4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x42: issue_slot<CG, 4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x21: issue_slot<CG, 2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x22: issue_slot<CG, 2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x11: issue_slot<CG, 1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    default: issue_slot<CG, 1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x41: issue_slot<CG, KIND, 4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x42: issue_slot<CG, KIND, 4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x21: issue_slot<CG, KIND, 2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x22: issue_slot<CG, KIND, 2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x11: issue_slot<CG, KIND, 1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    default: issue_slot<CG, KIND, 1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
     }
 }
 
@@ -107,7 +113,7 @@ __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tme
 // stride hoisted out of the loop, so the single issuing thread spends a few
 // uniform instructions per tcgen05.mma instead of a dependent chain of
 // constant loads and 64-bit adds per tap (measured: ~180 cycles per tap).
-template <int CG, int KH, int KW, int NK, int SSH, int TPW>
+template <int CG, int KIND, int KH, int KW, int NK, int SSH, int TPW>
 __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, uint64_t bd,
                                            uint32_t a_row16, uint32_t a_col16, uint32_t a_par16,
                                            uint32_t a_kstep, uint32_t b_slot16, uint32_t idesc,
@@ -123,13 +129,13 @@ __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, ui
             for (int k = 0; k < NK; ++k)
 #pragma unroll
                 for (int tt = 0; tt < TPW; ++tt)  // the tiles of the work item share the B slice
-                    mma_cg<CG>(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
+                    mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
                                idesc, (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
         }
 }
 
 // Dispatch to an unrolled specialisation; false if none matches.
-template <int CG>
+template <int CG, int KIND>
 __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16, uint32_t d_tmem,
                                                  uint64_t a_stage, uint64_t bd, uint32_t a_kstep,
                                                  uint32_t b_slot16, uint32_t idesc, bool first,
@@ -137,11 +143,11 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
     const int key = (p.tpw << 16) | (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
 #define DC_TAPS(KH, KW, NK, SS)                                                                   \
     case ((1 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<CG, KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<CG, KIND, KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;                                                                              \
     case ((2 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<CG, KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<CG, KIND, KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;
     switch (key) {
@@ -190,7 +196,7 @@ constexpr int kV2Threads = 352;
 
 // CG = 2: CTA pairs run tcgen05 with cta_group::2 (M = 256 per MMA; each CTA
 // holds its own A tile and half of every weight slot; the leader issues).
-template <int CG>
+template <int CG, int KIND>
 __global__ void __launch_bounds__(kV2Threads, 1)
     conv_v2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvV2Params p) {
@@ -329,6 +335,11 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             for (int g = g0; g < g1; ++g) {
                 const int s = a_it % p.a_stages;
                 if (a_it >= p.a_stages) mbar_wait(&a_empty[s], ((a_it / p.a_stages) - 1) & 1);
+                // 3xTF32 (a_seg > 0): the weights' K segments [w_hi | w_lo | w_hi]
+                // pair with the input's [x_hi | x_hi | x_lo]; the input buffer holds
+                // [x_hi | x_lo], so channels past the first segment read a_seg lower
+                int a_c = g * p.cg;
+                if (p.a_seg > 0 && a_c >= p.a_seg) a_c -= p.a_seg;
                 if (elect_one()) {
                     uint8_t *dst = sA + s * p.a_stage_bytes;
                     if ((p.dbg & 1) && a_it >= p.a_stages) {
@@ -338,26 +349,26 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         if (p.a_swz) {
                             expect_lead(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
                             for (int par = 0; par < p.s_in; ++par)
-                                tma_load_4d_cg2(dst + par * p.plane_bytes, &amap, lb, g * p.cg, w0 + par, h0, c.n);
+                                tma_load_4d_cg2(dst + par * p.plane_bytes, &amap, lb, a_c, w0 + par, h0, c.n);
                         } else {
                             expect_lead(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
                             for (int k8 = 0; k8 < p.cg / 8; ++k8)
                                 for (int par = 0; par < p.s_in; ++par)
                                     tma_load_4d_cg2(dst + (k8 * p.s_in + par) * p.plane_bytes, &amap, lb,
-                                                    g * p.cg + k8 * 8, w0 + par, h0, c.n);
+                                                    a_c + k8 * 8, w0 + par, h0, c.n);
                         }
                     } else if (p.a_swz) {
                         // one box per column parity: PH rows x PWs cols x cg channels
                         mbar_arrive_expect_tx(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
                         for (int par = 0; par < p.s_in; ++par)
-                            tma_load_4d(dst + par * p.plane_bytes, &amap, &a_full[s], g * p.cg,
+                            tma_load_4d(dst + par * p.plane_bytes, &amap, &a_full[s], a_c,
                                         w0 + par, h0, c.n);
                     } else {
                         mbar_arrive_expect_tx(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
                         for (int k8 = 0; k8 < p.cg / 8; ++k8)
                             for (int par = 0; par < p.s_in; ++par)
                                 tma_load_4d(dst + (k8 * p.s_in + par) * p.plane_bytes, &amap,
-                                            &a_full[s], g * p.cg + k8 * 8, w0 + par, h0, c.n);
+                                            &a_full[s], a_c + k8 * 8, w0 + par, h0, c.n);
                     }
                 }
                 __syncwarp();
@@ -401,7 +412,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         // Descriptor arithmetic: the start-address field is bits [0,14) in 16-byte
         // units and never carries (smem < 256 KB), so an operand at byte offset
         // `off` from a base descriptor is base + (off >> 4).
-        const uint32_t idesc = idesc_bf16(PAIR ? 256 : 128, p.bn, 0, 0);
+        const uint32_t idesc = KIND == 1 ? idesc_tf32(128, p.bn, 0, 0) : idesc_bf16(PAIR ? 256 : 128, p.bn, 0, 0);
         const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
         const uint64_t a_desc0 = p.a_swz ? smem_desc(sA_u, 16, p.a_sbo, swizzle_layout(p.a_swz))
                                                 : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
@@ -434,7 +445,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 if (p.b_resident) {
                     if (elect_one()) {
                         uint64_t bd = b_desc0 + (uint32_t)((g - g0) * p.T) * b_slot16;
-                        if (!do_mma || !issue_taps_fixed<CG>(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
+                        if (!do_mma || !issue_taps_fixed<CG, KIND>(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
                                                              idesc, g == g0, acc_cols, a_tile16)) {
                         uint64_t arow = a_stage;
                         for (int th = 0; th < p.kh; ++th) {
@@ -444,7 +455,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                                 for (int k16 = 0; k16 < nk16; ++k16)
                                     for (int tt = 0; tt < p.tpw; ++tt)
                                         if (do_mma)
-                                            mma_cg<CG>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
+                                            mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
                                                        bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
                                 bd += b_slot16;
                             }
@@ -469,7 +480,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const bool first = g == g0 && t == 0;
                         if (elect_one()) {
                             if (do_mma)
-                                issue_slot_any<CG>(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
+                                issue_slot_any<CG, KIND>(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
                                                    first);
                             if (PAIR)
                                 commit(&b_empty[sb]);
@@ -675,10 +686,24 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 if (ks > 1) {
                     if (valid && c.o0 + c16 * 16 < p.nout_p) {
                         float4 *dst = reinterpret_cast<float4 *>(wrow + c16 * 16);
+                        // (fp32 outputs pad channels to 8: a chunk may hold one valid half)
+                        const int nq = c.o0 + c16 * 16 + 8 < p.nout_p ? 4 : 2;
 #pragma unroll
                         for (int q = 0; q < 4; ++q)
+                            if (q < nq)
                             dst[q] = make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]),
                                                  __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
+                    }
+                } else if (p.out_f32) {
+                    // fp32 output (3xTF32 path): 16 columns = two 32-byte halves,
+                    // the second only when the (8-padded) channel count reaches it
+                    float *of = reinterpret_cast<float *>(p.out) + (long long)c.n * p.out_sn +
+                                (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+                                (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0 + c16 * 16;
+                    if (valid && !(p.dbg & 2)) {
+                        if (c.o0 + c16 * 16 < p.nout_p) st_global_v8(of, *reinterpret_cast<const uint32_t(*)[8]>(&v[0]));
+                        if (c.o0 + c16 * 16 + 8 < p.nout_p)
+                            st_global_v8(of + 8, *reinterpret_cast<const uint32_t(*)[8]>(&v[8]));
                     }
                 } else {
                     const bool st_ok = valid && c.o0 + c16 * 16 < p.nout_p;
@@ -857,7 +882,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     // cold inputs (92 -> 128 us: the leader waits for the slower of two tile
     // loads) and for 256-wide, resident or stride-2 tiles
     static const bool cg2 = std::getenv("DC_V2_CG2") != nullptr;
-    const bool cand2 = cg2 && p.bn == 128 && p.s_in == 1;
+    const bool cand2 = cg2 && p.bn == 128 && p.s_in == 1 && p.kind == 0;
     p.cta2 = 0;
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
     const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16 + (p.bn_stats ? 4 * 2 * p.bn * 8 : 0);
@@ -912,7 +937,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     // streamed weights: CTA pairs multicast each weight stage (half each), which
     // halves the L2 -> SM weight traffic without reducing the number of CTAs
     static const bool no_cluster = std::getenv("DC_V2_NO_CLUSTER") != nullptr;
-    p.cluster = p.cta2 ? 2 : (!p.b_resident && p.bn % 32 == 0 && !no_cluster) ? 2 : 1;
+    p.cluster = p.cta2 ? 2 : (!p.b_resident && p.bn % 32 == 0 && !no_cluster && p.kind == 0) ? 2 : 1;
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
 }
 
@@ -943,6 +968,13 @@ __global__ void conv_v2_reduce_kernel(const __grid_constant__ ConvV2Params p) {
             const float4 c = q[0], d = q[1];
             a.x += c.x, a.y += c.y, a.z += c.z, a.w += c.w;
             b.x += d.x, b.y += d.y, b.z += d.z, b.w += d.w;
+        }
+        if (p.out_f32) {
+            float4 *of = reinterpret_cast<float4 *>(reinterpret_cast<float *>(p.out) + (long long)n * p.out_sn +
+                                                    (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+                                                    (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + v * 8);
+            of[0] = a, of[1] = b;
+            continue;
         }
         uint4 o;
         o.x = pack2(__float_as_uint(a.x), __float_as_uint(a.y));
@@ -997,14 +1029,16 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     }
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(conv_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
-        cudaFuncSetAttribute(conv_v2_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
     if (p.cluster > 1 && !(p.dbg & 8)) {
         // persistent CTA pairs: as many as can be co-resident (GPCs need not hold
         // an even number of free SMs), a multiple of the split-K factor
         const size_t smem = conv_v2_smem_bytes(p);
-        auto kern = p.cta2 ? conv_v2_kernel<2> : conv_v2_kernel<1>;
+        DC_REQUIRE(p.kind == 0, DC_ERR_ARG, "conv_v2: tf32 runs without CTA pairs");
+        auto kern = p.cta2 ? conv_v2_kernel<2, 0> : conv_v2_kernel<1, 0>;
         const size_t key = smem * 2 + (size_t)p.cta2;
         static std::map<size_t, int> max_clusters;
         if (!max_clusters.count(key)) {
@@ -1044,7 +1078,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         ConvV2Params q = p;
         cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
         cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));
-        conv_v2_kernel<1><<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
+        conv_v2_kernel<1, 0><<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
         cudaStreamSynchronize(st);
         long long h[64 * 8];
         cudaMemcpy(h, q.dbg_out, sizeof h, cudaMemcpyDeviceToHost);
@@ -1056,14 +1090,27 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
                     h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
                     h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
     } else {
-        launch_k(conv_v2_kernel<1>, dim3(grid), dim3(kV2Threads), conv_v2_smem_bytes(p), st, 1, "conv_v2", amap,
-                 bmap, p);
+        launch_k(p.kind == 1 ? conv_v2_kernel<1, 1> : conv_v2_kernel<1, 0>, dim3(grid), dim3(kV2Threads),
+                 conv_v2_smem_bytes(p), st, 1, p.kind == 1 ? "conv_v2 (tf32)" : "conv_v2", amap, bmap, p);
         return grid;
     }
     cudaError_t e = cudaGetLastError();
     DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));
     ++g_launches;
     return grid;
+}
+
+
+// Loads this file's kernels now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which waits for the device: with the spinning
+// halo / BN protocol kernels of a loopback group in flight, that wait never
+// ends).
+void preload_conv_v2() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<1, 0>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<2, 0>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<1, 1>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_reduce_kernel));
 }
 
 }  // namespace dc

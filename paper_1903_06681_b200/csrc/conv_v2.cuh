@@ -105,6 +105,12 @@ struct ConvV2Params {
     // kept only inside [0, out_hmax) x [0, out_wmax)
     int subpix, sub_cp, out_hmax, out_wmax;
     int nout_p;
+    // 3xTF32 (DC_FP32_3XTF32): kind = 1 runs kind::tf32 MMAs on
+    // fp32 data seen as pairs of 16-bit "channels" (a 32-byte K step is 8 fp32
+    // = 16 bf16, so every smem / TMA / descriptor geometry is unchanged);
+    // a_seg > 0 maps weight K channels >= a_seg (in 16-bit units) a_seg lower
+    // in the input (x_hi x_hi x_lo against w_hi w_lo w_hi); out_f32 stores fp32.
+    int kind, a_seg, out_f32;
 };
 
 size_t conv_v2_smem_bytes(const ConvV2Params &p);

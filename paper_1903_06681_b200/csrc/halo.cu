@@ -317,4 +317,20 @@ void launch_bn_allreduce_p2p(const BnP2P &b, cudaStream_t st) {
     launch_k(bn_allreduce_p2p_kernel, dim3(1), dim3(256), 0, st, 1, "bn p2p", b);
 }
 
+
+// Loads this file's kernels now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which waits for the device: with the spinning
+// halo / BN protocol kernels of a loopback group in flight, that wait never
+// ends).
+void preload_halo() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(block_copy_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(signal_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_sums_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_reduce_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_finalize_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(p2p_exchange_kernel));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_allreduce_p2p_kernel));
+}
+
 }  // namespace dc

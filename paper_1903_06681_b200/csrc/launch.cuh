@@ -34,10 +34,19 @@ __device__ __forceinline__ void spin_until_geq(const uint32_t *p, uint32_t targe
     }
 }
 
+// Set while a loopback-group plan (capi.cu) launches: its virtual ranks share
+// one GPU's SMs, and a kernel launched early that waits on the previous one
+// could hold the SMs another virtual rank's halo kernel needs (deadlock).
+extern thread_local bool g_no_pdl;
 inline bool pdl_enabled() {
     static const bool on = std::getenv("DC_NO_PDL") == nullptr;
-    return on;
+    return on && !g_no_pdl;
 }
+struct NoPdlScope {
+    bool prev;
+    explicit NoPdlScope(bool on) : prev(g_no_pdl) { g_no_pdl = g_no_pdl || on; }
+    ~NoPdlScope() { g_no_pdl = prev; }
+};
 
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,

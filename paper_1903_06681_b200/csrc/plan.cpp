@@ -14,7 +14,7 @@ Range blocked(int64_t extent, int parts, int idx) {
     return r;
 }
 
-ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int S, int P) {
+ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int S, int P, int dt) {
     DC_REQUIRE(N > 0 && C > 0 && H > 0 && W > 0 && F > 0, DC_ERR_SHAPE,
                "non-positive extent (N=%lld C=%lld H=%lld W=%lld F=%lld)", (long long)N,
                (long long)C, (long long)H, (long long)W, (long long)F);
@@ -22,12 +22,13 @@ ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
     DC_REQUIRE(P >= 0 && P <= K / 2, DC_ERR_SHAPE, "need 0 <= P <= K/2 (P=%d, K=%d)", P, K);
     DC_REQUIRE(S >= 1, DC_ERR_SHAPE, "stride must be >= 1");
     DC_REQUIRE(S <= 2, DC_ERR_UNSUPPORTED, "stride %d not supported (1 or 2)", S);
-    ConvGeom g{N, C, H, W, F, K, S, P, 0, 0, 0, 0};
+    ConvGeom g{N, C, H, W, F, K, S, P, 0, 0, 0, 0, dt};
     DC_REQUIRE(H + 2 * P >= K && W + 2 * P >= K, DC_ERR_SHAPE, "input smaller than the kernel");
     g.Ho = (H + 2 * P - K) / S + 1;
     g.Wo = (W + 2 * P - K) / S + 1;
-    g.Cp = round_up(C, 16);
-    g.Fp = round_up(F, 16);
+    // 32-byte channel granules: 16 bf16 or 8 fp32 (one MMA K step either way)
+    g.Cp = round_up(C, dt ? 8 : 16);
+    g.Fp = round_up(F, dt ? 8 : 16);
     return g;
 }
 

@@ -43,11 +43,13 @@ struct ConvGeom {
     int64_t N, C, H, W, F;
     int K, S, P;
     int64_t Ho, Wo;
-    int64_t Cp, Fp;  // padded channel counts (innermost dim of the NHWC buffers)
+    int64_t Cp, Fp;  // padded channel counts: multiples of 16 (bf16) / 8 (fp32, 3xTF32)
+    int dt = 0;      // 0: bf16 (DC_BF16), 1: fp32 via 3xTF32 (DC_FP32_3XTF32)
+    int esz() const { return dt ? 4 : 2; }
 };
 
 // Validates and fills Ho/Wo/Cp/Fp. Throws DC_ERR_SHAPE / DC_ERR_UNSUPPORTED.
-ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int S, int P);
+ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int S, int P, int dt = 0);
 
 // Computes the split of one dimension; throws DC_ERR_PARTITION if the
 // partition is invalid for this rank (no output rows, or a halo wider than

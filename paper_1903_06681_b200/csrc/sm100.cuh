@@ -169,6 +169,18 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32: fp32 operands, of which the
+// tensor core reads the top 19 bits (sign, 8-bit exponent, 10-bit mantissa --
+// truncation, measured: tools/tf32_probe.cu), fp32 accumulate. K = 8 per
+// instruction (32 bytes, the same smem geometry as K = 16 bf16).
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
 // M = 256 over a CTA pair (issued by the leader): A rows 0-127 from CTA 0's smem,
 // 128-255 from CTA 1's (same offset), B columns split N/2 + N/2 likewise; each
 // CTA's TMEM receives its 128 rows.
@@ -242,6 +254,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, uint32
     return (1u << 4) | (1u << 7) | (1u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) |
            ((M >> 4) << 24);
 }
+
+// Instruction descriptor, kind::tf32: a/b format 2 (TF32), fp32 accumulate.
+// MN-major tf32 operands need descriptor layout kLayoutSw128Base32B.
+__host__ __device__ constexpr uint32_t idesc_tf32(uint32_t M, uint32_t N, uint32_t a_mn, uint32_t b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn << 15) | (b_mn << 16) | ((N >> 3) << 17) |
+           ((M >> 4) << 24);
+}
+// Descriptor layout 1: 128-byte rows swizzled in 32-byte granules (cute
+// Swizzle<2,5,2>: byte address bits [5,7) ^= bits [7,9); atom = 4 rows x 128 B),
+// the layout of MN-major 32-bit operands (measured, tools/tf32_probe.cu).
+constexpr uint32_t kLayoutSw128Base32B = 1;
 
 __host__ __device__ constexpr uint32_t swizzle_layout(int bytes) {
     return bytes == 128 ? 2u : bytes == 64 ? 4u : bytes == 32 ? 6u : 0u;

@@ -47,11 +47,11 @@ __host__ __device__ inline Atom atom_of(const WgradV2Params &p, int mt, int a, i
     const int A = 128 / p.cgw;
     auto offset = [&](int cg, int th, int tw) -> uint32_t {
         return (uint32_t)(((cg - cg_lo) * p.s_in + (tw % p.s_in)) * p.x_plane_bytes +
-                          (th * p.pitch + tw / p.s_in) * p.cgw * 2);
+                          (th * p.pitch + tw / p.s_in) * p.cgw * p.esz);
     };
-    if (p.mode == 2) {  // 1x1: channel groups 2mt, 2mt+1
-        const int cg = 2 * mt + a;
-        r.cg = cg < p.ncg ? cg : 2 * mt;
+    if (p.mode == 2) {  // 1x1: channel groups A mt .. A mt + A - 1
+        const int cg = A * mt + a;
+        r.cg = cg < p.ncg ? cg : A * mt;
         r.tap = cg < p.ncg ? 0 : -1;
         r.off = offset(r.cg, 0, 0);
     } else if (p.mode == 0) {  // pairs of taps inside one channel group
@@ -80,32 +80,40 @@ constexpr int kWMaxStages = 8;
 
 // The MMAs of one pixel block: G M tiles x 4 K16 steps, fully unrolled (the
 // descriptors are loop-invariant per CTA; only the stage offset moves).
-template <int G, int NKS>
+// (KIND 1: K = 8 pixel steps of kind::tf32, B rows 1024 bytes per step)
+template <int KIND, int G, int NKS>
 __device__ __forceinline__ void wgrad_issue(uint32_t tmem, const uint64_t (&adesc)[8], uint32_t xo, uint64_t bd,
                                             uint32_t ak16, uint32_t acc_cols, uint32_t idesc, bool first) {
+    constexpr uint32_t bk16 = (KIND == 1 ? 1024 : 2048) >> 4;
 #pragma unroll
     for (int i = 0; i < G; ++i)
 #pragma unroll
-        for (int k = 0; k < NKS; ++k)  // NKS x K16 steps of 16 pixels each
-            mma_bf16(tmem + i * acc_cols, adesc[i] + xo + k * ak16, bd + k * (2048 >> 4), idesc,
-                     (first && k == 0) ? 0u : 1u);
+        for (int k = 0; k < NKS; ++k) {  // NKS x K steps of 16 (bf16) / 8 (tf32) pixels
+            if constexpr (KIND == 1)
+                mma_tf32(tmem + i * acc_cols, adesc[i] + xo + k * ak16, bd + k * bk16, idesc,
+                         (first && k == 0) ? 0u : 1u);
+            else
+                mma_bf16(tmem + i * acc_cols, adesc[i] + xo + k * ak16, bd + k * bk16, idesc,
+                         (first && k == 0) ? 0u : 1u);
+        }
 }
-template <int NKS>
+template <int KIND, int NKS>
 __device__ __forceinline__ void wgrad_issue_g(int G, uint32_t tmem, const uint64_t (&adesc)[8], uint32_t xo,
                                               uint64_t bd, uint32_t ak16, uint32_t acc_cols, uint32_t idesc,
                                               bool first) {
     switch (G) {
-    case 1: wgrad_issue<1, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 2: wgrad_issue<2, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 3: wgrad_issue<3, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 4: wgrad_issue<4, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 5: wgrad_issue<5, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 6: wgrad_issue<6, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    case 7: wgrad_issue<7, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
-    default: wgrad_issue<8, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 1: wgrad_issue<KIND, 1, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 2: wgrad_issue<KIND, 2, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 3: wgrad_issue<KIND, 3, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 4: wgrad_issue<KIND, 4, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 5: wgrad_issue<KIND, 5, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 6: wgrad_issue<KIND, 6, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    case 7: wgrad_issue<KIND, 7, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
+    default: wgrad_issue<KIND, 8, NKS>(tmem, adesc, xo, bd, ak16, acc_cols, idesc, first); break;
     }
 }
 
+template <int KIND>
 __global__ void __launch_bounds__(192, 1)
     wgrad_v2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap dymap,
                     const __grid_constant__ WgradV2Params p) {
@@ -134,7 +142,7 @@ __global__ void __launch_bounds__(192, 1)
         G = min(p.G, per_cg - gi * p.G);
     }
     const int cg_lo = atom_of(p, mt0, 0, 0).cg;
-    const int cg_hi = p.mode == 2 ? min(p.ncg, 2 * (mt0 + G)) - 1 : cg_lo;
+    const int cg_hi = p.mode == 2 ? min(p.ncg, A * (mt0 + G)) - 1 : cg_lo;
     const int ncg = cg_hi - cg_lo + 1;
     const int b_begin = (int)((long long)split * p.nblocks / p.splits);
     const int b_end = (int)((long long)(split + 1) * p.nblocks / p.splits);
@@ -163,12 +171,16 @@ __global__ void __launch_bounds__(192, 1)
             tma_prefetch(&dymap);
         }
         const int per_n = p.tiles_h * p.tiles_w;
-        const uint32_t x_bytes = ncg * p.s_in * p.PH * p.pitch * p.cgw * 2;  // bytes the boxes deliver
-        const uint32_t d_bytes = (p.bn / 64) * 8 * p.bw * 128;
+        const uint32_t x_bytes = ncg * p.s_in * p.PH * p.pitch * p.cgw * p.esz;  // bytes the boxes deliver
+        const int fbox = 128 / p.esz;  // filters per dy box (one 128-byte row)
+        const uint32_t d_bytes = (p.bn / fbox) * 8 * p.bw * 128;
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % p.stages;
             if (kb >= p.stages) mbar_wait(&empty[s], ((kb / p.stages) - 1) & 1);
-            const int blk = b_begin + kb;
+            // 3xTF32: pass 0 x_hi dy_hi, 1 x_hi dy_lo, 2 x_lo dy_hi (one accumulation)
+            const int pass = (b_begin + kb) / p.nblocks_pix;
+            const int blk = b_begin + kb - pass * p.nblocks_pix;
+            const int xc = pass == 2 ? p.x_lo : 0, fc = pass == 1 ? p.dy_lo : 0;
             const int n = blk / per_n, rem = blk - n * per_n;
             const int i0 = (rem / p.tiles_w) * 8, j0 = (rem % p.tiles_w) * p.bw;
             if (elect_one()) {
@@ -178,10 +190,10 @@ __global__ void __launch_bounds__(192, 1)
                 for (int c = 0; c < ncg; ++c)
                     for (int par = 0; par < p.s_in; ++par)
                         tma_load_4d(xs + (c * p.s_in + par) * p.x_plane_bytes, &xmap, &full[s],
-                                    (cg_lo + c) * p.cgw, w0 + par, h0, n);
+                                    (cg_lo + c) * p.cgw + xc, w0 + par, h0, n);
                 uint8_t *ds = sD + s * p.dy_stage_bytes;
-                for (int q = 0; q < p.bn / 64; ++q)
-                    tma_load_4d(ds + q * 8 * p.bw * 128, &dymap, &full[s], f0 + q * 64, j0, i0, n);
+                for (int q = 0; q < p.bn / fbox; ++q)
+                    tma_load_4d(ds + q * 8 * p.bw * 128, &dymap, &full[s], f0 + q * fbox + fc, j0, i0, n);
             }
             __syncwarp();
         }
@@ -191,9 +203,11 @@ __global__ void __launch_bounds__(192, 1)
         // output row (cgw*2 bytes each); SBO = next output row; LBO = next atom.
         // K rows = pixels: 8-pixel groups (SBO) are the next 8 output pixels of a
         // row (bw = 16) or the next output row (bw = 8); a K16 step is 16 pixels
-        const uint32_t row_bytes = p.s_in * p.pitch * p.cgw * 2;
-        const uint32_t a_sbo = p.bw == 16 ? 8 * p.cgw * 2 : row_bytes;
-        const uint32_t layout = swizzle_layout(p.cgw * 2);
+        // tf32 (bw = 8): a K = 8 step is one output row, two groups of 4 pixels
+        // (SBO = 4 rows of 128 B), 32-byte-granule swizzle (layout 1)
+        const uint32_t row_bytes = p.s_in * p.pitch * p.cgw * p.esz;
+        const uint32_t a_sbo = KIND == 1 ? 4 * 128 : p.bw == 16 ? 8 * p.cgw * 2 : row_bytes;
+        const uint32_t layout = KIND == 1 ? kLayoutSw128Base32B : swizzle_layout(p.cgw * 2);
         uint64_t adesc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -213,10 +227,12 @@ __global__ void __launch_bounds__(192, 1)
         }
         // B (dy, MN-major SW128): atom = 64 filters; K rows = 8 pixels x 128 B;
         // SBO = 1024 (next 8 pixels = next output row), LBO = next 64 filters.
-        const uint64_t bdesc0 = smem_desc(smem_u32(sD), 8 * p.bw * 128, 1024, 2);
-        const uint32_t idesc = idesc_bf16(128, p.bn, 1, 1);
+        // (tf32: atom = 32 filters, 4-pixel groups: SBO = 512, layout 1)
+        const uint64_t bdesc0 = KIND == 1 ? smem_desc(smem_u32(sD), 8 * p.bw * 128, 512, kLayoutSw128Base32B)
+                                          : smem_desc(smem_u32(sD), 8 * p.bw * 128, 1024, 2);
+        const uint32_t idesc = KIND == 1 ? idesc_tf32(128, p.bn, 1, 1) : idesc_bf16(128, p.bn, 1, 1);
         const uint32_t acc_cols = p.bn_cols;
-        const uint32_t ak16 = (p.bw == 16 ? row_bytes : 2 * row_bytes) >> 4;
+        const uint32_t ak16 = (KIND == 1 || p.bw == 16 ? row_bytes : 2 * row_bytes) >> 4;
         const uint32_t xstep = (uint32_t)p.x_stage_bytes >> 4, dstep = (uint32_t)p.dy_stage_bytes >> 4;
         int s = 0;
         uint32_t ph = 0, xo = 0;
@@ -225,10 +241,10 @@ __global__ void __launch_bounds__(192, 1)
             mbar_wait(&full[s], ph);
             tc_fence_after();
             if (elect_one()) {
-                if (p.bw == 16)
-                    wgrad_issue_g<8>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
+                if (KIND == 1 || p.bw == 16)  // 8 steps: 8 x 16 (bf16) or 8 x 8 (tf32, bw 8) pixels
+                    wgrad_issue_g<KIND, 8>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
                 else
-                    wgrad_issue_g<4>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
+                    wgrad_issue_g<KIND, 4>(G, tmem, adesc, xo, bd, ak16, acc_cols, idesc, kb == 0);
                 mma_commit(&empty[s]);
             }
             __syncwarp();
@@ -302,12 +318,26 @@ int wgrad_v2_mgroups(const WgradV2Params &p) {
 }
 
 static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
-    if (p.Fp % 64 != 0 || p.kh * p.kw != p.T) return false;
-    p.cgw = p.cp % 64 == 0 ? 64 : p.cp % 32 == 0 ? 32 : 16;
-    p.ncg = p.cp / p.cgw;
+    const bool tf32 = p.kind == 1;
+    if ((!tf32 && p.Fp % 64 != 0) || p.kh * p.kw != p.T) return false;
+    p.esz = tf32 ? 4 : 2;
+    if (tf32) {
+        // MN-major tf32 atoms are 128-byte rows: 32 channels (the last group
+        // may reach into the lo half / past the buffer: those rows are
+        // discarded, or TMA zero-fills them)
+        p.cgw = 32;
+        p.ncg = (p.cp + 31) / 32;
+        bw = 8;
+    } else {
+        p.cgw = p.cp % 64 == 0 ? 64 : p.cp % 32 == 0 ? 32 : 16;
+        p.ncg = p.cp / p.cgw;
+    }
     if (8 + (p.kw - 1) / p.s_in > 32) return false;
     const int A = 128 / p.cgw;
-    if (p.T == 1 && p.cgw == 64) {
+    if (tf32) {
+        p.mode = p.T == 1 ? 2 : 1;
+        p.n_mtiles = p.T == 1 ? (p.ncg + A - 1) / A : p.ncg * p.kw * ((p.kh + A - 1) / A);
+    } else if (p.T == 1 && p.cgw == 64) {
         p.mode = 2;
         p.n_mtiles = (p.ncg + 1) / 2;
     } else if (p.cgw == 64) {
@@ -328,7 +358,7 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
     // round trips per pixel and fewer halo columns than 8 x 8)
     p.bw = bw;
     p.pitch = p.bw + (p.kw - 1) / p.s_in;
-    p.x_plane_bytes = (p.PH * p.pitch * p.cgw * 2 + 1023) / 1024 * 1024;
+    p.x_plane_bytes = (p.PH * p.pitch * p.cgw * p.esz + 1023) / 1024 * 1024;
     // N tile 256 (2 M tiles per x / dy stage in TMEM) once the launch has
     // >= 8192 output pixels, else 128 (4 M tiles per stage, half the bytes per
     // MMA). Measured, cold L2 (profiles/r1_wgrad_bn_sweep.txt): 256 wins
@@ -337,7 +367,8 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
     // 32^2 N = 1: 31 -> 36 us). DC_WGRAD_BN overrides.
     static const int bn_env = std::getenv("DC_WGRAD_BN") ? std::atoi(std::getenv("DC_WGRAD_BN")) : 0;
     const int bn_cap = bn_env > 0 ? bn_env : p.pixels_hint >= 8192 ? 256 : 128;
-    p.bn = p.Fp <= bn_cap ? p.Fp : bn_cap;
+    // (tf32: N tiles of whole 32-filter dy boxes; filters past F are discarded)
+    p.bn = tf32 ? std::min<int>(bn_cap, (p.Fp + 31) / 32 * 32) : p.Fp <= bn_cap ? p.Fp : bn_cap;
     p.bn_cols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
     p.G = std::max(1, std::min(8, 512 / p.bn_cols));
     if (p.mode != 2) {  // equal groups per channel group (e.g. 5 M tiles: 3 + 2, not 4 + 1):
@@ -345,10 +376,10 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
         const int per_cg = p.n_mtiles / p.ncg;
         p.G = (per_cg + (per_cg + p.G - 1) / p.G - 1) / ((per_cg + p.G - 1) / p.G);
     }
-    p.dy_stage_bytes = (p.bn / 64) * 8 * p.bw * 128;
+    p.dy_stage_bytes = (p.bn / (128 / p.esz)) * 8 * p.bw * 128;
     const int fixed = 1024 + (2 * kWMaxStages + 1) * 8 + 16;
     for (;;) {
-        const int ncg_stage = p.mode == 2 ? std::min(p.ncg, 2 * p.G) : 1;
+        const int ncg_stage = p.mode == 2 ? std::min(p.ncg, A * p.G) : 1;
         p.x_stage_bytes = (ncg_stage * p.s_in * p.x_plane_bytes + 1023) / 1024 * 1024;
         p.stages = std::min(kWMaxStages, (smem_limit - fixed) / (p.x_stage_bytes + p.dy_stage_bytes));
         if (p.stages >= 2 || p.G == 1) break;
@@ -359,7 +390,7 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
 
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
     // 8 x 16 pixel blocks unless two stages of them do not fit (stride 2 with
-    // 256-filter tiles), then 8 x 8
+    // 256-filter tiles), then 8 x 8 (tf32: always 8 x 8)
     static const bool bw8 = std::getenv("DC_WGRAD_BW8") != nullptr;
     const WgradV2Params in = p;
     if (!bw8 && wgrad_v2_configure_bw(p, smem_limit, 16)) return true;
@@ -371,11 +402,23 @@ void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const Wg
                      cudaStream_t st) {
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(wgrad_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(wgrad_v2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(wgrad_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
     const int ntiles = (p.Fp + p.bn - 1) / p.bn;
-    launch_k(wgrad_v2_kernel, dim3(wgrad_v2_mgroups(p), ntiles, p.splits), dim3(192), wgrad_v2_smem_bytes(p), st, 1,
-             "wgrad_v2", xmap, dymap, p);
+    launch_k(p.kind == 1 ? wgrad_v2_kernel<1> : wgrad_v2_kernel<0>, dim3(wgrad_v2_mgroups(p), ntiles, p.splits),
+             dim3(192), wgrad_v2_smem_bytes(p), st, 1, p.kind == 1 ? "wgrad_v2 (tf32)" : "wgrad_v2", xmap, dymap, p);
+}
+
+
+// Loads this file's kernels now (CUDA lazy loading would otherwise load a
+// kernel at its first launch, which waits for the device: with the spinning
+// halo / BN protocol kernels of a loopback group in flight, that wait never
+// ends).
+void preload_wgrad_v2() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(wgrad_v2_kernel<0>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(wgrad_v2_kernel<1>));
 }
 
 }  // namespace dc

@@ -24,6 +24,12 @@ struct WgradV2Params {
     long long ws_split;            // elements per split (a multiple of 4)
     int F, Fp, cp, C;              // filters, padded filters, padded / logical input channels
     long long pixels_hint;         // host: output pixels of this launch (N tile width choice)
+    // 3xTF32 (kind = 1): fp32 operands (esz = 4), 32-channel MN
+    // atoms (128-byte rows, descriptor layout SW128_BASE32B), 8 x 8 pixel blocks
+    // of eight K = 8 steps; the K range is `passes` copies of the pixel blocks,
+    // pass 0 = x_hi . dy_hi, 1 = x_hi . dy_lo (dy channels + dy_lo), 2 = x_lo .
+    // dy_hi (x channels + x_lo): the 3xTF32 product as one accumulation.
+    int kind, esz, passes, nblocks_pix, x_lo, dy_lo;
 };
 
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit);

@@ -49,11 +49,27 @@ def test_errors_are_status_codes_not_exceptions(dc):
         dc.dc_plan_create_virtual(1, 1, 8, 8, 1, 7, 1, 3, (1, 4, 1), 0)
     assert e.value.status == dc.DC_ERR_PARTITION
     with pytest.raises(dc.DCError) as e:
-        dc.dc_plan_create_virtual(1, 2, 16, 16, 4, 3, 1, 1, (1, 1, 1), 0, dtype=dc.DC_FP32_3XTF32)
-    assert e.value.status == dc.DC_ERR_UNSUPPORTED
+        dc.dc_plan_create_virtual(1, 2, 16, 16, 4, 3, 1, 1, (1, 1, 1), 0, dtype=7)     # unknown dtype
+    assert e.value.status == dc.DC_ERR_ARG
     # the thread-local message of the last failing call names the cause
-    assert "dtype" in str(e.value) or "implemented" in str(e.value), str(e.value)
+    assert "dtype" in str(e.value), str(e.value)
     assert dc.lib().dc_last_error().decode() in str(e.value)
+
+
+def test_fp32_plan_layouts(dc):
+    """DC_FP32_3XTF32 plans: channels padded to 8, margined x / dy hold
+    [hi | lo] fp32 halves, y / dx plain fp32, w fp32, dW unpadded."""
+    p = dc.dc_plan_create_virtual(2, 18, 20, 20, 12, 3, 1, 1, (1, 2, 1), 0, dtype=dc.DC_FP32_3XTF32)
+    try:
+        x, y = dc.dc_plan_query(p, dc.DC_X), dc.dc_plan_query(p, dc.DC_Y)
+        dy, w, dw = dc.dc_plan_query(p, dc.DC_DY), dc.dc_plan_query(p, dc.DC_W), dc.dc_plan_query(p, dc.DC_DW)
+        assert (x["c"], x["c_pad"], x["halo_s"]) == (18, 2 * 24, 1)
+        assert x["bytes"] == 2 * x["hb"] * x["wb"] * 48 * 4
+        assert (y["c_pad"], y["bytes"]) == (16, 2 * 10 * 20 * 16 * 4)
+        assert (dy["c_pad"], w["c_pad"], w["bytes"]) == (32, 24, 12 * 9 * 24 * 4)
+        assert (dw["c_pad"], dw["bytes"]) == (18, 12 * 9 * 18 * 4)
+    finally:
+        dc.dc_plan_destroy(p)
 
 
 def test_c1_shard_descriptors(dc):

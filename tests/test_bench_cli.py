@@ -22,3 +22,17 @@ def test_reference_arm_prints_one_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["config"]["workload"] == "mesh2k_n8"
+
+
+def test_resnet50_conv_stack_workload():
+    """The ResNet-50 conv-stack proxy (BASELINE.json configs[2]): 53
+    convolutions with Caffe's stride placement, 7.71 GFLOP per 224^2 image
+    forward (reading R21)."""
+    import bench
+    L = bench.resnet50_convs(1)
+    assert len(L) == 53
+    assert abs(sum(bench.layer_flops(l) for l in L) / 1e9 - 7.7118) < 1e-3
+    # the last stage runs at 7x7, the 3x3s have stride 1 and pad 1
+    assert all(l[3] == 7 for l in L if l[0].startswith("res5") and "branch2a" not in l[0] and "branch1" not in l[0])
+    assert all(l[6] == 3 and l[7] == 1 and l[8] == 1 for l in L if l[0].endswith("branch2b"))
+    assert bench.WORKLOADS["resnet50_n64"][0][1] == 64
