@@ -124,8 +124,16 @@ dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cud
  * IPC-mapped peer memory; the NCCL transports (DC_HALO_NCCL, the dW
  * allreduce, BN groups > 8) need real ranks and fail with
  * DC_ERR_UNSUPPORTED. Used to test the multi-rank device protocols on one
- * GPU. Destroy each with dc_comm_destroy. Errors: DC_ERR_ARG, DC_ERR_CUDA. */
+ * GPU. Each virtual rank owns two streams (dc_comm_stream: the one to issue
+ * its calls on; the other carries its exchanges), created so that no two
+ * ranks share a hardware queue: needs CUDA_DEVICE_MAX_CONNECTIONS >= 2 world
+ * in the environment before CUDA initializes (DC_ERR_ARG otherwise; default
+ * 8, i.e. up to 4 ranks). Destroy each with dc_comm_destroy.
+ * Errors: DC_ERR_ARG, DC_ERR_CUDA. */
 dc_status_t dc_comm_create_local(int world, int cuda_device, dc_comm_t *comms);
+/* The compute stream of a loopback rank (cudaStream_t): issue that rank's
+ * calls on it. Errors: DC_ERR_ARG (not a loopback communicator). */
+dc_status_t dc_comm_stream(dc_comm_t comm, void **stream);
 /* Write a fresh 128-byte ncclUniqueId to uid128 (rank 0 only). */
 dc_status_t dc_comm_unique_id(void *uid128);
 dc_status_t dc_comm_destroy(dc_comm_t comm);
@@ -177,10 +185,10 @@ dc_status_t dc_plan_decomp(dc_plan_t plan, dc_decomp_t *chosen, double *predicte
 /* Summation-order setting of the conv kernels: the split-K factor over
  * channel groups (the only choice that changes how an output is summed) is
  * picked for the global layer divided over `world` ranks. Default (world 0):
- * 8, whatever the plan's grid, so every partition of the same layer into up
- * to 8 ranks and its 1-GPU plan sum every y / dx element in the same order
- * (bit-identical outputs, north_star). Plans with equal settings agree bit
- * for bit; a different setting trades that for a split better fitted to one
+ * 1, i.e. from the undivided global layer whatever the plan's grid, so every
+ * partition of the layer and its 1-GPU plan sum every y / dx element in the
+ * same order (bit-identical outputs, north_star). Plans with equal settings
+ * agree bit for bit; another setting trades that for splits fitted to one
  * grid size. Host only; takes effect from the next compute call. */
 dc_status_t dc_plan_set_splitk_world(dc_plan_t plan, int world);
 dc_status_t dc_plan_destroy(dc_plan_t plan);

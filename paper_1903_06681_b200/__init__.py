@@ -28,7 +28,7 @@ DC_IMPORT_ASYNC, DC_SRC_BF16 = 0x1, 0x2
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "dc_comm_create", "dc_comm_create_local", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
+    "dc_comm_create", "dc_comm_create_local", "dc_comm_stream", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_tensor_import", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
@@ -83,6 +83,7 @@ def lib() -> ctypes.CDLL:
         "dc_comm_create": [i32, i32, vp, i32, P(vp)],
         "dc_comm_unique_id": [vp],
         "dc_comm_create_local": [i32, i32, P(vp)],
+        "dc_comm_stream": [vp, P(vp)],
         "dc_comm_destroy": [vp],
         "dc_plan_set_splitk_world": [vp, i32],
         "dc_comm_sync": [vp, vp],
@@ -161,6 +162,13 @@ def dc_comm_create_local(world: int, device: int = 0) -> list[int]:
     return [arr[i] for i in range(world)]
 
 
+def dc_comm_stream(comm: int) -> int:
+    """The compute stream (cudaStream_t) of a loopback rank."""
+    out = ctypes.c_void_p()
+    _check(lib().dc_comm_stream(comm, ctypes.byref(out)))
+    return out.value
+
+
 def dc_comm_destroy(comm: int):
     _check(lib().dc_comm_destroy(comm))
 
@@ -205,7 +213,7 @@ def dc_plan_decomp(plan: int) -> tuple[tuple[int, int, int], float]:
 
 
 def dc_plan_set_splitk_world(plan: int, world: int):
-    """Pick split-K as for the layer divided over `world` ranks (0: the library's basis, 8)."""
+    """Pick split-K as for the layer divided over `world` ranks (0: the library's basis, the global layer)."""
     _check(lib().dc_plan_set_splitk_world(plan, world))
 
 

@@ -36,6 +36,7 @@
 namespace dc {
 thread_local uint64_t g_launches = 0;
 thread_local bool g_no_pdl = false;
+thread_local bool g_dry_run = false;
 static thread_local std::string g_err;
 void set_last_error(const std::string &m) { g_err = m; }
 
@@ -100,6 +101,11 @@ struct dc_comm_s {
     bool grad_pending = false;  // allreduces queued since the last dc_comm_sync
     std::shared_ptr<LocalGroup> group;  // loopback group (no NCCL), or null
     int plan_seq = 0;                   // plans created on this communicator (loopback registry key)
+    // loopback: the virtual rank's two streams (its compute stream, handed to
+    // the caller by dc_comm_stream, and the side stream every plan of the rank
+    // uses for exchanges / boundary tiles), created back to back for all ranks
+    // so that no two of them share a hardware queue (see dc_comm_create_local)
+    cudaStream_t s_main = nullptr, s_side = nullptr;
 };
 
 namespace {
@@ -118,13 +124,16 @@ enum { FLAG_READY = 0, FLAG_DATA = 1 };
 
 }  // namespace
 
-// Split-K basis: the conv kernels' split-K factor over channel
-// groups -- the only choice that changes how an output element is summed -- is
-// picked for the GLOBAL layer divided over this many ranks, whatever the
-// plan's grid, so every partition of up to 8 ranks (one NVSwitch node) and
-// the 1-GPU plan of the same layer sum each y / dx element in the same order
-// (north_star: partitioned output bit-identical to 1 GPU).
-constexpr int kSplitKBasis = 8;
+// Split-K basis (reading R25): the conv kernels' split-K factor
+// over channel groups -- the only choice that changes how an output element
+// is summed -- is picked for the GLOBAL layer (undivided: basis 1), whatever
+// the plan's grid, so every partition and the 1-GPU plan of the same layer sum
+// each y / dx element in the same order (north_star: partitioned output
+// bit-identical to 1 GPU). (Measured: a basis of 8 -- splits sized for the
+// 8-way shards -- cost the 1-GPU mesh2k_n8 step 2.5 ms on its 64^2 / 32^2
+// 512-channel layers; an in-kernel split-order reduction chained the splits'
+// epilogues and was slower still.)
+constexpr int kSplitKBasis = 1;
 
 struct dc_plan_s {
     RankPlan rp;
@@ -134,6 +143,7 @@ struct dc_plan_s {
     bool bn_comm_owned = false;
     int bn_group = 1;
     cudaStream_t s_comm = nullptr;
+    bool s_comm_shared = false;  // (loopback: the virtual rank's side stream)
     cudaStream_t s_ph[4] = {nullptr, nullptr, nullptr, nullptr};  // stride-phase streams (bwd-data)
     cudaEvent_t ev_ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -214,7 +224,7 @@ struct dc_plan_s {
         if (bn_fpart) cudaFree(bn_fpart);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
-        if (s_comm) cudaStreamDestroy(s_comm);
+        if (s_comm && !s_comm_shared) cudaStreamDestroy(s_comm);
         for (auto sp : s_ph)
             if (sp) cudaStreamDestroy(sp);
         for (auto e : ev_ph)
@@ -1129,7 +1139,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     int nactive = 0;
     for (auto &f : ph) nactive += f.active ? 1 : 0;
     static const bool serial_phases = std::getenv("DC_SERIAL_PHASES") != nullptr;
-    if (!overlap && nactive > 1 && !serial_phases) {
+    if (!overlap && nactive > 1 && !serial_phases && pl->s_ph[0]) {
         // stride phases are independent GEMMs with disjoint outputs and split-K
         // workspaces: one stream each, so their ramp-up / tail / reduce overlap
         CK(cudaEventRecord(pl->ev_ph[0], st));
@@ -1340,11 +1350,11 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
 // the next exchange does not wait for a handshake. The exchange kernel also
 // signals ready for its own epoch, so this is an optimisation, never required.
 void signal_ready_next(dc_plan_s *pl, int which, const void *buf, cudaStream_t st) {
-    if (pl->is_virtual || pl->world() <= 1) return;
-    resolve_local_peers(pl);
-    if (pl->peer_flags.empty()) return;
+    if (pl->is_virtual || pl->world() <= 1 || g_dry_run) return;
     const BufState &B = pl->buf[which];
     if (B.ptr != buf) return;  // the P2P protocol applies to dc_buffer_alloc buffers only
+    resolve_local_peers(pl);
+    if (pl->peer_flags.empty()) return;
     const auto &recvs = which == 0 ? pl->rp.x_recv : pl->rp.dy_recv;
     if (recvs.empty()) return;
     std::vector<uint32_t *> fl;
@@ -1379,9 +1389,16 @@ void allreduce_dw_async(dc_plan_s *pl, float *dw, cudaStream_t st) {
 // plans, which may compute when no exchange / allreduce is requested).
 void ensure_local_resources(dc_plan_s *pl) {
     if (pl->s_comm) return;
-    CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
+    if (pl->comm && pl->comm->group) {
+        // loopback: the rank's side stream, no phase streams (phases run one
+        // after another): no extra hardware queues shared between ranks
+        pl->s_comm = pl->comm->s_side;
+        pl->s_comm_shared = true;
+    } else {
+        CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
+        for (auto &sp : pl->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
+    }
     for (auto &e : pl->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto &sp : pl->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
     for (auto &e : pl->ev_ph) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CK(cudaMalloc(&pl->bn_sums, sizeof(double) * 4 * pl->rp.g.Fp));  // local sums, global sums
 }
@@ -1391,6 +1408,31 @@ void join_import(dc_plan_s *pl, int which, cudaStream_t st) {
     if (!pl->import_pending[which]) return;
     CK(cudaStreamWaitEvent(st, pl->ev_copy_out[which], 0));
     pl->import_pending[which] = false;
+}
+
+// Size every workspace of a plan once at creation: a dry run of the host-side
+// configuration of each compute call (g_dry_run: nothing is launched), so no
+// compute call needs cudaMalloc later -- cudaMalloc can wait for the device,
+// which must not happen while this rank's (or, in a loopback group, another
+// virtual rank's) halo / BN kernels spin for a peer, nor in a timed step.
+void presize(dc_plan_s *pl) {
+    struct Scope {
+        Scope() { g_dry_run = true; }
+        ~Scope() { g_dry_run = false; }
+    } dry;
+    void *d = nullptr;  // any 16-byte aligned device address: TMA maps are encoded, never used
+    CK(cudaMalloc(&d, 4096));
+    cudaStream_t s = pl->s_comm;
+    const dc_status_t r1 = dc_conv_fwd(pl, d, d, d, DC_BN_STATS, s);
+    const dc_status_t r2 = dc_conv_bwd_data(pl, d, d, d, 0, s);
+    const dc_status_t r3 = dc_conv_bwd_filter(pl, d, d, reinterpret_cast<float *>(d), 0, s);
+    const dc_status_t r4 = dc_bn_spatial_stats(pl, d, reinterpret_cast<double *>(d), reinterpret_cast<double *>(d),
+                                              DC_BN_LOCAL, s);
+    CK(cudaFree(d));
+    pl->fwd_epoch = 0, pl->bn_fused_epoch = 0, pl->bn_fused_y = nullptr, pl->bn_fused_slots = 0;
+    DC_REQUIRE(r1 == DC_OK && r2 == DC_OK && r3 == DC_OK && r4 == DC_OK, DC_ERR_UNSUPPORTED,
+               "layer not supported by the kernels (%d %d %d %d): %s", (int)r1, (int)r2, (int)r3, (int)r4,
+               dc_last_error());
 }
 
 dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, bool is_virtual) {
@@ -1469,6 +1511,7 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
                 }
                 CK(cudaDeviceSynchronize());
             }
+            presize(pl);
         }
     } catch (...) {
         delete pl;
@@ -1528,14 +1571,35 @@ dc_status_t dc_comm_create_local(int world, int device, dc_comm_t *comms) {
     DC_REQUIRE(comms != nullptr && world >= 1 && world <= 64, DC_ERR_ARG, "bad loopback world %d", world);
     CK(cudaSetDevice(device));
     preload_kernels();
+    // Each virtual rank's kernels must be able to run while another rank's
+    // protocol kernel spins: no two ranks' streams may share one of the
+    // device's hardware queues (CUDA_DEVICE_MAX_CONNECTIONS, default 8; work of
+    // streams aliased onto one queue runs in order). 2 streams per rank,
+    // created back to back, map to distinct queues when 2 W <= connections.
+    const char *mc = std::getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    const int conns = mc ? std::atoi(mc) : 8;
+    DC_REQUIRE(2 * world <= conns, DC_ERR_ARG,
+               "a loopback group of %d ranks needs CUDA_DEVICE_MAX_CONNECTIONS >= %d (now %d), set before CUDA "
+               "initializes",
+               world, 2 * world, conns);
     auto G = std::make_shared<LocalGroup>();
     G->world = world;
     for (int r = 0; r < world; ++r) {
         auto *c = new dc_comm_s();
         c->rank = r, c->world = world, c->device = device;
         c->group = G;
+        CK(cudaStreamCreateWithFlags(&c->s_main, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking));
         comms[r] = c;
     }
+    DC_API_END
+}
+
+dc_status_t dc_comm_stream(dc_comm_t c, void **stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(c && stream, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(c->group != nullptr, DC_ERR_ARG, "dc_comm_stream: loopback communicators only");
+    *stream = c->s_main;
     DC_API_END
 }
 
@@ -1547,6 +1611,8 @@ dc_status_t dc_comm_destroy(dc_comm_t c) {
         if (c->grad_nccl) ncclCommDestroy(c->grad_nccl);
         if (c->nccl) ncclCommDestroy(c->nccl);
         if (c->s_grad) cudaStreamDestroy(c->s_grad);
+        if (c->s_main) cudaStreamDestroy(c->s_main);
+        if (c->s_side) cudaStreamDestroy(c->s_side);
         if (c->ev_in) cudaEventDestroy(c->ev_in);
         if (c->ev_out) cudaEventDestroy(c->ev_out);
         delete c;
@@ -1716,6 +1782,7 @@ dc_status_t dc_tensor_import(dc_plan_t pl, dc_tensor_t t, const void *src, void 
     CK(cudaPointerGetAttributes(&pa, src));
     const bool host = pa.type != cudaMemoryTypeDevice && pa.type != cudaMemoryTypeManaged;
     cudaStream_t st = (cudaStream_t)stream, cs = st;
+    if (is_local(pl)) flags &= ~DC_IMPORT_ASYNC;  // (loopback: no extra streams)
     if (flags & DC_IMPORT_ASYNC) {  // on the copy stream, after the caller's work so far
         if (!pl->s_copy) {
             CK(cudaStreamCreateWithFlags(&pl->s_copy, cudaStreamNonBlocking));

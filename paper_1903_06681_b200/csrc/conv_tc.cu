@@ -435,6 +435,7 @@ void launch_conv_gemm(const CUtensorMap &amap, const CUtensorMap &bmap, const Co
         cudaFuncSetAttribute(conv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
     });
+    if (g_dry_run) return;
     conv_gemm_kernel<<<dim3(tiles, nsamples, nout_tiles), 128, smem, st>>>(amap, bmap, p);
     CUDA_OK(cudaGetLastError());
     ++g_launches;
@@ -447,6 +448,7 @@ void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradP
     std::call_once(once, [] {
         cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
+    if (g_dry_run) return;
     wgrad_kernel<<<dim3(m_tiles, n_tiles, p.splits), 128, smem, st>>>(amap, bmap, p);
     CUDA_OK(cudaGetLastError());
     ++g_launches;

@@ -1073,6 +1073,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     }
     const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, device_sm_count()) : device_sm_count();
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, sms / p.ksplit));
+    if (g_dry_run) return grid;
     if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
         DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER=1 (and no DC_V2_CG2)");
         ConvV2Params q = p;

@@ -48,9 +48,14 @@ struct NoPdlScope {
     ~NoPdlScope() { g_no_pdl = prev; }
 };
 
+// Set while a plan sizes its workspaces at creation (capi.cu presize): the
+// host-side configuration runs and allocates, no kernel is launched.
+extern thread_local bool g_dry_run;
+
 template <typename... KArgs, typename... Args>
 void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
               const char *what, Args &&...args) {
+    if (g_dry_run) return;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[2];
     int na = 0;

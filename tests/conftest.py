@@ -1,6 +1,10 @@
 import os
 import sys
 
+# loopback groups (tests/test_loopback.py) give every virtual rank two streams
+# on distinct hardware queues: up to 16 ranks (set before CUDA initializes)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

@@ -64,3 +64,28 @@ def rel_l2(got: np.ndarray, ref: np.ndarray) -> float:
 def rel_max(got: np.ndarray, ref: np.ndarray) -> float:
     den = np.abs(ref).max()
     return float(np.abs(got - ref).max() / (den if den > 0 else 1.0))
+
+
+def elementwise_bound(ref: np.ndarray, S: np.ndarray, n_terms: int, k_step: int, out_bf16: bool,
+                      extra_adds: int = 32) -> np.ndarray:
+    """Per-element error bound of a tensor-core result against the exact value
+    (DESIGN.md §7): products of the (exactly representable) inputs are exact
+    in fp32; the fp32 accumulation adds one partial per K step of k_step
+    terms (16 bf16 / 8 tf32) plus at most `extra_adds` more (the reduction
+    inside an MMA, split-K partials), so |acc - exact| <= m 2^-24 S with
+    m = n_terms / k_step + extra_adds and S = sum of |terms| (the oracle run
+    on absolute values); a bf16 output adds its round-to-nearest error,
+    2^-8 |value| (8-bit significand)."""
+    m = n_terms / float(k_step) + extra_adds
+    acc = m * 2.0 ** -24 * S
+    if out_bf16:
+        return 2.0 ** -8 * (np.abs(ref) + acc) + acc + 1e-30
+    return acc + 1e-30
+
+
+def assert_elementwise(name: str, got: np.ndarray, ref: np.ndarray, bound: np.ndarray):
+    assert np.isfinite(got).all(), f"{name}: non-finite values"
+    err = np.abs(got - ref)
+    bad = err > bound
+    assert not bad.any(), (f"{name}: {int(bad.sum())} of {bad.size} elements over the derived bound "
+                           f"(worst {float((err / bound).max()):.2f}x, max err {float(err.max()):.3e})")

@@ -15,8 +15,8 @@ import torch
 
 import datagen
 import oracle
-from tests.gpu_util import (dw_to_fckk, empty_dense, fill_buffer, owned_nchw, rel_l2, rel_max,
-                            weights_gpu)
+from tests.gpu_util import (assert_elementwise, dw_to_fckk, elementwise_bound, empty_dense, fill_buffer,
+                            owned_nchw, rel_l2, rel_max, weights_gpu)
 
 pytestmark = pytest.mark.gpu
 
@@ -101,6 +101,15 @@ def test_single_gpu_parity(dc, shape):
     dx = owned_nchw(r["dx"], r["dxd"])
     dw = dw_to_fckk(r["dw"], C)
     assert np.isfinite(y).all() and np.isfinite(dx).all() and np.isfinite(dw).all()
+    # element by element within the derived bound ...
+    ax, aw, ady = np.abs(x), np.abs(w), np.abs(dy)
+    Ho, Wo = oracle.out_extent(H, K, S, P), oracle.out_extent(W, K, S, P)
+    assert_elementwise("y", y, y_ref, elementwise_bound(y_ref, oracle.conv_fwd(ax, aw, S, P), C * K * K, 16, True))
+    assert_elementwise("dx", dx, dx_ref, elementwise_bound(dx_ref, oracle.conv_bwd_data(ady, aw, H, W, S, P),
+                                                           F * K * K, 16, True))
+    assert_elementwise("dw", dw, dw_ref, elementwise_bound(dw_ref, oracle.conv_bwd_filter(ax, ady, K, S, P),
+                                                           N * Ho * Wo, 16, False, extra_adds=300))
+    # ... and at the norms north_star states
     e_y, e_dx, e_dw = rel_l2(y, y_ref), rel_l2(dx, dx_ref), rel_max(dw, dw_ref)
     assert e_y <= TOL_L2_SPEC and e_y <= TOL_L2_DERIVED, e_y
     assert e_dx <= TOL_L2_SPEC and e_dx <= TOL_L2_DERIVED, e_dx

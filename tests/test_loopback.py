@@ -67,7 +67,7 @@ class Ranks:
                                         (dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]))
             yd, dxd = q[dc.DC_Y], q[dc.DC_DX]
             self.r.append(dict(
-                plan=plan, q=q, xb=xb, dyb=dyb, stream=torch.cuda.Stream(),
+                plan=plan, q=q, xb=xb, dyb=dyb, stream=torch.cuda.ExternalStream(dc.dc_comm_stream(comm)),
                 y=torch.full((yd["n"], yd["h"], yd["w"], yd["c_pad"]), float("nan"), dtype=torch.bfloat16,
                              device="cuda"),
                 dx=torch.full((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), float("nan"), dtype=torch.bfloat16,

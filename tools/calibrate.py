@@ -2,9 +2,10 @@
 model ("we use empirically measured ... runtimes") on this
 GPU: for every unique layer of the bench workloads and every valid grid at
 1/2/4/8 ranks, rank 0's shard (the largest block) is run through the C ABI on
-one GPU (virtual plan, no exchange) with L2 evicted before each timed op, and
-the median time is written as a table row "op,n,c,h,w,f,k,s,pad,seconds" keyed
-by the local extents the model looks up (dc_model_load_table).
+one GPU (virtual plan, no exchange) with L2 evicted before each timed op:
+several warm-up runs, then the average of ten, written as a
+table row "op,n,c,h,w,f,k,s,pad,seconds" keyed by the local extents the model
+looks up (dc_model_load_table).
 
 usage: python tools/calibrate.py [--out profiles/cost_table_b200.csv] [--ranks 1,2,4,8]
 """
@@ -31,7 +32,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "cost_table_b200.csv"))
     ap.add_argument("--ranks", default="1,2,4,8")
-    ap.add_argument("--iters", type=int, default=5)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workloads", default="mesh2k,resnet_layers")
     a = ap.parse_args()
     import torch
@@ -71,7 +73,8 @@ def main():
                        "bpx": lambda: dc.dc_conv_bwd_data(plan, dy, w, dx, 0),
                        "bpw": lambda: dc.dc_conv_bwd_filter(plan, x, dy, dw, 0)}
                 for op, f in ops.items():
-                    f()
+                    for _ in range(a.warmup):
+                        f()
                     torch.cuda.synchronize()
                     ts = []
                     for _ in range(a.iters):
@@ -82,7 +85,7 @@ def main():
                         e1.record()
                         torch.cuda.synchronize()
                         ts.append(e0.elapsed_time(e1) / 1e3)
-                    rows.append((op,) + key + (statistics.median(ts),))
+                    rows.append((op,) + key + (statistics.mean(ts),))
                 dc.dc_plan_destroy(plan)
                 print(f"{(N, C, H, W, F, K, S, P)} grid {grid}: local {key[:4]} "
                       + " ".join(f"{r[0]} {r[-1] * 1e6:.1f}us" for r in rows[-3:]), flush=True)
