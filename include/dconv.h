@@ -142,6 +142,13 @@ dc_status_t dc_comm_destroy(dc_comm_t comm);
  * block the host; may be recorded into a CUDA graph, in the same capture as
  * the queuing calls). Nothing queued, or world == 1: no-op. */
 dc_status_t dc_comm_sync(dc_comm_t comm, void *stream);
+/* Bucketing of the DC_ALLREDUCE_ASYNC dW allreduces: the
+ * layers' dW buffers are collected until `bytes` (default 4 MiB) and issued
+ * as one grouped NCCL call on the gradient stream (after the work queued on
+ * the caller's stream so far); dc_comm_sync issues what is left. 0 issues
+ * every allreduce at its call. The buffers must not change until
+ * dc_comm_sync. Host only. Errors: DC_ERR_ARG. */
+dc_status_t dc_comm_set_bucket_bytes(dc_comm_t comm, size_t bytes);
 
 /* COLLECTIVE. Plan one convolution layer: global N, C, H, W, F, odd K,
  * stride in {1, 2}, pad 0 <= P <= K/2, grid `decomp` (product == world, or

@@ -28,7 +28,8 @@ DC_IMPORT_ASYNC, DC_SRC_BF16 = 0x1, 0x2
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "dc_comm_create", "dc_comm_create_local", "dc_comm_stream", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync", "dc_plan_create",
+    "dc_comm_create", "dc_comm_create_local", "dc_comm_stream", "dc_comm_unique_id", "dc_comm_destroy", "dc_comm_sync",
+    "dc_comm_set_bucket_bytes", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_tensor_import", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
@@ -87,6 +88,7 @@ def lib() -> ctypes.CDLL:
         "dc_comm_destroy": [vp],
         "dc_plan_set_splitk_world": [vp, i32],
         "dc_comm_sync": [vp, vp],
+        "dc_comm_set_bucket_bytes": [vp, ctypes.c_size_t],
         "dc_plan_create": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, vp, P(vp)],
         "dc_plan_create_virtual": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, i32, P(vp)],
         "dc_plan_halo_msgs": [vp, i32, P(dc_halo_msg_t), P(i32)],
@@ -176,6 +178,11 @@ def dc_comm_destroy(comm: int):
 def dc_comm_sync(comm: int, stream=None):
     """Make `stream` wait for the dW allreduces queued with DC_ALLREDUCE_ASYNC."""
     _check(lib().dc_comm_sync(comm, _stream(stream)))
+
+
+def dc_comm_set_bucket_bytes(comm: int, nbytes: int):
+    """Bucket the DC_ALLREDUCE_ASYNC dW allreduces up to nbytes (0: none)."""
+    _check(lib().dc_comm_set_bucket_bytes(comm, nbytes))
 
 
 def dc_plan_create(N, C, H, W, F, K, stride, pad, decomp=(0, 0, 0), dtype=DC_BF16, comm=None) -> int:

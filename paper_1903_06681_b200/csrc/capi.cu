@@ -99,6 +99,11 @@ struct dc_comm_s {
     cudaStream_t s_grad = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     bool grad_pending = false;  // allreduces queued since the last dc_comm_sync
+    // DC_ALLREDUCE_ASYNC bucket (the dW allreduces overlap the
+    // later layers' work, one at a time): layers' dW buffers collected until
+    // bucket_cap bytes, then issued as ONE grouped NCCL call on s_grad
+    std::vector<std::pair<float *, size_t>> bucket;
+    size_t bucket_bytes = 0, bucket_cap = 4u << 20;
     std::shared_ptr<LocalGroup> group;  // loopback group (no NCCL), or null
     int plan_seq = 0;                   // plans created on this communicator (loopback registry key)
     // loopback: the virtual rank's two streams (its compute stream, handed to
@@ -1373,16 +1378,30 @@ void allreduce_dw(dc_plan_s *pl, float *dw, cudaStream_t st) {
 // DC_ALLREDUCE_ASYNC: the allreduce waits for the work queued on `st` so far
 // (the filter gradient) and runs on the communicator's gradient stream; `st`
 // does not wait for it (dc_comm_sync joins).
+// Issue the collected bucket: s_grad waits for everything queued on `st` so
+// far (those layers' filter gradients), then one grouped NCCL call.
+void flush_bucket(dc_comm_s *c, cudaStream_t st) {
+    if (c->bucket.empty()) return;
+    CK(cudaEventRecord(c->ev_in, st));
+    CK(cudaStreamWaitEvent(c->s_grad, c->ev_in, 0));
+    NK(ncclGroupStart());
+    for (auto &b : c->bucket) NK(ncclAllReduce(b.first, b.first, b.second, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
+    NK(ncclGroupEnd());
+    c->bucket.clear();
+    c->bucket_bytes = 0;
+    c->grad_pending = true;
+}
+
 void allreduce_dw_async(dc_plan_s *pl, float *dw, cudaStream_t st) {
     if (pl->world() <= 1) return;
     DC_REQUIRE(!is_local(pl), DC_ERR_UNSUPPORTED, "dW allreduce needs real ranks (loopback group: DC_ALLREDUCE off)");
     dc_comm_s *c = pl->comm;
     DC_REQUIRE(c && c->grad_nccl, DC_ERR_ARG, "allreduce needs a communicator");
     const ConvGeom &g = pl->rp.g;
-    CK(cudaEventRecord(c->ev_in, st));
-    CK(cudaStreamWaitEvent(c->s_grad, c->ev_in, 0));
-    NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * g.C, ncclFloat32, ncclSum, c->grad_nccl, c->s_grad));
-    c->grad_pending = true;
+    const size_t n = (size_t)g.F * g.K * g.K * g.C;
+    c->bucket.emplace_back(dw, n);
+    c->bucket_bytes += n * 4;
+    if (c->bucket_bytes >= c->bucket_cap) flush_bucket(c, st);
 }
 
 // Streams, events and small scratch of this rank (created lazily for virtual
@@ -1620,9 +1639,17 @@ dc_status_t dc_comm_destroy(dc_comm_t c) {
     DC_API_END
 }
 
+dc_status_t dc_comm_set_bucket_bytes(dc_comm_t c, size_t bytes) {
+    DC_API_BEGIN
+    DC_REQUIRE(c != nullptr, DC_ERR_ARG, "null communicator");
+    c->bucket_cap = bytes;
+    DC_API_END
+}
+
 dc_status_t dc_comm_sync(dc_comm_t c, void *stream) {
     DC_API_BEGIN
     DC_REQUIRE(c != nullptr, DC_ERR_ARG, "null communicator");
+    if (c->s_grad) flush_bucket(c, (cudaStream_t)stream);
     if (c->s_grad && c->grad_pending) {  // (nothing queued: no-op, also inside a graph capture)
         CK(cudaEventRecord(c->ev_out, c->s_grad));
         CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_out, 0));
