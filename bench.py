@@ -79,6 +79,11 @@ WORKLOADS = {
     "mesh2k_n8": mesh_stack(2048, 8),
     "mesh2k": mesh_stack(2048, 1),
     "mesh1k": mesh_stack(1024, 1, per_block=3),
+    # BASELINE.json configs[3], end to end (NEXT-1): the same stack as ONE
+    # network -- BN + ReLU between the convolutions, the backward chained
+    # through them (NET_WORKLOADS below)
+    "mesh2k_n8_net": mesh_stack(2048, 8),
+    "mesh2k_net": mesh_stack(2048, 1),
     # BASELINE.json configs[2]: the 53 ResNet-50 convolutions at N = 64, 224^2
     "resnet50_n64": resnet50_convs(64),
     # BASELINE.json configs[1]: ResNet-50 conv layers at N=32, 224x224
@@ -91,6 +96,9 @@ WORKLOADS = {
     # BASELINE.json configs[0]
     "c1": [("c1", 1, 2, 16, 16, 4, 3, 1, 1)],
 }
+
+
+NET_WORKLOADS = {"mesh2k_n8_net", "mesh2k_net"}
 
 
 def layer_flops(l) -> float:
@@ -280,6 +288,7 @@ def main():
     ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
     args = ap.parse_args()
     layers = WORKLOADS[args.workload]
+    NET = args.workload in NET_WORKLOADS
     if args.impl == "reference":
         return run_reference(args, layers, args.workload)
 
@@ -338,11 +347,31 @@ def main():
     dc.dc_model_set_comm(MODEL_COMM["alpha_s"], MODEL_COMM["beta_s_per_byte"])
     dc.dc_model_set_strided_latency(MODEL_COMM["alpha_strided_extra_s"])
     dc.dc_model_set_overlap(MODEL_COMM["overlap"])
+    # ---- one grid for a whole network (its layers hand activations over in
+    # place): the pure spatial grid with the least total model cost over the
+    # layers (PAPER.md:218-226 with no redistribution between layers) ----
+    net_grid = None
+    if NET:
+        if args.decomp in ("auto", "spatial"):
+            best = None
+            for ph in range(world, 0, -1):
+                if world % ph:
+                    continue
+                g = (1, ph, world // ph)
+                try:
+                    t = sum(dc.dc_model_layer_cost(*l[1:], g) for l in layers)
+                except dc.DCError:
+                    continue  # invalid for some layer
+                if best is None or t < best[0]:
+                    best = (t, g)
+            net_grid = best[1]
+        else:
+            net_grid = tuple(int(v) for v in args.decomp.split(","))
     # ---- per-layer plans and resident inputs ----
     L = []
     for l in layers:
         name, N, C, H, W, F, K, S, P = l
-        decomp = {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
+        decomp = net_grid or {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
             int(v) for v in args.decomp.split(","))
         plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, DTYPE, comm)
         if args.splitk_basis:
@@ -379,35 +408,72 @@ def main():
         dw = torch.empty((F, K, K, C), dtype=torch.float32, device="cuda")
         bn_mean = torch.empty(F, dtype=torch.float64, device="cuda")
         bn_var = torch.empty(F, dtype=torch.float64, device="cuda")
+        # BN scale / shift of the network workloads (and their gradients)
+        gamma = torch.tensor(1.0 + 0.25 * datagen.gen_block((1, F, 1, 1), datagen.SEED, 7).ravel(),
+                             dtype=torch.float32, device="cuda")
+        beta = torch.tensor(0.1 * datagen.gen_block((1, F, 1, 1), datagen.SEED, 8).ravel(), dtype=torch.float32,
+                            device="cuda")
+        dgamma, dbeta = torch.empty_like(gamma), torch.empty_like(beta)
         # pinned host copies for the end-to-end leg (dense, logical channels)
         host = {"x": x_own.cpu().pin_memory(), "dy": dy_own.cpu().pin_memory(), "w": wt.cpu().pin_memory(),
                 "dw": torch.empty(dw.shape, dtype=torch.float32).pin_memory()}
         L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
-                      dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, host=host))
+                      dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, gamma=gamma, beta=beta, dgamma=dgamma,
+                      dbeta=dbeta, host=host))
     torch.cuda.synchronize()
 
-    def op_calls(d):
-        """The calls of one layer, in step order: (name, fn)."""
-        # the forward epilogue accumulates the BN statistics of y (DC_BN_STATS);
-        # dc_bn_spatial_stats then reduces those partials (+ the NVLink allreduce)
-        fused = not ("bn" in ablate or args.no_fused_bn)
+    fused = not ("bn" in ablate or args.no_fused_bn)
+
+    def conv_fwd_ops(i, d):
+        """Forward of layer i: conv (+ fused BN partials) and the spatially
+        aggregated BN statistics of its output."""
         fwd_flags = FLAGS | (dc.DC_BN_STATS if fused else 0)
         bn_flags = dc.DC_BN_FROM_FWD if fused else 0
-        ops = [("fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], fwd_flags, sp)),
-               # spatially aggregated BN statistics of the layer output (SURVEY.md 8(a) a7)
-               ("bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"], bn_flags, sp))]
-        if "bn" in ablate:
-            ops.pop()
+        ops = [(i, "fwd", lambda: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), d["w"], d["y"], fwd_flags, sp))]
+        if "bn" not in ablate:
+            ops.append((i, "bn", lambda: dc.dc_bn_spatial_stats(d["plan"], d["y"], d["bn_mean"], d["bn_var"],
+                                                                bn_flags, sp)))
+        return ops
+
+    def conv_bwd_ops(i, d):
         if world == 1:
             # no halo / allreduce at one rank: the two backward kernels are
             # called separately so each gets its own timing
-            ops.append(("bpw", lambda: dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(),
-                                                             d["dw"], FLAGS, sp)))
-            ops.append(("bpx", lambda: dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"],
-                                                           FLAGS, sp)))
-        else:
-            ops.append(("bwd", lambda: dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"],
-                                                      d["dx"], d["dw"], FLAGS, sp)))
+            return [(i, "bpw", lambda: dc.dc_conv_bwd_filter(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(),
+                                                             d["dw"], FLAGS, sp)),
+                    (i, "bpx", lambda: dc.dc_conv_bwd_data(d["plan"], d["dyb"].data_ptr(), d["w"], d["dx"], FLAGS,
+                                                           sp))]
+        return [(i, "bwd", lambda: dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), d["w"],
+                                                  d["dx"], d["dw"], FLAGS, sp))]
+
+    def step_ops():
+        """The calls of one step in order: (layer, op name, fn).
+        Conv-stack workloads: every layer forward and backward on its own
+        resident inputs. Network workloads (NEXT-1): the forward chains
+        conv -> BN statistics -> BN apply + ReLU straight into the next layer's
+        margined input; the backward runs from the last layer down, each
+        layer's dx going through the BN / ReLU backward (group sums over the
+        spatial group) into the previous layer's margined dy."""
+        ops = []
+        if not NET:
+            for i, d in enumerate(L):
+                ops += conv_fwd_ops(i, d) + conv_bwd_ops(i, d)
+            return ops
+        for i, d in enumerate(L):
+            ops += conv_fwd_ops(i, d)
+            if i + 1 < len(L):
+                n = L[i + 1]
+                ops.append((i, "act", lambda d=d, n=n: dc.dc_bn_apply(
+                    d["plan"], d["y"], d["bn_mean"], d["bn_var"], d["gamma"], d["beta"], 1e-5, None, dc.DC_RELU,
+                    n["plan"], n["xb"].data_ptr(), sp)))
+        for i in range(len(L) - 1, -1, -1):
+            d = L[i]
+            ops += conv_bwd_ops(i, d)
+            if i > 0:
+                p = L[i - 1]
+                ops.append((i - 1, "bnb", lambda d=d, p=p: dc.dc_bn_backward(
+                    p["plan"], d["dx"], p["y"], p["bn_mean"], p["bn_var"], p["gamma"], p["beta"],
+                    p["dyb"].data_ptr(), 1e-5, None, dc.DC_RELU, p["dgamma"], p["dbeta"], None, sp)))
         return ops
 
     def step(e2e=False):
@@ -416,14 +482,17 @@ def main():
             # (dc_tensor_import with host pointers): every layer's copies are
             # queued up front on the plans' copy streams, so they overlap the
             # compute of the earlier layers; each layer's first call joins them
-            for d in L:
-                dc.dc_tensor_import(d["plan"], dc.DC_X, d["host"]["x"], d["xb"], IMPORT_SRC | dc.DC_IMPORT_ASYNC, sp)
-                dc.dc_tensor_import(d["plan"], dc.DC_DY, d["host"]["dy"], d["dyb"], IMPORT_SRC | dc.DC_IMPORT_ASYNC,
-                                    sp)
+            # (network workloads: only the network input and the loss gradient)
+            for i, d in enumerate(L):
+                if not NET or i == 0:
+                    dc.dc_tensor_import(d["plan"], dc.DC_X, d["host"]["x"], d["xb"],
+                                        IMPORT_SRC | dc.DC_IMPORT_ASYNC, sp)
+                if not NET or i == len(L) - 1:
+                    dc.dc_tensor_import(d["plan"], dc.DC_DY, d["host"]["dy"], d["dyb"],
+                                        IMPORT_SRC | dc.DC_IMPORT_ASYNC, sp)
                 d["w"].copy_(d["host"]["w"], non_blocking=True)
-        for d in L:
-            for _, f in op_calls(d):
-                f()
+        for _, _, f in step_ops():
+            f()
         dc.dc_comm_sync(comm, sp)
         if e2e:  # dW is final after the queued allreduces are joined
             for d in L:
@@ -451,8 +520,7 @@ def main():
         torch.cuda.synchronize()
         if use_graph:
             g_step, g_e2e = capture(step), capture(lambda: step(e2e=True))
-            g_ops = [[(name, capture(lambda f=f: (f(), dc.dc_comm_sync(comm, sp)))) for name, f in op_calls(d)]
-                     for d in L]
+            g_ops = [(i, name, capture(lambda f=f: (f(), dc.dc_comm_sync(comm, sp)))) for i, name, f in step_ops()]
             run_step, run_e2e = g_step.replay, g_e2e.replay
             for _ in range(2):
                 run_step()
@@ -493,20 +561,17 @@ def main():
         ms_e2e = e0.elapsed_time(e1)
         # ---- per-op device times: an instrumented pass, events between ops ----
         barrier()
-        ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in L] for _ in range(args.steps)]
+        ops_list = g_ops if g_ops else step_ops()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(len(ops_list) + 1)] for _ in range(args.steps)]
         for k in range(args.steps):
-            for i, d in enumerate(L):
-                ops = g_ops[i] if g_ops else op_calls(d)
-                ev[k][i][0].record(stream)
-                for j, (name, f) in enumerate(ops):
-                    if g_ops:
-                        f.replay()
-                    else:
-                        f()
-                        dc.dc_comm_sync(comm, sp)
-                    ev[k][i][j + 1].record(stream)
-                for j in range(len(ops) + 1, 5):
-                    ev[k][i][j].record(stream)
+            ev[k][0].record(stream)
+            for j, (i, name, f) in enumerate(ops_list):
+                if g_ops:
+                    f.replay()
+                else:
+                    f()
+                    dc.dc_comm_sync(comm, sp)
+                ev[k][j + 1].record(stream)
         torch.cuda.synchronize()
 
     t = torch.tensor([ms, ms_e2e], dtype=torch.float64, device="cuda")
@@ -520,21 +585,23 @@ def main():
     d2h = sum(d["host"]["dw"].numel() * 4 for d in L)
 
     # ---- per-op device times on the launching stream, from the timed steps ----
-    def avg(i, a, b):
-        # median over the instrumented steps: one op hit by a stray clock dip
-        # must not become the reported roofline kernel
-        return statistics.median(ev[k][i][a].elapsed_time(ev[k][i][b]) for k in range(args.steps))
+    # median over the instrumented steps (one op hit by a stray clock dip must
+    # not become the reported roofline kernel), indexed by (layer, op name)
+    op_t = [dict() for _ in L]
+    for j, (i, name, _) in enumerate(ops_list):
+        op_t[i][name] = statistics.median(ev[k][j].elapsed_time(ev[k][j + 1]) for k in range(args.steps))
     per = []
     for i, d in enumerate(L):
-        f_ms, bn_ms, w_ms, x_ms = avg(i, 0, 1), avg(i, 1, 2), avg(i, 2, 3), avg(i, 3, 4)
-        d["bn_ms"] = bn_ms
-        per.append((d, f_ms, w_ms, x_ms))
+        t = op_t[i]
+        bwd = t.get("bwd", t.get("bpw", 0.0) + t.get("bpx", 0.0))
+        d["bn_ms"] = t.get("bn", 0.0)
+        per.append((d, t["fwd"], bwd, t))
     peaks, peak_src = load_peaks()
     # dominant kernel: conv_v2_kernel (the implicit-GEMM forward / backward-data
     # kernel, the largest share of the step in profiles/r1_launches_*.txt),
     # reported on the layer whose forward takes longest -- at one GPU that op
     # is exactly one conv_v2 launch (no split-K on the large layers).
-    op_ms, d = max(((f_ms, d) for d, f_ms, w_ms, x_ms in per), key=lambda c: c[0])
+    op_ms, d = max(((f_ms, d) for d, f_ms, b_ms, t in per), key=lambda c: c[0])
     op = "fp"
     loc = d["l"]
     # algorithmic work of THIS rank's shard (blocked split: global / world)
@@ -593,12 +660,17 @@ def main():
             "config": {"workload": args.workload, "global_batch": layers[0][1],
                        "layers": [{"name": d["l"][0], "shape_NCHW_F_K_S_P": list(d["l"][1:]),
                                    "decomp": list(d["decomp"]), "model_pred_ms": d["pred"] * 1e3,
-                                   "fwd_ms": f_ms, "bn_stats_ms": d["bn_ms"], "bwd_ms": w_ms + x_ms,
-                                   "bwd_filter_ms": w_ms,
-                                   "bwd_data_ms": x_ms,
+                                   "fwd_ms": f_ms, "bn_stats_ms": d["bn_ms"], "bwd_ms": b_ms,
+                                   **({"bwd_filter_ms": t["bpw"], "bwd_data_ms": t["bpx"]} if "bpw" in t else {}),
+                                   **({"bn_apply_relu_ms": t["act"]} if "act" in t else {}),
+                                   **({"bn_relu_bwd_ms": t["bnb"]} if "bnb" in t else {}),
                                    "fwd_tflops": layer_flops(d["l"]) / (f_ms / 1e3) / 1e12,
-                                   "bwd_tflops": 2 * layer_flops(d["l"]) / ((w_ms + x_ms) / 1e3) / 1e12}
-                                  for d, f_ms, w_ms, x_ms in per],
+                                   "bwd_tflops": 2 * layer_flops(d["l"]) / (b_ms / 1e3) / 1e12}
+                                  for d, f_ms, b_ms, t in per],
+                       "network": ("end to end: conv -> spatial BN -> BN apply + ReLU into the next layer's "
+                                   "margined input; backward through BN / ReLU (group sums) into the previous "
+                                   "layer's margined dy; one grid for all layers") if NET else
+                                  "conv stack: every layer on its own resident inputs",
                        "parallelism": {"auto": "per-layer model-chosen (pN,pH,pW)",
                                        "spatial": "pure spatial, per-layer model-chosen (1,pH,pW)"}.get(
                                            args.decomp, args.decomp),
@@ -618,11 +690,12 @@ def main():
     if args.cost_table and rank == 0:
         with open(args.cost_table, "w") as f:
             f.write("op,n,c,h,w,f,k,s,pad,seconds\n")
-            for d, f_ms, w_ms, x_ms in per:
+            for d, f_ms, b_ms, t in per:
                 _, N, C, H, W, F, K, S, P = d["l"]
                 xd = d["xd"]
-                for op, t in (("fp", f_ms), ("bpw", w_ms), ("bpx", x_ms)):
-                    f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{t / 1e3}\n")
+                for op, tt in (("fp", f_ms), ("bpw", t.get("bpw")), ("bpx", t.get("bpx"))):
+                    if tt is not None:
+                        f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{tt / 1e3}\n")
     # graphs hold NCCL persistent resources: release them before the communicator
     del run_step, run_e2e
     g_step = g_e2e = g_ops = ops = f = None

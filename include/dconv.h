@@ -284,6 +284,38 @@ dc_status_t dc_conv_bwd(dc_plan_t plan, const void *x_margined, void *dy_margine
 dc_status_t dc_bn_spatial_stats(dc_plan_t plan, const void *t, double *mean_dev,
                                 double *var_dev, unsigned flags, void *stream);
 
+/* ---- the layers between the convolutions ---- */
+#define DC_RELU 0x4u
+/* Batch-norm apply on this rank's shard of a layer output y (DC_Y layout of
+ * `plan`, bf16 or fp32 per the plan), with the group statistics mean / var
+ * (device fp64 [F], from dc_bn_spatial_stats) and gamma / beta (device fp32
+ * [F]): out = gamma (y - mean) / sqrt(var + eps) + beta [+ residual (DC_Y
+ * layout)] [then ReLU with DC_RELU] (reading R27).
+ * The result goes straight into the next layer's margined input when
+ * dst_plan is given (dst = its DC_X buffer; its owned block must be this
+ * plan's output block -- the same decomposition of the activation, else
+ * DC_ERR_PARTITION -- fp32 plans store the [hi | lo] split), or to dst as a
+ * dense tensor of the DC_Y layout. Elementwise, stream-ordered, not
+ * collective. Errors: DC_ERR_ARG, DC_ERR_PARTITION. */
+dc_status_t dc_bn_apply(dc_plan_t plan, const void *y, const double *mean, const double *var, const float *gamma,
+                        const float *beta, double eps, const void *residual, unsigned flags, dc_plan_t dst_plan,
+                        void *dst, void *stream);
+/* Backward of dc_bn_apply: dout = the gradient of its output (DC_Y layout of
+ * `plan`, e.g. the next layer's dx), y / mean / var / gamma / beta / eps /
+ * residual / flags as in the forward. With g = dout masked by the ReLU
+ * (recomputed from y) and y_hat = (y - mean) / sqrt(var + eps), the sums
+ * sum(g) and sum(g y_hat) are aggregated over the spatial group of the
+ * forward statistics (COLLECTIVE over that group; DC_BN_LOCAL
+ * for the purely local variant) and dy = gamma / sqrt(var + eps) (g - sum g
+ * / M - y_hat sum(g y_hat) / M), M = the group's pixels, is written into
+ * the owned block of dy_margined (this plan's DC_DY buffer, ready for the
+ * dy halo exchange of the convolution's backward). dgamma = sum(g y_hat),
+ * dbeta = sum g (device fp32 [F], may be NULL); dresidual (DC_Y layout, may
+ * be NULL) receives g. Errors: DC_ERR_ARG, DC_ERR_COMM. */
+dc_status_t dc_bn_backward(dc_plan_t plan, const void *dout, const void *y, const double *mean, const double *var,
+                           const float *gamma, const float *beta, double eps, const void *residual, unsigned flags,
+                           float *dgamma, float *dbeta, void *dresidual, void *dy_margined, void *stream);
+
 /* Number of kernels this library launched on this thread so far (for the
  * bench's gpu_launches claim). */
 uint64_t dc_kernel_launches(void);

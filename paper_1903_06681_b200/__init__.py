@@ -25,6 +25,7 @@ DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DET
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 DC_BN_LOCAL, DC_BN_FROM_FWD = 0x1, 0x2
 DC_IMPORT_ASYNC, DC_SRC_BF16 = 0x1, 0x2
+DC_RELU = 0x4
 
 # every symbol include/dconv.h declares (checked by tests/test_abi.py)
 EXPORTS = [
@@ -32,7 +33,8 @@ EXPORTS = [
     "dc_comm_set_bucket_bytes", "dc_plan_create",
     "dc_plan_create_virtual", "dc_plan_halo_msgs", "dc_plan_query", "dc_plan_decomp", "dc_plan_set_splitk_world",
     "dc_plan_destroy", "dc_buffer_alloc", "dc_tensor_import", "dc_halo_exchange", "dc_conv_fwd", "dc_conv_bwd_data",
-    "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_kernel_launches",
+    "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_bn_apply", "dc_bn_backward",
+    "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
     "dc_model_choose", "dc_model_choose_fixed",
 ]
@@ -103,6 +105,8 @@ def lib() -> ctypes.CDLL:
         "dc_conv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_conv_bwd": [vp, vp, vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_bn_spatial_stats": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_bn_apply": [vp, vp, vp, vp, vp, vp, ctypes.c_double, vp, ctypes.c_uint, vp, vp, vp],
+        "dc_bn_backward": [vp, vp, vp, vp, vp, vp, vp, ctypes.c_double, vp, ctypes.c_uint, vp, vp, vp, vp, vp],
         "dc_model_set_comm": [ctypes.c_double, ctypes.c_double],
         "dc_model_load_table": [ctypes.c_char_p],
         "dc_model_set_overlap": [i32],
@@ -285,6 +289,21 @@ def dc_bn_spatial_stats(plan: int, t, mean, var, flags: int = 0, stream=None, lo
     """flags: DC_BN_LOCAL | DC_BN_FROM_FWD (local_only=True is DC_BN_LOCAL)."""
     flags = int(flags) | (DC_BN_LOCAL if local_only else 0)
     _check(lib().dc_bn_spatial_stats(plan, _ptr(t), _ptr(mean), _ptr(var), flags, _stream(stream)))
+
+
+def dc_bn_apply(plan: int, y, mean, var, gamma, beta, eps: float = 1e-5, residual=None, flags: int = DC_RELU,
+                dst_plan: int | None = None, dst=None, stream=None):
+    """out = [relu](BN(y) + residual) into dst (dst_plan's margined input, or dense)."""
+    _check(lib().dc_bn_apply(plan, _ptr(y), _ptr(mean), _ptr(var), _ptr(gamma), _ptr(beta), eps, _ptr(residual),
+                             flags, dst_plan, _ptr(dst), _stream(stream)))
+
+
+def dc_bn_backward(plan: int, dout, y, mean, var, gamma, beta, dy_margined, eps: float = 1e-5, residual=None,
+                   flags: int = DC_RELU, dgamma=None, dbeta=None, dresidual=None, stream=None):
+    """dy (into the owned block of the plan's margined dy buffer), dgamma, dbeta, dresidual."""
+    _check(lib().dc_bn_backward(plan, _ptr(dout), _ptr(y), _ptr(mean), _ptr(var), _ptr(gamma), _ptr(beta), eps,
+                                _ptr(residual), flags, _ptr(dgamma), _ptr(dbeta), _ptr(dresidual), _ptr(dy_margined),
+                                _stream(stream)))
 
 
 def dc_kernel_launches() -> int:

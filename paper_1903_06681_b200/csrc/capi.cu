@@ -31,6 +31,7 @@
 #include "launch.cuh"
 #include "wgrad_v2.cuh"
 #include "tf32.cuh"
+#include "bn.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -46,6 +47,7 @@ void preload_conv_v2();
 void preload_halo();
 void preload_tf32();
 void preload_wgrad_v2();
+void preload_bn();
 // Every kernel of the library loaded into this context (see preload_*):
 // once, at communicator creation.
 void preload_kernels() {
@@ -56,6 +58,7 @@ void preload_kernels() {
         preload_halo();
         preload_tf32();
         preload_wgrad_v2();
+        preload_bn();
     });
 }
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
@@ -167,6 +170,12 @@ struct dc_plan_s {
     double *bn_part = nullptr;
     size_t bn_part_bytes = 0;
     double *bn_sums = nullptr;
+    float *bn_coef = nullptr;        // BN apply / backward coefficients [4][Fp]
+    size_t bn_coef_bytes = 0;
+    double *bnb_part = nullptr;      // BN backward partials [blocks][2][Fp]
+    size_t bnb_part_bytes = 0;
+    double *bn_scratch = nullptr;    // (mean / var outputs the backward's group sum does not need)
+    size_t bn_scratch_bytes = 0;
     double *bn_fpart = nullptr;      // fused BN partials of the last DC_BN_STATS forward
     size_t bn_fpart_bytes = 0;
     const void *bn_fused_y = nullptr;  // its y (stats of any other tensor: bn_sums_kernel)
@@ -227,6 +236,9 @@ struct dc_plan_s {
         if (bn_part) cudaFree(bn_part);
         if (bn_sums) cudaFree(bn_sums);
         if (bn_fpart) cudaFree(bn_fpart);
+        if (bn_coef) cudaFree(bn_coef);
+        if (bnb_part) cudaFree(bnb_part);
+        if (bn_scratch) cudaFree(bn_scratch);
         for (auto e : ev)
             if (e) cudaEventDestroy(e);
         if (s_comm && !s_comm_shared) cudaStreamDestroy(s_comm);
@@ -1447,11 +1459,15 @@ void presize(dc_plan_s *pl) {
     const dc_status_t r3 = dc_conv_bwd_filter(pl, d, d, reinterpret_cast<float *>(d), 0, s);
     const dc_status_t r4 = dc_bn_spatial_stats(pl, d, reinterpret_cast<double *>(d), reinterpret_cast<double *>(d),
                                               DC_BN_LOCAL, s);
+    double *dd = reinterpret_cast<double *>(d);
+    float *df = reinterpret_cast<float *>(d);
+    const dc_status_t r5 = dc_bn_backward(pl, d, d, dd, dd, df, df, 1e-5, nullptr, DC_BN_LOCAL, nullptr, nullptr,
+                                          nullptr, d, s);
     CK(cudaFree(d));
     pl->fwd_epoch = 0, pl->bn_fused_epoch = 0, pl->bn_fused_y = nullptr, pl->bn_fused_slots = 0;
-    DC_REQUIRE(r1 == DC_OK && r2 == DC_OK && r3 == DC_OK && r4 == DC_OK, DC_ERR_UNSUPPORTED,
-               "layer not supported by the kernels (%d %d %d %d): %s", (int)r1, (int)r2, (int)r3, (int)r4,
-               dc_last_error());
+    DC_REQUIRE(r1 == DC_OK && r2 == DC_OK && r3 == DC_OK && r4 == DC_OK && r5 == DC_OK, DC_ERR_UNSUPPORTED,
+               "layer not supported by the kernels (%d %d %d %d %d): %s", (int)r1, (int)r2, (int)r3, (int)r4,
+               (int)r5, dc_last_error());
 }
 
 dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, bool is_virtual) {
@@ -2023,6 +2039,114 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
         launch_bn_finalize(pl->bn_sums, (int)g.Fp, (int)g.F, (double)rp.nrange.size() * g.Ho * g.Wo, mean,
                            var, st);
     }
+    DC_API_END
+}
+
+namespace {
+// Sum 2 * Fp per-channel doubles (local at `local`) over this plan's BN group
+// (the ranks with this rank's i_N): the plan's NVLink mailbox,
+// or NCCL; returns the device pointer of the group sums. mean / var of the
+// mailbox kernel go to `mean`, `var` (scratch when the caller needs none).
+const double *bn_group_sum(dc_plan_s *pl, double *local, double *mean, double *var, cudaStream_t st) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    if (pl->bn_p2p) {
+        resolve_local_peers(pl);
+        BnP2P b{};
+        b.gsize = pl->bn_group;
+        for (int k = 0; k < b.gsize; ++k) {
+            DC_REQUIRE(pl->bn_peer_mail[k] != nullptr, DC_ERR_ARG, "BN mailbox of group member %d not mapped", k);
+            b.peer_box[k] = reinterpret_cast<double *>(pl->bn_peer_mail[k] + 256);
+            b.peer_flags[k] = reinterpret_cast<uint32_t *>(pl->bn_peer_mail[k]);
+        }
+        b.my_box = reinterpret_cast<const double *>(pl->bn_mail + 256);
+        b.my_flags = reinterpret_cast<const uint32_t *>(pl->bn_mail);
+        b.my_idx = rp.rank - rp.in * pl->bn_group;
+        b.epoch = pl->bn_epoch;
+        b.local = local;
+        b.cpad = (int)g.Fp, b.c = (int)g.F;
+        b.count = (double)rp.nrange.size() * g.Ho * g.Wo;
+        b.sums = local + 2 * g.Fp;
+        b.mean = mean, b.var = var;
+        launch_bn_allreduce_p2p(b, st);
+        return local + 2 * g.Fp;
+    }
+    DC_REQUIRE(pl->bn_comm != nullptr, DC_ERR_ARG, "spatial BN needs a communicator");
+    NK(ncclAllReduce(local, local, 2 * g.Fp, ncclFloat64, ncclSum, pl->bn_comm, st));
+    return local;
+}
+
+BnArgs bn_args(dc_plan_s *pl, const void *y, const void *res, const void *dout, bool relu) {
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    BnArgs a{};
+    a.y = y, a.res = res, a.dout = dout, a.coef = pl->bn_coef;
+    a.esz = g.esz(), a.relu = relu ? 1 : 0;
+    a.n = (int)rp.nrange.size(), a.h = (int)rp.h.out.size(), a.w = (int)rp.w.out.size();
+    a.npix = (long long)a.n * a.h * a.w;
+    a.cpad = (int)g.Fp, a.c = (int)g.F;
+    return a;
+}
+}  // namespace
+
+dc_status_t dc_bn_apply(dc_plan_t pl, const void *y, const double *mean, const double *var, const float *gamma,
+                        const float *beta, double eps, const void *residual, unsigned flags, dc_plan_t dst_plan,
+                        void *dst, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && y && mean && var && gamma && beta && dst, DC_ERR_ARG, "null argument");
+    DC_REQUIRE((flags & ~DC_RELU) == 0, DC_ERR_ARG, "unknown BN apply flags 0x%x", flags);
+    NoPdlScope no_pdl(is_local(pl));
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    const ConvGeom &g = pl->rp.g;
+    ensure_alloc(pl->grave, pl->bn_coef, pl->bn_coef_bytes, sizeof(float) * 4 * g.Fp);
+    launch_bn_coeff(mean, var, gamma, beta, eps, (int)g.F, (int)g.Fp, pl->bn_coef, st);
+    BnArgs a = bn_args(pl, y, residual, nullptr, (flags & DC_RELU) != 0);
+    a.dst = dst;
+    if (dst_plan) {  // the next layer's margined input: the same block of the activation
+        const dc_shard_desc_t yd = describe(pl->rp, DC_Y), xd = describe(dst_plan->rp, DC_X);
+        DC_REQUIRE(dst_plan->rp.g.dt == g.dt && xd.c == yd.c && xd.n0 == yd.n0 && xd.n == yd.n && xd.h0 == yd.h0 &&
+                       xd.h == yd.h && xd.w0 == yd.w0 && xd.w == yd.w,
+                   DC_ERR_PARTITION,
+                   "dc_bn_apply: the next layer's input block differs from this layer's output block "
+                   "(a different decomposition needs a redistribution)");
+        a.hb = (int)xd.hb, a.wb = (int)xd.wb, a.r0 = xd.halo_n, a.c0 = xd.halo_w, a.dcp = (int)xd.c_pad;
+        a.split = g.dt;
+    } else {
+        a.hb = a.h, a.wb = a.w, a.r0 = 0, a.c0 = 0, a.dcp = a.cpad, a.split = 0;
+    }
+    launch_bn_apply(a, st);
+    DC_API_END
+}
+
+dc_status_t dc_bn_backward(dc_plan_t pl, const void *dout, const void *y, const double *mean, const double *var,
+                           const float *gamma, const float *beta, double eps, const void *residual, unsigned flags,
+                           float *dgamma, float *dbeta, void *dresidual, void *dy_margined, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(pl && dout && y && mean && var && gamma && beta && dy_margined, DC_ERR_ARG, "null argument");
+    DC_REQUIRE((flags & ~(DC_RELU | DC_BN_LOCAL)) == 0, DC_ERR_ARG, "unknown BN backward flags 0x%x", flags);
+    NoPdlScope no_pdl(is_local(pl));
+    ensure_local_resources(pl);
+    cudaStream_t st = (cudaStream_t)stream;
+    const RankPlan &rp = pl->rp;
+    const ConvGeom &g = rp.g;
+    ensure_alloc(pl->grave, pl->bn_coef, pl->bn_coef_bytes, sizeof(float) * 4 * g.Fp);
+    ensure_alloc(pl->grave, pl->bn_scratch, pl->bn_scratch_bytes, sizeof(double) * 2 * g.Fp);
+    launch_bn_coeff(mean, var, gamma, beta, eps, (int)g.F, (int)g.Fp, pl->bn_coef, st);
+    BnArgs a = bn_args(pl, y, residual, dout, (flags & DC_RELU) != 0);
+    const int blocks = bn_bwd_blocks(a.npix, a.cpad);
+    ensure_alloc(pl->grave, pl->bnb_part, pl->bnb_part_bytes, sizeof(double) * 2 * g.Fp * blocks);
+    launch_bn_bwd_partials(a, pl->bnb_part, blocks, st);
+    launch_bn_reduce(pl->bnb_part, blocks, (int)g.Fp, pl->bn_sums, (int)g.F, (double)a.npix, nullptr, nullptr, st);
+    const bool global = !(flags & DC_BN_LOCAL) && pl->bn_group > 1;
+    const double *sums = global ? bn_group_sum(pl, pl->bn_sums, pl->bn_scratch, pl->bn_scratch + g.Fp, st)
+                                : pl->bn_sums;
+    const double count = global ? (double)rp.nrange.size() * g.Ho * g.Wo : (double)a.npix;
+    const dc_shard_desc_t dyd = describe(rp, DC_DY);
+    a.dst = dy_margined;
+    a.hb = (int)dyd.hb, a.wb = (int)dyd.wb, a.r0 = dyd.halo_n, a.c0 = dyd.halo_w, a.dcp = (int)dyd.c_pad;
+    a.split = g.dt;
+    launch_bn_bwd_apply(a, sums, count, gamma, dgamma, dbeta, dresidual, st);
     DC_API_END
 }
 

@@ -880,7 +880,9 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     // opt-in DC_V2_CG2=1: faster for streamed 128-wide weight tiles at stride 1
     // with warm L2 (conv2_2 fwd 85 -> 69 us) but slower in the bench step with
     // cold inputs (92 -> 128 us: the leader waits for the slower of two tile
-    // loads) and for 256-wide, resident or stride-2 tiles
+    // loads) and for 256-wide, resident or stride-2 tiles (round 2, resident
+    // 64-channel weights, cold L2: conv1_2 fwd 660 -> 735 us, bwd-data 639 ->
+    // 887 us; profiles/r2_cg2_resident_ab.txt)
     static const bool cg2 = std::getenv("DC_V2_CG2") != nullptr;
     const bool cand2 = cg2 && p.bn == 128 && p.s_in == 1 && p.kind == 0;
     p.cta2 = 0;
@@ -894,19 +896,6 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.b_resident = 1;
         p.b_stages = 0;
         p.a_stages = std::min(4, (smem_limit - fixed - resident_b) / p.a_stage_bytes);
-        // (experiment, DC_V2_CG2R=1) CTA pairs on resident weights: M = 256
-        // over two SMs, each holding half of the N columns, so an N = 64 / 128
-        // MMA reads 4 KB of A + 1 / 2 KB of B per SM instead of 4 + 2 / 4
-        static const bool cg2r = std::getenv("DC_V2_CG2R") != nullptr;
-        if (cg2r && p.kind == 0 && (p.bn == 64 || p.bn == 128)) {
-            const int half_slot = (int)round_up((int64_t)(p.bn / 2) * p.cg * 2, 1024);
-            const int rb = p.T * (p.ncg / p.ksplit) * half_slot;
-            if (rb + 2 * p.a_stage_bytes + fixed <= smem_limit) {
-                p.cta2 = 1;
-                p.b_slot_bytes = half_slot;
-                p.a_stages = std::min(4, (smem_limit - fixed - rb) / p.a_stage_bytes);
-            }
-        }
         // resident weights: a work item of two stacked tiles halves the per-item
         // overheads (barriers, accumulator hand-off) and the A halo rows
         static const bool res_pair = std::getenv("DC_V2_RES_TPW1") == nullptr;

@@ -26,9 +26,13 @@ ConvGeom make_geom(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K,
     DC_REQUIRE(H + 2 * P >= K && W + 2 * P >= K, DC_ERR_SHAPE, "input smaller than the kernel");
     g.Ho = (H + 2 * P - K) / S + 1;
     g.Wo = (W + 2 * P - K) / S + 1;
-    // 32-byte channel granules: 16 bf16 or 8 fp32 (one MMA K step either way)
-    g.Cp = round_up(C, dt ? 8 : 16);
-    g.Fp = round_up(F, dt ? 8 : 16);
+    // 32-byte channel granules: 16 bf16 or 8 fp32 (one MMA K step either way);
+    // fp32 channel counts above 8 go to multiples of 32, so the 3xTF32 K
+    // segments (6 x C_pad 16-bit units per tap) fill 128-byte (64-unit) stages
+    // (C = 18: 24 channels gave 16-unit stages, measured 6x slower)
+    auto pad = [&](int64_t c) { return dt ? (c <= 8 ? 8 : round_up(c, 32)) : round_up(c, 16); };
+    g.Cp = pad(C);
+    g.Fp = pad(F);
     return g;
 }
 

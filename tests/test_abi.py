@@ -57,17 +57,20 @@ def test_errors_are_status_codes_not_exceptions(dc):
 
 
 def test_fp32_plan_layouts(dc):
-    """DC_FP32_3XTF32 plans: channels padded to 8, margined x / dy hold
-    [hi | lo] fp32 halves, y / dx plain fp32, w fp32, dW unpadded."""
+    """DC_FP32_3XTF32 plans: channels padded to 8 (C <= 8) or 32, margined
+    x / dy hold [hi | lo] fp32 halves, y / dx plain fp32, w fp32, dW unpadded."""
     p = dc.dc_plan_create_virtual(2, 18, 20, 20, 12, 3, 1, 1, (1, 2, 1), 0, dtype=dc.DC_FP32_3XTF32)
     try:
         x, y = dc.dc_plan_query(p, dc.DC_X), dc.dc_plan_query(p, dc.DC_Y)
         dy, w, dw = dc.dc_plan_query(p, dc.DC_DY), dc.dc_plan_query(p, dc.DC_W), dc.dc_plan_query(p, dc.DC_DW)
-        assert (x["c"], x["c_pad"], x["halo_s"]) == (18, 2 * 24, 1)
-        assert x["bytes"] == 2 * x["hb"] * x["wb"] * 48 * 4
-        assert (y["c_pad"], y["bytes"]) == (16, 2 * 10 * 20 * 16 * 4)
-        assert (dy["c_pad"], w["c_pad"], w["bytes"]) == (32, 24, 12 * 9 * 24 * 4)
+        assert (x["c"], x["c_pad"], x["halo_s"]) == (18, 2 * 32, 1)
+        assert x["bytes"] == 2 * x["hb"] * x["wb"] * 64 * 4
+        assert (y["c_pad"], y["bytes"]) == (32, 2 * 10 * 20 * 32 * 4)
+        assert (dy["c_pad"], w["c_pad"], w["bytes"]) == (64, 32, 12 * 9 * 32 * 4)
         assert (dw["c_pad"], dw["bytes"]) == (18, 12 * 9 * 18 * 4)
+        p2 = dc.dc_plan_create_virtual(1, 3, 8, 8, 4, 3, 1, 1, (1, 1, 1), 0, dtype=dc.DC_FP32_3XTF32)
+        assert dc.dc_plan_query(p2, dc.DC_X)["c_pad"] == 2 * 8 and dc.dc_plan_query(p2, dc.DC_Y)["c_pad"] == 8
+        dc.dc_plan_destroy(p2)
     finally:
         dc.dc_plan_destroy(p)
 

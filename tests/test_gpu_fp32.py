@@ -199,9 +199,12 @@ def test_fp32_bn_stats(dc):
     plan = dc.dc_plan_create_virtual(N, C, H, W, F, K, S, P, (1, 1, 1), 0, dtype=dc.DC_FP32_3XTF32)
     try:
         t = datagen.gen_block((N, F, H, W), 7, 9, kind="act24")
+        cp = dc.dc_plan_query(plan, dc.DC_Y)["c_pad"]
+        tt = torch.zeros((N, H, W, cp), dtype=torch.float32, device="cuda")
+        tt[..., :F] = nhwc32(t)
         mean = torch.zeros(F, dtype=torch.float64, device="cuda")
         var = torch.zeros(F, dtype=torch.float64, device="cuda")
-        dc.dc_bn_spatial_stats(plan, nhwc32(t), mean, var, dc.DC_BN_LOCAL)
+        dc.dc_bn_spatial_stats(plan, tt, mean, var, dc.DC_BN_LOCAL)
         torch.cuda.synchronize()
         m_ref, v_ref = oracle.bn_stats(t)
         np.testing.assert_allclose(mean.cpu().numpy(), m_ref, rtol=0, atol=1e-12)

@@ -208,10 +208,12 @@ def test_full_size_sampled_parity(dc, layer):
         # ---- >= 1024 dW entries: all K x K taps of enough (c, f) pairs,
         # each an N Ho Wo dot product over whole channels (Eq. 2) ----
         dwh = dw.double().cpu().numpy()  # F K K C
-        pairs = -(-1024 // (K * K))                 # (c, f) pairs for >= 1024 entries
-        nc = min(C, max(8, int(np.ceil(np.sqrt(pairs)))))
+        pairs = -(-min(1024, F * C * K * K) // (K * K))   # (c, f) pairs for >= 1024 entries
+        nf = min(F, max(1, int(np.ceil(np.sqrt(pairs)))))
+        nc = min(C, -(-pairs // nf))
+        nf = min(F, -(-pairs // nc))
         cs = sorted(set(int(c) for c in np.linspace(0, C - 1, nc).round()))
-        fs = sorted(set(int(f) for f in np.linspace(0, F - 1, min(F, -(-pairs // len(cs)))).round()))
+        fs = sorted(set(int(f) for f in np.linspace(0, F - 1, nf).round()))
         gen_dev = dict(dtype=torch.float64, device="cuda")
         xcs = {c: datagen.gen_block_nhwc_torch((N, C, H, W), datagen.SEED, datagen.TID_X, c=(c, c + 1), **gen_dev)
                .permute(0, 3, 1, 2).cpu().numpy() for c in cs}
