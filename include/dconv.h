@@ -357,6 +357,32 @@ dc_status_t dc_model_choose_fixed(int64_t N, int64_t C, int64_t H, int64_t W, in
                                   int stride, int pad, int world, dc_decomp_t fix, dc_decomp_t *best,
                                   double *seconds);
 
+/* ---- parallel execution strategies (NEXT-3) ---- */
+/* Shuffle(D_i, D_j): seconds to move an N x Ch x H x W activation (2-byte
+ * words) from grid `from`'s blocked distribution to grid `to`'s with a
+ * pairwise-exchange all-to-all -- the max over ranks of the sum over peers of
+ * SR(words sent); 0 when the grids agree. */
+dc_status_t dc_model_shuffle_cost(int64_t N, int64_t Ch, int64_t H, int64_t W, dc_decomp_t from, dc_decomp_t to,
+                                  double *seconds);
+/* One layer of a network for dc_model_strategy: its conv shape and the layers
+ * whose outputs it reads (-1: none / the network input; a residual join has
+ * two parents; shapes must chain: parent F, Ho, Wo = this C, H, W). */
+typedef struct {
+    int64_t N, C, H, W, F;
+    int32_t K, stride, pad;
+    int32_t parent, parent2;
+} dc_layer_t;
+/* A parallel execution strategy: one grid per layer minimising the sum of the
+ * layers' Cost_D(l) (dc_model_layer_cost) and the shuffles of every edge,
+ * forward and backward (reading R28). A line network is solved
+ * exactly by the shortest path over per-layer candidates;
+ * with branches, the longest remaining path is solved first and fixed, and
+ * so on. fix_pn > 0 restricts the candidates to p_N = fix_pn
+ * (1: pure spatial). grids: n entries out; total_seconds (may be NULL): the
+ * strategy's model time. Errors: DC_ERR_ARG, DC_ERR_SHAPE, DC_ERR_PARTITION. */
+dc_status_t dc_model_strategy(const dc_layer_t *layers, int n, int world, int fix_pn, dc_decomp_t *grids,
+                              double *total_seconds);
+
 #ifdef __cplusplus
 }
 #endif

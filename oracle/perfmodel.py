@@ -11,6 +11,7 @@ accounting), R17 (tie-break), R22 (degenerate partitions rejected).
 """
 from __future__ import annotations
 
+import functools
 import math
 
 from . import out_extent
@@ -137,3 +138,82 @@ def choose(layer: dict, P_tot: int, cost, alpha: float, beta: float, **kw):
         if best is None or key < best[0]:
             best = (key, g, t)
     return None if best is None else (best[1], best[2])
+
+
+# ---------------------------------------------------------------------------
+# Parallel execution strategies (SURVEY.md 8(f)
+# NEXT-3), written from the definitions: brute-force index ownership for the
+# shuffle volumes, exhaustive enumeration for the best strategy.
+# ---------------------------------------------------------------------------
+def owner(N: int, H: int, W: int, grid, n: int, h: int, w: int) -> int:
+    """Rank owning element (n, h, w) under the blocked distribution of grid
+    (rank = (i_N p_H + i_H) p_W + i_W, reading R8)."""
+    pn, ph, pw = grid
+
+    def idx(x, X, p):
+        for i in range(p):
+            lo, hi = blocked(X, p, i)
+            if lo <= x < hi:
+                return i
+        raise AssertionError
+    return (idx(n, N, pn) * ph + idx(h, H, ph)) * pw + idx(w, W, pw)
+
+
+@functools.lru_cache(maxsize=None)
+def _shuffle_words(N: int, Ch: int, H: int, W: int, A: tuple, B: tuple) -> tuple:
+    out = {}
+    for n in range(N):
+        for h in range(H):
+            for w in range(W):
+                r, q = owner(N, H, W, A, n, h, w), owner(N, H, W, B, n, h, w)
+                if r != q:
+                    out[(r, q)] = out.get((r, q), 0) + Ch
+    return tuple(sorted(out.items()))
+
+
+def shuffle_words(N: int, Ch: int, H: int, W: int, A, B) -> dict:
+    """{(r, q): words} moved from rank r (owner under A) to rank q (owner
+    under B), r != q: every element counted one by one (a
+    processor sends the indices it no longer owns). (Memoised: a pure
+    function of its arguments.)"""
+    return dict(_shuffle_words(N, Ch, H, W, tuple(A), tuple(B)))
+
+
+def shuffle_cost(N: int, Ch: int, H: int, W: int, A, B, alpha: float, beta: float) -> float:
+    """Shuffle(D_i, D_j) as a pairwise-exchange all-to-all: the
+    max over ranks of the sum over its peers of SR(words to that peer), 2-byte
+    words; 0 when nothing moves."""
+    per = {}
+    for (r, q), n in shuffle_words(N, Ch, H, W, A, B).items():
+        per[r] = per.get(r, 0.0) + sr(n, alpha, beta, 2)
+    return max(per.values()) if per else 0.0
+
+
+def strategy_total(layers: list, parents: list, grids: list, cost, alpha: float, beta: float, **kw) -> float:
+    """Model time of a strategy: sum of Cost_D(l) (layer_cost) + on every
+    parent -> child edge the shuffle of the parent's output forward and of its
+    gradient backward (reading R28)."""
+    t = 0.0
+    for i, (l, g) in enumerate(zip(layers, grids)):
+        t += layer_cost(l, g, cost, alpha, beta, **kw)["total"]
+        for p in parents[i]:
+            if p >= 0:
+                lp = layers[p]
+                Ho = out_extent(lp["H"], lp["K"], lp.get("S", 1), lp.get("P", lp["K"] // 2))
+                Wo = out_extent(lp["W"], lp["K"], lp.get("S", 1), lp.get("P", lp["K"] // 2))
+                t += shuffle_cost(lp["N"], lp["F"], Ho, Wo, grids[p], g, alpha, beta)
+                t += shuffle_cost(lp["N"], lp["F"], Ho, Wo, g, grids[p], alpha, beta)
+    return t
+
+
+def strategy_exhaustive(layers: list, parents: list, P_tot: int, cost, alpha: float, beta: float, **kw):
+    """The best strategy by enumerating every assignment of valid grids
+    (the quantity the paper's shortest path minimises)."""
+    import itertools
+    cands = [[g for g in candidates(P_tot) if valid(l, g)] for l in layers]
+    best = None
+    for combo in itertools.product(*cands):
+        t = strategy_total(layers, parents, list(combo), cost, alpha, beta, **kw)
+        if best is None or t < best[1] - 1e-15:
+            best = (list(combo), t)
+    return best

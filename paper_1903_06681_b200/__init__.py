@@ -36,12 +36,18 @@ EXPORTS = [
     "dc_conv_bwd_filter", "dc_conv_bwd", "dc_bn_spatial_stats", "dc_bn_apply", "dc_bn_backward",
     "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
-    "dc_model_choose", "dc_model_choose_fixed",
+    "dc_model_choose", "dc_model_choose_fixed", "dc_model_shuffle_cost", "dc_model_strategy",
 ]
 
 
 class dc_decomp_t(ctypes.Structure):
     _fields_ = [("pn", ctypes.c_int32), ("ph", ctypes.c_int32), ("pw", ctypes.c_int32)]
+
+
+class dc_layer_t(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("C", ctypes.c_int64), ("H", ctypes.c_int64), ("W", ctypes.c_int64),
+                ("F", ctypes.c_int64), ("K", ctypes.c_int32), ("stride", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("parent", ctypes.c_int32), ("parent2", ctypes.c_int32)]
 
 
 class dc_shard_desc_t(ctypes.Structure):
@@ -114,6 +120,8 @@ def lib() -> ctypes.CDLL:
         "dc_model_layer_cost": [i64] * 5 + [i32, i32, i32, dc_decomp_t, i32, P(ctypes.c_double)],
         "dc_model_choose": [i64] * 5 + [i32, i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
         "dc_model_choose_fixed": [i64] * 5 + [i32, i32, i32, i32, dc_decomp_t, P(dc_decomp_t), P(ctypes.c_double)],
+        "dc_model_shuffle_cost": [i64] * 4 + [dc_decomp_t, dc_decomp_t, P(ctypes.c_double)],
+        "dc_model_strategy": [P(dc_layer_t), i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -345,3 +353,22 @@ def dc_model_choose_fixed(N, C, H, W, F, K, stride, pad, world, fix) -> tuple[tu
     _check(lib().dc_model_choose_fixed(N, C, H, W, F, K, stride, pad, world, dc_decomp_t(*fix), ctypes.byref(d),
                                        ctypes.byref(s)))
     return (d.pn, d.ph, d.pw), s.value
+
+
+def dc_model_shuffle_cost(N, Ch, H, W, src, dst) -> float:
+    """Shuffle(D_i, D_j) of an N x Ch x H x W activation between two grids."""
+    t = ctypes.c_double()
+    _check(lib().dc_model_shuffle_cost(N, Ch, H, W, dc_decomp_t(*src), dc_decomp_t(*dst), ctypes.byref(t)))
+    return t.value
+
+
+def dc_model_strategy(layers, world: int, fix_pn: int = 0):
+    """layers: [(N, C, H, W, F, K, stride, pad, parent[, parent2])]; returns
+    ([(pN, pH, pW)] per layer, model seconds)."""
+    arr = (dc_layer_t * len(layers))()
+    for i, l in enumerate(layers):
+        arr[i] = dc_layer_t(*l[:9], l[9] if len(l) > 9 else -1)
+    out = (dc_decomp_t * len(layers))()
+    t = ctypes.c_double()
+    _check(lib().dc_model_strategy(arr, len(layers), world, fix_pn, out, ctypes.byref(t)))
+    return [(d.pn, d.ph, d.pw) for d in out], t.value

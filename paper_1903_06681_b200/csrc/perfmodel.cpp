@@ -20,6 +20,9 @@
 #include <sstream>
 #include <string>
 #include <tuple>
+#include <algorithm>
+#include <array>
+#include <vector>
 
 #include "plan.hpp"
 
@@ -126,9 +129,199 @@ bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid
     return found;
 }
 
+// ---------------------------------------------------------------------------
+// Parallel execution strategies (PAPER.md:151-153,
+// 216-228): Shuffle(D_i, D_j) and the shortest path over per-layer candidates
+// ---------------------------------------------------------------------------
+namespace {
+int64_t overlap(Range a, Range b) { return std::max<int64_t>(0, std::min(a.hi, b.hi) - std::max(a.lo, b.lo)); }
+}  // namespace
+
+// Pairwise-exchange all-to-all moving an N x Ch x H x W activation (2-byte
+// words) from the blocked distribution of grid A to that of grid B
+// (each rank sends the indices it no longer owns): the max
+// over ranks of the sum over its peers of SR(words sent to that peer); 0 when
+// A == B.
+double model_shuffle_cost(int64_t N, int64_t Ch, int64_t H, int64_t W, Grid A, Grid B) {
+    if (A.pn == B.pn && A.ph == B.ph && A.pw == B.pw) return 0.0;
+    const int P = A.size();
+    double worst = 0.0;
+    for (int r = 0; r < P; ++r) {
+        int an, ah, aw;
+        A.coords(r, an, ah, aw);
+        const Range rn = blocked(N, A.pn, an), rh = blocked(H, A.ph, ah), rw = blocked(W, A.pw, aw);
+        double t = 0.0;
+        for (int q = 0; q < P; ++q) {
+            if (q == r) continue;
+            int bn, bh, bw;
+            B.coords(q, bn, bh, bw);
+            const double words = (double)overlap(rn, blocked(N, B.pn, bn)) * overlap(rh, blocked(H, B.ph, bh)) *
+                                 overlap(rw, blocked(W, B.pw, bw)) * Ch;
+            if (words > 0) t += sr(words, 2);
+        }
+        worst = std::max(worst, t);
+    }
+    return worst;
+}
+
+namespace {
+// the activation between parent p and child c: p's output (N, F_p, Ho_p, Wo_p)
+double edge_cost(const ConvGeom &p, Grid dp, Grid dc_) {
+    // forward (activation) and backward (its gradient) both move
+    return model_shuffle_cost(p.N, p.F, p.Ho, p.Wo, dp, dc_) + model_shuffle_cost(p.N, p.F, p.Ho, p.Wo, dc_, dp);
+}
+}  // namespace
+
+// Strategy over a network given as layers with up to two parents each (-1:
+// the network input, provided in the first layer's distribution).
+// A line network is solved exactly as a shortest path; with
+// branches, the longest remaining path (by the layers' 1-GPU cost, counting
+// only unassigned layers) is solved first with the already assigned layers
+// fixed, repeated until every layer is assigned. Returns the
+// strategy's total: sum of Cost_D(l) + the shuffles on every edge.
+double model_strategy(const std::vector<ConvGeom> &L, const std::vector<std::array<int, 2>> &par, int world,
+                      int fix_pn, std::vector<Grid> &out) {
+    const int n = (int)L.size();
+    std::vector<std::vector<Grid>> cand(n);
+    std::vector<std::vector<double>> cost(n);
+    for (int i = 0; i < n; ++i) {
+        for (int pn = world; pn >= 1; --pn) {
+            if (world % pn || (fix_pn > 0 && pn != fix_pn)) continue;
+            const int rest = world / pn;
+            for (int ph = rest; ph >= 1; --ph) {
+                if (rest % ph) continue;
+                Grid d{pn, ph, rest / ph};
+                if (!grid_valid(L[i], d)) continue;
+                cand[i].push_back(d);
+                cost[i].push_back(model_layer_cost(L[i], d, true));
+            }
+        }
+        DC_REQUIRE(!cand[i].empty(), DC_ERR_PARTITION, "layer %d has no valid grid of %d ranks", i, world);
+    }
+    std::vector<std::vector<int>> kids(n);
+    for (int i = 0; i < n; ++i)
+        for (int p : par[i])
+            if (p >= 0) {
+                DC_REQUIRE(p < i, DC_ERR_ARG, "layer %d: parent %d must come earlier", i, p);
+                kids[p].push_back(i);
+            }
+    std::vector<double> weight(n);
+    for (int i = 0; i < n; ++i) weight[i] = model_layer_cost(L[i], Grid{1, 1, 1}, false);
+    std::vector<int> assigned(n, -1);  // candidate index
+    for (;;) {
+        // longest path over unassigned weight (DAG in index order)
+        std::vector<double> best(n, -1.0);
+        std::vector<int> from(n, -1);
+        int end = -1;
+        for (int i = 0; i < n; ++i) {
+            const double w = assigned[i] < 0 ? weight[i] : 0.0;
+            best[i] = w;
+            for (int p : par[i])
+                if (p >= 0 && best[p] + w > best[i]) best[i] = best[p] + w, from[i] = p;
+        }
+        for (int i = 0; i < n; ++i)
+            if (kids[i].empty() && (end < 0 || best[i] > best[end])) end = i;
+        std::vector<int> path;
+        for (int i = end; i >= 0; i = from[i]) path.push_back(i);
+        std::reverse(path.begin(), path.end());
+        bool any = false;
+        for (int i : path) any = any || assigned[i] < 0;
+        if (!any) {  // every sink path assigned: remaining layers (if any) start new paths
+            int u = -1;
+            for (int i = 0; i < n && u < 0; ++i)
+                if (assigned[i] < 0) u = i;
+            if (u < 0) break;
+            path.clear();  // a chain down from u through unassigned first children
+            for (int i = u; i >= 0;) {
+                path.push_back(i);
+                int nx = -1;
+                for (int k : kids[i])
+                    if (assigned[k] < 0) {
+                        nx = k;
+                        break;
+                    }
+                i = nx;
+            }
+        }
+        // shortest path along `path`, assigned layers restricted to their grid
+        const int m = (int)path.size();
+        std::vector<std::vector<double>> dist(m);
+        std::vector<std::vector<int>> back(m);
+        for (int k = 0; k < m; ++k) {
+            const int i = path[k];
+            const int nc = (int)cand[i].size();
+            dist[k].assign(nc, 1e300);
+            back[k].assign(nc, -1);
+            for (int a = 0; a < nc; ++a) {
+                if (assigned[i] >= 0 && assigned[i] != a) continue;
+                if (k == 0) {
+                    dist[k][a] = cost[i][a];
+                    continue;
+                }
+                const int ip = path[k - 1];
+                for (int b = 0; b < (int)cand[ip].size(); ++b) {
+                    if (dist[k - 1][b] >= 1e299) continue;
+                    const double t = dist[k - 1][b] + edge_cost(L[ip], cand[ip][b], cand[i][a]) + cost[i][a];
+                    if (t < dist[k][a]) dist[k][a] = t, back[k][a] = b;  // strict: first candidate on ties
+                }
+            }
+        }
+        int a = 0;
+        for (int c = 1; c < (int)dist[m - 1].size(); ++c)
+            if (dist[m - 1][c] < dist[m - 1][a]) a = c;
+        for (int k = m - 1; k >= 0; --k) {
+            assigned[path[k]] = a;
+            a = back[k][a];
+        }
+    }
+    out.resize(n);
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) {
+        out[i] = cand[i][assigned[i]];
+        total += cost[i][assigned[i]];
+        for (int p : par[i])
+            if (p >= 0) total += edge_cost(L[p], out[p], out[i]);
+    }
+    return total;
+}
+
 }  // namespace dc
 
 using namespace dc;
+
+extern "C" dc_status_t dc_model_shuffle_cost(int64_t N, int64_t Ch, int64_t H, int64_t W, dc_decomp_t from,
+                                             dc_decomp_t to, double *seconds) {
+    DC_API_BEGIN
+    DC_REQUIRE(seconds && N > 0 && Ch > 0 && H > 0 && W > 0, DC_ERR_ARG, "bad arguments");
+    Grid A{from.pn, from.ph, from.pw}, B{to.pn, to.ph, to.pw};
+    DC_REQUIRE(A.size() == B.size() && A.size() > 0, DC_ERR_ARG, "grids of different sizes");
+    *seconds = model_shuffle_cost(N, Ch, H, W, A, B);
+    DC_API_END
+}
+
+extern "C" dc_status_t dc_model_strategy(const dc_layer_t *layers, int n, int world, int fix_pn, dc_decomp_t *grids,
+                                         double *total_seconds) {
+    DC_API_BEGIN
+    DC_REQUIRE(layers && grids && n > 0 && world >= 1 && fix_pn >= 0, DC_ERR_ARG, "bad arguments");
+    std::vector<ConvGeom> L;
+    std::vector<std::array<int, 2>> par;
+    for (int i = 0; i < n; ++i) {
+        const dc_layer_t &l = layers[i];
+        L.push_back(make_geom(l.N, l.C, l.H, l.W, l.F, l.K, l.stride, l.pad));
+        par.push_back({l.parent, l.parent2});
+        for (int p : par.back())
+            if (p >= 0) {
+                DC_REQUIRE(p < i, DC_ERR_ARG, "layer %d: parent %d must come earlier", i, p);
+                DC_REQUIRE(L[p].N == L[i].N && L[p].F == L[i].C && L[p].Ho == L[i].H && L[p].Wo == L[i].W,
+                           DC_ERR_SHAPE, "layer %d does not read layer %d's output shape", i, p);
+            }
+    }
+    std::vector<Grid> out;
+    const double t = model_strategy(L, par, world, fix_pn, out);
+    for (int i = 0; i < n; ++i) grids[i] = dc_decomp_t{out[i].pn, out[i].ph, out[i].pw};
+    if (total_seconds) *total_seconds = t;
+    DC_API_END
+}
 
 extern "C" dc_status_t dc_model_set_comm(double alpha, double beta) {
     DC_API_BEGIN
