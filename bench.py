@@ -271,6 +271,8 @@ def main():
                     help="spatial (model picks pH x pW, pN = 1: BASELINE configs[3]) | auto (model, all grids) | "
                          "pn,ph,pw (0 entries: model's choice)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="ablation: finish each halo exchange before the conv (DC_NO_OVERLAP)")
     ap.add_argument("--dtype", default="bf16", choices=["bf16", "fp32"],
                     help="bf16: bf16 x bf16 -> fp32 (DC_BF16); fp32: the paper's single precision via 3xTF32 "
                          "(DC_FP32_3XTF32)")
@@ -326,6 +328,8 @@ def main():
     # dW allreduces are queued on the communicator's gradient stream and joined
     # once at the end of the step (overlapped with later layers)
     FLAGS = dc.DC_EXCHANGE | dc.DC_ALLREDUCE | halo_flag | (0 if args.ar_sync else dc.DC_ALLREDUCE_ASYNC)
+    if args.no_overlap:
+        FLAGS |= dc.DC_NO_OVERLAP
     ablate = set(a for a in args.ablate.split(",") if a)  # diagnostics only: the JSON says so
     if "exchange" in ablate:
         FLAGS &= ~dc.DC_EXCHANGE
@@ -674,7 +678,7 @@ def main():
                        "parallelism": {"auto": "per-layer model-chosen (pN,pH,pW)",
                                        "spatial": "pure spatial, per-layer model-chosen (1,pH,pW)"}.get(
                                            args.decomp, args.decomp),
-                       "halo": args.halo, "l2": "working set per step > L2 (126 MB); no explicit flush",
+                       "halo": args.halo + ("+no-overlap" if args.no_overlap else ""), "l2": "working set per step > L2 (126 MB); no explicit flush",
                        "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
                        "perf_model_comm": MODEL_COMM,
                        "cuda_graph": use_graph, "dw_allreduce": "sync" if args.ar_sync else "async (joined at step end)",

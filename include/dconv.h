@@ -105,6 +105,10 @@ typedef struct dc_plan_s *dc_plan_t;
                                   communicator's gradient stream instead of joining it
                                   into the call (overlaps the later layers' work,
                                   PAPER.md:204, 214); dW is final after dc_comm_sync */
+#define DC_NO_OVERLAP    0x80u /* with DC_EXCHANGE (conv_fwd / conv_bwd_data): finish the halo
+                                  exchange on the caller's stream, then compute the whole
+                                  shard in one pass -- the non-overlapped schedule of the
+                                  performance model (no overlap)      */
 #define DC_DEFAULT_FLAGS (DC_EXCHANGE | DC_ALLREDUCE)
 
 /* COLLECTIVE. Create the communicator of `world` ranks. nccl_uid128 points to

@@ -336,9 +336,8 @@ int pick_bkc(int64_t cin_p) { return cin_p % 64 == 0 ? 64 : cin_p % 32 == 0 ? 32
 // M = 128 needs N % 16 == 0; fp32 plans pad channels only to 8, the extra
 // weight rows are TMA zero fill and the epilogue stores only nout_p)
 int pick_bn(int64_t nout_p) {
-    static const int cap = std::getenv("DC_V2_BN") ? std::atoi(std::getenv("DC_V2_BN")) : 256;
     const int64_t n16 = round_up(nout_p, 16);
-    return n16 <= cap ? (int)n16 : cap;
+    return n16 <= 256 ? (int)n16 : 256;
 }
 int pick_stages(int bkc, int bn) {
     const int stage = 128 * bkc * 2 + bn * bkc * 2;
@@ -447,8 +446,6 @@ struct GemmLaunch {
     int bn_slot = 0, bn_slot_cap = 0;
     bool bn_ok = true;
     int dep[4] = {0, 0, 0, 0};       // output rows/cols reading the halo: top, bottom, left, right
-    const P2PExchange *halo = nullptr;  // fused P2P exchange (conv_v2 warp 6)
-    int halo_rect0 = 0;
     int subpix = 0, sub_cp = 0, out_hmax = 0, out_wmax = 0;  // sub-pixel backward-data
     float *ws = nullptr;       // its fp32 partials
     int ws_h = 0, ws_w = 0;
@@ -466,9 +463,7 @@ OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
 // Split-K over channel groups for the v2 kernel, chosen from the GLOBAL problem
 // (tiles of the unpartitioned layer) so that every decomposition sums each
 // output element in the same order (partitioned == 1 GPU, bitwise).
-bool use_v1();
 int choose_ksplit(int64_t global_tiles, int64_t cin_p) {
-    if (use_v1()) return 1;
     const int ncg = (int)(cin_p / pick_bkc(cin_p));
     int k = 1;
     while (2 * k <= ncg && ncg % (2 * k) == 0 && global_tiles * 2 * k <= device_sm_count() * 3 / 2) k *= 2;
@@ -555,11 +550,6 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
 
 // Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
 // box shape is baked into the tensor map).
-bool use_v1() {
-    static const int v = std::getenv("DC_CONV_V1") ? 1 : 0;
-    return v != 0;
-}
-
 // The persistent tile-reuse kernel (conv_v2.cu); false if it does not apply.
 // One launch of the persistent tile-reuse kernel (conv_v2.cu) over `rects`
 // with tile shape 2^twl columns; false if the configuration does not fit.
@@ -576,7 +566,6 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.cin_p = (int)cin_p;
     q.ksplit = L.ksplit;
     q.kind = L.kind, q.a_seg = L.a_seg, q.out_f32 = L.out_f32 ? 1 : 0;
-    if (L.halo) q.halo = 1, q.hx = *L.halo, q.halo_rect0 = L.halo_rect0;
     q.subpix = L.subpix, q.sub_cp = L.sub_cp, q.out_hmax = L.out_hmax, q.out_wmax = L.out_wmax;
     q.ws = L.ws;
     q.ws_h = L.ws_h;
@@ -682,7 +671,7 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
 // Thin rects (boundary strips of an H split) use 1 x 128 tiles, the rest 16 x 8.
 bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
                      const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
-    if (use_v1() || L.p.T == 0) return false;
+    if (L.p.T == 0) return false;
     std::vector<OutRect> tall, thin;
     for (auto &r : rects)
         (L.p.s_in == 1 && r.nh < 8 && r.nw >= 64 ? thin : tall).push_back(r);
@@ -715,34 +704,6 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
 P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf);
 bool is_local(const dc_plan_s *pl);
 void resolve_local_peers(dc_plan_s *pl);
-
-// Forward with the P2P halo exchange fused into the single conv_v2 launch:
-// tile-aligned rects (16 x 8 tiles, pairs of 32 rows) with the interior first
-// and the bands whose outputs read the halo last. False: not applicable.
-bool fused_fwd(dc_plan_s *pl, GemmLaunch &L, void *x, const dc_shard_desc_t &xd, int nl, cudaStream_t st) {
-    // opt-in (DC_FUSED_HALO=1): measured slower than the two-stream overlap at
-    // 2 and 4 GPUs because 32-row tile pairs put up to half a thin shard into
-    // the halo-dependent bands
-    static const bool on = std::getenv("DC_FUSED_HALO") != nullptr;
-    if (!on || use_v1() || L.p.T == 0 || L.kind != 0) return false;
-    const int ho = (int)pl->rp.h.out.size(), wo = (int)pl->rp.w.out.size();
-    const int rt = std::min(ho, (int)round_up(L.dep[0], 32));
-    const int ie = rt + 32 * std::max(0, (ho - L.dep[1] - rt) / 32);
-    const int cl = std::min(wo, (int)round_up(L.dep[2], 8));
-    const int je = cl + 8 * std::max(0, (wo - L.dep[3] - cl) / 8);
-    std::vector<OutRect> rects;
-    if (ie > rt && je > cl) rects.push_back(OutRect{rt, cl, ie - rt, je - cl});
-    const int r0 = (int)rects.size();
-    for (const OutRect &r : {OutRect{0, 0, rt, wo}, OutRect{ie, 0, ho - ie, wo}, OutRect{rt, 0, ie - rt, cl},
-                             OutRect{rt, je, ie - rt, wo - je}})
-        if (r.nh > 0 && r.nw > 0) rects.push_back(r);
-    const P2PExchange hx = build_p2p(pl, 0, x);
-    L.halo = &hx;
-    L.halo_rect0 = r0;
-    const bool ok = launch_v2_shape(L, rects, 3, x, xd, L.cin, nl, st);
-    L.halo = nullptr;
-    return ok;
-}
 
 // The P2P protocol of one exchange of tensor `which` (0: x, 1: dy) of the
 // registered buffer `buf`: my slabs -> the neighbours' mapped margins, their
@@ -983,9 +944,7 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
                          bool *exchanged) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
-    static const bool off = std::getenv("DC_NO_SUBPIX") != nullptr;
-    static const int max_c = std::getenv("DC_SUBPIX_MAXC") ? std::atoi(std::getenv("DC_SUBPIX_MAXC")) : 32;
-    if (off || use_v1() || g.dt != 0 || g.S != 2 || g.Cp > max_c || 4 * g.Cp > 256) return false;
+    if (g.dt != 0 || g.S != 2 || g.Cp > 32) return false;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
     const int K = g.K, P = g.P;
     const int dmin = -(int)floor_div(K - 1 - P, 2), dmax = (int)floor_div(P + 1, 2);
@@ -1147,7 +1106,9 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             const OutRect b = whole(L[i]);
             L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2 + ks_off[i] / sizeof(float);
         }
-    const bool overlap = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
+    const bool need_dy = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
+    if (need_dy && (flags & DC_NO_OVERLAP)) exchange(pl, 1, dy, flags, st);  // exchange, then compute
+    const bool overlap = need_dy && !(flags & DC_NO_OVERLAP);
     if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
@@ -1155,8 +1116,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     }
     int nactive = 0;
     for (auto &f : ph) nactive += f.active ? 1 : 0;
-    static const bool serial_phases = std::getenv("DC_SERIAL_PHASES") != nullptr;
-    if (!overlap && nactive > 1 && !serial_phases && pl->s_ph[0]) {
+    if (!overlap && nactive > 1 && pl->s_ph[0]) {
         // stride phases are independent GEMMs with disjoint outputs and split-K
         // workspaces: one stream each, so their ramp-up / tail / reduce overlap
         CK(cudaEventRecord(pl->ev_ph[0], st));
@@ -1202,7 +1162,7 @@ int wgrad_splits(const WgradV2Params &q, int ctas, long long per_split, bool all
     const int nks = q.kind == 1 ? 8 : q.bw / 2;  // MMAs per block and M tile (K = 8 tf32 / 16 bf16)
     const double mma_ns = nks * q.G * (27.0 + 0.41 * q.bn) / 1.9;
     const double stage_bytes = q.x_stage_bytes + q.dy_stage_bytes;
-    static const double sm_gbs = std::getenv("DC_WGRAD_SM_GBS") ? std::atof(std::getenv("DC_WGRAD_SM_GBS")) : 40.0;
+    const double sm_gbs = 40.0;  // (re-swept in round 2: 25 / 60 / 100 no better, tools/gbs_sweep.sh)
     int best = 1;
     bool best_atomic = false;
     double best_t = 1e30;
@@ -1245,7 +1205,7 @@ void run_bwd_filter(dc_plan_s *pl, const void *x, const void *dy, float *dw, cud
     // dy WITHOUT its halo: maps over the owned block only
     const void *dy_owned = reinterpret_cast<const uint8_t *>(dy) +
                            (size_t)(dyd.halo_n * dyd.wb + dyd.halo_w) * dyd.c_pad * esz;
-    if (!use_v1() && (f32 || g.Fp % 64 == 0)) {
+    if (f32 || g.Fp % 64 == 0) {
         // tile-reuse kernel (wgrad_v2.cu)
         WgradV2Params q;
         std::memset(&q, 0, sizeof q);
@@ -1498,10 +1458,9 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
                 CK(cudaMemset(pl->dev_epochs, 0, sizeof(uint32_t) * 4));
                 pl->buf[0].dev_epoch = pl->dev_epochs;
                 pl->buf[1].dev_epoch = pl->dev_epochs + 2;
-                // the BN group's one-shot NVLink mailbox (<= 8 members; NCCL beyond,
-                // or with DC_BN_NCCL on real ranks)
+                // the BN group's one-shot NVLink mailbox (<= 8 members; NCCL beyond)
                 const int gsz = pl->bn_group;
-                if (gsz > 1 && gsz <= kMaxBnGroup && (local || !std::getenv("DC_BN_NCCL"))) {
+                if (gsz > 1 && gsz <= kMaxBnGroup) {
                     const size_t bytes = 256 + (size_t)2 * gsz * 2 * g.Fp * sizeof(double);
                     CK(cudaMalloc(&pl->bn_mail, bytes));
                     CK(cudaMemset(pl->bn_mail, 0, bytes));
@@ -1884,13 +1843,10 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     const dc_shard_desc_t xd = describe(pl->rp, DC_X);
     const int nl = (int)pl->rp.nrange.size();
     const bool need_x = (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
-    static const int no_overlap_env = std::getenv("DC_NO_OVERLAP") ? std::atoi(std::getenv("DC_NO_OVERLAP")) : 0;
-    const bool overlap = need_x && !no_overlap_env;
+    const bool overlap = need_x && !(flags & DC_NO_OVERLAP);
     if (need_x && !overlap) {  // exchange, then one launch over the whole shard
         exchange(pl, 0, x, flags, st);
         launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);
-    } else if (overlap && !(flags & DC_HALO_NCCL) && fused_fwd(pl, L, x, xd, nl, st)) {
-        // one kernel: P2P halo stores + interior tiles, halo-dependent tiles last
     } else if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
@@ -1898,13 +1854,9 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         // interior tiles on the caller's stream, concurrently with the exchange;
         // the halo-dependent boundary tiles right after it on the comm stream
         // (disjoint outputs, and disjoint split-K workspace pixels), joined below.
-        // DC_HALO_RESERVE=k caps the persistent interior grid at SMs - k so the
-        // exchange and the boundary kernel can run beside it.
-        // (measured neutral at 4 GPUs with 8 or 16 reserved SMs: default 0)
-        static const int reserve = std::getenv("DC_HALO_RESERVE") ? std::atoi(std::getenv("DC_HALO_RESERVE")) : 0;
-        L.max_ctas = std::max(1, device_sm_count() - reserve);
+        // (capping the interior grid to leave SMs to the exchange measured
+        // neutral at 4 GPUs with 8 or 16 reserved SMs)
         launch_rects(L, L.interior, x, xd, L.cin, nl, st);
-        L.max_ctas = 0;
         launch_rects(L, L.boundary, x, xd, L.cin, nl, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));

@@ -13,8 +13,6 @@
 //               global stores (+ fused BN statistics); double-buffered TMEM
 //               accumulators let the epilogue of tile i overlap the MMAs of
 //               tile i+1.
-//   warp 6      fused P2P halo exchange (opt-in, ConvV2Params::halo): slices
-//               of this rank's slabs stored into the neighbours' margins.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -69,42 +67,38 @@ constexpr int kMaxBar = 16;
 // one tcgen05.mma of the kernel's CTA group (1: this SM; 2: the pair, M = 256)
 // KIND 0: kind::f16 (bf16 x bf16 -> fp32); KIND 1: kind::tf32 (fp32 operands
 // read as tf32, 8 per 32-byte K step: the same smem geometry as 16 bf16)
-template <int CG, int KIND>
-__device__ __forceinline__ void mma_cg(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    if constexpr (KIND == 1) {
-        static_assert(CG == 1, "tf32 kernels run on single CTAs");
+template <int KIND>
+__device__ __forceinline__ void mma_k(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    if constexpr (KIND == 1)
         mma_tf32(d, a, b, idesc, acc);
-    } else if constexpr (CG == 2) {
-        mma_bf16_cg2(d, a, b, idesc, acc);
-    } else {
+    else
         mma_bf16(d, a, b, idesc, acc);
-    }
 }
 
 // Streamed weights: the MMAs of one weight slot (one tap of one channel group):
 // NK x K16 steps for each of TPW stacked tiles, fully unrolled (compile-time
 // multiples of hoisted strides, no per-MMA descriptor arithmetic chains).
-template <int CG, int KIND, int NK, int TPW>
+template <int KIND, int NK, int TPW>
 __device__ __forceinline__ void issue_slot(uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t a_kstep,
                                            uint32_t a_tile16, uint32_t acc_cols, uint32_t idesc, bool first) {
 #pragma unroll
     for (int k16 = 0; k16 < NK; ++k16)
 #pragma unroll
         for (int tt = 0; tt < TPW; ++tt)
-            mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
+            mma_k<KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16, bd + 2 * k16, idesc,
                        (first && k16 == 0) ? 0u : 1u);
 }
-template <int CG, int KIND>
+template <int KIND>
 __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tmem, uint64_t ad, uint64_t bd,
                                                uint32_t a_kstep, uint32_t a_tile16, uint32_t acc_cols,
                                                uint32_t idesc, bool first) {
     switch ((nk16 << 4) | tpw) {
-    case 0x41: issue_slot<CG, KIND, 4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x42: issue_slot<CG, KIND, 4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x21: issue_slot<CG, KIND, 2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x22: issue_slot<CG, KIND, 2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    case 0x11: issue_slot<CG, KIND, 1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
-    default: issue_slot<CG, KIND, 1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x41: issue_slot<KIND, 4, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x42: issue_slot<KIND, 4, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x21: issue_slot<KIND, 2, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x22: issue_slot<KIND, 2, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    case 0x11: issue_slot<KIND, 1, 1>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
+    default: issue_slot<KIND, 1, 2>(d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc, first); break;
     }
 }
 
@@ -113,7 +107,7 @@ __device__ __forceinline__ void issue_slot_any(int nk16, int tpw, uint32_t d_tme
 // stride hoisted out of the loop, so the single issuing thread spends a few
 // uniform instructions per tcgen05.mma instead of a dependent chain of
 // constant loads and 64-bit adds per tap (measured: ~180 cycles per tap).
-template <int CG, int KIND, int KH, int KW, int NK, int SSH, int TPW>
+template <int KIND, int KH, int KW, int NK, int SSH, int TPW>
 __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, uint64_t bd,
                                            uint32_t a_row16, uint32_t a_col16, uint32_t a_par16,
                                            uint32_t a_kstep, uint32_t b_slot16, uint32_t idesc,
@@ -129,13 +123,13 @@ __device__ __forceinline__ void issue_taps(uint32_t d_tmem, uint64_t a_stage, ui
             for (int k = 0; k < NK; ++k)
 #pragma unroll
                 for (int tt = 0; tt < TPW; ++tt)  // the tiles of the work item share the B slice
-                    mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
+                    mma_k<KIND>(d_tmem + tt * acc_cols, ad + (uint32_t)k * a_kstep + tt * a_tile16, b + 2 * k,
                                idesc, (first_group && th == 0 && tw == 0 && k == 0) ? 0u : 1u);
         }
 }
 
 // Dispatch to an unrolled specialisation; false if none matches.
-template <int CG, int KIND>
+template <int KIND>
 __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16, uint32_t d_tmem,
                                                  uint64_t a_stage, uint64_t bd, uint32_t a_kstep,
                                                  uint32_t b_slot16, uint32_t idesc, bool first,
@@ -143,11 +137,11 @@ __device__ __forceinline__ bool issue_taps_fixed(const ConvV2Params &p, int nk16
     const int key = (p.tpw << 16) | (p.kh << 12) | (p.kw << 8) | (nk16 << 4) | p.s_shift;
 #define DC_TAPS(KH, KW, NK, SS)                                                                   \
     case ((1 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<CG, KIND, KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<KIND, KH, KW, NK, SS, 1>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;                                                                              \
     case ((2 << 16) | (KH << 12) | (KW << 8) | (NK << 4) | SS):                                   \
-        issue_taps<CG, KIND, KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
+        issue_taps<KIND, KH, KW, NK, SS, 2>(d_tmem, a_stage, bd, p.a_row16, p.a_col16, p.a_par16,        \
                                       a_kstep, b_slot16, idesc, first, acc_cols, a_tile16);       \
         return true;
     switch (key) {
@@ -189,18 +183,15 @@ __device__ __forceinline__ void warp_chunk_reduce(float (&a)[16], float (&q)[16]
     }
 }
 
-// warp 0 TMA, 1 MMA, 2-5 epilogue, 6 fused halo exchange, 7-10 second epilogue
-// group (p.epi2: the two groups split each tile's 16-column chunks, so twice as
-// many TMEM loads and stores are in flight; the other warps idle when !epi2)
+// warp 0 TMA, 1 MMA, 2-5 epilogue, 7-10 second epilogue group (p.epi2: the
+// two groups split each tile's 16-column chunks, so twice as many TMEM loads
+// and stores are in flight; warp 6 and, without epi2, 7-10 idle)
 constexpr int kV2Threads = 352;
 
-// CG = 2: CTA pairs run tcgen05 with cta_group::2 (M = 256 per MMA; each CTA
-// holds its own A tile and half of every weight slot; the leader issues).
-template <int CG, int KIND>
+template <int KIND>
 __global__ void __launch_bounds__(kV2Threads, 1)
     conv_v2_kernel(const __grid_constant__ CUtensorMap amap, const __grid_constant__ CUtensorMap bmap,
                    const __grid_constant__ ConvV2Params p) {
-    constexpr bool PAIR = CG == 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = align1024(smem_raw);
     uint8_t *sB = smem;  // B first: its slots need 1024-byte alignment (swizzle)
@@ -223,30 +214,23 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     const uint32_t buf_cols = p.tpw * acc_cols;
     const uint32_t ncols = NB * buf_cols;
 
-    // PAIR: the leader's full barriers collect both CTAs' loads (2 arrivals),
-    // its accumulator-empty barriers both CTAs' epilogue warps (8)
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.a_stages; ++s) {
-            mbar_init(&a_full[s], PAIR ? 2 : 1);
+            mbar_init(&a_full[s], 1);
             mbar_init(&a_empty[s], 1);
         }
         for (int s = 0; s < p.b_stages; ++s) {
-            mbar_init(&b_full[s], PAIR ? 2 : 1);
-            mbar_init(&b_empty[s], PAIR ? 1 : p.cluster);  // released by the MMAs of every CTA that reads it
+            mbar_init(&b_full[s], 1);
+            mbar_init(&b_empty[s], p.cluster);  // released by the MMAs of every CTA that reads it
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&acc_full[s], 1);
-            mbar_init(&acc_empty[s], (PAIR ? 2 : 1) * (p.epi2 ? 8 : 4));
+            mbar_init(&acc_empty[s], p.epi2 ? 8 : 4);
         }
-        mbar_init(b_res, PAIR ? 2 : 1);
+        mbar_init(b_res, 1);
         fence_mbar_init();
     }
-    if (warp == 1) {
-        if constexpr (PAIR)
-            tmem_alloc_cg2(tmem_slot, ncols);
-        else
-            tmem_alloc(tmem_slot, ncols);
-    }
+    if (warp == 1) tmem_alloc(tmem_slot, ncols);
     tc_fence_before();
     if (p.cluster > 1)
         cluster_sync();  // the partner's barriers exist before any multicast reaches them
@@ -257,20 +241,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
     // everything above touched only this CTA's smem / TMEM: with PDL it overlaps
     // the previous kernel's tail; global memory only after its completion
     pdl_wait();
-    // fused halo exchange: this launch's epoch (published by the last CTA at exit)
-    const uint32_t halo_e = p.halo ? *reinterpret_cast<volatile uint32_t *>(p.hx.epoch_ctr) + 1 : 0u;
     // Work units: a CTA (cluster == 1) or a CTA pair (cluster == 2: tiles 2k and
     // 2k+1 of the same N tile, each CTA loading half of every weight stage and
     // multicasting it to both; an odd tail tile gives the second CTA a phantom
     // copy of its partner's tile whose results are not stored).
     const int cl = p.cluster;
     const uint32_t cr = cl > 1 ? cluster_ctarank() : 0;
-    const bool leader = cr == 0;
-    // PAIR: arrive-with-bytes on the leader's barrier (remote for CTA 1)
-    auto expect_lead = [&](uint64_t *bar, uint32_t bytes) {
-        if (leader) mbar_arrive_expect_tx(bar, bytes);
-        else mbar_arrive_expect_tx_cluster(mapa_u32(smem_u32(bar), 0), bytes);
-    };
     const int ks = p.ksplit;
     const int unit = blockIdx.x / cl;
     const int split = unit % ks;
@@ -299,34 +275,17 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         }
         int cur_o0 = -1;
         int a_it = 0, b_it = 0;
-        bool halo_ready = !p.halo;
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
             const TileCoord c = decode(p, item_of(w, phantom));
-            if (!halo_ready && c.r >= p.halo_rect0) {
-                // the neighbours' slabs of this epoch are in my margins
-                if ((int)lane < p.hx.n_data_in) spin_until_geq(p.hx.data_in[lane], kP2PBlocks * halo_e);
-                __syncwarp();
-                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-                halo_ready = true;
-            }
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {
-                    if constexpr (PAIR) {  // my half (bn/2 rows) of every slot
-                        expect_lead(b_res, p.T * (g1 - g0) * (p.bn / 2) * p.cg * 2);
-                        const uint32_t lb = mapa_u32(smem_u32(b_res), 0);
-                        for (int g = g0; g < g1; ++g)
-                            for (int t = 0; t < p.T; ++t)
-                                tma_load_2d_cg2(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, lb,
-                                                t * p.cin_p + g * p.cg, c.o0 + (int)cr * (p.bn / 2));
-                    } else {
-                        mbar_arrive_expect_tx(b_res, p.T * (g1 - g0) * p.bn * p.cg * 2);
-                        for (int g = g0; g < g1; ++g)
-                            for (int t = 0; t < p.T; ++t)
-                                tma_load_2d(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, b_res,
-                                            t * p.cin_p + g * p.cg, c.o0);
-                    }
+                    mbar_arrive_expect_tx(b_res, p.T * (g1 - g0) * p.bn * p.cg * 2);
+                    for (int g = g0; g < g1; ++g)
+                        for (int t = 0; t < p.T; ++t)
+                            tma_load_2d(sB + ((g - g0) * p.T + t) * p.b_slot_bytes, &bmap, b_res,
+                                        t * p.cin_p + g * p.cg, c.o0);
                 }
                 __syncwarp();
                 cur_o0 = c.o0;
@@ -342,22 +301,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 if (p.a_seg > 0 && a_c >= p.a_seg) a_c -= p.a_seg;
                 if (elect_one()) {
                     uint8_t *dst = sA + s * p.a_stage_bytes;
-                    if ((p.dbg & 1) && a_it >= p.a_stages) {
-                        mbar_arrive(&a_full[s]);
-                    } else if (PAIR) {  // my tile, completing on the leader's barrier
-                        const uint32_t lb = mapa_u32(smem_u32(&a_full[s]), 0);
-                        if (p.a_swz) {
-                            expect_lead(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
-                            for (int par = 0; par < p.s_in; ++par)
-                                tma_load_4d_cg2(dst + par * p.plane_bytes, &amap, lb, a_c, w0 + par, h0, c.n);
-                        } else {
-                            expect_lead(&a_full[s], (p.cg / 8) * p.s_in * p.PH * p.PWs * 16);
-                            for (int k8 = 0; k8 < p.cg / 8; ++k8)
-                                for (int par = 0; par < p.s_in; ++par)
-                                    tma_load_4d_cg2(dst + (k8 * p.s_in + par) * p.plane_bytes, &amap, lb,
-                                                    a_c + k8 * 8, w0 + par, h0, c.n);
-                        }
-                    } else if (p.a_swz) {
+                    if (p.a_swz) {
                         // one box per column parity: PH rows x PWs cols x cg channels
                         mbar_arrive_expect_tx(&a_full[s], p.s_in * p.PH * p.PWs * p.cg * 2);
                         for (int par = 0; par < p.s_in; ++par)
@@ -378,11 +322,6 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const int sb = b_it % p.b_stages;
                         if (b_it >= p.b_stages) mbar_wait(&b_empty[sb], ((b_it / p.b_stages) - 1) & 1);
                         if (elect_one()) {
-                            if constexpr (PAIR) {  // my half of the slot, in my smem
-                                expect_lead(&b_full[sb], (p.bn / 2) * p.cg * 2);
-                                tma_load_2d_cg2(sB + sb * p.b_slot_bytes, &bmap, mapa_u32(smem_u32(&b_full[sb]), 0),
-                                                t * p.cin_p + g * p.cg, c.o0 + (int)cr * (p.bn / 2));
-                            } else {
                             mbar_arrive_expect_tx(&b_full[sb], p.bn * p.cg * 2);
                             if (cl > 1)  // my half of the slot, into both CTAs
                                 tma_load_2d_mc(sB + sb * p.b_slot_bytes + cr * (p.bn / 2) * p.cg * 2, &bmap,
@@ -391,7 +330,6 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                             else
                                 tma_load_2d(sB + sb * p.b_slot_bytes, &bmap, &b_full[sb],
                                             t * p.cin_p + g * p.cg, c.o0);
-                            }
                         }
                         __syncwarp();
                         ++b_it;
@@ -400,19 +338,12 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             }
         }
     } else if (warp == 1) {
-      if (!PAIR || leader) {  // (the non-leader's warp 1 only owns TMEM)
         // ============ tcgen05.mma issuer: warp-uniform loop, elected lane issues ============
-        // (PAIR: the leader issues for both CTAs; its commits multicast to both)
-        auto commit = [&](uint64_t *bar) {
-            if constexpr (PAIR)
-                mma_commit_cg2(bar, 0x3);
-            else
-                mma_commit(bar);
-        };
+        auto commit = [&](uint64_t *bar) { mma_commit(bar); };
         // Descriptor arithmetic: the start-address field is bits [0,14) in 16-byte
         // units and never carries (smem < 256 KB), so an operand at byte offset
         // `off` from a base descriptor is base + (off >> 4).
-        const uint32_t idesc = KIND == 1 ? idesc_tf32(128, p.bn, 0, 0) : idesc_bf16(PAIR ? 256 : 128, p.bn, 0, 0);
+        const uint32_t idesc = KIND == 1 ? idesc_tf32(128, p.bn, 0, 0) : idesc_bf16(128, p.bn, 0, 0);
         const uint32_t sA_u = smem_u32(sA), sB_u = smem_u32(sB);
         const uint64_t a_desc0 = p.a_swz ? smem_desc(sA_u, 16, p.a_sbo, swizzle_layout(p.a_swz))
                                                 : smem_desc(sA_u, p.s_in * p.plane_bytes, p.a_sbo, 0);
@@ -421,7 +352,6 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         // second tile of a work item: 16 output rows (= 16 SBO strides) further down
         const uint32_t a_tile16 = (16 * p.a_sbo) >> 4;
         const int nk16 = p.cg / 16;
-        const bool do_mma = !(p.dbg & 4);
         int a_it = 0, b_it = 0, acc_it = 0;
         bool res_ready = false;
         for (int w = w0_; w < total_w; w += w_step) {
@@ -430,23 +360,19 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 res_ready = true;
             }
             const int acc = acc_it % NB;
-            const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && lane == 0;
-            if (tr) p.dbg_out[acc_it * 8 + 0] = clock64();
             if (acc_it >= NB) mbar_wait(&acc_empty[acc], ((acc_it / NB) - 1) & 1);
-            if (tr) p.dbg_out[acc_it * 8 + 1] = clock64();
             tc_fence_after();
             const uint32_t d_tmem = tmem + acc * buf_cols;
             for (int g = g0; g < g1; ++g) {
                 const int s = a_it % p.a_stages;
                 mbar_wait(&a_full[s], (a_it / p.a_stages) & 1);
-                if (tr && g == 0) p.dbg_out[acc_it * 8 + 2] = clock64();
                 tc_fence_after();
                 const uint64_t a_stage = a_desc0 + ((uint32_t)(s * p.a_stage_bytes) >> 4);
                 if (p.b_resident) {
                     if (elect_one()) {
                         uint64_t bd = b_desc0 + (uint32_t)((g - g0) * p.T) * b_slot16;
-                        if (!do_mma || !issue_taps_fixed<CG, KIND>(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16,
-                                                             idesc, g == g0, acc_cols, a_tile16)) {
+                        if (!issue_taps_fixed<KIND>(p, nk16, d_tmem, a_stage, bd, a_kstep, b_slot16, idesc, g == g0,
+                                                    acc_cols, a_tile16)) {
                         uint64_t arow = a_stage;
                         for (int th = 0; th < p.kh; ++th) {
                             for (int tw = 0; tw < p.kw; ++tw) {
@@ -454,9 +380,8 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                                                     (uint32_t)(tw & p.s_shift) * p.a_par16;
                                 for (int k16 = 0; k16 < nk16; ++k16)
                                     for (int tt = 0; tt < p.tpw; ++tt)
-                                        if (do_mma)
-                                            mma_cg<CG, KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
-                                                       bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
+                                        mma_k<KIND>(d_tmem + tt * acc_cols, ad + k16 * a_kstep + tt * a_tile16,
+                                                    bd + 2 * k16, idesc, ((g - g0) | th | tw | k16) != 0);
                                 bd += b_slot16;
                             }
                             arow += p.a_row16;
@@ -479,12 +404,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                         const uint64_t bd = b_desc0 + (uint32_t)sb * b_slot16;
                         const bool first = g == g0 && t == 0;
                         if (elect_one()) {
-                            if (do_mma)
-                                issue_slot_any<CG, KIND>(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
-                                                   first);
-                            if (PAIR)
-                                commit(&b_empty[sb]);
-                            else if (cl > 1)
+                            issue_slot_any<KIND>(nk16, p.tpw, d_tmem, ad, bd, a_kstep, a_tile16, acc_cols, idesc,
+                                                 first);
+                            if (cl > 1)
                                 mma_commit_mc(&b_empty[sb], 0x3);  // the slot is shared by both CTAs
                             else
                                 mma_commit(&b_empty[sb]);
@@ -501,39 +423,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             }
             if (elect_one()) commit(&acc_full[acc]);
             __syncwarp();
-            if (tr) p.dbg_out[acc_it * 8 + 3] = clock64();
             ++acc_it;
-        }
-      }
-    } else if (warp == 6) {
-        // ===================== fused P2P halo exchange (slices) =====================
-        if (p.halo) {
-            const P2PExchange &x = p.hx;
-            if (blockIdx.x == 0 && (int)lane < x.n_ready_out) {  // my margins are free for epoch e
-                __threadfence_system();
-                asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(x.ready_out[lane]), "r"(halo_e) : "memory");
-            }
-            for (int sl = blockIdx.x; sl < kP2PBlocks; sl += gridDim.x) {
-                if ((int)lane < x.n_ready_in) spin_until_geq(x.ready_in[lane], halo_e);
-                __syncwarp();
-                for (int k = 0; k < x.copies.count; ++k) {
-                    const BlockCopy &cp = x.copies.c[k];
-                    const long long run = (long long)cp.cols * cp.vec16;
-                    const long long tot = (long long)cp.nn * cp.rows * run;
-                    const long long hi = tot * (sl + 1) / kP2PBlocks;
-                    for (long long idx = tot * sl / kP2PBlocks + lane; idx < hi; idx += 32) {
-                        const long long nr = idx / run, kk = idx - nr * run;
-                        const int n = (int)(nr / cp.rows), r = (int)(nr - (long long)n * cp.rows);
-                        const int col = (int)(kk / cp.vec16), v = (int)(kk - (long long)col * cp.vec16);
-                        cp.dst[n * cp.d_sn + r * cp.d_sh + col * cp.d_sw + v] =
-                            cp.src[n * cp.s_sn + r * cp.s_sh + col * cp.s_sw + v];
-                    }
-                }
-                __syncwarp();
-                __threadfence_system();
-                __syncwarp();
-                if ((int)lane < x.n_data_out) atomicAdd_system(x.data_out[lane], 1u);
-            }
         }
     } else if (warp < 6 || p.epi2) {
         // ========================= epilogue =========================
@@ -640,12 +530,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 }
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) {
-                    if (PAIR && !leader)
-                        mbar_arrive_cluster(mapa_u32(smem_u32(&acc_empty[acc]), 0));
-                    else
-                        mbar_arrive(&acc_empty[acc]);
-                }
+                if (lane == 0) mbar_arrive(&acc_empty[acc]);
                 ++acc_it;
                 if (++since == 16) flush(), since = 0;
             }
@@ -664,10 +549,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                 seg_o0 = c.o0;
             }
             const int acc = acc_it % NB;
-            const bool tr = (p.dbg & 8) && blockIdx.x == 0 && acc_it < 64 && warp == 2 && lane == 0;
-            if (tr) p.dbg_out[acc_it * 8 + 4] = clock64();
             mbar_wait(&acc_full[acc], (acc_it / NB) & 1);
-            if (tr) p.dbg_out[acc_it * 8 + 5] = clock64();
             tc_fence_after();
             for (int tt = 0; tt < p.tpw; ++tt) {
             const int i = c.i0 + tt * 16 + ti, j = c.j0 + tj;
@@ -700,7 +582,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                     float *of = reinterpret_cast<float *>(p.out) + (long long)c.n * p.out_sn +
                                 (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
                                 (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0 + c16 * 16;
-                    if (valid && !(p.dbg & 2)) {
+                    if (valid) {
                         if (c.o0 + c16 * 16 < p.nout_p) st_global_v8(of, *reinterpret_cast<const uint32_t(*)[8]>(&v[0]));
                         if (c.o0 + c16 * 16 + 8 < p.nout_p)
                             st_global_v8(of + 8, *reinterpret_cast<const uint32_t(*)[8]>(&v[8]));
@@ -710,7 +592,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                     uint32_t pk[8];
 #pragma unroll
                     for (int e = 0; e < 8; ++e) pk[e] = pack2(v[2 * e], v[2 * e + 1]);
-                    if (st_ok && !(p.dbg & 2)) {
+                    if (st_ok) {
                         if (p.subpix) {  // this 16-channel chunk belongs to one stride phase
                             const int col = c.o0 + c16 * 16, ph = col / p.sub_cp, ch = col - ph * p.sub_cp;
                             const int row = p.out_h0 + p.out_dh * i + (ph >> 1);
@@ -779,13 +661,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             }  // tt
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) {
-                if (PAIR && !leader)  // the leader's MMA warp reuses this buffer of both CTAs
-                    mbar_arrive_cluster(mapa_u32(smem_u32(&acc_empty[acc]), 0));
-                else
-                    mbar_arrive(&acc_empty[acc]);
-            }
-            if (tr) p.dbg_out[acc_it * 8 + 6] = clock64();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);
             ++acc_it;
         }
         }  // (bn_stats != 2)
@@ -796,20 +672,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         cluster_sync();  // no CTA leaves while its partner may still multicast into it
     else
         __syncthreads();
-    if (warp == 1) {
-        if constexpr (PAIR)
-            tmem_dealloc_cg2(tmem, ncols);
-        else
-            tmem_dealloc(tmem, ncols);
-    }
-    if (p.halo && threadIdx.x == 0) {  // the last CTA publishes the epoch and resets the count
-        const uint32_t prev = atomicAdd(p.hx.epoch_ctr + 1, 1u);
-        if (prev == gridDim.x - 1) {
-            p.hx.epoch_ctr[1] = 0;
-            __threadfence();
-            *reinterpret_cast<volatile uint32_t *>(p.hx.epoch_ctr) = halo_e;
-        }
-    }
+    if (warp == 1) tmem_dealloc(tmem, ncols);
 }
 
 // ---------------------------------------------------------------------------
@@ -838,10 +701,8 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     if (p.tpw < 1) p.tpw = 1;
     if (TW != 8) p.tpw = 1;
     p.PH = p.s_in * (TH * p.tpw - 1) + kh;
-    static const bool force_planes = std::getenv("DC_V2_PLANES") != nullptr;
-    static const bool wide_pitch = std::getenv("DC_V2_PITCH16") != nullptr;
-    const int pitch = wide_pitch ? (TW == 8 ? 16 : 136) : TW + (kw - 1) / p.s_in;  // pixels per smem row
-    if (!force_planes && TW + (kw - 1) / p.s_in <= pitch && pitch * p.s_in <= 256) {
+    const int pitch = TW + (kw - 1) / p.s_in;  // pixels per smem row
+    if (pitch * p.s_in <= 256) {
         // swizzled rows of cg channels (32/64/128-byte swizzle), one plane per
         // column parity (TMA element stride = s_in). The swizzle is a function
         // of the absolute smem address (measured), so a tap shift only moves
@@ -876,16 +737,6 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.a_par16 = p.plane_bytes >> 4;
         p.a_kstep16 = (2 * p.s_in * p.plane_bytes) >> 4;
     }
-    // CTA pairs (cta_group::2, each CTA stages half of every weight slot),
-    // opt-in DC_V2_CG2=1: faster for streamed 128-wide weight tiles at stride 1
-    // with warm L2 (conv2_2 fwd 85 -> 69 us) but slower in the bench step with
-    // cold inputs (92 -> 128 us: the leader waits for the slower of two tile
-    // loads) and for 256-wide, resident or stride-2 tiles (round 2, resident
-    // 64-channel weights, cold L2: conv1_2 fwd 660 -> 735 us, bwd-data 639 ->
-    // 887 us; profiles/r2_cg2_resident_ab.txt)
-    static const bool cg2 = std::getenv("DC_V2_CG2") != nullptr;
-    const bool cand2 = cg2 && p.bn == 128 && p.s_in == 1 && p.kind == 0;
-    p.cta2 = 0;
     p.b_slot_bytes = (int)round_up((int64_t)p.bn * p.cg * 2, 1024);
     const int fixed = 1024 + (4 * kMaxBar + 5) * 8 + 16 + (p.bn_stats ? 4 * 2 * p.bn * 8 : 0);
     if (p.ksplit < 1 || p.ncg % p.ksplit) return false;
@@ -898,8 +749,7 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         p.a_stages = std::min(4, (smem_limit - fixed - resident_b) / p.a_stage_bytes);
         // resident weights: a work item of two stacked tiles halves the per-item
         // overheads (barriers, accumulator hand-off) and the A halo rows
-        static const bool res_pair = std::getenv("DC_V2_RES_TPW1") == nullptr;
-        if (res_pair && p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems && !std::getenv("DC_V2_TPW1")) {
+        if (p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems) {
             ConvV2Params q = p;
             q.tpw = 2;
             if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.b_resident && q.a_stages >= 2) p = q;
@@ -907,14 +757,6 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     } else {
         p.b_resident = 0;
         p.a_stages = 2;
-        if (cand2) {
-            p.cta2 = 1;
-            p.b_slot_bytes = (int)round_up((int64_t)(p.bn / 2) * p.cg * 2, 1024);
-            // half-size weight slots leave room for a deeper A ring: each stage
-            // waits for both CTAs' tile loads
-            static const int a2 = std::getenv("DC_V2_CG2_ASTAGES") ? std::atoi(std::getenv("DC_V2_CG2_ASTAGES")) : 3;
-            if (smem_limit - fixed - a2 * p.a_stage_bytes >= 4 * p.b_slot_bytes) p.a_stages = a2;
-        }
         p.b_stages = std::min(8, (smem_limit - fixed - p.a_stages * p.a_stage_bytes) / p.b_slot_bytes);
         if (p.b_stages < 2) {
             p.a_stages = 1;  // (cannot happen for cg <= 64, bn <= 256)
@@ -923,12 +765,12 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
         if (p.b_stages < 2) return false;
         // streamed weights: let a work item cover two stacked 16 x 8 tiles that
         // share every weight stage (halves the L2 weight traffic per FLOP)
-        if (p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems && !std::getenv("DC_V2_TPW1")) {
+        if (p.tpw == 1 && TW == 8 && p.work_hint >= kPairMinItems) {
             ConvV2Params q = p;
             q.tpw = 2;
             if (conv_v2_configure(q, smem_limit) && q.tpw == 2 && q.a_stages >= 2 && q.b_stages >= 2) {
                 p = q;
-            } else if (p.cg == 64 && p.s_in == 2 && p.allow_cg32 && !std::getenv("DC_V2_NO_CG32")) {
+            } else if (p.cg == 64 && p.s_in == 2 && p.allow_cg32) {
                 // stride 2: a 32-row stacked tile pair is too tall for 64-channel
                 // stages; 32-channel stages make it fit (same weight reuse)
                 q.cg = 32;
@@ -938,8 +780,9 @@ bool conv_v2_configure(ConvV2Params &p, int smem_limit) {
     }
     // streamed weights: CTA pairs multicast each weight stage (half each), which
     // halves the L2 -> SM weight traffic without reducing the number of CTAs
-    static const bool no_cluster = std::getenv("DC_V2_NO_CLUSTER") != nullptr;
-    p.cluster = p.cta2 ? 2 : (!p.b_resident && p.bn % 32 == 0 && !no_cluster && p.kind == 0) ? 2 : 1;
+    // (CTA pairs with cta_group::2 were measured slower in the step with cold
+    // inputs and resident weights -- profiles/r2_cg2_resident_ab.txt -- and removed)
+    p.cluster = (!p.b_resident && p.bn % 32 == 0 && p.kind == 0) ? 2 : 1;
     return p.a_stages >= 1 && p.a_stages <= kMaxBar && p.b_stages <= kMaxBar;
 }
 
@@ -1011,10 +854,7 @@ int device_sm_count() {
 int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV2Params &p_in,
                    cudaStream_t st) {
     if (p_in.total_tiles == 0) return 0;
-    // DC_V2_DBG (debug only): 1 skip A loads, 2 skip stores, 4 skip MMAs, 8 trace CTA 0
-    static const int dbg_env = std::getenv("DC_V2_DBG") ? std::atoi(std::getenv("DC_V2_DBG")) : 0;
     ConvV2Params p = p_in;
-    p.dbg = dbg_env;
     // second epilogue warp group, where the epilogue paces the tile loop
     // (measured A/B, N = 8 mesh layers, cold L2): the sub-pixel backward-data
     // (4 phases per tile, short K: conv1_1 1183 -> 783 us) and 256-wide N
@@ -1022,26 +862,23 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     // slows the 64/128-wide stride-1/2 tiles (conv1_2 bwd-data 633 -> 680 us,
     // conv2_1 fwd 322 -> 343 us). Not for the register-accumulated BN path
     // (bn_stats == 2) and only while the wider BN scratch still fits.
-    static const bool epi4 = std::getenv("DC_V2_EPI4") != nullptr;
-    static const bool epi8 = std::getenv("DC_V2_EPI8") != nullptr;  // force on (A/B runs)
     p.epi2 = 0;
-    if (!epi4 && p.bn_stats != 2 && (epi8 || p.subpix || p.bn >= 256)) {
+    if (p.bn_stats != 2 && (p.subpix || p.bn >= 256)) {
         p.epi2 = 1;
         if (conv_v2_smem_bytes(p) > (size_t)kV2SmemLimit) p.epi2 = 0;
     }
     static std::once_flag once;
     std::call_once(once, [] {
-        cudaFuncSetAttribute(conv_v2_kernel<1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
-        cudaFuncSetAttribute(conv_v2_kernel<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
-        cudaFuncSetAttribute(conv_v2_kernel<1, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
+        cudaFuncSetAttribute(conv_v2_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kV2SmemLimit);
     });
-    if (p.cluster > 1 && !(p.dbg & 8)) {
+    if (p.cluster > 1) {
         // persistent CTA pairs: as many as can be co-resident (GPCs need not hold
         // an even number of free SMs), a multiple of the split-K factor
         const size_t smem = conv_v2_smem_bytes(p);
         DC_REQUIRE(p.kind == 0, DC_ERR_ARG, "conv_v2: tf32 runs without CTA pairs");
-        auto kern = p.cta2 ? conv_v2_kernel<2, 0> : conv_v2_kernel<1, 0>;
-        const size_t key = smem * 2 + (size_t)p.cta2;
+        auto kern = conv_v2_kernel<0>;
+        const size_t key = smem;
         static std::map<size_t, int> max_clusters;
         if (!max_clusters.count(key)) {
             cudaLaunchConfig_t cfg{};
@@ -1061,45 +898,14 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
         const int total_w = p.nout_tiles * ((per_o + 1) / 2);
         const int cap_units = p.max_ctas > 0 ? std::min(max_clusters[key], p.max_ctas / 2) : max_clusters[key];
         const int units = p.ksplit * std::max(1, std::min(total_w, cap_units / p.ksplit));
-        cudaLaunchConfig_t cfg{};
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = 2, at[0].val.clusterDim.y = 1, at[0].val.clusterDim.z = 1;
-        cfg.gridDim = dim3(2 * units);
-        cfg.blockDim = dim3(kV2Threads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = st;
-        cfg.attrs = at, cfg.numAttrs = 1;
         launch_k(kern, dim3(2 * units), dim3(kV2Threads), smem, st, 2, "conv_v2 (pairs)", amap, bmap, p);
         return 2 * units;
     }
     const int sms = p.max_ctas > 0 ? std::min(p.max_ctas, device_sm_count()) : device_sm_count();
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, sms / p.ksplit));
     if (g_dry_run) return grid;
-    if (p.dbg & 8) {  // timing trace of CTA 0 (debug only)
-        DC_REQUIRE(p.cluster == 1, DC_ERR_ARG, "DC_V2_DBG trace needs DC_V2_NO_CLUSTER=1 (and no DC_V2_CG2)");
-        ConvV2Params q = p;
-        cudaMalloc(&q.dbg_out, 64 * 8 * sizeof(long long));
-        cudaMemset(q.dbg_out, 0, 64 * 8 * sizeof(long long));
-        conv_v2_kernel<1, 0><<<grid, kV2Threads, conv_v2_smem_bytes(q), st>>>(amap, bmap, q);
-        cudaStreamSynchronize(st);
-        long long h[64 * 8];
-        cudaMemcpy(h, q.dbg_out, sizeof h, cudaMemcpyDeviceToHost);
-        cudaFree(q.dbg_out);
-        long long t0 = h[0];
-        fprintf(stderr, "trace (cycles from first stamp): mma[acc_wait0, acc_ok, afull_ok, committed] epi[wait0, acc_ok, arrived]\n");
-        for (int i = 0; i < 12; ++i)
-            fprintf(stderr, "tile %2d: mma %7lld %7lld %7lld %7lld | epi %7lld %7lld %7lld\n", i, h[i * 8] - t0,
-                    h[i * 8 + 1] - t0, h[i * 8 + 2] - t0, h[i * 8 + 3] - t0, h[i * 8 + 4] - t0,
-                    h[i * 8 + 5] - t0, h[i * 8 + 6] - t0);
-    } else {
-        launch_k(p.kind == 1 ? conv_v2_kernel<1, 1> : conv_v2_kernel<1, 0>, dim3(grid), dim3(kV2Threads),
-                 conv_v2_smem_bytes(p), st, 1, p.kind == 1 ? "conv_v2 (tf32)" : "conv_v2", amap, bmap, p);
-        return grid;
-    }
-    cudaError_t e = cudaGetLastError();
-    DC_REQUIRE(e == cudaSuccess, DC_ERR_CUDA, "conv_v2 launch: %s", cudaGetErrorString(e));
-    ++g_launches;
+    launch_k(p.kind == 1 ? conv_v2_kernel<1> : conv_v2_kernel<0>, dim3(grid), dim3(kV2Threads),
+             conv_v2_smem_bytes(p), st, 1, p.kind == 1 ? "conv_v2 (tf32)" : "conv_v2", amap, bmap, p);
     return grid;
 }
 
@@ -1110,9 +916,8 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
 // ends).
 void preload_conv_v2() {
     cudaFuncAttributes a;
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<1, 0>));
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<2, 0>));
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<1, 1>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<0>));
+    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_kernel<1>));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(conv_v2_reduce_kernel));
 }
 

@@ -46,23 +46,12 @@ struct ConvV2Params {
                                    // 3 -> 16 x 8 (default), 7 -> 1 x 128 (thin boundary strips)
     uint32_t a_sbo;                // A descriptor SBO: byte distance between 8-pixel groups
     uint32_t a_kstep16;            // A descriptor delta between 16-channel K slices
-    int dbg;                   // timing experiments: 1 skip steady-state A TMA, 2 skip stores, 4 skip MMAs, 8 trace
-    long long *dbg_out;        // trace buffer (dbg & 8): CTA 0, [tile][8] clock64 stamps
     // Fused BN statistics of the stored y: per CTA, fp64 sum and
     // sum of squares of every channel over the CTA's tiles, written to
     // bn_part[blockIdx.x][2][nout_p] (needs ksplit == 1 and nout_tiles == 1)
     int bn_stats;
     int epi2;                  // device: 8 epilogue warps (two groups split the 16-column chunks)
     double *bn_part;
-    // Fused P2P halo exchange of the input (one kernel per GPU):
-    // warp 6 of the CTAs holding slice s (s = blockIdx.x, + gridDim.x, ... <
-    // kP2PBlocks) stores slice s of this rank's slabs into the neighbours'
-    // mapped margins after their ready flags, then bumps their data counters;
-    // the TMA producer waits for all neighbours' data (acquire + async-proxy
-    // fence) before the first tile of a rect >= halo_rect0, which are the
-    // tiles that read the margins (scheduled last).
-    int halo, halo_rect0;
-    P2PExchange hx;
     int s_in;                  // A element stride (conv stride for fwd, 1 for bwd-data)
     int origin_h, origin_w;    // input coord of GEMM pixel (0,0) at tap offset 0
     int T;                     // taps
@@ -91,8 +80,6 @@ struct ConvV2Params {
     int work_hint;             // work items of THIS launch at tpw = 1 (x ksplit): pairing only when plentiful
     int max_ctas;              // host: persistent grid cap (0: SM count)
     int cluster;               // 2: CTA pairs share (multicast) every streamed weight stage; 1: none
-    int cta2;                  // 1: CTA pairs with tcgen05 cta_group::2 (M = 256; each CTA holds half of
-                               // every weight slot, bn/2 rows); implies cluster = 2
     int allow_cg32;            // stride 2: may narrow 64-channel stages to 32 for tile pairs (changes the
                                // summation order: decided from the GLOBAL layer, see capi.cu)
     float *ws;

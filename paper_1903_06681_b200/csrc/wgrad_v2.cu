@@ -364,9 +364,8 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
     // MMA). Measured, cold L2 (profiles/r1_wgrad_bn_sweep.txt): 256 wins
     // 8-25% from 16K pixels up (512-ch 128^2 N = 8: 561 -> 458 us; 256-ch
     // 256^2: 510 -> 470 us), ties at 4K-8K, loses up to 14% below (512-ch
-    // 32^2 N = 1: 31 -> 36 us). DC_WGRAD_BN overrides.
-    static const int bn_env = std::getenv("DC_WGRAD_BN") ? std::atoi(std::getenv("DC_WGRAD_BN")) : 0;
-    const int bn_cap = bn_env > 0 ? bn_env : p.pixels_hint >= 8192 ? 256 : 128;
+    // 32^2 N = 1: 31 -> 36 us).
+    const int bn_cap = p.pixels_hint >= 8192 ? 256 : 128;
     // (tf32: N tiles of whole 32-filter dy boxes; filters past F are discarded)
     p.bn = tf32 ? std::min<int>(bn_cap, (p.Fp + 31) / 32 * 32) : p.Fp <= bn_cap ? p.Fp : bn_cap;
     p.bn_cols = p.bn <= 32 ? 32 : p.bn <= 64 ? 64 : p.bn <= 128 ? 128 : 256;
@@ -391,9 +390,8 @@ static bool wgrad_v2_configure_bw(WgradV2Params &p, int smem_limit, int bw) {
 bool wgrad_v2_configure(WgradV2Params &p, int smem_limit) {
     // 8 x 16 pixel blocks unless two stages of them do not fit (stride 2 with
     // 256-filter tiles), then 8 x 8 (tf32: always 8 x 8)
-    static const bool bw8 = std::getenv("DC_WGRAD_BW8") != nullptr;
     const WgradV2Params in = p;
-    if (!bw8 && wgrad_v2_configure_bw(p, smem_limit, 16)) return true;
+    if (wgrad_v2_configure_bw(p, smem_limit, 16)) return true;
     p = in;
     return wgrad_v2_configure_bw(p, smem_limit, 8);
 }

@@ -241,17 +241,18 @@ def test_wgrad_deterministic_default(dc, shape):
         dc.dc_plan_destroy(plan)
 
 
-def test_cta_pair_mode_parity():
-    """The opt-in CTA-pair path (DC_V2_CG2=1: tcgen05 cta_group::2, M = 256)
-    must produce the same parity as the default kernel: run the single-GPU
-    parity tests of the shapes it applies to in a child process."""
+def test_no_pdl_parity():
+    """DC_NO_PDL=1 (the one kernel-launch switch left in csrc/, launch.cuh)
+    launches every kernel without programmatic dependent launch: the same
+    single-GPU parity and bitwise partition tests pass in a child process."""
     import subprocess
     import sys
-    env = dict(os.environ, DC_V2_CG2="1")
+    env = dict(os.environ, DC_NO_PDL="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
                         "test_single_gpu_parity or test_partition_bitwise"],
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout and "failed" not in r.stdout, r.stdout[-2000:]
 
 
 def test_launch_counter_and_errors(dc):

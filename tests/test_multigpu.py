@@ -94,6 +94,22 @@ def _worker(rank, world, port, errq, env=None):
             torch.cuda.synchronize()
             ys = Y[yd["n0"]:yd["n0"] + yd["n"], yd["h0"]:yd["h0"] + yd["h"], yd["w0"]:yd["w0"] + yd["w"]]
             assert torch.equal(y, ys), f"{tag}: y not bitwise equal to 1-GPU"
+            # (2b) the non-overlapped schedule (exchange, then one pass): same bits
+            xb.copy_(fill_owned_only(x, xd))
+            y.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y, dc.DC_EXCHANGE | dc.DC_NO_OVERLAP)
+            torch.cuda.synchronize()
+            assert torch.equal(y, ys), f"{tag}: y (DC_NO_OVERLAP) not bitwise equal to 1-GPU"
+            dyb.copy_(fill_owned_only(dy, dyd))
+            dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
+            torch.cuda.synchronize()
+            dist.barrier()
+            dc.dc_conv_bwd_data(plan, dyb.data_ptr(), wb, dx, dc.DC_EXCHANGE | dc.DC_NO_OVERLAP)
+            torch.cuda.synchronize()
+            dxs = DX[dxd["n0"]:dxd["n0"] + dxd["n"], dxd["h0"]:dxd["h0"] + dxd["h"], dxd["w0"]:dxd["w0"] + dxd["w"]]
+            assert torch.equal(dx, dxs), f"{tag}: dx (DC_NO_OVERLAP) not bitwise equal to 1-GPU"
             # (3) backward with dy exchange || wgrad, allreduce || dgrad
             dyb.copy_(fill_owned_only(dy, dyd))
             dx = torch.empty((dxd["n"], dxd["h"], dxd["w"], dxd["c_pad"]), dtype=torch.bfloat16, device="cuda")
@@ -189,10 +205,8 @@ def _worker(rank, world, port, errq, env=None):
         raise
 
 
-@pytest.mark.parametrize("world,env", [(2, None), (4, None), (2, {"DC_FUSED_HALO": "1"})])
+@pytest.mark.parametrize("world,env", [(2, None), (4, None)])
 def test_multigpu_parity(world, env):
-    """env DC_FUSED_HALO=1: the forward exchanges its halo inside the conv
-    kernel (conv_v2 warp 6) instead of a separate exchange launch."""
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import torch.multiprocessing as mp
