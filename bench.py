@@ -700,9 +700,14 @@ def main():
                 for op, tt in (("fp", f_ms), ("bpw", t.get("bpw")), ("bpx", t.get("bpx"))):
                     if tt is not None:
                         f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{tt / 1e3}\n")
-    # graphs hold NCCL persistent resources: release them before the communicator
+    # teardown watchdog: a teardown stuck for 120 s prints every thread's stack
+    # to stderr and exits (the result line is already out)
+    import faulthandler
+    faulthandler.dump_traceback_later(120, exit=True)
+    # graphs hold NCCL persistent resources: release every reference to them
+    # (the per-op list included) before the communicator
     del run_step, run_e2e
-    g_step = g_e2e = g_ops = ops = f = None
+    g_step = g_e2e = g_ops = ops = f = ops_list = None
     import gc
     gc.collect()
     torch.cuda.synchronize()
@@ -711,6 +716,7 @@ def main():
     dc.dc_comm_destroy(comm)
     if world > 1:
         dist.destroy_process_group()
+    faulthandler.cancel_dump_traceback_later()
 
 
 if __name__ == "__main__":

@@ -320,6 +320,39 @@ dc_status_t dc_bn_backward(dc_plan_t plan, const void *dout, const void *y, cons
                            const float *gamma, const float *beta, double eps, const void *residual, unsigned flags,
                            float *dgamma, float *dbeta, void *dresidual, void *dy_margined, void *stream);
 
+/* ---- redistribution between decompositions ----
+ * Shuffle(D_i, D_j): when consecutive layers use different grids, each
+ * activation (and, backward, each gradient) moves from the owned blocks of
+ * one decomposition to those of the other; the element (n, c, h, w) goes from
+ * its owner under D_i to its owner under D_j, every channel, nothing else.
+ * The destination's margins are NOT filled (the next layer's halo exchange
+ * does that). */
+typedef struct dc_redist_s *dc_redist_t;
+/* COLLECTIVE over the plans' communicator (virtual plans: host-only
+ * geometry for dc_redist_bytes). Source: tensor tf (DC_Y / DC_DX: the dense
+ * owned shard; DC_X / DC_DY: the owned interior of the margined buffer) of
+ * plan `from`; destination: the owned interior of the margined tensor tt
+ * (DC_X / DC_DY) of plan `to`, whose dc_buffer_alloc buffer must exist on
+ * every rank before this call (it is mapped into the senders for the direct
+ * transport). The two tensors must have the same global N, H, W, channels
+ * and pixel layout (fp32 plans: margined source only, DC_ERR_UNSUPPORTED
+ * otherwise). Errors: DC_ERR_ARG, DC_ERR_SHAPE, DC_ERR_UNSUPPORTED. */
+dc_status_t dc_redist_create(dc_plan_t from, dc_tensor_t tf, dc_plan_t to, dc_tensor_t tt, dc_redist_t *out);
+/* Bytes this rank sends to / receives from each rank (arrays of world
+ * entries; the block a rank keeps appears at its own index). */
+dc_status_t dc_redist_bytes(dc_redist_t r, int64_t *send_bytes, int64_t *recv_bytes);
+/* COLLECTIVE, stream-ordered. Moves src (the source shard, layout of tf)
+ * into dst (the destination plan's dc_buffer_alloc buffer of tt). Default
+ * transport: ONE kernel per rank stores every piece straight into its new
+ * owner's buffer over NVLink peer memory, after that owner's ready flag, and
+ * returns when every piece for this rank has arrived (device epochs, CUDA
+ * graph replayable; <= 8 ranks). flags = DC_HALO_NCCL: pack, grouped
+ * ncclSend / ncclRecv, unpack (real ranks; dst may then be any buffer of the
+ * tt layout). src and dst may be reused / read after the call on `stream`.
+ * Errors: DC_ERR_ARG, DC_ERR_UNSUPPORTED, DC_ERR_COMM, DC_ERR_CUDA. */
+dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned flags, void *stream);
+dc_status_t dc_redist_destroy(dc_redist_t r);
+
 /* Number of kernels this library launched on this thread so far (for the
  * bench's gpu_launches claim). */
 uint64_t dc_kernel_launches(void);

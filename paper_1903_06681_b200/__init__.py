@@ -38,6 +38,7 @@ EXPORTS = [
     "dc_kernel_launches",
     "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
     "dc_model_choose", "dc_model_choose_fixed", "dc_model_shuffle_cost", "dc_model_strategy",
+    "dc_redist_create", "dc_redist_bytes", "dc_redistribute", "dc_redist_destroy",
 ]
 
 
@@ -123,6 +124,10 @@ def lib() -> ctypes.CDLL:
         "dc_model_choose_fixed": [i64] * 5 + [i32, i32, i32, i32, dc_decomp_t, P(dc_decomp_t), P(ctypes.c_double)],
         "dc_model_shuffle_cost": [i64] * 4 + [dc_decomp_t, dc_decomp_t, P(ctypes.c_double)],
         "dc_model_strategy": [P(dc_layer_t), i32, i32, i32, P(dc_decomp_t), P(ctypes.c_double)],
+        "dc_redist_create": [vp, i32, vp, i32, P(vp)],
+        "dc_redist_bytes": [vp, P(i64), P(i64)],
+        "dc_redistribute": [vp, vp, vp, ctypes.c_uint, vp],
+        "dc_redist_destroy": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -373,3 +378,26 @@ def dc_model_strategy(layers, world: int, fix_pn: int = 0):
     t = ctypes.c_double()
     _check(lib().dc_model_strategy(arr, len(layers), world, fix_pn, out, ctypes.byref(t)))
     return [(d.pn, d.ph, d.pw) for d in out], t.value
+
+
+def dc_redist_create(src_plan: int, src_t: int, dst_plan: int, dst_t: int) -> int:
+    """Redistribution (Shuffle) of tensor src_t of src_plan
+    into the margined tensor dst_t of dst_plan (collective)."""
+    out = ctypes.c_void_p()
+    _check(lib().dc_redist_create(src_plan, src_t, dst_plan, dst_t, ctypes.byref(out)))
+    return out.value
+
+
+def dc_redist_bytes(r: int, world: int):
+    """([bytes sent to rank q], [bytes received from rank q]) on this rank."""
+    snd, rcv = (ctypes.c_int64 * world)(), (ctypes.c_int64 * world)()
+    _check(lib().dc_redist_bytes(r, snd, rcv))
+    return list(snd), list(rcv)
+
+
+def dc_redistribute(r: int, src, dst, flags: int = 0, stream=None):
+    _check(lib().dc_redistribute(r, _ptr(src), _ptr(dst), flags, _stream(stream)))
+
+
+def dc_redist_destroy(r: int):
+    _check(lib().dc_redist_destroy(r))

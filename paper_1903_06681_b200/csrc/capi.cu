@@ -32,6 +32,7 @@
 #include "wgrad_v2.cuh"
 #include "tf32.cuh"
 #include "bn.cuh"
+#include "redist.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -48,6 +49,7 @@ void preload_halo();
 void preload_tf32();
 void preload_wgrad_v2();
 void preload_bn();
+void preload_redist();
 // Every kernel of the library loaded into this context (see preload_*):
 // once, at communicator creation.
 void preload_kernels() {
@@ -59,6 +61,7 @@ void preload_kernels() {
         preload_tf32();
         preload_wgrad_v2();
         preload_bn();
+        preload_redist();
     });
 }
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
@@ -78,6 +81,7 @@ using namespace dc;
     } while (0)
 
 struct dc_plan_s;
+struct dc_redist_s;
 
 namespace dc {
 // Loopback group: `world` virtual ranks of one process on ONE device
@@ -90,6 +94,7 @@ struct LocalGroup {
     std::mutex mu;
     std::map<std::pair<int, int>, dc_plan_s *> plans;  // (plan sequence number, rank)
     std::map<int, std::array<int, 3>> grids;            // sequence number -> grid of its first rank
+    std::map<std::pair<int, int>, dc_redist_s *> redists;  // (redistribution sequence number, rank)
 };
 }  // namespace dc
 
@@ -109,6 +114,7 @@ struct dc_comm_s {
     size_t bucket_bytes = 0, bucket_cap = 4u << 20;
     std::shared_ptr<LocalGroup> group;  // loopback group (no NCCL), or null
     int plan_seq = 0;                   // plans created on this communicator (loopback registry key)
+    int redist_seq = 0;                 // redistributions created on it (likewise)
     // loopback: the virtual rank's two streams (its compute stream, handed to
     // the caller by dc_comm_stream, and the side stream every plan of the rank
     // uses for exchanges / boundary tiles), created back to back for all ranks
@@ -2099,6 +2105,320 @@ dc_status_t dc_bn_backward(dc_plan_t pl, const void *dout, const void *y, const 
     a.hb = (int)dyd.hb, a.wb = (int)dyd.wb, a.r0 = dyd.halo_n, a.c0 = dyd.halo_w, a.dcp = (int)dyd.c_pad;
     a.split = g.dt;
     launch_bn_bwd_apply(a, sums, count, gamma, dgamma, dbeta, dresidual, st);
+    DC_API_END
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Redistribution between decompositions (Shuffle(D_i, D_j))
+// ===========================================================================
+struct dc_redist_s {
+    dc_plan_s *from = nullptr, *to = nullptr;
+    dc_tensor_t tf = DC_Y, tt = DC_X;
+    dc_comm_s *comm = nullptr;
+    bool is_virtual = false;
+    int rank = 0, world = 1, which = 0, seq = -1;
+    int esz = 2;
+    // global block (samples, rows, cols) moving between this rank and `peer`
+    struct Piece {
+        int peer;
+        int64_t n0, n, h0, h, w0, w;
+    };
+    std::vector<Piece> sends, recvs;  // ascending peer order
+    dc_shard_desc_t src_d{};              // my source shard
+    std::vector<dc_shard_desc_t> dst_all; // every rank's destination shard
+    uint32_t *flags = nullptr;  // [2][world]: ready flag of rank p at p, data counter from p at world + p
+    uint32_t *epoch = nullptr;  // {epoch, blocks done}
+    std::map<int, uint32_t *> peer_flags;  // peer -> its flag array mapped here
+    std::map<int, void *> peer_dst;        // receiver -> its destination buffer mapped here
+    void *stage = nullptr;                 // NCCL transport: [send | recv]
+    size_t stage_bytes = 0;
+    std::vector<void *> grave;
+
+    ~dc_redist_s() {
+        const bool local = comm && comm->group;
+        if (local) {
+            std::lock_guard<std::mutex> lk(comm->group->mu);
+            comm->group->redists.erase({seq, rank});
+        } else {
+            for (auto &kv : peer_flags)
+                if (kv.first != rank) cudaIpcCloseMemHandle(kv.second);
+            for (auto &kv : peer_dst)
+                if (kv.first != rank) cudaIpcCloseMemHandle(kv.second);
+        }
+        for (void *q : grave) cudaFree(q);
+        if (stage) cudaFree(stage);
+        if (flags) cudaFree(flags);
+        if (epoch) cudaFree(epoch);
+    }
+};
+
+namespace {
+
+// The global extents (N, H, W, channels) of a plan's tensor.
+std::array<int64_t, 4> global_extent(const ConvGeom &g, dc_tensor_t t) {
+    if (t == DC_X || t == DC_DX) return {g.N, g.H, g.W, g.C};
+    return {g.N, g.Ho, g.Wo, g.F};
+}
+
+Range isect(int64_t a0, int64_t an, int64_t b0, int64_t bn) {
+    return Range{std::max(a0, b0), std::min(a0 + an, b0 + bn)};
+}
+
+// One piece as a copy: rows of `run` 16-byte vectors from the block at its
+// place in shard `a` (pointer pa) to its place in shard `b` (pb); pass a
+// null shard for a contiguous staging block [n][h][w] at pa / pb.
+RedistPiece make_piece(const dc_redist_s::Piece &p, const dc_shard_desc_t *a, const void *pa,
+                       const dc_shard_desc_t *b, void *pb, int esz) {
+    const int64_t px = (a ? a->c_pad : b->c_pad) * esz / 16;  // vectors per pixel
+    RedistPiece c{};
+    auto place = [&](const dc_shard_desc_t *d, int64_t &sn, int64_t &sh) -> int64_t {
+        if (!d) {
+            sh = p.w * px, sn = p.h * sh;
+            return 0;
+        }
+        sn = d->stride_n * esz / 16, sh = d->stride_h * esz / 16;
+        return (p.n0 - d->n0) * sn + (p.h0 - d->h0 + d->halo_n) * sh + (p.w0 - d->w0 + d->halo_w) * px;
+    };
+    int64_t sn, sh, dn, dh;
+    const int64_t so = place(a, sn, sh), dof = place(b, dn, dh);
+    c.src = reinterpret_cast<const uint4 *>(pa) + so;
+    c.dst = reinterpret_cast<uint4 *>(pb) + dof;
+    c.s_sn = sn, c.s_sh = sh, c.d_sn = dn, c.d_sh = dh;
+    c.nn = (int)p.n, c.rows = (int)p.h, c.run = (int)(p.w * px);
+    return c;
+}
+
+int64_t piece_bytes(const dc_redist_s::Piece &p, int64_t pixel_bytes) { return p.n * p.h * p.w * pixel_bytes; }
+
+void resolve_redist_peers(dc_redist_s *r) {
+    if (!(r->comm && r->comm->group)) return;
+    LocalGroup &G = *r->comm->group;
+    for (int pass = 0; pass < 2; ++pass)
+        for (auto &p : pass ? r->recvs : r->sends) {
+            dc_redist_s *q = nullptr;
+            {
+                std::lock_guard<std::mutex> lk(G.mu);
+                auto it = G.redists.find({r->seq, p.peer});
+                DC_REQUIRE(it != G.redists.end(), DC_ERR_ARG,
+                           "loopback group: rank %d has not created redistribution #%d", p.peer, r->seq);
+                q = it->second;
+            }
+            r->peer_flags[p.peer] = q->flags;
+            if (!pass) {
+                void *d = local_peer(r->to, p.peer)->buf[r->which].ptr;
+                DC_REQUIRE(d != nullptr, DC_ERR_ARG, "redistribution: rank %d has no dc_buffer_alloc buffer",
+                           p.peer);
+                r->peer_dst[p.peer] = d;
+            }
+        }
+}
+
+void redist_p2p(dc_redist_s *r, const void *src, cudaStream_t st) {
+    resolve_redist_peers(r);
+    DC_REQUIRE((int)r->sends.size() <= kRedistMaxPeers && (int)r->recvs.size() <= kRedistMaxPeers,
+               DC_ERR_UNSUPPORTED, "P2P redistribution: more than %d peers (use DC_HALO_NCCL)", kRedistMaxPeers);
+    RedistP2P x{};
+    x.epoch_ctr = r->epoch;
+    // blocks per launch, equal on all ranks of the group; a loopback group's
+    // ranks share one GPU, and all of their blocks must be resident at once
+    // (each waits for the others' flags): at most 4 blocks per SM in total
+    x.nblocks = kRedistBlocks;
+    if (r->comm->group) x.nblocks = std::max(8, std::min(kRedistBlocks, 4 * device_sm_count() / r->world));
+    const int W = r->world;
+    for (auto &p : r->sends) {
+        x.piece[x.npiece++] = make_piece(p, &r->src_d, src, &r->dst_all[p.peer], r->peer_dst.at(p.peer), r->esz);
+        x.ready_in[x.n_ready_in++] = r->flags + p.peer;
+        x.data_out[x.n_data_out++] = r->peer_flags.at(p.peer) + W + r->rank;
+    }
+    for (auto &p : r->recvs) {
+        x.ready_out[x.n_ready_out++] = r->peer_flags.at(p.peer) + r->rank;
+        x.data_in[x.n_data_in++] = r->flags + W + p.peer;
+    }
+    launch_redist_p2p(x, st);
+}
+
+void redist_nccl(dc_redist_s *r, const void *src, void *dst, cudaStream_t st) {
+    const int64_t pxb = r->src_d.c_pad * r->esz;
+    size_t sb = 0, rb = 0;
+    for (auto &p : r->sends)
+        if (p.peer != r->rank) sb += piece_bytes(p, pxb);
+    for (auto &p : r->recvs)
+        if (p.peer != r->rank) rb += piece_bytes(p, pxb);
+    ensure_alloc(r->grave, reinterpret_cast<uint8_t *&>(r->stage), r->stage_bytes, sb + rb);
+    uint8_t *sbuf = reinterpret_cast<uint8_t *>(r->stage), *rbuf = sbuf + sb;
+    const dc_shard_desc_t &me = r->dst_all[r->rank];
+    std::vector<RedistPiece> pack, unpack;
+    size_t off = 0;
+    for (auto &p : r->sends) {
+        if (p.peer == r->rank) {
+            pack.push_back(make_piece(p, &r->src_d, src, &me, dst, r->esz));  // the piece I keep
+            continue;
+        }
+        pack.push_back(make_piece(p, &r->src_d, src, nullptr, sbuf + off, r->esz));
+        off += piece_bytes(p, pxb);
+    }
+    launch_redist_copy(pack.data(), (int)pack.size(), st);
+    NK(ncclGroupStart());
+    off = 0;
+    for (auto &p : r->sends)
+        if (p.peer != r->rank) {
+            NK(ncclSend(sbuf + off, piece_bytes(p, pxb), ncclUint8, p.peer, r->comm->nccl, st));
+            off += piece_bytes(p, pxb);
+        }
+    off = 0;
+    for (auto &p : r->recvs)
+        if (p.peer != r->rank) {
+            NK(ncclRecv(rbuf + off, piece_bytes(p, pxb), ncclUint8, p.peer, r->comm->nccl, st));
+            off += piece_bytes(p, pxb);
+        }
+    NK(ncclGroupEnd());
+    off = 0;
+    for (auto &p : r->recvs)
+        if (p.peer != r->rank) {
+            unpack.push_back(make_piece(p, nullptr, rbuf + off, &me, dst, r->esz));
+            off += piece_bytes(p, pxb);
+        }
+    launch_redist_copy(unpack.data(), (int)unpack.size(), st);
+}
+
+}  // namespace
+
+extern "C" {
+
+dc_status_t dc_redist_create(dc_plan_t from, dc_tensor_t tf, dc_plan_t to, dc_tensor_t tt, dc_redist_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(from && to && out, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(tf == DC_X || tf == DC_Y || tf == DC_DX || tf == DC_DY, DC_ERR_ARG, "bad source tensor");
+    DC_REQUIRE(tt == DC_X || tt == DC_DY, DC_ERR_ARG, "the destination is a margined x or dy (DC_X / DC_DY)");
+    DC_REQUIRE(from->is_virtual == to->is_virtual, DC_ERR_ARG, "both plans virtual, or neither");
+    DC_REQUIRE(from->rp.rank == to->rp.rank && from->world() == to->world(), DC_ERR_ARG,
+               "plans of different ranks / world sizes");
+    DC_REQUIRE(from->is_virtual || from->comm == to->comm, DC_ERR_ARG, "plans on different communicators");
+    const ConvGeom &gf = from->rp.g, &gt = to->rp.g;
+    DC_REQUIRE(gf.dt == gt.dt, DC_ERR_ARG, "plans of different dtypes");
+    const auto ef = global_extent(gf, tf), et = global_extent(gt, tt);
+    DC_REQUIRE(ef == et, DC_ERR_SHAPE, "tensors differ: (%lld,%lld,%lld,%lld) vs (%lld,%lld,%lld,%lld)",
+               (long long)ef[0], (long long)ef[1], (long long)ef[2], (long long)ef[3], (long long)et[0],
+               (long long)et[1], (long long)et[2], (long long)et[3]);
+    std::unique_ptr<dc_redist_s> r(new dc_redist_s());
+    r->from = from, r->to = to, r->tf = tf, r->tt = tt;
+    r->comm = from->comm, r->is_virtual = from->is_virtual;
+    r->rank = from->rp.rank, r->world = from->world();
+    r->which = tt == DC_X ? 0 : 1;
+    r->esz = gf.esz();
+    r->src_d = describe(from->rp, tf);
+    DC_REQUIRE(r->src_d.c_pad == describe(to->rp, tt).c_pad, DC_ERR_UNSUPPORTED,
+               "pixel layouts differ (fp32 plans: the source must be a margined x / dy, whose pixels are "
+               "already split into tf32 [hi | lo])");
+    // every rank's owned blocks under both decompositions (host integer math)
+    std::vector<dc_shard_desc_t> src_all(r->world);
+    r->dst_all.resize(r->world);
+    for (int q = 0; q < r->world; ++q) {
+        src_all[q] = q == r->rank ? r->src_d : describe(make_rank_plan(gf, from->rp.grid, q), tf);
+        r->dst_all[q] = describe(q == r->rank ? to->rp : make_rank_plan(gt, to->rp.grid, q), tt);
+    }
+    auto piece = [&](int peer, const dc_shard_desc_t &a, const dc_shard_desc_t &b, std::vector<dc_redist_s::Piece> &v) {
+        const Range n = isect(a.n0, a.n, b.n0, b.n), h = isect(a.h0, a.h, b.h0, b.h), w = isect(a.w0, a.w, b.w0, b.w);
+        if (!n.empty() && !h.empty() && !w.empty())
+            v.push_back({peer, n.lo, n.size(), h.lo, h.size(), w.lo, w.size()});
+    };
+    for (int q = 0; q < r->world; ++q) {
+        piece(q, r->src_d, r->dst_all[q], r->sends);
+        piece(q, src_all[q], r->dst_all[r->rank], r->recvs);
+    }
+    if (!r->is_virtual && r->world > 1) {
+        dc_comm_s *c = r->comm;
+        DC_REQUIRE(c && (c->nccl || c->group), DC_ERR_ARG, "redistribution needs a communicator");
+        void *dst = to->buf[r->which].ptr;
+        DC_REQUIRE(dst != nullptr, DC_ERR_ARG,
+                   "redistribution: allocate the destination with dc_buffer_alloc (on every rank) first");
+        r->seq = c->redist_seq++;
+        CK(cudaMalloc(&r->flags, sizeof(uint32_t) * 2 * r->world));
+        CK(cudaMemset(r->flags, 0, sizeof(uint32_t) * 2 * r->world));
+        CK(cudaMalloc(&r->epoch, sizeof(uint32_t) * 2));
+        CK(cudaMemset(r->epoch, 0, sizeof(uint32_t) * 2));
+        if (c->group) {
+            std::lock_guard<std::mutex> lk(c->group->mu);
+            c->group->redists[{r->seq, r->rank}] = r.get();
+        } else {
+            struct Handles {
+                cudaIpcMemHandle_t flags, dst;
+            } h{};
+            CK(cudaIpcGetMemHandle(&h.flags, r->flags));
+            CK(cudaIpcGetMemHandle(&h.dst, dst));
+            auto all = comm_allgather(c, &h, sizeof h);
+            auto at = [&](int q) {
+                Handles x;
+                std::memcpy(&x, all.data() + q * sizeof x, sizeof x);
+                return x;
+            };
+            for (int pass = 0; pass < 2; ++pass)
+                for (auto &p : pass ? r->recvs : r->sends) {
+                    if (p.peer == r->rank) {
+                        r->peer_flags[p.peer] = r->flags;
+                        if (!pass) r->peer_dst[p.peer] = dst;
+                        continue;
+                    }
+                    if (!r->peer_flags.count(p.peer)) {
+                        void *ptr = nullptr;
+                        CK(cudaIpcOpenMemHandle(&ptr, at(p.peer).flags, cudaIpcMemLazyEnablePeerAccess));
+                        r->peer_flags[p.peer] = reinterpret_cast<uint32_t *>(ptr);
+                    }
+                    if (!pass) {
+                        void *ptr = nullptr;
+                        CK(cudaIpcOpenMemHandle(&ptr, at(p.peer).dst, cudaIpcMemLazyEnablePeerAccess));
+                        r->peer_dst[p.peer] = ptr;
+                    }
+                }
+        }
+        CK(cudaDeviceSynchronize());
+    }
+    *out = r.release();
+    DC_API_END
+}
+
+dc_status_t dc_redist_bytes(dc_redist_t r, int64_t *send_bytes, int64_t *recv_bytes) {
+    DC_API_BEGIN
+    DC_REQUIRE(r && send_bytes && recv_bytes, DC_ERR_ARG, "null argument");
+    const int64_t pxb = r->src_d.c_pad * r->esz;
+    for (int q = 0; q < r->world; ++q) send_bytes[q] = recv_bytes[q] = 0;
+    for (auto &p : r->sends) send_bytes[p.peer] = piece_bytes(p, pxb);
+    for (auto &p : r->recvs) recv_bytes[p.peer] = piece_bytes(p, pxb);
+    DC_API_END
+}
+
+dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(r && src && dst, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(!r->is_virtual, DC_ERR_ARG, "virtual plans have no data");
+    DC_REQUIRE((flags & ~DC_HALO_NCCL) == 0, DC_ERR_ARG, "unknown redistribution flags 0x%x", flags);
+    DC_REQUIRE(src != dst, DC_ERR_ARG, "redistribution is not in place");
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool local = r->comm && r->comm->group;
+    NoPdlScope no_pdl(local);  // (loopback: ranks share the SMs)
+    join_import(r->to, r->which, st);
+    if (r->tf == DC_X || r->tf == DC_DY) join_import(r->from, r->tf == DC_X ? 0 : 1, st);
+    if (r->world == 1) {
+        const dc_shard_desc_t &me = r->dst_all[0];
+        std::vector<RedistPiece> one;
+        for (auto &p : r->sends) one.push_back(make_piece(p, &r->src_d, src, &me, dst, r->esz));
+        launch_redist_copy(one.data(), (int)one.size(), st);
+    } else if (flags & DC_HALO_NCCL) {
+        DC_REQUIRE(!local, DC_ERR_UNSUPPORTED, "DC_HALO_NCCL needs real ranks (loopback group)");
+        redist_nccl(r, src, dst, st);
+    } else {
+        DC_REQUIRE(dst == r->to->buf[r->which].ptr, DC_ERR_ARG,
+                   "P2P redistribution writes the destination plan's dc_buffer_alloc buffer");
+        redist_p2p(r, src, st);
+    }
+    DC_API_END
+}
+
+dc_status_t dc_redist_destroy(dc_redist_t r) {
+    DC_API_BEGIN
+    delete r;
     DC_API_END
 }
 
