@@ -353,6 +353,47 @@ dc_status_t dc_redist_bytes(dc_redist_t r, int64_t *send_bytes, int64_t *recv_by
 dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned flags, void *stream);
 dc_status_t dc_redist_destroy(dc_redist_t r);
 
+/* ---- channel / filter parallelism ----
+ * A p_N x p_C grid of ranks (rank = i_N p_C + i_C): rank (i_N, i_C) owns the
+ * samples block i_N and, of the channel dimensions, the input-channel block
+ * i_C of x / dx / dW and the filter block i_C of y / dy ("if the input x is
+ * partitioned on its C dimension, the output y is partitioned on its F
+ * dimension"). Blocks are equal: C and F multiples of 16 p_C;
+ * bf16 plans; the filter bank w is replicated (every rank holds all of it).
+ *   forward:         y[F_r] = sum over the group's channel blocks of the
+ *                    partial convolutions -- a reduce-scatter over F
+ *                     fused into the conv GEMM: its epilogue
+ *                    stores each fp32 partial tile into the owner's receive
+ *                    slot over peer memory; the owner sums the p_C slots in
+ *                    rank order and rounds to bf16 once;
+ *   backward-data:   dx[C_r] likewise, a reduce-scatter over C;
+ *   backward-filter: dy gathered over the group ("may require
+ *                    data to be gathered"; one P2P all-to-all launch), then
+ *                    dW[:, C_r] locally; DC_ALLREDUCE sums it over the p_N
+ *                    sample groups (NCCL; real ranks).
+ * All local tensors are dense NHWC without margins (dc_cplan_query). */
+typedef struct dc_cplan_s *dc_cplan_t;
+/* COLLECTIVE (comm of p_N p_C ranks, or NULL for 1 x 1). Errors: DC_ERR_ARG,
+ * DC_ERR_SHAPE, DC_ERR_PARTITION, DC_ERR_UNSUPPORTED (fp32, C or F not a
+ * multiple of 16 p_C, p_C > 8), DC_ERR_COMM. */
+dc_status_t dc_cplan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int stride, int pad,
+                            int pn, int pc, dc_dtype_t dtype, dc_comm_t comm, dc_cplan_t *out);
+/* Host-only geometry of rank `rank` (dc_cplan_query only). */
+dc_status_t dc_cplan_create_virtual(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int stride,
+                                    int pad, int pn, int pc, int rank, dc_cplan_t *out);
+/* Local shard of t: X / DX [n][H][W][C_r], Y / DY [n][Ho][Wo][F_r], W the
+ * whole [F][K][K][C] bf16 bank, DW [F][K][K][C_r] fp32; *c0 (may be NULL) =
+ * the first global channel (X, DX, DW: of C; Y, DY: of F; W: 0). */
+dc_status_t dc_cplan_query(dc_cplan_t plan, dc_tensor_t t, dc_shard_desc_t *desc, int64_t *c0);
+/* COLLECTIVE over the channel group, stream-ordered; flags 0. */
+dc_status_t dc_cconv_fwd(dc_cplan_t plan, const void *x, const void *w, void *y, unsigned flags, void *stream);
+dc_status_t dc_cconv_bwd_data(dc_cplan_t plan, const void *dy, const void *w, void *dx, unsigned flags,
+                              void *stream);
+/* flags: 0 or DC_ALLREDUCE. */
+dc_status_t dc_cconv_bwd_filter(dc_cplan_t plan, const void *x, const void *dy, float *dw, unsigned flags,
+                                void *stream);
+dc_status_t dc_cplan_destroy(dc_cplan_t plan);
+
 /* Number of kernels this library launched on this thread so far (for the
  * bench's gpu_launches claim). */
 uint64_t dc_kernel_launches(void);

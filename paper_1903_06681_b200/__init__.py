@@ -39,6 +39,8 @@ EXPORTS = [
     "dc_last_error", "dc_model_set_comm", "dc_model_set_overlap", "dc_model_set_strided_latency", "dc_model_load_table", "dc_model_layer_cost",
     "dc_model_choose", "dc_model_choose_fixed", "dc_model_shuffle_cost", "dc_model_strategy",
     "dc_redist_create", "dc_redist_bytes", "dc_redistribute", "dc_redist_destroy",
+    "dc_cplan_create", "dc_cplan_create_virtual", "dc_cplan_query", "dc_cconv_fwd", "dc_cconv_bwd_data",
+    "dc_cconv_bwd_filter", "dc_cplan_destroy",
 ]
 
 
@@ -128,6 +130,13 @@ def lib() -> ctypes.CDLL:
         "dc_redist_bytes": [vp, P(i64), P(i64)],
         "dc_redistribute": [vp, vp, vp, ctypes.c_uint, vp],
         "dc_redist_destroy": [vp],
+        "dc_cplan_create": [i64] * 5 + [i32, i32, i32, i32, i32, i32, vp, P(vp)],
+        "dc_cplan_create_virtual": [i64] * 5 + [i32, i32, i32, i32, i32, i32, P(vp)],
+        "dc_cplan_query": [vp, i32, P(dc_shard_desc_t), P(i64)],
+        "dc_cconv_fwd": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_cconv_bwd_data": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_cconv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_cplan_destroy": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -401,3 +410,42 @@ def dc_redistribute(r: int, src, dst, flags: int = 0, stream=None):
 
 def dc_redist_destroy(r: int):
     _check(lib().dc_redist_destroy(r))
+
+
+def dc_cplan_create(N, C, H, W, F, K, stride, pad, pn: int, pc: int, dtype=DC_BF16, comm=None) -> int:
+    """Channel / filter parallel plan on a p_N x p_C grid."""
+    out = ctypes.c_void_p()
+    _check(lib().dc_cplan_create(N, C, H, W, F, K, stride, pad, pn, pc, dtype, comm, ctypes.byref(out)))
+    return out.value
+
+
+def dc_cplan_create_virtual(N, C, H, W, F, K, stride, pad, pn: int, pc: int, rank: int) -> int:
+    out = ctypes.c_void_p()
+    _check(lib().dc_cplan_create_virtual(N, C, H, W, F, K, stride, pad, pn, pc, rank, ctypes.byref(out)))
+    return out.value
+
+
+def dc_cplan_query(plan: int, t: int) -> dict:
+    """Shard descriptor of t plus "c0", its first global channel."""
+    d = dc_shard_desc_t()
+    c0 = ctypes.c_int64()
+    _check(lib().dc_cplan_query(plan, t, ctypes.byref(d), ctypes.byref(c0)))
+    out = d.as_dict()
+    out["c0"] = c0.value
+    return out
+
+
+def dc_cconv_fwd(plan: int, x, w, y, flags: int = 0, stream=None):
+    _check(lib().dc_cconv_fwd(plan, _ptr(x), _ptr(w), _ptr(y), flags, _stream(stream)))
+
+
+def dc_cconv_bwd_data(plan: int, dy, w, dx, flags: int = 0, stream=None):
+    _check(lib().dc_cconv_bwd_data(plan, _ptr(dy), _ptr(w), _ptr(dx), flags, _stream(stream)))
+
+
+def dc_cconv_bwd_filter(plan: int, x, dy, dw, flags: int = 0, stream=None):
+    _check(lib().dc_cconv_bwd_filter(plan, _ptr(x), _ptr(dy), _ptr(dw), flags, _stream(stream)))
+
+
+def dc_cplan_destroy(plan: int):
+    _check(lib().dc_cplan_destroy(plan))

@@ -33,6 +33,7 @@
 #include "tf32.cuh"
 #include "bn.cuh"
 #include "redist.cuh"
+#include "cfpar.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -50,6 +51,7 @@ void preload_tf32();
 void preload_wgrad_v2();
 void preload_bn();
 void preload_redist();
+void preload_cfpar();
 // Every kernel of the library loaded into this context (see preload_*):
 // once, at communicator creation.
 void preload_kernels() {
@@ -62,6 +64,7 @@ void preload_kernels() {
         preload_wgrad_v2();
         preload_bn();
         preload_redist();
+        preload_cfpar();
     });
 }
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
@@ -82,6 +85,7 @@ using namespace dc;
 
 struct dc_plan_s;
 struct dc_redist_s;
+struct dc_cplan_s;
 
 namespace dc {
 // Loopback group: `world` virtual ranks of one process on ONE device
@@ -95,6 +99,7 @@ struct LocalGroup {
     std::map<std::pair<int, int>, dc_plan_s *> plans;  // (plan sequence number, rank)
     std::map<int, std::array<int, 3>> grids;            // sequence number -> grid of its first rank
     std::map<std::pair<int, int>, dc_redist_s *> redists;  // (redistribution sequence number, rank)
+    std::map<std::pair<int, int>, dc_cplan_s *> cplans;    // (channel plan sequence number, rank)
 };
 }  // namespace dc
 
@@ -115,6 +120,7 @@ struct dc_comm_s {
     std::shared_ptr<LocalGroup> group;  // loopback group (no NCCL), or null
     int plan_seq = 0;                   // plans created on this communicator (loopback registry key)
     int redist_seq = 0;                 // redistributions created on it (likewise)
+    int cplan_seq = 0;                  // channel / filter parallel plans (likewise)
     // loopback: the virtual rank's two streams (its compute stream, handed to
     // the caller by dc_comm_stream, and the side stream every plan of the rank
     // uses for exchanges / boundary tiles), created back to back for all ranks
@@ -206,6 +212,11 @@ struct dc_plan_s {
     size_t stage_bytes[2] = {0, 0};
     std::vector<void *> grave;       // outgrown workspaces (freed with the plan; see ensure_alloc)
     double predicted = 0.0;
+    // set by a channel / filter parallel plan on its sub-plans (dc_cconv_*):
+    // every conv GEMM of this plan stores fp32 partials scattered by
+    // output-channel block (GemmLaunch::scat)
+    float *scat[8] = {};
+    int scat_seg = 0;
 
     ~dc_plan_s() {
         for (void *q : grave) cudaFree(q);
@@ -462,6 +473,10 @@ struct GemmLaunch {
     int64_t a_cvirt = 0;
     bool out_f32 = false;
     int64_t cin = 0;           // K per tap of the B matrix, 16-bit units
+    // channel / filter parallelism: fp32 output scattered by output-channel
+    // block into the owners' receive slots (ConvV2Params::scat)
+    float *scat[8] = {};
+    int scat_seg = 0;
 };
 
 OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
@@ -485,6 +500,14 @@ void attach_ksplit(dc_plan_s *pl, GemmLaunch &L, int nl) {
     L.ws_h = b.nh, L.ws_w = b.nw;
     ensure_alloc(pl->grave, pl->ws2, pl->ws2_bytes, ksplit_bytes(L, nl));
     L.ws = pl->ws2;
+}
+
+// Channel / filter parallel sub-plans: fp32 partials to the owners' slots.
+void apply_scatter(const dc_plan_s *pl, GemmLaunch &L) {
+    if (!pl->scat_seg) return;
+    L.out_f32 = true;
+    std::memcpy(L.scat, pl->scat, sizeof L.scat);
+    L.scat_seg = pl->scat_seg;
 }
 
 void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunch &L, cudaStream_t st) {
@@ -552,6 +575,7 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
                            (int64_t)pl->splitk_world());
     L.ksplit = choose_ksplit(L.work_hint, L.cin);
     attach_ksplit(pl, L, (int)rp.nrange.size());
+    apply_scatter(pl, L);
 }
 
 // Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
@@ -583,6 +607,12 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
     q.nout_p = L.p.nout_p;
     q.max_ctas = L.max_ctas;
+    if (L.scat_seg) {  // the receive slots have channel pitch scat_seg
+        std::memcpy(q.scat, L.scat, sizeof q.scat);
+        q.scat_seg = L.scat_seg;
+        const long long cp = L.p.out_sw;
+        q.out_sw = L.scat_seg, q.out_sh = L.p.out_sh / cp * L.scat_seg, q.out_sn = L.p.out_sn / cp * L.scat_seg;
+    }
     const int TW = 1 << twl, TH = 128 >> twl;
     // (1) choices that change the summation order (channel-stage width) come
     // from the GLOBAL layer, so every partition computes the 1-GPU bits
@@ -692,6 +722,7 @@ void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *
     if (rects.empty()) return;
     if (launch_rects_v2(L, rects, in_base, ind, cin_p, nsamples, st)) return;
     DC_REQUIRE(L.kind == 0, DC_ERR_UNSUPPORTED, "3xTF32: the tile-reuse kernel does not fit this layer");
+    DC_REQUIRE(L.scat_seg == 0, DC_ERR_UNSUPPORTED, "channel-parallel partials: the tile-reuse kernel does not fit");
     L.bn_ok = false;  // (the v1 kernel has no fused statistics)
     std::map<int, std::vector<OutRect>> by_twl;
     for (auto &r : rects) by_twl[pick_twl(r.nh, r.nw, 128)].push_back(r);
@@ -950,7 +981,7 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
                          bool *exchanged) {
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
-    if (g.dt != 0 || g.S != 2 || g.Cp > 32) return false;
+    if (g.dt != 0 || g.S != 2 || g.Cp > 32 || pl->scat_seg) return false;
     const dc_shard_desc_t dyd = describe(rp, DC_DY), dxd = describe(rp, DC_DX);
     const int K = g.K, P = g.P;
     const int dmin = -(int)floor_div(K - 1 - P, 2), dmax = (int)floor_div(P + 1, 2);
@@ -1096,6 +1127,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
                                       L[i].nout_tiles,
                                   (int64_t)pl->splitk_world());
         L[i].ksplit = choose_ksplit(L[i].work_hint, kc);
+        apply_scatter(pl, L[i]);
     }
     // one split-K workspace region per phase: the phases' interior and
     // boundary launches may run concurrently on two streams
@@ -2419,6 +2451,344 @@ dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned 
 dc_status_t dc_redist_destroy(dc_redist_t r) {
     DC_API_BEGIN
     delete r;
+    DC_API_END
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Channel / filter parallelism
+// ===========================================================================
+// Ranks form a pN x pC grid (rank = i_N pC + i_C). Rank (i_N, i_C) owns the
+// samples block i_N, the input channels block i_C (x, dx, its columns of w and
+// dW) and the filters block i_C (y, dy): "if the input x to a layer is
+// partitioned on its C dimension, the output y is partitioned on its F
+// dimension". Forward: every rank of a channel group computes
+// the partial y of ALL filters over its channels and the sum over channels
+// is a reduce-scatter over F; backward-data likewise over F
+// with a reduce-scatter over C; backward-filter gathers dy over the group
+// ("may require data to be gathered") and computes its dW
+// columns, summed over the sample groups (DC_ALLREDUCE). The reduce-scatter
+// runs inside the conv GEMM: its epilogue stores each fp32 partial tile
+// straight into the receive slot of the block's owner over peer memory, the
+// owner sums the p slots in rank order.
+struct dc_cplan_s {
+    ConvGeom g;
+    int pn = 1, pc = 1, rank = 0, in = 0, ic = 0;
+    Range nr, cr, fr;  // my samples, input channels, filters (global)
+    bool is_virtual = false;
+    dc_comm_s *comm = nullptr;
+    int seq = -1;
+    dc_plan_s *fwd = nullptr;  // (N_l, C_r, H, W, F): forward, backward-filter
+    dc_plan_s *bwd = nullptr;  // (N_l, C, H, W, F_r): backward-data
+    __nv_bfloat16 *wslice = nullptr;  // w[:, C_r] as [F][K][K][C_r]
+    size_t wslice_bytes = 0;
+    float *slots = nullptr;          // [pc][slot_elems] fp32 partials received
+    int64_t slot_elems = 0;
+    __nv_bfloat16 *dyfull = nullptr; // [N_l][Ho][Wo][F]: dy gathered over the group
+    uint32_t *flags = nullptr;       // [4][pc]: conv ready, conv data, gather ready, gather data
+    uint32_t *epochs = nullptr;      // [2][2]: conv exchange {epoch, count}, gather {epoch, count}
+    float *peer_slots[kCfMaxGroup] = {};
+    uint32_t *peer_flags[kCfMaxGroup] = {};
+    __nv_bfloat16 *peer_dyfull[kCfMaxGroup] = {};
+    bool resolved = false;
+    ncclComm_t sample_comm = nullptr;  // ranks with my i_C (dW allreduce over the samples)
+
+    int64_t npix_y() const { return nr.size() * g.Ho * g.Wo; }
+    int64_t npix_x() const { return nr.size() * g.H * g.W; }
+    int member(int k) const { return in * pc + k; }
+    ~dc_cplan_s() {
+        const bool local = comm && comm->group;
+        if (local) {
+            std::lock_guard<std::mutex> lk(comm->group->mu);
+            comm->group->cplans.erase({seq, rank});
+        } else {
+            for (int k = 0; k < pc; ++k) {
+                if (k == ic) continue;
+                if (peer_slots[k]) cudaIpcCloseMemHandle(peer_slots[k]);
+                if (peer_flags[k]) cudaIpcCloseMemHandle(peer_flags[k]);
+                if (peer_dyfull[k]) cudaIpcCloseMemHandle(peer_dyfull[k]);
+            }
+        }
+        if (sample_comm) ncclCommDestroy(sample_comm);
+        delete fwd;
+        delete bwd;
+        if (wslice) cudaFree(wslice);
+        if (slots) cudaFree(slots);
+        if (dyfull) cudaFree(dyfull);
+        if (flags) cudaFree(flags);
+        if (epochs) cudaFree(epochs);
+    }
+};
+
+namespace {
+
+dc_cplan_s *create_cplan(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int S, int P, int pn, int pc,
+                         int rank, dc_comm_s *comm, bool is_virtual) {
+    DC_REQUIRE(pn >= 1 && pc >= 1 && pc <= kCfMaxGroup, DC_ERR_ARG, "bad channel grid (%d, %d)", pn, pc);
+    std::unique_ptr<dc_cplan_s> c(new dc_cplan_s());
+    c->g = make_geom(N, C, H, W, F, K, S, P, 0);
+    DC_REQUIRE(C % (16 * pc) == 0 && F % (16 * pc) == 0, DC_ERR_UNSUPPORTED,
+               "channel / filter parallelism: C and F must be multiples of 16 x p_C (C=%lld F=%lld p_C=%d)",
+               (long long)C, (long long)F, pc);
+    DC_REQUIRE(pn <= N, DC_ERR_PARTITION, "p_N = %d > N = %lld", pn, (long long)N);
+    c->pn = pn, c->pc = pc, c->rank = rank, c->in = rank / pc, c->ic = rank % pc;
+    c->nr = blocked(N, pn, c->in);
+    c->cr = blocked(C, pc, c->ic);
+    c->fr = blocked(F, pc, c->ic);
+    c->is_virtual = is_virtual;
+    c->comm = comm;
+    const int64_t nl = c->nr.size();
+    c->fwd = create_plan(make_geom(nl, c->cr.size(), H, W, F, K, S, P, 0), Grid{1, 1, 1}, 0, comm, is_virtual);
+    c->bwd = create_plan(make_geom(nl, C, H, W, c->fr.size(), K, S, P, 0), Grid{1, 1, 1}, 0, comm, is_virtual);
+    if (is_virtual) return c.release();
+    const ConvGeom &g = c->g;
+    c->slot_elems = std::max(c->npix_y() * c->fr.size(), c->npix_x() * c->cr.size());
+    CK(cudaMalloc(&c->wslice, (size_t)F * K * K * c->cr.size() * 2));
+    CK(cudaMalloc(&c->slots, (size_t)pc * c->slot_elems * 4));
+    CK(cudaMalloc(&c->dyfull, (size_t)c->npix_y() * F * 2));
+    CK(cudaMemset(c->dyfull, 0, (size_t)c->npix_y() * F * 2));
+    CK(cudaMalloc(&c->flags, sizeof(uint32_t) * 4 * pc));
+    CK(cudaMemset(c->flags, 0, sizeof(uint32_t) * 4 * pc));
+    CK(cudaMalloc(&c->epochs, sizeof(uint32_t) * 4));
+    CK(cudaMemset(c->epochs, 0, sizeof(uint32_t) * 4));
+    (void)g;
+    const int world = pn * pc;
+    if (world > 1) {
+        DC_REQUIRE(comm && comm->world == world && comm->rank == rank, DC_ERR_ARG,
+                   "channel grid (%d, %d) needs a communicator of %d ranks", pn, pc, world);
+        c->seq = comm->cplan_seq++;
+        if (comm->group) {
+            std::lock_guard<std::mutex> lk(comm->group->mu);
+            comm->group->cplans[{c->seq, rank}] = c.get();
+        } else {
+            if (pn > 1) NK(ncclCommSplit(comm->nccl, c->ic, rank, &c->sample_comm, nullptr));
+            struct Handles {
+                cudaIpcMemHandle_t slots, flags, dyfull;
+            } h{};
+            CK(cudaIpcGetMemHandle(&h.slots, c->slots));
+            CK(cudaIpcGetMemHandle(&h.flags, c->flags));
+            CK(cudaIpcGetMemHandle(&h.dyfull, c->dyfull));
+            auto all = comm_allgather(comm, &h, sizeof h);
+            for (int k = 0; k < pc; ++k) {
+                if (k == c->ic) continue;
+                Handles x;
+                std::memcpy(&x, all.data() + c->member(k) * sizeof x, sizeof x);
+                void *p = nullptr;
+                CK(cudaIpcOpenMemHandle(&p, x.slots, cudaIpcMemLazyEnablePeerAccess));
+                c->peer_slots[k] = reinterpret_cast<float *>(p);
+                CK(cudaIpcOpenMemHandle(&p, x.flags, cudaIpcMemLazyEnablePeerAccess));
+                c->peer_flags[k] = reinterpret_cast<uint32_t *>(p);
+                CK(cudaIpcOpenMemHandle(&p, x.dyfull, cudaIpcMemLazyEnablePeerAccess));
+                c->peer_dyfull[k] = reinterpret_cast<__nv_bfloat16 *>(p);
+            }
+            c->resolved = true;
+        }
+    }
+    c->peer_slots[c->ic] = c->slots, c->peer_flags[c->ic] = c->flags, c->peer_dyfull[c->ic] = c->dyfull;
+    if (world == 1) c->resolved = true;
+    CK(cudaDeviceSynchronize());
+    return c.release();
+}
+
+void resolve_cplan(dc_cplan_s *c) {
+    if (c->resolved) return;
+    LocalGroup &G = *c->comm->group;
+    std::lock_guard<std::mutex> lk(G.mu);
+    for (int k = 0; k < c->pc; ++k) {
+        auto it = G.cplans.find({c->seq, c->member(k)});
+        DC_REQUIRE(it != G.cplans.end(), DC_ERR_ARG, "loopback group: rank %d has not created channel plan #%d",
+                   c->member(k), c->seq);
+        c->peer_slots[k] = it->second->slots;
+        c->peer_flags[k] = it->second->flags;
+        c->peer_dyfull[k] = it->second->dyfull;
+    }
+    c->resolved = true;
+}
+
+// flags kind: 0 conv ready, 1 conv data, 2 gather ready, 3 gather data
+CfFlags cf_flags(const dc_cplan_s *c, int kind) {
+    CfFlags f{};
+    f.n = c->pc;
+    for (int k = 0; k < c->pc; ++k) {
+        f.out[k] = c->peer_flags[k] + kind * c->pc + c->ic;
+        f.in[k] = c->flags + kind * c->pc + k;
+    }
+    f.epoch = c->epochs;
+    return f;
+}
+
+// The reduce-scatter half of a channel-parallel conv call: the partial of
+// block k goes to member k's slot [my index]; after the GEMM (queued by
+// `gemm`), wait for every member's partial and sum them into `out`.
+template <class Gemm>
+void cf_reduce_scatter(dc_cplan_s *c, dc_plan_s *sub, int64_t seg, int64_t npix, void *out, cudaStream_t st,
+                       Gemm &&gemm) {
+    resolve_cplan(c);
+    launch_cf_handshake(cf_flags(c, 0), st);  // every owner's slots are free
+    for (int k = 0; k < c->pc; ++k) sub->scat[k] = c->peer_slots[k] + (int64_t)c->ic * c->slot_elems;
+    sub->scat_seg = (int)seg;
+    try {
+        gemm();
+    } catch (...) {
+        sub->scat_seg = 0;
+        throw;
+    }
+    sub->scat_seg = 0;
+    const CfFlags d = cf_flags(c, 1);
+    launch_signal(const_cast<uint32_t *const *>(d.out), d.n, 0, c->epochs, st);
+    launch_cf_wait(d, st);
+    launch_cf_reduce(c->slots, c->pc, npix, (int)seg, out, (int)seg, c->epochs, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+dc_status_t dc_cplan_create(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int stride, int pad,
+                            int pn, int pc, dc_dtype_t dtype, dc_comm_t comm, dc_cplan_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
+    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "channel / filter parallelism: bf16 plans only");
+    const int rank = comm ? comm->rank : 0;
+    if (comm) CK(cudaSetDevice(comm->device));
+    *out = create_cplan(N, C, H, W, F, K, stride, pad, pn, pc, rank, comm, false);
+    DC_API_END
+}
+
+dc_status_t dc_cplan_create_virtual(int64_t N, int64_t C, int64_t H, int64_t W, int64_t F, int K, int stride,
+                                    int pad, int pn, int pc, int rank, dc_cplan_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr && rank >= 0 && rank < pn * pc, DC_ERR_ARG, "bad argument");
+    *out = create_cplan(N, C, H, W, F, K, stride, pad, pn, pc, rank, nullptr, true);
+    DC_API_END
+}
+
+dc_status_t dc_cplan_query(dc_cplan_t c, dc_tensor_t t, dc_shard_desc_t *desc, int64_t *c0) {
+    DC_API_BEGIN
+    DC_REQUIRE(c && desc, DC_ERR_ARG, "null argument");
+    int64_t first = 0;
+    switch (t) {
+    case DC_X:
+    case DC_DX:
+        *desc = describe(c->fwd->rp, t);
+        first = c->cr.lo;
+        break;
+    case DC_Y:
+    case DC_DY:
+        *desc = describe(c->bwd->rp, t);
+        first = c->fr.lo;
+        break;
+    case DC_W: {  // replicated: the whole [F][K][K][C] bf16 filter bank
+        const ConvGeom &g = c->g;
+        dc_shard_desc_t d{};
+        d.n = g.F, d.h = g.K, d.w = g.K, d.c = g.C, d.c_pad = g.C, d.hb = g.K, d.wb = g.K;
+        d.stride_w = g.C, d.stride_h = g.K * g.C, d.stride_n = g.K * g.K * g.C;
+        d.bytes = (size_t)g.F * g.K * g.K * g.C * 2;
+        *desc = d;
+        break;
+    }
+    case DC_DW:
+        *desc = describe(c->fwd->rp, DC_DW);
+        first = c->cr.lo;
+        break;
+    default:
+        fail(DC_ERR_ARG, "unknown tensor kind");
+    }
+    desc->n0 = t == DC_W || t == DC_DW ? 0 : c->nr.lo;
+    if (c0) *c0 = first;
+    DC_API_END
+}
+
+dc_status_t dc_cconv_fwd(dc_cplan_t c, const void *x, const void *w, void *y, unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(c && x && w && y, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(!c->is_virtual, DC_ERR_ARG, "virtual plans have no data");
+    DC_REQUIRE(flags == 0, DC_ERR_ARG, "unknown flags 0x%x", flags);
+    const bool local = c->comm && c->comm->group;
+    NoPdlScope no_pdl(local);
+    cudaStream_t st = (cudaStream_t)stream;
+    const ConvGeom &g = c->g;
+    const int64_t cl = c->cr.size();
+    // my columns of the replicated filter bank: w[:, :, :, C_r]
+    RedistPiece wp{};
+    wp.src = reinterpret_cast<const uint4 *>(reinterpret_cast<const __nv_bfloat16 *>(w) + c->cr.lo);
+    wp.dst = reinterpret_cast<uint4 *>(c->wslice);
+    wp.nn = 1, wp.rows = (int)(g.F * g.K * g.K), wp.run = (int)(cl * 2 / 16);
+    wp.s_sh = g.C * 2 / 16, wp.d_sh = cl * 2 / 16;
+    launch_redist_copy(&wp, 1, st);
+    dc_plan_s *sub = c->fwd;
+    ensure_local_resources(sub);
+    cf_reduce_scatter(c, sub, c->fr.size(), c->npix_y(), y, st, [&] {
+        GemmLaunch L;
+        prepare_fwd(sub, x, c->wslice, y, L, st);
+        launch_rects(L, {whole(L)}, x, describe(sub->rp, DC_X), L.cin, (int)sub->rp.nrange.size(), st);
+    });
+    DC_API_END
+}
+
+dc_status_t dc_cconv_bwd_data(dc_cplan_t c, const void *dy, const void *w, void *dx, unsigned flags,
+                              void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(c && dy && w && dx, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(!c->is_virtual, DC_ERR_ARG, "virtual plans have no data");
+    DC_REQUIRE(flags == 0, DC_ERR_ARG, "unknown flags 0x%x", flags);
+    const bool local = c->comm && c->comm->group;
+    NoPdlScope no_pdl(local);
+    cudaStream_t st = (cudaStream_t)stream;
+    const ConvGeom &g = c->g;
+    dc_plan_s *sub = c->bwd;
+    ensure_local_resources(sub);
+    // my filters' rows of the replicated bank: w[F_r, :, :, :]
+    const __nv_bfloat16 *wf = reinterpret_cast<const __nv_bfloat16 *>(w) + c->fr.lo * g.K * g.K * g.C;
+    cf_reduce_scatter(c, sub, c->cr.size(), c->npix_x(), dx, st,
+                      [&] { run_bwd_data(sub, const_cast<void *>(dy), wf, dx, 0, st); });
+    DC_API_END
+}
+
+dc_status_t dc_cconv_bwd_filter(dc_cplan_t c, const void *x, const void *dy, float *dw, unsigned flags,
+                                void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(c && x && dy && dw, DC_ERR_ARG, "null argument");
+    DC_REQUIRE(!c->is_virtual, DC_ERR_ARG, "virtual plans have no data");
+    DC_REQUIRE((flags & ~DC_ALLREDUCE) == 0, DC_ERR_ARG, "unknown flags 0x%x", flags);
+    const bool local = c->comm && c->comm->group;
+    NoPdlScope no_pdl(local);
+    cudaStream_t st = (cudaStream_t)stream;
+    const ConvGeom &g = c->g;
+    resolve_cplan(c);
+    // gather dy over the channel group: my filters' block of every pixel into
+    // every member's [N_l][Ho][Wo][F] (one P2P all-to-all launch)
+    const int64_t fl = c->fr.size();
+    RedistP2P x2{};
+    x2.epoch_ctr = c->epochs + 2;
+    x2.nblocks = local ? std::max(8, std::min(kRedistBlocks, 4 * device_sm_count() / (c->pn * c->pc)))
+                       : kRedistBlocks;
+    for (int k = 0; k < c->pc; ++k) {
+        RedistPiece &p = x2.piece[x2.npiece++];
+        p.src = reinterpret_cast<const uint4 *>(dy);
+        p.dst = reinterpret_cast<uint4 *>(c->peer_dyfull[k] + c->fr.lo);
+        p.nn = 1, p.rows = (int)c->npix_y(), p.run = (int)(fl * 2 / 16);
+        p.s_sh = fl * 2 / 16, p.d_sh = g.F * 2 / 16;
+        x2.ready_out[x2.n_ready_out++] = c->peer_flags[k] + 2 * c->pc + c->ic;
+        x2.ready_in[x2.n_ready_in++] = c->flags + 2 * c->pc + k;
+        x2.data_out[x2.n_data_out++] = c->peer_flags[k] + 3 * c->pc + c->ic;
+        x2.data_in[x2.n_data_in++] = c->flags + 3 * c->pc + k;
+    }
+    launch_redist_p2p(x2, st);
+    dc_plan_s *sub = c->fwd;
+    ensure_local_resources(sub);
+    run_bwd_filter(sub, x, c->dyfull, dw, st, false);
+    if ((flags & DC_ALLREDUCE) && c->pn > 1) {
+        DC_REQUIRE(!local, DC_ERR_UNSUPPORTED, "dW allreduce needs real ranks (loopback group: DC_ALLREDUCE off)");
+        NK(ncclAllReduce(dw, dw, (size_t)g.F * g.K * g.K * c->cr.size(), ncclFloat32, ncclSum, c->sample_comm, st));
+    }
+    DC_API_END
+}
+
+dc_status_t dc_cplan_destroy(dc_cplan_t c) {
+    DC_API_BEGIN
+    delete c;
     DC_API_END
 }
 

@@ -32,6 +32,18 @@ __device__ __forceinline__ uint8_t *align1024(uint8_t *p) {
     const uint32_t a = smem_u32(p);
     return p + ((1024 - (a & 1023)) & 1023);
 }
+// fp32 output column `col` of GEMM pixel (i, j) of sample n: plain out, or
+// the scatter target of the column's channel block (ConvV2Params::scat)
+__device__ __forceinline__ float *f32_out(const ConvV2Params &p, int n, int i, int j, int col) {
+    float *base = reinterpret_cast<float *>(p.out);
+    if (p.scat_seg) {
+        const int ow = col / p.scat_seg;
+        base = p.scat[ow];
+        col -= ow * p.scat_seg;
+    }
+    return base + (long long)n * p.out_sn + (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
+           (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + col;
+}
 __device__ __forceinline__ uint32_t pack2(uint32_t lo, uint32_t hi) {
     __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(lo), __uint_as_float(hi));
     return *reinterpret_cast<uint32_t *>(&v);
@@ -577,11 +589,10 @@ __global__ void __launch_bounds__(kV2Threads, 1)
                                                  __uint_as_float(v[4 * q + 2]), __uint_as_float(v[4 * q + 3]));
                     }
                 } else if (p.out_f32) {
-                    // fp32 output (3xTF32 path): 16 columns = two 32-byte halves,
-                    // the second only when the (8-padded) channel count reaches it
-                    float *of = reinterpret_cast<float *>(p.out) + (long long)c.n * p.out_sn +
-                                (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
-                                (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + c.o0 + c16 * 16;
+                    // fp32 output (3xTF32 path, channel-parallel partials): 16
+                    // columns = two 32-byte halves, the second only when the
+                    // (8-padded) channel count reaches it
+                    float *of = f32_out(p, c.n, i, j, c.o0 + c16 * 16);
                     if (valid) {
                         if (c.o0 + c16 * 16 < p.nout_p) st_global_v8(of, *reinterpret_cast<const uint32_t(*)[8]>(&v[0]));
                         if (c.o0 + c16 * 16 + 8 < p.nout_p)
@@ -815,9 +826,7 @@ __global__ void conv_v2_reduce_kernel(const __grid_constant__ ConvV2Params p) {
             b.x += d.x, b.y += d.y, b.z += d.z, b.w += d.w;
         }
         if (p.out_f32) {
-            float4 *of = reinterpret_cast<float4 *>(reinterpret_cast<float *>(p.out) + (long long)n * p.out_sn +
-                                                    (long long)(p.out_h0 + p.out_dh * i) * p.out_sh +
-                                                    (long long)(p.out_w0 + p.out_dw * j) * p.out_sw + v * 8);
+            float4 *of = reinterpret_cast<float4 *>(f32_out(p, n, i, j, v * 8));
             of[0] = a, of[1] = b;
             continue;
         }

@@ -98,6 +98,12 @@ struct ConvV2Params {
     // a_seg > 0 maps weight K channels >= a_seg (in 16-bit units) a_seg lower
     // in the input (x_hi x_hi x_lo against w_hi w_lo w_hi); out_f32 stores fp32.
     int kind, a_seg, out_f32;
+    // fp32 output scattered by output-channel block (channel / filter
+    // parallelism, capi.cu dc_cconv_*): column o goes to scat[o / scat_seg] at
+    // channel o % scat_seg of a tensor with channel pitch scat_seg (out_s*
+    // strides in that pitch); scat_seg = 0: plain out
+    float *scat[8];
+    int scat_seg;
 };
 
 size_t conv_v2_smem_bytes(const ConvV2Params &p);
