@@ -126,8 +126,10 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled (every 100 ms) during the
-    timed region. Field names differ across drivers: probe and fall back."""
+    """SM clock + clock-event (throttle) reasons sampled every ~5 ms through
+    NVML during the timed region (a 120 ms region still gets ~20 samples);
+    nvidia-smi at 100 ms as the fallback. Field names differ across drivers:
+    probe and fall back."""
     REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     VARIANTS = [",".join(["clocks.sm", "clocks.max.sm"] + [f"clocks_event_reasons.{r}" for r in REASONS]),
                 ",".join(["clocks.sm", "clocks.max.sm"] + [f"clocks_throttle_reasons.{r}" for r in REASONS]),
@@ -135,8 +137,43 @@ class ClockSampler:
 
     def __init__(self, gpu: int):
         self.gpu, self.proc, self.lines, self.q = gpu, None, [], None
+        self.nvml, self.samples, self.stop_flag = None, [], threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.gpu)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
 
     def start(self):
+        try:
+            nv, h = self._nvml_handle()
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop_flag.is_set():
+                    try:
+                        sm = float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+                        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, [n for n, b in bits.items() if r & b]))
+                    except Exception:
+                        pass
+                    time.sleep(0.005)
+            self.nvml = threading.Thread(target=poll, daemon=True)
+            self.nvml.start()
+            time.sleep(0.05)
+            return
+        except Exception:
+            self.nvml = None
         for q in self.VARIANTS:
             try:
                 r = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
@@ -158,6 +195,15 @@ class ClockSampler:
         time.sleep(0.3)
 
     def stop(self):
+        if self.nvml is not None:
+            self.stop_flag.set()
+            self.nvml.join(timeout=2)
+            sm = [s for s, _ in self.samples]
+            reasons = sorted({n for _, rs in self.samples for n in rs})
+            mx = self.max_mhz
+            load = [v for v in sm if mx and v > 0.3 * mx] or sm
+            return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": reasons,
+                    "samples": len(sm), "fields": "NVML clocks (SM) + current clock-event reasons, 5 ms"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         time.sleep(0.25)
@@ -269,7 +315,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--decomp", default="spatial",
                     help="spatial (model picks pH x pW, pN = 1: BASELINE configs[3]) | auto (model, all grids) | "
-                         "pn,ph,pw (0 entries: model's choice)")
+                         "pn,ph,pw (0 entries: model's choice) | strategy (network workloads: the model's "
+                         "parallel execution strategy, one grid per layer with redistributions between, "
+                         "PAPER.md:216-228)")
     ap.add_argument("--halo", default="p2p", choices=["p2p", "nccl"])
     ap.add_argument("--no-overlap", action="store_true",
                     help="ablation: finish each halo exchange before the conv (DC_NO_OVERLAP)")
@@ -355,7 +403,16 @@ def main():
     # place): the pure spatial grid with the least total model cost over the
     # layers (PAPER.md:218-226 with no redistribution between layers) ----
     net_grid = None
-    if NET:
+    strategy = None
+    if args.decomp == "strategy":
+        if not NET:
+            raise SystemExit("--decomp strategy needs a network workload (*_net)")
+        # one grid per layer: the shortest path over the per-layer candidates
+        # with Shuffle edges (chain: parent = previous layer)
+        chain = [tuple(l[1:]) + (i - 1,) for i, l in enumerate(layers)]
+        sgrids, stotal = dc.dc_model_strategy(chain, world)
+        strategy = {"grids": [list(g) for g in sgrids], "model_step_ms": stotal * 1e3}
+    elif NET:
         if args.decomp in ("auto", "spatial"):
             best = None
             for ph in range(world, 0, -1):
@@ -373,10 +430,13 @@ def main():
             net_grid = tuple(int(v) for v in args.decomp.split(","))
     # ---- per-layer plans and resident inputs ----
     L = []
-    for l in layers:
+    for li, l in enumerate(layers):
         name, N, C, H, W, F, K, S, P = l
-        decomp = net_grid or {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
-            int(v) for v in args.decomp.split(","))
+        if strategy:
+            decomp = tuple(strategy["grids"][li])
+        else:
+            decomp = net_grid or {"auto": (0, 0, 0), "spatial": (1, 0, 0)}.get(args.decomp) or tuple(
+                int(v) for v in args.decomp.split(","))
         plan = dc.dc_plan_create(N, C, H, W, F, K, S, P, decomp, DTYPE, comm)
         if args.splitk_basis:
             dc.dc_plan_set_splitk_world(plan, args.splitk_basis)
@@ -424,6 +484,23 @@ def main():
         L.append(dict(l=l, plan=plan, decomp=chosen, pred=pred, xd=xd, dyd=dyd, xb=xb, dyb=dyb, w=wt, y=y,
                       dx=dx, dw=dw, bn_mean=bn_mean, bn_var=bn_var, gamma=gamma, beta=beta, dgamma=dgamma,
                       dbeta=dbeta, host=host))
+    # ---- redistributions where consecutive layers use different grids
+    # (PAPER.md:151-153): forward the BN / ReLU output (dense, this layer's
+    # grid) into the next layer's margined x; backward the next layer's dx
+    # into this layer's dense BN-output gradient ----
+    n_shuffles = 0
+    if NET:
+        for i in range(len(L) - 1):
+            d, n = L[i], L[i + 1]
+            if tuple(d["decomp"]) == tuple(n["decomp"]):
+                continue
+            yd = dc.dc_plan_query(d["plan"], dc.DC_Y)
+            d["act"] = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=TDT, device="cuda")
+            d["dout"] = dc.wrap_device_buffer(dc.dc_buffer_alloc(d["plan"], dc.DC_Y),
+                                              (yd["n"], yd["h"], yd["w"], yd["c_pad"]), TDT)
+            d["r_fwd"] = dc.dc_redist_create(d["plan"], dc.DC_Y, n["plan"], dc.DC_X)
+            d["r_bwd"] = dc.dc_redist_create(n["plan"], dc.DC_DX, d["plan"], dc.DC_Y)
+            n_shuffles += 1
     torch.cuda.synchronize()
 
     fused = not ("bn" in ablate or args.no_fused_bn)
@@ -467,6 +544,13 @@ def main():
             ops += conv_fwd_ops(i, d)
             if i + 1 < len(L):
                 n = L[i + 1]
+                if "r_fwd" in d:  # a different grid next: BN / ReLU densely, then the shuffle
+                    ops.append((i, "act", lambda d=d: dc.dc_bn_apply(
+                        d["plan"], d["y"], d["bn_mean"], d["bn_var"], d["gamma"], d["beta"], 1e-5, None,
+                        dc.DC_RELU, None, d["act"], sp)))
+                    ops.append((i, "shuf", lambda d=d, n=n: dc.dc_redistribute(d["r_fwd"], d["act"], n["xb"], 0,
+                                                                               sp)))
+                    continue
                 ops.append((i, "act", lambda d=d, n=n: dc.dc_bn_apply(
                     d["plan"], d["y"], d["bn_mean"], d["bn_var"], d["gamma"], d["beta"], 1e-5, None, dc.DC_RELU,
                     n["plan"], n["xb"].data_ptr(), sp)))
@@ -475,8 +559,13 @@ def main():
             ops += conv_bwd_ops(i, d)
             if i > 0:
                 p = L[i - 1]
-                ops.append((i - 1, "bnb", lambda d=d, p=p: dc.dc_bn_backward(
-                    p["plan"], d["dx"], p["y"], p["bn_mean"], p["bn_var"], p["gamma"], p["beta"],
+                dout = d["dx"]
+                if "r_bwd" in p:  # the gradient back onto the previous layer's grid
+                    ops.append((i - 1, "shufb", lambda d=d, p=p: dc.dc_redistribute(p["r_bwd"], d["dx"], p["dout"],
+                                                                                    0, sp)))
+                    dout = p["dout"]
+                ops.append((i - 1, "bnb", lambda d=d, p=p, dout=dout: dc.dc_bn_backward(
+                    p["plan"], dout, p["y"], p["bn_mean"], p["bn_var"], p["gamma"], p["beta"],
                     p["dyb"].data_ptr(), 1e-5, None, dc.DC_RELU, p["dgamma"], p["dbeta"], None, sp)))
         return ops
 
@@ -668,15 +757,21 @@ def main():
                                    **({"bwd_filter_ms": t["bpw"], "bwd_data_ms": t["bpx"]} if "bpw" in t else {}),
                                    **({"bn_apply_relu_ms": t["act"]} if "act" in t else {}),
                                    **({"bn_relu_bwd_ms": t["bnb"]} if "bnb" in t else {}),
+                                   **({"shuffle_fwd_ms": t["shuf"]} if "shuf" in t else {}),
+                                   **({"shuffle_bwd_ms": t["shufb"]} if "shufb" in t else {}),
                                    "fwd_tflops": layer_flops(d["l"]) / (f_ms / 1e3) / 1e12,
                                    "bwd_tflops": 2 * layer_flops(d["l"]) / (b_ms / 1e3) / 1e12}
                                   for d, f_ms, b_ms, t in per],
                        "network": ("end to end: conv -> spatial BN -> BN apply + ReLU into the next layer's "
                                    "margined input; backward through BN / ReLU (group sums) into the previous "
-                                   "layer's margined dy; one grid for all layers") if NET else
+                                   "layer's margined dy; " + (
+                                       f"one grid per layer (model strategy), {n_shuffles} redistributions "
+                                       "each way" if strategy else "one grid for all layers")) if NET else
                                   "conv stack: every layer on its own resident inputs",
+                       **({"strategy": strategy} if strategy else {}),
                        "parallelism": {"auto": "per-layer model-chosen (pN,pH,pW)",
-                                       "spatial": "pure spatial, per-layer model-chosen (1,pH,pW)"}.get(
+                                       "spatial": "pure spatial, per-layer model-chosen (1,pH,pW)",
+                                       "strategy": "model strategy: per-layer grids + redistribution"}.get(
                                            args.decomp, args.decomp),
                        "halo": args.halo + ("+no-overlap" if args.no_overlap else ""), "l2": "working set per step > L2 (126 MB); no explicit flush",
                        "perf_model_table": os.path.relpath(table, ROOT) if table else "roofline estimate",
@@ -711,6 +806,10 @@ def main():
     import gc
     gc.collect()
     torch.cuda.synchronize()
+    for d in L:
+        for k in ("r_fwd", "r_bwd"):
+            if k in d:
+                dc.dc_redist_destroy(d[k])
     for d in L:
         dc.dc_plan_destroy(d["plan"])
     dc.dc_comm_destroy(comm)

@@ -206,7 +206,9 @@ dc_status_t dc_plan_destroy(dc_plan_t plan);
 
 /* COLLECTIVE. Allocate (and zero) the margined buffer of t in {DC_X, DC_DY}
  * with cudaMalloc and map it into the neighbours' address spaces for direct
- * P2P halo stores. Owned by the plan; freed by dc_plan_destroy. */
+ * P2P halo stores; or (t in {DC_Y, DC_DX}, not collective) a dense shard
+ * buffer that a redistribution may target (dc_redist_create maps it into the
+ * senders). Owned by the plan; freed by dc_plan_destroy. */
 dc_status_t dc_buffer_alloc(dc_plan_t plan, dc_tensor_t t, void **dev_ptr);
 
 /* Fill the OWNED block of a margined buffer (t in {DC_X, DC_DY}, dst from
@@ -331,10 +333,10 @@ typedef struct dc_redist_s *dc_redist_t;
 /* COLLECTIVE over the plans' communicator (virtual plans: host-only
  * geometry for dc_redist_bytes). Source: tensor tf (DC_Y / DC_DX: the dense
  * owned shard; DC_X / DC_DY: the owned interior of the margined buffer) of
- * plan `from`; destination: the owned interior of the margined tensor tt
- * (DC_X / DC_DY) of plan `to`, whose dc_buffer_alloc buffer must exist on
- * every rank before this call (it is mapped into the senders for the direct
- * transport). The two tensors must have the same global N, H, W, channels
+ * plan `from`; destination: tensor tt of plan `to` (the owned interior of the
+ * margined DC_X / DC_DY, or the dense DC_Y / DC_DX), whose dc_buffer_alloc
+ * buffer must exist on every rank before this call (it is mapped into the
+ * senders for the direct transport). The two tensors must have the same global N, H, W, channels
  * and pixel layout (fp32 plans: margined source only, DC_ERR_UNSUPPORTED
  * otherwise). Errors: DC_ERR_ARG, DC_ERR_SHAPE, DC_ERR_UNSUPPORTED. */
 dc_status_t dc_redist_create(dc_plan_t from, dc_tensor_t tf, dc_plan_t to, dc_tensor_t tt, dc_redist_t *out);

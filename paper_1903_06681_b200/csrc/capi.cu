@@ -168,6 +168,7 @@ struct dc_plan_s {
     cudaEvent_t ev_ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     BufState buf[2];                 // 0: X, 1: DY
+    BufState dense[2];               // dc_buffer_alloc'd dense 0: Y, 1: DX (redistribution targets)
     uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
     std::map<int, uint32_t *> peer_flags;
     uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local)
@@ -226,6 +227,8 @@ struct dc_plan_s {
             if (b.owned && b.ptr) cudaFree(b.ptr);
             if (b.stage) cudaFree(b.stage);
         }
+        for (auto &b : dense)
+            if (b.owned && b.ptr) cudaFree(b.ptr);
         const bool ipc = !(comm && comm->group);
         if (comm && comm->group) {
             std::lock_guard<std::mutex> lk(comm->group->mu);
@@ -1156,13 +1159,21 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     for (auto &f : ph) nactive += f.active ? 1 : 0;
     if (!overlap && nactive > 1 && pl->s_ph[0]) {
         // stride phases are independent GEMMs with disjoint outputs and split-K
-        // workspaces: one stream each, so their ramp-up / tail / reduce overlap
+        // workspaces: one stream each, run side by side on SM shares
+        // proportional to their taps (their work per tile), so all of them
+        // sweep dy in the same tile order at the same pace and read each dy
+        // tile from HBM once (L2 serves the other phases) instead of once per
+        // phase
         CK(cudaEventRecord(pl->ev_ph[0], st));
+        int taps = 0;
+        for (auto &f : ph) taps += f.active ? f.T : 0;
+        const int sms = device_sm_count();
         int k = 0;
         for (size_t i = 0; i < ph.size(); ++i) {
             if (!ph[i].active) continue;
             cudaStream_t sp = pl->s_ph[k];
             CK(cudaStreamWaitEvent(sp, pl->ev_ph[0], 0));
+            L[i].max_ctas = std::max(2, sms * ph[i].T / taps);
             launch_rects(L[i], {whole(L[i])}, dy, dyd, kc, (int)rp.nrange.size(), sp);
             CK(cudaEventRecord(pl->ev_ph[1 + k], sp));
             ++k;
@@ -1776,8 +1787,21 @@ dc_status_t dc_plan_destroy(dc_plan_t plan) {
 
 dc_status_t dc_buffer_alloc(dc_plan_t pl, dc_tensor_t t, void **dev_ptr) {
     DC_API_BEGIN
-    DC_REQUIRE(pl && dev_ptr && (t == DC_X || t == DC_DY), DC_ERR_ARG, "bad argument");
+    DC_REQUIRE(pl && dev_ptr && (t == DC_X || t == DC_DY || t == DC_Y || t == DC_DX), DC_ERR_ARG, "bad argument");
     DC_REQUIRE(!pl->is_virtual, DC_ERR_ARG, "virtual plan has no device buffers");
+    if (t == DC_Y || t == DC_DX) {  // dense: a redistribution target (mapped by dc_redist_create)
+        BufState &D = pl->dense[t == DC_Y ? 0 : 1];
+        DC_REQUIRE(D.ptr == nullptr, DC_ERR_ARG, "buffer already allocated for this tensor");
+        const dc_shard_desc_t d = describe(pl->rp, t);
+        cudaError_t e = cudaMalloc(&D.ptr, std::max<size_t>(d.bytes, 256));
+        DC_REQUIRE(e == cudaSuccess, DC_ERR_OOM, "cudaMalloc(%zu): %s", d.bytes, cudaGetErrorString(e));
+        D.owned = true;
+        D.bytes = d.bytes;
+        CK(cudaMemset(D.ptr, 0, std::max<size_t>(d.bytes, 256)));
+        CK(cudaDeviceSynchronize());
+        *dev_ptr = D.ptr;
+        return DC_OK;
+    }
     const int which = t == DC_X ? 0 : 1;
     BufState &B = pl->buf[which];
     const dc_shard_desc_t d = describe(pl->rp, t);
@@ -2194,6 +2218,17 @@ std::array<int64_t, 4> global_extent(const ConvGeom &g, dc_tensor_t t) {
     return {g.N, g.Ho, g.Wo, g.F};
 }
 
+// The dc_buffer_alloc buffer of tensor t of a plan (margined X / DY, dense Y / DX).
+void *alloc_buffer(const dc_plan_s *pl, dc_tensor_t t) {
+    switch (t) {
+    case DC_X: return pl->buf[0].ptr;
+    case DC_DY: return pl->buf[1].ptr;
+    case DC_Y: return pl->dense[0].ptr;
+    case DC_DX: return pl->dense[1].ptr;
+    default: return nullptr;
+    }
+}
+
 Range isect(int64_t a0, int64_t an, int64_t b0, int64_t bn) {
     return Range{std::max(a0, b0), std::min(a0 + an, b0 + bn)};
 }
@@ -2239,7 +2274,7 @@ void resolve_redist_peers(dc_redist_s *r) {
             }
             r->peer_flags[p.peer] = q->flags;
             if (!pass) {
-                void *d = local_peer(r->to, p.peer)->buf[r->which].ptr;
+                void *d = alloc_buffer(local_peer(r->to, p.peer), r->tt);
                 DC_REQUIRE(d != nullptr, DC_ERR_ARG, "redistribution: rank %d has no dc_buffer_alloc buffer",
                            p.peer);
                 r->peer_dst[p.peer] = d;
@@ -2323,7 +2358,7 @@ dc_status_t dc_redist_create(dc_plan_t from, dc_tensor_t tf, dc_plan_t to, dc_te
     DC_API_BEGIN
     DC_REQUIRE(from && to && out, DC_ERR_ARG, "null argument");
     DC_REQUIRE(tf == DC_X || tf == DC_Y || tf == DC_DX || tf == DC_DY, DC_ERR_ARG, "bad source tensor");
-    DC_REQUIRE(tt == DC_X || tt == DC_DY, DC_ERR_ARG, "the destination is a margined x or dy (DC_X / DC_DY)");
+    DC_REQUIRE(tt == DC_X || tt == DC_Y || tt == DC_DX || tt == DC_DY, DC_ERR_ARG, "bad destination tensor");
     DC_REQUIRE(from->is_virtual == to->is_virtual, DC_ERR_ARG, "both plans virtual, or neither");
     DC_REQUIRE(from->rp.rank == to->rp.rank && from->world() == to->world(), DC_ERR_ARG,
                "plans of different ranks / world sizes");
@@ -2363,7 +2398,7 @@ dc_status_t dc_redist_create(dc_plan_t from, dc_tensor_t tf, dc_plan_t to, dc_te
     if (!r->is_virtual && r->world > 1) {
         dc_comm_s *c = r->comm;
         DC_REQUIRE(c && (c->nccl || c->group), DC_ERR_ARG, "redistribution needs a communicator");
-        void *dst = to->buf[r->which].ptr;
+        void *dst = alloc_buffer(to, tt);
         DC_REQUIRE(dst != nullptr, DC_ERR_ARG,
                    "redistribution: allocate the destination with dc_buffer_alloc (on every rank) first");
         r->seq = c->redist_seq++;
@@ -2430,7 +2465,7 @@ dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned 
     cudaStream_t st = (cudaStream_t)stream;
     const bool local = r->comm && r->comm->group;
     NoPdlScope no_pdl(local);  // (loopback: ranks share the SMs)
-    join_import(r->to, r->which, st);
+    if (r->tt == DC_X || r->tt == DC_DY) join_import(r->to, r->which, st);
     if (r->tf == DC_X || r->tf == DC_DY) join_import(r->from, r->tf == DC_X ? 0 : 1, st);
     if (r->world == 1) {
         const dc_shard_desc_t &me = r->dst_all[0];
@@ -2441,7 +2476,7 @@ dc_status_t dc_redistribute(dc_redist_t r, const void *src, void *dst, unsigned 
         DC_REQUIRE(!local, DC_ERR_UNSUPPORTED, "DC_HALO_NCCL needs real ranks (loopback group)");
         redist_nccl(r, src, dst, st);
     } else {
-        DC_REQUIRE(dst == r->to->buf[r->which].ptr, DC_ERR_ARG,
+        DC_REQUIRE(dst == alloc_buffer(r->to, r->tt), DC_ERR_ARG,
                    "P2P redistribution writes the destination plan's dc_buffer_alloc buffer");
         redist_p2p(r, src, st);
     }

@@ -113,8 +113,8 @@ def test_redist_errors(dc):
     try:
         with pytest.raises(dc.DCError):          # channel counts differ (y of a: 32, x of c: 16)
             dc.dc_redist_create(a, dc.DC_Y, c, dc.DC_X)
-        with pytest.raises(dc.DCError):          # destination must be margined x / dy
-            dc.dc_redist_create(a, dc.DC_Y, b, dc.DC_Y)
+        with pytest.raises(dc.DCError):          # the destination is an activation / gradient
+            dc.dc_redist_create(a, dc.DC_Y, b, dc.DC_W)
         with pytest.raises(dc.DCError):          # fp32: dense y -> split [hi | lo] x
             dc.dc_redist_create(f32a, dc.DC_Y, f32b, dc.DC_X)
         with pytest.raises(dc.DCError):          # mixed dtypes

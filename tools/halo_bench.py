@@ -5,7 +5,8 @@ send/recv baseline), one process per GPU:
 
 For each layer (shapes of the mesh2k_n8 stack plus larger slabs) and each
 transport, times 50 back-to-back dc_halo_exchange calls of x on the layer's
-pure H split with CUDA events (after warm-up and a barrier; max over ranks)
+pure H split, captured in one CUDA graph and replayed, with CUDA events
+(after warm-up and a barrier; max over ranks)
 and reports the bytes each rank sends per exchange, the time per exchange and
 the achieved send bandwidth per GPU (GB/s, NVLink 5: 900 GB/s per direction).
 Prints one JSON line per case on rank 0."""
@@ -45,18 +46,28 @@ def main():
         sent = sum(m["rows"] * m["cols"] for m in dc.dc_plan_halo_msgs(plan, dc.DC_X) if m["is_send"])
         sent_bytes = sent * xd["n"] * xd["c_pad"] * 2
         for label, flags in (("p2p", 0), ("nccl", dc.DC_HALO_NCCL)):
+            reps = 50
             with torch.cuda.stream(s):
                 for _ in range(5):
                     dc.dc_halo_exchange(plan, dc.DC_X, buf, flags, s)
                 torch.cuda.synchronize()
+                # the 50 exchanges replayed from one CUDA graph: device time,
+                # not the host's per-call launch cost
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=s):
+                    for _ in range(reps):
+                        dc.dc_halo_exchange(plan, dc.DC_X, buf, flags, s)
+                torch.cuda.synchronize()
+                dist.barrier()
+                g.replay()
+                torch.cuda.synchronize()
                 dist.barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(s)
-                reps = 50
-                for _ in range(reps):
-                    dc.dc_halo_exchange(plan, dc.DC_X, buf, flags, s)
+                g.replay()
                 e1.record(s)
                 torch.cuda.synchronize()
+                del g
             t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             b = torch.tensor([float(sent_bytes)], dtype=torch.float64, device="cuda")
