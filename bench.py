@@ -336,7 +336,12 @@ def main():
     ap.add_argument("--cost-table-in", default=os.path.join(ROOT, "profiles", "cost_table_b200.csv"),
                     help="measured local conv costs for the performance model ('' = roofline estimate)")
     ap.add_argument("--cost-table", default=None, help="write the per-op timings as a cost table CSV")
+    ap.add_argument("--watchdog", type=float, default=1500.0,
+                    help="seconds after which a run that has not finished prints every thread's stack and exits")
     args = ap.parse_args()
+    import faulthandler
+    if args.watchdog > 0:
+        faulthandler.dump_traceback_later(args.watchdog, exit=True)
     layers = WORKLOADS[args.workload]
     NET = args.workload in NET_WORKLOADS
     if args.impl == "reference":
@@ -797,7 +802,6 @@ def main():
                         f.write(f"{op},{xd['n']},{C},{xd['h']},{xd['w']},{F},{K},{S},{P},{tt / 1e3}\n")
     # teardown watchdog: a teardown stuck for 120 s prints every thread's stack
     # to stderr and exits (the result line is already out)
-    import faulthandler
     faulthandler.dump_traceback_later(120, exit=True)
     # graphs hold NCCL persistent resources: release every reference to them
     # (the per-op list included) before the communicator

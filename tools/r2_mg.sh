@@ -1,18 +1,25 @@
-# multi-GPU round-2 measurement on P GPUs (P = number visible): new multi-GPU
-# tests, C5 sweep + E7, redistribution / channel-parallel microbenchmarks, bench
+# multi-GPU round-2 measurement on P GPUs (P = number visible): bench, halo /
+# redistribution / channel-parallel microbenchmarks, new multi-GPU tests,
+# C5 sweep + E7, ResNet-50 sample vs hybrid, network-level strategy
 P=$(nvidia-smi -L | wc -l)
 export NCCL_DEBUG=WARN
 python -m paper_1903_06681_b200.build > /dev/null
-timeout 1200 python -m pytest tests/test_cfpar.py tests/test_redist.py tests/test_multigpu.py -m gpu -x -q > gpurun_out/mg${P}_newtests.log 2>&1; echo "tests rc=$?"; tail -3 gpurun_out/mg${P}_newtests.log
-timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29530 tools/halo_bench.py > gpurun_out/halo_bench_${P}gpu.jsonl 2> gpurun_out/halo_bench_${P}gpu.err; echo "halo rc=$?"; cat gpurun_out/halo_bench_${P}gpu.jsonl
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29531 tools/redist_bench.py --out gpurun_out/redist_bench_${P}gpu.jsonl > gpurun_out/redist_bench_${P}gpu.log 2>&1; echo "redist rc=$?"; cat gpurun_out/redist_bench_${P}gpu.jsonl
-timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29532 bench.py --gpus $P --steps 10 --warmup 5 > gpurun_out/mg${P}_bench.json 2> gpurun_out/mg${P}_bench.err; echo "bench rc=$?"; tail -c 400 gpurun_out/mg${P}_bench.json
-timeout 1800 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29533 tools/c5_sweep.py --out gpurun_out/c5_e7_${P}gpu.jsonl > gpurun_out/c5_${P}gpu.log 2>&1; echo "c5 rc=$?"; tail -25 gpurun_out/c5_${P}gpu.log
-# ResNet-50 conv stack (configs[1]/[2], C2): sample vs hybrid grids
-for dec in "$P,1,1" "$((P/2)),2,1"; do
-  timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29534 bench.py --gpus $P --workload resnet50_n64 --decomp $dec --steps 10 --warmup 5 > gpurun_out/mg${P}_resnet_${dec//,/_}.json 2> gpurun_out/mg${P}_resnet_${dec//,/_}.err; echo "resnet $dec rc=$?"; python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'])" gpurun_out/mg${P}_resnet_${dec//,/_}.json
-done
-# network level (E7): the model's strategy (per-layer grids + shuffles) and its pure-spatial restriction
+run() {  # name, timeout, command...
+  local n=$1 t=$2; shift 2
+  timeout -k 20 $t "$@" > gpurun_out/mg${P}_$n.out 2> gpurun_out/mg${P}_$n.err; echo "$n rc=$?"
+}
+TR="python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1"
+run bench 420 $TR --master-port 29532 bench.py --gpus $P --steps 10 --warmup 5 --watchdog 300
+tail -c 300 gpurun_out/mg${P}_bench.out; grep -A12 "Thread 0x\|most recent call first" gpurun_out/mg${P}_bench.err | head -40
+run halo 300 $TR --master-port 29530 tools/halo_bench.py; cat gpurun_out/mg${P}_halo.out
+run redist 600 $TR --master-port 29531 tools/redist_bench.py; cat gpurun_out/mg${P}_redist.out
+run tests 1500 python -m pytest tests/test_cfpar.py tests/test_redist.py tests/test_multigpu.py -m gpu -x -q --durations=15; tail -25 gpurun_out/mg${P}_tests.out
 for dec in strategy spatial; do
-  timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node $P --master-addr 127.0.0.1 --master-port 29535 bench.py --gpus $P --workload mesh2k_n8_net --decomp $dec --steps 10 --warmup 5 > gpurun_out/mg${P}_net_${dec}.json 2> gpurun_out/mg${P}_net_${dec}.err; echo "net $dec rc=$?"; python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'],d['config'].get('strategy',{}).get('model_step_ms'))" gpurun_out/mg${P}_net_${dec}.json
+  run net_$dec 420 $TR --master-port 29535 bench.py --gpus $P --workload mesh2k_n8_net --decomp $dec --steps 10 --warmup 5 --watchdog 300
+  python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'],d['config'].get('strategy',{}).get('model_step_ms'))" gpurun_out/mg${P}_net_$dec.out
 done
+for dec in "$P,1,1" "$((P/2)),2,1"; do
+  run resnet_${dec//,/_} 420 $TR --master-port 29534 bench.py --gpus $P --workload resnet50_n64 --decomp $dec --steps 10 --warmup 5 --watchdog 300
+  python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'])" gpurun_out/mg${P}_resnet_${dec//,/_}.out
+done
+run c5 1800 $TR --master-port 29533 tools/c5_sweep.py --out gpurun_out/c5_e7_${P}gpu.jsonl; tail -25 gpurun_out/mg${P}_c5.out
