@@ -215,18 +215,23 @@ def test_full_size_sampled_parity(dc, layer):
         cs = sorted(set(int(c) for c in np.linspace(0, C - 1, nc).round()))
         fs = sorted(set(int(f) for f in np.linspace(0, F - 1, nf).round()))
         gen_dev = dict(dtype=torch.float64, device="cuda")
-        xcs = {c: datagen.gen_block_nhwc_torch((N, C, H, W), datagen.SEED, datagen.TID_X, c=(c, c + 1), **gen_dev)
-               .permute(0, 3, 1, 2).cpu().numpy() for c in cs}
+        # the selected channels of x and dy, stacked: ONE oracle call computes
+        # every (f, c) pair (Eq. 2 is independent per pair; its OpenMP loop
+        # runs over the pairs)
+        xs = np.concatenate([datagen.gen_block_nhwc_torch((N, C, H, W), datagen.SEED, datagen.TID_X, c=(c, c + 1),
+                                                          **gen_dev).permute(0, 3, 1, 2).cpu().numpy() for c in cs], 1)
+        dys = np.concatenate([datagen.gen_block_nhwc_torch((N, F, Ho, Wo), datagen.SEED, datagen.TID_DY,
+                                                           c=(f, f + 1), **gen_dev).permute(0, 3, 1, 2).cpu().numpy()
+                              for f in fs], 1)
+        ref = oracle.conv_bwd_filter(xs, dys, K, S, P)                     # nf x nc x K x K
+        Sb = oracle.conv_bwd_filter(np.abs(xs), np.abs(dys), K, S, P)
+        del xs, dys
         nent = 0
-        for f in fs:
-            dyf = datagen.gen_block_nhwc_torch((N, F, Ho, Wo), datagen.SEED, datagen.TID_DY, c=(f, f + 1),
-                                               **gen_dev).permute(0, 3, 1, 2).cpu().numpy()
-            for c in cs:
-                ref = oracle.conv_bwd_filter(xcs[c], dyf, K, S, P)[0, 0]                 # K x K
-                Sb = oracle.conv_bwd_filter(np.abs(xcs[c]), np.abs(dyf), K, S, P)[0, 0]
+        for a_, f in enumerate(fs):
+            for b_, c in enumerate(cs):
                 got = dwh[f, :, :, c]
-                assert_elementwise(f"{name}: dW[{f}, {c}]", got, ref,
-                                   elementwise_bound(ref, Sb, N * Ho * Wo, 16, False, extra_adds=300))
+                assert_elementwise(f"{name}: dW[{f}, {c}]", got, ref[a_, b_],
+                                   elementwise_bound(ref[a_, b_], Sb[a_, b_], N * Ho * Wo, 16, False, extra_adds=300))
                 nent += K * K
         assert nent >= min(1024, F * C * K * K)
     finally:

@@ -3,7 +3,7 @@
 # the review, the cost-table refit (warm-ups + mean of 10)
 export CUDA_VISIBLE_DEVICES=0
 python -m paper_1903_06681_b200.build > /dev/null
-timeout 900 python -m pytest tests/test_cfpar.py tests/test_redist.py tests/test_gpu_conv.py -m gpu -x -q > gpurun_out/p_newtests.log 2>&1; echo "newtests $?"; tail -3 gpurun_out/p_newtests.log
+timeout 1800 python -m pytest tests -m gpu -q --durations=40 > gpurun_out/p_gputests.log 2>&1; echo "gputests $?"; tail -45 gpurun_out/p_gputests.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/p_smoke.log 2>&1; echo "smoke $?"; tail -2 gpurun_out/p_smoke.log
 timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/p_bench_bf16.json 2> gpurun_out/p_bench_bf16.err; echo "bf16 $?"
 timeout 900 python bench.py --dtype fp32 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/p_bench_fp32.json 2> gpurun_out/p_bench_fp32.err; echo "fp32 $?"
