@@ -396,6 +396,34 @@ dc_status_t dc_cconv_bwd_filter(dc_cplan_t plan, const void *x, const void *dy, 
                                 void *stream);
 dc_status_t dc_cplan_destroy(dc_cplan_t plan);
 
+/* ---- max pooling on the decomposition ----
+ * "Pooling layers are parallelized similarly" to convolution,
+ * with "halo exchanges before ... pooling": window K, stride,
+ * pad (out-of-range positions are not part of a window), the same blocked
+ * sample x spatial grid as a convolution. The gradient of a window goes to
+ * its FIRST maximum in (a, b) order. bf16 plans.
+ * The pooling owns two plans of its grid: `in_plan` holds the input x as a
+ * margined DC_X buffer with a halo of K - 1 on every side (allocate it with
+ * dc_buffer_alloc(in_plan, DC_X); dc_bn_apply may write into it with
+ * dst_plan = in_plan), and `out_plan` describes y (DC_Y, dense), dy (DC_DY,
+ * margined: dc_buffer_alloc(out_plan, DC_DY)) and dx (DC_DX, dense). The
+ * backward recomputes each window's first maximum from the wide x, so no
+ * argmax tensor is stored or exchanged. */
+typedef struct dc_pool_s *dc_pool_t;
+/* COLLECTIVE. decomp entries must all be > 0. Errors: DC_ERR_ARG,
+ * DC_ERR_SHAPE, DC_ERR_PARTITION (a window of an owned output reaches past
+ * the neighbouring input blocks), DC_ERR_UNSUPPORTED (fp32, 2K - 1 > 15). */
+dc_status_t dc_pool_create(int64_t N, int64_t C, int64_t H, int64_t W, int K, int stride, int pad, dc_decomp_t decomp,
+                           dc_dtype_t dtype, dc_comm_t comm, dc_pool_t *out);
+dc_status_t dc_pool_plans(dc_pool_t pool, dc_plan_t *in_plan, dc_plan_t *out_plan);
+/* y = maxpool(x) on the owned outputs; flags DC_EXCHANGE: exchange x's halo
+ * first (x must then be in_plan's dc_buffer_alloc buffer; | DC_HALO_NCCL). */
+dc_status_t dc_pool_fwd(dc_pool_t pool, void *x, void *y, unsigned flags, void *stream);
+/* dx on the owned inputs from dy (out_plan's margined dy; DC_EXCHANGE
+ * exchanges its halo first) and x (with its halo, as the forward left it). */
+dc_status_t dc_pool_bwd(dc_pool_t pool, const void *x, void *dy, void *dx, unsigned flags, void *stream);
+dc_status_t dc_pool_destroy(dc_pool_t pool);
+
 /* Number of kernels this library launched on this thread so far (for the
  * bench's gpu_launches claim). */
 uint64_t dc_kernel_launches(void);

@@ -41,6 +41,7 @@ EXPORTS = [
     "dc_redist_create", "dc_redist_bytes", "dc_redistribute", "dc_redist_destroy",
     "dc_cplan_create", "dc_cplan_create_virtual", "dc_cplan_query", "dc_cconv_fwd", "dc_cconv_bwd_data",
     "dc_cconv_bwd_filter", "dc_cplan_destroy",
+    "dc_pool_create", "dc_pool_plans", "dc_pool_fwd", "dc_pool_bwd", "dc_pool_destroy",
 ]
 
 
@@ -137,6 +138,11 @@ def lib() -> ctypes.CDLL:
         "dc_cconv_bwd_data": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_cconv_bwd_filter": [vp, vp, vp, vp, ctypes.c_uint, vp],
         "dc_cplan_destroy": [vp],
+        "dc_pool_create": [i64] * 4 + [i32, i32, i32, dc_decomp_t, i32, vp, P(vp)],
+        "dc_pool_plans": [vp, P(vp), P(vp)],
+        "dc_pool_fwd": [vp, vp, vp, ctypes.c_uint, vp],
+        "dc_pool_bwd": [vp, vp, vp, vp, ctypes.c_uint, vp],
+        "dc_pool_destroy": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -449,3 +455,29 @@ def dc_cconv_bwd_filter(plan: int, x, dy, dw, flags: int = 0, stream=None):
 
 def dc_cplan_destroy(plan: int):
     _check(lib().dc_cplan_destroy(plan))
+
+
+def dc_pool_create(N, C, H, W, K, stride, pad, decomp, dtype=DC_BF16, comm=None) -> int:
+    """Max pooling on a sample x spatial grid."""
+    out = ctypes.c_void_p()
+    _check(lib().dc_pool_create(N, C, H, W, K, stride, pad, dc_decomp_t(*decomp), dtype, comm, ctypes.byref(out)))
+    return out.value
+
+
+def dc_pool_plans(pool: int):
+    """(in_plan, out_plan): x's wide-halo plan, the y / dy / dx plan."""
+    a, b = ctypes.c_void_p(), ctypes.c_void_p()
+    _check(lib().dc_pool_plans(pool, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def dc_pool_fwd(pool: int, x, y, flags: int = DC_EXCHANGE, stream=None):
+    _check(lib().dc_pool_fwd(pool, _ptr(x), _ptr(y), flags, _stream(stream)))
+
+
+def dc_pool_bwd(pool: int, x, dy, dx, flags: int = DC_EXCHANGE, stream=None):
+    _check(lib().dc_pool_bwd(pool, _ptr(x), _ptr(dy), _ptr(dx), flags, _stream(stream)))
+
+
+def dc_pool_destroy(pool: int):
+    _check(lib().dc_pool_destroy(pool))

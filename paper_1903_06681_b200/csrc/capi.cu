@@ -34,6 +34,7 @@
 #include "bn.cuh"
 #include "redist.cuh"
 #include "cfpar.cuh"
+#include "pool.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -52,6 +53,7 @@ void preload_wgrad_v2();
 void preload_bn();
 void preload_redist();
 void preload_cfpar();
+void preload_pool();
 // Every kernel of the library loaded into this context (see preload_*):
 // once, at communicator creation.
 void preload_kernels() {
@@ -65,6 +67,7 @@ void preload_kernels() {
         preload_bn();
         preload_redist();
         preload_cfpar();
+        preload_pool();
     });
 }
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
@@ -86,6 +89,7 @@ using namespace dc;
 struct dc_plan_s;
 struct dc_redist_s;
 struct dc_cplan_s;
+struct dc_pool_s;
 
 namespace dc {
 // Loopback group: `world` virtual ranks of one process on ONE device
@@ -2828,3 +2832,110 @@ dc_status_t dc_cplan_destroy(dc_cplan_t c) {
 }
 
 }  // extern "C"
+
+// ===========================================================================
+// Max pooling on the decomposition ("Pooling layers are
+// parallelized similarly"; "halo exchanges before ... pooling")
+// ===========================================================================
+// Two plans of one grid: the OUTPUT plan has the pooling window's geometry
+// (K, S, P: y / dy ownership, the dy halo of the backward); the INPUT plan's
+// x buffer carries a halo of K - 1 on every side (a K' = 2K - 1, S' = 1,
+// P' = K - 1 geometry), wide enough that the backward can recompute the first
+// maximum of every window that touches an owned input -- including windows
+// of outputs owned by a neighbour -- from x (no argmax tensor to store or
+// exchange).
+struct dc_pool_s {
+    dc_plan_s *in = nullptr, *out = nullptr;
+    PoolGeom pg{};
+    ~dc_pool_s() {
+        delete out;
+        delete in;
+    }
+};
+
+extern "C" {
+
+dc_status_t dc_pool_create(int64_t N, int64_t C, int64_t H, int64_t W, int K, int stride, int pad, dc_decomp_t decomp,
+                           dc_dtype_t dtype, dc_comm_t comm, dc_pool_t *out) {
+    DC_API_BEGIN
+    DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
+    DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "pooling: bf16 plans only");
+    DC_REQUIRE(decomp.pn > 0 && decomp.ph > 0 && decomp.pw > 0, DC_ERR_ARG, "pooling needs an explicit grid");
+    DC_REQUIRE(K >= 1 && 2 * K - 1 <= 15 && pad < K, DC_ERR_UNSUPPORTED, "pooling window K=%d pad=%d", K, pad);
+    const Grid grid{decomp.pn, decomp.ph, decomp.pw};
+    const int rank = comm ? comm->rank : 0;
+    DC_REQUIRE(grid.size() == 1 || (comm && comm->world == grid.size()), DC_ERR_ARG,
+               "grid of %d ranks needs a communicator of that size", grid.size());
+    if (comm) CK(cudaSetDevice(comm->device));
+    std::unique_ptr<dc_pool_s> p(new dc_pool_s());
+    p->in = create_plan(make_geom(N, C, H, W, C, 2 * K - 1, 1, K - 1, 0), grid, rank, comm, false);
+    p->out = create_plan(make_geom(N, C, H, W, C, K, stride, pad, 0), grid, rank, comm, false);
+    const RankPlan &ri = p->in->rp, &ro = p->out->rp;
+    const ConvGeom &g = ro.g;
+    // every window the forward (owned outputs) and the backward (outputs in
+    // the dy buffer) evaluate lies inside the wide x buffer
+    auto covered = [&](const DimSplit &o, const DimSplit &x, int64_t X) {
+        for (const Range &r : {o.out, o.dbuf}) {
+            if (r.empty()) continue;
+            const int64_t lo = std::max<int64_t>(0, stride * r.lo - pad);
+            const int64_t hi = std::min<int64_t>(X, stride * (r.hi - 1) - pad + K);
+            if (lo < x.xbuf.lo || hi > x.xbuf.hi) return false;
+        }
+        return x.in.lo == o.in.lo && x.in.hi == o.in.hi;
+    };
+    DC_REQUIRE(covered(ro.h, ri.h, H) && covered(ro.w, ri.w, W), DC_ERR_PARTITION,
+               "pooling: the windows of this rank's outputs reach past the neighbouring input blocks");
+    PoolGeom &q = p->pg;
+    q.K = K, q.S = stride, q.P = pad, q.H = (int)H, q.W = (int)W;
+    q.n = (int)ro.nrange.size(), q.cpad = (int)g.Cp;
+    q.xr0 = (int)ri.h.xbuf.lo, q.xc0 = (int)ri.w.xbuf.lo;
+    q.xhb = (int)ri.h.xbuf.size(), q.xwb = (int)ri.w.xbuf.size();
+    q.oh0 = (int)ro.h.out.lo, q.ow0 = (int)ro.w.out.lo, q.oh = (int)ro.h.out.size(), q.ow = (int)ro.w.out.size();
+    q.gi0 = (int)ro.h.in.lo, q.gj0 = (int)ro.w.in.lo, q.ih = (int)ro.h.in.size(), q.iw = (int)ro.w.in.size();
+    q.dr0 = (int)ro.h.dbuf.lo, q.dc0 = (int)ro.w.dbuf.lo;
+    q.dhb = (int)ro.h.dbuf.size(), q.dwb = (int)ro.w.dbuf.size();
+    q.Ho = (int)g.Ho, q.Wo = (int)g.Wo;
+    *out = p.release();
+    DC_API_END
+}
+
+dc_status_t dc_pool_plans(dc_pool_t p, dc_plan_t *in_plan, dc_plan_t *out_plan) {
+    DC_API_BEGIN
+    DC_REQUIRE(p, DC_ERR_ARG, "null pool");
+    if (in_plan) *in_plan = p->in;
+    if (out_plan) *out_plan = p->out;
+    DC_API_END
+}
+
+dc_status_t dc_pool_fwd(dc_pool_t p, void *x, void *y, unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(p && x && y, DC_ERR_ARG, "null argument");
+    DC_REQUIRE((flags & ~(DC_EXCHANGE | DC_HALO_NCCL)) == 0, DC_ERR_ARG, "unknown pooling flags 0x%x", flags);
+    NoPdlScope no_pdl(is_local(p->in));
+    cudaStream_t st = (cudaStream_t)stream;
+    join_import(p->in, 0, st);
+    if (flags & DC_EXCHANGE) exchange(p->in, 0, x, flags & DC_HALO_NCCL, st);
+    launch_maxpool_fwd(p->pg, x, y, st);
+    DC_API_END
+}
+
+dc_status_t dc_pool_bwd(dc_pool_t p, const void *x, void *dy, void *dx, unsigned flags, void *stream) {
+    DC_API_BEGIN
+    DC_REQUIRE(p && x && dy && dx, DC_ERR_ARG, "null argument");
+    DC_REQUIRE((flags & ~(DC_EXCHANGE | DC_HALO_NCCL)) == 0, DC_ERR_ARG, "unknown pooling flags 0x%x", flags);
+    NoPdlScope no_pdl(is_local(p->out));
+    cudaStream_t st = (cudaStream_t)stream;
+    join_import(p->out, 1, st);
+    if (flags & DC_EXCHANGE) exchange(p->out, 1, dy, flags & DC_HALO_NCCL, st);
+    launch_maxpool_bwd(p->pg, x, dy, dx, st);
+    DC_API_END
+}
+
+dc_status_t dc_pool_destroy(dc_pool_t p) {
+    DC_API_BEGIN
+    delete p;
+    DC_API_END
+}
+
+}  // extern "C"
+
