@@ -2677,7 +2677,7 @@ void cf_reduce_scatter(dc_cplan_s *c, dc_plan_s *sub, int64_t seg, int64_t npix,
     const CfFlags d = cf_flags(c, 1);
     launch_signal(const_cast<uint32_t *const *>(d.out), d.n, 0, c->epochs, st);
     launch_cf_wait(d, st);
-    launch_cf_reduce(c->slots, c->pc, npix, (int)seg, out, (int)seg, c->epochs, st);
+    launch_cf_reduce(c->slots, c->pc, c->slot_elems, npix, (int)seg, out, (int)seg, c->epochs, st);
 }
 
 }  // namespace

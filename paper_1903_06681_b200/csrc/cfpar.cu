@@ -35,12 +35,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<const uint32_t *>(&v);
 }
 
-__global__ void __launch_bounds__(256) cf_reduce_kernel(const float *__restrict__ slots, int n, long long npix,
-                                                        int seg, __nv_bfloat16 *__restrict__ out, int out_pitch,
-                                                        uint32_t *epoch) {
+__global__ void __launch_bounds__(256) cf_reduce_kernel(const float *__restrict__ slots, int n, long long slot,
+                                                        long long npix, int seg, __nv_bfloat16 *__restrict__ out,
+                                                        int out_pitch, uint32_t *epoch) {
     pdl_wait();  // (launch.cuh: PDL)
     const int vecs = seg / 8;
-    const long long total = npix * vecs, slot = npix * seg;
+    const long long total = npix * vecs;
     for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         const long long pix = idx / vecs;
@@ -82,12 +82,12 @@ void launch_cf_wait(const CfFlags &f, cudaStream_t st) {
     launch_k(cf_wait_kernel, dim3(1), dim3(32), 0, st, 1, "cf wait", f);
 }
 
-void launch_cf_reduce(const float *slots, int n, long long npix, int seg, void *out, int out_pitch,
-                      uint32_t *epoch, cudaStream_t st) {
+void launch_cf_reduce(const float *slots, int n, long long slot_stride, long long npix, int seg, void *out,
+                      int out_pitch, uint32_t *epoch, cudaStream_t st) {
     DC_REQUIRE(seg % 8 == 0 && out_pitch % 8 == 0, DC_ERR_ARG, "cf reduce: channel blocks of 8");
     const long long work = npix * (seg / 8);
     const int blocks = (int)std::max<long long>(1, std::min<long long>((work + 255) / 256, 148 * 8));
-    launch_k(cf_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "cf reduce", slots, n, npix, seg,
+    launch_k(cf_reduce_kernel, dim3(blocks), dim3(256), 0, st, 1, "cf reduce", slots, n, slot_stride, npix, seg,
              reinterpret_cast<__nv_bfloat16 *>(out), out_pitch, epoch);
 }
 

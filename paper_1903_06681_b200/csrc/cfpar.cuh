@@ -29,9 +29,10 @@ void launch_cf_handshake(const CfFlags &f, cudaStream_t st);
 void launch_cf_wait(const CfFlags &f, cudaStream_t st);
 
 // out[pix][c] = bf16( sum_{s = 0..n-1} slots[s][pix][c] ) for c < seg (fixed
-// rank order); slots: n x npix x seg fp32, out channel pitch out_pitch.
+// rank order); slot s starts slot_stride floats after slot s - 1 and holds
+// npix x seg fp32; out channel pitch out_pitch.
 // The last block publishes the epoch (epoch[0] = epoch[0] + 1).
-void launch_cf_reduce(const float *slots, int n, long long npix, int seg, void *out, int out_pitch,
-                      uint32_t *epoch, cudaStream_t st);
+void launch_cf_reduce(const float *slots, int n, long long slot_stride, long long npix, int seg, void *out,
+                      int out_pitch, uint32_t *epoch, cudaStream_t st);
 
 }  // namespace dc
