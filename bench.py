@@ -28,6 +28,10 @@ import sys
 import threading
 import time
 
+# the library's side streams (dconv.h: dc_comm_create) on distinct hardware
+# queues: set before CUDA initialises (the runtime's default is 8)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -115,6 +115,10 @@ typedef struct dc_plan_s *dc_plan_t;
  * the 128-byte ncclUniqueId produced by dc_comm_unique_id on rank 0 and
  * broadcast by the caller (e.g. through torch.distributed). world == 1
  * needs no id (may be NULL). cuda_device is this rank's device ordinal.
+ * Every plan of the communicator shares its few side streams (exchanges,
+ * stride phases, imports, the dW allreduces); run the process with
+ * CUDA_DEVICE_MAX_CONNECTIONS >= 16 so that they do not alias onto one
+ * hardware queue with the caller's streams (bench.py sets 32).
  * Errors: DC_ERR_ARG (rank/world), DC_ERR_COMM (NCCL). */
 dc_status_t dc_comm_create(int rank, int world, const void *nccl_uid128, int cuda_device,
                            dc_comm_t *out);

@@ -130,6 +130,14 @@ struct dc_comm_s {
     // uses for exchanges / boundary tiles), created back to back for all ranks
     // so that no two of them share a hardware queue (see dc_comm_create_local)
     cudaStream_t s_main = nullptr, s_side = nullptr;
+    // real ranks: the side-stream set every plan of this communicator shares
+    // (exchanges / boundary tiles on s_side, backward-data stride phases on
+    // s_ph, host imports on s_copy) -- a handful of streams per process
+    // however many layers, so that streams never alias onto one hardware
+    // queue (a spinning protocol kernel ahead of unrelated work in an aliased
+    // queue would stall that work; peers waiting for it would never finish)
+    cudaStream_t s_ph[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaStream_t s_copy = nullptr;
 };
 
 namespace {
@@ -167,7 +175,7 @@ struct dc_plan_s {
     bool bn_comm_owned = false;
     int bn_group = 1;
     cudaStream_t s_comm = nullptr;
-    bool s_comm_shared = false;  // (loopback: the virtual rank's side stream)
+    bool s_comm_shared = false;  // s_comm, s_ph, s_copy are the communicator's (not destroyed here)
     cudaStream_t s_ph[4] = {nullptr, nullptr, nullptr, nullptr};  // stride-phase streams (bwd-data)
     cudaEvent_t ev_ph[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -250,7 +258,7 @@ struct dc_plan_s {
             if (ev_copy_in[i]) cudaEventDestroy(ev_copy_in[i]);
             if (ev_copy_out[i]) cudaEventDestroy(ev_copy_out[i]);
         }
-        if (s_copy) cudaStreamDestroy(s_copy);
+        if (s_copy && !s_comm_shared) cudaStreamDestroy(s_copy);
         if (flags) cudaFree(flags);
         if (dev_epochs) cudaFree(dev_epochs);
         if (wt) cudaFree(wt);
@@ -267,7 +275,7 @@ struct dc_plan_s {
             if (e) cudaEventDestroy(e);
         if (s_comm && !s_comm_shared) cudaStreamDestroy(s_comm);
         for (auto sp : s_ph)
-            if (sp) cudaStreamDestroy(sp);
+            if (sp && !s_comm_shared) cudaStreamDestroy(sp);
         for (auto e : ev_ph)
             if (e) cudaEventDestroy(e);
         if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
@@ -1438,6 +1446,11 @@ void ensure_local_resources(dc_plan_s *pl) {
         // after another): no extra hardware queues shared between ranks
         pl->s_comm = pl->comm->s_side;
         pl->s_comm_shared = true;
+    } else if (pl->comm && pl->comm->s_side) {  // the communicator's shared set
+        pl->s_comm = pl->comm->s_side;
+        for (int k = 0; k < 4; ++k) pl->s_ph[k] = pl->comm->s_ph[k];
+        pl->s_copy = pl->comm->s_copy;
+        pl->s_comm_shared = true;
     } else {
         CK(cudaStreamCreateWithFlags(&pl->s_comm, cudaStreamNonBlocking));
         for (auto &sp : pl->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
@@ -1609,6 +1622,9 @@ dc_status_t dc_comm_create(int rank, int world, const void *uid128, int device, 
         CK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming));
     }
+    CK(cudaStreamCreateWithFlags(&c->s_side, cudaStreamNonBlocking));
+    for (auto &sp : c->s_ph) CK(cudaStreamCreateWithFlags(&sp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_copy, cudaStreamNonBlocking));
     *out = c;
     DC_API_END
 }
@@ -1660,6 +1676,9 @@ dc_status_t dc_comm_destroy(dc_comm_t c) {
         if (c->s_grad) cudaStreamDestroy(c->s_grad);
         if (c->s_main) cudaStreamDestroy(c->s_main);
         if (c->s_side) cudaStreamDestroy(c->s_side);
+        for (auto sp : c->s_ph)
+            if (sp) cudaStreamDestroy(sp);
+        if (c->s_copy) cudaStreamDestroy(c->s_copy);
         if (c->ev_in) cudaEventDestroy(c->ev_in);
         if (c->ev_out) cudaEventDestroy(c->ev_out);
         delete c;
@@ -1852,8 +1871,9 @@ dc_status_t dc_tensor_import(dc_plan_t pl, dc_tensor_t t, const void *src, void 
     cudaStream_t st = (cudaStream_t)stream, cs = st;
     if (is_local(pl)) flags &= ~DC_IMPORT_ASYNC;  // (loopback: no extra streams)
     if (flags & DC_IMPORT_ASYNC) {  // on the copy stream, after the caller's work so far
-        if (!pl->s_copy) {
-            CK(cudaStreamCreateWithFlags(&pl->s_copy, cudaStreamNonBlocking));
+        ensure_local_resources(pl);
+        if (!pl->ev_copy_in[0]) {
+            if (!pl->s_copy) CK(cudaStreamCreateWithFlags(&pl->s_copy, cudaStreamNonBlocking));
             for (int i = 0; i < 2; ++i) {
                 CK(cudaEventCreateWithFlags(&pl->ev_copy_in[i], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&pl->ev_copy_out[i], cudaEventDisableTiming));
