@@ -2306,6 +2306,29 @@ void resolve_redist_peers(dc_redist_s *r) {
         }
 }
 
+// One P2P all-to-all (redist.cuh). Real ranks: the one-kernel protocol.
+// Loopback group: the same flags in four launches -- a one-block ready
+// handshake, the piece copies, the data flags, a one-block wait -- because the
+// virtual ranks share the SMs: many spinning blocks of one rank could leave
+// no room for the GEMM another rank must finish before it joins.
+void run_redist_p2p(const RedistP2P &x, bool local, cudaStream_t st) {
+    if (!local) {
+        launch_redist_p2p(x, st);
+        return;
+    }
+    CfFlags rdy{};
+    for (int k = 0; k < x.n_ready_out; ++k) rdy.out[k] = x.ready_out[k];
+    for (int k = 0; k < x.n_ready_in; ++k) rdy.in[k] = x.ready_in[k];
+    rdy.n = x.n_ready_out, rdy.n_in = x.n_ready_in, rdy.epoch = x.epoch_ctr;
+    launch_cf_handshake(rdy, st);
+    launch_redist_copy(x.piece, x.npiece, st);
+    launch_signal(const_cast<uint32_t *const *>(x.data_out), x.n_data_out, 0, x.epoch_ctr, st);
+    CfFlags dat{};
+    for (int k = 0; k < x.n_data_in; ++k) dat.in[k] = x.data_in[k];
+    dat.n = 0, dat.n_in = x.n_data_in, dat.epoch = x.epoch_ctr, dat.publish = 1;
+    launch_cf_wait(dat, st);
+}
+
 void redist_p2p(dc_redist_s *r, const void *src, cudaStream_t st) {
     resolve_redist_peers(r);
     DC_REQUIRE((int)r->sends.size() <= kRedistMaxPeers && (int)r->recvs.size() <= kRedistMaxPeers,
@@ -2327,7 +2350,7 @@ void redist_p2p(dc_redist_s *r, const void *src, cudaStream_t st) {
         x.ready_out[x.n_ready_out++] = r->peer_flags.at(p.peer) + r->rank;
         x.data_in[x.n_data_in++] = r->flags + W + p.peer;
     }
-    launch_redist_p2p(x, st);
+    run_redist_p2p(x, r->comm->group != nullptr, st);
 }
 
 void redist_nccl(dc_redist_s *r, const void *src, void *dst, cudaStream_t st) {
@@ -2834,7 +2857,7 @@ dc_status_t dc_cconv_bwd_filter(dc_cplan_t c, const void *x, const void *dy, flo
         x2.data_out[x2.n_data_out++] = c->peer_flags[k] + 3 * c->pc + c->ic;
         x2.data_in[x2.n_data_in++] = c->flags + 3 * c->pc + k;
     }
-    launch_redist_p2p(x2, st);
+    run_redist_p2p(x2, local, st);
     dc_plan_s *sub = c->fwd;
     ensure_local_resources(sub);
     run_bwd_filter(sub, x, c->dyfull, dw, st, false);

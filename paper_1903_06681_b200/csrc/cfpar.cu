@@ -13,11 +13,12 @@ namespace {
 __global__ void __launch_bounds__(32) cf_handshake_kernel(const __grid_constant__ CfFlags f) {
     pdl_wait();  // (launch.cuh: PDL)
     const uint32_t e = *reinterpret_cast<const volatile uint32_t *>(f.epoch) + 1;
+    const int n_in = f.n_in > 0 ? f.n_in : f.n;
     if ((int)threadIdx.x < f.n) {
         __threadfence_system();
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.out[threadIdx.x]), "r"(e) : "memory");
-        spin_until_geq(f.in[threadIdx.x], e);
     }
+    if ((int)threadIdx.x < n_in) spin_until_geq(f.in[threadIdx.x], e);
     __syncwarp();
     __threadfence_system();
 }
@@ -25,9 +26,11 @@ __global__ void __launch_bounds__(32) cf_handshake_kernel(const __grid_constant_
 __global__ void __launch_bounds__(32) cf_wait_kernel(const __grid_constant__ CfFlags f) {
     pdl_wait();  // (launch.cuh: PDL)
     const uint32_t e = *reinterpret_cast<const volatile uint32_t *>(f.epoch) + 1;
-    if ((int)threadIdx.x < f.n) spin_until_geq(f.in[threadIdx.x], e);
+    const int n_in = f.n_in > 0 ? f.n_in : f.n;
+    if ((int)threadIdx.x < n_in) spin_until_geq(f.in[threadIdx.x], e);
     __syncwarp();
     __threadfence_system();
+    if (f.publish && threadIdx.x == 0) *reinterpret_cast<volatile uint32_t *>(f.epoch) = e;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -73,12 +76,14 @@ __global__ void __launch_bounds__(256) cf_reduce_kernel(const float *__restrict_
 }  // namespace
 
 void launch_cf_handshake(const CfFlags &f, cudaStream_t st) {
-    DC_REQUIRE(f.n >= 1 && f.n <= kCfMaxGroup, DC_ERR_ARG, "channel group of %d", f.n);
+    DC_REQUIRE(f.n >= 0 && f.n <= kCfMaxGroup && f.n_in >= 0 && f.n_in <= kCfMaxGroup, DC_ERR_ARG,
+               "flag group of %d / %d", f.n, f.n_in);
     launch_k(cf_handshake_kernel, dim3(1), dim3(32), 0, st, 1, "cf handshake", f);
 }
 
 void launch_cf_wait(const CfFlags &f, cudaStream_t st) {
-    DC_REQUIRE(f.n >= 1 && f.n <= kCfMaxGroup, DC_ERR_ARG, "channel group of %d", f.n);
+    DC_REQUIRE(f.n >= 0 && f.n <= kCfMaxGroup && f.n_in >= 0 && f.n_in <= kCfMaxGroup, DC_ERR_ARG,
+               "flag group of %d / %d", f.n, f.n_in);
     launch_k(cf_wait_kernel, dim3(1), dim3(32), 0, st, 1, "cf wait", f);
 }
 

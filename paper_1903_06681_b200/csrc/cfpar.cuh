@@ -13,10 +13,12 @@ constexpr int kCfMaxGroup = 8;
 
 // Flags of one exchange, epoch e = *epoch + 1 (device, graph-replayable).
 struct CfFlags {
-    uint32_t *out[kCfMaxGroup];  // my flag in each peer's array (peer k = group member k)
-    const uint32_t *in[kCfMaxGroup];  // each peer's flag in my array
-    int n;                       // group size (me included)
-    const uint32_t *epoch;       // {epoch, blocks done}
+    uint32_t *out[kCfMaxGroup];       // my flag in each peer's array
+    const uint32_t *in[kCfMaxGroup];  // peers' flags in my array
+    int n;                            // flags in `out` (and in `in`, unless n_in > 0)
+    int n_in;                         // flags in `in` when it differs from n (0: n)
+    uint32_t *epoch;                  // {epoch, blocks done}
+    int publish;                      // launch_cf_wait: publish epoch e when done
 };
 
 // One block: raise my flag (value e) in every peer's array, then wait until
@@ -25,7 +27,8 @@ struct CfFlags {
 // completed) and every owner's slots are free, so the GEMM may store.
 void launch_cf_handshake(const CfFlags &f, cudaStream_t st);
 // One block: wait until every peer's flag in my array reached e (the
-// senders' "data" flags, raised by launch_signal after their GEMMs).
+// senders' "data" flags, raised by launch_signal after their GEMMs); with
+// `publish`, then advance the epoch.
 void launch_cf_wait(const CfFlags &f, cudaStream_t st);
 
 // out[pix][c] = bf16( sum_{s = 0..n-1} slots[s][pix][c] ) for c < seg (fixed
