@@ -429,7 +429,7 @@ void launch_conv_gemm(const CUtensorMap &amap, const CUtensorMap &bmap, const Co
                       int nsamples, int nout_tiles, cudaStream_t st) {
     const int tiles = p.rect_start[p.nrect];
     if (tiles == 0 || nsamples == 0 || nout_tiles == 0) return;
-    const size_t smem = conv_gemm_smem_bytes(p.bkc, p.bn, p.stages);
+    const size_t smem = tmem_kernel_smem(conv_gemm_smem_bytes(p.bkc, p.bn, p.stages));
     static std::once_flag once;
     std::call_once(once, [] {
         cudaFuncSetAttribute(conv_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -443,7 +443,7 @@ void launch_conv_gemm(const CUtensorMap &amap, const CUtensorMap &bmap, const Co
 
 void launch_wgrad(const CUtensorMap &amap, const CUtensorMap &bmap, const WgradParams &p,
                   int m_tiles, int n_tiles, cudaStream_t st) {
-    const size_t smem = wgrad_smem_bytes(p.bkc, p.bf, p.bn, p.stages);
+    const size_t smem = tmem_kernel_smem(wgrad_smem_bytes(p.bkc, p.bf, p.bn, p.stages));
     static std::once_flag once;
     std::call_once(once, [] {
         cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(kV2Threads, 1)
             __syncwarp();
             ++acc_it;
         }
-    } else if (warp < 6 || p.epi2) {
+    } else if (warp < 6 || (p.epi2 && warp > 6)) {  // (warp 6 idles)
         // ========================= epilogue =========================
         const int eq = warp & 3;  // TMEM lane quarter this warp may access
         const int m = eq * 32 + lane;
@@ -884,7 +884,7 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     if (p.cluster > 1) {
         // persistent CTA pairs: as many as can be co-resident (GPCs need not hold
         // an even number of free SMs), a multiple of the split-K factor
-        const size_t smem = conv_v2_smem_bytes(p);
+        const size_t smem = tmem_kernel_smem(conv_v2_smem_bytes(p));
         DC_REQUIRE(p.kind == 0, DC_ERR_ARG, "conv_v2: tf32 runs without CTA pairs");
         auto kern = conv_v2_kernel<0>;
         const size_t key = smem;
@@ -914,7 +914,8 @@ int launch_conv_v2(const CUtensorMap &amap, const CUtensorMap &bmap, const ConvV
     const int grid = p.ksplit * std::max(1, std::min(p.total_tiles, sms / p.ksplit));
     if (g_dry_run) return grid;
     launch_k(p.kind == 1 ? conv_v2_kernel<1> : conv_v2_kernel<0>, dim3(grid), dim3(kV2Threads),
-             conv_v2_smem_bytes(p), st, 1, p.kind == 1 ? "conv_v2 (tf32)" : "conv_v2", amap, bmap, p);
+             tmem_kernel_smem(conv_v2_smem_bytes(p)), st, 1, p.kind == 1 ? "conv_v2 (tf32)" : "conv_v2", amap, bmap,
+             p);
     return grid;
 }
 

@@ -48,6 +48,17 @@ struct NoPdlScope {
     ~NoPdlScope() { g_no_pdl = prev; }
 };
 
+// Dynamic shared memory floor of every kernel that allocates tensor memory
+// (conv_v2, wgrad_v2, conv_gemm, wgrad): more than half of an SM's 228 KB, so
+// two such CTAs never share an SM. Their TMEM allocations could otherwise
+// exceed the SM's 512 columns; tcgen05.alloc then blocks until the other CTA
+// exits, and when both belong to CTA pairs (cluster launches) of two kernels
+// running side by side -- stride phases on their own streams, interior and
+// boundary tiles, virtual ranks of a loopback group -- each pair waits for its
+// partner, which waits for the other pair's TMEM: a deadlock.
+constexpr size_t kTmemExclusiveSmem = 116 * 1024;
+inline size_t tmem_kernel_smem(size_t need) { return need > kTmemExclusiveSmem ? need : kTmemExclusiveSmem; }
+
 // Set while a plan sizes its workspaces at creation (capi.cu presize): the
 // host-side configuration runs and allocates, no kernel is launched.
 extern thread_local bool g_dry_run;

@@ -405,7 +405,7 @@ void launch_wgrad_v2(const CUtensorMap &xmap, const CUtensorMap &dymap, const Wg
     });
     const int ntiles = (p.Fp + p.bn - 1) / p.bn;
     launch_k(p.kind == 1 ? wgrad_v2_kernel<1> : wgrad_v2_kernel<0>, dim3(wgrad_v2_mgroups(p), ntiles, p.splits),
-             dim3(192), wgrad_v2_smem_bytes(p), st, 1, p.kind == 1 ? "wgrad_v2 (tf32)" : "wgrad_v2", xmap, dymap, p);
+             dim3(192), tmem_kernel_smem(wgrad_v2_smem_bytes(p)), st, 1, p.kind == 1 ? "wgrad_v2 (tf32)" : "wgrad_v2", xmap, dymap, p);
 }
 
 

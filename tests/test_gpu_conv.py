@@ -86,6 +86,11 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     (1, 32, 21, 19, 128, 3, 1, 1),     # wgrad mode 1: 32-channel atoms stacked along th
     (2, 16, 13, 15, 64, 5, 1, 2),      # wgrad mode 1: 16-channel atoms, phantom taps
     (1, 256, 12, 14, 128, 3, 2, 1),    # wgrad mode 0, stride 2, four channel groups
+    # enough tiles that every persistent CTA reuses its TMEM accumulators,
+    # with the second epilogue warp group on (256-wide N tiles; the sub-pixel
+    # backward-data): the accumulator hand-off must count exactly its warps
+    (2, 64, 96, 128, 256, 3, 1, 1),
+    (2, 16, 192, 256, 64, 3, 2, 1),
 ]
 
 
