@@ -402,7 +402,8 @@ dc_status_t dc_cplan_destroy(dc_cplan_t plan);
 
 /* ---- max pooling on the decomposition ----
  * "Pooling layers are parallelized similarly" to convolution,
- * with "halo exchanges before ... pooling": window K, stride,
+ * with "halo exchanges before ... pooling": window K (odd, as
+ * for the convolutions), stride,
  * pad (out-of-range positions are not part of a window), the same blocked
  * sample x spatial grid as a convolution. The gradient of a window goes to
  * its FIRST maximum in (a, b) order. bf16 plans.

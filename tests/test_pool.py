@@ -31,7 +31,9 @@ def test_pool_errors(dc):
     with pytest.raises(dc.DCError):   # the model cannot pick a pooling grid
         dc.dc_pool_create(1, 16, 8, 8, 3, 2, 1, (0, 1, 1))
     with pytest.raises(dc.DCError):   # pad >= K
-        dc.dc_pool_create(1, 16, 8, 8, 2, 2, 2, (1, 1, 1))
+        dc.dc_pool_create(1, 16, 8, 8, 3, 2, 3, (1, 1, 1))
+    with pytest.raises(dc.DCError):   # even windows (the conv geometry's odd-K reading)
+        dc.dc_pool_create(1, 16, 8, 8, 2, 2, 0, (1, 1, 1))
 
 
 CASES = [  # (N, C, H, W, K, S, P), grid
@@ -40,7 +42,7 @@ CASES = [  # (N, C, H, W, K, S, P), grid
     ((2, 64, 24, 20, 3, 2, 1), (1, 1, 2)),
     ((2, 64, 24, 20, 3, 2, 1), (1, 2, 2)),    # 2D grid: corners
     ((2, 32, 25, 23, 3, 2, 1), (2, 2, 1)),    # ragged, hybrid sample x spatial
-    ((1, 16, 32, 16, 2, 2, 0), (1, 4, 1)),    # non-overlapping windows
+    ((1, 16, 32, 16, 3, 3, 0), (1, 4, 1)),    # non-overlapping windows (K = S)
     ((1, 16, 20, 18, 3, 1, 1), (1, 2, 1)),    # stride 1
 ]
 
