@@ -2904,7 +2904,8 @@ dc_status_t dc_pool_create(int64_t N, int64_t C, int64_t H, int64_t W, int K, in
     DC_REQUIRE(out != nullptr, DC_ERR_ARG, "null out");
     DC_REQUIRE(dtype == DC_BF16, DC_ERR_UNSUPPORTED, "pooling: bf16 plans only");
     DC_REQUIRE(decomp.pn > 0 && decomp.ph > 0 && decomp.pw > 0, DC_ERR_ARG, "pooling needs an explicit grid");
-    DC_REQUIRE(K >= 1 && 2 * K - 1 <= 15 && pad < K, DC_ERR_UNSUPPORTED, "pooling window K=%d pad=%d", K, pad);
+    DC_REQUIRE(K >= 1 && K % 2 == 1, DC_ERR_SHAPE, "pooling window K=%d: odd (PAPER.md:57)", K);
+    DC_REQUIRE(2 * K - 1 <= 15 && pad < K, DC_ERR_UNSUPPORTED, "pooling window K=%d pad=%d", K, pad);
     const Grid grid{decomp.pn, decomp.ph, decomp.pw};
     const int rank = comm ? comm->rank : 0;
     DC_REQUIRE(grid.size() == 1 || (comm && comm->world == grid.size()), DC_ERR_ARG,
