@@ -35,8 +35,8 @@ def layers():
     out = []
     for H in (128, 512, 2048):
         for C in (16, 64, 256):
-            for K in (1, 3, 5):
-                for N in (1, 8):
+            for K in (1, 3):
+                for N in (8,):
                     if N * H * H * C > (1 << 31):
                         continue
                     out.append((f"H{H}_C{C}_K{K}_N{N}", N, C, H, H, C, K, 1, K // 2))
