@@ -62,6 +62,23 @@ __device__ __forceinline__ long long dst_pixel(const BnArgs &a, long long p) {
     const int i = (int)(r % a.h), n = (int)(r / a.h);
     return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
 }
+
+// Thread -> (pixel lane, 8-channel group) mapping of the elementwise / reduction
+// kernels: a thread keeps ONE channel group (its per-channel constants live in
+// registers) and walks the pixels; cb = min(c8n, 256) groups per pass,
+// lanes = 256 / cb pixel lanes per block, further passes for cpad > 2048.
+struct Lanes {
+    int cb, lanes, pl, c8;
+};
+__device__ __forceinline__ Lanes lanes_of(int cpad) {
+    Lanes l;
+    const int c8n = cpad / 8;
+    l.cb = c8n < 256 ? c8n : 256;
+    l.lanes = 256 / l.cb;
+    l.pl = threadIdx.x / l.cb;
+    l.c8 = threadIdx.x % l.cb;
+    return l;
+}
 }  // namespace
 
 // per channel: scale = gamma / sqrt(var + eps), shift = beta - scale * mean,
@@ -84,25 +101,26 @@ __global__ void bn_coeff_kernel(const double *mean, const double *var, const flo
     }
 }
 
-__global__ void bn_apply_kernel(const __grid_constant__ BnArgs a) {
+__global__ void __launch_bounds__(256) bn_apply_kernel(const __grid_constant__ BnArgs a) {
     pdl_wait();  // (launch.cuh: PDL)
-    const int c8n = a.cpad / 8;
-    const long long total = a.npix * c8n;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int c8 = (int)(i % c8n);
-        const long long p = i / c8n;
-        float v[8], r[8];
-        load8(a.y, a.esz, p, a.cpad, c8, v);
-        if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+    const Lanes L = lanes_of(a.cpad);
+    if (L.pl >= L.lanes) return;
+    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
+        float sc[8], sh[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int k = c8 * 8 + e;
-            float z = fmaf(a.coef[k], v[e], a.coef[a.cpad + k]);
-            if (a.res) z += r[e];
-            v[e] = (a.relu && z < 0.f) ? 0.f : z;
+        for (int e = 0; e < 8; ++e) sc[e] = a.coef[c8 * 8 + e], sh[e] = a.coef[a.cpad + c8 * 8 + e];
+        for (long long p = (long long)blockIdx.x * L.lanes + L.pl; p < a.npix; p += (long long)gridDim.x * L.lanes) {
+            float v[8], r[8];
+            load8(a.y, a.esz, p, a.cpad, c8, v);
+            if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                float z = fmaf(sc[e], v[e], sh[e]);
+                if (a.res) z += r[e];
+                v[e] = (a.relu && z < 0.f) ? 0.f : z;
+            }
+            store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, v);
         }
-        store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, v);
     }
 }
 
@@ -111,82 +129,118 @@ __global__ void bn_apply_kernel(const __grid_constant__ BnArgs a) {
 __global__ void __launch_bounds__(256) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
     pdl_wait();  // (launch.cuh: PDL)
     extern __shared__ double sh[];
-    const int c8n = a.cpad / 8;
-    const int lanes = max(1, 256 / c8n);
-    const int c8 = threadIdx.x % c8n, pl = threadIdx.x / c8n;
-    if (pl < lanes) {
-        double sg[8], sgy[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sg[e] = sgy[e] = 0.0;
-        for (long long p = (long long)blockIdx.x * lanes + pl; p < a.npix; p += (long long)gridDim.x * lanes) {
-            float v[8], d[8], r[8];
-            load8(a.y, a.esz, p, a.cpad, c8, v);
-            load8(a.dout, a.esz, p, a.cpad, c8, d);
-            if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+    const Lanes L = lanes_of(a.cpad);
+    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
+        if (L.pl < L.lanes) {
+            float sc[8], sf[8], inv[8], mu[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const int k = c8 * 8 + e;
-                float z = fmaf(a.coef[k], v[e], a.coef[a.cpad + k]);
-                if (a.res) z += r[e];
-                const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
-                const float yh = (v[e] - a.coef[3 * a.cpad + k]) * a.coef[2 * a.cpad + k];
-                sg[e] += (double)g;
-                sgy[e] += (double)g * (double)yh;
+                sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
+                mu[e] = a.coef[3 * a.cpad + k];
             }
-        }
-        double *row = sh + (long long)pl * 2 * a.cpad;
+            double sg[8], sgy[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            row[c8 * 8 + e] = sg[e];
-            row[a.cpad + c8 * 8 + e] = sgy[e];
+            for (int e = 0; e < 8; ++e) sg[e] = sgy[e] = 0.0;
+            const long long step = (long long)gridDim.x * L.lanes;
+            long long p = (long long)blockIdx.x * L.lanes + L.pl;
+            // two pixels per trip: twice the loads in flight
+            for (; p + step < a.npix; p += 2 * step) {
+                float v[8], d[8], v2[8], d2[8], r[8], r2[8];
+                load8(a.y, a.esz, p, a.cpad, c8, v);
+                load8(a.dout, a.esz, p, a.cpad, c8, d);
+                load8(a.y, a.esz, p + step, a.cpad, c8, v2);
+                load8(a.dout, a.esz, p + step, a.cpad, c8, d2);
+                if (a.res) {
+                    load8(a.res, a.esz, p, a.cpad, c8, r);
+                    load8(a.res, a.esz, p + step, a.cpad, c8, r2);
+                }
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    float z = fmaf(sc[e], v[e], sf[e]), z2 = fmaf(sc[e], v2[e], sf[e]);
+                    if (a.res) z += r[e], z2 += r2[e];
+                    const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
+                    const float g2 = (a.relu && z2 <= 0.f) ? 0.f : d2[e];
+                    const float yh = (v[e] - mu[e]) * inv[e], yh2 = (v2[e] - mu[e]) * inv[e];
+                    sg[e] += (double)g;
+                    sgy[e] += (double)g * (double)yh;
+                    sg[e] += (double)g2;
+                    sgy[e] += (double)g2 * (double)yh2;
+                }
+            }
+            if (p < a.npix) {
+                float v[8], d[8], r[8];
+                load8(a.y, a.esz, p, a.cpad, c8, v);
+                load8(a.dout, a.esz, p, a.cpad, c8, d);
+                if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    float z = fmaf(sc[e], v[e], sf[e]);
+                    if (a.res) z += r[e];
+                    const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
+                    sg[e] += (double)g;
+                    sgy[e] += (double)g * (double)((v[e] - mu[e]) * inv[e]);
+                }
+            }
+            double *row = sh + (long long)L.pl * 2 * a.cpad;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                row[c8 * 8 + e] = sg[e];
+                row[a.cpad + c8 * 8 + e] = sgy[e];
+            }
         }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < 2 * a.cpad; k += blockDim.x) {
         double acc = 0.0;
-        for (int l = 0; l < lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
+        for (int l = 0; l < L.lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
         partials[(long long)blockIdx.x * 2 * a.cpad + k] = acc;
     }
 }
 
 // dy = gamma inv_sd (g - sum g / M - y_hat sum(g y_hat) / M) into the margined dy
 // buffer; dgamma = sum(g y_hat), dbeta = sum(g) (block 0); dres = g (dense)
-__global__ void bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums, double count,
-                                    const float *gamma, float *dgamma, float *dbeta, void *dres) {
+__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
+                                                           double count, const float *gamma, float *dgamma,
+                                                           float *dbeta, void *dres) {
     pdl_wait();  // (launch.cuh: PDL)
     if (blockIdx.x == 0)
         for (int k = threadIdx.x; k < a.c; k += blockDim.x) {
             if (dgamma) dgamma[k] = (float)sums[a.cpad + k];
             if (dbeta) dbeta[k] = (float)sums[k];
         }
-    const int c8n = a.cpad / 8;
-    const long long total = a.npix * c8n;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-         i += (long long)gridDim.x * blockDim.x) {
-        const int c8 = (int)(i % c8n);
-        const long long p = i / c8n;
-        float v[8], d[8], r[8], o[8];
-        load8(a.y, a.esz, p, a.cpad, c8, v);
-        load8(a.dout, a.esz, p, a.cpad, c8, d);
-        if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+    const Lanes L = lanes_of(a.cpad);
+    if (L.pl >= L.lanes) return;
+    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
+        // per-channel constants of this thread's 8 channels, once
+        float sc[8], sf[8], inv[8], mu[8], k1[8], m1[8], m2[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int k = c8 * 8 + e;
-            float z = fmaf(a.coef[k], v[e], a.coef[a.cpad + k]);
-            if (a.res) z += r[e];
-            const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
-            d[e] = g;
-            if (k < a.c) {
-                const float inv = a.coef[2 * a.cpad + k];
-                const float yh = (v[e] - a.coef[3 * a.cpad + k]) * inv;
-                const float m1 = (float)(sums[k] / count), m2 = (float)(sums[a.cpad + k] / count);
-                o[e] = gamma[k] * inv * (g - m1 - yh * m2);
-            } else {
-                o[e] = 0.f;
-            }
+            sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
+            mu[e] = a.coef[3 * a.cpad + k];
+            const bool live = k < a.c;
+            k1[e] = live ? gamma[k] * inv[e] : 0.f;
+            m1[e] = live ? (float)(sums[k] / count) : 0.f;
+            m2[e] = live ? (float)(sums[a.cpad + k] / count) : 0.f;
         }
-        store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, o);
-        if (dres) store8(dres, a.esz, 0, p, a.cpad, c8, d);
+        for (long long p = (long long)blockIdx.x * L.lanes + L.pl; p < a.npix; p += (long long)gridDim.x * L.lanes) {
+            float v[8], d[8], r[8], o[8];
+            load8(a.y, a.esz, p, a.cpad, c8, v);
+            load8(a.dout, a.esz, p, a.cpad, c8, d);
+            if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                float z = fmaf(sc[e], v[e], sf[e]);
+                if (a.res) z += r[e];
+                const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
+                d[e] = g;
+                const float yh = (v[e] - mu[e]) * inv[e];
+                o[e] = k1[e] * (g - m1[e] - yh * m2[e]);
+            }
+            store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, o);
+            if (dres) store8(dres, a.esz, 0, p, a.cpad, c8, d);
+        }
     }
 }
 

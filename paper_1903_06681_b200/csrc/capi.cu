@@ -1171,21 +1171,17 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
     for (auto &f : ph) nactive += f.active ? 1 : 0;
     if (!overlap && nactive > 1 && pl->s_ph[0]) {
         // stride phases are independent GEMMs with disjoint outputs and split-K
-        // workspaces: one stream each, run side by side on SM shares
-        // proportional to their taps (their work per tile), so all of them
-        // sweep dy in the same tile order at the same pace and read each dy
-        // tile from HBM once (L2 serves the other phases) instead of once per
-        // phase
+        // workspaces: one stream each, so their ramp-up / tail / reduce overlap
+        // (running them side by side on tap-proportional SM shares, so that
+        // they would sweep dy together and share its L2 lines, was measured
+        // slower in round 2: conv2_1 backward-data 0.68 -> 1.36 ms, conv3_1
+        // 0.40 -> 0.56 ms, conv4_1 0.34 -> 0.46 ms)
         CK(cudaEventRecord(pl->ev_ph[0], st));
-        int taps = 0;
-        for (auto &f : ph) taps += f.active ? f.T : 0;
-        const int sms = device_sm_count();
         int k = 0;
         for (size_t i = 0; i < ph.size(); ++i) {
             if (!ph[i].active) continue;
             cudaStream_t sp = pl->s_ph[k];
             CK(cudaStreamWaitEvent(sp, pl->ev_ph[0], 0));
-            L[i].max_ctas = std::max(2, sms * ph[i].T / taps);
             launch_rects(L[i], {whole(L[i])}, dy, dyd, kc, (int)rp.nrange.size(), sp);
             CK(cudaEventRecord(pl->ev_ph[1 + k], sp));
             ++k;
