@@ -662,9 +662,13 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     // forwards (conv4_1 fwd 0.31 -> 0.41 ms) for no net gain)
     static const bool nt_multi = std::getenv("DC_BN_FUSE_NT") != nullptr;
     const bool nt_ok = (q.nout_tiles == 1 || (q.bn > 64 && nt_multi)) && !L.out_f32;
+    // (256-wide N tiles: not fused -- measured in round 2, cold L2, N = 8:
+    // conv3_1 forward 310 -> 471 us fused, conv3_2 436 -> 528 us, against a
+    // ~55 us separate pass over y; 128-wide: conv2_2 579 -> 616 us, about the
+    // separate pass; 64-wide register accumulation: +6 us)
     q.bn_stats = !(L.bn_part && L.ksplit == 1 && nt_ok) ? 0
                  : q.bn <= 64                                      ? 2
-                 : (int64_t)q.cin_p * q.T >= 1152                  ? 1
+                 : q.bn <= 128 && (int64_t)q.cin_p * q.T >= 1152  ? 1
                                                                    : 0;
     if (L.bn_part && !q.bn_stats) L.bn_ok = false;
     if (q.bn_stats) {
