@@ -656,12 +656,10 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     // C_pad x taps >= 1152, measured: fusing a K = 576 layer costs more than
     // the separate pass over y)
     // (N tiles <= 64: register accumulation, cheap enough for any K)
-    // (several N tiles: the epilogue keeps per-CTA segments, one per N tile,
-    // for N tiles > 64 -- parity-green but opt-in, DC_BN_FUSE_NT=1: measured
-    // on the N = 8 mesh step it moves 0.31 ms from the BN pass into the
-    // forwards (conv4_1 fwd 0.31 -> 0.41 ms) for no net gain)
-    static const bool nt_multi = std::getenv("DC_BN_FUSE_NT") != nullptr;
-    const bool nt_ok = (q.nout_tiles == 1 || (q.bn > 64 && nt_multi)) && !L.out_f32;
+    // (several N tiles: not fused -- measured in round 1 on the N = 8 mesh
+    // step, per-CTA segments per N tile moved 0.31 ms from the BN pass into
+    // the forwards, conv4_1 fwd 0.31 -> 0.41 ms, for no net gain)
+    const bool nt_ok = q.nout_tiles == 1 && !L.out_f32;
     // (256-wide N tiles: not fused -- measured in round 2, cold L2, N = 8:
     // conv3_1 forward 310 -> 471 us fused, conv3_2 436 -> 528 us, against a
     // ~55 us separate pass over y; 128-wide: conv2_2 579 -> 616 us, about the

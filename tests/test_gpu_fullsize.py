@@ -237,15 +237,3 @@ def test_full_size_sampled_parity(dc, layer):
     finally:
         dc.dc_plan_destroy(plan)
 
-
-def test_bn_fused_multi_ntile_full_size():
-    """The opt-in fused BN statistics for layers with several N tiles
-    (DC_BN_FUSE_NT=1: per-CTA segments, one per N tile) on the full-size
-    512-filter layers (two N tiles of 256): same checks, child process."""
-    import subprocess
-    env = dict(os.environ, DC_BN_FUSE_NT="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__, "-k",
-                        "test_full_size_sampled_parity and (conv4_2 or conv6_2)"],
-                       env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
-    assert "2 passed" in r.stdout, r.stdout[-2000:]
