@@ -7,6 +7,8 @@
 // kernels: 16-byte vector loads, one thread per 8 channels of a pixel.
 #include <cuda_bf16.h>
 
+#include <mutex>
+
 #include "bn.cuh"
 #include "common.hpp"
 #include "launch.cuh"
@@ -61,6 +63,33 @@ __device__ __forceinline__ long long dst_pixel(const BnArgs &a, long long p) {
     const long long r = p / a.w;
     const int i = (int)(r % a.h), n = (int)(r / a.h);
     return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
+}
+
+// 2 channels (pair c2) of pixel p of a dense NHWC tensor as fp32
+__device__ __forceinline__ void load2(const void *t, int esz, long long p, int cpad, int c2, float &x0, float &x1) {
+    if (esz == 2) {
+        const uint32_t r = reinterpret_cast<const uint32_t *>(t)[(p * cpad) / 2 + c2];
+        x0 = __uint_as_float(r << 16), x1 = __uint_as_float(r & 0xffff0000u);
+    } else {
+        const float2 f = reinterpret_cast<const float2 *>(t)[(p * cpad) / 2 + c2];
+        x0 = f.x, x1 = f.y;
+    }
+}
+
+// 2 channels into a (margined) buffer pixel q: bf16, or the fp32 [hi | lo] split
+__device__ __forceinline__ void store2(void *dst, int esz, int split, long long q, int dcp, int c2, float x0,
+                                       float x1) {
+    if (esz == 2) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+        reinterpret_cast<__nv_bfloat162 *>(dst)[(q * dcp) / 2 + c2] = h;
+    } else if (split) {
+        float *d = reinterpret_cast<float *>(dst) + q * dcp + 2 * c2;
+        const float h0 = hi_tf32(x0), h1 = hi_tf32(x1);
+        d[0] = h0, d[1] = h1;
+        d[dcp / 2] = x0 - h0, d[dcp / 2 + 1] = x1 - h1;
+    } else {
+        reinterpret_cast<float2 *>(dst)[(q * dcp) / 2 + c2] = make_float2(x0, x1);
+    }
 }
 
 // Thread -> (pixel lane, 8-channel group) mapping of the elementwise / reduction
@@ -126,74 +155,60 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __grid_constant__ B
 
 // backward partials: per block fp64 sums of g and g * y_hat per channel, g the
 // output gradient through the ReLU mask (recomputed from y) -> [blocks][2][cpad]
+// Backward kernels: a thread keeps ONE channel pair (4-byte loads; a warp
+// covers 64 channels of a pixel, coalesced) and four pixels in flight per trip,
+// with few registers, so enough warps stay resident to keep HBM busy
+// (the 8-channel version with fp64 accumulators ran at 164 registers, one
+// block per SM and 16% of DRAM bandwidth).
+constexpr int kBnPix = 4;
+
 __global__ void __launch_bounds__(256) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
     pdl_wait();  // (launch.cuh: PDL)
     extern __shared__ double sh[];
-    const Lanes L = lanes_of(a.cpad);
-    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
-        if (L.pl < L.lanes) {
-            float sc[8], sf[8], inv[8], mu[8];
+    const int c2n = a.cpad / 2;
+    const int cb = c2n < 256 ? c2n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c2 = threadIdx.x % cb;
+    for (int k = threadIdx.x; k < lanes * 2 * a.cpad; k += blockDim.x) sh[k] = 0.0;
+    __syncthreads();
+    if (pl < lanes) {
+        for (int cc = c2; cc < c2n; cc += cb) {
+            const int k0 = 2 * cc;
+            const float sc0 = a.coef[k0], sc1 = a.coef[k0 + 1], sf0 = a.coef[a.cpad + k0], sf1 = a.coef[a.cpad + k0 + 1];
+            const float in0 = a.coef[2 * a.cpad + k0], in1 = a.coef[2 * a.cpad + k0 + 1];
+            const float mu0 = a.coef[3 * a.cpad + k0], mu1 = a.coef[3 * a.cpad + k0 + 1];
+            double sg0 = 0, sg1 = 0, sy0 = 0, sy1 = 0;
+            const long long step = (long long)gridDim.x * lanes;
+            for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
+                float v[kBnPix][2], d[kBnPix][2], r[kBnPix][2];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const int k = c8 * 8 + e;
-                sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
-                mu[e] = a.coef[3 * a.cpad + k];
-            }
-            double sg[8], sgy[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) sg[e] = sgy[e] = 0.0;
-            const long long step = (long long)gridDim.x * L.lanes;
-            long long p = (long long)blockIdx.x * L.lanes + L.pl;
-            // two pixels per trip: twice the loads in flight
-            for (; p + step < a.npix; p += 2 * step) {
-                float v[8], d[8], v2[8], d2[8], r[8], r2[8];
-                load8(a.y, a.esz, p, a.cpad, c8, v);
-                load8(a.dout, a.esz, p, a.cpad, c8, d);
-                load8(a.y, a.esz, p + step, a.cpad, c8, v2);
-                load8(a.dout, a.esz, p + step, a.cpad, c8, d2);
-                if (a.res) {
-                    load8(a.res, a.esz, p, a.cpad, c8, r);
-                    load8(a.res, a.esz, p + step, a.cpad, c8, r2);
+                for (int u = 0; u < kBnPix; ++u) {
+                    const long long p = p0 + u * step;
+                    v[u][0] = v[u][1] = d[u][0] = d[u][1] = r[u][0] = r[u][1] = 0.f;
+                    if (p < a.npix) {
+                        load2(a.y, a.esz, p, a.cpad, cc, v[u][0], v[u][1]);
+                        load2(a.dout, a.esz, p, a.cpad, cc, d[u][0], d[u][1]);
+                        if (a.res) load2(a.res, a.esz, p, a.cpad, cc, r[u][0], r[u][1]);
+                    }
                 }
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    float z = fmaf(sc[e], v[e], sf[e]), z2 = fmaf(sc[e], v2[e], sf[e]);
-                    if (a.res) z += r[e], z2 += r2[e];
-                    const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
-                    const float g2 = (a.relu && z2 <= 0.f) ? 0.f : d2[e];
-                    const float yh = (v[e] - mu[e]) * inv[e], yh2 = (v2[e] - mu[e]) * inv[e];
-                    sg[e] += (double)g;
-                    sgy[e] += (double)g * (double)yh;
-                    sg[e] += (double)g2;
-                    sgy[e] += (double)g2 * (double)yh2;
+                for (int u = 0; u < kBnPix; ++u) {
+                    if (p0 + u * step >= a.npix) break;
+                    const float z0 = fmaf(sc0, v[u][0], sf0) + r[u][0], z1 = fmaf(sc1, v[u][1], sf1) + r[u][1];
+                    const float g0 = (a.relu && z0 <= 0.f) ? 0.f : d[u][0];
+                    const float g1 = (a.relu && z1 <= 0.f) ? 0.f : d[u][1];
+                    sg0 += (double)g0, sg1 += (double)g1;
+                    sy0 += (double)g0 * (double)((v[u][0] - mu0) * in0);
+                    sy1 += (double)g1 * (double)((v[u][1] - mu1) * in1);
                 }
             }
-            if (p < a.npix) {
-                float v[8], d[8], r[8];
-                load8(a.y, a.esz, p, a.cpad, c8, v);
-                load8(a.dout, a.esz, p, a.cpad, c8, d);
-                if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    float z = fmaf(sc[e], v[e], sf[e]);
-                    if (a.res) z += r[e];
-                    const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
-                    sg[e] += (double)g;
-                    sgy[e] += (double)g * (double)((v[e] - mu[e]) * inv[e]);
-                }
-            }
-            double *row = sh + (long long)L.pl * 2 * a.cpad;
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                row[c8 * 8 + e] = sg[e];
-                row[a.cpad + c8 * 8 + e] = sgy[e];
-            }
+            double *row = sh + (long long)pl * 2 * a.cpad;
+            row[k0] = sg0, row[k0 + 1] = sg1, row[a.cpad + k0] = sy0, row[a.cpad + k0 + 1] = sy1;
         }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < 2 * a.cpad; k += blockDim.x) {
         double acc = 0.0;
-        for (int l = 0; l < L.lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
+        for (int l = 0; l < lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
         partials[(long long)blockIdx.x * 2 * a.cpad + k] = acc;
     }
 }
@@ -209,14 +224,16 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant
             if (dgamma) dgamma[k] = (float)sums[a.cpad + k];
             if (dbeta) dbeta[k] = (float)sums[k];
         }
-    const Lanes L = lanes_of(a.cpad);
-    if (L.pl >= L.lanes) return;
-    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
-        // per-channel constants of this thread's 8 channels, once
-        float sc[8], sf[8], inv[8], mu[8], k1[8], m1[8], m2[8];
+    const int c2n = a.cpad / 2;
+    const int cb = c2n < 256 ? c2n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c2 = threadIdx.x % cb;
+    if (pl >= lanes) return;
+    for (int cc = c2; cc < c2n; cc += cb) {
+        // the pair's constants, once
+        float sc[2], sf[2], inv[2], mu[2], k1[2], m1[2], m2[2];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int k = c8 * 8 + e;
+        for (int e = 0; e < 2; ++e) {
+            const int k = 2 * cc + e;
             sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
             mu[e] = a.coef[3 * a.cpad + k];
             const bool live = k < a.c;
@@ -224,30 +241,42 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant
             m1[e] = live ? (float)(sums[k] / count) : 0.f;
             m2[e] = live ? (float)(sums[a.cpad + k] / count) : 0.f;
         }
-        for (long long p = (long long)blockIdx.x * L.lanes + L.pl; p < a.npix; p += (long long)gridDim.x * L.lanes) {
-            float v[8], d[8], r[8], o[8];
-            load8(a.y, a.esz, p, a.cpad, c8, v);
-            load8(a.dout, a.esz, p, a.cpad, c8, d);
-            if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+        const long long step = (long long)gridDim.x * lanes;
+        for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
+            float v[kBnPix][2], d[kBnPix][2], r[kBnPix][2];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                float z = fmaf(sc[e], v[e], sf[e]);
-                if (a.res) z += r[e];
-                const float g = (a.relu && z <= 0.f) ? 0.f : d[e];
-                d[e] = g;
-                const float yh = (v[e] - mu[e]) * inv[e];
-                o[e] = k1[e] * (g - m1[e] - yh * m2[e]);
+            for (int u = 0; u < kBnPix; ++u) {
+                const long long p = p0 + u * step;
+                v[u][0] = v[u][1] = d[u][0] = d[u][1] = r[u][0] = r[u][1] = 0.f;
+                if (p < a.npix) {
+                    load2(a.y, a.esz, p, a.cpad, cc, v[u][0], v[u][1]);
+                    load2(a.dout, a.esz, p, a.cpad, cc, d[u][0], d[u][1]);
+                    if (a.res) load2(a.res, a.esz, p, a.cpad, cc, r[u][0], r[u][1]);
+                }
             }
-            store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, o);
-            if (dres) store8(dres, a.esz, 0, p, a.cpad, c8, d);
+#pragma unroll
+            for (int u = 0; u < kBnPix; ++u) {
+                const long long p = p0 + u * step;
+                if (p >= a.npix) break;
+                float o[2], g[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
+                    g[e] = (a.relu && z <= 0.f) ? 0.f : d[u][e];
+                    const float yh = (v[u][e] - mu[e]) * inv[e];
+                    o[e] = k1[e] * (g[e] - m1[e] - yh * m2[e]);
+                }
+                store2(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, cc, o[0], o[1]);
+                if (dres) store2(dres, a.esz, 0, p, a.cpad, cc, g[0], g[1]);
+            }
         }
     }
 }
 
 int bn_bwd_blocks(long long npix, int cpad) {
-    const int lanes = std::max(1, 256 / (cpad / 8));
-    const long long iters = (npix + lanes - 1) / lanes;
-    return (int)std::max<long long>(1, std::min<long long>((iters + 15) / 16, 148 * 2));
+    const int c2n = cpad / 2, lanes = std::max(1, 256 / std::min(c2n, 256));
+    const long long trips = (npix + lanes - 1) / lanes;
+    return (int)std::max<long long>(1, std::min<long long>((trips + 4 * kBnPix - 1) / (4 * kBnPix), 148 * 8));
 }
 
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
@@ -265,18 +294,20 @@ void launch_bn_apply(const BnArgs &a, cudaStream_t st) {
 }
 
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st) {
-    DC_REQUIRE(a.cpad % 8 == 0 && a.cpad / 8 <= 256, DC_ERR_UNSUPPORTED, "BN backward: channels");
-    const int lanes = std::max(1, 256 / (a.cpad / 8));
-    launch_k(bn_bwd_partials_kernel, dim3(blocks), dim3(256), (size_t)lanes * 2 * a.cpad * sizeof(double), st, 1,
-             "bn bwd partials", a, partials);
+    DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 4096, DC_ERR_UNSUPPORTED, "BN backward: channels");
+    const int lanes = std::max(1, 256 / std::min(a.cpad / 2, 256));
+    const size_t smem = (size_t)lanes * 2 * a.cpad * sizeof(double);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaFuncSetAttribute(bn_bwd_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    });
+    launch_k(bn_bwd_partials_kernel, dim3(blocks), dim3(256), smem, st, 1, "bn bwd partials", a, partials);
 }
 
 void launch_bn_bwd_apply(const BnArgs &a, const double *sums, double count, const float *gamma, float *dgamma,
                          float *dbeta, void *dres, cudaStream_t st) {
-    const long long total = a.npix * (a.cpad / 8);
-    const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, 148 * 16));
-    launch_k(bn_bwd_apply_kernel, dim3(blocks), dim3(256), 0, st, 1, "bn bwd apply", a, sums, count, gamma, dgamma,
-             dbeta, dres);
+    launch_k(bn_bwd_apply_kernel, dim3(bn_bwd_blocks(a.npix, a.cpad)), dim3(256), 0, st, 1, "bn bwd apply", a, sums,
+             count, gamma, dgamma, dbeta, dres);
 }
 
 // Loads this file's kernels (see preload_conv_v2)
