@@ -8,8 +8,8 @@ Tolerances: apply -- the fp32 evaluation a y + b (+ r) is
 within 4 u (|a y| + |b| + |r|) of the exact value, then the bf16 store adds
 2^-8 |out|; backward -- dy = k (g - m1 - y_hat m2) evaluated in fp32 from
 fp64 group sums: within 8 u |k| (|g| + |m1| + |y_hat| |m2|) + 2^-8 |dy|;
-dgamma, dbeta (fp64 sums of fp32 terms): within 4 u sum |g y_hat|, u sum |g|
-(u = 2^-24)."""
+dgamma, dbeta (fp32 sums of <= 4 pixels, then fp64): within 6 u sum |g y_hat|,
+5 u sum |g| (u = 2^-24)."""
 import numpy as np
 import pytest
 import torch
@@ -87,8 +87,10 @@ def check_backward(got_dy, got_dg, got_db, dout, y, m, v, g, b, res, relu):
     bound = 8 * U * mag + 2.0 ** -8 * np.abs(dy) + 1e-30
     err = np.abs(got_dy - dy)
     assert (err <= bound).all(), f"BN bwd dy: {(err > bound).sum()} over bound (worst {(err / bound).max():.2f}x)"
-    tg = 4 * U * np.abs(gm * yh).sum(axis=(0, 2, 3)) + 1e-12
-    tb = 2 * U * np.abs(gm).sum(axis=(0, 2, 3)) + 1e-12
+    # per-thread fp32 sums over a trip of <= 4 pixels (4 fused adds), then fp64
+    # (DESIGN.md §7): <= 4 u sum|term|, plus the final fp32 rounding of the sum
+    tg = 6 * U * np.abs(gm * yh).sum(axis=(0, 2, 3)) + 1e-12
+    tb = 5 * U * np.abs(gm).sum(axis=(0, 2, 3)) + 1e-12
     assert (np.abs(got_dg - dgam) <= tg).all(), "dgamma"
     assert (np.abs(got_db - dbet) <= tb).all(), "dbeta"
 

@@ -42,7 +42,7 @@ CASES = [  # (N, C, H, W, K, S, P), grid
     ((2, 64, 24, 20, 3, 2, 1), (1, 1, 2)),
     ((2, 64, 24, 20, 3, 2, 1), (1, 2, 2)),    # 2D grid: corners
     ((2, 32, 25, 23, 3, 2, 1), (2, 2, 1)),    # ragged, hybrid sample x spatial
-    ((1, 16, 32, 16, 3, 3, 0), (1, 4, 1)),    # non-overlapping windows (K = S)
+    ((1, 16, 33, 17, 3, 2, 0), (1, 4, 1)),    # no padding, thin 4-way H split
     ((1, 16, 20, 18, 3, 1, 1), (1, 2, 1)),    # stride 1
 ]
 
