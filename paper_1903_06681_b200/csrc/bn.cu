@@ -65,32 +65,55 @@ __device__ __forceinline__ long long dst_pixel(const BnArgs &a, long long p) {
     return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
 }
 
-// 2 channels (pair c2) of pixel p of a dense NHWC tensor as fp32
-__device__ __forceinline__ void load2(const void *t, int esz, long long p, int cpad, int c2, float &x0, float &x1) {
+// 4 channels (quad c4) of pixel p of a dense NHWC tensor as fp32
+__device__ __forceinline__ void load4(const void *t, int esz, long long p, int cpad, int c4, float (&x)[4]) {
     if (esz == 2) {
-        const uint32_t r = reinterpret_cast<const uint32_t *>(t)[(p * cpad) / 2 + c2];
-        x0 = __uint_as_float(r << 16), x1 = __uint_as_float(r & 0xffff0000u);
+        const uint2 r = reinterpret_cast<const uint2 *>(t)[(p * cpad) / 4 + c4];
+        x[0] = __uint_as_float(r.x << 16), x[1] = __uint_as_float(r.x & 0xffff0000u);
+        x[2] = __uint_as_float(r.y << 16), x[3] = __uint_as_float(r.y & 0xffff0000u);
     } else {
-        const float2 f = reinterpret_cast<const float2 *>(t)[(p * cpad) / 2 + c2];
-        x0 = f.x, x1 = f.y;
+        const float4 f = reinterpret_cast<const float4 *>(t)[(p * cpad) / 4 + c4];
+        x[0] = f.x, x[1] = f.y, x[2] = f.z, x[3] = f.w;
     }
 }
 
-// 2 channels into a (margined) buffer pixel q: bf16, or the fp32 [hi | lo] split
-__device__ __forceinline__ void store2(void *dst, int esz, int split, long long q, int dcp, int c2, float x0,
-                                       float x1) {
+// 4 channels into a (margined) buffer pixel q: bf16, or the fp32 [hi | lo] split
+__device__ __forceinline__ void store4(void *dst, int esz, int split, long long q, int dcp, int c4,
+                                       const float (&x)[4]) {
     if (esz == 2) {
-        const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-        reinterpret_cast<__nv_bfloat162 *>(dst)[(q * dcp) / 2 + c2] = h;
+        const __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
+        uint2 r;
+        r.x = *reinterpret_cast<const uint32_t *>(&h0), r.y = *reinterpret_cast<const uint32_t *>(&h1);
+        reinterpret_cast<uint2 *>(dst)[(q * dcp) / 4 + c4] = r;
     } else if (split) {
-        float *d = reinterpret_cast<float *>(dst) + q * dcp + 2 * c2;
-        const float h0 = hi_tf32(x0), h1 = hi_tf32(x1);
-        d[0] = h0, d[1] = h1;
-        d[dcp / 2] = x0 - h0, d[dcp / 2 + 1] = x1 - h1;
+        float *d = reinterpret_cast<float *>(dst) + q * dcp + 4 * c4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const float h = hi_tf32(x[e]);
+            d[e] = h, d[dcp / 2 + e] = x[e] - h;
+        }
     } else {
-        reinterpret_cast<float2 *>(dst)[(q * dcp) / 2 + c2] = make_float2(x0, x1);
+        reinterpret_cast<float4 *>(dst)[(q * dcp) / 4 + c4] = make_float4(x[0], x[1], x[2], x[3]);
     }
 }
+
+// Pixel p = (n, i, j) of an n x h x w block walked with a fixed stride: the
+// margined-buffer position without a division per step.
+struct PixWalk {
+    int n, i, j, sn, si, sj;
+    __device__ __forceinline__ void init(const BnArgs &a, long long p, long long step) {
+        j = (int)(p % a.w), i = (int)((p / a.w) % a.h), n = (int)(p / ((long long)a.w * a.h));
+        sj = (int)(step % a.w), si = (int)((step / a.w) % a.h), sn = (int)(step / ((long long)a.w * a.h));
+    }
+    __device__ __forceinline__ void next(const BnArgs &a) {
+        j += sj, i += si, n += sn;
+        if (j >= a.w) j -= a.w, ++i;
+        if (i >= a.h) i -= a.h, ++n;
+    }
+    __device__ __forceinline__ long long pos(const BnArgs &a) const {
+        return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
+    }
+};
 
 // Thread -> (pixel lane, 8-channel group) mapping of the elementwise / reduction
 // kernels: a thread keeps ONE channel group (its per-channel constants live in
@@ -155,58 +178,64 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __grid_constant__ B
 
 // backward partials: per block fp64 sums of g and g * y_hat per channel, g the
 // output gradient through the ReLU mask (recomputed from y) -> [blocks][2][cpad]
-// Backward kernels: a thread keeps ONE channel pair (4-byte loads; a warp
-// covers 64 channels of a pixel, coalesced) and four pixels in flight per trip,
-// with few registers, so enough warps stay resident to keep HBM busy
-// (the 8-channel version with fp64 accumulators ran at 164 registers, one
-// block per SM and 16% of DRAM bandwidth).
-constexpr int kBnPix = 4;
+// Backward kernels: a thread keeps ONE quad of channels (8-byte loads; a
+// warp covers 128 channels of a pixel, coalesced) with its per-channel
+// constants in registers, and two pixels in flight per trip; the margined
+// output position is walked, not divided out. (The 8-channel version with
+// fp64 accumulators ran at 164 registers and 16% of DRAM bandwidth; a
+// 2-channel one at 4-byte loads and a 64-bit division per pixel at 19%.)
+constexpr int kBnPix = 2;
 
-__global__ void __launch_bounds__(256) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
+__global__ void __launch_bounds__(256, 3) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
     pdl_wait();  // (launch.cuh: PDL)
     extern __shared__ double sh[];
-    const int c2n = a.cpad / 2;
-    const int cb = c2n < 256 ? c2n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c2 = threadIdx.x % cb;
+    const int c4n = a.cpad / 4;
+    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
     for (int k = threadIdx.x; k < lanes * 2 * a.cpad; k += blockDim.x) sh[k] = 0.0;
     __syncthreads();
     if (pl < lanes) {
-        for (int cc = c2; cc < c2n; cc += cb) {
-            const int k0 = 2 * cc;
-            const float sc0 = a.coef[k0], sc1 = a.coef[k0 + 1], sf0 = a.coef[a.cpad + k0], sf1 = a.coef[a.cpad + k0 + 1];
-            const float in0 = a.coef[2 * a.cpad + k0], in1 = a.coef[2 * a.cpad + k0 + 1];
-            const float mu0 = a.coef[3 * a.cpad + k0], mu1 = a.coef[3 * a.cpad + k0 + 1];
-            double sg0 = 0, sg1 = 0, sy0 = 0, sy1 = 0;
+        for (int cc = c4; cc < c4n; cc += cb) {
+            float sc[4], sf[4], inv[4], mu[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int k = 4 * cc + e;
+                sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
+                mu[e] = a.coef[3 * a.cpad + k];
+            }
+            double sg[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
             const long long step = (long long)gridDim.x * lanes;
             for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
-                float v[kBnPix][2], d[kBnPix][2], r[kBnPix][2];
+                float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
 #pragma unroll
                 for (int u = 0; u < kBnPix; ++u) {
                     const long long p = p0 + u * step;
-                    v[u][0] = v[u][1] = d[u][0] = d[u][1] = r[u][0] = r[u][1] = 0.f;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
                     if (p < a.npix) {
-                        load2(a.y, a.esz, p, a.cpad, cc, v[u][0], v[u][1]);
-                        load2(a.dout, a.esz, p, a.cpad, cc, d[u][0], d[u][1]);
-                        if (a.res) load2(a.res, a.esz, p, a.cpad, cc, r[u][0], r[u][1]);
+                        load4(a.y, a.esz, p, a.cpad, cc, v[u]);
+                        load4(a.dout, a.esz, p, a.cpad, cc, d[u]);
+                        if (a.res) load4(a.res, a.esz, p, a.cpad, cc, r[u]);
                     }
                 }
-                // fp32 sums of the trip's <= 4 pixels, then one fp64 add per
-                // trip (fp64 arithmetic per element ran the kernel at 1.6 ms
-                // for 2.1 GB; error <= (3 + 1) u sum|term|)
-                float tg0 = 0.f, tg1 = 0.f, ty0 = 0.f, ty1 = 0.f;
+                // fp32 sums of the trip's pixels, then one fp64 add per trip
+                // (fp64 per element was slow; error bound: DESIGN.md §7)
 #pragma unroll
-                for (int u = 0; u < kBnPix; ++u) {
-                    const float z0 = fmaf(sc0, v[u][0], sf0) + r[u][0], z1 = fmaf(sc1, v[u][1], sf1) + r[u][1];
-                    const float g0 = (a.relu && z0 <= 0.f) ? 0.f : d[u][0];   // (padding pixels: d = 0)
-                    const float g1 = (a.relu && z1 <= 0.f) ? 0.f : d[u][1];
-                    tg0 += g0, tg1 += g1;
-                    ty0 = fmaf(g0, (v[u][0] - mu0) * in0, ty0);
-                    ty1 = fmaf(g1, (v[u][1] - mu1) * in1, ty1);
+                for (int e = 0; e < 4; ++e) {
+                    float tg = 0.f, ty = 0.f;
+#pragma unroll
+                    for (int u = 0; u < kBnPix; ++u) {
+                        const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
+                        const float g = (a.relu && z <= 0.f) ? 0.f : d[u][e];  // (padding pixels: d = 0)
+                        tg += g;
+                        ty = fmaf(g, (v[u][e] - mu[e]) * inv[e], ty);
+                    }
+                    sg[e] += (double)tg, sy[e] += (double)ty;
                 }
-                sg0 += (double)tg0, sg1 += (double)tg1, sy0 += (double)ty0, sy1 += (double)ty1;
             }
             double *row = sh + (long long)pl * 2 * a.cpad;
-            row[k0] = sg0, row[k0 + 1] = sg1, row[a.cpad + k0] = sy0, row[a.cpad + k0 + 1] = sy1;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) row[4 * cc + e] = sg[e], row[a.cpad + 4 * cc + e] = sy[e];
         }
     }
     __syncthreads();
@@ -219,7 +248,7 @@ __global__ void __launch_bounds__(256) bn_bwd_partials_kernel(const __grid_const
 
 // dy = gamma inv_sd (g - sum g / M - y_hat sum(g y_hat) / M) into the margined dy
 // buffer; dgamma = sum(g y_hat), dbeta = sum(g) (block 0); dres = g (dense)
-__global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
+__global__ void __launch_bounds__(256, 3) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
                                                            double count, const float *gamma, float *dgamma,
                                                            float *dbeta, void *dres) {
     pdl_wait();  // (launch.cuh: PDL)
@@ -228,16 +257,16 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant
             if (dgamma) dgamma[k] = (float)sums[a.cpad + k];
             if (dbeta) dbeta[k] = (float)sums[k];
         }
-    const int c2n = a.cpad / 2;
-    const int cb = c2n < 256 ? c2n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c2 = threadIdx.x % cb;
+    const int c4n = a.cpad / 4;
+    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
     if (pl >= lanes) return;
-    for (int cc = c2; cc < c2n; cc += cb) {
-        // the pair's constants, once
-        float sc[2], sf[2], inv[2], mu[2], k1[2], m1[2], m2[2];
+    for (int cc = c4; cc < c4n; cc += cb) {
+        // the quad's constants, once
+        float sc[4], sf[4], inv[4], mu[4], k1[4], m1[4], m2[4];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int k = 2 * cc + e;
+        for (int e = 0; e < 4; ++e) {
+            const int k = 4 * cc + e;
             sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
             mu[e] = a.coef[3 * a.cpad + k];
             const bool live = k < a.c;
@@ -246,41 +275,47 @@ __global__ void __launch_bounds__(256) bn_bwd_apply_kernel(const __grid_constant
             m2[e] = live ? (float)(sums[a.cpad + k] / count) : 0.f;
         }
         const long long step = (long long)gridDim.x * lanes;
-        for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
-            float v[kBnPix][2], d[kBnPix][2], r[kBnPix][2];
+        long long p = (long long)blockIdx.x * lanes + pl;
+        if (p >= a.npix) continue;
+        PixWalk q;
+        q.init(a, p, step);
+        while (p < a.npix) {
+            float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
 #pragma unroll
             for (int u = 0; u < kBnPix; ++u) {
-                const long long p = p0 + u * step;
-                v[u][0] = v[u][1] = d[u][0] = d[u][1] = r[u][0] = r[u][1] = 0.f;
-                if (p < a.npix) {
-                    load2(a.y, a.esz, p, a.cpad, cc, v[u][0], v[u][1]);
-                    load2(a.dout, a.esz, p, a.cpad, cc, d[u][0], d[u][1]);
-                    if (a.res) load2(a.res, a.esz, p, a.cpad, cc, r[u][0], r[u][1]);
+                const long long pu = p + u * step;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
+                if (pu < a.npix) {
+                    load4(a.y, a.esz, pu, a.cpad, cc, v[u]);
+                    load4(a.dout, a.esz, pu, a.cpad, cc, d[u]);
+                    if (a.res) load4(a.res, a.esz, pu, a.cpad, cc, r[u]);
                 }
             }
 #pragma unroll
             for (int u = 0; u < kBnPix; ++u) {
-                const long long p = p0 + u * step;
                 if (p >= a.npix) break;
-                float o[2], g[2];
+                float o[4], g[4];
 #pragma unroll
-                for (int e = 0; e < 2; ++e) {
+                for (int e = 0; e < 4; ++e) {
                     const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
                     g[e] = (a.relu && z <= 0.f) ? 0.f : d[u][e];
                     const float yh = (v[u][e] - mu[e]) * inv[e];
                     o[e] = k1[e] * (g[e] - m1[e] - yh * m2[e]);
                 }
-                store2(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, cc, o[0], o[1]);
-                if (dres) store2(dres, a.esz, 0, p, a.cpad, cc, g[0], g[1]);
+                store4(a.dst, a.esz, a.split, q.pos(a), a.dcp, cc, o);
+                if (dres) store4(dres, a.esz, 0, p, a.cpad, cc, g);
+                p += step;
+                q.next(a);
             }
         }
     }
 }
 
 int bn_bwd_blocks(long long npix, int cpad) {
-    const int c2n = cpad / 2, lanes = std::max(1, 256 / std::min(c2n, 256));
+    const int c4n = cpad / 4, lanes = std::max(1, 256 / std::min(c4n, 256));
     const long long trips = (npix + lanes - 1) / lanes;
-    return (int)std::max<long long>(1, std::min<long long>((trips + 4 * kBnPix - 1) / (4 * kBnPix), 148 * 8));
+    return (int)std::max<long long>(1, std::min<long long>((trips + 8 * kBnPix - 1) / (8 * kBnPix), 148 * 8));
 }
 
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
@@ -299,7 +334,7 @@ void launch_bn_apply(const BnArgs &a, cudaStream_t st) {
 
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st) {
     DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 4096, DC_ERR_UNSUPPORTED, "BN backward: channels");
-    const int lanes = std::max(1, 256 / std::min(a.cpad / 2, 256));
+    const int lanes = std::max(1, 256 / std::min(a.cpad / 4, 256));
     const size_t smem = (size_t)lanes * 2 * a.cpad * sizeof(double);
     static std::once_flag once;
     std::call_once(once, [] {

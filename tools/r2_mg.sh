@@ -22,9 +22,9 @@ for dec in "$P,1,1" "$((P/2)),2,1"; do
   run resnet_${dec//,/_} 420 $TR --master-port 29534 bench.py --gpus $P --workload resnet50_n64 --decomp $dec --steps 10 --warmup 5 --watchdog 300
   python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(d['value'],d['ms_per_step'])" gpurun_out/mg${P}_resnet_${dec//,/_}.out
 done
-run c5 1800 $TR --master-port 29533 tools/c5_sweep.py --out gpurun_out/c5_e7_${P}gpu.jsonl; tail -25 gpurun_out/mg${P}_c5.out
 # halo hiding: the same step with the non-overlapped schedule and with the exchanges removed (diagnostic)
 run noov 420 $TR --master-port 29536 bench.py --gpus $P --steps 10 --warmup 5 --no-overlap --watchdog 300
 python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print('no-overlap',d['value'],d['ms_per_step'])" gpurun_out/mg${P}_noov.out
 run noex 420 $TR --master-port 29537 bench.py --gpus $P --steps 10 --warmup 5 --ablate exchange --watchdog 300
 python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print('no-exchange',d['value'],d['ms_per_step'])" gpurun_out/mg${P}_noex.out
+run c5 1500 $TR --master-port 29533 tools/c5_sweep.py --out gpurun_out/c5_e7_${P}gpu.jsonl; tail -25 gpurun_out/mg${P}_c5.out
