@@ -492,7 +492,17 @@ struct GemmLaunch {
     // block into the owners' receive slots (ConvV2Params::scat)
     float *scat[8] = {};
     int scat_seg = 0;
+    // a 1x1 stride-1 conv on a margin-free shard is a plain GEMM over pixels:
+    // the shard is launched as ONE row of n h w pixels in 1 x 128 tiles, which
+    // cross image rows and samples (small images waste no tile rows)
+    bool flat = false;
 };
+
+// The 1x1 stride-1 flattening applies (no padding, no margins on the input).
+bool flat_ok(const ConvGeom &g, const dc_shard_desc_t &in) {
+    return g.K == 1 && g.S == 1 && g.P == 0 && in.halo_n == 0 && in.halo_s == 0 && in.halo_w == 0 &&
+           in.halo_e == 0 && in.n * in.hb * in.wb < (int64_t(1) << 31);
+}
 
 OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
 
@@ -591,6 +601,7 @@ void prepare_fwd(dc_plan_s *pl, const void *x, const void *w, void *y, GemmLaunc
     L.ksplit = choose_ksplit(L.work_hint, L.cin);
     attach_ksplit(pl, L, (int)rp.nrange.size());
     apply_scatter(pl, L);
+    L.flat = flat_ok(g, xd) && L.interior.size() + L.boundary.size() == 1;
 }
 
 // Launch a conv GEMM over `rects`; one launch per distinct tile width (the A
@@ -737,6 +748,17 @@ bool launch_rects_v2(GemmLaunch &L, const std::vector<OutRect> &rects, const voi
 void launch_rects(GemmLaunch &L, const std::vector<OutRect> &rects, const void *in_base,
                   const dc_shard_desc_t &ind, int64_t cin_p, int nsamples, cudaStream_t st) {
     if (rects.empty()) return;
+    if (L.flat) {  // the whole shard as one row of pixels (the rects cover it all)
+        dc_shard_desc_t f = ind;
+        f.wb = f.w = ind.n * ind.hb * ind.wb;
+        f.n = 1, f.hb = f.h = 1;
+        const int ws_h = L.ws_h, ws_w = L.ws_w;
+        L.ws_h = 1, L.ws_w = (int)f.wb;
+        const bool ok = launch_rects_v2(L, {OutRect{0, 0, 1, (int)f.wb}}, in_base, f, cin_p, 1, st);
+        L.ws_h = ws_h, L.ws_w = ws_w;
+        DC_REQUIRE(ok, DC_ERR_UNSUPPORTED, "1x1 conv: the tile-reuse kernel does not fit");
+        return;
+    }
     if (launch_rects_v2(L, rects, in_base, ind, cin_p, nsamples, st)) return;
     DC_REQUIRE(L.kind == 0, DC_ERR_UNSUPPORTED, "3xTF32: the tile-reuse kernel does not fit this layer");
     DC_REQUIRE(L.scat_seg == 0, DC_ERR_UNSUPPORTED, "channel-parallel partials: the tile-reuse kernel does not fit");
@@ -1145,6 +1167,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
                                   (int64_t)pl->splitk_world());
         L[i].ksplit = choose_ksplit(L[i].work_hint, kc);
         apply_scatter(pl, L[i]);
+        L[i].flat = S == 1 && flat_ok(g, dyd) && L[i].interior.size() + L[i].boundary.size() == 1;
     }
     // one split-K workspace region per phase: the phases' interior and
     // boundary launches may run concurrently on two streams

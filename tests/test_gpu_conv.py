@@ -91,6 +91,10 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     # backward-data): the accumulator hand-off must count exactly its warps
     (2, 64, 96, 128, 256, 3, 1, 1),
     (2, 16, 192, 256, 64, 3, 2, 1),
+    # 1x1 stride 1 on small images: launched as one row of n h w pixels
+    # (1 x 128 tiles across images), with a ragged last tile
+    (16, 256, 7, 7, 512, 1, 1, 0),
+    (5, 64, 13, 11, 128, 1, 1, 0),
 ]
 
 
