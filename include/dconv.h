@@ -109,6 +109,11 @@ typedef struct dc_plan_s *dc_plan_t;
                                   exchange on the caller's stream, then compute the whole
                                   shard in one pass -- the non-overlapped schedule of the
                                   performance model (no overlap)      */
+#define DC_FORCE_OVERLAP 0x100u /* with DC_EXCHANGE: always run the interior tiles while the
+                                  halo arrives and the boundary tiles after it.
+                                  Default: that overlap only for halos of >= 8 MB per rank;
+                                  smaller ones are exchanged first and the shard computed in
+                                  one launch (measured faster) */
 #define DC_DEFAULT_FLAGS (DC_EXCHANGE | DC_ALLREDUCE)
 
 /* COLLECTIVE. Create the communicator of `world` ranks. nccl_uid128 points to

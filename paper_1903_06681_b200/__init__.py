@@ -23,6 +23,7 @@ DC_X, DC_Y, DC_DY, DC_DX, DC_W, DC_DW = range(6)
 DC_EXCHANGE, DC_ALLREDUCE, DC_HALO_NCCL, DC_ALLREDUCE_ASYNC, DC_BN_STATS, DC_DETERMINISTIC, DC_DW_ATOMIC = (
     0x1, 0x2, 0x4, 0x8, 0x10, 0x20, 0x40)
 DC_NO_OVERLAP = 0x80
+DC_FORCE_OVERLAP = 0x100
 DC_DEFAULT_FLAGS = DC_EXCHANGE | DC_ALLREDUCE
 DC_BN_LOCAL, DC_BN_FROM_FWD = 0x1, 0x2
 DC_IMPORT_ASYNC, DC_SRC_BF16 = 0x1, 0x2

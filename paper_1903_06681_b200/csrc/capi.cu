@@ -827,6 +827,23 @@ P2PExchange build_p2p(dc_plan_s *pl, int which, void *buf) {
     return x;
 }
 
+// Halo bytes this rank receives for tensor `which` (0: x, 1: dy).
+size_t halo_recv_bytes(const dc_plan_s *pl, int which) {
+    const RankPlan &rp = pl->rp;
+    const int64_t px = describe(rp, which == 0 ? DC_X : DC_DY).c_pad * rp.g.esz();
+    size_t b = 0;
+    for (auto &m : which == 0 ? rp.x_recv : rp.dy_recv) b += (size_t)rp.nrange.size() * m.rows.size() * m.cols.size() * px;
+    return b;
+}
+
+// Interior / boundary overlap of an exchange only when the
+// halo is large: measured in round 2 on the mesh2k_n8 step, where every halo
+// is <= 2 MB (one row), exchanging first and computing the whole shard in one
+// launch beat the two-launch overlap (2 GPUs 20.46 -> 20.27 ms, 4 GPUs 12.15
+// -> 11.81 ms; the whole step's exchanges cost 0.7 / 1.0 ms): a ~15 us
+// exchange is cheaper than the extra boundary launch that hides it.
+constexpr size_t kOverlapMinHaloBytes = size_t(8) << 20;
+
 void exchange(dc_plan_s *pl, int which, void *buf, unsigned flags, cudaStream_t st) {
     const RankPlan &rp = pl->rp;
     const auto &sends = which == 0 ? rp.x_send : rp.dy_send;
@@ -1185,8 +1202,9 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2 + ks_off[i] / sizeof(float);
         }
     const bool need_dy = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
-    if (need_dy && (flags & DC_NO_OVERLAP)) exchange(pl, 1, dy, flags, st);  // exchange, then compute
-    const bool overlap = need_dy && !(flags & DC_NO_OVERLAP);
+    const bool overlap = need_dy && !(flags & DC_NO_OVERLAP) &&
+                         ((flags & DC_FORCE_OVERLAP) || halo_recv_bytes(pl, 1) >= kOverlapMinHaloBytes);
+    if (need_dy && !overlap) exchange(pl, 1, dy, flags, st);  // exchange, then compute
     if (overlap) {
         CK(cudaEventRecord(pl->ev[0], st));
         CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
@@ -1950,7 +1968,8 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     const dc_shard_desc_t xd = describe(pl->rp, DC_X);
     const int nl = (int)pl->rp.nrange.size();
     const bool need_x = (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
-    const bool overlap = need_x && !(flags & DC_NO_OVERLAP);
+    const bool overlap = need_x && !(flags & DC_NO_OVERLAP) &&
+                         ((flags & DC_FORCE_OVERLAP) || halo_recv_bytes(pl, 0) >= kOverlapMinHaloBytes);
     if (need_x && !overlap) {  // exchange, then one launch over the whole shard
         exchange(pl, 0, x, flags, st);
         launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);

@@ -163,7 +163,8 @@ def test_loopback_overlapped_fwd_bwd_bitwise(dc, shape, grid):
     R = Ranks(dc, shape, grid)
     try:
         R.load_owned(x, dy)
-        R.each(lambda d: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), wb, d["y"], dc.DC_EXCHANGE, d["stream"]))
+        R.each(lambda d: dc.dc_conv_fwd(d["plan"], d["xb"].data_ptr(), wb, d["y"],
+                                        dc.DC_EXCHANGE | dc.DC_FORCE_OVERLAP, d["stream"]))
         R.each(lambda d: dc.dc_conv_bwd(d["plan"], d["xb"].data_ptr(), d["dyb"].data_ptr(), wb, d["dx"], d["dw"],
                                         dc.DC_EXCHANGE, d["stream"]))
         dw_sum = torch.zeros_like(DW)

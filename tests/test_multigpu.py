@@ -90,7 +90,7 @@ def _worker(rank, world, port, errq, env=None):
             y = torch.empty((yd["n"], yd["h"], yd["w"], yd["c_pad"]), dtype=torch.bfloat16, device="cuda")
             torch.cuda.synchronize()
             dist.barrier()
-            dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y, dc.DC_EXCHANGE)
+            dc.dc_conv_fwd(plan, xb.data_ptr(), wb, y, dc.DC_EXCHANGE | dc.DC_FORCE_OVERLAP)
             torch.cuda.synchronize()
             ys = Y[yd["n0"]:yd["n0"] + yd["n"], yd["h0"]:yd["h0"] + yd["h"], yd["w0"]:yd["w0"] + yd["w"]]
             assert torch.equal(y, ys), f"{tag}: y not bitwise equal to 1-GPU"
