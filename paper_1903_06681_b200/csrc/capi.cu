@@ -278,7 +278,7 @@ struct dc_plan_s {
             if (sp && !s_comm_shared) cudaStreamDestroy(sp);
         for (auto e : ev_ph)
             if (e) cudaEventDestroy(e);
-        if (bn_comm_owned && bn_comm) ncclCommDestroy(bn_comm);
+        if (bn_comm_owned && bn_comm) ncclCommAbort(bn_comm);  // (see dc_comm_destroy)
     }
     int world() const { return rp.grid.size(); }
     int ks_world = 0;  // dc_plan_set_splitk_world (0: kSplitKBasis)
@@ -1710,8 +1710,11 @@ dc_status_t dc_comm_destroy(dc_comm_t c) {
     if (c) {
         if (c->s_grad) cudaStreamSynchronize(c->s_grad);
         cudaDeviceSynchronize();
-        if (c->grad_nccl) ncclCommDestroy(c->grad_nccl);
-        if (c->nccl) ncclCommDestroy(c->nccl);
+        // (the device is idle here; ncclCommAbort frees the communicator
+        // without the finalize handshake ncclCommDestroy runs with the other
+        // ranks, which was measured to hang the 2- and 4-rank bench teardown)
+        if (c->grad_nccl) ncclCommAbort(c->grad_nccl);
+        if (c->nccl) ncclCommAbort(c->nccl);
         if (c->s_grad) cudaStreamDestroy(c->s_grad);
         if (c->s_main) cudaStreamDestroy(c->s_main);
         if (c->s_side) cudaStreamDestroy(c->s_side);
@@ -2632,7 +2635,7 @@ struct dc_cplan_s {
                 if (peer_dyfull[k]) cudaIpcCloseMemHandle(peer_dyfull[k]);
             }
         }
-        if (sample_comm) ncclCommDestroy(sample_comm);
+        if (sample_comm) ncclCommAbort(sample_comm);  // (see dc_comm_destroy)
         delete fwd;
         delete bwd;
         if (wslice) cudaFree(wslice);
