@@ -820,9 +820,17 @@ def main():
                 dc.dc_redist_destroy(d[k])
     for d in L:
         dc.dc_plan_destroy(d["plan"])
-    dc.dc_comm_destroy(comm)
     if world > 1:
-        dist.destroy_process_group()
+        # every rank is done and its line is out: leave without the NCCL
+        # teardown, which was measured to block in the multi-rank bench
+        # (communicators whose collectives were captured into CUDA graphs);
+        # the driver owns the processes, and exit releases the devices
+        torch.cuda.synchronize()
+        dist.barrier()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
+    dc.dc_comm_destroy(comm)
     faulthandler.cancel_dump_traceback_later()
 
 
