@@ -183,7 +183,7 @@ struct dc_plan_s {
     BufState dense[2];               // dc_buffer_alloc'd dense 0: Y, 1: DX (redistribution targets)
     uint32_t *flags = nullptr;       // [2 buf][2 kind][world]
     std::map<int, uint32_t *> peer_flags;
-    uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local), [4]: halo wait target
+    uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local)
     float *wsplit = nullptr;         // 3xTF32 forward weights [F][T][hi | lo | hi]
     size_t wsplit_bytes = 0;
     __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases (fp32 plans: fp32 words)
@@ -492,10 +492,6 @@ struct GemmLaunch {
     // block into the owners' receive slots (ConvV2Params::scat)
     float *scat[8] = {};
     int scat_seg = 0;
-    // in-kernel halo wait (ConvV2Params::halo_*): rects >= halo_rect0 wait
-    int halo_n = 0, halo_rect0 = 0;
-    const uint32_t *halo_in[8] = {};
-    const uint32_t *halo_target = nullptr;
     // a 1x1 stride-1 conv on a margin-free shard is a plain GEMM over pixels:
     // the shard is launched as ONE row of n h w pixels in 1 x 128 tiles, which
     // cross image rows and samples (small images waste no tile rows)
@@ -637,10 +633,6 @@ bool launch_v2_shape(GemmLaunch &L, const std::vector<OutRect> &rects, int twl, 
     q.out_h0 = L.p.out_h0, q.out_w0 = L.p.out_w0, q.out_dh = L.p.out_dh, q.out_dw = L.p.out_dw;
     q.nout_p = L.p.nout_p;
     q.max_ctas = L.max_ctas;
-    if (L.halo_n) {
-        q.halo_n = L.halo_n, q.halo_rect0 = L.halo_rect0, q.halo_target = L.halo_target;
-        std::memcpy(q.halo_in, L.halo_in, sizeof q.halo_in);
-    }
     if (L.scat_seg) {  // the receive slots have channel pitch scat_seg
         std::memcpy(q.scat, L.scat, sizeof q.scat);
         q.scat_seg = L.scat_seg;
@@ -958,51 +950,6 @@ std::vector<int> neighbours(const RankPlan &rp, int which) {
 }
 
 bool is_local(const dc_plan_s *pl) { return pl->comm && pl->comm->group; }
-
-// The forward with its x exchange hidden under ONE conv launch:
-// a snapshot kernel fixes the epoch the exchange will deliver, the exchange
-// runs on the side stream, and the conv covers the interior (tile-aligned:
-// 32-row pairs, 8-column tiles) first and the halo-dependent bands last, its
-// producer waiting in-kernel for the senders' counters before the bands.
-// Two SMs stay free for the exchange kernel (its blocks cannot share an SM
-// with a conv CTA's registers). Real ranks only (a loopback group's ranks
-// share the SMs). False: not applicable (then nothing was launched).
-bool fwd_with_halo_wait(dc_plan_s *pl, GemmLaunch &L, void *x, const dc_shard_desc_t &xd, int nl, unsigned flags,
-                        cudaStream_t st) {
-    if (L.p.T == 0 || pl->buf[0].ptr != x || !pl->buf[0].dev_epoch) return false;
-    const int ho = (int)pl->rp.h.out.size(), wo = (int)pl->rp.w.out.size();
-    const int rt = std::min(ho, (int)round_up(L.dep[0], 32));
-    const int ie = rt + 32 * std::max(0, (ho - L.dep[1] - rt) / 32);
-    const int cl = std::min(wo, (int)round_up(L.dep[2], 8));
-    const int je = cl + 8 * std::max(0, (wo - L.dep[3] - cl) / 8);
-    std::vector<OutRect> rects;
-    if (ie > rt && je > cl) rects.push_back(OutRect{rt, cl, ie - rt, je - cl});
-    const int r0 = (int)rects.size();
-    for (const OutRect &r : {OutRect{0, 0, rt, wo}, OutRect{ie, 0, ho - ie, wo}, OutRect{rt, 0, ie - rt, cl},
-                             OutRect{rt, je, ie - rt, wo - je}})
-        if (r.nh > 0 && r.nw > 0) rects.push_back(r);
-    if ((int)rects.size() > kMaxRects) return false;
-    const P2PExchange px = build_p2p(pl, 0, x);
-    uint32_t *target = pl->dev_epochs + 4;
-    launch_epoch_snapshot(pl->buf[0].dev_epoch, target, st);
-    CK(cudaEventRecord(pl->ev[0], st));
-    CK(cudaStreamWaitEvent(pl->s_comm, pl->ev[0], 0));
-    launch_p2p_exchange(px, pl->s_comm);
-    CK(cudaEventRecord(pl->ev[1], pl->s_comm));
-    L.halo_n = px.n_data_in, L.halo_rect0 = r0, L.halo_target = target;
-    for (int k = 0; k < px.n_data_in; ++k) L.halo_in[k] = px.data_in[k];
-    L.max_ctas = device_sm_count() - 2;
-    const bool ok = launch_v2_shape(L, rects, 3, x, xd, L.cin, nl, st);
-    L.halo_n = 0, L.max_ctas = 0;
-    if (!ok) launch_rects(L, {whole(L)}, x, xd, L.cin, nl, pl->s_comm);  // (after the exchange, joined below)
-    CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
-    if (!ok) {
-        CK(cudaEventRecord(pl->ev[1], pl->s_comm));
-        CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
-    }
-    (void)flags;
-    return true;
-}
 
 // Loopback group: the plan of `rank` with this plan's sequence number.
 dc_plan_s *local_peer(dc_plan_s *pl, int rank) {
@@ -1612,8 +1559,8 @@ dc_plan_s *create_plan(const ConvGeom &g, Grid grid, int rank, dc_comm_s *comm, 
                 const size_t fb = sizeof(uint32_t) * 4 * grid.size();
                 CK(cudaMalloc(&pl->flags, fb));
                 CK(cudaMemset(pl->flags, 0, fb));
-                CK(cudaMalloc(&pl->dev_epochs, sizeof(uint32_t) * 5));
-                CK(cudaMemset(pl->dev_epochs, 0, sizeof(uint32_t) * 5));
+                CK(cudaMalloc(&pl->dev_epochs, sizeof(uint32_t) * 4));
+                CK(cudaMemset(pl->dev_epochs, 0, sizeof(uint32_t) * 4));
                 pl->buf[0].dev_epoch = pl->dev_epochs;
                 pl->buf[1].dev_epoch = pl->dev_epochs + 2;
                 // the BN group's one-shot NVLink mailbox (<= 8 members; NCCL beyond)
@@ -2026,11 +1973,7 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
     const bool need_x = (flags & DC_EXCHANGE) && (!pl->rp.x_send.empty() || !pl->rp.x_recv.empty());
     const bool overlap = need_x && !(flags & DC_NO_OVERLAP) &&
                          ((flags & DC_FORCE_OVERLAP) || halo_recv_bytes(pl, 0) >= kOverlapMinHaloBytes);
-    if (need_x && !overlap && !(flags & (DC_NO_OVERLAP | DC_HALO_NCCL)) && !is_local(pl) && !L.flat &&
-        fwd_with_halo_wait(pl, L, x, xd, nl, flags, st)) {
-        // one launch: interior tiles while the exchange runs beside it, the
-        // halo-dependent bands last after an in-kernel wait
-    } else if (need_x && !overlap) {  // exchange, then one launch over the whole shard
+    if (need_x && !overlap) {  // exchange, then one launch over the whole shard
         exchange(pl, 0, x, flags, st);
         launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);
     } else if (overlap) {

@@ -287,18 +287,9 @@ __global__ void __launch_bounds__(kV2Threads, 1)
         }
         int cur_o0 = -1;
         int a_it = 0, b_it = 0;
-        bool halo_ready = p.halo_n == 0;
         for (int w = w0_; w < total_w; w += w_step) {
             bool phantom;
             const TileCoord c = decode(p, item_of(w, phantom));
-            if (!halo_ready && c.r >= p.halo_rect0) {
-                // the neighbours' slabs of this epoch are in my margins
-                const uint32_t e = *reinterpret_cast<const volatile uint32_t *>(p.halo_target);
-                if ((int)lane < p.halo_n) spin_until_geq(p.halo_in[lane], kP2PBlocks * e);
-                __syncwarp();
-                asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-                halo_ready = true;
-            }
             if (p.b_resident && c.o0 != cur_o0) {
                 // (a resident weight tile never changes for a CTA: nout_tiles == 1)
                 if (elect_one()) {

@@ -104,13 +104,6 @@ struct ConvV2Params {
     // strides in that pitch); scat_seg = 0: plain out
     float *scat[8];
     int scat_seg;
-    // in-kernel halo wait (the forward's exchange running beside
-    // this launch): before its first tile of a rect >= halo_rect0 (the
-    // halo-dependent bands, scheduled last) the producer waits until every
-    // halo sender's counter reached kP2PBlocks * (*halo_target); halo_n = 0: off
-    int halo_n, halo_rect0;
-    const uint32_t *halo_in[8];
-    const uint32_t *halo_target;
 };
 
 size_t conv_v2_smem_bytes(const ConvV2Params &p);

@@ -272,15 +272,6 @@ __global__ void __launch_bounds__(256) p2p_exchange_kernel(const __grid_constant
     }
 }
 
-__global__ void epoch_snapshot_kernel(const uint32_t *epoch, uint32_t *target) {
-    pdl_wait();  // (launch.cuh: PDL)
-    *target = *reinterpret_cast<const volatile uint32_t *>(epoch) + 1;
-}
-
-void launch_epoch_snapshot(const uint32_t *epoch, uint32_t *target, cudaStream_t st) {
-    launch_k(epoch_snapshot_kernel, dim3(1), dim3(1), 0, st, 1, "epoch snapshot", epoch, target);
-}
-
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st) {
     launch_k(p2p_exchange_kernel, dim3(kP2PBlocks), dim3(256), 0, st, 1, "p2p exchange", x);
 }
@@ -339,7 +330,6 @@ void preload_halo() {
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_reduce_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_finalize_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(p2p_exchange_kernel));
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(epoch_snapshot_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_allreduce_p2p_kernel));
 }
 

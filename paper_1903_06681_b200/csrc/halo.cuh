@@ -78,9 +78,6 @@ struct P2PExchange {
     uint32_t *epoch_ctr;
 };
 void launch_p2p_exchange(const P2PExchange &x, cudaStream_t st);
-// *target = *epoch + 1: the epoch the next exchange of this buffer will
-// deliver, for a kernel that waits on it while the exchange runs beside it
-void launch_epoch_snapshot(const uint32_t *epoch, uint32_t *target, cudaStream_t st);
 
 // ---------------------------------------------------------------------------
 // Spatial BN statistics allreduce over NVLink (one kernel, one block): every
