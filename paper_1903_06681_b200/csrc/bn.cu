@@ -178,114 +178,95 @@ __global__ void __launch_bounds__(256) bn_apply_kernel(const __grid_constant__ B
 
 // backward partials: per block fp64 sums of g and g * y_hat per channel, g the
 // output gradient through the ReLU mask (recomputed from y) -> [blocks][2][cpad]
-// Backward kernels: a thread takes 8 channels of a pixel (16-byte loads) and
-// FOUR pixels per trip, all loads issued before any use: 128 bytes in flight
-// per thread, as the forward statistics kernel does. Memory-level
-// parallelism is what bounds these kernels -- the earlier versions kept one
-// or two pixels in flight per thread (8 channels, 1 pixel: 16% of DRAM
-// bandwidth; 4 channels, 2 pixels: 23%) -- so the per-channel constants stay
-// in registers and two blocks per SM suffice.
-constexpr int kBnPix = 4;
+// Backward kernels: a thread keeps ONE quad of channels (8-byte loads; a
+// warp covers 128 channels of a pixel, coalesced) with its per-channel
+// constants in registers, and two pixels in flight per trip; the margined
+// output position is walked, not divided out. (The 8-channel version with
+// fp64 accumulators ran at 164 registers and 16% of DRAM bandwidth; a
+// 2-channel one at 4-byte loads and a 64-bit division per pixel at 19%.)
+constexpr int kBnPix = 2;
 
-__global__ void __launch_bounds__(256, 1) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
+__global__ void __launch_bounds__(256, 3) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
     pdl_wait();  // (launch.cuh: PDL)
     extern __shared__ double sh[];
-    const int c8n = a.cpad / 8;
-    const int cb = c8n < 256 ? c8n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c8t = threadIdx.x % cb;
+    const int c4n = a.cpad / 4;
+    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
     for (int k = threadIdx.x; k < lanes * 2 * a.cpad; k += blockDim.x) sh[k] = 0.0;
     __syncthreads();
     if (pl < lanes) {
-        double *row = sh + (size_t)pl * 2 * a.cpad;
-        const long long step = (long long)gridDim.x * lanes;
-        for (int c8 = c8t; c8 < c8n; c8 += cb) {
-            const int k0 = 8 * c8;
-            float sc[8], sf[8], inv[8], mu[8];
+        for (int cc = c4; cc < c4n; cc += cb) {
+            float sc[4], sf[4], inv[4], mu[4];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                sc[e] = a.coef[k0 + e], sf[e] = a.coef[a.cpad + k0 + e];
-                inv[e] = a.coef[2 * a.cpad + k0 + e], mu[e] = a.coef[3 * a.cpad + k0 + e];
+            for (int e = 0; e < 4; ++e) {
+                const int k = 4 * cc + e;
+                sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
+                mu[e] = a.coef[3 * a.cpad + k];
             }
-            double sg[8], sy[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) sg[e] = sy[e] = 0.0;
+            double sg[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
+            const long long step = (long long)gridDim.x * lanes;
             for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
-                float v[kBnPix][8], d[kBnPix][8];
+                float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
 #pragma unroll
                 for (int u = 0; u < kBnPix; ++u) {
                     const long long p = p0 + u * step;
 #pragma unroll
-                    for (int e = 0; e < 8; ++e) v[u][e] = d[u][e] = 0.f;
+                    for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
                     if (p < a.npix) {
-                        load8(a.y, a.esz, p, a.cpad, c8, v[u]);
-                        load8(a.dout, a.esz, p, a.cpad, c8, d[u]);
+                        load4(a.y, a.esz, p, a.cpad, cc, v[u]);
+                        load4(a.dout, a.esz, p, a.cpad, cc, d[u]);
+                        if (a.res) load4(a.res, a.esz, p, a.cpad, cc, r[u]);
                     }
                 }
-                if (a.res) {  // (residual blocks: the ReLU mask is of BN(y) + residual)
+                // fp32 sums of the trip's pixels, then one fp64 add per trip
+                // (fp64 per element was slow; error bound: DESIGN.md §7)
 #pragma unroll
-                    for (int u = 0; u < kBnPix; ++u) {
-                        float r[8];
-                        const long long p = p0 + u * step;
-                        if (p >= a.npix) break;
-                        load8(a.res, a.esz, p, a.cpad, c8, r);
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (a.relu && fmaf(sc[e], v[u][e], sf[e]) + r[e] <= 0.f) d[u][e] = 0.f;
-                    }
-                } else if (a.relu) {
-#pragma unroll
-                    for (int u = 0; u < kBnPix; ++u)
-#pragma unroll
-                        for (int e = 0; e < 8; ++e)
-                            if (fmaf(sc[e], v[u][e], sf[e]) <= 0.f) d[u][e] = 0.f;
-                }
-                // fp32 sums of the trip's pixels (padding pixels: d = 0), then
-                // one fp64 add per trip
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
+                for (int e = 0; e < 4; ++e) {
                     float tg = 0.f, ty = 0.f;
 #pragma unroll
                     for (int u = 0; u < kBnPix; ++u) {
-                        tg += d[u][e];
-                        ty = fmaf(d[u][e], (v[u][e] - mu[e]) * inv[e], ty);
+                        const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
+                        const float g = (a.relu && z <= 0.f) ? 0.f : d[u][e];  // (padding pixels: d = 0)
+                        tg += g;
+                        ty = fmaf(g, (v[u][e] - mu[e]) * inv[e], ty);
                     }
                     sg[e] += (double)tg, sy[e] += (double)ty;
                 }
             }
+            double *row = sh + (long long)pl * 2 * a.cpad;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) row[k0 + e] = sg[e], row[a.cpad + k0 + e] = sy[e];
+            for (int e = 0; e < 4; ++e) row[4 * cc + e] = sg[e], row[a.cpad + 4 * cc + e] = sy[e];
         }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < 2 * a.cpad; k += blockDim.x) {
         double acc = 0.0;
-        for (int l = 0; l < lanes; ++l) acc += sh[(size_t)l * 2 * a.cpad + k];
+        for (int l = 0; l < lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
         partials[(long long)blockIdx.x * 2 * a.cpad + k] = acc;
     }
 }
 
 // dy = gamma inv_sd (g - sum g / M - y_hat sum(g y_hat) / M) into the margined dy
 // buffer; dgamma = sum(g y_hat), dbeta = sum(g) (block 0); dres = g (dense)
-__global__ void __launch_bounds__(256, 1) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
-                                                              double count, const float *gamma, float *dgamma,
-                                                              float *dbeta, void *dres) {
+__global__ void __launch_bounds__(256, 3) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
+                                                           double count, const float *gamma, float *dgamma,
+                                                           float *dbeta, void *dres) {
     pdl_wait();  // (launch.cuh: PDL)
     if (blockIdx.x == 0)
         for (int k = threadIdx.x; k < a.c; k += blockDim.x) {
             if (dgamma) dgamma[k] = (float)sums[a.cpad + k];
             if (dbeta) dbeta[k] = (float)sums[k];
         }
-    const int c8n = a.cpad / 8;
-    const int cb = c8n < 256 ? c8n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c8t = threadIdx.x % cb;
+    const int c4n = a.cpad / 4;
+    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
+    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
     if (pl >= lanes) return;
-    const long long step = (long long)gridDim.x * lanes;
-    for (int c8 = c8t; c8 < c8n; c8 += cb) {
-        const int k0 = 8 * c8;
-        float sc[8], sf[8], inv[8], mu[8], k1[8], m1[8], m2[8];
+    for (int cc = c4; cc < c4n; cc += cb) {
+        // the quad's constants, once
+        float sc[4], sf[4], inv[4], mu[4], k1[4], m1[4], m2[4];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int k = k0 + e;
+        for (int e = 0; e < 4; ++e) {
+            const int k = 4 * cc + e;
             sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
             mu[e] = a.coef[3 * a.cpad + k];
             const bool live = k < a.c;
@@ -293,36 +274,37 @@ __global__ void __launch_bounds__(256, 1) bn_bwd_apply_kernel(const __grid_const
             m1[e] = live ? (float)(sums[k] / count) : 0.f;
             m2[e] = live ? (float)(sums[a.cpad + k] / count) : 0.f;
         }
+        const long long step = (long long)gridDim.x * lanes;
         long long p = (long long)blockIdx.x * lanes + pl;
         if (p >= a.npix) continue;
         PixWalk q;
         q.init(a, p, step);
         while (p < a.npix) {
-            float v[kBnPix][8], d[kBnPix][8];
+            float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
 #pragma unroll
             for (int u = 0; u < kBnPix; ++u) {
                 const long long pu = p + u * step;
 #pragma unroll
-                for (int e = 0; e < 8; ++e) v[u][e] = d[u][e] = 0.f;
+                for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
                 if (pu < a.npix) {
-                    load8(a.y, a.esz, pu, a.cpad, c8, v[u]);
-                    load8(a.dout, a.esz, pu, a.cpad, c8, d[u]);
+                    load4(a.y, a.esz, pu, a.cpad, cc, v[u]);
+                    load4(a.dout, a.esz, pu, a.cpad, cc, d[u]);
+                    if (a.res) load4(a.res, a.esz, pu, a.cpad, cc, r[u]);
                 }
             }
 #pragma unroll
             for (int u = 0; u < kBnPix; ++u) {
                 if (p >= a.npix) break;
-                float r[8], o[8];
-                if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+                float o[4], g[4];
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float z = fmaf(sc[e], v[u][e], sf[e]) + (a.res ? r[e] : 0.f);
-                    d[u][e] = (a.relu && z <= 0.f) ? 0.f : d[u][e];   // g
+                for (int e = 0; e < 4; ++e) {
+                    const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
+                    g[e] = (a.relu && z <= 0.f) ? 0.f : d[u][e];
                     const float yh = (v[u][e] - mu[e]) * inv[e];
-                    o[e] = k1[e] * (d[u][e] - m1[e] - yh * m2[e]);
+                    o[e] = k1[e] * (g[e] - m1[e] - yh * m2[e]);
                 }
-                store8(a.dst, a.esz, a.split, q.pos(a), a.dcp, c8, o);
-                if (dres) store8(dres, a.esz, 0, p, a.cpad, c8, d[u]);
+                store4(a.dst, a.esz, a.split, q.pos(a), a.dcp, cc, o);
+                if (dres) store4(dres, a.esz, 0, p, a.cpad, cc, g);
                 p += step;
                 q.next(a);
             }
@@ -331,9 +313,9 @@ __global__ void __launch_bounds__(256, 1) bn_bwd_apply_kernel(const __grid_const
 }
 
 int bn_bwd_blocks(long long npix, int cpad) {
-    const int c8n = cpad / 8, lanes = std::max(1, 256 / std::min(c8n, 256));
+    const int c4n = cpad / 4, lanes = std::max(1, 256 / std::min(c4n, 256));
     const long long trips = (npix + lanes - 1) / lanes;
-    return (int)std::max<long long>(1, std::min<long long>((trips + 4 * kBnPix - 1) / (4 * kBnPix), 148 * 2));
+    return (int)std::max<long long>(1, std::min<long long>((trips + 8 * kBnPix - 1) / (8 * kBnPix), 148 * 8));
 }
 
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
@@ -352,7 +334,7 @@ void launch_bn_apply(const BnArgs &a, cudaStream_t st) {
 
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st) {
     DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 4096, DC_ERR_UNSUPPORTED, "BN backward: channels");
-    const int lanes = std::max(1, 256 / std::min(a.cpad / 8, 256));
+    const int lanes = std::max(1, 256 / std::min(a.cpad / 4, 256));
     const size_t smem = (size_t)lanes * 2 * a.cpad * sizeof(double);
     static std::once_flag once;
     std::call_once(once, [] {
