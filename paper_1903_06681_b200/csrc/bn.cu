@@ -12,25 +12,12 @@
 #include "bn.cuh"
 #include "common.hpp"
 #include "launch.cuh"
+#include "sm100.cuh"
 
 namespace dc {
 
 namespace {
 __device__ __forceinline__ float hi_tf32(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
-
-// 8 channels of pixel p of a dense NHWC tensor (bf16 or fp32) as fp32
-__device__ __forceinline__ void load8(const void *t, int esz, long long p, int cpad, int c8, float (&v)[8]) {
-    if (esz == 2) {
-        const uint4 r = reinterpret_cast<const uint4 *>(t)[(p * cpad) / 8 + c8];
-        const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&r);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(h[e]);
-    } else {
-        const float4 *f = reinterpret_cast<const float4 *>(t) + (p * cpad) / 4 + 2 * c8;
-        const float4 a = f[0], b = f[1];
-        v[0] = a.x, v[1] = a.y, v[2] = a.z, v[3] = a.w, v[4] = b.x, v[5] = b.y, v[6] = b.z, v[7] = b.w;
-    }
-}
 
 // 8 channels into a (margined) buffer pixel q: bf16, or the fp32 [hi | lo] split
 __device__ __forceinline__ void store8(void *dst, int esz, int split, long long q, int dcp, int c8,
@@ -40,7 +27,7 @@ __device__ __forceinline__ void store8(void *dst, int esz, int split, long long 
         __nv_bfloat16 *h = reinterpret_cast<__nv_bfloat16 *>(&r);
 #pragma unroll
         for (int e = 0; e < 8; ++e) h[e] = __float2bfloat16_rn(v[e]);
-        reinterpret_cast<uint4 *>(dst)[(q * dcp) / 8 + c8] = r;
+        reinterpret_cast<uint4 *>(dst)[(unsigned long long)q * dcp / 8 + c8] = r;
     } else {
         float *d = reinterpret_cast<float *>(dst) + q * dcp + c8 * 8;
         if (split) {
@@ -58,79 +45,44 @@ __device__ __forceinline__ void store8(void *dst, int esz, int split, long long 
     }
 }
 
-__device__ __forceinline__ long long dst_pixel(const BnArgs &a, long long p) {
-    const int j = (int)(p % a.w);
-    const long long r = p / a.w;
-    const int i = (int)(r % a.h), n = (int)(r / a.h);
-    return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
-}
-
-// 4 channels (quad c4) of pixel p of a dense NHWC tensor as fp32
-__device__ __forceinline__ void load4(const void *t, int esz, long long p, int cpad, int c4, float (&x)[4]) {
-    if (esz == 2) {
-        const uint2 r = reinterpret_cast<const uint2 *>(t)[(p * cpad) / 4 + c4];
-        x[0] = __uint_as_float(r.x << 16), x[1] = __uint_as_float(r.x & 0xffff0000u);
-        x[2] = __uint_as_float(r.y << 16), x[3] = __uint_as_float(r.y & 0xffff0000u);
-    } else {
-        const float4 f = reinterpret_cast<const float4 *>(t)[(p * cpad) / 4 + c4];
-        x[0] = f.x, x[1] = f.y, x[2] = f.z, x[3] = f.w;
-    }
-}
-
-// 4 channels into a (margined) buffer pixel q: bf16, or the fp32 [hi | lo] split
-__device__ __forceinline__ void store4(void *dst, int esz, int split, long long q, int dcp, int c4,
-                                       const float (&x)[4]) {
-    if (esz == 2) {
-        const __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]), h1 = __floats2bfloat162_rn(x[2], x[3]);
-        uint2 r;
-        r.x = *reinterpret_cast<const uint32_t *>(&h0), r.y = *reinterpret_cast<const uint32_t *>(&h1);
-        reinterpret_cast<uint2 *>(dst)[(q * dcp) / 4 + c4] = r;
-    } else if (split) {
-        float *d = reinterpret_cast<float *>(dst) + q * dcp + 4 * c4;
+// 8 channels at byte offset `off` of a staged chunk (bf16 or fp32) as fp32
+template <int ESZ>
+__device__ __forceinline__ void lds8(const unsigned char *chunk, uint32_t off, float (&v)[8]) {
+    if (ESZ == 2) {
+        const uint4 r = *reinterpret_cast<const uint4 *>(chunk + off);
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const float h = hi_tf32(x[e]);
-            d[e] = h, d[dcp / 2 + e] = x[e] - h;
-        }
+        for (int e = 0; e < 4; ++e) v[2 * e] = __uint_as_float(w[e] << 16), v[2 * e + 1] = __uint_as_float(w[e] & 0xffff0000u);
     } else {
-        reinterpret_cast<float4 *>(dst)[(q * dcp) / 4 + c4] = make_float4(x[0], x[1], x[2], x[3]);
+        const float4 *f = reinterpret_cast<const float4 *>(chunk + off);
+        const float4 x = f[0], y = f[1];
+        v[0] = x.x, v[1] = x.y, v[2] = x.z, v[3] = x.w, v[4] = y.x, v[5] = y.y, v[6] = y.z, v[7] = y.w;
     }
 }
 
-// Pixel p = (n, i, j) of an n x h x w block walked with a fixed stride: the
-// margined-buffer position without a division per step.
-struct PixWalk {
-    int n, i, j, sn, si, sj;
-    __device__ __forceinline__ void init(const BnArgs &a, long long p, long long step) {
-        j = (int)(p % a.w), i = (int)((p / a.w) % a.h), n = (int)(p / ((long long)a.w * a.h));
-        sj = (int)(step % a.w), si = (int)((step / a.w) % a.h), sn = (int)(step / ((long long)a.w * a.h));
+// n / d for 32-bit n by a multiply-high (Granlund-Montgomery; d >= 1)
+struct FastDiv {
+    uint32_t m, l;
+    __device__ __forceinline__ void init(uint32_t d) {
+        l = d > 1 ? 32 - __clz(d - 1) : 0;  // ceil(log2 d)
+        m = (uint32_t)((((1ull << l) - d) << 32) / d + 1);
     }
-    __device__ __forceinline__ void next(const BnArgs &a) {
-        j += sj, i += si, n += sn;
-        if (j >= a.w) j -= a.w, ++i;
-        if (i >= a.h) i -= a.h, ++n;
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        if (l == 0) return n;
+        const uint32_t t = __umulhi(m, n);
+        return (t + ((n - t) >> 1)) >> (l - 1);
     }
-    __device__ __forceinline__ long long pos(const BnArgs &a) const {
+};
+
+// pixel p = (n, i, j) of the n x h x w block -> its pixel in the margined dst
+struct DstMap {
+    FastDiv fw, fh;
+    __device__ __forceinline__ void init(const BnArgs &a) { fw.init(a.w), fh.init(a.h); }
+    __device__ __forceinline__ long long pos(const BnArgs &a, uint32_t p) const {
+        const uint32_t r = fw.div(p), j = p - r * a.w, n = fh.div(r), i = r - n * a.h;
         return ((long long)n * a.hb + a.r0 + i) * a.wb + a.c0 + j;
     }
 };
-
-// Thread -> (pixel lane, 8-channel group) mapping of the elementwise / reduction
-// kernels: a thread keeps ONE channel group (its per-channel constants live in
-// registers) and walks the pixels; cb = min(c8n, 256) groups per pass,
-// lanes = 256 / cb pixel lanes per block, further passes for cpad > 2048.
-struct Lanes {
-    int cb, lanes, pl, c8;
-};
-__device__ __forceinline__ Lanes lanes_of(int cpad) {
-    Lanes l;
-    const int c8n = cpad / 8;
-    l.cb = c8n < 256 ? c8n : 256;
-    l.lanes = 256 / l.cb;
-    l.pl = threadIdx.x / l.cb;
-    l.c8 = threadIdx.x % l.cb;
-    return l;
-}
 }  // namespace
 
 // per channel: scale = gamma / sqrt(var + eps), shift = beta - scale * mean,
@@ -153,169 +105,191 @@ __global__ void bn_coeff_kernel(const double *mean, const double *var, const flo
     }
 }
 
-__global__ void __launch_bounds__(256) bn_apply_kernel(const __grid_constant__ BnArgs a) {
+// The three passes over a shard (forward apply; backward partial sums;
+// backward apply) stream their dense inputs -- y, dout, the residual --
+// through shared memory: a producer warp issues one bulk copy per tensor per
+// chunk of P whole pixels (TMA, cp.async.bulk) into a ring of stages, 16
+// consumer warps evaluate it. The copies in flight do not depend on the
+// consumers' registers, which hold one 8-channel group's constants: thread t
+// keeps channel group c8 = t % (cpad / 8) for the whole launch and takes pixel
+// lanes t / (cpad / 8), t / (cpad / 8) + lanes, ... of every chunk. (The
+// register-staged kernels before this -- 4 or 8 channels, 1-4 pixels in
+// flight per thread -- ran the backward at 1.3-1.9 TB/s, bound by the loads a
+// thread could keep in flight next to its constants.)
+constexpr int kBnWarps = 12, kBnThreads = 32 * kBnWarps, kBnMaxStages = 8;
+constexpr size_t kBnRingBytes = 192 * 1024;
+
+struct BnRing {
+    long long nchunks;
+    int P, stages;
+};
+
+enum { kBnFwdApply = 0, kBnBwdPartials = 1, kBnBwdApply = 2 };
+
+template <int MODE, int ESZ, bool RES, bool RELU>
+__global__ void __launch_bounds__(kBnThreads + 32, 1)
+    bn_staged_kernel(const __grid_constant__ BnArgs a, const __grid_constant__ BnRing r, double *partials,
+                     const double *sums, double count, const float *gamma, float *dgamma, float *dbeta, void *dres) {
+    constexpr int T = (MODE == kBnFwdApply ? 1 : 2) + (RES ? 1 : 0);  // staged tensors: y, dout, res
+    constexpr int PPT = ESZ == 2 ? 2 : 1;                              // pixels per thread per chunk
+    extern __shared__ __align__(128) unsigned char ring[];
+    __shared__ uint64_t full[kBnMaxStages], empty[kBnMaxStages];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    const uint32_t rowb = (uint32_t)a.cpad * ESZ, chunkb = (uint32_t)r.P * rowb;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < r.stages; ++s) sm100::mbar_init(&full[s], 1), sm100::mbar_init(&empty[s], kBnWarps);
+        sm100::fence_mbar_init();
+    }
+    __syncthreads();
     pdl_wait();  // (launch.cuh: PDL)
-    const Lanes L = lanes_of(a.cpad);
-    if (L.pl >= L.lanes) return;
-    for (int c8 = L.c8; c8 < a.cpad / 8; c8 += L.cb) {
-        float sc[8], sh[8];
+
+    const int c8n = a.cpad / 8, lanes = kBnThreads / c8n;
+    const int c8 = threadIdx.x % c8n, pl = threadIdx.x / c8n;
+    const bool active = warp < kBnWarps && pl < lanes;
+    double sg[8], sy[8];  // (kBnBwdPartials)
 #pragma unroll
-        for (int e = 0; e < 8; ++e) sc[e] = a.coef[c8 * 8 + e], sh[e] = a.coef[a.cpad + c8 * 8 + e];
-        for (long long p = (long long)blockIdx.x * L.lanes + L.pl; p < a.npix; p += (long long)gridDim.x * L.lanes) {
-            float v[8], r[8];
-            load8(a.y, a.esz, p, a.cpad, c8, v);
-            if (a.res) load8(a.res, a.esz, p, a.cpad, c8, r);
+    for (int e = 0; e < 8; ++e) sg[e] = sy[e] = 0.0;
+
+    if (warp == kBnWarps) {  // producer
+        if (lane == 0) {
+            const unsigned char *src[3] = {static_cast<const unsigned char *>(a.y),
+                                           static_cast<const unsigned char *>(MODE == kBnFwdApply ? a.res : a.dout),
+                                           static_cast<const unsigned char *>(a.res)};
+            int s = 0;
+            uint32_t ph = 0;
+            for (long long k = blockIdx.x; k < r.nchunks; k += gridDim.x) {
+                sm100::mbar_wait(&empty[s], ph ^ 1);
+                const long long p0 = k * r.P;
+                const uint32_t bytes = (uint32_t)(a.npix - p0 < r.P ? a.npix - p0 : (long long)r.P) * rowb;
+                sm100::mbar_arrive_expect_tx(&full[s], T * bytes);
+                unsigned char *dst = ring + (size_t)s * T * chunkb;
+#pragma unroll
+                for (int j = 0; j < T; ++j)
+                    sm100::bulk_load_1d(dst + j * chunkb, src[j] + (size_t)p0 * rowb, bytes, &full[s]);
+                if (++s == r.stages) s = 0, ph ^= 1;
+            }
+        }
+        __syncwarp();
+    } else {
+        // the channel group's constants (kBnBwdApply: dy = k1 (g - m1 - y_hat m2))
+        float sc[8], sf[8], mu[8], inv[8], k1[8], m1[8], m2[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int k = 8 * c8 + e;
+            sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k];
+            mu[e] = inv[e] = k1[e] = m1[e] = m2[e] = 0.f;
+            if (MODE != kBnFwdApply) inv[e] = a.coef[2 * a.cpad + k], mu[e] = a.coef[3 * a.cpad + k];
+            if (MODE == kBnBwdApply && k < a.c) {
+                k1[e] = gamma[k] * inv[e];
+                m1[e] = (float)(sums[k] / count);
+                m2[e] = (float)(sums[a.cpad + k] / count);
+            }
+        }
+        DstMap dm;
+        dm.init(a);
+        unsigned char *const dst = static_cast<unsigned char *>(a.dst);
+        const uint32_t c8b = (uint32_t)c8 * 8 * ESZ;
+        int s = 0;
+        uint32_t ph = 0;
+        for (long long k = blockIdx.x; k < r.nchunks; k += gridDim.x) {
+            sm100::mbar_wait(&full[s], ph);
+            const unsigned char *yc = ring + (size_t)s * T * chunkb;
+            const long long p0 = k * r.P;
+            const int np = (int)(a.npix - p0 < r.P ? a.npix - p0 : (long long)r.P);
+            float tg[8], ty[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) tg[e] = ty[e] = 0.f;
+#pragma unroll
+            for (int u = 0; u < PPT; ++u) {
+                const int pp = pl + u * lanes;
+                if (!active || pp >= np) break;
+                const uint32_t off = (uint32_t)pp * rowb + c8b;
+                float v[8], d[8], rr[8];
+                lds8<ESZ>(yc, off, v);
+                if (MODE != kBnFwdApply) lds8<ESZ>(yc + chunkb, off, d);
+                if (RES) lds8<ESZ>(yc + (T - 1) * chunkb, off, rr);
+                if (MODE == kBnFwdApply) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        float z = fmaf(sc[e], v[e], sf[e]);
+                        if (RES) z += rr[e];
+                        v[e] = (RELU && z < 0.f) ? 0.f : z;
+                    }
+                    store8(dst, ESZ, a.split, dm.pos(a, (uint32_t)(p0 + pp)), a.dcp, c8, v);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        float z = fmaf(sc[e], v[e], sf[e]);
+                        if (RES) z += rr[e];
+                        d[e] = (RELU && z <= 0.f) ? 0.f : d[e];  // g
+                    }
+                    if (MODE == kBnBwdPartials) {
+                        // fp32 sums of this chunk's <= 2 pixels, then one fp64 add
+                        // per chunk (error bound: DESIGN.md §7)
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) tg[e] += d[e], ty[e] = fmaf(d[e], (v[e] - mu[e]) * inv[e], ty[e]);
+                    } else {
+                        float o[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) o[e] = k1[e] * (d[e] - m1[e] - (v[e] - mu[e]) * inv[e] * m2[e]);
+                        store8(dst, ESZ, a.split, dm.pos(a, (uint32_t)(p0 + pp)), a.dcp, c8, o);
+                        if (RES && dres) store8(dres, ESZ, 0, p0 + pp, a.cpad, c8, d);
+                    }
+                }
+            }
+            if (MODE == kBnBwdPartials) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) sg[e] += (double)tg[e], sy[e] += (double)ty[e];
+            }
+            __syncwarp();
+            if (lane == 0) sm100::mbar_arrive(&empty[s]);
+            if (++s == r.stages) s = 0, ph ^= 1;
+        }
+    }
+    if (MODE == kBnBwdPartials) {  // the block's sums per channel -> partials[block][2][cpad]
+        __syncthreads();           // (every chunk consumed: the ring is free)
+        double *red = reinterpret_cast<double *>(ring);
+        if (active) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                float z = fmaf(sc[e], v[e], sh[e]);
-                if (a.res) z += r[e];
-                v[e] = (a.relu && z < 0.f) ? 0.f : z;
+                red[(size_t)pl * 2 * a.cpad + 8 * c8 + e] = sg[e];
+                red[(size_t)pl * 2 * a.cpad + a.cpad + 8 * c8 + e] = sy[e];
             }
-            store8(a.dst, a.esz, a.split, dst_pixel(a, p), a.dcp, c8, v);
+        }
+        __syncthreads();
+        for (int k = threadIdx.x; k < 2 * a.cpad; k += blockDim.x) {
+            double acc = 0.0;
+            for (int l = 0; l < lanes; ++l) acc += red[(size_t)l * 2 * a.cpad + k];
+            partials[(size_t)blockIdx.x * 2 * a.cpad + k] = acc;
         }
     }
-}
-
-// backward partials: per block fp64 sums of g and g * y_hat per channel, g the
-// output gradient through the ReLU mask (recomputed from y) -> [blocks][2][cpad]
-// Backward kernels: a thread keeps ONE quad of channels (8-byte loads; a
-// warp covers 128 channels of a pixel, coalesced) with its per-channel
-// constants in registers, and two pixels in flight per trip; the margined
-// output position is walked, not divided out. (The 8-channel version with
-// fp64 accumulators ran at 164 registers and 16% of DRAM bandwidth; a
-// 2-channel one at 4-byte loads and a 64-bit division per pixel at 19%.)
-constexpr int kBnPix = 2;
-
-__global__ void __launch_bounds__(256, 3) bn_bwd_partials_kernel(const __grid_constant__ BnArgs a, double *partials) {
-    pdl_wait();  // (launch.cuh: PDL)
-    extern __shared__ double sh[];
-    const int c4n = a.cpad / 4;
-    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
-    for (int k = threadIdx.x; k < lanes * 2 * a.cpad; k += blockDim.x) sh[k] = 0.0;
-    __syncthreads();
-    if (pl < lanes) {
-        for (int cc = c4; cc < c4n; cc += cb) {
-            float sc[4], sf[4], inv[4], mu[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int k = 4 * cc + e;
-                sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
-                mu[e] = a.coef[3 * a.cpad + k];
-            }
-            double sg[4] = {0, 0, 0, 0}, sy[4] = {0, 0, 0, 0};
-            const long long step = (long long)gridDim.x * lanes;
-            for (long long p0 = (long long)blockIdx.x * lanes + pl; p0 < a.npix; p0 += kBnPix * step) {
-                float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
-#pragma unroll
-                for (int u = 0; u < kBnPix; ++u) {
-                    const long long p = p0 + u * step;
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
-                    if (p < a.npix) {
-                        load4(a.y, a.esz, p, a.cpad, cc, v[u]);
-                        load4(a.dout, a.esz, p, a.cpad, cc, d[u]);
-                        if (a.res) load4(a.res, a.esz, p, a.cpad, cc, r[u]);
-                    }
-                }
-                // fp32 sums of the trip's pixels, then one fp64 add per trip
-                // (fp64 per element was slow; error bound: DESIGN.md §7)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    float tg = 0.f, ty = 0.f;
-#pragma unroll
-                    for (int u = 0; u < kBnPix; ++u) {
-                        const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
-                        const float g = (a.relu && z <= 0.f) ? 0.f : d[u][e];  // (padding pixels: d = 0)
-                        tg += g;
-                        ty = fmaf(g, (v[u][e] - mu[e]) * inv[e], ty);
-                    }
-                    sg[e] += (double)tg, sy[e] += (double)ty;
-                }
-            }
-            double *row = sh + (long long)pl * 2 * a.cpad;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) row[4 * cc + e] = sg[e], row[a.cpad + 4 * cc + e] = sy[e];
-        }
-    }
-    __syncthreads();
-    for (int k = threadIdx.x; k < 2 * a.cpad; k += blockDim.x) {
-        double acc = 0.0;
-        for (int l = 0; l < lanes; ++l) acc += sh[(long long)l * 2 * a.cpad + k];
-        partials[(long long)blockIdx.x * 2 * a.cpad + k] = acc;
-    }
-}
-
-// dy = gamma inv_sd (g - sum g / M - y_hat sum(g y_hat) / M) into the margined dy
-// buffer; dgamma = sum(g y_hat), dbeta = sum(g) (block 0); dres = g (dense)
-__global__ void __launch_bounds__(256, 3) bn_bwd_apply_kernel(const __grid_constant__ BnArgs a, const double *sums,
-                                                           double count, const float *gamma, float *dgamma,
-                                                           float *dbeta, void *dres) {
-    pdl_wait();  // (launch.cuh: PDL)
-    if (blockIdx.x == 0)
+    if (MODE == kBnBwdApply && blockIdx.x == 0)
         for (int k = threadIdx.x; k < a.c; k += blockDim.x) {
             if (dgamma) dgamma[k] = (float)sums[a.cpad + k];
             if (dbeta) dbeta[k] = (float)sums[k];
         }
-    const int c4n = a.cpad / 4;
-    const int cb = c4n < 256 ? c4n : 256, lanes = 256 / cb;
-    const int pl = threadIdx.x / cb, c4 = threadIdx.x % cb;
-    if (pl >= lanes) return;
-    for (int cc = c4; cc < c4n; cc += cb) {
-        // the quad's constants, once
-        float sc[4], sf[4], inv[4], mu[4], k1[4], m1[4], m2[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-            const int k = 4 * cc + e;
-            sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k], inv[e] = a.coef[2 * a.cpad + k];
-            mu[e] = a.coef[3 * a.cpad + k];
-            const bool live = k < a.c;
-            k1[e] = live ? gamma[k] * inv[e] : 0.f;
-            m1[e] = live ? (float)(sums[k] / count) : 0.f;
-            m2[e] = live ? (float)(sums[a.cpad + k] / count) : 0.f;
-        }
-        const long long step = (long long)gridDim.x * lanes;
-        long long p = (long long)blockIdx.x * lanes + pl;
-        if (p >= a.npix) continue;
-        PixWalk q;
-        q.init(a, p, step);
-        while (p < a.npix) {
-            float v[kBnPix][4], d[kBnPix][4], r[kBnPix][4];
-#pragma unroll
-            for (int u = 0; u < kBnPix; ++u) {
-                const long long pu = p + u * step;
-#pragma unroll
-                for (int e = 0; e < 4; ++e) v[u][e] = d[u][e] = r[u][e] = 0.f;
-                if (pu < a.npix) {
-                    load4(a.y, a.esz, pu, a.cpad, cc, v[u]);
-                    load4(a.dout, a.esz, pu, a.cpad, cc, d[u]);
-                    if (a.res) load4(a.res, a.esz, pu, a.cpad, cc, r[u]);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kBnPix; ++u) {
-                if (p >= a.npix) break;
-                float o[4], g[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float z = fmaf(sc[e], v[u][e], sf[e]) + r[u][e];
-                    g[e] = (a.relu && z <= 0.f) ? 0.f : d[u][e];
-                    const float yh = (v[u][e] - mu[e]) * inv[e];
-                    o[e] = k1[e] * (g[e] - m1[e] - yh * m2[e]);
-                }
-                store4(a.dst, a.esz, a.split, q.pos(a), a.dcp, cc, o);
-                if (dres) store4(dres, a.esz, 0, p, a.cpad, cc, g);
-                p += step;
-                q.next(a);
-            }
-        }
-    }
 }
 
-int bn_bwd_blocks(long long npix, int cpad) {
-    const int c4n = cpad / 4, lanes = std::max(1, 256 / std::min(c4n, 256));
-    const long long trips = (npix + lanes - 1) / lanes;
-    return (int)std::max<long long>(1, std::min<long long>((trips + 8 * kBnPix - 1) / (8 * kBnPix), 148 * 8));
+using BnKernel = void (*)(BnArgs, BnRing, double *, const double *, double, const float *, float *, float *, void *);
+
+template <int MODE>
+BnKernel staged_kernel(int esz, bool res, bool relu) {
+    if (esz == 2)
+        return res ? (relu ? bn_staged_kernel<MODE, 2, true, true> : bn_staged_kernel<MODE, 2, true, false>)
+                   : (relu ? bn_staged_kernel<MODE, 2, false, true> : bn_staged_kernel<MODE, 2, false, false>);
+    return res ? (relu ? bn_staged_kernel<MODE, 4, true, true> : bn_staged_kernel<MODE, 4, true, false>)
+               : (relu ? bn_staged_kernel<MODE, 4, false, true> : bn_staged_kernel<MODE, 4, false, false>);
+}
+
+template <typename F>
+void for_each_staged(F &&f) {
+    for (int esz : {2, 4})
+        for (int res = 0; res < 2; ++res)
+            for (int relu = 0; relu < 2; ++relu) {
+                f(staged_kernel<kBnFwdApply>(esz, res, relu));
+                f(staged_kernel<kBnBwdPartials>(esz, res, relu));
+                f(staged_kernel<kBnBwdApply>(esz, res, relu));
+            }
 }
 
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
@@ -324,38 +298,73 @@ void launch_bn_coeff(const double *mean, const double *var, const float *gamma, 
              eps, c, cpad, coef);
 }
 
+namespace {
+BnRing bn_ring(const BnArgs &a, int tensors) {
+    DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 8 * kBnThreads && a.dcp % 8 == 0, DC_ERR_UNSUPPORTED,
+               "BN: channels must be multiples of 8, at most %d", 8 * kBnThreads);
+    DC_REQUIRE(a.npix < (1ll << 31), DC_ERR_UNSUPPORTED, "BN: more than 2^31 pixels per shard");
+    for (const void *t : {a.y, a.dout, a.res})
+        DC_REQUIRE(reinterpret_cast<uintptr_t>(t) % 16 == 0, DC_ERR_ARG, "BN: tensors must be 16-byte aligned");
+    BnRing r;
+    const int lanes = kBnThreads / (a.cpad / 8);
+    r.P = (a.esz == 2 ? 2 : 1) * lanes;  // <= 16 KB per tensor, <= 2 pixels per thread
+    r.nchunks = (a.npix + r.P - 1) / r.P;
+    const size_t stage = (size_t)tensors * r.P * a.cpad * a.esz;
+    r.stages = (int)std::min<size_t>(kBnMaxStages, kBnRingBytes / stage);
+    return r;
+}
+
+size_t bn_smem(const BnArgs &a, const BnRing &r, int tensors) {
+    const size_t ring = (size_t)r.stages * tensors * r.P * a.cpad * a.esz;
+    const size_t red = (size_t)(kBnThreads / (a.cpad / 8)) * 2 * a.cpad * sizeof(double);
+    return std::max(ring, red);
+}
+
+template <int MODE>
+void launch_staged(const BnArgs &a, int blocks, double *partials, const double *sums, double count,
+                   const float *gamma, float *dgamma, float *dbeta, void *dres, cudaStream_t st, const char *what) {
+    DC_REQUIRE(a.esz == 2 || a.esz == 4, DC_ERR_ARG, "BN: element size %d", a.esz);
+    const int tensors = (MODE == kBnFwdApply ? 1 : 2) + (a.res ? 1 : 0);
+    const BnRing r = bn_ring(a, tensors);
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for_each_staged([](BnKernel k) {
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBnRingBytes);
+        });
+    });
+    launch_k(staged_kernel<MODE>(a.esz, a.res != nullptr, a.relu != 0), dim3(blocks), dim3(kBnThreads + 32),
+             bn_smem(a, r, tensors), st, 1, what, a, r, partials, sums, count, gamma, dgamma, dbeta, dres);
+}
+}  // namespace
+
+int bn_bwd_blocks(const BnArgs &a) {
+    const int lanes = kBnThreads / std::max(1, a.cpad / 8);
+    const long long P = (a.esz == 2 ? 2 : 1) * lanes;
+    return (int)std::max<long long>(1, std::min<long long>((a.npix + P - 1) / P, 148));
+}
+
 void launch_bn_apply(const BnArgs &a, cudaStream_t st) {
-    DC_REQUIRE(a.cpad % 8 == 0 && a.dcp % 8 == 0, DC_ERR_UNSUPPORTED, "BN apply: channels must be multiples of 8");
-    const long long total = a.npix * (a.cpad / 8);
-    if (total == 0) return;
-    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
-    launch_k(bn_apply_kernel, dim3(blocks), dim3(256), 0, st, 1, "bn apply", a);
+    if (a.npix == 0) return;
+    launch_staged<kBnFwdApply>(a, bn_bwd_blocks(a), nullptr, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, st,
+                               "bn apply");
 }
 
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st) {
-    DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 4096, DC_ERR_UNSUPPORTED, "BN backward: channels");
-    const int lanes = std::max(1, 256 / std::min(a.cpad / 4, 256));
-    const size_t smem = (size_t)lanes * 2 * a.cpad * sizeof(double);
-    static std::once_flag once;
-    std::call_once(once, [] {
-        cudaFuncSetAttribute(bn_bwd_partials_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
-    });
-    launch_k(bn_bwd_partials_kernel, dim3(blocks), dim3(256), smem, st, 1, "bn bwd partials", a, partials);
+    launch_staged<kBnBwdPartials>(a, blocks, partials, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, st,
+                                  "bn bwd partials");
 }
 
 void launch_bn_bwd_apply(const BnArgs &a, const double *sums, double count, const float *gamma, float *dgamma,
                          float *dbeta, void *dres, cudaStream_t st) {
-    launch_k(bn_bwd_apply_kernel, dim3(bn_bwd_blocks(a.npix, a.cpad)), dim3(256), 0, st, 1, "bn bwd apply", a, sums,
-             count, gamma, dgamma, dbeta, dres);
+    launch_staged<kBnBwdApply>(a, bn_bwd_blocks(a), nullptr, sums, count, gamma, dgamma, dbeta, dres, st,
+                               "bn bwd apply");
 }
 
 // Loads this file's kernels (see preload_conv_v2)
 void preload_bn() {
     cudaFuncAttributes at;
     cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(bn_coeff_kernel));
-    cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(bn_apply_kernel));
-    cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(bn_bwd_partials_kernel));
-    cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(bn_bwd_apply_kernel));
+    for_each_staged([&](BnKernel k) { cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(k)); });
 }
 
 }  // namespace dc

@@ -23,7 +23,7 @@ struct BnArgs {
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
                      int c, int cpad, float *coef, cudaStream_t st);
 void launch_bn_apply(const BnArgs &a, cudaStream_t st);
-int bn_bwd_blocks(long long npix, int cpad);
+int bn_bwd_blocks(const BnArgs &a);  // grid of the backward partials (one block per SM at most)
 // partials [blocks][2][cpad]: sum g, sum g y_hat (fp64; reduce with launch_bn_reduce)
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st);
 // sums[2][cpad] = the group's sum g, sum g y_hat; count = the group's pixels

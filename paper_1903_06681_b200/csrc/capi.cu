@@ -2215,7 +2215,7 @@ dc_status_t dc_bn_backward(dc_plan_t pl, const void *dout, const void *y, const 
     ensure_alloc(pl->grave, pl->bn_scratch, pl->bn_scratch_bytes, sizeof(double) * 2 * g.Fp);
     launch_bn_coeff(mean, var, gamma, beta, eps, (int)g.F, (int)g.Fp, pl->bn_coef, st);
     BnArgs a = bn_args(pl, y, residual, dout, (flags & DC_RELU) != 0);
-    const int blocks = bn_bwd_blocks(a.npix, a.cpad);
+    const int blocks = bn_bwd_blocks(a);
     ensure_alloc(pl->grave, pl->bnb_part, pl->bnb_part_bytes, sizeof(double) * 2 * g.Fp * blocks);
     launch_bn_bwd_partials(a, pl->bnb_part, blocks, st);
     launch_bn_reduce(pl->bnb_part, blocks, (int)g.Fp, pl->bn_sums, (int)g.F, (double)a.npix, nullptr, nullptr, st);

@@ -66,25 +66,25 @@ def stats_of(dc, plan, y, F, stream=None):
     return mean, var
 
 
-def check_apply(got, y, m, v, g, b, res, relu):
+def check_apply(got, y, m, v, g, b, res, relu, store=2.0 ** -8):
     ref = net.bn_relu_forward(y, m, v, g, b, 1e-5, residual=res, relu=relu)
     a = g / np.sqrt(v + 1e-5)
     mag = np.abs(a[None, :, None, None] * y) + np.abs((b - a * m))[None, :, None, None]
     if res is not None:
         mag = mag + np.abs(res)
-    bound = 4 * U * mag + 2.0 ** -8 * np.abs(ref) + 1e-30
+    bound = 4 * U * mag + store * np.abs(ref) + 1e-30
     err = np.abs(got - ref)
     assert (err <= bound).all(), f"BN apply: {(err > bound).sum()} elements over bound (worst {(err / bound).max():.2f}x)"
 
 
-def check_backward(got_dy, got_dg, got_db, dout, y, m, v, g, b, res, relu):
+def check_backward(got_dy, got_dg, got_db, dout, y, m, v, g, b, res, relu, store=2.0 ** -8):
     dy, dgam, dbet, gm = net.bn_relu_backward(dout, y, m, v, g, b, 1e-5, residual=res, relu=relu)
     M = y.shape[0] * y.shape[2] * y.shape[3]
     k = g / np.sqrt(v + 1e-5)
     yh = (y - m[None, :, None, None]) / np.sqrt(v + 1e-5)[None, :, None, None]
     mag = np.abs(k)[None, :, None, None] * (np.abs(gm) + np.abs(dbet / M)[None, :, None, None]
                                             + np.abs(yh) * np.abs(dgam / M)[None, :, None, None])
-    bound = 8 * U * mag + 2.0 ** -8 * np.abs(dy) + 1e-30
+    bound = 8 * U * mag + store * np.abs(dy) + 1e-30
     err = np.abs(got_dy - dy)
     assert (err <= bound).all(), f"BN bwd dy: {(err > bound).sum()} over bound (worst {(err / bound).max():.2f}x)"
     # per-thread fp32 sums over a trip of <= 4 pixels (4 fused adds), then fp64
@@ -95,8 +95,12 @@ def check_backward(got_dy, got_dg, got_db, dout, y, m, v, g, b, res, relu):
     assert (np.abs(got_db - dbet) <= tb).all(), "dbeta"
 
 
+# many chunks per block (the staged kernels' ring of stages wraps, ragged last chunk)
+BIG = ((2, 16, 256, 250, 64, 3, 1, 1), (1, 1, 1))
+
+
 @pytest.mark.parametrize("relu,use_res", [(True, False), (True, True), (False, False)])
-@pytest.mark.parametrize("case", CASES[:2])
+@pytest.mark.parametrize("case", CASES[:2] + [BIG])
 def test_bn_apply_backward_one_gpu(dc, case, relu, use_res):
     (N, C, H, W, F, K, S, P), _ = case
     Ho, Wo = oracle.out_extent(H, K, S, P), oracle.out_extent(W, K, S, P)
@@ -134,6 +138,55 @@ def test_bn_apply_backward_one_gpu(dc, case, relu, use_res):
         ow = dyb[:, dyd["halo_n"]:dyd["halo_n"] + dyd["h"], dyd["halo_w"]:dyd["halo_w"] + dyd["w"]]
         check_backward(nchw(ow, F), dg.double().cpu().numpy(), db.double().cpu().numpy(), dout, y, m, v, g, b,
                        res, relu)
+        if use_res:
+            gm = net.bn_relu_backward(dout, y, m, v, g, b, 1e-5, residual=res, relu=relu)[3]
+            assert np.array_equal(nchw(dres, F), gm), "dresidual = the ReLU-masked gradient (exact)"
+    finally:
+        dc.dc_plan_destroy(nxt)
+        dc.dc_plan_destroy(plan)
+
+
+@pytest.mark.parametrize("relu,use_res", [(True, True), (False, False)])
+def test_bn_fp32_split(dc, relu, use_res):
+    """fp32 plans (DC_FP32_3XTF32): BN apply / backward evaluate in fp32 and
+    store the [hi | lo] halves into the next layer's margined input / this
+    layer's margined dy; hi is tf32 and hi + lo the fp32 value (no bf16
+    rounding: the bounds without the store term)."""
+    N, C, H, W, F = 2, 16, 21, 19, 40
+    plan = dc.dc_plan_create(N, C, H, W, F, 3, 1, 1, (1, 1, 1), dc.DC_FP32_3XTF32, None)
+    nxt = dc.dc_plan_create(N, F, H, W, 16, 3, 1, 1, (1, 1, 1), dc.DC_FP32_3XTF32, None)
+    try:
+        yd, dyd, xd = dc.dc_plan_query(plan, dc.DC_Y), dc.dc_plan_query(plan, dc.DC_DY), dc.dc_plan_query(nxt, dc.DC_X)
+        cp = yd["c_pad"]
+        y = datagen.gen_block((N, F, H, W), 23, 1)
+        res = datagen.gen_block((N, F, H, W), 23, 2) if use_res else None
+        dout = datagen.gen_block((N, F, H, W), 23, 3)
+        g, b = params(F)
+        yt = nhwc(y, cp, torch.float32)
+        rt = nhwc(res, cp, torch.float32) if use_res else None
+        mean, var = stats_of(dc, plan, yt, F)
+        gt, bt = torch.tensor(g, dtype=torch.float32, device="cuda"), torch.tensor(b, dtype=torch.float32, device="cuda")
+        flags = dc.DC_RELU if relu else 0
+        xb = torch.full((xd["n"], xd["hb"], xd["wb"], xd["c_pad"]), float("nan"), device="cuda")
+        dc.dc_bn_apply(plan, yt, mean, var, gt, bt, 1e-5, rt, flags, nxt, xb)
+        dyb = torch.full((dyd["n"], dyd["hb"], dyd["wb"], dyd["c_pad"]), float("nan"), device="cuda")
+        dg, db = torch.zeros(F, device="cuda"), torch.zeros(F, device="cuda")
+        dres = torch.zeros_like(yt) if use_res else None
+        dc.dc_bn_backward(plan, nhwc(dout, cp, torch.float32), yt, mean, var, gt, bt, dyb, 1e-5, rt, flags, dg, db,
+                          dres)
+        torch.cuda.synchronize()
+
+        def owned(buf, d):
+            o = buf[:, d["halo_n"]:d["halo_n"] + d["h"], d["halo_w"]:d["halo_w"] + d["w"]]
+            half = d["c_pad"] // 2
+            hi, lo = o[..., :half], o[..., half:]
+            assert (hi.view(torch.int32) & 0x1FFF == 0).all(), "hi half is not tf32"
+            return hi + lo  # exact: lo = v - hi
+
+        m, v = oracle.bn_stats(y)
+        check_apply(nchw(owned(xb, xd), F), y, m, v, g, b, res, relu, store=U)
+        check_backward(nchw(owned(dyb, dyd), F), dg.double().cpu().numpy(), db.double().cpu().numpy(), dout, y, m, v,
+                       g, b, res, relu, store=U)
         if use_res:
             gm = net.bn_relu_backward(dout, y, m, v, g, b, 1e-5, residual=res, relu=relu)[3]
             assert np.array_equal(nchw(dres, F), gm), "dresidual = the ReLU-masked gradient (exact)"
