@@ -124,14 +124,14 @@ struct BnRing {
     int P, stages;
 };
 
-enum { kBnFwdApply = 0, kBnBwdPartials = 1, kBnBwdApply = 2 };
+enum { kBnFwdApply = 0, kBnBwdPartials = 1, kBnBwdApply = 2, kBnStats = 3 };
 
 template <int MODE, int ESZ, bool RES, bool RELU>
 __global__ void __launch_bounds__(kBnThreads + 32, 1)
     bn_staged_kernel(const __grid_constant__ BnArgs a, const __grid_constant__ BnRing r, double *partials,
                      const double *sums, double count, const float *gamma, float *dgamma, float *dbeta, void *dres) {
-    constexpr int T = (MODE == kBnFwdApply ? 1 : 2) + (RES ? 1 : 0);  // staged tensors: y, dout, res
-    constexpr int PPT = ESZ == 2 ? 2 : 1;                              // pixels per thread per chunk
+    constexpr int T = (MODE == kBnFwdApply || MODE == kBnStats ? 1 : 2) + (RES ? 1 : 0);  // y, dout, res
+    constexpr int PPT = (ESZ == 2 ? 2 : 1) * (MODE == kBnStats ? 2 : 1);  // pixels per thread per chunk
     extern __shared__ __align__(128) unsigned char ring[];
     __shared__ uint64_t full[kBnMaxStages], empty[kBnMaxStages];
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
     const int c8n = a.cpad / 8, lanes = kBnThreads / c8n;
     const int c8 = threadIdx.x % c8n, pl = threadIdx.x / c8n;
     const bool active = warp < kBnWarps && pl < lanes;
-    double sg[8], sy[8];  // (kBnBwdPartials)
+    double sg[8], sy[8];  // (kBnBwdPartials, kBnStats)
 #pragma unroll
     for (int e = 0; e < 8; ++e) sg[e] = sy[e] = 0.0;
 
@@ -176,9 +176,9 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int k = 8 * c8 + e;
-            sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k];
-            mu[e] = inv[e] = k1[e] = m1[e] = m2[e] = 0.f;
-            if (MODE != kBnFwdApply) inv[e] = a.coef[2 * a.cpad + k], mu[e] = a.coef[3 * a.cpad + k];
+            sc[e] = sf[e] = mu[e] = inv[e] = k1[e] = m1[e] = m2[e] = 0.f;
+            if (MODE != kBnStats) sc[e] = a.coef[k], sf[e] = a.coef[a.cpad + k];
+            if (MODE == kBnBwdPartials || MODE == kBnBwdApply) inv[e] = a.coef[2 * a.cpad + k], mu[e] = a.coef[3 * a.cpad + k];
             if (MODE == kBnBwdApply && k < a.c) {
                 k1[e] = gamma[k] * inv[e];
                 m1[e] = (float)(sums[k] / count);
@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
             }
         }
         DstMap dm;
-        dm.init(a);
+        if (MODE == kBnFwdApply || MODE == kBnBwdApply) dm.init(a);
         unsigned char *const dst = static_cast<unsigned char *>(a.dst);
         const uint32_t c8b = (uint32_t)c8 * 8 * ESZ;
         int s = 0;
@@ -206,9 +206,13 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
                 const uint32_t off = (uint32_t)pp * rowb + c8b;
                 float v[8], d[8], rr[8];
                 lds8<ESZ>(yc, off, v);
-                if (MODE != kBnFwdApply) lds8<ESZ>(yc + chunkb, off, d);
+                if (MODE == kBnBwdPartials || MODE == kBnBwdApply) lds8<ESZ>(yc + chunkb, off, d);
                 if (RES) lds8<ESZ>(yc + (T - 1) * chunkb, off, rr);
-                if (MODE == kBnFwdApply) {
+                if (MODE == kBnStats) {
+                    // sum y, sum y^2 (y^2 of a bf16 is exact in fp32)
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) tg[e] += v[e], ty[e] = fmaf(v[e], v[e], ty[e]);
+                } else if (MODE == kBnFwdApply) {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         float z = fmaf(sc[e], v[e], sf[e]);
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
                     }
                 }
             }
-            if (MODE == kBnBwdPartials) {
+            if (MODE == kBnBwdPartials || MODE == kBnStats) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) sg[e] += (double)tg[e], sy[e] += (double)ty[e];
             }
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(kBnThreads + 32, 1)
             if (++s == r.stages) s = 0, ph ^= 1;
         }
     }
-    if (MODE == kBnBwdPartials) {  // the block's sums per channel -> partials[block][2][cpad]
+    if (MODE == kBnBwdPartials || MODE == kBnStats) {  // the block's sums per channel -> partials[block][2][cpad]
         __syncthreads();           // (every chunk consumed: the ring is free)
         double *red = reinterpret_cast<double *>(ring);
         if (active) {
@@ -290,6 +294,7 @@ void for_each_staged(F &&f) {
                 f(staged_kernel<kBnBwdPartials>(esz, res, relu));
                 f(staged_kernel<kBnBwdApply>(esz, res, relu));
             }
+    f(bn_staged_kernel<kBnStats, 2, false, false>);
 }
 
 void launch_bn_coeff(const double *mean, const double *var, const float *gamma, const float *beta, double eps,
@@ -299,7 +304,7 @@ void launch_bn_coeff(const double *mean, const double *var, const float *gamma, 
 }
 
 namespace {
-BnRing bn_ring(const BnArgs &a, int tensors) {
+BnRing bn_ring(const BnArgs &a, int tensors, bool stats) {
     DC_REQUIRE(a.cpad % 8 == 0 && a.cpad <= 8 * kBnThreads && a.dcp % 8 == 0, DC_ERR_UNSUPPORTED,
                "BN: channels must be multiples of 8, at most %d", 8 * kBnThreads);
     DC_REQUIRE(a.npix < (1ll << 31), DC_ERR_UNSUPPORTED, "BN: more than 2^31 pixels per shard");
@@ -307,7 +312,7 @@ BnRing bn_ring(const BnArgs &a, int tensors) {
         DC_REQUIRE(reinterpret_cast<uintptr_t>(t) % 16 == 0, DC_ERR_ARG, "BN: tensors must be 16-byte aligned");
     BnRing r;
     const int lanes = kBnThreads / (a.cpad / 8);
-    r.P = (a.esz == 2 ? 2 : 1) * lanes;  // <= 16 KB per tensor, <= 2 pixels per thread
+    r.P = (a.esz == 2 ? 2 : 1) * (stats ? 2 : 1) * lanes;  // 12 KB per tensor (statistics: 24 KB)
     r.nchunks = (a.npix + r.P - 1) / r.P;
     const size_t stage = (size_t)tensors * r.P * a.cpad * a.esz;
     r.stages = (int)std::min<size_t>(kBnMaxStages, kBnRingBytes / stage);
@@ -324,15 +329,20 @@ template <int MODE>
 void launch_staged(const BnArgs &a, int blocks, double *partials, const double *sums, double count,
                    const float *gamma, float *dgamma, float *dbeta, void *dres, cudaStream_t st, const char *what) {
     DC_REQUIRE(a.esz == 2 || a.esz == 4, DC_ERR_ARG, "BN: element size %d", a.esz);
-    const int tensors = (MODE == kBnFwdApply ? 1 : 2) + (a.res ? 1 : 0);
-    const BnRing r = bn_ring(a, tensors);
+    const int tensors = (MODE == kBnFwdApply || MODE == kBnStats ? 1 : 2) + (a.res ? 1 : 0);
+    const BnRing r = bn_ring(a, tensors, MODE == kBnStats);
     static std::once_flag once;
     std::call_once(once, [] {
         for_each_staged([](BnKernel k) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBnRingBytes);
         });
     });
-    launch_k(staged_kernel<MODE>(a.esz, a.res != nullptr, a.relu != 0), dim3(blocks), dim3(kBnThreads + 32),
+    BnKernel k;
+    if constexpr (MODE == kBnStats)
+        k = bn_staged_kernel<kBnStats, 2, false, false>;
+    else
+        k = staged_kernel<MODE>(a.esz, a.res != nullptr, a.relu != 0);
+    launch_k(k, dim3(blocks), dim3(kBnThreads + 32),
              bn_smem(a, r, tensors), st, 1, what, a, r, partials, sums, count, gamma, dgamma, dbeta, dres);
 }
 }  // namespace
@@ -358,6 +368,19 @@ void launch_bn_bwd_apply(const BnArgs &a, const double *sums, double count, cons
                          float *dbeta, void *dres, cudaStream_t st) {
     launch_staged<kBnBwdApply>(a, bn_bwd_blocks(a), nullptr, sums, count, gamma, dgamma, dbeta, dres, st,
                                "bn bwd apply");
+}
+
+int bn_stats_blocks(long long npix, int cpad) {
+    BnArgs a{};
+    a.npix = npix, a.cpad = cpad, a.esz = 2;
+    return bn_bwd_blocks(a);
+}
+
+void launch_bn_stats(const void *y, long long npix, int cpad, double *partials, int blocks, cudaStream_t st) {
+    if (npix == 0) return;
+    BnArgs a{};
+    a.y = y, a.npix = npix, a.cpad = cpad, a.c = cpad, a.esz = 2, a.dcp = cpad;
+    launch_staged<kBnStats>(a, blocks, partials, nullptr, 0.0, nullptr, nullptr, nullptr, nullptr, st, "bn stats");
 }
 
 // Loads this file's kernels (see preload_conv_v2)

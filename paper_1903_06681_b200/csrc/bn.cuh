@@ -27,6 +27,10 @@ int bn_bwd_blocks(const BnArgs &a);  // grid of the backward partials (one block
 // partials [blocks][2][cpad]: sum g, sum g y_hat (fp64; reduce with launch_bn_reduce)
 void launch_bn_bwd_partials(const BnArgs &a, double *partials, int blocks, cudaStream_t st);
 // sums[2][cpad] = the group's sum g, sum g y_hat; count = the group's pixels
+// BN statistics of a dense bf16 NHWC tensor [npix][cpad]: partials
+// [blocks][2][cpad] = per-block sum y, sum y^2 (fp64; reduce with launch_bn_reduce)
+int bn_stats_blocks(long long npix, int cpad);
+void launch_bn_stats(const void *y, long long npix, int cpad, double *partials, int blocks, cudaStream_t st);
 void launch_bn_bwd_apply(const BnArgs &a, const double *sums, double count, const float *gamma, float *dgamma,
                          float *dbeta, void *dres, cudaStream_t st);
 

@@ -203,7 +203,7 @@ struct dc_plan_s {
     size_t bn_scratch_bytes = 0;
     double *bn_fpart = nullptr;      // fused BN partials of the last DC_BN_STATS forward
     size_t bn_fpart_bytes = 0;
-    const void *bn_fused_y = nullptr;  // its y (stats of any other tensor: bn_sums_kernel)
+    const void *bn_fused_y = nullptr;  // its y (stats of any other tensor: the staged pass, bn.cu)
     int bn_fused_slots = 0;
     uint64_t fwd_epoch = 0;          // forwards run by this plan
     uint64_t bn_fused_epoch = 0;     // the forward whose partials bn_fpart holds (0: none)
@@ -2073,12 +2073,12 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
     const RankPlan &rp = pl->rp;
     const ConvGeom &g = rp.g;
     const long long npix = rp.nrange.size() * rp.h.out.size() * rp.w.out.size();
-    const int nblk = g.dt ? bn_partial_blocks_f32(npix, (int)g.Fp) : bn_partial_blocks(npix, (int)g.Fp);
+    const int nblk = g.dt ? bn_partial_blocks_f32(npix, (int)g.Fp) : bn_stats_blocks(npix, (int)g.Fp);
     ensure_alloc(pl->grave, pl->bn_part, pl->bn_part_bytes, sizeof(double) * 2 * g.Fp * nblk);
     const bool global = !(flags & DC_BN_LOCAL) && pl->bn_group > 1;
     // the partials of this plan's latest forward, if it ran with DC_BN_STATS
     // on this tensor and the caller states t is unchanged since (DC_BN_FROM_FWD);
-    // consumed once. Otherwise t is read (bn_sums_kernel).
+    // consumed once. Otherwise t is read (bn.cu, bn_staged_kernel<kBnStats>).
     const bool fused = (flags & DC_BN_FROM_FWD) && pl->bn_fused_y == t && pl->bn_fused_epoch != 0 &&
                        pl->bn_fused_epoch == pl->fwd_epoch && pl->bn_fused_slots > 0;
     // single group: the reduce kernel also finalises mean/var (no allreduce between)
@@ -2089,9 +2089,11 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t pl, const void *t, double *mean, doubl
         launch_bn_partials_f32(reinterpret_cast<const float *>(t), npix, (int)g.Fp, pl->bn_part, st);
         launch_bn_reduce(pl->bn_part, nblk, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix, global ? nullptr : mean,
                          global ? nullptr : var, st);
-    } else
-        launch_bn_sums(reinterpret_cast<const __nv_bfloat16 *>(t), npix, (int)g.Fp, pl->bn_part, pl->bn_sums,
-                       (int)g.F, (double)npix, global ? nullptr : mean, global ? nullptr : var, st);
+    } else {  // bf16 y: the staged pass (bn.cu), the same reduction
+        launch_bn_stats(t, npix, (int)g.Fp, pl->bn_part, nblk, st);
+        launch_bn_reduce(pl->bn_part, nblk, (int)g.Fp, pl->bn_sums, (int)g.F, (double)npix, global ? nullptr : mean,
+                         global ? nullptr : var, st);
+    }
     pl->bn_fused_y = nullptr;
     pl->bn_fused_epoch = 0;
     if (global && pl->bn_p2p) {

@@ -59,97 +59,9 @@ void launch_signal(uint32_t *const *flags, int n, uint32_t value, const uint32_t
 }
 
 // ---------------------------------------------------------------------------
-// BN statistics: per-channel sum and sum of squares in fp64.
-// Block: 256 threads; thread -> (pixel lane, 8-channel vector).
+// BN statistics: the per-block partial sums come from the staged pass
+// (bn.cu, bn_staged_kernel<kBnStats>) or the fused conv epilogue.
 // ---------------------------------------------------------------------------
-constexpr int kBnThreads = 256;
-
-__global__ void bn_sums_kernel(const uint4 *__restrict__ t, long long npix, int cpad,
-                               double *__restrict__ partials);
-
-// One wave of resident blocks (never more blocks than the tensor has
-// 8-load batches): a function of (npix, cpad) only, so deterministic.
-int bn_partial_blocks(long long npix, int cpad) {
-    static int per_sm = -1;
-    if (per_sm < 0) {
-        int b = 0;  // dynamic smem = pix_lanes * 2 * cpad doubles = 32 KB for any cpad
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, bn_sums_kernel, kBnThreads, 32 * 1024);
-        per_sm = std::max(1, std::min(b, 4));
-    }
-    const int vecs = cpad / 8;
-    const int pix_per_iter = std::max(1, kBnThreads / vecs);
-    const long long iters = (npix + pix_per_iter - 1) / pix_per_iter;
-    return (int)std::max<long long>(1, std::min<long long>((iters + 7) / 8, 148LL * per_sm));
-}
-
-__global__ void __launch_bounds__(kBnThreads) bn_sums_kernel(const uint4 *__restrict__ t, long long npix, int cpad,
-                                                             double *__restrict__ partials) {
-    pdl_wait();  // (launch.cuh: PDL)
-    // sh[pl][2][cpad]: per-pixel-lane partials, summed below in a fixed order
-    // so the result does not depend on scheduling (deterministic).
-    extern __shared__ double sh[];
-    const int vecs = cpad / 8;
-    const int pix_lanes = max(1, kBnThreads / vecs);
-    const int v = threadIdx.x % vecs, pl = threadIdx.x / vecs;
-    if (pl < pix_lanes) {
-        double s[8], q[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s[e] = q[e] = 0.0;
-        // 4 independent 16-byte loads in flight per thread (memory-level
-        // parallelism), then fp64 accumulation (x^2 of a bf16 is exact in fp32)
-        // groups of 8 pixels are summed in fp32 (|error| <= 7 u sum|x| per group,
-        // DESIGN.md §7; a double-float group sum was measured 1.8x slower) and
-        // flushed to the fp64 accumulators once per group
-        const long long step = (long long)gridDim.x * pix_lanes;
-        long long p = (long long)blockIdx.x * pix_lanes + pl;
-        for (; p + 7 * step < npix; p += 8 * step) {
-            uint4 raw[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) raw[u] = __ldg(&t[(p + u * step) * vecs + v]);
-            float fs[8], fq[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) fs[e] = fq[e] = 0.f;
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&raw[u]);
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float x = __bfloat162float(h[e]);
-                    fs[e] += x;
-                    fq[e] = fmaf(x, x, fq[e]);  // x*x exact (8-bit significand)
-                }
-            }
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                s[e] += (double)fs[e];
-                q[e] += (double)fq[e];
-            }
-        }
-        for (; p < npix; p += step) {
-            const uint4 raw = __ldg(&t[p * vecs + v]);
-            const __nv_bfloat16 *h = reinterpret_cast<const __nv_bfloat16 *>(&raw);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const float x = __bfloat162float(h[e]);
-                s[e] += (double)x;
-                q[e] += (double)(x * x);
-            }
-        }
-        double *row = sh + (long long)pl * 2 * cpad;
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            row[v * 8 + e] = s[e];
-            row[cpad + v * 8 + e] = q[e];
-        }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 2 * cpad; i += blockDim.x) {
-        double acc = 0.0;
-        for (int l = 0; l < pix_lanes; ++l) acc += sh[(long long)l * 2 * cpad + i];
-        partials[(long long)blockIdx.x * 2 * cpad + i] = acc;
-    }
-}
-
 // Fixed-order reduction of the per-block partials (deterministic).
 // One warp per output value: lane l sums the partials of blocks l, l+32, ...
 // in that order, loading 8 of them at a time (independent loads in flight),
@@ -189,18 +101,6 @@ __global__ void bn_reduce_kernel(const double *__restrict__ partials, int blocks
             var[warp] = v > 0.0 ? v : 0.0;
         }
     }
-}
-
-void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
-                    double *out, int c, double count, double *mean, double *var, cudaStream_t st) {
-    DC_REQUIRE(cpad % 8 == 0 && cpad / 8 <= kBnThreads, DC_ERR_UNSUPPORTED,
-               "BN stats: channels must be a multiple of 8 and <= 2048");
-    const int blocks = bn_partial_blocks(npix, cpad);
-    const int pix_lanes = std::max(1, kBnThreads / (cpad / 8));
-    launch_k(bn_sums_kernel, dim3(blocks), dim3(kBnThreads), (size_t)pix_lanes * 2 * cpad * sizeof(double), st, 1,
-             "bn sums", reinterpret_cast<const uint4 *>(t), npix, cpad, partials);
-    launch_k(bn_reduce_kernel, dim3((cpad * 32 + 255) / 256), dim3(256), 0, st, 1, "bn reduce",
-             (const double *)partials, blocks, cpad, out, c, count, mean, var);
 }
 
 void launch_bn_reduce(const double *partials, int blocks, int cpad, double *out, int c, double count, double *mean,
@@ -326,7 +226,6 @@ void preload_halo() {
     cudaFuncAttributes a;
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(block_copy_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(signal_kernel));
-    cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_sums_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_reduce_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(bn_finalize_kernel));
     cudaFuncGetAttributes(&a, reinterpret_cast<const void *>(p2p_exchange_kernel));

@@ -32,17 +32,9 @@ void launch_block_copies(const CopyBatch &b, cudaStream_t st);
 // value = *epoch_src + 1 when epoch_src is set (device epoch, graph-replayable)
 void launch_signal(uint32_t *const *flags, int n, uint32_t value, const uint32_t *epoch_src, cudaStream_t st);
 
-// BN statistics of a dense NHWC bf16 tensor [npix][cpad]: per-channel fp64
-// sum and sum of squares over all pixels (deterministic two-stage reduce).
-// partials must hold blocks * 2 * cpad doubles; out holds 2 * cpad doubles
-// (sums then sums of squares).
-int bn_partial_blocks(long long npix, int cpad);
-// Per-channel sum / sum of squares of an owned NHWC bf16 block into out[2][cpad]
-// (fp64, fixed order); with `mean` non-null also mean/var over `count` pixels.
-void launch_bn_sums(const __nv_bfloat16 *t, long long npix, int cpad, double *partials,
-                    double *out, int c, double count, double *mean, double *var, cudaStream_t st);
 // Fixed-order reduction of `blocks` partials [blocks][2][cpad] into out[2][cpad]
-// (+ mean / var when `mean` is set), e.g. the fused forward-epilogue partials.
+// (+ mean / var when `mean` is set): the fused forward-epilogue partials, or
+// those of the staged pass (bn.cuh launch_bn_stats).
 void launch_bn_reduce(const double *partials, int blocks, int cpad, double *out, int c, double count, double *mean,
                       double *var, cudaStream_t st);
 // mean = s / count, var = ss / count - mean^2 (biased), first `c` channels.

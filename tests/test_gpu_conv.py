@@ -184,7 +184,7 @@ def test_bn_stats_local(dc):
 def bn_tol(yn, depth):
     """Derived bound of the BN statistics: groups of values are
     summed in fp32 (a pairwise tree of depth 5 over a warp's 32 pixels in the
-    fused epilogue; 8 sequential adds, depth 7, in bn_sums_kernel), |err| <=
+    fused epilogue; <= 2 pixels per thread and chunk in the staged pass), |err| <=
     depth u sum|x| (u = 2^-24), the same for x^2 (exact for bf16); everything
     after is fp64. Per channel: |d mean| <= depth u mean|x|,
     |d var| <= depth u E[x^2] + 2 |mean| |d mean| (+ fp64 slack)."""
@@ -215,7 +215,7 @@ def test_fused_bn_stats(dc, shape):
         dc.dc_bn_spatial_stats(plan, y1, mean, var, dc.DC_BN_LOCAL | dc.DC_BN_FROM_FWD)
         torch.cuda.synchronize()
         assert torch.equal(y0, y1), "DC_BN_STATS changed y"
-        # (layers that cannot fuse fall back to bn_sums_kernel: depth 7 covers both)
+        # (layers that cannot fuse fall back to the staged pass: depth 40 covers both)
         yn = y1[..., :F].permute(0, 3, 1, 2).double().cpu().numpy()
         m_ref, v_ref = oracle.bn_stats(yn)
         tm, tv = bn_tol(yn, 40)  # fused: <= 2 x 16 in-register adds + depth-5 tree

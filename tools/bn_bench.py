@@ -34,7 +34,8 @@ def main():
     dg, db = torch.empty_like(g), torch.empty_like(b)
     dc.dc_bn_spatial_stats(plan, y, mean, var, 0)
     by = N * H * W * yd["c_pad"] * 2
-    ops = {"apply": (lambda: dc.dc_bn_apply(plan, y, mean, var, g, b, 1e-5, None, dc.DC_RELU, plan, xb), 2 * by),
+    ops = {"stats": (lambda: dc.dc_bn_spatial_stats(plan, y, mean, var, 0), by),
+           "apply": (lambda: dc.dc_bn_apply(plan, y, mean, var, g, b, 1e-5, None, dc.DC_RELU, plan, xb), 2 * by),
            "backward": (lambda: dc.dc_bn_backward(plan, dout, y, mean, var, g, b, dyb, 1e-5, None, dc.DC_RELU, dg, db),
                         5 * by)}
     for name, (f, nbytes) in ops.items():
