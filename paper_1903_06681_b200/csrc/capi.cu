@@ -35,6 +35,7 @@
 #include "redist.cuh"
 #include "cfpar.cuh"
 #include "pool.cuh"
+#include "subsample.cuh"
 #include "plan.hpp"
 
 namespace dc {
@@ -54,6 +55,7 @@ void preload_bn();
 void preload_redist();
 void preload_cfpar();
 void preload_pool();
+void preload_subsample();
 // Every kernel of the library loaded into this context (see preload_*):
 // once, at communicator creation.
 void preload_kernels() {
@@ -68,6 +70,7 @@ void preload_kernels() {
         preload_redist();
         preload_cfpar();
         preload_pool();
+        preload_subsample();
     });
 }
 bool model_choose(const ConvGeom &g, int world, Grid &best, double &best_t, Grid fix);
@@ -185,6 +188,8 @@ struct dc_plan_s {
     std::map<int, uint32_t *> peer_flags;
     uint32_t *dev_epochs = nullptr;  // [2 buf][epoch, blocks done] (local)
     float *wsplit = nullptr;         // 3xTF32 forward weights [F][T][hi | lo | hi]
+    void *xsub = nullptr;            // 1x1 stride-2 forward: the gathered input pixels
+    size_t xsub_bytes = 0;
     size_t wsplit_bytes = 0;
     __nv_bfloat16 *wt = nullptr;     // backward-data weights, all phases (fp32 plans: fp32 words)
     size_t wt_bytes = 0;
@@ -263,6 +268,7 @@ struct dc_plan_s {
         if (dev_epochs) cudaFree(dev_epochs);
         if (wt) cudaFree(wt);
         if (wsplit) cudaFree(wsplit);
+        if (xsub) cudaFree(xsub);
         if (ws) cudaFree(ws);
         if (ws2) cudaFree(ws2);
         if (bn_part) cudaFree(bn_part);
@@ -505,6 +511,15 @@ bool flat_ok(const ConvGeom &g, const dc_shard_desc_t &in) {
 }
 
 OutRect whole(const GemmLaunch &L) { return whole_of(L.interior, L.boundary); }
+
+// 1x1 stride-2 forward through the gathered pixels (subsample.cuh): bf16, no
+// padding, no input margins, one output rect (no halo-dependent tiles).
+bool sub2_ok(const dc_plan_s *pl, const GemmLaunch &L, const dc_shard_desc_t &xd) {
+    const ConvGeom &g = pl->rp.g;
+    return g.K == 1 && g.S == 2 && g.P == 0 && g.dt == 0 && L.kind == 0 && !L.scat_seg && xd.halo_n == 0 &&
+           xd.halo_s == 0 && xd.halo_w == 0 && xd.halo_e == 0 && L.interior.size() + L.boundary.size() == 1 &&
+           pl->rp.nrange.size() * pl->rp.h.out.size() * pl->rp.w.out.size() < (int64_t(1) << 31);
+}
 
 // Split-K over channel groups for the v2 kernel, chosen from the GLOBAL problem
 // (tiles of the unpartitioned layer) so that every decomposition sums each
@@ -1090,6 +1105,33 @@ bool run_bwd_data_subpix(dc_plan_s *pl, void *dy, const void *w, void *dx, unsig
     return launch_v2_shape(L, whole_rect, 3, dy, dyd, g.Fp, (int)rp.nrange.size(), st);
 }
 
+// 1x1 stride 2 (bf16, no padding): of the four stride phases one holds the
+// tap and three only zeros. The tap's GEMM runs flattened over the whole dy
+// buffer into a dense temporary, then one pass writes dx (the products at the
+// even positions, zeros elsewhere) -- instead of four phase launches, three of
+// them zero-weight GEMMs. False: not applicable (dy window != dy buffer).
+bool run_bwd_data_sub2(dc_plan_s *pl, const std::vector<Phase> &ph, std::vector<GemmLaunch> &L, void *dy,
+                       const dc_shard_desc_t &dyd, const dc_shard_desc_t &dxd, void *dx, int64_t kc,
+                       cudaStream_t st) {
+    const ConvGeom &g = pl->rp.g;
+    if (!(g.K == 1 && g.S == 2 && g.P == 0 && g.dt == 0 && !pl->scat_seg) || ph.size() != 4) return false;
+    const Phase &f = ph[0];
+    if (!f.active || f.T != 1 || ph[1].T || ph[2].T || ph[3].T || L[0].scat_seg) return false;
+    if (f.origin_h != 0 || f.origin_w != 0 || f.nt_h != dyd.hb || f.nt_w != dyd.wb || dyd.halo_n || dyd.halo_s ||
+        dyd.halo_w || dyd.halo_e || dyd.n * dyd.hb * dyd.wb >= (int64_t(1) << 31))
+        return false;
+    GemmLaunch &G = L[0];
+    if (G.interior.size() + G.boundary.size() != 1) return false;
+    ensure_alloc(pl->grave, pl->xsub, pl->xsub_bytes, (size_t)(dyd.n * f.nt_h * f.nt_w * g.Cp * 2));
+    G.p.out = reinterpret_cast<__nv_bfloat16 *>(pl->xsub);
+    G.p.out_sw = g.Cp, G.p.out_sh = f.nt_w * g.Cp, G.p.out_sn = f.nt_h * f.nt_w * g.Cp;
+    G.p.out_h0 = 0, G.p.out_w0 = 0, G.p.out_dh = 1, G.p.out_dw = 1;
+    G.flat = true;
+    launch_rects(G, {whole(G)}, dy, dyd, kc, (int)pl->rp.nrange.size(), st);
+    launch_scatter2(pl->xsub, dyd.n, f.nt_h, f.nt_w, (int)(g.Cp * 2), f.out_h0, f.out_w0, dxd.h, dxd.w, dx, st);
+    return true;
+}
+
 void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned flags,
                   cudaStream_t st) {
     bool exchanged = false;
@@ -1201,6 +1243,7 @@ void run_bwd_data(dc_plan_s *pl, void *dy, const void *w, void *dx, unsigned fla
             const OutRect b = whole(L[i]);
             L[i].ws_h = b.nh, L[i].ws_w = b.nw, L[i].ws = pl->ws2 + ks_off[i] / sizeof(float);
         }
+    if (run_bwd_data_sub2(pl, ph, L, dy, dyd, dxd, dx, kc, st)) return;
     const bool need_dy = (flags & DC_EXCHANGE) && (!rp.dy_send.empty() || !rp.dy_recv.empty());
     const bool overlap = need_dy && !(flags & DC_NO_OVERLAP) &&
                          ((flags & DC_FORCE_OVERLAP) || halo_recv_bytes(pl, 1) >= kOverlapMinHaloBytes);
@@ -1989,6 +2032,21 @@ dc_status_t dc_conv_fwd(dc_plan_t pl, void *x, const void *w, void *y, unsigned 
         launch_rects(L, L.boundary, x, xd, L.cin, nl, pl->s_comm);
         CK(cudaEventRecord(pl->ev[1], pl->s_comm));
         CK(cudaStreamWaitEvent(st, pl->ev[1], 0));
+    } else if (sub2_ok(pl, L, xd)) {
+        // 1x1 stride 2: the pixels the filter reads gathered into a dense
+        // buffer, then the flattened GEMM over them (the stride-2 tiles of the
+        // tile-reuse kernel leave most rows of a 16 x 8 tile empty on 7^2-28^2
+        // images and re-read every weight stage per tile)
+        const dc_shard_desc_t yd = describe(pl->rp, DC_Y);
+        ensure_alloc(pl->grave, pl->xsub, pl->xsub_bytes, (size_t)(yd.n * yd.h * yd.w * L.cin * 2));
+        launch_subsample2(x, xd.n, xd.hb, xd.wb, (int)(L.cin * 2), L.p.origin_h, L.p.origin_w, yd.h, yd.w, pl->xsub,
+                          st);
+        dc_shard_desc_t f = xd;
+        f.h = f.hb = yd.h, f.w = f.wb = yd.w;
+        f.halo_n = f.halo_s = f.halo_w = f.halo_e = 0;
+        L.p.s_in = 1, L.p.origin_h = 0, L.p.origin_w = 0;
+        L.flat = true;
+        launch_rects(L, {whole(L)}, pl->xsub, f, L.cin, nl, st);
     } else {
         launch_rects(L, {whole(L)}, x, xd, L.cin, nl, st);
     }

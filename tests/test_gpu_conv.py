@@ -95,6 +95,10 @@ SHAPES = [  # (N, C, H, W, F, K, S, P)
     # (1 x 128 tiles across images), with a ragged last tile
     (16, 256, 7, 7, 512, 1, 1, 0),
     (5, 64, 13, 11, 128, 1, 1, 0),
+    # 1x1 stride 2 forward through the gathered pixels + the flattened GEMM
+    # (ResNet projection shortcuts): ragged last tile, two N tiles; odd H, W
+    (9, 256, 14, 14, 512, 1, 2, 0),
+    (3, 64, 13, 15, 64, 1, 2, 0),
 ]
 
 
@@ -132,7 +136,7 @@ GRIDS = [(1, 2, 1), (1, 1, 2), (1, 2, 2), (2, 2, 1), (1, 3, 1), (1, 4, 2)]
 
 
 @pytest.mark.parametrize("shape", [SHAPES[0], SHAPES[2], SHAPES[3], SHAPES[4], SHAPES[5], SHAPES[9], SHAPES[12], SHAPES[15],
-                                   SHAPES[21]])
+                                   SHAPES[21], SHAPES[13], SHAPES[24]])
 @pytest.mark.parametrize("grid", GRIDS)
 def test_partition_bitwise(dc, shape, grid):
     """Every rank's owned y and dx from its own margined shard is bitwise equal
