@@ -311,7 +311,9 @@ dc_status_t dc_bn_spatial_stats(dc_plan_t plan, const void *t, double *mean_dev,
  * plan's output block -- the same decomposition of the activation, else
  * DC_ERR_PARTITION -- fp32 plans store the [hi | lo] split), or to dst as a
  * dense tensor of the DC_Y layout. Elementwise, stream-ordered, not
- * collective. Errors: DC_ERR_ARG, DC_ERR_PARTITION. */
+ * collective. y and residual are read by bulk copies: 16-byte aligned device
+ * pointers (torch allocations are), else DC_ERR_ARG. Errors: DC_ERR_ARG,
+ * DC_ERR_PARTITION, DC_ERR_UNSUPPORTED (more than 3072 padded channels). */
 dc_status_t dc_bn_apply(dc_plan_t plan, const void *y, const double *mean, const double *var, const float *gamma,
                         const float *beta, double eps, const void *residual, unsigned flags, dc_plan_t dst_plan,
                         void *dst, void *stream);
@@ -326,7 +328,9 @@ dc_status_t dc_bn_apply(dc_plan_t plan, const void *y, const double *mean, const
  * the owned block of dy_margined (this plan's DC_DY buffer, ready for the
  * dy halo exchange of the convolution's backward). dgamma = sum(g y_hat),
  * dbeta = sum g (device fp32 [F], may be NULL); dresidual (DC_Y layout, may
- * be NULL) receives g. Errors: DC_ERR_ARG, DC_ERR_COMM. */
+ * be NULL) receives g. dout, y and residual: 16-byte aligned device
+ * pointers. Errors: DC_ERR_ARG, DC_ERR_COMM, DC_ERR_UNSUPPORTED (more than
+ * 3072 padded channels). */
 dc_status_t dc_bn_backward(dc_plan_t plan, const void *dout, const void *y, const double *mean, const double *var,
                            const float *gamma, const float *beta, double eps, const void *residual, unsigned flags,
                            float *dgamma, float *dbeta, void *dresidual, void *dy_margined, void *stream);
