@@ -3,8 +3,10 @@
 // spatially aggregated statistics (+ residual add, ReLU), written straight
 // into the next layer's margined input, and its backward, whose per-channel
 // sums sum(g), sum(g y_hat) are aggregated over the spatial group like the
-// forward statistics. Memory-bound elementwise / reduction
-// kernels: 16-byte vector loads, one thread per 8 channels of a pixel.
+// forward statistics, and the statistics pass itself.
+// Memory-bound elementwise / reduction kernels: the inputs stream through a
+// ring of shared-memory stages filled by bulk copies (bn_staged_kernel), one
+// consumer thread per 8 channels of a pixel.
 #include <cuda_bf16.h>
 
 #include <mutex>
