@@ -683,7 +683,13 @@ def main():
     flops_step = sum(3 * layer_flops(d["l"]) for d in L)
     value = flops_step * args.steps / (ms / 1e3) / 1e12
     value_e2e = flops_step * args.steps / (ms_e2e / 1e3) / 1e12
-    h2d = sum(d["host"][k].numel() * d["host"][k].element_size() for d in L for k in ("x", "dy", "w"))
+    # the bytes step(e2e=True) copies: every layer's x, dy and w, or for a
+    # network only the input x of the first layer and the loss gradient dy of
+    # the last (the activations flow through the layers on the device)
+    def nbytes(t):
+        return t.numel() * t.element_size()
+    h2d = sum(nbytes(d["host"]["w"]) + (nbytes(d["host"]["x"]) if not NET or i == 0 else 0) +
+              (nbytes(d["host"]["dy"]) if not NET or i == len(L) - 1 else 0) for i, d in enumerate(L))
     d2h = sum(d["host"]["dw"].numel() * 4 for d in L)
 
     # ---- per-op device times on the launching stream, from the timed steps ----
