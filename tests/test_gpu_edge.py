@@ -57,3 +57,16 @@ def test_edge_bn_one_gpu(dc, case):
     from tests import test_gpu_network as tn
     tn.test_bn_apply_backward_one_gpu(dc, case, True, True)
     tn.test_bn_apply_backward_one_gpu(dc, case, False, False)
+
+
+@pytest.mark.parametrize("shape,grid", [
+    ((1, 16, 1, 1, 3, 1, 1), (1, 1, 1)),    # 1 x 1 image: the window is the pixel itself
+    ((2, 16, 3, 3, 3, 2, 0), (1, 1, 1)),    # one output pixel
+    ((1, 16, 5, 5, 1, 1, 0), (1, 1, 1)),    # K = 1: identity
+    ((2, 16, 8, 4, 3, 2, 1), (1, 4, 1)),    # two input rows per rank, windows across two ranks
+])
+def test_edge_maxpool(dc, shape, grid):
+    """Max pooling with its halo exchange (reading R31)
+    on the smallest windows and shards."""
+    from tests import test_pool as tp
+    tp.test_maxpool_parity(dc, shape, grid)
