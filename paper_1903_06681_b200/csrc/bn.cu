@@ -389,7 +389,12 @@ void launch_bn_stats(const void *y, long long npix, int cpad, double *partials, 
 void preload_bn() {
     cudaFuncAttributes at;
     cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(bn_coeff_kernel));
-    for_each_staged([&](BnKernel k) { cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(k)); });
+    for_each_staged([&](BnKernel k) {
+        cudaFuncGetAttributes(&at, reinterpret_cast<const void *>(k));
+        // (set here, at communicator creation, so that no first launch inside
+        // a stream capture has to change a function attribute)
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kBnRingBytes);
+    });
 }
 
 }  // namespace dc
